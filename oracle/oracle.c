@@ -1,0 +1,854 @@
+/*
+ * oracle.c -- plain, slow, fp64 CPU oracle of the cuRobo (arXiv 2310.17274) hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Never linked into, imported by, or called from the
+ * product path.  No blocking, fusion or reordering beyond the paper's definitions: every function
+ * follows its passage step by step in the paper's order and notation.  Compiled -O2, no fast-math,
+ * -ffp-contract=off (the fp32 selection mirror depends on it).
+ *
+ * P:n = /root/reference/PAPER.md line n.  O1..O10 / A1..A37 = SURVEY.md §8(c) steps and readings
+ * (also listed in DESIGN.md).
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_INF (1.0 / 0.0)
+
+static void upd_margin(double *margin, double v) {
+    if (margin && fabs(v) < *margin) *margin = fabs(v);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* 4x4 homogeneous matrices, Table 6                                              */
+/* ------------------------------------------------------------------------------------------ */
+
+static void mat4_identity(double M[4][4]) {
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) M[i][j] = (i == j) ? 1.0 : 0.0;
+}
+
+static void mat4_mul(double A[4][4], double B[4][4], double C[4][4]) {
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 4; ++k) s += A[i][k] * B[k][j];
+            C[i][j] = s;
+        }
+}
+
+/* Table 6 "Joint Transformation" column.  A25: the revolute-X full-link entry
+ * (3,3) typo does not arise here because we multiply F * J explicitly. */
+static void joint_transform(int type, double v, double J[4][4]) {
+    mat4_identity(J);
+    double c = cos(v), s = sin(v);
+    switch (type) {
+        case 0: break;                           /* fixed                     */
+        case 1: J[0][3] = v; break;              /* prismatic x: d_x          */
+        case 2: J[1][3] = v; break;              /* prismatic y: d_y          */
+        case 3: J[2][3] = v; break;              /* prismatic z: d_z          */
+        case 4:                                  /* revolute x                */
+            J[1][1] = c; J[1][2] = -s; J[2][1] = s; J[2][2] = c; break;
+        case 5:                                  /* revolute y                */
+            J[0][0] = c; J[0][2] = s; J[2][0] = -s; J[2][2] = c; break;
+        case 6:                                  /* revolute z                */
+            J[0][0] = c; J[0][1] = -s; J[1][0] = s; J[1][1] = c; break;
+    }
+}
+
+/* (w,x,y,z) unit quaternion -> rotation (A31; normalised first). */
+void orc_quat_to_mat(const double *q, double *R) {
+    double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    double w = q[0] / n, x = q[1] / n, y = q[2] / n, z = q[3] / n;
+    R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
+    R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+    R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+}
+
+/* Matrix -> quaternion (Alg. 7 mat_to_quat P:2649): Shepperd's method, branch on the
+ * largest of trace / diagonal, canonical hemisphere w >= 0 (A31). */
+void orc_mat_to_quat(const double *R, double *q) {
+    double tr = R[0] + R[4] + R[8];
+    double w, x, y, z;
+    if (tr >= R[0] && tr >= R[4] && tr >= R[8]) {
+        w = 0.5 * sqrt(1.0 + tr);
+        x = (R[7] - R[5]) / (4 * w); y = (R[2] - R[6]) / (4 * w); z = (R[3] - R[1]) / (4 * w);
+    } else if (R[0] >= R[4] && R[0] >= R[8]) {
+        x = 0.5 * sqrt(1.0 + R[0] - R[4] - R[8]);
+        w = (R[7] - R[5]) / (4 * x); y = (R[1] + R[3]) / (4 * x); z = (R[2] + R[6]) / (4 * x);
+    } else if (R[4] >= R[8]) {
+        y = 0.5 * sqrt(1.0 - R[0] + R[4] - R[8]);
+        w = (R[2] - R[6]) / (4 * y); x = (R[1] + R[3]) / (4 * y); z = (R[5] + R[7]) / (4 * y);
+    } else {
+        z = 0.5 * sqrt(1.0 - R[0] - R[4] + R[8]);
+        w = (R[3] - R[1]) / (4 * z); x = (R[2] + R[6]) / (4 * z); y = (R[5] + R[7]) / (4 * z);
+    }
+    if (w < 0) { w = -w; x = -x; y = -y; z = -z; }
+    q[0] = w; q[1] = x; q[2] = y; q[3] = z;
+}
+
+/* O4 / Alg. 7: T_l = T_{p(l)} * F_l * J_type(x[a(l)]), T_{p(0)} = I;
+ * sphere centres w_m = R_{link(m)} c_m + t_{link(m)}; EE (p, quat). */
+static void fk_full(const orc_robot *rb, const double *q, double (*T)[4][4]) {
+    for (int l = 0; l < rb->n_links; ++l) {
+        double P[4][4], F[4][4], J[4][4], PF[4][4];
+        if (rb->parent[l] < 0) mat4_identity(P);
+        else memcpy(P, T[rb->parent[l]], sizeof(P));
+        mat4_identity(F);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 4; ++j) F[i][j] = rb->fixed[l * 12 + i * 4 + j];
+        double v = (rb->dof[l] >= 0) ? q[rb->dof[l]] : 0.0;
+        joint_transform(rb->jtype[l], v, J);
+        mat4_mul(P, F, PF);
+        mat4_mul(PF, J, T[l]);
+    }
+}
+
+void orc_fk(const orc_robot *rb, const double *q, double *link_T, double *spheres, double *ee) {
+    double (*T)[4][4] = malloc(sizeof(double[4][4]) * (size_t)rb->n_links);
+    fk_full(rb, q, T);
+    if (link_T)
+        for (int l = 0; l < rb->n_links; ++l)
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 4; ++j) link_T[l * 12 + i * 4 + j] = T[l][i][j];
+    if (spheres)
+        for (int m = 0; m < rb->n_spheres; ++m) {
+            int l = rb->sph_link[m];
+            for (int i = 0; i < 3; ++i)
+                spheres[m * 4 + i] = T[l][i][0] * rb->sph[m * 4 + 0] + T[l][i][1] * rb->sph[m * 4 + 1] +
+                                     T[l][i][2] * rb->sph[m * 4 + 2] + T[l][i][3];
+            spheres[m * 4 + 3] = rb->sph[m * 4 + 3];
+        }
+    if (ee) {
+        int e = rb->ee_link;
+        double R[9];
+        for (int i = 0; i < 3; ++i) {
+            ee[i] = T[e][i][3];
+            for (int j = 0; j < 3; ++j) R[i * 3 + j] = T[e][i][j];
+        }
+        orc_mat_to_quat(R, ee + 3);
+    }
+    free(T);
+}
+
+static int is_ancestor_or_self(const orc_robot *rb, int anc, int l) {
+    while (l >= 0) {
+        if (l == anc) return 1;
+        l = rb->parent[l];
+    }
+    return 0;
+}
+
+/* Hamilton product a (x) b, (w,x,y,z). */
+static void quat_mul(const double *a, const double *b, double *c) {
+    c[0] = a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3];
+    c[1] = a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2];
+    c[2] = a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1];
+    c[3] = a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0];
+}
+
+static void cross3(const double *a, const double *b, double *c) {
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+/* O6 / Alg. 8 + Table 7: for every actuated link l, sum over spheres
+ * (and the EE point) whose link has l as ancestor-or-self: revolute G^T (k x (w - o)),
+ * prismatic G^T k; EE quaternion: (dC/dq)^T (1/2 (0,k) (x) q) for revolute (A27). */
+void orc_fk_backward(const orc_robot *rb, const double *q, const double *g_sph, const double *g_p,
+                     const double *g_q, double *g_theta) {
+    int L = rb->n_links;
+    double (*T)[4][4] = malloc(sizeof(double[4][4]) * (size_t)L);
+    fk_full(rb, q, T);
+    for (int d = 0; d < rb->n_dof; ++d) g_theta[d] = 0.0;
+    double ee_p[3], ee_q[4], R[9];
+    int e = rb->ee_link;
+    for (int i = 0; i < 3; ++i) {
+        ee_p[i] = T[e][i][3];
+        for (int j = 0; j < 3; ++j) R[i * 3 + j] = T[e][i][j];
+    }
+    orc_mat_to_quat(R, ee_q);
+    for (int l = 0; l < L; ++l) {
+        int a = rb->dof[l];
+        if (a < 0) continue;
+        int type = rb->jtype[l];
+        int axis = (type >= 4) ? type - 4 : type - 1;
+        double k[3] = {T[l][0][axis], T[l][1][axis], T[l][2][axis]};
+        double o[3] = {T[l][0][3], T[l][1][3], T[l][2][3]};
+        double acc = 0.0;
+        if (g_sph) {
+            for (int m = 0; m < rb->n_spheres; ++m) {
+                if (!is_ancestor_or_self(rb, l, rb->sph_link[m])) continue;
+                int lm = rb->sph_link[m];
+                double w[3];
+                for (int i = 0; i < 3; ++i)
+                    w[i] = T[lm][i][0] * rb->sph[m * 4 + 0] + T[lm][i][1] * rb->sph[m * 4 + 1] +
+                           T[lm][i][2] * rb->sph[m * 4 + 2] + T[lm][i][3];
+                const double *G = g_sph + m * 3;
+                if (type >= 4) {
+                    double r[3] = {w[0] - o[0], w[1] - o[1], w[2] - o[2]}, kx[3];
+                    cross3(k, r, kx);
+                    acc += G[0] * kx[0] + G[1] * kx[1] + G[2] * kx[2];
+                } else {
+                    acc += G[0] * k[0] + G[1] * k[1] + G[2] * k[2];
+                }
+            }
+        }
+        if (is_ancestor_or_self(rb, l, e)) {
+            if (g_p) {
+                if (type >= 4) {
+                    double r[3] = {ee_p[0] - o[0], ee_p[1] - o[1], ee_p[2] - o[2]}, kx[3];
+                    cross3(k, r, kx);
+                    acc += g_p[0] * kx[0] + g_p[1] * kx[1] + g_p[2] * kx[2];
+                } else {
+                    acc += g_p[0] * k[0] + g_p[1] * k[1] + g_p[2] * k[2];
+                }
+            }
+            if (g_q && type >= 4) {
+                double k4[4] = {0.0, k[0], k[1], k[2]}, dq[4];
+                quat_mul(k4, ee_q, dq);
+                for (int i = 0; i < 4; ++i) acc += g_q[i] * 0.5 * dq[i];
+            }
+        }
+        g_theta[a] += acc;
+    }
+    free(T);
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* World geometry: §3.5 OBB, Alg. 10, reading A4                      */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Exact Euclidean box SDF from the closest point (A4): p_loc = R^T (p - t); q = |p_loc| - h;
+ * outside: sd = ||max(q,0)||, grad_loc = sign(p_loc) * max(q,0) / sd; inside: sd = max_i q_i,
+ * grad_loc = sign(p_loc_i*) e_i* with i* the first arg-max (x<y<z).  sign(0) := +1.
+ * Returns sd, writes grad = R grad_loc (world frame) if grad != NULL. */
+static double box_sdf_impl(const double *p, const double *pos, const double *quat,
+                           const double *half, double *grad, double *margin) {
+    double R[9];
+    orc_quat_to_mat(quat, R);
+    double dpw[3] = {p[0] - pos[0], p[1] - pos[1], p[2] - pos[2]};
+    double pl[3], qv[3], gl[3] = {0, 0, 0};
+    for (int i = 0; i < 3; ++i) pl[i] = R[0 * 3 + i] * dpw[0] + R[1 * 3 + i] * dpw[1] + R[2 * 3 + i] * dpw[2];
+    for (int i = 0; i < 3; ++i) qv[i] = fabs(pl[i]) - half[i];
+    double qmax = qv[0];
+    int imax = 0;
+    for (int i = 1; i < 3; ++i)
+        if (qv[i] > qmax) { qmax = qv[i]; imax = i; }
+    double sd;
+    if (qmax > 0) {
+        double s2 = 0;
+        for (int i = 0; i < 3; ++i) {
+            double mq = qv[i] > 0 ? qv[i] : 0.0;
+            s2 += mq * mq;
+        }
+        sd = sqrt(s2);
+        for (int i = 0; i < 3; ++i) {
+            double mq = qv[i] > 0 ? qv[i] : 0.0;
+            gl[i] = (pl[i] >= 0 ? 1.0 : -1.0) * mq / sd;
+        }
+    } else {
+        sd = qmax;
+        gl[imax] = pl[imax] >= 0 ? 1.0 : -1.0;
+        if (margin) {
+            /* arg-max tie margin on the inside branch */
+            double second = -ORC_INF;
+            for (int i = 0; i < 3; ++i)
+                if (i != imax && qv[i] > second) second = qv[i];
+            upd_margin(margin, qmax - second);
+        }
+    }
+    if (margin) upd_margin(margin, qmax);
+    if (grad)
+        for (int i = 0; i < 3; ++i) grad[i] = R[i * 3 + 0] * gl[0] + R[i * 3 + 1] * gl[1] + R[i * 3 + 2] * gl[2];
+    return sd;
+}
+
+double orc_box_sdf(const double *p, const double *pos, const double *quat, const double *half,
+                   double *grad) {
+    return box_sdf_impl(p, pos, quat, half, grad, NULL);
+}
+
+/* Eq. smooth-distance-cases in penetration-positive form (A2): with
+ * d' = r' - sd (r' = r + eta) and d = d' - eta,
+ * phi = 0 (d' <= 0), d'^2 / (2 eta) (0 < d' <= eta), d' - eta/2 (d' > eta). */
+double orc_activation(double dprime, double eta, double *dphi) {
+    if (dprime <= 0) { if (dphi) *dphi = 0.0; return 0.0; }
+    if (dprime <= eta) { if (dphi) *dphi = dprime / eta; return dprime * dprime / (2.0 * eta); }
+    if (dphi) *dphi = 1.0;
+    return dprime - 0.5 * eta;
+}
+
+/* One box test at point p for inflated radius rp: returns phi, accumulates scale*phi'*(-grad sd). */
+static double box_term(const orc_world *w, int k, const double *p, double rp, double eta,
+                       double scale, double *G, double *sd_out, double *margin) {
+    double g[3];
+    double sd = box_sdf_impl(p, w->pos + 3 * k, w->quat + 4 * k, w->half + 3 * k, g, NULL);
+    double dprime = rp - sd;
+    if (sd_out) *sd_out = sd;
+    upd_margin(margin, dprime);
+    upd_margin(margin, dprime - eta);
+    if (dprime > 0) {
+        if (margin) box_sdf_impl(p, w->pos + 3 * k, w->quat + 4 * k, w->half + 3 * k, NULL, margin);
+        double dphi;
+        double phi = orc_activation(dprime, eta, &dphi);
+        for (int i = 0; i < 3; ++i) G[i] += scale * dphi * (-g[i]);
+        return phi;
+    }
+    return 0.0;
+}
+
+/* O5 world term for one sphere (centre c, radius r >= 0) -- Alg. 10 (discrete) and §3.4 /
+ * Fig. 4 / Algs. 11-12 (swept) under readings A6-A12:
+ *   E = sum_k phi(r' - sd_k(c));  G = sum_k phi' (-grad sd_k(c))
+ *   swept: for each box k and each existing neighbour n in {prev, next}:
+ *     L = ||n - c||, gap = L - 2r' (skip if gap <= 0), bound = L/2,
+ *     j = J0 = (r' - sd_k(c) > 0) ? r' : sd_k(c)   (reset per direction, A10)
+ *     repeat <= n_s: if j >= bound stop; kappa = j/L; p = c + kappa (n - c); d' = r' - sd_k(p);
+ *        hit: E += phi(d'), G += (1-kappa) phi'(d') (-grad sd_k(p)), j += r'   (A9, A12)
+ *        else j += sd_k(p)                                                     (A8)
+ * Returns E; G accumulates (without beta_2 * speed).  samples (optional) records
+ * (k, dir, kappa, hit) per sweep sample. */
+double orc_sphere_world(const orc_world *w, const double *c, const double *cprev,
+                        const double *cnext, double r, double eta, int sweep, int steps,
+                        double *G, double *samples, int max_samples, int *n_samples,
+                        double *margin, long long *counters) {
+    double rp = r + eta;   /* Alg. 10 line "sph.radius += eta" */
+    double E = 0.0;
+    if (n_samples) *n_samples = 0;
+    for (int k = 0; k < w->n_boxes; ++k) {
+        if (!w->enabled[k]) continue;
+        double sd0;
+        double phi = box_term(w, k, c, rp, eta, 1.0, G, &sd0, margin);
+        E += phi;
+        if (counters) { counters[ORC_CNT_BOX_TESTS]++; if (rp - sd0 > 0) counters[ORC_CNT_BOX_HITS]++; }
+        if (!sweep) continue;
+        for (int dir = 0; dir < 2; ++dir) {
+            const double *n = (dir == 0) ? cprev : cnext;
+            if (!n) continue;
+            double dv[3] = {n[0] - c[0], n[1] - c[1], n[2] - c[2]};
+            double L = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
+            double gap = L - 2.0 * rp;
+            upd_margin(margin, gap);
+            if (gap <= 0) continue;
+            double bound = 0.5 * L;
+            double j = (rp - sd0 > 0) ? rp : sd0;
+            for (int s = 0; s < steps; ++s) {
+                upd_margin(margin, j - bound);
+                if (j >= bound) break;
+                double kappa = j / L;
+                double p[3] = {c[0] + kappa * dv[0], c[1] + kappa * dv[1], c[2] + kappa * dv[2]};
+                double sdp;
+                double phis = box_term(w, k, p, rp, eta, 1.0 - kappa, G, &sdp, margin);
+                int hit = (rp - sdp > 0);
+                if (counters) { counters[ORC_CNT_SWEEP_SAMPLES]++; if (hit) counters[ORC_CNT_SWEEP_HITS]++; }
+                if (samples && n_samples && *n_samples < max_samples) {
+                    double *sm = samples + 4 * (*n_samples);
+                    sm[0] = k; sm[1] = dir; sm[2] = kappa; sm[3] = hit;
+                    (*n_samples)++;
+                }
+                if (hit) { E += phis; j += rp; }
+                else j += sdp;
+            }
+        }
+    }
+    return E;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Self-collision: Eq. self-collision, Alg. 9, readings A28-A30        */
+/* ------------------------------------------------------------------------------------------ */
+double orc_self_collision(const orc_robot *rb, const double *spheres, double beta, double *g,
+                          int *arg_pair, double *margin, long long *counters) {
+    double best = -ORC_INF, second = -ORC_INF;
+    int ibest = -1;
+    for (int p = 0; p < rb->n_pairs; ++p) {
+        int i = rb->pairs[2 * p], j = rb->pairs[2 * p + 1];
+        double ri = rb->sph[i * 4 + 3] + (rb->sph_off ? rb->sph_off[i] : 0.0);
+        double rj = rb->sph[j * 4 + 3] + (rb->sph_off ? rb->sph_off[j] : 0.0);
+        if (ri <= 0.0 || rj <= 0.0) continue;            /* Alg. 9 "continue" */
+        double dx = spheres[i * 4] - spheres[j * 4], dy = spheres[i * 4 + 1] - spheres[j * 4 + 1],
+               dz = spheres[i * 4 + 2] - spheres[j * 4 + 2];
+        double P = ri + rj - sqrt(dx * dx + dy * dy + dz * dz);
+        if (counters) { counters[ORC_CNT_PAIR_TESTS]++; if (P > 0) counters[ORC_CNT_PAIR_PEN]++; }
+        if (P > best) { second = best; best = P; ibest = p; }   /* first maximal pair (A28) */
+        else if (P > second) second = P;
+    }
+    if (arg_pair) *arg_pair = -1;
+    if (ibest < 0) return 0.0;
+    upd_margin(margin, best);
+    if (best <= 0) return 0.0;
+    if (margin && second > -ORC_INF) upd_margin(margin, best - second);
+    if (arg_pair) *arg_pair = ibest;
+    int i = rb->pairs[2 * ibest], j = rb->pairs[2 * ibest + 1];
+    double u[3] = {spheres[i * 4] - spheres[j * 4], spheres[i * 4 + 1] - spheres[j * 4 + 1],
+                   spheres[i * 4 + 2] - spheres[j * 4 + 2]};
+    double nu = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    if (nu < 1e-12) { u[0] = 1; u[1] = 0; u[2] = 0; }
+    else for (int t = 0; t < 3; ++t) u[t] /= nu;
+    if (g)
+        for (int t = 0; t < 3; ++t) {
+            g[i * 3 + t] += -beta * u[t];
+            g[j * 3 + t] += beta * u[t];
+        }
+    return beta * best;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Bound, smoothness, pose (Appendix A)                                            */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Eq. bound_cost, the five branches in the paper's order. */
+double orc_bound(double x, double lo, double hi, double eta2, double *dx) {
+    if (x < lo) { if (dx) *dx = -1.0; return lo - x + 0.5 * eta2; }
+    if (lo + eta2 > x && x >= lo) {
+        if (dx) *dx = -(lo - x + eta2) / eta2;
+        return 0.5 / eta2 * (lo - x + eta2) * (lo - x + eta2);
+    }
+    if (x > hi) { if (dx) *dx = 1.0; return x - hi + 0.5 * eta2; }
+    if (hi - eta2 < x && x <= hi) {
+        if (dx) *dx = (x - hi + eta2) / eta2;
+        return 0.5 / eta2 * (x - hi + eta2) * (x - hi + eta2);
+    }
+    if (dx) *dx = 0.0;
+    return 0.0;
+}
+
+static void bound_margin(double *margin, double x, double lo, double hi, double eta2) {
+    upd_margin(margin, x - lo);
+    upd_margin(margin, x - (lo + eta2));
+    upd_margin(margin, x - hi);
+    upd_margin(margin, x - (hi - eta2));
+}
+
+/* log cosh in the overflow-safe form |x| + log1p(exp(-2|x|)) - log 2. */
+double orc_logcosh(double x) {
+    double ax = fabs(x);
+    return ax + log1p(exp(-2.0 * ax)) - log(2.0);
+}
+
+/* Eq. pose_cost_term with reading A1: e_r = 1 - |<q_g, q>|. */
+double orc_pose_cost(const orc_params *pr, const double *ee, const double *goal, double *gp,
+                     double *gq) {
+    double ep[3] = {goal[0] - ee[0], goal[1] - ee[1], goal[2] - ee[2]};
+    double n = sqrt(ep[0] * ep[0] + ep[1] * ep[1] + ep[2] * ep[2]);
+    double d = goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6];
+    double er = 1.0 - fabs(d);
+    double C = pr->a0 * orc_logcosh(pr->a2 * n) + pr->a1 * orc_logcosh(pr->a3 * er);
+    if (gp) {
+        /* dC/dp = -a0 a2 tanh(a2 n)/n e_p, limit -a0 a2^2 e_p as n -> 0 */
+        double f = (n > 1e-12) ? tanh(pr->a2 * n) / n : pr->a2;
+        for (int i = 0; i < 3; ++i) gp[i] = -pr->a0 * pr->a2 * f * ep[i];
+    }
+    if (gq) {
+        double sg = (d >= 0) ? 1.0 : -1.0;
+        double f = -pr->a1 * pr->a3 * tanh(pr->a3 * er) * sg;
+        for (int i = 0; i < 4; ++i) gq[i] = f * goal[3 + i];
+    }
+    return C;
+}
+
+/* O2 state map (A14, Table 5 last row P:2097): x has H+5 rows, row i <-> h = i-2. */
+void orc_state_map(const double *start, const double *V, int H, int D, double *x) {
+#define XR(h) (x + ((h) + 2) * D)
+    for (int h = 1; h <= H; ++h) memcpy(XR(h), V + (h - 1) * D, sizeof(double) * D);
+    for (int h = 1; h <= 3; ++h) memcpy(XR(h), start, sizeof(double) * D);          /* pin   */
+    for (int h = H - 3; h <= H - 1; ++h) memcpy(XR(h), XR(H), sizeof(double) * D);  /* alias */
+    for (int h = -2; h <= 0; ++h) memcpy(XR(h), start, sizeof(double) * D);         /* pads  */
+    for (int h = H + 1; h <= H + 2; ++h) memcpy(XR(h), XR(H), sizeof(double) * D);
+#undef XR
+}
+
+/* O3 five-point stencil (§A.5; reading A15), at h = 1..H; outputs [H][D]. */
+void orc_derivs(const double *x, int H, int D, double dt, double *v, double *a, double *j) {
+#define X(h, d) x[((h) + 2) * D + (d)]
+    for (int h = 1; h <= H; ++h)
+        for (int d = 0; d < D; ++d) {
+            double xm2 = X(h - 2, d), xm1 = X(h - 1, d), x0 = X(h, d), xp1 = X(h + 1, d), xp2 = X(h + 2, d);
+            v[(h - 1) * D + d] = (-xp2 + 8 * xp1 - 8 * xm1 + xm2) / (12 * dt);
+            a[(h - 1) * D + d] = (-xp2 + 16 * xp1 - 30 * x0 + 16 * xm1 - xm2) / (12 * dt * dt);
+            j[(h - 1) * D + d] = (xp2 - 2 * xp1 + 2 * xm1 - xm2) / (2 * dt * dt * dt);
+        }
+#undef X
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O7: whole evaluation                                                                        */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Per-configuration bound cost; returns cost, writes dC/dx into gx (may be NULL).
+ * kind: 0 pos, 1 vel, 2 acc, 3 jerk. */
+static double bound_vec(const orc_robot *rb, const orc_params *pr, int kind, const double *x,
+                        double *gx, double *margin) {
+    double c = 0.0;
+    for (int d = 0; d < rb->n_dof; ++d) {
+        double lo, hi;
+        switch (kind) {
+            case 0: lo = rb->lo[d]; hi = rb->hi[d]; break;
+            case 1: lo = -rb->vmax[d]; hi = rb->vmax[d]; break;
+            case 2: lo = -rb->amax[d]; hi = rb->amax[d]; break;
+            default: lo = -rb->jmax[d]; hi = rb->jmax[d]; break;
+        }
+        double dx;
+        c += pr->w_bound[kind] * orc_bound(x[d], lo, hi, pr->eta_bound, &dx);
+        bound_margin(margin, x[d], lo, hi, pr->eta_bound);
+        if (gx) gx[d] = pr->w_bound[kind] * dx;
+    }
+    return c;
+}
+
+double orc_eval_traj(const orc_robot *rb, const orc_world *w, const orc_params *pr,
+                     const double *start, const double *goal, const double *V, int H,
+                     double *grad, double *terms, double *margin, long long *counters) {
+    int D = rb->n_dof, M = rb->n_spheres;
+    double *x = calloc((size_t)(H + 5) * D, sizeof(double));
+    double *v = calloc((size_t)H * D, sizeof(double)), *a = calloc((size_t)H * D, sizeof(double)),
+           *jk = calloc((size_t)H * D, sizeof(double));
+    double *gxf = calloc((size_t)(H + 5) * D, sizeof(double));      /* dC/dx_h, h = -2..H+2 */
+    double *gv = calloc((size_t)H * D, sizeof(double)), *ga = calloc((size_t)H * D, sizeof(double)),
+           *gj = calloc((size_t)H * D, sizeof(double));
+    double *sph = calloc((size_t)(H + 1) * M * 4, sizeof(double));  /* w[h][m], h = 1..H */
+    double *gs = calloc((size_t)(H + 1) * M * 3, sizeof(double));
+    double *tmp = calloc((size_t)D, sizeof(double));
+    double ee[7], tm[5] = {0, 0, 0, 0, 0};
+
+    orc_state_map(start, V, H, D, x);                                /* O2 */
+    orc_derivs(x, H, D, pr->dt, v, a, jk);                           /* O3 */
+#define XR(h) (x + ((h) + 2) * D)
+#define GX(h) (gxf + ((h) + 2) * D)
+    for (int h = 1; h <= H; ++h) {
+        /* bound (Eq. bound_cost) on pos/vel/acc/jerk and smoothness (Eq. smooth_cost, A16) */
+        tm[1] += bound_vec(rb, pr, 0, XR(h), tmp, margin);
+        for (int d = 0; d < D; ++d) GX(h)[d] += tmp[d];
+        tm[1] += bound_vec(rb, pr, 1, v + (h - 1) * D, gv + (h - 1) * D, margin);
+        tm[1] += bound_vec(rb, pr, 2, a + (h - 1) * D, ga + (h - 1) * D, margin);
+        tm[1] += bound_vec(rb, pr, 3, jk + (h - 1) * D, gj + (h - 1) * D, margin);
+        for (int d = 0; d < D; ++d) {
+            double ad = a[(h - 1) * D + d], jd = jk[(h - 1) * D + d];
+            tm[2] += pr->a8 * ad * ad;
+            ga[(h - 1) * D + d] += 2 * pr->a8 * ad;
+            if (pr->flags & ORC_JERK) {
+                tm[2] += pr->a9 * jd * jd;
+                gj[(h - 1) * D + d] += 2 * pr->a9 * jd;
+            }
+        }
+        /* FK (O4) */
+        orc_fk(rb, XR(h), NULL, sph + h * M * 4, (h == H) ? ee : NULL);
+        /* self-collision (O5) */
+        tm[3] += orc_self_collision(rb, sph + h * M * 4, pr->beta_self, gs + h * M * 3, NULL,
+                                    margin, counters);
+    }
+    /* world: discrete + swept + speed (O5, Eq. world-collision-cost) */
+    int sweep = (pr->flags & ORC_SWEEP) != 0;
+    for (int h = 1; h <= H; ++h)
+        for (int m = 0; m < M; ++m) {
+            double r = rb->sph[m * 4 + 3];
+            if (r < 0) continue;
+            const double *c = sph + (h * M + m) * 4;
+            const double *cp = (h > 1) ? sph + ((h - 1) * M + m) * 4 : NULL;
+            const double *cn = (h < H) ? sph + ((h + 1) * M + m) * 4 : NULL;
+            double sp = 1.0;
+            if (pr->flags & ORC_SPEED) {                                 /* A13 */
+                const double *pa = cp ? cp : c, *pb = cn ? cn : c;
+                double dx = pb[0] - pa[0], dy = pb[1] - pa[1], dz = pb[2] - pa[2];
+                sp = sqrt(dx * dx + dy * dy + dz * dz) / (2.0 * pr->dt);
+            }
+            double G[3] = {0, 0, 0};
+            double E = orc_sphere_world(w, c, sweep ? cp : NULL, sweep ? cn : NULL, r, pr->eta, sweep,
+                                        pr->sweep_steps, G, NULL, 0, NULL, margin, counters);
+            if (counters && E > 0) counters[ORC_CNT_ACTIVE_SPHERES]++;
+            tm[4] += pr->beta_world * sp * E;
+            for (int i = 0; i < 3; ++i) gs[(h * M + m) * 3 + i] += pr->beta_world * sp * G[i];
+        }
+    /* pose at x_H (Eq. pose_cost_term) */
+    double gp[3], gq[4];
+    tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
+    if (margin) {
+        double ep[3] = {goal[0] - ee[0], goal[1] - ee[1], goal[2] - ee[2]};
+        upd_margin(margin, sqrt(ep[0] * ep[0] + ep[1] * ep[1] + ep[2] * ep[2]));
+        upd_margin(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
+    }
+    /* backward (O6) per evaluated configuration */
+    for (int h = 1; h <= H; ++h) {
+        orc_fk_backward(rb, XR(h), gs + h * M * 3, (h == H) ? gp : NULL, (h == H) ? gq : NULL, tmp);
+        for (int d = 0; d < D; ++d) GX(h)[d] += tmp[d];
+    }
+    /* transposed stencil: chain rule through O3 */
+    for (int h = 1; h <= H; ++h)
+        for (int d = 0; d < D; ++d) {
+            double gvd = gv[(h - 1) * D + d], gad = ga[(h - 1) * D + d], gjd = gj[(h - 1) * D + d];
+            double cv[5] = {1.0 / (12 * pr->dt), -8.0 / (12 * pr->dt), 0.0, 8.0 / (12 * pr->dt), -1.0 / (12 * pr->dt)};
+            double dt2 = pr->dt * pr->dt, dt3 = dt2 * pr->dt;
+            double ca[5] = {-1.0 / (12 * dt2), 16.0 / (12 * dt2), -30.0 / (12 * dt2), 16.0 / (12 * dt2), -1.0 / (12 * dt2)};
+            double cj[5] = {-1.0 / (2 * dt3), 2.0 / (2 * dt3), 0.0, -2.0 / (2 * dt3), 1.0 / (2 * dt3)};
+            for (int o = -2; o <= 2; ++o) GX(h + o)[d] += cv[o + 2] * gvd + ca[o + 2] * gad + cj[o + 2] * gjd;
+        }
+    /* transposed state map (O2 gradient routing) */
+    if (grad) {
+        memset(grad, 0, sizeof(double) * (size_t)H * D);
+        for (int h = 4; h <= H - 4; ++h)
+            for (int d = 0; d < D; ++d) grad[(h - 1) * D + d] = GX(h)[d];
+        for (int d = 0; d < D; ++d) {
+            double s = GX(H)[d] + GX(H - 1)[d] + GX(H - 2)[d] + GX(H - 3)[d] + GX(H + 1)[d] + GX(H + 2)[d];
+            grad[(H - 1) * D + d] = s;
+        }
+    }
+#undef XR
+#undef GX
+    if (terms) memcpy(terms, tm, sizeof(tm));
+    double C = tm[0] + tm[1] + tm[2] + tm[3] + tm[4];
+    free(x); free(v); free(a); free(jk); free(gxf); free(gv); free(ga); free(gj);
+    free(sph); free(gs); free(tmp);
+    return C;
+}
+
+/* IK mode (A34): pose + self + discrete world (speed 1) + position bound. */
+double orc_eval_ik(const orc_robot *rb, const orc_world *w, const orc_params *pr,
+                   const double *goal, const double *q, double *grad, double *terms,
+                   double *margin, long long *counters) {
+    int D = rb->n_dof, M = rb->n_spheres;
+    double *sph = calloc((size_t)M * 4, sizeof(double)), *gs = calloc((size_t)M * 3, sizeof(double));
+    double *gb = calloc((size_t)D, sizeof(double));
+    double ee[7], tm[5] = {0, 0, 0, 0, 0};
+    orc_fk(rb, q, NULL, sph, ee);
+    tm[1] = bound_vec(rb, pr, 0, q, gb, margin);
+    tm[3] = orc_self_collision(rb, sph, pr->beta_self, gs, NULL, margin, counters);
+    for (int m = 0; m < M; ++m) {
+        double r = rb->sph[m * 4 + 3];
+        if (r < 0) continue;
+        double G[3] = {0, 0, 0};
+        double E = orc_sphere_world(w, sph + m * 4, NULL, NULL, r, pr->eta, 0, 0, G, NULL, 0, NULL,
+                                    margin, counters);
+        if (counters && E > 0) counters[ORC_CNT_ACTIVE_SPHERES]++;
+        tm[4] += pr->beta_world * E;
+        for (int i = 0; i < 3; ++i) gs[m * 3 + i] += pr->beta_world * G[i];
+    }
+    double gp[3], gq[4];
+    tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
+    if (margin) {
+        double ep[3] = {goal[0] - ee[0], goal[1] - ee[1], goal[2] - ee[2]};
+        upd_margin(margin, sqrt(ep[0] * ep[0] + ep[1] * ep[1] + ep[2] * ep[2]));
+        upd_margin(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
+    }
+    if (grad) {
+        orc_fk_backward(rb, q, gs, gp, gq, grad);
+        for (int d = 0; d < D; ++d) grad[d] += gb[d];
+    }
+    if (terms) memcpy(terms, tm, sizeof(tm));
+    free(sph); free(gs); free(gb);
+    return tm[0] + tm[1] + tm[2] + tm[3] + tm[4];
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* O8: L-BFGS (Alg. 6) + parallel noisy line search (Alg. 1)           */
+/* ------------------------------------------------------------------------------------------ */
+
+static double dot(int n, const double *a, const double *b) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+}
+
+/* Two-loop recursion (Nocedal & Wright, Alg. 6) over `count` stored pairs, index 0
+ * oldest .. count-1 newest; H0 = gamma I, gamma = s^T y / y^T y of the newest pair (A19), 1 if
+ * empty; d = -r (A18). */
+void orc_lbfgs_direction(int n, int count, const double *S, const double *Y, const double *rho,
+                         const double *g, double *d) {
+    double *q = malloc(sizeof(double) * (size_t)n);
+    double alpha[64];
+    memcpy(q, g, sizeof(double) * (size_t)n);
+    for (int i = count - 1; i >= 0; --i) {
+        alpha[i] = rho[i] * dot(n, S + (size_t)i * n, q);
+        for (int t = 0; t < n; ++t) q[t] -= alpha[i] * Y[(size_t)i * n + t];
+    }
+    double gamma = 1.0;
+    if (count > 0) {
+        const double *s = S + (size_t)(count - 1) * n, *y = Y + (size_t)(count - 1) * n;
+        gamma = dot(n, s, y) / dot(n, y, y);
+    }
+    for (int t = 0; t < n; ++t) q[t] *= gamma;       /* r = H0 q */
+    for (int i = 0; i < count; ++i) {
+        double beta = rho[i] * dot(n, Y + (size_t)i * n, q);
+        for (int t = 0; t < n; ++t) q[t] += (alpha[i] - beta) * S[(size_t)i * n + t];
+    }
+    for (int t = 0; t < n; ++t) d[t] = -q[t];
+    free(q);
+}
+
+/* Alg. 1 lines 4-9 in fp64 (A17, A22): Armijo c_a <= c0 + c1 alpha_a g0d; Wolfe g_a^T d >= c2 g0d;
+ * strong |g_a^T d| <= c2 |g0d|; largest index with all conditions true, else 0. */
+int orc_ls_select(int A, const double *alpha, double c0, double g0d, const double *ca,
+                  const double *gda, double c1, double c2, int mode) {
+    int best = 0;
+    for (int a = 0; a < A; ++a) {
+        int ok = ca[a] <= c0 + (c1 * alpha[a]) * g0d;
+        if (mode == 1) ok = ok && (gda[a] >= c2 * g0d);
+        if (mode == 2) ok = ok && (fabs(gda[a]) <= c2 * fabs(g0d));
+        if (ok) best = a;
+    }
+    return best;
+}
+
+/* fp32 mirror of the pure selection function: fixed operation order, no FMA
+ * contraction (-ffp-contract=off), NaN compares false. */
+int orc_ls_select_f32(int A, const float *alpha, float c0, float g0d, const float *ca,
+                      const float *gda, float c1, float c2, int mode) {
+    int best = 0;
+    for (int a = 0; a < A; ++a) {
+        volatile float t1 = c1 * alpha[a];
+        volatile float t2 = t1 * g0d;
+        volatile float rhs = c0 + t2;
+        int ok = ca[a] <= rhs;
+        if (mode == 1) { volatile float w = c2 * g0d; ok = ok && (gda[a] >= w); }
+        if (mode == 2) { volatile float w = c2 * fabsf(g0d); ok = ok && (fabsf(gda[a]) <= w); }
+        if (ok) best = a;
+    }
+    return best;
+}
+
+/* O9 selection: argmin with ties to the lowest index, NaN treated as +inf. */
+int orc_argmin_f32(int n, const float *c) {
+    int best = 0;
+    float bv = (c[0] != c[0]) ? (float)ORC_INF : c[0];
+    for (int i = 1; i < n; ++i) {
+        float v = (c[i] != c[i]) ? (float)ORC_INF : c[i];
+        if (v < bv) { bv = v; best = i; }
+    }
+    return best;
+}
+
+/* O8 per-seed solver in fp64: evaluate at x0, then `iters` iterations of
+ * L-BFGS step -> clipped candidates -> batched evaluation -> selection -> best update. */
+void orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
+                     const double *hi, const orc_solver *sp, double *best_x, double *best_c,
+                     double *trace) {
+    int m = sp->history, A = sp->n_alpha;
+    double *x = malloc(sizeof(double) * n), *g = malloc(sizeof(double) * n);
+    double *xp = malloc(sizeof(double) * n), *gpv = malloc(sizeof(double) * n);
+    double *d = malloc(sizeof(double) * n);
+    double *S = malloc(sizeof(double) * (size_t)m * n), *Y = malloc(sizeof(double) * (size_t)m * n);
+    double *rho = malloc(sizeof(double) * m);
+    double *xa = malloc(sizeof(double) * (size_t)A * n), *ga = malloc(sizeof(double) * (size_t)A * n);
+    double ca[8], gda[8];
+    int count = 0;
+    memcpy(x, x0, sizeof(double) * n);
+    double c = f(ctx, x, g);
+    double bc = c;
+    memcpy(best_x, x, sizeof(double) * n);
+    if (trace) trace[0] = bc;
+    for (int it = 0; it < sp->iters; ++it) {
+        if (it > 0) {
+            double *s = malloc(sizeof(double) * n), *y = malloc(sizeof(double) * n);
+            for (int t = 0; t < n; ++t) { s[t] = x[t] - xp[t]; y[t] = g[t] - gpv[t]; }
+            double sy = dot(n, s, y);
+            if (sy > 1e-12) {                             /* A20 */
+                if (count == m) {                         /* shift buffers (Alg. 6 line 1) */
+                    memmove(S, S + n, sizeof(double) * (size_t)(m - 1) * n);
+                    memmove(Y, Y + n, sizeof(double) * (size_t)(m - 1) * n);
+                    memmove(rho, rho + 1, sizeof(double) * (m - 1));
+                    count = m - 1;
+                }
+                memcpy(S + (size_t)count * n, s, sizeof(double) * n);
+                memcpy(Y + (size_t)count * n, y, sizeof(double) * n);
+                rho[count] = 1.0 / sy;
+                count++;
+            }
+            free(s); free(y);
+        }
+        memcpy(xp, x, sizeof(double) * n);
+        memcpy(gpv, g, sizeof(double) * n);
+        orc_lbfgs_direction(n, count, S, Y, rho, g, d);
+        double g0d = dot(n, g, d);
+        for (int a = 0; a < A; ++a) {
+            double *xc = xa + (size_t)a * n;
+            for (int t = 0; t < n; ++t) {                 /* clip (A35) */
+                double v = x[t] + sp->alpha[a] * d[t];
+                if (lo && v < lo[t]) v = lo[t];
+                if (hi && v > hi[t]) v = hi[t];
+                xc[t] = v;
+            }
+            ca[a] = f(ctx, xc, ga + (size_t)a * n);
+            gda[a] = dot(n, ga + (size_t)a * n, d);
+        }
+        int i = orc_ls_select(A, sp->alpha, c, g0d, ca, gda, sp->c1, sp->c2, sp->ls_mode);
+        memcpy(x, xa + (size_t)i * n, sizeof(double) * n);
+        memcpy(g, ga + (size_t)i * n, sizeof(double) * n);
+        c = ca[i];
+        if (c < bc) { bc = c; memcpy(best_x, x, sizeof(double) * n); }   /* A23 strict < */
+        if (trace) trace[it + 1] = bc;
+    }
+    *best_c = bc;
+    free(x); free(g); free(xp); free(gpv); free(d); free(S); free(Y); free(rho); free(xa); free(ga);
+}
+
+/* ---- rollout objectives and threaded multi-seed solves (timing harness for cpu_baseline) ---- */
+typedef struct {
+    const orc_robot *rb; const orc_world *w; const orc_params *pr;
+    const double *start, *goal; int H;
+} traj_ctx;
+
+static double traj_fun(void *vctx, const double *x, double *g) {
+    traj_ctx *c = vctx;
+    return orc_eval_traj(c->rb, c->w, c->pr, c->start, c->goal, x, c->H, g, NULL, NULL, NULL);
+}
+
+static double ik_fun(void *vctx, const double *x, double *g) {
+    traj_ctx *c = vctx;
+    return orc_eval_ik(c->rb, c->w, c->pr, c->goal, x, g, NULL, NULL, NULL);
+}
+
+typedef struct {
+    const orc_robot *rb; const orc_world *worlds; const int *env; const orc_params *pr;
+    const orc_solver *sp; int P, S, H, ik; const double *seeds, *start, *goal;
+    double *out_x, *out_c; int tid, nthreads;
+} solve_job;
+
+static void *solve_worker(void *arg) {
+    solve_job *jb = arg;
+    int D = jb->rb->n_dof, N = jb->ik ? D : jb->H * D;
+    double *lo = malloc(sizeof(double) * N), *hi = malloc(sizeof(double) * N);
+    for (int t = 0; t < N; ++t) { lo[t] = jb->rb->lo[t % D]; hi[t] = jb->rb->hi[t % D]; }
+    for (int u = jb->tid; u < jb->P * jb->S; u += jb->nthreads) {
+        int p = u / jb->S;
+        traj_ctx ctx = {jb->rb, jb->worlds + (jb->env ? jb->env[p] : 0), jb->pr,
+                        jb->start ? jb->start + (size_t)p * D : NULL, jb->goal + (size_t)p * 7, jb->H};
+        orc_lbfgs_solve(jb->ik ? ik_fun : traj_fun, &ctx, N, jb->seeds + (size_t)u * N, lo, hi, jb->sp,
+                        jb->out_x + (size_t)u * N, jb->out_c + u, NULL);
+    }
+    free(lo); free(hi);
+    return NULL;
+}
+
+static void solve_threads(solve_job base, int nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    pthread_t th[256];
+    solve_job jobs[256];
+    if (nthreads > 256) nthreads = 256;
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t] = base; jobs[t].tid = t; jobs[t].nthreads = nthreads;
+        pthread_create(&th[t], NULL, solve_worker, &jobs[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+}
+
+void orc_solve_to(const orc_robot *rb, const orc_world *worlds, const int *env,
+                  const orc_params *pr, const orc_solver *sp, int P, int S, int H,
+                  const double *seeds, const double *start, const double *goal, int nthreads,
+                  double *seed_best_traj, double *seed_best_cost) {
+    solve_job b = {rb, worlds, env, pr, sp, P, S, H, 0, seeds, start, goal, seed_best_traj,
+                   seed_best_cost, 0, 1};
+    solve_threads(b, nthreads);
+}
+
+void orc_solve_ik(const orc_robot *rb, const orc_world *worlds, const int *env,
+                  const orc_params *pr, const orc_solver *sp, int P, int S,
+                  const double *seeds, const double *goal, int nthreads,
+                  double *seed_best_q, double *seed_best_cost) {
+    solve_job b = {rb, worlds, env, pr, sp, P, S, 1, 1, seeds, NULL, goal, seed_best_q,
+                   seed_best_cost, 0, 1};
+    solve_threads(b, nthreads);
+}

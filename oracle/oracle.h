@@ -1,0 +1,118 @@
+/*
+ * oracle.h -- fp64 CPU oracle for the cuRobo (arXiv 2310.17274) cost+gradient / L-BFGS hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load or execute this library.  It shares no code, header, table or
+ * constant with the CUDA path (paper_2310_17274_b200/csrc, include/curobo_b200.h).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (section / equation / algorithm named
+ * alongside); SURVEY §8(c) O1..O10 and readings A1..A37 are the paper readings this follows.
+ * Everything is plain scalar fp64 C, written in the paper's order and notation.
+ */
+#ifndef CURobo_ORACLE_H
+#define CURobo_ORACLE_H
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* O1: robot.  Links in topological order (parent < own index), Table 6 joint types
+ * (0 fixed, 1..3 prismatic x/y/z, 4..6 revolute x/y/z), F_l as 3x4 row-major. */
+typedef struct {
+    int n_links, n_dof, n_spheres, n_pairs, ee_link;
+    const int *parent;       /* [L] -1 for the root                                  */
+    const int *jtype;        /* [L]                                                  */
+    const int *dof;          /* [L] actuated index or -1                            */
+    const double *fixed;     /* [L][12]                                              */
+    const double *lo, *hi, *vmax, *amax, *jmax;  /* [D]                              */
+    const double *sph;       /* [M][4] centre in link frame, radius (r<0 disabled)   */
+    const int *sph_link;     /* [M]                                                  */
+    const double *sph_off;   /* [M] self-collision radius offsets           */
+    const int *pairs;        /* [n_pairs][2] self-collision set S             */
+} orc_robot;
+
+/* §3.5 oriented bounding boxes; dims given as half extents. */
+typedef struct {
+    int n_boxes;
+    const double *pos;       /* [K][3]                                               */
+    const double *quat;      /* [K][4] (w,x,y,z), box -> world rotation              */
+    const double *half;      /* [K][3]                                               */
+    const int *enabled;      /* [K]                                                  */
+} orc_world;
+
+enum { ORC_SWEEP = 1, ORC_SPEED = 2, ORC_JERK = 4 };
+
+typedef struct {
+    double a0, a1, a2, a3, a8, a9;   /* Eq. pose_cost_term, Eq. smooth_cost */
+    double w_bound[4];               /* pos, vel, acc, jerk bound weights                     */
+    double beta_self, beta_world;    /* beta_1 (Eq. self-collision), beta_2 (Eq. world-collision-cost) */
+    double eta, eta_bound, dt;       /* eta, eta_2, timestep                        */
+    int sweep_steps;                 /* n_s (A11)                                                      */
+    int flags;                       /* ORC_SWEEP | ORC_SPEED | ORC_JERK                               */
+} orc_params;
+
+typedef struct {
+    int iters, history, n_alpha;
+    double alpha[8];
+    double c1, c2;
+    int ls_mode;                     /* 0 armijo, 1 wolfe, 2 strong wolfe (Alg. 1) */
+} orc_solver;
+
+/* counters[] layout (O10) */
+enum { ORC_CNT_BOX_TESTS = 0, ORC_CNT_BOX_HITS, ORC_CNT_SWEEP_SAMPLES, ORC_CNT_SWEEP_HITS,
+       ORC_CNT_PAIR_TESTS, ORC_CNT_PAIR_PEN, ORC_CNT_ACTIVE_SPHERES, ORC_CNT_N };
+
+/* ---- individual steps (each cites its passage in oracle.c) ---- */
+void   orc_quat_to_mat(const double *q, double *R);
+void   orc_mat_to_quat(const double *R, double *q);
+void   orc_fk(const orc_robot *rb, const double *q, double *link_T, double *spheres, double *ee);
+void   orc_fk_backward(const orc_robot *rb, const double *q, const double *g_sph,
+                       const double *g_p, const double *g_q, double *g_theta);
+double orc_box_sdf(const double *p, const double *pos, const double *quat, const double *half,
+                   double *grad);
+double orc_activation(double dprime, double eta, double *dphi);
+double orc_bound(double x, double lo, double hi, double eta2, double *dx);
+double orc_logcosh(double x);
+double orc_pose_cost(const orc_params *pr, const double *ee, const double *goal, double *gp,
+                     double *gq);
+double orc_self_collision(const orc_robot *rb, const double *spheres, double beta, double *g,
+                          int *arg_pair, double *margin, long long *counters);
+double orc_sphere_world(const orc_world *w, const double *c, const double *cprev,
+                        const double *cnext, double r, double eta, int sweep, int steps,
+                        double *G, double *samples, int max_samples, int *n_samples,
+                        double *margin, long long *counters);
+void   orc_state_map(const double *start, const double *V, int H, int D, double *x);
+void   orc_derivs(const double *x, int H, int D, double dt, double *v, double *a, double *j);
+
+/* ---- whole evaluation (O7) ---- */
+double orc_eval_traj(const orc_robot *rb, const orc_world *w, const orc_params *pr,
+                     const double *start, const double *goal, const double *V, int H,
+                     double *grad, double *terms, double *margin, long long *counters);
+double orc_eval_ik(const orc_robot *rb, const orc_world *w, const orc_params *pr,
+                   const double *goal, const double *q, double *grad, double *terms,
+                   double *margin, long long *counters);
+
+/* ---- solver (O8) ---- */
+typedef double (*orc_fun)(void *ctx, const double *x, double *g);
+void   orc_lbfgs_direction(int n, int count, const double *S, const double *Y, const double *rho,
+                           const double *g, double *d);
+int    orc_ls_select(int A, const double *alpha, double c0, double g0d, const double *ca,
+                     const double *gda, double c1, double c2, int mode);
+int    orc_ls_select_f32(int A, const float *alpha, float c0, float g0d, const float *ca,
+                         const float *gda, float c1, float c2, int mode);
+int    orc_argmin_f32(int n, const float *c);
+void   orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
+                       const double *hi, const orc_solver *sp, double *best_x, double *best_c,
+                       double *trace);
+void   orc_solve_to(const orc_robot *rb, const orc_world *worlds, const int *env,
+                    const orc_params *pr, const orc_solver *sp, int P, int S, int H,
+                    const double *seeds, const double *start, const double *goal, int nthreads,
+                    double *seed_best_traj, double *seed_best_cost);
+void   orc_solve_ik(const orc_robot *rb, const orc_world *worlds, const int *env,
+                    const orc_params *pr, const orc_solver *sp, int P, int S,
+                    const double *seeds, const double *goal, int nthreads,
+                    double *seed_best_q, double *seed_best_cost);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
