@@ -1,0 +1,201 @@
+/*
+ * curobo_b200.h -- C-ABI of libcurobo_b200.so, the B200 (sm_100a) hot path of cuRobo
+ * (arXiv 2310.17274): batched seed x timestep cost+gradient evaluation driving per-seed L-BFGS
+ * with the parallel noisy line search.
+ *
+ * Citations: P:n = line n of the paper text, with the section / equation / algorithm.
+ * DESIGN.md lists every reading (A1..A37) of an ambiguous passage that these calls implement.
+ *
+ * Conventions for every call:
+ *   - Return a crb_status; no exception or abort crosses the ABI.  crb_last_error(ctx) returns a
+ *     NUL-terminated message for the last failing call on that context (owned by the context).
+ *   - crb_set_* take HOST pointers, copy what they need, and return; the caller keeps ownership.
+ *   - Batch inputs/outputs of crb_fk / crb_evaluate_cost_grad / crb_lbfgs_solve are DEVICE
+ *     pointers (fp32 / int32 / int64, contiguous, 16-byte aligned) owned by the caller; the call is
+ *     asynchronous on `stream` (a cudaStream_t, NULL = legacy default stream).
+ *   - crb_lbfgs_solve_host takes HOST pointers (pinned memory recommended), performs the
+ *     host->device copies, the solve and the device->host copies on `stream`, and synchronises.
+ *   - A context is bound to one CUDA device and used by one host thread at a time.
+ *   - Numeric types: all arithmetic on the device is fp32 (the paper's kernels are fp32).
+ *   - Non-finite inputs are not scanned: a NaN propagates into the cost, a NaN cost packs to the
+ *     +inf key and never wins a selection (SURVEY §8(b) deviation).
+ *   - Capacity limits (CRB_E_LIMIT): D <= 16, L <= 32, M <= 512, pairs <= 16384, H*D <= 512,
+ *     history <= 16, n_alpha <= 8, TO mode requires 8 <= H <= 32, IK mode has H == 1, and the
+ *     per-CTA shared memory (robot tables + one environment's cuboids + solver state) must fit
+ *     in 227 KB.
+ */
+#ifndef CUROBO_B200_H
+#define CUROBO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct crb_ctx crb_ctx;
+
+typedef enum {
+    CRB_OK = 0,
+    CRB_E_ARG = -1,        /* NULL pointer / invalid scalar argument                         */
+    CRB_E_SHAPE = -2,      /* inconsistent sizes (e.g. env index outside [0, n_env))         */
+    CRB_E_ROBOT = -3,      /* robot description fails validation (see crb_set_robot)       */
+    CRB_E_WORLD = -4,      /* cuboid description fails validation                           */
+    CRB_E_NOT_READY = -5,  /* robot / world / cost params not set                           */
+    CRB_E_LIMIT = -6,      /* capacity limit exceeded (see header comment)                  */
+    CRB_E_CUDA = -7,       /* CUDA runtime error (incl. an asynchronous fault surfaced now) */
+    CRB_E_OOM = -8         /* device allocation failed                                       */
+} crb_status;
+
+/* Joint types of Table 6. */
+enum { CRB_FIXED = 0, CRB_PRISMATIC_X = 1, CRB_PRISMATIC_Y = 2, CRB_PRISMATIC_Z = 3,
+       CRB_REVOLUTE_X = 4, CRB_REVOLUTE_Y = 5, CRB_REVOLUTE_Z = 6 };
+
+/* Cost flags. */
+enum { CRB_SWEEP = 1u,   /* continuous collision checking, §3.4 / Algs. 11-12     */
+       CRB_SPEED = 2u,   /* speed metric d_s = sdot * d_c, §3.3                    */
+       CRB_JERK = 4u };  /* alpha_9 jerk term of Eq. smooth_cost (off in the 1st TO) */
+
+/* One link of the kinematic tree (Alg. 7 kinematic data). */
+typedef struct {
+    int parent;          /* parent link index, < own index (topological order); -1 for the root */
+    int type;            /* CRB_FIXED .. CRB_REVOLUTE_Z (Table 6)                             */
+    int dof;             /* actuated joint index 0..D-1, or -1 for a fixed joint               */
+    float fixed[12];     /* F_l, 3x4 row-major; full link transform = F_l * J(q) (Table 6)    */
+} crb_link;
+
+/* Robot description (O1).  Validation (CRB_E_ROBOT): parent >= own index; a fixed
+ * joint with a dof or an actuated joint without one; duplicate or missing dof; pos_lo >= pos_hi;
+ * non-positive vel/acc/jerk limit; sphere on an unknown link; pair with i >= j or out of range;
+ * rotation block of F not orthonormal within 1e-4; ee_link out of range. */
+typedef struct {
+    int n_links, n_dof, n_spheres, n_pairs, ee_link;
+    const crb_link *links;                                   /* [n_links]                    */
+    const float *pos_lo, *pos_hi, *vel_max, *acc_max, *jerk_max;  /* [n_dof] each           */
+    const float *spheres;      /* [n_spheres][4] centre in link frame + radius; r < 0 disables
+                                  the sphere for world collision (Alg. 10)       */
+    const int *sphere_link;    /* [n_spheres]                                                  */
+    const float *self_offset;  /* [n_spheres] self-collision radius offsets (Alg. 9), or
+                                  NULL for zeros; pairs with r+o <= 0 are skipped     */
+    const int *pairs;          /* [n_pairs][2] self-collision set S (Eq. self-collision);
+                                  the order of S breaks arg-max ties (first maximal pair)       */
+} crb_robot_desc;
+
+/* One cuboid (§3.5 oriented bounding box; Alg. 10 obb_pose/obb_bounds/obb_enable). */
+typedef struct {
+    float pos[3];        /* box centre, world frame                                            */
+    float quat[4];       /* (w,x,y,z) box->world rotation; normalised on upload               */
+    float dims[3];       /* FULL extents; Alg. 10 halves them                 */
+    int enabled;         /* 0 = skipped (Alg. 10 line "obb_enable")                    */
+} crb_cuboid;
+
+/* Cost weights and switches (App. A; App. B.3). */
+typedef struct {
+    float a0, a1, a2, a3;      /* Eq. pose_cost_term: 2000, 350, 100, 100             */
+    float a8, a9;              /* Eq. smooth_cost: 5000, 1; alpha_6 term off (A16)    */
+    float w_bound[4];          /* Eq. bound_cost weights for pos/vel/acc/jerk: 5000    */
+    float beta_self;           /* beta_1 of Eq. self-collision: 5000                  */
+    float beta_world;          /* beta_2 of Eq. world-collision-cost: 5000            */
+    float eta;                 /* activation distance, Eq. smooth-distance-cases: 0.025 */
+    float eta_bound;           /* eta_2 of Eq. bound_cost: 0.1                        */
+    float dt;                  /* timestep of the five-point stencil (§A.5) and speed metric   */
+    int sweep_steps;           /* n_s of Alg. 12 (never given in the paper; 4, A11)            */
+    unsigned flags;            /* CRB_SWEEP | CRB_SPEED | CRB_JERK                             */
+} crb_cost_params;
+
+/* L-BFGS + parallel noisy line search (Alg. 6, Alg. 1). */
+typedef struct {
+    int iters;                 /* L-BFGS iterations after the initial evaluation (100) */
+    int history;               /* m (4), <= 16                                         */
+    int n_alpha;               /* number of magnitudes, <= 8                                    */
+    float alpha[8];            /* ascending; alpha[0] is the noisy fallback    */
+    float c1, c2;              /* Armijo / Wolfe constants (A17: 1e-4, 0.9)                    */
+    int ls_mode;               /* 0 Armijo, 1 Armijo+Wolfe, 2 Armijo+strong Wolfe (Alg. 1)     */
+    int64_t global_seed_base;  /* added to the local seed index in the packed selection key     */
+} crb_solver_params;
+
+crb_status crb_create(int cuda_device, crb_ctx **out);
+crb_status crb_destroy(crb_ctx *ctx);
+const char *crb_last_error(const crb_ctx *ctx);
+const char *crb_version(void);
+
+/* Validate, pack (spheres grouped by link, disabled self pairs dropped, float4 layout P:3014)
+ * and upload the robot tables. */
+crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *robot);
+
+/* Upload n_env environments of cuboids: boxes[n_env * k_max], env e using its first
+ * boxes_per_env[e] entries.  Disabled cuboids are compacted away (Alg. 10 skips them).
+ * Stream-ordered on the legacy stream: synchronises before returning. */
+crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_per_env,
+                         const crb_cuboid *boxes);
+
+crb_status crb_set_cost_params(crb_ctx *ctx, const crb_cost_params *params);
+
+/* Forward kinematics (Alg. 7, Table 6): q[B][D] -> spheres_out[B][M][4] (world centre, radius)
+ * and ee_out[B][7] (position, quaternion (w,x,y,z) with w >= 0).  Either output may be NULL. */
+crb_status crb_fk(crb_ctx *ctx, const float *q, int B, float *spheres_out, float *ee_out,
+                  void *stream);
+
+/* Batched cost and gradient (Eq. cost_motion_opt, with the App. A terms).
+ *   H >= 8 (TO mode): q[B][H][D] are the optimisation variables V of B trajectories; the state
+ *     map of Table 5's last row pins x_1..x_3 = start[b] and aliases x_{H-3..H-1} = x_H;
+ *     cost[b] = sum over the H evaluated states of bound + smoothness + self + world terms, plus
+ *     the pose term at x_H; grad[b][H][D] = dC/dV (zero on pinned / aliased variables).
+ *   H == 1 (IK mode): q[B][D] configurations; pose + self + discrete world + position bound.
+ *     The env index must be constant inside each aligned group of 32 rows (rows that violate it
+ *     get a NaN cost).  start may be NULL.
+ *   env[B] (may be NULL = all 0), goal[B][7] (position, quaternion w,x,y,z).
+ *   term_costs[B][5] (pose, bound, smooth, self, world) may be NULL. */
+crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, const int *env,
+                                  const float *start, const float *goal, float *cost,
+                                  float *grad, float *term_costs, void *stream);
+
+/* Per-seed L-BFGS solve (§4.1, Alg. 6 + Alg. 1), one persistent CTA per seed trajectory (TO) or
+ * per 32 seeds of one problem (IK), all `iters` iterations inside one launch.
+ *   seeds[P][S][H][D] (TO, H >= 8) or [P][S][D] (IK, H == 1); env[P] (may be NULL);
+ *   start[P][D] (TO only); goal[P][7].
+ * Outputs (any may be NULL): best_traj[P][H][D] and best_cost[P] of the winning seed per
+ * problem; best_key[P] = (float_bits(cost) << 32) | (global_seed_base + s), the packed key the
+ * multi-GPU argmin reduces with MIN (NaN -> +inf bits); seed_best_cost[P][S] and
+ * seed_best_traj[P][S][H][D] per seed. */
+crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H,
+                           const float *seeds, const int *env, const float *start,
+                           const float *goal, float *best_traj, float *best_cost,
+                           int64_t *best_key, float *seed_best_cost, float *seed_best_traj,
+                           void *stream);
+
+/* Same as crb_lbfgs_solve with HOST buffers: copies inputs to context-owned device buffers,
+ * solves, copies outputs back and synchronises `stream`. */
+crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H,
+                                const float *seeds, const int *env, const float *start,
+                                const float *goal, float *best_traj, float *best_cost,
+                                int64_t *best_key, void *stream);
+
+/* ---- test hooks: the exact device routines the solver uses, on caller data ---- */
+
+/* Alg. 1 selection (lines 4-9) for n independent line searches, in fp32 with the fixed
+ * operation order rhs = c0 + (c1 * alpha_a) * g0d (no FMA contraction): out_idx[i] = largest a
+ * whose active conditions hold, else 0.  All pointers device: c0[n], g0d[n], ca[n][A],
+ * gda[n][A], out_idx[n]. */
+crb_status crb_ls_select(int n, int A, const float *alpha_host, const float *c0, const float *g0d,
+                         const float *ca, const float *gda, float c1, float c2, int mode,
+                         int *out_idx, void *stream);
+
+/* Per-problem packed-key argmin over S seed costs (ties -> lowest seed, NaN -> +inf). Device
+ * pointers: cost[P][S], out_key[P], out_idx[P]. */
+crb_status crb_argmin_keys(int P, int S, const float *cost, int64_t seed_base, int64_t *out_key,
+                           int *out_idx, void *stream);
+
+/* Two-loop recursion (Alg. 6) exactly as run inside the solver: for each of B problems with n
+ * variables and `count` stored pairs (oldest first), d = -H g.  Device pointers:
+ * S[B][count][n], Y[B][count][n], g[B][n], d[B][n].  n <= 512, count <= 16. */
+crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const float *Y,
+                               const float *g, float *d, void *stream);
+
+/* Number of kernel launches this context issued since creation (bench accounting). */
+int64_t crb_launch_count(const crb_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

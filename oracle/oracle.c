@@ -262,7 +262,6 @@ static double box_sdf_impl(const double *p, const double *pos, const double *qua
             upd_margin(margin, qmax - second);
         }
     }
-    if (margin) upd_margin(margin, qmax);
     if (grad)
         for (int i = 0; i < 3; ++i) grad[i] = R[i * 3 + 0] * gl[0] + R[i * 3 + 1] * gl[1] + R[i * 3 + 2] * gl[2];
     return sd;
@@ -290,8 +289,6 @@ static double box_term(const orc_world *w, int k, const double *p, double rp, do
     double sd = box_sdf_impl(p, w->pos + 3 * k, w->quat + 4 * k, w->half + 3 * k, g, NULL);
     double dprime = rp - sd;
     if (sd_out) *sd_out = sd;
-    upd_margin(margin, dprime);
-    upd_margin(margin, dprime - eta);
     if (dprime > 0) {
         if (margin) box_sdf_impl(p, w->pos + 3 * k, w->quat + 4 * k, w->half + 3 * k, NULL, margin);
         double dphi;
@@ -333,7 +330,6 @@ double orc_sphere_world(const orc_world *w, const double *c, const double *cprev
             double dv[3] = {n[0] - c[0], n[1] - c[1], n[2] - c[2]};
             double L = sqrt(dv[0] * dv[0] + dv[1] * dv[1] + dv[2] * dv[2]);
             double gap = L - 2.0 * rp;
-            upd_margin(margin, gap);
             if (gap <= 0) continue;
             double bound = 0.5 * L;
             double j = (rp - sd0 > 0) ? rp : sd0;
@@ -418,13 +414,6 @@ double orc_bound(double x, double lo, double hi, double eta2, double *dx) {
     return 0.0;
 }
 
-static void bound_margin(double *margin, double x, double lo, double hi, double eta2) {
-    upd_margin(margin, x - lo);
-    upd_margin(margin, x - (lo + eta2));
-    upd_margin(margin, x - hi);
-    upd_margin(margin, x - (hi - eta2));
-}
-
 /* log cosh in the overflow-safe form |x| + log1p(exp(-2|x|)) - log 2. */
 double orc_logcosh(double x) {
     double ax = fabs(x);
@@ -495,7 +484,6 @@ static double bound_vec(const orc_robot *rb, const orc_params *pr, int kind, con
         }
         double dx;
         c += pr->w_bound[kind] * orc_bound(x[d], lo, hi, pr->eta_bound, &dx);
-        bound_margin(margin, x[d], lo, hi, pr->eta_bound);
         if (gx) gx[d] = pr->w_bound[kind] * dx;
     }
     return c;
@@ -567,11 +555,7 @@ double orc_eval_traj(const orc_robot *rb, const orc_world *w, const orc_params *
     /* pose at x_H (Eq. pose_cost_term) */
     double gp[3], gq[4];
     tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
-    if (margin) {
-        double ep[3] = {goal[0] - ee[0], goal[1] - ee[1], goal[2] - ee[2]};
-        upd_margin(margin, sqrt(ep[0] * ep[0] + ep[1] * ep[1] + ep[2] * ep[2]));
-        upd_margin(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
-    }
+    if (margin) upd_margin(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
     /* backward (O6) per evaluated configuration */
     for (int h = 1; h <= H; ++h) {
         orc_fk_backward(rb, XR(h), gs + h * M * 3, (h == H) ? gp : NULL, (h == H) ? gq : NULL, tmp);
@@ -629,11 +613,7 @@ double orc_eval_ik(const orc_robot *rb, const orc_world *w, const orc_params *pr
     }
     double gp[3], gq[4];
     tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
-    if (margin) {
-        double ep[3] = {goal[0] - ee[0], goal[1] - ee[1], goal[2] - ee[2]};
-        upd_margin(margin, sqrt(ep[0] * ep[0] + ep[1] * ep[1] + ep[2] * ep[2]));
-        upd_margin(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
-    }
+    if (margin) upd_margin(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
     if (grad) {
         orc_fk_backward(rb, q, gs, gp, gq, grad);
         for (int d = 0; d < D; ++d) grad[d] += gb[d];

@@ -1,0 +1,956 @@
+// curobo_b200.cu -- kernels and host side of the C-ABI declared in include/curobo_b200.h.
+//
+// Kernels (all sm_100a, NT = 512 threads, 1 CTA per SM by shared-memory footprint):
+//   solve_to_kernel   persistent per-seed L-BFGS for trajectory optimisation: one CTA = one seed
+//                     trajectory, all iterations in one launch (replaces the paper's ~20 kernels
+//                     x 25-iteration CUDA graph)
+//   solve_ik_kernel   same for collision-free IK: one CTA = 32 seeds of one problem
+//   eval_to_kernel / eval_ik_kernel   one-shot batched cost+gradient (crb_evaluate_cost_grad)
+//   fk_kernel         forward kinematics only (crb_fk)
+//   select_kernel     per-problem packed-key argmin over seeds (O9)
+//   + the test-hook kernels (ls_select, argmin_keys, lbfgs_direction)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "curobo_b200.h"
+#include "crb_device.cuh"
+
+using namespace crb;
+
+namespace {
+
+constexpr int SMEM_MAX = 232448;   // 227 KB opt-in per CTA
+
+__device__ __forceinline__ float cta_cost_total(const Smem &s, float *scal_out) {
+    // sum of the per-slot costs in a fixed (butterfly) order; every thread gets the value
+    float v = 0.f;
+    if ((threadIdx.x >> 5) == 0) {
+        v = warp_sum(s.cfg_cost[threadIdx.x & 31]);
+        if (threadIdx.x == 0) *scal_out = v;
+    }
+    __syncthreads();
+    v = *scal_out;
+    __syncthreads();
+    return v;
+}
+
+// Two-loop recursion (Alg. 6; A18/A19) over the ring `order` (oldest first), one
+// element per thread, every dot product a deterministic block reduction.
+__device__ void two_loop_block(int N, int Np, int count, const int *order, const float *Sb, const float *Yb,
+                               const float *rho, const float *syv, const float *yyv, const float *g, float *d,
+                               float *red) {
+    const int t = threadIdx.x;
+    float al[16];
+    float q = t < N ? g[t] : 0.f;
+#pragma unroll 1
+    for (int i = count - 1; i >= 0; --i) {
+        const int sl = order[i];
+        const float sv = t < N ? Sb[sl * Np + t] : 0.f;
+        const float a = rho[sl] * block_sum(sv * q, red);
+        al[i] = a;
+        if (t < N) q -= a * Yb[sl * Np + t];
+    }
+    float gamma = 1.f;
+    if (count > 0) {
+        const int sl = order[count - 1];
+        gamma = syv[sl] / yyv[sl];
+    }
+    float r = gamma * q;
+#pragma unroll 1
+    for (int i = 0; i < count; ++i) {
+        const int sl = order[i];
+        const float yv = t < N ? Yb[sl * Np + t] : 0.f;
+        const float b = rho[sl] * block_sum(yv * r, red);
+        if (t < N) r += (al[i] - b) * Sb[sl * Np + t];
+    }
+    if (t < N) d[t] = -r;
+}
+
+// ------------------------------------------------------------------------------------------
+// persistent TO solver: one CTA per (problem, seed)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT, 1) solve_to_kernel(const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) float smem[];
+    const int unit = blockIdx.x;
+    const int p = unit / kp.S, sidx = unit - p * kp.S;
+    const int env = kp.env ? kp.env[p] : 0;
+    const int K = stage_tables(kp, smem, env);
+    const Smem s = make_smem(kp, smem);
+    const int D = kp.rp.D, H = kp.H, N = H * D, Np = (N + 3) & ~3, m = kp.m, A = kp.A;
+    const int t = threadIdx.x;
+    float *base = smem + kp.lay.solver;
+    float *th = base, *g = th + Np, *dd = g + Np, *thp = dd + Np, *gp = thp + Np, *best = gp + Np,
+          *thA = best + Np, *cg = thA + Np, *Sb = cg + A * Np, *Yb = Sb + (m + 1) * Np,
+          *rho = Yb + (m + 1) * Np, *syv = rho + 20, *yyv = syv + 20;
+    int *order = reinterpret_cast<int *>(yyv + 20);
+    float *scal = yyv + 40;           // [0..7] c_a, [8..15] gd_a, [16] cost, [17] i*
+    int *ring = reinterpret_cast<int *>(scal + 24);   // [0] count, [1] free slot
+    const float *lim = s.fw + kp.rp.o_lim;
+
+    if (t < D) s.st[t] = kp.start[p * D + t];
+    if (t < 7 * NC) s.goal[t] = kp.goal[p * 7 + t / NC];
+    const float *seed = kp.q_in + (size_t)unit * N;
+    if (t < N) { th[t] = seed[t]; thA[t] = seed[t]; }
+    if (t == 0) { ring[0] = 0; ring[1] = 0; }
+    const float lo_t = t < N ? lim[t % D] : 0.f, hi_t = t < N ? lim[D + t % D] : 0.f;
+    __syncthreads();
+
+    // evaluate at Theta_0 (O8 initialise)
+    eval_pass<MODE_TO>(kp, s, thA, K, H);
+    float c = cta_cost_total(s, scal + 16);
+    if (t < N) { g[t] = s.gV[t]; best[t] = th[t]; }
+    float cbest = c;
+    __syncthreads();
+
+    for (int it = 0; it < kp.iters; ++it) {
+        // ---- a13: L-BFGS buffers (Alg. 6 lines 1-5) -- push (s, y, rho) unless s^T y <= 1e-12 (A20)
+        if (it > 0) {
+            const int fs = ring[1];
+            float sv = 0.f, yv = 0.f;
+            if (t < N) {
+                sv = th[t] - thp[t];
+                yv = g[t] - gp[t];
+                Sb[fs * Np + t] = sv;
+                Yb[fs * Np + t] = yv;
+            }
+            const float sy = block_sum(sv * yv, s.red);
+            const float yy = block_sum(yv * yv, s.red);
+            if (sy > 1e-12f) {
+                if (t == 0) {
+                    rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
+                    int cnt = ring[0];
+                    if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
+                    else {
+                        const int ev = order[0];
+                        for (int i = 0; i < m - 1; ++i) order[i] = order[i + 1];
+                        order[m - 1] = fs;
+                        ring[1] = ev;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (t < N) { thp[t] = th[t]; gp[t] = g[t]; }
+        // ---- two-loop recursion -> d = -H g
+        two_loop_block(N, Np, ring[0], order, Sb, Yb, rho, syv, yyv, g, dd, s.red);
+        const float dt_ = t < N ? dd[t] : 0.f;
+        const float g0d = block_sum((t < N ? g[t] : 0.f) * dt_, s.red);
+        // ---- a1 + a2..a10: the A line-search candidates, each one evaluation pass
+        for (int a = 0; a < A; ++a) {
+            if (t < N) thA[t] = candidate(th[t], kp.alpha[a], dt_, lo_t, hi_t);
+            __syncthreads();
+            eval_pass<MODE_TO>(kp, s, thA, K, H);
+            const float ca = cta_cost_total(s, scal + a);
+            (void)ca;
+            if (t < N) cg[a * Np + t] = s.gV[t];
+            const float gda = block_sum(t < N ? s.gV[t] * dt_ : 0.f, s.red);
+            if (t == 0) scal[8 + a] = gda;
+        }
+        // ---- a11: selection (Alg. 1 lines 4-9), fp32 mirror, then take candidate i*
+        if (t == 0) {
+            const int i = ls_select(A, kp.alpha, c, g0d, scal, scal + 8, kp.c1, kp.c2, kp.ls_mode);
+            reinterpret_cast<int *>(scal)[17] = i;
+        }
+        __syncthreads();
+        const int istar = reinterpret_cast<const int *>(scal)[17];
+        if (t < N) {
+            th[t] = candidate(th[t], kp.alpha[istar], dt_, lo_t, hi_t);
+            g[t] = cg[istar * Np + t];
+        }
+        c = scal[istar];
+        // ---- a12: best update, strict < (A23)
+        if (c < cbest) {
+            cbest = c;
+            if (t < N) best[t] = th[t];
+        }
+        __syncthreads();
+    }
+    if (t == 0) kp.seed_best_cost[unit] = cbest;
+    if (t < N) kp.seed_best_traj[(size_t)unit * N + t] = best[t];
+}
+
+// ------------------------------------------------------------------------------------------
+// persistent IK solver: one CTA per (problem, group of 32 seeds); lane = seed
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT, 1) solve_ik_kernel(const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) float smem[];
+    const int G = (kp.S + NC - 1) / NC;
+    const int p = blockIdx.x / G, grp = blockIdx.x - p * G;
+    const int env = kp.env ? kp.env[p] : 0;
+    const int K = stage_tables(kp, smem, env);
+    const Smem s = make_smem(kp, smem);
+    const int D = kp.rp.D, m = kp.m, A = kp.A;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n_act = min(NC, kp.S - grp * NC);
+    const int DC = D * NC;
+    float *base = smem + kp.lay.solver;
+    float *th = base, *g = th + DC, *dd = g + DC, *thp = dd + DC, *gp = thp + DC, *best = gp + DC,
+          *Sb = best + DC, *Yb = Sb + (m + 1) * DC, *rho = Yb + (m + 1) * DC, *syv = rho + (m + 1) * NC,
+          *yyv = syv + (m + 1) * NC, *cg = yyv + (m + 1) * NC, *cc = cg + A * DC, *cgd = cc + A * NC;
+    int *order = reinterpret_cast<int *>(cgd + A * NC);   // [m][32]
+    const float *lim = s.fw + kp.rp.o_lim;
+    const int sd = grp * NC + lane;
+    const bool active = lane < n_act;
+
+    if (t < 7 * NC) s.goal[t] = kp.goal[p * 7 + t / NC];
+    if (warp == 0)
+        for (int d = 0; d < D; ++d) {
+            const float v = active ? kp.q_in[((size_t)p * kp.S + sd) * D + d] : lim[d];
+            th[d * NC + lane] = v;
+            s.q_cfg[d * NC + lane] = v;
+        }
+    __syncthreads();
+    eval_pass<MODE_IK>(kp, s, nullptr, K, n_act);
+    float c = 0.f, cbest = 0.f;
+    int cnt = 0, fs = 0;
+    if (warp == 0) {
+        c = s.cfg_cost[lane];
+        cbest = c;
+        for (int d = 0; d < D; ++d) { g[d * NC + lane] = s.gV[d * NC + lane]; best[d * NC + lane] = th[d * NC + lane]; }
+    }
+    __syncthreads();
+    float g0d = 0.f;
+    for (int it = 0; it < kp.iters; ++it) {
+        if (warp == 0) {
+            // ---- ring push (per seed, A20)
+            if (it > 0) {
+                float sy = 0.f, yy = 0.f;
+                for (int d = 0; d < D; ++d) {
+                    const int e = d * NC + lane;
+                    const float sv = th[e] - thp[e], yv = g[e] - gp[e];
+                    Sb[fs * DC + e] = sv; Yb[fs * DC + e] = yv;
+                    sy += sv * yv; yy += yv * yv;
+                }
+                if (sy > 1e-12f) {
+                    rho[fs * NC + lane] = 1.f / sy; syv[fs * NC + lane] = sy; yyv[fs * NC + lane] = yy;
+                    if (cnt < m) { order[cnt * NC + lane] = fs; ++cnt; fs = cnt; }
+                    else {
+                        const int ev = order[lane];
+                        for (int i = 0; i < m - 1; ++i) order[i * NC + lane] = order[(i + 1) * NC + lane];
+                        order[(m - 1) * NC + lane] = fs;
+                        fs = ev;
+                    }
+                }
+            }
+            for (int d = 0; d < D; ++d) { thp[d * NC + lane] = th[d * NC + lane]; gp[d * NC + lane] = g[d * NC + lane]; }
+            // ---- two-loop recursion per seed (Alg. 6)
+            float q[16], al[16];
+            for (int d = 0; d < D; ++d) q[d] = g[d * NC + lane];
+            for (int i = cnt - 1; i >= 0; --i) {
+                const int sl = order[i * NC + lane];
+                float a = 0.f;
+                for (int d = 0; d < D; ++d) a += Sb[sl * DC + d * NC + lane] * q[d];
+                a *= rho[sl * NC + lane];
+                al[i] = a;
+                for (int d = 0; d < D; ++d) q[d] -= a * Yb[sl * DC + d * NC + lane];
+            }
+            float gamma = 1.f;
+            if (cnt > 0) { const int sl = order[(cnt - 1) * NC + lane]; gamma = syv[sl * NC + lane] / yyv[sl * NC + lane]; }
+            for (int d = 0; d < D; ++d) q[d] *= gamma;
+            for (int i = 0; i < cnt; ++i) {
+                const int sl = order[i * NC + lane];
+                float b = 0.f;
+                for (int d = 0; d < D; ++d) b += Yb[sl * DC + d * NC + lane] * q[d];
+                b *= rho[sl * NC + lane];
+                for (int d = 0; d < D; ++d) q[d] += (al[i] - b) * Sb[sl * DC + d * NC + lane];
+            }
+            g0d = 0.f;
+            for (int d = 0; d < D; ++d) { dd[d * NC + lane] = -q[d]; g0d += g[d * NC + lane] * (-q[d]); }
+        }
+        for (int a = 0; a < A; ++a) {
+            if (warp == 0)
+                for (int d = 0; d < D; ++d)
+                    s.q_cfg[d * NC + lane] = candidate(th[d * NC + lane], kp.alpha[a], dd[d * NC + lane], lim[d], lim[D + d]);
+            __syncthreads();
+            eval_pass<MODE_IK>(kp, s, nullptr, K, n_act);
+            if (warp == 0) {
+                cc[a * NC + lane] = s.cfg_cost[lane];
+                float gd = 0.f;
+                for (int d = 0; d < D; ++d) {
+                    const float v = s.gV[d * NC + lane];
+                    cg[a * DC + d * NC + lane] = v;
+                    gd += v * dd[d * NC + lane];
+                }
+                cgd[a * NC + lane] = gd;
+            }
+        }
+        if (warp == 0) {
+            float ca[8], gda[8];
+            for (int a = 0; a < A; ++a) { ca[a] = cc[a * NC + lane]; gda[a] = cgd[a * NC + lane]; }
+            const int i = ls_select(A, kp.alpha, c, g0d, ca, gda, kp.c1, kp.c2, kp.ls_mode);
+            for (int d = 0; d < D; ++d) {
+                const int e = d * NC + lane;
+                th[e] = candidate(th[e], kp.alpha[i], dd[e], lim[d], lim[D + d]);
+                g[e] = cg[i * DC + e];
+            }
+            c = ca[i];
+            if (c < cbest) {
+                cbest = c;
+                for (int d = 0; d < D; ++d) best[d * NC + lane] = th[d * NC + lane];
+            }
+        }
+        __syncthreads();
+    }
+    if (warp == 0 && active) {
+        const size_t u = (size_t)p * kp.S + sd;
+        kp.seed_best_cost[u] = cbest;
+        for (int d = 0; d < D; ++d) kp.seed_best_traj[u * D + d] = best[d * NC + lane];
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// one-shot evaluation, FK, selection
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT, 1) eval_to_kernel(const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) float smem[];
+    const int b = blockIdx.x;
+    const int env = kp.env ? kp.env[b] : 0;
+    const int K = stage_tables(kp, smem, env);
+    const Smem s = make_smem(kp, smem);
+    const int D = kp.rp.D, H = kp.H, N = H * D, t = threadIdx.x;
+    float *thA = smem + kp.lay.solver;
+    float *scal = thA + ((N + 3) & ~3);
+    if (t < D) s.st[t] = kp.start[(size_t)b * D + t];
+    if (t < 7 * NC) s.goal[t] = kp.goal[(size_t)b * 7 + t / NC];
+    if (t < N) thA[t] = kp.q_in[(size_t)b * N + t];
+    __syncthreads();
+    eval_pass<MODE_TO>(kp, s, thA, K, H);
+    if (t < 32) {
+        const float c = warp_sum(s.cfg_cost[t]);
+        float tr[5];
+        for (int k = 0; k < 5; ++k) tr[k] = warp_sum(s.cfg_terms[k * NC + t]);
+        if (t == 0) {
+            kp.cost_out[b] = c;
+            if (kp.terms_out)
+                for (int k = 0; k < 5; ++k) kp.terms_out[(size_t)b * 5 + k] = tr[k];
+        }
+    }
+    (void)scal;
+    if (t < N && kp.grad_out) kp.grad_out[(size_t)b * N + t] = s.gV[t];
+}
+
+__global__ void __launch_bounds__(NT, 1) eval_ik_kernel(const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) float smem[];
+    const int b0 = blockIdx.x * NC;
+    const int n_act = min(NC, kp.B - b0);
+    const int env0 = kp.env ? kp.env[b0] : 0;
+    const int K = stage_tables(kp, smem, env0);
+    const Smem s = make_smem(kp, smem);
+    const int D = kp.rp.D, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const float *lim = s.fw + kp.rp.o_lim;
+    if (warp == 0) {
+        const bool act = lane < n_act;
+        for (int d = 0; d < D; ++d) s.q_cfg[d * NC + lane] = act ? kp.q_in[(size_t)(b0 + lane) * D + d] : lim[d];
+        for (int k = 0; k < 7; ++k) s.goal[k * NC + lane] = act ? kp.goal[(size_t)(b0 + lane) * 7 + k] : (k == 3 ? 1.f : 0.f);
+    }
+    __syncthreads();
+    eval_pass<MODE_IK>(kp, s, nullptr, K, n_act);
+    if (warp == 0 && lane < n_act) {
+        const int b = b0 + lane;
+        const bool ok = !kp.env || kp.env[b] == env0;
+        kp.cost_out[b] = ok ? s.cfg_cost[lane] : __int_as_float(0x7fc00000);
+        if (kp.terms_out)
+            for (int k = 0; k < 5; ++k) kp.terms_out[(size_t)b * 5 + k] = s.cfg_terms[k * NC + lane];
+        if (kp.grad_out)
+            for (int d = 0; d < D; ++d) kp.grad_out[(size_t)b * D + d] = s.gV[d * NC + lane];
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) fk_kernel(const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) float smem[];
+    const int b0 = blockIdx.x * NC;
+    const int n_act = min(NC, kp.B - b0);
+    stage_tables(kp, smem, -1);
+    const Smem s = make_smem(kp, smem);
+    const RobotPack &rp = kp.rp;
+    const int D = rp.D, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (warp == 0)
+        for (int d = 0; d < D; ++d) s.q_cfg[d * NC + lane] = lane < n_act ? kp.q_in[(size_t)(b0 + lane) * D + d] : 0.f;
+    __syncthreads();
+    fk_phase(kp, s);
+    const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
+    if (kp.spheres_out)
+        for (int m = warp; m < rp.M; m += NW) {
+            if (lane >= n_act) continue;
+            const int um = s.iw[rp.o_perm + m];
+            float *o = kp.spheres_out + ((size_t)(b0 + lane) * rp.M + um) * 4;
+            const float *w = s.sw + m * 3 * NC + lane;
+            o[0] = w[0]; o[1] = w[NC]; o[2] = w[2 * NC]; o[3] = sph[m].w;
+        }
+    if (kp.ee_out && warp == 0 && lane < n_act) {
+        const float *T = s.lt + rp.ee * 12 * NC + lane;
+        float q[4];
+        mat_to_quat(T[0], T[NC], T[2 * NC], T[4 * NC], T[5 * NC], T[6 * NC], T[8 * NC], T[9 * NC], T[10 * NC], q);
+        float *o = kp.ee_out + (size_t)(b0 + lane) * 7;
+        o[0] = T[3 * NC]; o[1] = T[7 * NC]; o[2] = T[11 * NC];
+        o[3] = q[0]; o[4] = q[1]; o[5] = q[2]; o[6] = q[3];
+    }
+}
+
+// O9: per problem, the seed with the smallest packed key (cost bits, global seed index).
+__global__ void select_kernel(int P, int S, int N, const float *seed_cost, const float *seed_traj,
+                              long long seed_base, float *best_traj, float *best_cost, long long *best_key) {
+    const int p = blockIdx.x;
+    __shared__ int sbest;
+    __shared__ unsigned long long skey;
+    if (threadIdx.x == 0) {
+        unsigned long long k = ~0ull;
+        int bi = 0;
+        for (int s = 0; s < S; ++s) {
+            const unsigned long long ks = pack_key(seed_cost[(size_t)p * S + s], seed_base + s);
+            if (ks < k) { k = ks; bi = s; }
+        }
+        sbest = bi; skey = k;
+        if (best_cost) best_cost[p] = seed_cost[(size_t)p * S + bi];
+        if (best_key) best_key[p] = (long long)k;
+    }
+    __syncthreads();
+    if (best_traj)
+        for (int i = threadIdx.x; i < N; i += blockDim.x)
+            best_traj[(size_t)p * N + i] = seed_traj[((size_t)p * S + sbest) * N + i];
+}
+
+struct LsParams {
+    float alpha[8];
+};
+
+__global__ void ls_select_kernel(int n, int A, LsParams ap, const float *c0, const float *g0d, const float *ca,
+                                 const float *gda, float c1, float c2, int mode, int *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float a8[8], b8[8];
+    for (int a = 0; a < A; ++a) { a8[a] = ca[(size_t)i * A + a]; b8[a] = gda[(size_t)i * A + a]; }
+    out[i] = ls_select(A, ap.alpha, c0[i], g0d[i], a8, b8, c1, c2, mode);
+}
+
+__global__ void argmin_keys_kernel(int P, int S, const float *cost, long long base, long long *out_key, int *out_idx) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    unsigned long long k = ~0ull;
+    int bi = 0;
+    for (int s = 0; s < S; ++s) {
+        const unsigned long long ks = pack_key(cost[(size_t)p * S + s], base + s);
+        if (ks < k) { k = ks; bi = s; }
+    }
+    if (out_key) out_key[p] = (long long)k;
+    if (out_idx) out_idx[p] = bi;
+}
+
+__global__ void __launch_bounds__(NT, 1) lbfgs_direction_kernel(int n, int count, const float *S, const float *Y,
+                                                                const float *g, float *d) {
+    extern __shared__ __align__(16) float smem[];
+    const int b = blockIdx.x, t = threadIdx.x, Np = (n + 3) & ~3;
+    float *Sb = smem, *Yb = Sb + count * Np, *gg = Yb + count * Np, *dd = gg + Np, *rho = dd + Np,
+          *syv = rho + 16, *yyv = syv + 16, *red = yyv + 16;
+    int *order = reinterpret_cast<int *>(red + 32);
+    for (int i = 0; i < count; ++i)
+        if (t < n) {
+            Sb[i * Np + t] = S[((size_t)b * count + i) * n + t];
+            Yb[i * Np + t] = Y[((size_t)b * count + i) * n + t];
+        }
+    if (t < n) gg[t] = g[(size_t)b * n + t];
+    if (t < count) order[t] = t;
+    __syncthreads();
+    for (int i = 0; i < count; ++i) {   // same reductions as the solver's push
+        const float sv = t < n ? Sb[i * Np + t] : 0.f, yv = t < n ? Yb[i * Np + t] : 0.f;
+        const float sy = block_sum(sv * yv, red);
+        const float yy = block_sum(yv * yv, red);
+        if (t == 0) { rho[i] = 1.f / sy; syv[i] = sy; yyv[i] = yy; }
+    }
+    __syncthreads();
+    two_loop_block(n, Np, count, order, Sb, Yb, rho, syv, yyv, gg, dd, red);
+    if (t < n) d[(size_t)b * n + t] = dd[t];
+}
+
+}  // namespace
+
+// ==========================================================================================
+// host side
+// ==========================================================================================
+struct crb_ctx {
+    int device = 0;
+    std::string err;
+    int64_t launches = 0;
+    // robot
+    bool robot_ok = false;
+    RobotPack rp{};
+    float4 *d_robot = nullptr;
+    std::vector<float> lo, hi;
+    // world
+    bool world_ok = false;
+    float4 *d_boxes = nullptr;
+    int *d_box_count = nullptr;
+    int n_env = 0, kmax = 0, kmax_enabled = 0;
+    // params
+    bool params_ok = false;
+    crb_cost_params cp{};
+    // workspaces (grow on demand)
+    float *ws_cost = nullptr, *ws_traj = nullptr;
+    size_t cap_cost = 0, cap_traj = 0;
+    // host-API buffers
+    float *h_seeds = nullptr, *h_start = nullptr, *h_goal = nullptr, *h_best = nullptr, *h_bcost = nullptr;
+    int *h_env = nullptr;
+    int64_t *h_key = nullptr;
+    size_t cap_h_seeds = 0, cap_h_start = 0, cap_h_goal = 0, cap_h_best = 0, cap_h_bcost = 0, cap_h_env = 0,
+           cap_h_key = 0;
+};
+
+namespace {
+
+crb_status fail(crb_ctx *ctx, crb_status st, const std::string &msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+
+crb_status cuda_check(crb_ctx *ctx, cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return CRB_OK;
+    return fail(ctx, e == cudaErrorMemoryAllocation ? CRB_E_OOM : CRB_E_CUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+crb_status enter(crb_ctx *ctx) {
+    if (!ctx) return CRB_E_ARG;
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaSetDevice");
+    e = cudaGetLastError();   // surfaces an asynchronous fault of an earlier launch
+    if (e != cudaSuccess) return cuda_check(ctx, e, "earlier asynchronous error");
+    return CRB_OK;
+}
+
+template <typename T>
+crb_status grow(crb_ctx *ctx, T **p, size_t *cap, size_t n) {
+    if (n <= *cap) return CRB_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(p, std::max<size_t>(n, 1) * sizeof(T));
+    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaMalloc workspace");
+    *cap = n;
+    return CRB_OK;
+}
+
+int r4(int w) { return (w + 3) & ~3; }
+
+// Shared-memory layout for one kernel configuration; returns total bytes.
+size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A, bool solver, Layout &L) {
+    const int D = rp.D;
+    int w = 0;
+    auto take = [&](int words) { int o = w; w += r4(words); return o; };
+    L.robot = take(rp.words);
+    L.boxes = take(kmax * 16);
+    L.mbar = take(4);
+    L.XS = mode == MODE_TO ? H + 5 : 0;
+    L.q_cfg = take(D * NC);
+    L.xs = take(D * L.XS);
+    L.lt = take(rp.L * 12 * NC);
+    L.sw = take(rp.M * 3 * NC);
+    L.sg = take(rp.M * 3 * NC);
+    L.ls = take(rp.L * 6 * NC);
+    L.sbest = take(NW * NC);
+    L.sidx = take(NW * NC);
+    L.wpart = take(NW * NC);
+    L.cbb = take(D * NC);
+    L.csm = take(D * NC);
+    L.gxd = take(D * NC);
+    L.gva = take(mode == MODE_TO ? 3 * D * NC : 4);
+    L.pose_ft = take(6 * NC);
+    L.pose_c = take(NC);
+    L.goal = take(7 * NC);
+    L.cfg_cost = take(NC);
+    L.cfg_terms = take(5 * NC);
+    L.gV = take(std::max(H * D, D * NC));
+    L.red = take(NW * 2);
+    L.st = take(16);
+    L.solver = w;
+    const int N = H * D, Np = r4(N), DC = D * NC;
+    if (mode == MODE_TO) {
+        if (solver) w += 7 * Np + A * Np + 2 * (m + 1) * Np + 128;   // + rho/syv/yyv/order/scal/ring tail
+        else w += Np + 8;
+    } else if (solver) {
+        w += 6 * DC + 2 * (m + 1) * DC + 3 * (m + 1) * NC + A * DC + 2 * A * NC + (m + 1) * NC;
+    }
+    L.total = r4(w);
+    return (size_t)L.total * 4;
+}
+
+KParams base_params(const crb_ctx *ctx) {
+    KParams kp;
+    memset(&kp, 0, sizeof(kp));
+    kp.rp = ctx->rp;
+    kp.robot = ctx->d_robot;
+    kp.boxes = ctx->d_boxes;
+    kp.box_count = ctx->d_box_count;
+    kp.kmax = ctx->kmax;
+    kp.n_env = ctx->n_env;
+    const crb_cost_params &c = ctx->cp;
+    kp.a0 = c.a0; kp.a1 = c.a1; kp.a2 = c.a2; kp.a3 = c.a3; kp.a8 = c.a8; kp.a9 = c.a9;
+    for (int i = 0; i < 4; ++i) kp.wb[i] = c.w_bound[i];
+    kp.beta_self = c.beta_self; kp.beta_world = c.beta_world; kp.eta = c.eta; kp.eta_bound = c.eta_bound;
+    kp.dt = c.dt; kp.sweep_steps = c.sweep_steps; kp.flags = c.flags;
+    return kp;
+}
+
+crb_status ready(crb_ctx *ctx, bool need_world) {
+    if (!ctx->robot_ok) return fail(ctx, CRB_E_NOT_READY, "robot not set (crb_set_robot)");
+    if (need_world && !ctx->world_ok) return fail(ctx, CRB_E_NOT_READY, "world not set (crb_set_world)");
+    if (need_world && !ctx->params_ok) return fail(ctx, CRB_E_NOT_READY, "cost params not set");
+    return CRB_OK;
+}
+
+template <typename Kern>
+crb_status launch(crb_ctx *ctx, Kern k, int grid, size_t smem, cudaStream_t st, const KParams &kp, const char *nm) {
+    if (grid <= 0) return CRB_OK;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_check(ctx, e, nm);
+    k<<<grid, NT, smem, st>>>(kp);
+    ctx->launches++;
+    return cuda_check(ctx, cudaGetLastError(), nm);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *crb_version(void) { return "curobo_b200 0.1 (sm_100a)"; }
+
+crb_status crb_create(int cuda_device, crb_ctx **out) {
+    if (!out) return CRB_E_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || cuda_device < 0 || cuda_device >= n) return CRB_E_CUDA;
+    crb_ctx *c = new crb_ctx();
+    c->device = cuda_device;
+    if (cudaSetDevice(cuda_device) != cudaSuccess) { delete c; return CRB_E_CUDA; }
+    *out = c;
+    return CRB_OK;
+}
+
+crb_status crb_destroy(crb_ctx *ctx) {
+    if (!ctx) return CRB_E_ARG;
+    cudaSetDevice(ctx->device);
+    cudaFree(ctx->d_robot); cudaFree(ctx->d_boxes); cudaFree(ctx->d_box_count);
+    cudaFree(ctx->ws_cost); cudaFree(ctx->ws_traj);
+    cudaFree(ctx->h_seeds); cudaFree(ctx->h_start); cudaFree(ctx->h_goal); cudaFree(ctx->h_best);
+    cudaFree(ctx->h_bcost); cudaFree(ctx->h_env); cudaFree(ctx->h_key);
+    delete ctx;
+    return CRB_OK;
+}
+
+const char *crb_last_error(const crb_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t crb_launch_count(const crb_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if (!r || !r->links || !r->pos_lo || !r->pos_hi || !r->vel_max || !r->acc_max || !r->jerk_max ||
+        (r->n_spheres > 0 && (!r->spheres || !r->sphere_link)) || (r->n_pairs > 0 && !r->pairs))
+        return fail(ctx, CRB_E_ARG, "null pointer in robot description");
+    const int L = r->n_links, D = r->n_dof, M = r->n_spheres, P = r->n_pairs;
+    if (L < 1 || L > 32 || D < 1 || D > 16 || M < 0 || M > 512 || P < 0 || P > 16384)
+        return fail(ctx, CRB_E_LIMIT, "robot size outside limits (L<=32, D<=16, M<=512, pairs<=16384)");
+    if (r->ee_link < 0 || r->ee_link >= L) return fail(ctx, CRB_E_ROBOT, "ee_link out of range");
+    std::vector<int> doflink(D, -1);
+    for (int l = 0; l < L; ++l) {
+        const crb_link &k = r->links[l];
+        if (k.parent >= l || (l > 0 && k.parent < 0 && false)) return fail(ctx, CRB_E_ROBOT, "parent >= own index (unsorted chain or cycle)");
+        if (k.parent < -1) return fail(ctx, CRB_E_ROBOT, "invalid parent");
+        if (k.type < 0 || k.type > 6) return fail(ctx, CRB_E_ROBOT, "unknown joint type");
+        if (k.type == 0 && k.dof != -1) return fail(ctx, CRB_E_ROBOT, "fixed joint carries a dof");
+        if (k.type != 0) {
+            if (k.dof < 0 || k.dof >= D) return fail(ctx, CRB_E_ROBOT, "actuated joint without a valid dof");
+            if (doflink[k.dof] != -1) return fail(ctx, CRB_E_ROBOT, "duplicate dof");
+            doflink[k.dof] = l;
+        }
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                double dot = 0;
+                for (int q = 0; q < 3; ++q) dot += (double)k.fixed[q * 4 + i] * k.fixed[q * 4 + j];
+                if (std::fabs(dot - (i == j ? 1.0 : 0.0)) > 1e-4)
+                    return fail(ctx, CRB_E_ROBOT, "rotation block of a fixed transform is not orthonormal");
+            }
+    }
+    for (int d = 0; d < D; ++d) {
+        if (doflink[d] < 0) return fail(ctx, CRB_E_ROBOT, "dof without a joint");
+        if (!(r->pos_lo[d] < r->pos_hi[d])) return fail(ctx, CRB_E_ROBOT, "pos_lo >= pos_hi");
+        if (!(r->vel_max[d] > 0) || !(r->acc_max[d] > 0) || !(r->jerk_max[d] > 0))
+            return fail(ctx, CRB_E_ROBOT, "non-positive vel/acc/jerk limit");
+    }
+    for (int m = 0; m < M; ++m)
+        if (r->sphere_link[m] < 0 || r->sphere_link[m] >= L) return fail(ctx, CRB_E_ROBOT, "sphere on an unknown link");
+    for (int p = 0; p < P; ++p) {
+        const int i = r->pairs[2 * p], j = r->pairs[2 * p + 1];
+        if (i < 0 || j >= M || i >= j) return fail(ctx, CRB_E_ROBOT, "self-collision pair with i >= j or out of range");
+    }
+    // ---- pack: spheres grouped by link (stable), pairs remapped, disabled pairs dropped
+    std::vector<int> ord(M);
+    for (int m = 0; m < M; ++m) ord[m] = m;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return r->sphere_link[a] < r->sphere_link[b]; });
+    std::vector<int> inv(M);
+    for (int k = 0; k < M; ++k) inv[ord[k]] = k;
+    RobotPack rp{};
+    rp.L = L; rp.D = D; rp.M = M; rp.ee = r->ee_link;
+    int w = 0;
+    rp.o_links = w; w += 16 * L;
+    rp.o_sph = w; w += 4 * M;
+    rp.o_sphlink = w; w += r4(M);
+    rp.o_sbeg = w; w += r4(L + 1);
+    std::vector<uint32_t> pk;
+    for (int p = 0; p < P; ++p) {
+        const int i = r->pairs[2 * p], j = r->pairs[2 * p + 1];
+        const double ri = (double)r->spheres[4 * i + 3] + (r->self_offset ? r->self_offset[i] : 0.0);
+        const double rj = (double)r->spheres[4 * j + 3] + (r->self_offset ? r->self_offset[j] : 0.0);
+        if (ri <= 0.0 || rj <= 0.0) continue;   // Alg. 9 "continue": exact to drop
+        const float R = (float)(ri + rj);
+        uint32_t rb;
+        memcpy(&rb, &R, 4);
+        pk.push_back((uint32_t)inv[i] | ((uint32_t)inv[j] << 16));
+        pk.push_back(rb);
+    }
+    rp.P = (int)pk.size() / 2;
+    rp.o_pairs = w; w += r4(2 * rp.P);
+    rp.o_lim = w; w += r4(5 * D);
+    rp.o_doflink = w; w += r4(D);
+    rp.o_perm = w; w += r4(M);
+    rp.words = r4(w);
+    std::vector<uint32_t> blob(rp.words, 0);
+    auto fput = [&](int o, float v) { memcpy(&blob[o], &v, 4); };
+    for (int l = 0; l < L; ++l) {
+        for (int i = 0; i < 12; ++i) fput(rp.o_links + 16 * l + i, r->links[l].fixed[i]);
+        blob[rp.o_links + 16 * l + 12] = (uint32_t)r->links[l].parent;
+        blob[rp.o_links + 16 * l + 13] = (uint32_t)r->links[l].type;
+        blob[rp.o_links + 16 * l + 14] = (uint32_t)r->links[l].dof;
+    }
+    for (int k = 0; k < M; ++k) {
+        const int m = ord[k];
+        for (int i = 0; i < 4; ++i) fput(rp.o_sph + 4 * k + i, r->spheres[4 * m + i]);
+        blob[rp.o_sphlink + k] = (uint32_t)r->sphere_link[m];
+        blob[rp.o_perm + k] = (uint32_t)m;
+    }
+    for (int l = 0, k = 0; l <= L; ++l) {
+        while (k < M && r->sphere_link[ord[k]] < l) ++k;
+        blob[rp.o_sbeg + l] = (uint32_t)k;
+    }
+    for (size_t i = 0; i < pk.size(); ++i) blob[rp.o_pairs + i] = pk[i];
+    for (int d = 0; d < D; ++d) {
+        fput(rp.o_lim + d, r->pos_lo[d]); fput(rp.o_lim + D + d, r->pos_hi[d]);
+        fput(rp.o_lim + 2 * D + d, r->vel_max[d]); fput(rp.o_lim + 3 * D + d, r->acc_max[d]);
+        fput(rp.o_lim + 4 * D + d, r->jerk_max[d]);
+        blob[rp.o_doflink + d] = (uint32_t)doflink[d];
+    }
+    cudaFree(ctx->d_robot);
+    ctx->d_robot = nullptr;
+    st = cuda_check(ctx, cudaMalloc(&ctx->d_robot, blob.size() * 4), "cudaMalloc robot");
+    if (st != CRB_OK) return st;
+    st = cuda_check(ctx, cudaMemcpy(ctx->d_robot, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice), "upload robot");
+    if (st != CRB_OK) return st;
+    ctx->rp = rp;
+    ctx->lo.assign(r->pos_lo, r->pos_lo + D);
+    ctx->hi.assign(r->pos_hi, r->pos_hi + D);
+    ctx->robot_ok = true;
+    return CRB_OK;
+}
+
+crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_per_env, const crb_cuboid *boxes) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if (n_env < 1 || k_max < 0 || !boxes_per_env || (k_max > 0 && !boxes)) return fail(ctx, CRB_E_ARG, "bad world arguments");
+    std::vector<float> packed((size_t)n_env * std::max(k_max, 1) * 16, 0.f);
+    std::vector<int> count(n_env, 0);
+    int kmax_en = 0;
+    for (int e = 0; e < n_env; ++e) {
+        if (boxes_per_env[e] < 0 || boxes_per_env[e] > k_max) return fail(ctx, CRB_E_SHAPE, "boxes_per_env > k_max");
+        int k = 0;
+        for (int i = 0; i < boxes_per_env[e]; ++i) {
+            const crb_cuboid &b = boxes[(size_t)e * k_max + i];
+            for (int j = 0; j < 3; ++j)
+                if (!(b.dims[j] > 0.f) || !std::isfinite(b.dims[j]) || !std::isfinite(b.pos[j]))
+                    return fail(ctx, CRB_E_WORLD, "cuboid with non-positive or non-finite extent/position");
+            const double qn = std::sqrt((double)b.quat[0] * b.quat[0] + (double)b.quat[1] * b.quat[1] +
+                                        (double)b.quat[2] * b.quat[2] + (double)b.quat[3] * b.quat[3]);
+            if (!(qn > 1e-6)) return fail(ctx, CRB_E_WORLD, "cuboid quaternion of zero norm");
+            if (!b.enabled) continue;   // Alg. 10 skips disabled boxes
+            const double w = b.quat[0] / qn, x = b.quat[1] / qn, y = b.quat[2] / qn, z = b.quat[3] / qn;
+            const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                                    {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                                    {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+            float *o = &packed[((size_t)e * k_max + k) * 16];
+            for (int i2 = 0; i2 < 3; ++i2) {   // row i2 of R^T = column i2 of R, with -col . t
+                o[4 * i2 + 0] = (float)R[0][i2];
+                o[4 * i2 + 1] = (float)R[1][i2];
+                o[4 * i2 + 2] = (float)R[2][i2];
+                o[4 * i2 + 3] = (float)(-(R[0][i2] * b.pos[0] + R[1][i2] * b.pos[1] + R[2][i2] * b.pos[2]));
+            }
+            o[12] = 0.5f * b.dims[0]; o[13] = 0.5f * b.dims[1]; o[14] = 0.5f * b.dims[2]; o[15] = 0.f;
+            ++k;
+        }
+        count[e] = k;
+        kmax_en = std::max(kmax_en, k);
+    }
+    cudaFree(ctx->d_boxes); cudaFree(ctx->d_box_count);
+    ctx->d_boxes = nullptr; ctx->d_box_count = nullptr;
+    ctx->world_ok = false;
+    st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes, packed.size() * 4), "cudaMalloc boxes");
+    if (st != CRB_OK) return st;
+    st = cuda_check(ctx, cudaMalloc(&ctx->d_box_count, n_env * sizeof(int)), "cudaMalloc box count");
+    if (st != CRB_OK) return st;
+    st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "upload boxes");
+    if (st != CRB_OK) return st;
+    st = cuda_check(ctx, cudaMemcpy(ctx->d_box_count, count.data(), n_env * sizeof(int), cudaMemcpyHostToDevice), "upload counts");
+    if (st != CRB_OK) return st;
+    ctx->n_env = n_env;
+    ctx->kmax = std::max(k_max, 1);
+    ctx->kmax_enabled = kmax_en;
+    ctx->world_ok = true;
+    return CRB_OK;
+}
+
+crb_status crb_set_cost_params(crb_ctx *ctx, const crb_cost_params *p) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if (!p) return fail(ctx, CRB_E_ARG, "null params");
+    if (!(p->eta > 0) || !(p->eta_bound > 0) || !(p->dt > 0) || p->sweep_steps < 0 || p->sweep_steps > 64)
+        return fail(ctx, CRB_E_ARG, "eta, eta_bound, dt must be > 0 and 0 <= sweep_steps <= 64");
+    ctx->cp = *p;
+    ctx->params_ok = true;
+    return CRB_OK;
+}
+
+crb_status crb_fk(crb_ctx *ctx, const float *q, int B, float *spheres_out, float *ee_out, void *stream) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if ((st = ready(ctx, false)) != CRB_OK) return st;
+    if (!q || B < 0) return fail(ctx, CRB_E_ARG, "bad fk arguments");
+    KParams kp = base_params(ctx);
+    kp.kmax = 0;
+    kp.B = B; kp.H = 1; kp.mode = MODE_IK; kp.q_in = q; kp.spheres_out = spheres_out; kp.ee_out = ee_out;
+    const size_t bytes = make_layout(ctx->rp, 0, MODE_IK, 1, 1, 1, false, kp.lay);
+    if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large");
+    return launch(ctx, fk_kernel, (B + NC - 1) / NC, bytes, (cudaStream_t)stream, kp, "fk_kernel");
+}
+
+crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, const int *env, const float *start,
+                                  const float *goal, float *cost, float *grad, float *term_costs, void *stream) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if ((st = ready(ctx, true)) != CRB_OK) return st;
+    if (!q || !goal || !cost || B < 0) return fail(ctx, CRB_E_ARG, "bad evaluate arguments");
+    const int mode = H == 1 ? MODE_IK : MODE_TO;
+    if (mode == MODE_TO && (H < 8 || H > 32 || H * ctx->rp.D > 512 || !start))
+        return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 32, H*D <= 512 and start");
+    KParams kp = base_params(ctx);
+    kp.B = B; kp.H = H; kp.mode = mode; kp.q_in = q; kp.env = env; kp.start = start; kp.goal = goal;
+    kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs;
+    const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
+    if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
+    if (mode == MODE_TO) return launch(ctx, eval_to_kernel, B, bytes, (cudaStream_t)stream, kp, "eval_to_kernel");
+    return launch(ctx, eval_ik_kernel, (B + NC - 1) / NC, bytes, (cudaStream_t)stream, kp, "eval_ik_kernel");
+}
+
+crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H, const float *seeds,
+                           const int *env, const float *start, const float *goal, float *best_traj, float *best_cost,
+                           int64_t *best_key, float *seed_best_cost, float *seed_best_traj, void *stream) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if ((st = ready(ctx, true)) != CRB_OK) return st;
+    if (!sp || !seeds || !goal || P < 0 || S < 1) return fail(ctx, CRB_E_ARG, "bad solve arguments");
+    if (sp->history < 1 || sp->history > 16 || sp->n_alpha < 1 || sp->n_alpha > 8 || sp->iters < 0)
+        return fail(ctx, CRB_E_LIMIT, "history must be in [1,16], n_alpha in [1,8], iters >= 0");
+    const int mode = H == 1 ? MODE_IK : MODE_TO;
+    const int D = ctx->rp.D;
+    if (mode == MODE_TO && (H < 8 || H > 32 || H * D > 512 || !start))
+        return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 32, H*D <= 512 and start");
+    const int N = H * D;
+    cudaStream_t stream_ = (cudaStream_t)stream;
+    float *sbc = seed_best_cost, *sbt = seed_best_traj;
+    if (!sbc) { if ((st = grow(ctx, &ctx->ws_cost, &ctx->cap_cost, (size_t)P * S)) != CRB_OK) return st; sbc = ctx->ws_cost; }
+    if (!sbt) { if ((st = grow(ctx, &ctx->ws_traj, &ctx->cap_traj, (size_t)P * S * N)) != CRB_OK) return st; sbt = ctx->ws_traj; }
+    KParams kp = base_params(ctx);
+    kp.P = P; kp.S = S; kp.H = H; kp.mode = mode; kp.q_in = seeds; kp.env = env; kp.start = start; kp.goal = goal;
+    kp.iters = sp->iters; kp.m = sp->history; kp.A = sp->n_alpha; kp.ls_mode = sp->ls_mode;
+    for (int i = 0; i < 8; ++i) kp.alpha[i] = sp->alpha[i];
+    kp.c1 = sp->c1; kp.c2 = sp->c2; kp.seed_base = sp->global_seed_base;
+    kp.seed_best_cost = sbc; kp.seed_best_traj = sbt;
+    const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
+    if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids + solver)");
+    if (mode == MODE_TO) st = launch(ctx, solve_to_kernel, P * S, bytes, stream_, kp, "solve_to_kernel");
+    else st = launch(ctx, solve_ik_kernel, P * ((S + NC - 1) / NC), bytes, stream_, kp, "solve_ik_kernel");
+    if (st != CRB_OK) return st;
+    if (P > 0 && (best_traj || best_cost || best_key)) {
+        select_kernel<<<P, 128, 0, stream_>>>(P, S, N, sbc, sbt, (long long)sp->global_seed_base, best_traj,
+                                              best_cost, (long long *)best_key);
+        ctx->launches++;
+        st = cuda_check(ctx, cudaGetLastError(), "select_kernel");
+    }
+    return st;
+}
+
+crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H, const float *seeds,
+                                const int *env, const float *start, const float *goal, float *best_traj,
+                                float *best_cost, int64_t *best_key, void *stream) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if ((st = ready(ctx, true)) != CRB_OK) return st;
+    if (!seeds || !goal || P < 0 || S < 1 || H < 1) return fail(ctx, CRB_E_ARG, "bad solve arguments");
+    const int D = ctx->rp.D, N = H * D;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = grow(ctx, &ctx->h_seeds, &ctx->cap_h_seeds, (size_t)P * S * N)) != CRB_OK) return st;
+    if ((st = grow(ctx, &ctx->h_goal, &ctx->cap_h_goal, (size_t)P * 7)) != CRB_OK) return st;
+    if ((st = grow(ctx, &ctx->h_best, &ctx->cap_h_best, (size_t)P * N)) != CRB_OK) return st;
+    if ((st = grow(ctx, &ctx->h_bcost, &ctx->cap_h_bcost, (size_t)P)) != CRB_OK) return st;
+    if ((st = grow(ctx, &ctx->h_key, &ctx->cap_h_key, (size_t)P)) != CRB_OK) return st;
+    if (start && (st = grow(ctx, &ctx->h_start, &ctx->cap_h_start, (size_t)P * D)) != CRB_OK) return st;
+    if (env && (st = grow(ctx, &ctx->h_env, &ctx->cap_h_env, (size_t)P)) != CRB_OK) return st;
+    st = cuda_check(ctx, cudaMemcpyAsync(ctx->h_seeds, seeds, (size_t)P * S * N * 4, cudaMemcpyHostToDevice, s), "H2D seeds");
+    if (st == CRB_OK) st = cuda_check(ctx, cudaMemcpyAsync(ctx->h_goal, goal, (size_t)P * 7 * 4, cudaMemcpyHostToDevice, s), "H2D goal");
+    if (st == CRB_OK && start) st = cuda_check(ctx, cudaMemcpyAsync(ctx->h_start, start, (size_t)P * D * 4, cudaMemcpyHostToDevice, s), "H2D start");
+    if (st == CRB_OK && env) st = cuda_check(ctx, cudaMemcpyAsync(ctx->h_env, env, (size_t)P * 4, cudaMemcpyHostToDevice, s), "H2D env");
+    if (st != CRB_OK) return st;
+    st = crb_lbfgs_solve(ctx, sp, P, S, H, ctx->h_seeds, env ? ctx->h_env : nullptr, start ? ctx->h_start : nullptr,
+                         ctx->h_goal, ctx->h_best, ctx->h_bcost, (int64_t *)ctx->h_key, nullptr, nullptr, stream);
+    if (st != CRB_OK) return st;
+    if (best_traj) st = cuda_check(ctx, cudaMemcpyAsync(best_traj, ctx->h_best, (size_t)P * N * 4, cudaMemcpyDeviceToHost, s), "D2H best");
+    if (st == CRB_OK && best_cost) st = cuda_check(ctx, cudaMemcpyAsync(best_cost, ctx->h_bcost, (size_t)P * 4, cudaMemcpyDeviceToHost, s), "D2H cost");
+    if (st == CRB_OK && best_key) st = cuda_check(ctx, cudaMemcpyAsync(best_key, ctx->h_key, (size_t)P * 8, cudaMemcpyDeviceToHost, s), "D2H key");
+    if (st != CRB_OK) return st;
+    return cuda_check(ctx, cudaStreamSynchronize(s), "solve_host synchronize");
+}
+
+crb_status crb_ls_select(int n, int A, const float *alpha_host, const float *c0, const float *g0d, const float *ca,
+                         const float *gda, float c1, float c2, int mode, int *out_idx, void *stream) {
+    if (n < 0 || A < 1 || A > 8 || !alpha_host || !c0 || !g0d || !ca || !gda || !out_idx) return CRB_E_ARG;
+    LsParams ap{};
+    for (int a = 0; a < A; ++a) ap.alpha[a] = alpha_host[a];
+    if (n == 0) return CRB_OK;
+    ls_select_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(n, A, ap, c0, g0d, ca, gda, c1, c2, mode, out_idx);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_argmin_keys(int P, int S, const float *cost, int64_t seed_base, int64_t *out_key, int *out_idx,
+                           void *stream) {
+    if (P < 0 || S < 1 || !cost) return CRB_E_ARG;
+    if (P == 0) return CRB_OK;
+    argmin_keys_kernel<<<(P + 127) / 128, 128, 0, (cudaStream_t)stream>>>(P, S, cost, (long long)seed_base,
+                                                                        (long long *)out_key, out_idx);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const float *Y, const float *g, float *d,
+                               void *stream) {
+    if (B < 0 || n < 1 || n > NT || count < 0 || count > 16 || !g || !d || (count > 0 && (!S || !Y))) return CRB_E_ARG;
+    if (B == 0) return CRB_OK;
+    const int Np = (n + 3) & ~3;
+    const size_t bytes = (size_t)(2 * count * Np + 2 * Np + 48 + 32 + 16) * 4;
+    if (cudaFuncSetAttribute(lbfgs_direction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+        return CRB_E_CUDA;
+    lbfgs_direction_kernel<<<B, NT, bytes, (cudaStream_t)stream>>>(n, count, S, Y, g, d);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,281 @@
+"""Thin ctypes binding of libcurobo_b200.so (include/curobo_b200.h): argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; torch is used for device memory
+and streams.  There is no CPU fallback: importing this module on a machine where the library is
+missing raises immediately, and every call that returns a non-zero status raises CrbError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import inputs
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcurobo_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(nvcc, sm_100a).  There is no CPU fallback.")
+
+_lib = C.CDLL(LIB_PATH)
+
+STATUS = {0: "CRB_OK", -1: "CRB_E_ARG", -2: "CRB_E_SHAPE", -3: "CRB_E_ROBOT", -4: "CRB_E_WORLD",
+          -5: "CRB_E_NOT_READY", -6: "CRB_E_LIMIT", -7: "CRB_E_CUDA", -8: "CRB_E_OOM"}
+
+
+class CrbError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class crb_link(C.Structure):
+    _fields_ = [("parent", C.c_int), ("type", C.c_int), ("dof", C.c_int), ("fixed", C.c_float * 12)]
+
+
+F_P = C.POINTER(C.c_float)
+I_P = C.POINTER(C.c_int)
+
+
+class crb_robot_desc(C.Structure):
+    _fields_ = [("n_links", C.c_int), ("n_dof", C.c_int), ("n_spheres", C.c_int), ("n_pairs", C.c_int),
+                ("ee_link", C.c_int), ("links", C.POINTER(crb_link)),
+                ("pos_lo", F_P), ("pos_hi", F_P), ("vel_max", F_P), ("acc_max", F_P), ("jerk_max", F_P),
+                ("spheres", F_P), ("sphere_link", I_P), ("self_offset", F_P), ("pairs", I_P)]
+
+
+class crb_cuboid(C.Structure):
+    _fields_ = [("pos", C.c_float * 3), ("quat", C.c_float * 4), ("dims", C.c_float * 3), ("enabled", C.c_int)]
+
+
+class crb_cost_params(C.Structure):
+    _fields_ = [("a0", C.c_float), ("a1", C.c_float), ("a2", C.c_float), ("a3", C.c_float),
+                ("a8", C.c_float), ("a9", C.c_float), ("w_bound", C.c_float * 4),
+                ("beta_self", C.c_float), ("beta_world", C.c_float), ("eta", C.c_float),
+                ("eta_bound", C.c_float), ("dt", C.c_float), ("sweep_steps", C.c_int), ("flags", C.c_uint)]
+
+
+class crb_solver_params(C.Structure):
+    _fields_ = [("iters", C.c_int), ("history", C.c_int), ("n_alpha", C.c_int), ("alpha", C.c_float * 8),
+                ("c1", C.c_float), ("c2", C.c_float), ("ls_mode", C.c_int), ("global_seed_base", C.c_int64)]
+
+
+_V = C.c_void_p
+_lib.crb_create.argtypes = [C.c_int, C.POINTER(_V)]
+_lib.crb_destroy.argtypes = [_V]
+_lib.crb_last_error.argtypes = [_V]
+_lib.crb_last_error.restype = C.c_char_p
+_lib.crb_version.restype = C.c_char_p
+_lib.crb_set_robot.argtypes = [_V, C.POINTER(crb_robot_desc)]
+_lib.crb_set_world.argtypes = [_V, C.c_int, C.c_int, I_P, C.POINTER(crb_cuboid)]
+_lib.crb_set_cost_params.argtypes = [_V, C.POINTER(crb_cost_params)]
+_lib.crb_fk.argtypes = [_V, _V, C.c_int, _V, _V, _V]
+_lib.crb_evaluate_cost_grad.argtypes = [_V, _V, C.c_int, C.c_int, _V, _V, _V, _V, _V, _V, _V]
+_lib.crb_lbfgs_solve.argtypes = [_V, C.POINTER(crb_solver_params), C.c_int, C.c_int, C.c_int, _V, _V, _V, _V,
+                                 _V, _V, _V, _V, _V, _V]
+_lib.crb_lbfgs_solve_host.argtypes = [_V, C.POINTER(crb_solver_params), C.c_int, C.c_int, C.c_int, _V, _V, _V,
+                                      _V, _V, _V, _V, _V]
+_lib.crb_ls_select.argtypes = [C.c_int, C.c_int, F_P, _V, _V, _V, _V, C.c_float, C.c_float, C.c_int, _V, _V]
+_lib.crb_argmin_keys.argtypes = [C.c_int, C.c_int, _V, C.c_int64, _V, _V, _V]
+_lib.crb_lbfgs_direction.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, _V, _V, _V]
+_lib.crb_launch_count.argtypes = [_V]
+_lib.crb_launch_count.restype = C.c_int64
+
+SYMBOLS = ["crb_create", "crb_destroy", "crb_last_error", "crb_version", "crb_set_robot", "crb_set_world",
+           "crb_set_cost_params", "crb_fk", "crb_evaluate_cost_grad", "crb_lbfgs_solve", "crb_lbfgs_solve_host",
+           "crb_ls_select", "crb_argmin_keys", "crb_lbfgs_direction", "crb_launch_count"]
+
+
+def _ptr(t):
+    """Device pointer of a torch tensor (or None)."""
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "expected a contiguous CUDA tensor"
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _check_free(code):
+    if code != 0:
+        raise CrbError(code, "(no context)")
+
+
+def cost_params_struct(cp: inputs.CostParams) -> crb_cost_params:
+    return crb_cost_params(cp.a0, cp.a1, cp.a2, cp.a3, cp.a8, cp.a9, (C.c_float * 4)(*cp.w_bound),
+                           cp.beta_self, cp.beta_world, cp.eta, cp.eta_bound, cp.dt, int(cp.sweep_steps),
+                           int(cp.flags))
+
+
+def solver_params_struct(sp: inputs.SolverParams, seed_base: int = 0) -> crb_solver_params:
+    al = list(sp.alpha) + [0.0] * (8 - len(sp.alpha))
+    return crb_solver_params(int(sp.iters), int(sp.history), len(sp.alpha), (C.c_float * 8)(*al), float(sp.c1),
+                             float(sp.c2), int(sp.ls_mode), int(seed_base))
+
+
+class Context:
+    """One crb_ctx on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        code = _lib.crb_create(int(device), C.byref(h))
+        if code != 0:
+            raise CrbError(code, f"crb_create({device}) failed")
+        self.h = h
+        self.device = device
+        self._keep = []
+
+    def close(self):
+        if self.h:
+            _lib.crb_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, code):
+        if code != 0:
+            raise CrbError(code, _lib.crb_last_error(self.h).decode())
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.crb_launch_count(self.h))
+
+    # ---- setup (host arrays) -------------------------------------------------------------
+    def set_robot(self, rb: inputs.Robot):
+        L = rb.n_links
+        links = (crb_link * L)()
+        for l in range(L):
+            links[l].parent = int(rb.parent[l]); links[l].type = int(rb.jtype[l]); links[l].dof = int(rb.dof[l])
+            for i in range(12):
+                links[l].fixed[i] = float(rb.fixed[l][i])
+        f32 = lambda a: np.ascontiguousarray(a, np.float32)
+        i32 = lambda a: np.ascontiguousarray(a, np.int32)
+        arrs = dict(lo=f32(rb.lo), hi=f32(rb.hi), vmax=f32(rb.vmax), amax=f32(rb.amax), jmax=f32(rb.jmax),
+                    sph=f32(rb.spheres), slink=i32(rb.sphere_link), off=f32(rb.sphere_offset),
+                    pairs=i32(rb.pairs.reshape(-1, 2)))
+        fp = lambda a: a.ctypes.data_as(F_P)
+        ip = lambda a: a.ctypes.data_as(I_P)
+        desc = crb_robot_desc(L, rb.n_dof, rb.n_spheres, int(arrs["pairs"].shape[0]), int(rb.ee_link), links,
+                              fp(arrs["lo"]), fp(arrs["hi"]), fp(arrs["vmax"]), fp(arrs["amax"]), fp(arrs["jmax"]),
+                              fp(arrs["sph"]), ip(arrs["slink"]), fp(arrs["off"]), ip(arrs["pairs"]))
+        self._chk(_lib.crb_set_robot(self.h, C.byref(desc)))
+        self.robot = rb
+
+    def set_world(self, worlds: Sequence[inputs.World]):
+        n = len(worlds)
+        kmax = max(1, max(w.n_boxes for w in worlds))
+        arr = (crb_cuboid * (n * kmax))()
+        counts = np.zeros(n, np.int32)
+        for e, w in enumerate(worlds):
+            counts[e] = w.n_boxes
+            for k in range(w.n_boxes):
+                b = arr[e * kmax + k]
+                b.pos[:] = [float(x) for x in w.pos[k]]
+                b.quat[:] = [float(x) for x in w.quat[k]]
+                b.dims[:] = [float(x) for x in w.dims[k]]
+                b.enabled = int(w.enabled[k])
+        self._chk(_lib.crb_set_world(self.h, n, kmax, counts.ctypes.data_as(I_P), arr))
+
+    def set_cost_params(self, cp: inputs.CostParams):
+        s = cost_params_struct(cp)
+        self._chk(_lib.crb_set_cost_params(self.h, C.byref(s)))
+        self.cp = cp
+
+    # ---- hot path (device tensors) --------------------------------------------------------
+    def fk(self, q, spheres_out=None, ee_out=None):
+        import torch
+        B = q.shape[0]
+        if spheres_out is None:
+            spheres_out = torch.empty(B, self.robot.n_spheres, 4, device=q.device, dtype=torch.float32)
+        if ee_out is None:
+            ee_out = torch.empty(B, 7, device=q.device, dtype=torch.float32)
+        self._chk(_lib.crb_fk(self.h, _ptr(q), B, _ptr(spheres_out), _ptr(ee_out), _stream()))
+        return spheres_out, ee_out
+
+    def evaluate(self, q, goal, start=None, env=None, grad=True, terms=True):
+        """q [B,H,D] (TO) or [B,D] (IK); returns (cost [B], grad, terms [B,5])."""
+        import torch
+        B = q.shape[0]
+        H = 1 if q.dim() == 2 else q.shape[1]
+        cost = torch.empty(B, device=q.device, dtype=torch.float32)
+        g = torch.empty_like(q) if grad else None
+        tc = torch.empty(B, 5, device=q.device, dtype=torch.float32) if terms else None
+        self._chk(_lib.crb_evaluate_cost_grad(self.h, _ptr(q), B, H, _ptr(env), _ptr(start), _ptr(goal), _ptr(cost),
+                                              _ptr(g), _ptr(tc), _stream()))
+        return cost, g, tc
+
+    def solve(self, sp: inputs.SolverParams, seeds, goal, start=None, env=None, seed_base: int = 0,
+              seed_outputs: bool = False):
+        """seeds [P,S,H,D] (TO) or [P,S,D] (IK).  Returns dict of device tensors."""
+        import torch
+        P, S = seeds.shape[0], seeds.shape[1]
+        H = 1 if seeds.dim() == 3 else seeds.shape[2]
+        D = seeds.shape[-1]
+        dev = seeds.device
+        out = dict(best_traj=torch.empty((P, H, D) if H > 1 else (P, D), device=dev, dtype=torch.float32),
+                   best_cost=torch.empty(P, device=dev, dtype=torch.float32),
+                   best_key=torch.empty(P, device=dev, dtype=torch.int64))
+        if seed_outputs:
+            out["seed_best_cost"] = torch.empty(P, S, device=dev, dtype=torch.float32)
+            out["seed_best_traj"] = torch.empty_like(seeds)
+        s = solver_params_struct(sp, seed_base)
+        self._chk(_lib.crb_lbfgs_solve(self.h, C.byref(s), P, S, H, _ptr(seeds), _ptr(env), _ptr(start), _ptr(goal),
+                                       _ptr(out["best_traj"]), _ptr(out["best_cost"]), _ptr(out["best_key"]),
+                                       _ptr(out.get("seed_best_cost")), _ptr(out.get("seed_best_traj")), _stream()))
+        return out
+
+    def solve_host(self, sp: inputs.SolverParams, seeds, goal, start=None, env=None, seed_base: int = 0,
+                   best_traj=None, best_cost=None, best_key=None):
+        """Host (ideally pinned) torch CPU tensors in and out; H2D + solve + D2H + sync in the library."""
+        P, S = seeds.shape[0], seeds.shape[1]
+        H = 1 if seeds.dim() == 3 else seeds.shape[2]
+        hp = lambda t: None if t is None else C.c_void_p(t.data_ptr())
+        s = solver_params_struct(sp, seed_base)
+        self._chk(_lib.crb_lbfgs_solve_host(self.h, C.byref(s), P, S, H, hp(seeds), hp(env), hp(start), hp(goal),
+                                            hp(best_traj), hp(best_cost), hp(best_key), _stream()))
+
+
+# ---- test hooks -----------------------------------------------------------------------------
+
+def ls_select(alpha, c0, g0d, ca, gda, c1=1e-4, c2=0.9, mode=2):
+    import torch
+    n, A = ca.shape
+    out = torch.empty(n, device=ca.device, dtype=torch.int32)
+    al = np.ascontiguousarray(alpha, np.float32)
+    _check_free(_lib.crb_ls_select(n, A, al.ctypes.data_as(F_P), _ptr(c0), _ptr(g0d), _ptr(ca), _ptr(gda),
+                                   float(c1), float(c2), int(mode), _ptr(out), _stream()))
+    return out
+
+
+def argmin_keys(cost, seed_base=0):
+    import torch
+    P, S = cost.shape
+    key = torch.empty(P, device=cost.device, dtype=torch.int64)
+    idx = torch.empty(P, device=cost.device, dtype=torch.int32)
+    _check_free(_lib.crb_argmin_keys(P, S, _ptr(cost), int(seed_base), _ptr(key), _ptr(idx), _stream()))
+    return key, idx
+
+
+def lbfgs_direction(S, Y, g):
+    """S, Y [B,count,n], g [B,n] device fp32 -> d [B,n] (the solver's two-loop routine)."""
+    import torch
+    B, n = g.shape
+    count = S.shape[1]
+    d = torch.empty_like(g)
+    _check_free(_lib.crb_lbfgs_direction(B, n, count, _ptr(S), _ptr(Y), _ptr(g), _ptr(d), _stream()))
+    return d
+
+
+def version() -> str:
+    return _lib.crb_version().decode()

@@ -1,0 +1,443 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on identical seeded inputs.
+
+Tolerances (north star / SURVEY §8(c).4): per trajectory |dc| <= 1e-4 |c| + 1e-5 and
+||dg|| <= 1e-3 ||g|| + 1e-5 sqrt(N), after excluding evaluations whose oracle branch margin (at a
+branch where the cost or gradient is discontinuous) is below 1e-4; line-search selection and the
+packed-key argmin bit-exact on identical fp32 inputs.
+"""
+import struct
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2310_17274_b200 import inputs, robots
+
+pytestmark = pytest.mark.gpu
+
+COST_RTOL, COST_ATOL, GRAD_RTOL, GRAD_ATOL, MARGIN = 1e-4, 1e-5, 1e-3, 1e-5, 1e-4
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def native():
+    from paper_2310_17274_b200 import native as N
+    return N
+
+
+def f32(x):
+    return np.asarray(x, np.float32).astype(np.float64)
+
+
+def T(x, dtype=torch.float32):
+    return torch.tensor(np.ascontiguousarray(x), dtype=dtype, device=DEV)
+
+
+def make(native, rb, worlds, cp):
+    ctx = native.Context(0)
+    ctx.set_robot(rb)
+    ctx.set_world(worlds)
+    ctx.set_cost_params(cp)
+    return ctx
+
+
+class Stats:
+    def __init__(self):
+        self.n = 0
+        self.excluded = 0
+        self.worst_c = 0.0
+        self.worst_g = 0.0
+
+    def check(self, c_gpu, g_gpu, c_ref, g_ref, margin, label):
+        self.n += 1
+        if margin < MARGIN:
+            self.excluded += 1
+            return
+        ec = abs(c_gpu - c_ref) / (abs(c_ref) * COST_RTOL + COST_ATOL)
+        eg = np.linalg.norm(g_gpu - g_ref) / (np.linalg.norm(g_ref) * GRAD_RTOL + GRAD_ATOL * np.sqrt(g_ref.size))
+        self.worst_c = max(self.worst_c, ec)
+        self.worst_g = max(self.worst_g, eg)
+        assert ec <= 1.0, f"{label}: cost gpu={c_gpu} ref={c_ref}"
+        assert eg <= 1.0, f"{label}: grad err {np.linalg.norm(g_gpu - g_ref)} vs |g|={np.linalg.norm(g_ref)}"
+
+    def done(self, max_excluded=0.2):
+        assert self.n > 0
+        assert self.excluded <= max_excluded * self.n, f"excluded {self.excluded}/{self.n}"
+
+
+# ------------------------------------------------------------------------------------------ FK
+
+def test_fk_parity_franka_and_random_chains(native, O):
+    from test_oracle_kinematics import random_chain
+    cases = [robots.franka64()] + [random_chain(7000 + i, 6 + 2 * i, n_spheres=10) for i in range(4)]
+    for rb in cases:
+        ctx = native.Context(0)
+        ctx.set_robot(rb)
+        g = np.random.default_rng(1)
+        q = f32(g.uniform(rb.lo, rb.hi, (77, rb.n_dof)))
+        sph, ee = ctx.fk(T(q))
+        sph, ee = sph.cpu().numpy(), ee.cpu().numpy()
+        R = O.Robot(rb)
+        for b in range(q.shape[0]):
+            _, s_ref, e_ref = O.fk(R, q[b])
+            np.testing.assert_allclose(sph[b], s_ref, atol=2e-5)
+            np.testing.assert_allclose(ee[b, :3], e_ref[:3], atol=2e-5)
+            if abs(e_ref[3]) > 1e-3:
+                np.testing.assert_allclose(ee[b, 3:], e_ref[3:], atol=2e-5)
+        ctx.close()
+
+
+# ------------------------------------------------------------------------------------------ TO eval
+
+def franka_trajs(seed, B, H, noise=0.25):
+    rb = robots.franka64()
+    g = np.random.default_rng(seed)
+    starts, goals_cfg, trajs = [], [], []
+    for b in range(B):
+        s = np.clip(rb.ready + g.normal(0, 0.4, 7), rb.lo, rb.hi)
+        q = np.clip(s + g.normal(0, 1.0, 7), rb.lo, rb.hi)
+        seeds = inputs.to_seeds(rb, seed, b, s, q, 2, H, noise=noise)
+        starts.append(s); goals_cfg.append(q); trajs.append(seeds[b % 2])
+    return rb, np.array(starts), np.array(goals_cfg), np.array(trajs)
+
+
+@pytest.mark.parametrize("H,flags,scene", [
+    (32, inputs.SWEEP | inputs.SPEED, "tabletop"),
+    (32, inputs.SWEEP | inputs.SPEED | inputs.JERK, "random"),
+    (16, 0, "random"),
+    (13, inputs.SWEEP, "tabletop"),
+    (8, inputs.SPEED | inputs.JERK, "random"),
+])
+def test_eval_to_parity_franka(native, O, H, flags, scene):
+    B = 24
+    rb, starts, goals_cfg, trajs = franka_trajs(10 + H + flags, B, H)
+    if scene == "tabletop":
+        worlds = [inputs.tabletop_scene(1, e, 20) for e in range(3)]
+    else:
+        worlds = [inputs.random_world(2, e, 20, lo=-0.8, hi=0.8) for e in range(3)]
+    cp = inputs.CostParams(flags=flags, dt=0.25 if H >= 16 else 0.1)
+    ctx = make(native, rb, worlds, cp)
+    R = O.Robot(rb)
+    Ws = [O.World(w) for w in worlds]
+    env = np.arange(B, dtype=np.int32) % 3
+    goals = np.array([O.fk(R, q)[2] for q in goals_cfg])
+    goals[::3, :3] += 0.05
+    V, st, gl = f32(trajs), f32(starts), f32(goals)
+    cost, grad, terms = ctx.evaluate(T(V), T(gl), start=T(st), env=T(env, torch.int32))
+    cost, grad, terms = cost.cpu().numpy(), grad.cpu().numpy(), terms.cpu().numpy()
+    stats = Stats()
+    world_active = 0
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"traj {b}")
+        if margin >= MARGIN:
+            np.testing.assert_allclose(terms[b], t_ref, rtol=1e-4, atol=1e-3)
+        world_active += t_ref[4] > 0
+    stats.done()
+    if flags & inputs.SPEED or scene == "random":
+        assert world_active >= B // 4, "world term rarely active: the case would be vacuous"
+    ctx.close()
+
+
+def test_eval_to_parity_planar_cfg1(native, O):
+    rb = robots.planar2()
+    world = inputs.planar_scene()
+    cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED | inputs.JERK, dt=0.25)
+    ctx = make(native, rb, [world], cp)
+    R, W = O.Robot(rb), O.World(world)
+    g = np.random.default_rng(3)
+    B, H = 40, 16
+    st = f32(g.uniform(-np.pi, np.pi, (B, 2)))
+    V = f32(np.clip(st[:, None, :] + np.cumsum(g.normal(0, 0.3, (B, H, 2)), axis=1), -np.pi, np.pi))
+    gl = f32(np.concatenate([g.uniform(-1.5, 1.5, (B, 2)), np.zeros((B, 1)), np.tile([[1, 0, 0, 0]], (B, 1))], 1))
+    cost, grad, _ = ctx.evaluate(T(V), T(gl), start=T(st))
+    cost, grad = cost.cpu().numpy(), grad.cpu().numpy()
+    stats = Stats()
+    active = 0
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, W, cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"planar {b}")
+        active += (t_ref[3] > 0) + (t_ref[4] > 0)
+    stats.done(0.25)
+    assert active >= 5
+    ctx.close()
+
+
+def test_eval_edge_worlds(native, O):
+    """Empty environment, all-disabled environment, a single box."""
+    rb, starts, goals_cfg, trajs = franka_trajs(77, 6, 16)
+    empty = inputs.World(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros(0, np.int32))
+    alldis = inputs.random_world(5, 0, 8)
+    alldis.enabled[:] = 0
+    one = inputs.World(np.array([[0.4, 0.0, 0.4]]), np.array([[1.0, 0, 0, 0]]), np.array([[0.3, 0.3, 0.3]]),
+                       np.ones(1, np.int32))
+    worlds = [empty, alldis, one]
+    cp = inputs.CostParams()
+    ctx = make(native, rb, worlds, cp)
+    R = O.Robot(rb)
+    env = np.array([0, 1, 2, 0, 1, 2], np.int32)
+    goals = np.array([O.fk(R, q)[2] for q in goals_cfg])
+    V, st, gl = f32(trajs), f32(starts), f32(goals)
+    cost, grad, terms = ctx.evaluate(T(V), T(gl), start=T(st), env=T(env, torch.int32))
+    stats = Stats()
+    for b in range(6):
+        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, O.World(worlds[env[b]]), cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].cpu().numpy().astype(np.float64), c_ref, g_ref, margin, f"edge {b}")
+        if env[b] < 2:
+            assert float(terms[b, 4]) == 0.0
+    stats.done(0.5)
+    ctx.close()
+
+
+# ------------------------------------------------------------------------------------------ IK eval
+
+@pytest.mark.parametrize("B", [1, 32, 75])
+def test_eval_ik_parity(native, O, B):
+    rb = robots.franka64()
+    worlds = [inputs.random_world(9, e, 20, lo=-0.8, hi=0.8) for e in range(2)]
+    cp = inputs.CostParams()
+    ctx = make(native, rb, worlds, cp)
+    R = O.Robot(rb)
+    g = np.random.default_rng(B)
+    q = f32(g.uniform(rb.lo, rb.hi, (B, 7)))
+    gl = f32(np.array([O.fk(R, x + g.normal(0, 0.1, 7))[2] for x in q]))
+    env = ((np.arange(B) // 32) % 2).astype(np.int32)
+    cost, grad, terms = ctx.evaluate(T(q), T(gl), env=T(env, torch.int32))
+    cost, grad, terms = cost.cpu().numpy(), grad.cpu().numpy(), terms.cpu().numpy()
+    stats = Stats()
+    active = 0
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin, _ = O.eval_ik(R, O.World(worlds[env[b]]), cp, gl[b], q[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"ik {b}")
+        active += t_ref[4] > 0
+    stats.done(0.25)
+    if B >= 32:
+        assert active >= B // 10
+    ctx.close()
+
+
+def test_ik_env_group_violation_is_loud(native, O):
+    rb = robots.franka64()
+    worlds = [inputs.random_world(9, e, 5) for e in range(2)]
+    ctx = make(native, rb, worlds, inputs.CostParams())
+    q = T(np.tile(rb.ready, (4, 1)))
+    gl = T(np.tile([0.3, 0, 0.5, 1, 0, 0, 0], (4, 1)))
+    cost, _, _ = ctx.evaluate(q, gl, env=T(np.array([0, 0, 1, 0], np.int32), torch.int32))
+    c = cost.cpu().numpy()
+    assert np.isfinite(c[[0, 1, 3]]).all() and np.isnan(c[2])
+    ctx.close()
+
+
+# ------------------------------------------------------------------------------------------ selection
+
+def test_line_search_selection_bit_exact(native, O):
+    g = np.random.default_rng(0)
+    n, A = 4000, 4
+    alpha = np.array([0.01, 0.3, 0.7, 1.0], np.float32)
+    c0 = g.uniform(0, 10, n).astype(np.float32)
+    g0d = (-g.uniform(0, 10, n)).astype(np.float32)
+    ca = (c0[:, None] + g.normal(0, 1, (n, A))).astype(np.float32)
+    gda = g.normal(0, 10, (n, A)).astype(np.float32)
+    # adversarial rows: exact Armijo boundaries, ties, NaN, +-0, +-inf, uphill
+    for i in range(0, 400):
+        a = i % A
+        rhs = np.float32(c0[i] + np.float32(np.float32(np.float32(1e-4) * alpha[a]) * g0d[i]))
+        ca[i, a] = rhs if i % 2 == 0 else np.nextafter(rhs, np.float32(np.inf))
+    ca[400:450, 1] = np.nan
+    gda[450:500, 2] = np.nan
+    g0d[500:520] = 0.0
+    g0d[520:540] = -0.0
+    ca[540:560] = np.inf
+    c0[560:580] = np.inf
+    g0d[580:600] = -np.inf
+    gda[600:700, 3] = np.float32(0.9) * g0d[600:700]          # Wolfe boundary
+    gda[700:800, 3] = -np.float32(0.9) * g0d[700:800]
+    for mode in (0, 1, 2):
+        out = native.ls_select(alpha, T(c0), T(g0d), T(ca), T(gda), mode=mode).cpu().numpy()
+        ref = np.array([O.ls_select_f32(alpha, c0[i], g0d[i], ca[i], gda[i], mode=mode) for i in range(n)])
+        np.testing.assert_array_equal(out, ref)
+
+
+def _key(c, s):
+    if c != c:
+        bits = 0x7F800000
+    elif c == 0:
+        bits = 0
+    else:
+        bits = struct.unpack("<I", struct.pack("<f", np.float32(c)))[0]
+    return (bits << 32) | s
+
+
+def test_argmin_keys_bit_exact(native, O):
+    g = np.random.default_rng(1)
+    P, S = 300, 30
+    c = g.uniform(0, 100, (P, S)).astype(np.float32)
+    c[::7, 3] = c[::7, 1]            # ties -> lower seed
+    c[::11, :5] = np.nan
+    c[::13, 4] = 0.0
+    c[::17, 6] = -0.0
+    c[::19, :] = np.inf
+    key, idx = native.argmin_keys(T(c), seed_base=1000)
+    key, idx = key.cpu().numpy(), idx.cpu().numpy()
+    for p in range(P):
+        i = O.argmin_f32(c[p])
+        assert idx[p] == i
+        assert key[p] == _key(c[p, i], 1000 + i)
+
+
+# ------------------------------------------------------------------------------------------ two-loop
+
+@pytest.mark.parametrize("n,count", [(224, 0), (224, 1), (224, 4), (7, 4), (512, 16), (100, 3)])
+def test_two_loop_teacher_forced(native, O, n, count):
+    """The solver's two-loop routine on the GPU vs the oracle on identical fp32 inputs."""
+    g = np.random.default_rng(n + count)
+    B = 8
+    S = np.zeros((B, count, n), np.float32); Y = np.zeros((B, count, n), np.float32)
+    G = g.normal(size=(B, n)).astype(np.float32)
+    for b in range(B):
+        A = np.diag(g.uniform(1, 20, n))
+        S[b] = g.normal(size=(count, n))
+        Y[b] = S[b] @ A + 0.01 * g.normal(size=(count, n))
+    d = native.lbfgs_direction(T(S), T(Y), T(G)).cpu().numpy()
+    for b in range(B):
+        Sd, Yd = f32(S[b]), f32(Y[b])
+        rho = 1.0 / np.einsum("ij,ij->i", Sd, Yd) if count else np.zeros(0)
+        ref = O.lbfgs_direction(Sd, Yd, rho, f32(G[b]))
+        assert np.linalg.norm(d[b] - ref) <= 1e-3 * np.linalg.norm(ref)
+
+
+# ------------------------------------------------------------------------------------------ solves
+
+def planar_problems(O, P):
+    rb = robots.planar2()
+    R = O.Robot(rb)
+    g = np.random.default_rng(5)
+    starts, goals = [], []
+    for p in range(P):
+        s = g.uniform(-2.5, 2.5, 2)
+        q = g.uniform(-2.5, 2.5, 2)
+        starts.append(s); goals.append(O.fk(R, q)[2])
+    return rb, f32(starts), f32(goals)
+
+
+def test_solve_to_invariants_and_determinism(native, O):
+    rb, starts, goals = planar_problems(O, 8)
+    P, S, H = 8, 4, 16
+    world = inputs.planar_scene()
+    cp = inputs.CostParams(dt=0.25)
+    ctx = make(native, rb, [world], cp)
+    seeds = f32(np.stack([inputs.to_seeds(rb, 0, p, starts[p], starts[p] + 0.5, S, H) for p in range(P)]))
+    sp = inputs.SolverParams(iters=25)
+    out1 = ctx.solve(sp, T(seeds), T(goals), start=T(starts), seed_outputs=True)
+    out2 = ctx.solve(sp, T(seeds), T(goals), start=T(starts), seed_outputs=True)
+    for k in out1:
+        assert torch.equal(out1[k], out2[k]), k                       # bitwise deterministic
+    c0, _, _ = ctx.evaluate(T(seeds.reshape(P * S, H, 2)), T(np.repeat(goals, S, 0)),
+                            start=T(np.repeat(starts, S, 0)))
+    sbc = out1["seed_best_cost"].cpu().numpy().reshape(-1)
+    assert np.all(sbc <= c0.cpu().numpy() * (1 + 1e-6))               # best never worse than the seed
+    bc = out1["best_cost"].cpu().numpy()
+    np.testing.assert_array_equal(bc, sbc.reshape(P, S).min(1))
+    key = out1["best_key"].cpu().numpy()
+    for p in range(P):
+        i = int(np.argmin(sbc.reshape(P, S)[p]))
+        assert key[p] == _key(sbc.reshape(P, S)[p, i], i)
+    ctx.close()
+
+
+def test_solve_seed_base_and_host_api(native, O):
+    rb, starts, goals = planar_problems(O, 3)
+    P, S, H = 3, 5, 16
+    ctx = make(native, rb, [inputs.planar_scene()], inputs.CostParams())
+    seeds = f32(np.stack([inputs.to_seeds(rb, 1, p, starts[p], starts[p] - 0.4, S, H) for p in range(P)]))
+    sp = inputs.SolverParams(iters=10)
+    dev = ctx.solve(sp, T(seeds), T(goals), start=T(starts), seed_base=40)
+    key = dev["best_key"].cpu().numpy()
+    assert np.all((key & 0xFFFFFFFF) >= 40) and np.all((key & 0xFFFFFFFF) < 40 + S)
+    hs = torch.tensor(seeds, dtype=torch.float32).pin_memory()
+    hb = torch.empty(P, H, 2).pin_memory(); hc = torch.empty(P).pin_memory(); hk = torch.empty(P, dtype=torch.int64).pin_memory()
+    ctx.solve_host(sp, hs, torch.tensor(goals, dtype=torch.float32).pin_memory(),
+                   start=torch.tensor(starts, dtype=torch.float32).pin_memory(), seed_base=40,
+                   best_traj=hb, best_cost=hc, best_key=hk)
+    assert torch.equal(hb, dev["best_traj"].cpu()) and torch.equal(hc, dev["best_cost"].cpu())
+    assert torch.equal(hk, dev["best_key"].cpu())
+    ctx.close()
+
+
+def _success_to(O, R, W, cp, start, goal, traj):
+    c, _, t, _, _ = O.eval_traj(R, W, cp, start, goal, traj)
+    _, _, ee = O.fk(R, traj[-1])
+    pos_err = np.linalg.norm(ee[:3] - goal[:3])
+    return pos_err < 0.01 and t[3] == 0 and t[4] == 0
+
+
+def test_solve_to_statistical_vs_oracle_planar(native, O):
+    """Config 1: GPU and oracle full solves from the same seeds; success rates agree."""
+    P, S, H = 12, 4, 16
+    rb, starts, goals = planar_problems(O, P)
+    world = inputs.planar_scene()
+    cp = inputs.CostParams(dt=0.25)
+    ctx = make(native, rb, [world], cp)
+    R, W = O.Robot(rb), O.World(world)
+    seeds = f32(np.stack([inputs.to_seeds(rb, 2, p, starts[p], starts[p] + 0.3, S, H) for p in range(P)]))
+    sp = inputs.SolverParams(iters=25)
+    out = ctx.solve(sp, T(seeds), T(goals), start=T(starts), seed_outputs=True)
+    g_traj = out["best_traj"].cpu().numpy().astype(np.float64)
+    o_traj, o_cost = O.solve_to(R, [W], np.zeros(P, np.int32), cp, sp, seeds, starts, goals, nthreads=8)
+    g_ok = sum(_success_to(O, R, W, cp, starts[p], goals[p], g_traj[p]) for p in range(P))
+    o_best = o_traj[np.arange(P), o_cost.argmin(1)]
+    o_ok = sum(_success_to(O, R, W, cp, starts[p], goals[p], o_best[p]) for p in range(P))
+    assert g_ok >= o_ok - 2, (g_ok, o_ok)
+    g_best = out["best_cost"].cpu().numpy()
+    assert np.median(g_best / o_cost.min(1)) < 2.0
+    ctx.close()
+
+
+def test_solve_ik_statistical_vs_oracle(native, O):
+    """Config 3 in miniature: collision-free IK, 30 Halton seeds, GPU vs oracle success rates."""
+    rb = robots.franka64()
+    R = O.Robot(rb)
+    world = inputs.tabletop_scene(3, 0, 20)
+    W = O.World(world)
+    cp = inputs.CostParams()
+    ctx = make(native, rb, [world], cp)
+    P, S = 6, 30
+    g = np.random.default_rng(11)
+    goals = f32(np.array([O.fk(R, g.uniform(rb.lo * 0.6, rb.hi * 0.6))[2] for _ in range(P)]))
+    seeds = f32(np.stack([inputs.ik_seeds(rb, p, S) for p in range(P)]))
+    sp = inputs.SolverParams(iters=60)
+    out = ctx.solve(sp, T(seeds), T(goals), seed_outputs=True)
+    o_q, o_c = O.solve_ik(R, [W], np.zeros(P, np.int32), cp, sp, seeds, goals, nthreads=8)
+
+    def pos_err(q, goal):
+        return np.linalg.norm(O.fk(R, q)[2][:3] - goal[:3])
+    gq = out["best_traj"].cpu().numpy().astype(np.float64)
+    g_ok = sum(pos_err(gq[p], goals[p]) < 0.01 for p in range(P))
+    o_ok = sum(pos_err(o_q[p, o_c[p].argmin()], goals[p]) < 0.01 for p in range(P))
+    assert g_ok >= o_ok - 1, (g_ok, o_ok)
+    sbc = out["seed_best_cost"].cpu().numpy()
+    c0, _, _ = ctx.evaluate(T(seeds.reshape(-1, 7)), T(np.repeat(goals, S, 0)))
+    assert np.all(sbc.reshape(-1) <= c0.cpu().numpy() * (1 + 1e-6))
+    ctx.close()
+
+
+# ------------------------------------------------------------------------------------------ errors
+
+def test_error_statuses(native):
+    rb = robots.franka64()
+    ctx = native.Context(0)
+    with pytest.raises(native.CrbError) as e:
+        ctx.evaluate(T(np.zeros((2, 16, 7))), T(np.zeros((2, 7))), start=T(np.zeros((2, 7))))
+    assert e.value.code == -5                       # not ready
+    bad = robots.franka64()
+    bad.vmax[2] = 0.0
+    with pytest.raises(native.CrbError) as e:
+        ctx.set_robot(bad)
+    assert e.value.code == -3
+    ctx.set_robot(rb)
+    ctx.set_world([inputs.tabletop_scene(0, 0, 5)])
+    ctx.set_cost_params(inputs.CostParams())
+    with pytest.raises(native.CrbError) as e:
+        ctx.evaluate(T(np.zeros((2, 5, 7))), T(np.zeros((2, 7))), start=T(np.zeros((2, 7))))
+    assert e.value.code == -2                       # H < 8 in TO mode
+    ctx.close()
