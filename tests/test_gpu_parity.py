@@ -1,9 +1,12 @@
 """GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on identical seeded inputs.
 
 Tolerances (north star / SURVEY §8(c).4): per trajectory |dc| <= 1e-4 |c| + 1e-5 and
-||dg|| <= 1e-3 ||g|| + 1e-5 sqrt(N), after excluding evaluations whose oracle branch margin (at a
-branch where the cost or gradient is discontinuous) is below 1e-4; line-search selection and the
-packed-key argmin bit-exact on identical fp32 inputs.
+||dg|| <= 1e-3 ||g|| + 1e-5 sqrt(N), after excluding evaluations whose oracle branch margin (the
+distance to a branch where the cost or gradient is DISCONTINUOUS, oracle.h O10) is below 2e-5 m:
+100x the fp32 rounding of a world-frame position (~1e-7 m), so only evaluations whose discrete
+decision can actually differ between fp32 and fp64 are excluded.  The
+excluded fraction is asserted small.  Line-search selection and the packed-key argmin are
+bit-exact on identical fp32 inputs.
 """
 import struct
 
@@ -15,7 +18,7 @@ from paper_2310_17274_b200 import inputs, robots
 
 pytestmark = pytest.mark.gpu
 
-COST_RTOL, COST_ATOL, GRAD_RTOL, GRAD_ATOL, MARGIN = 1e-4, 1e-5, 1e-3, 1e-5, 1e-4
+COST_RTOL, COST_ATOL, GRAD_RTOL, GRAD_ATOL, MARGIN = 1e-4, 1e-5, 1e-3, 1e-5, 2e-5
 DEV = torch.device("cuda:0")
 
 
