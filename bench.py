@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path: batched per-seed L-BFGS trajectory optimisation (BASELINE.json
+configs[1], Franka 7-DoF, 64 spheres, 20 cuboids, 32 seeds x 32 timesteps, 100 iterations),
+P problems per GPU (weak scaling over GPUs, problem-sharded, no data-path collective).
+
+One step = one crb_lbfgs_solve over the whole per-GPU batch: every candidate evaluation of every
+seed (a1..a15 of SURVEY §8(a)).  value = seed-timestep cost+grad evals/s over all ranks, timed on
+the device with CUDA events around each solve (L2 flushed between steps, outside the events),
+max over ranks.  e2e = the same metric through crb_lbfgs_solve_host with pinned host buffers
+(H2D of seeds/starts/goals, solve, D2H of the winners, synchronise) timed by the host clock.
+
+--impl reference times the fp64 CPU oracle (oracle/, the correctness reference of this repo) on a
+bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "seed-timestep cost+grad evals/s"
+UNIT = "evals/s"
+FP32_LANES_PER_SM, SMS = 128, 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--problems", type=int, default=64, help="problems per GPU (32 seeds each)")
+    ap.add_argument("--iters", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(path))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_sample_rate(wl, problem: int, iters: int, nthreads: int):
+    """Time the fp64 oracle (as it stands) on problem `problem` of the workload: S seeds x iters."""
+    from oracle import oracle as O
+    from paper_2310_17274_b200 import inputs
+    R = O.Robot(wl.robot)
+    W = O.World(wl.worlds[wl.env[problem]])
+    sp = inputs.SolverParams(iters=iters, history=wl.solver.history, alpha=wl.solver.alpha, c1=wl.solver.c1,
+                             c2=wl.solver.c2, ls_mode=wl.solver.ls_mode)
+    seeds = wl.seeds[problem:problem + 1].astype(np.float64)
+    t0 = time.perf_counter()
+    if wl.H > 1:
+        O.solve_to(R, [W], np.zeros(1, np.int32), wl.cost, sp, seeds, wl.start[problem:problem + 1].astype(np.float64),
+                   wl.goal[problem:problem + 1].astype(np.float64), nthreads=nthreads)
+    else:
+        O.solve_ik(R, [W], np.zeros(1, np.int32), wl.cost, sp, seeds, wl.goal[problem:problem + 1].astype(np.float64),
+                   nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    A = len(sp.alpha)
+    evals = wl.S * (A * wl.H * iters + wl.H)
+    return evals / dt, dt, evals
+
+
+def cpu_baseline(wl, target_s: float = 12.0):
+    """Oracle on the host cores, bounded sample of problem 0 (about target_s seconds)."""
+    nthreads = os.cpu_count() or 1
+    rate1, dt1, _ = oracle_sample_rate(wl, 0, 1, nthreads)
+    per_iter = dt1 / 1.0
+    iters = int(max(1, min(wl.solver.iters, target_s / max(per_iter, 1e-3))))
+    rate, dt, evals = oracle_sample_rate(wl, 0, iters, nthreads)
+    return {"value": rate, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+            "sample": f"problem 0 of {wl.name}: {wl.S} seeds x {iters} L-BFGS iterations ({evals} evals, {dt:.1f} s, "
+                      f"fp64 C oracle, {nthreads} threads)"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2310_17274_b200 import robots, workload
+
+    class OracleKin:
+        def __init__(self):
+            self.R = O.Robot(robots.franka64())
+
+        def fk(self, q):
+            out = [O.fk(self.R, x) for x in q]
+            return np.array([o[1] for o in out]), np.array([o[2] for o in out])
+
+        def self_free(self, q):
+            return np.array([O.self_collision(self.R, O.fk(self.R, x)[1], 1.0)[0] == 0.0 for x in q])
+
+    wl = workload.franka_to(0, [0], S=32, H=32, iters=args.iters, kin=OracleKin())
+    nthreads = os.cpu_count() or 1
+    _, dt1, _ = oracle_sample_rate(wl, 0, 1, nthreads)
+    # each step a bounded sample: ~ 150 s / (steps + warmup) of oracle work in total
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    iters = int(max(1, min(args.iters, budget / max(dt1, 1e-3))))
+    for _ in range(args.warmup):
+        oracle_sample_rate(wl, 0, iters, nthreads)
+    times, evals = [], 0
+    for _ in range(args.steps):
+        r, dt, ev = oracle_sample_rate(wl, 0, iters, nthreads)
+        times.append(dt); evals += ev
+    value = evals / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg2_franka_to", "problems_per_step": 1, "seeds": 32, "timesteps": 32,
+                       "iters_per_step": iters, "boxes": 20, "spheres": 64, "dof": 7},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+                             "sample": f"1 problem x 32 seeds x {iters} iterations per step (fp64 C oracle)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2310_17274_b200 import native, parallel, workload
+
+    P = args.problems
+    lo = rank * P
+    wl = workload.franka_to(local, list(range(lo, lo + P)), S=32, H=32, iters=args.iters)
+    ctx = native.Context(local)
+    ctx.set_robot(wl.robot)
+    ctx.set_world(wl.worlds)
+    ctx.set_cost_params(wl.cost)
+    seeds = torch.tensor(wl.seeds, device=dev)
+    goal = torch.tensor(wl.goal, device=dev)
+    start = torch.tensor(wl.start, device=dev)
+    env = torch.tensor(wl.env, device=dev)
+    sp = wl.solver
+    evals_per_step = wl.evals_per_solve()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+
+    for _ in range(args.warmup):
+        ctx.solve(sp, seeds, goal, start=start, env=env)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()                       # L2 flush, outside the timed events
+            evs[k][0].record(stream)
+            out = ctx.solve(sp, seeds, goal, start=start, env=env)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    if world > 1:
+        total_ms = parallel.max_over_ranks(total_ms, dev)
+    evals_all = evals_per_step * args.steps * world
+    value = evals_all / (total_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (solve_to_kernel; the select kernel is ~us)
+    pk = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    peak_tf = SMS * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+    flops_eval = workload.nominal_flops_per_eval(wl)
+    launch_s = statistics.mean(step_ms) * 1e-3
+    achieved_tf = evals_per_step * flops_eval / launch_s / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("solve_to_kernel_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the host C-ABI call
+    e2e = None
+    if not args.no_e2e:
+        hs = seeds.cpu().pin_memory(); hg = goal.cpu().pin_memory(); hst = start.cpu().pin_memory()
+        he = env.cpu().pin_memory()
+        hb = torch.empty(P, 32, 7).pin_memory(); hc = torch.empty(P).pin_memory()
+        hk = torch.empty(P, dtype=torch.int64).pin_memory()
+        ctx.solve_host(sp, hs, hg, start=hst, env=he, best_traj=hb, best_cost=hc, best_key=hk)
+        tt = 0.0
+        for k in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            ctx.solve_host(sp, hs, hg, start=hst, env=he, best_traj=hb, best_cost=hc, best_key=hk)
+            tt += time.perf_counter() - t0
+        if world > 1:
+            tt = parallel.max_over_ranks(tt, dev)
+        h2d = hs.numel() * 4 + hg.numel() * 4 + hst.numel() * 4 + he.numel() * 4
+        d2h = hb.numel() * 4 + hc.numel() * 4 + hk.numel() * 8
+        e2e = {"value": evals_all / tt, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "cfg2_franka_to_batched", "problems_per_gpu": P, "global_problems": P * world,
+                           "seeds": 32, "timesteps": 32, "dof": 7, "spheres": 64, "self_pairs": int(len(wl.robot.pairs)),
+                           "boxes": 20, "iters": args.iters, "line_search": list(sp.alpha), "history": sp.history,
+                           "flags": "sweep+speed", "evals_per_step_per_gpu": evals_per_step,
+                           "l2": "flushed between timed steps (256 MB write, outside the events)",
+                           "parallelism": f"problem-sharded x{world}, no data-path collective"},
+                "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                             "frac": achieved_tf / peak_tf, "traffic": traffic,
+                             "kernel": "solve_to_kernel", "flops_per_eval": flops_eval,
+                             "peak_basis": f"148 SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"},
+                "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_native(args)
+
+
+if __name__ == "__main__":
+    main()
