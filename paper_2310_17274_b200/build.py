@@ -14,6 +14,7 @@ LIB = os.path.join(HERE, "libcurobo_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+         "-prec-div=false", "-prec-sqrt=false",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}",
          "--expt-relaxed-constexpr"]
 

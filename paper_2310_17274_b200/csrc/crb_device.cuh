@@ -1,10 +1,12 @@
 // crb_device.cuh -- sm_100a device code of the fused cost+gradient evaluation (one CTA, 32
 // configurations per pass) shared by the evaluate, FK and persistent-solver kernels.
 //
-// Mapping: a CTA of NT = 512 threads (16 warps); the 32 lanes of every
-// warp are the 32 configuration slots of the pass (TO: the H timesteps of one candidate
-// trajectory; IK: 32 seeds of one problem).  Warps split the kinematic-chain rows (FK), the
-// spheres (world collision), the pair list (self-collision) and the (dof, config) elements; all
+// Mapping: a CTA of NT = 256 threads (8 warps), two CTAs resident per SM
+// (shared-memory footprint ~100 KB for the Franka problem) so one CTA's barrier phases overlap
+// the other's arithmetic.  The 32 lanes of every warp are the 32 configuration slots of the pass
+// (TO: the H timesteps of one candidate trajectory; IK: 32 seeds of one problem).  Warps split
+// the kinematic-chain rows (FK), the spheres (world collision, two spheres per thread per cuboid
+// load), the pair list (self-collision, CSR order by first sphere) and the (dof, slot) elements;
 // cross-warp combination goes through shared memory in a fixed order, so every result is
 // bitwise deterministic.  The robot tables and this environment's cuboids are staged into shared
 // memory once per CTA with TMA bulk copies (cp.async.bulk + mbarrier).
@@ -15,7 +17,7 @@
 
 namespace crb {
 
-constexpr int NT = 512;          // threads per CTA
+constexpr int NT = 256;          // threads per CTA
 constexpr int NW = NT / 32;      // warps per CTA
 constexpr int NC = 32;           // configuration slots per pass (= lanes)
 constexpr unsigned FULL = 0xffffffffu;
@@ -31,7 +33,11 @@ struct RobotPack {
     int o_sph;      // M float4 (centre in link frame, radius), spheres grouped by link
     int o_sphlink;  // M ints
     int o_sbeg;     // L+1 ints: spheres of link l are [sbeg[l], sbeg[l+1])
-    int o_pairs;    // P x 2 words: (i | j << 16), float bits of r_i+o_i+r_j+o_j
+    int o_rself;    // M floats: self-collision radius r + o (Alg. 9)
+    int o_blocks;   // NB x uint2: pair block (ia | (na-1) << 9 | jb << 11 | len << 20, rank base):
+                    //   the pairs {ia..ia+na-1} x {jb..jb+len-1}, all in S (na <= 4)
+    int o_wblk;     // NW+1 ints: blocks of warp w are [wblk[w], wblk[w+1]) (balanced on the host)
+    int o_rank;     // u16 ranks in S of the block pairs, [block][u][v] from the block's rank base
     int o_lim;      // 5 x D floats: lo, hi, vmax, amax, jmax
     int o_doflink;  // D ints: link carrying dof d
     int o_perm;     // M ints: packed sphere index -> caller's sphere index
@@ -41,24 +47,29 @@ struct RobotPack {
 // Shared-memory layout (offsets in 4-byte words from the dynamic smem base).
 struct Layout {
     int robot, boxes, mbar;
-    int q_cfg, xs, lt, sw, sg, ls, sbest, sidx, wpart, cbb, csm, gxd, gva, pose_ft, pose_c,
-        goal, cfg_cost, cfg_terms, gV, red, st;
+    int q_cfg, xs, ltg, frames, swl, sbest, srank, sij, wpart, cbb, csm, gxd, gq, gva, pose_ft, pose_c,
+        goal, cfg_cost, cfg_terms, gV, red, st, scal;
     int solver;      // start of the solver region
     int total;       // words
     int XS;          // row length of xs (H + 5)
 };
 
+// Cost parameters (App. A), copied by value into registers by eval_pass.
+struct CostP {
+    float a0, a1, a2, a3, a8, a9, wb[4], beta_self, beta_world, eta, eta_bound, dt;
+    float inv_eta, inv_2dt;   // host-computed reciprocals (no divisions in the hot loops)
+    int sweep_steps, H;
+    unsigned flags;
+};
+
 struct KParams {
     RobotPack rp;
     Layout lay;
+    CostP cp;
     const float4 *robot;     // packed robot blob (global)
     const float4 *boxes;     // [n_env][kmax][4] float4: (R col i, -col_i . t) x3, (h, 0)
     const int *box_count;    // [n_env] enabled (compacted) boxes
     int kmax, n_env;
-    // cost parameters (App. A)
-    float a0, a1, a2, a3, a8, a9, wb[4], beta_self, beta_world, eta, eta_bound, dt;
-    int sweep_steps;
-    unsigned flags;
     // solver parameters (Alg. 6, Alg. 1)
     int iters, m, A, ls_mode;
     float alpha[8], c1, c2;
@@ -86,16 +97,20 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// Deterministic CTA-wide sum of one value per thread (fixed order over warps).
-__device__ __forceinline__ float block_sum(float v, float *red) {
+// Deterministic CTA-wide sum of one value per thread, fixed order over warps.  `red` holds two
+// NW-slot halves used alternately (`ph` flips per call), so one barrier per call is enough: a
+// thread can only overwrite a half after every thread has passed the barrier of the call in
+// between, i.e. finished reading that half.
+__device__ __forceinline__ float block_sum(float v, float *red, int &ph) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     v = warp_sum(v);
-    if (lane == 0) red[warp] = v;
+    float *r = red + ph * NW;
+    if (lane == 0) r[warp] = v;
     __syncthreads();
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) s += red[w];
-    __syncthreads();
+    for (int w = 0; w < NW; ++w) s += r[w];
+    ph ^= 1;
     return s;
 }
 
@@ -129,11 +144,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
 // each, P:3014 float4 layout).  Must be called by all threads; ends with the data visible.
 __device__ __forceinline__ int stage_tables(const KParams &kp, float *smem, int env) {
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + kp.lay.mbar);
-    int K = (env >= 0 && env < kp.n_env) ? kp.box_count[env] : 0;
+    const int K = (env >= 0 && env < kp.n_env) ? kp.box_count[env] : 0;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        uint32_t rbytes = (uint32_t)kp.rp.words * 4u;
-        uint32_t bbytes = (uint32_t)K * 64u;
+        const uint32_t rbytes = (uint32_t)kp.rp.words * 4u;
+        const uint32_t bbytes = (uint32_t)K * 64u;
         mbar_expect_tx(bar, rbytes + bbytes);
         bulk_g2s(smem + kp.lay.robot, kp.robot, rbytes, bar);
         if (K > 0) bulk_g2s(smem + kp.lay.boxes, kp.boxes + (size_t)env * kp.kmax * 4, bbytes, bar);
@@ -148,9 +163,9 @@ __device__ __forceinline__ int stage_tables(const KParams &kp, float *smem, int 
 // ------------------------------------------------------------------------------------------
 
 // Eq. smooth-distance-cases in penetration-positive form d' = r' - sd (A2).
-__device__ __forceinline__ float activation(float dp, float eta, float &dphi) {
+__device__ __forceinline__ float activation(float dp, float eta, float inv_eta, float &dphi) {
     if (dp <= 0.f) { dphi = 0.f; return 0.f; }
-    if (dp <= eta) { dphi = dp / eta; return dp * dp / (2.f * eta); }
+    if (dp <= eta) { dphi = dp * inv_eta; return 0.5f * dp * dp * inv_eta; }
     dphi = 1.f;
     return dp - 0.5f * eta;
 }
@@ -176,9 +191,7 @@ __device__ __forceinline__ float logcoshf(float x) {
     return ax + log1pf(expf(-2.f * ax)) - 0.69314718055994531f;
 }
 
-// Signed distance of a point to one cuboid stored as 4 float4 (R columns with -col.t, half
-// extents): exact Euclidean box SDF (A4).  Returns sd; `out` = outside flag; writes the local
-// gradient on request.
+// One cuboid as 4 float4: rows of R^T with -col_i . t, then the half extents.
 struct BoxView {
     float4 c0, c1, c2, h;
 };
@@ -195,21 +208,21 @@ __device__ __forceinline__ void box_local(const BoxView &b, float px, float py, 
     lz = fmaf(b.c2.x, px, fmaf(b.c2.y, py, fmaf(b.c2.z, pz, b.c2.w)));
 }
 
-// Full SDF + world-frame gradient at a point (used on hits and sweep samples).
+// Exact Euclidean box SDF (A4) + world-frame gradient at a point (hits and sweep samples).
 __device__ __forceinline__ float box_sdf_grad(const BoxView &b, float px, float py, float pz, float &gx,
                                               float &gy, float &gz) {
     float lx, ly, lz;
     box_local(b, px, py, pz, lx, ly, lz);
-    float qx = fabsf(lx) - b.h.x, qy = fabsf(ly) - b.h.y, qz = fabsf(lz) - b.h.z;
-    float qm = fmaxf(qx, fmaxf(qy, qz));
+    const float qx = fabsf(lx) - b.h.x, qy = fabsf(ly) - b.h.y, qz = fabsf(lz) - b.h.z;
+    const float qm = fmaxf(qx, fmaxf(qy, qz));
     float glx = 0.f, gly = 0.f, glz = 0.f, sd;
     if (qm > 0.f) {
-        float mx = fmaxf(qx, 0.f), my = fmaxf(qy, 0.f), mz = fmaxf(qz, 0.f);
+        const float mx = fmaxf(qx, 0.f), my = fmaxf(qy, 0.f), mz = fmaxf(qz, 0.f);
         sd = sqrtf(mx * mx + my * my + mz * mz);
-        float inv = 1.f / sd;
-        glx = copysignf(mx * inv, lx >= 0.f ? 1.f : -1.f);
-        gly = copysignf(my * inv, ly >= 0.f ? 1.f : -1.f);
-        glz = copysignf(mz * inv, lz >= 0.f ? 1.f : -1.f);
+        const float inv = __frcp_rn(sd);
+        glx = (lx >= 0.f ? mx : -mx) * inv;
+        gly = (ly >= 0.f ? my : -my) * inv;
+        glz = (lz >= 0.f ? mz : -mz) * inv;
     } else {
         sd = qm;  // first arg-max in x, y, z order; sign(0) = +1
         if (qx >= qy && qx >= qz) glx = lx >= 0.f ? 1.f : -1.f;
@@ -229,7 +242,7 @@ __device__ __forceinline__ int ls_select(int A, const float *alpha, float c0, fl
                                          const float *gda, float c1, float c2, int mode) {
     int best = 0;
     for (int a = 0; a < A; ++a) {
-        float rhs = __fadd_rn(c0, __fmul_rn(__fmul_rn(c1, alpha[a]), g0d));
+        const float rhs = __fadd_rn(c0, __fmul_rn(__fmul_rn(c1, alpha[a]), g0d));
         bool ok = ca[a] <= rhs;
         if (mode == 1) ok = ok && (gda[a] >= __fmul_rn(c2, g0d));
         if (mode == 2) ok = ok && (fabsf(gda[a]) <= __fmul_rn(c2, fabsf(g0d)));
@@ -260,9 +273,9 @@ struct Smem {
     const int *iw;          // robot blob as ints
     const float *fw;        // robot blob as floats
     const float *boxes;
-    float *q_cfg, *xs, *lt, *sw, *sg, *ls, *sbest, *wpart, *cbb, *csm, *gxd, *gva, *pose_ft, *pose_c,
-        *goal, *cfg_cost, *cfg_terms, *gV, *red, *st;
-    int *sidx;
+    float *q_cfg, *xs, *lt, *sg, *frames, *sw, *ls, *sbest, *wpart, *cbb, *csm, *gxd, *gq, *gva, *pose_ft,
+        *pose_c, *goal, *cfg_cost, *cfg_terms, *gV, *red, *st, *scal;
+    int *srank, *sij;
 };
 
 __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
@@ -271,24 +284,32 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     s.iw = reinterpret_cast<const int *>(smem + L.robot);
     s.fw = smem + L.robot;
     s.boxes = smem + L.boxes;
-    s.q_cfg = smem + L.q_cfg; s.xs = smem + L.xs; s.lt = smem + L.lt; s.sw = smem + L.sw;
-    s.sg = smem + L.sg; s.ls = smem + L.ls; s.sbest = smem + L.sbest;
-    s.sidx = reinterpret_cast<int *>(smem + L.sidx);
+    s.q_cfg = smem + L.q_cfg; s.xs = smem + L.xs;
+    s.lt = smem + L.ltg; s.sg = smem + L.ltg;          // sg aliases lt (lt dead after sphere placement)
+    s.frames = smem + L.frames;
+    s.sw = smem + L.swl; s.ls = smem + L.swl;          // ls aliases sw (written after a barrier)
+    s.sbest = smem + L.sbest;
+    s.srank = reinterpret_cast<int *>(smem + L.srank);
+    s.sij = reinterpret_cast<int *>(smem + L.sij);
     s.wpart = smem + L.wpart; s.cbb = smem + L.cbb; s.csm = smem + L.csm; s.gxd = smem + L.gxd;
-    s.gva = smem + L.gva; s.pose_ft = smem + L.pose_ft; s.pose_c = smem + L.pose_c;
+    s.gq = smem + L.gq; s.gva = smem + L.gva; s.pose_ft = smem + L.pose_ft; s.pose_c = smem + L.pose_c;
     s.goal = smem + L.goal; s.cfg_cost = smem + L.cfg_cost; s.cfg_terms = smem + L.cfg_terms;
-    s.gV = smem + L.gV; s.red = smem + L.red; s.st = smem + L.st;
+    s.gV = smem + L.gV; s.red = smem + L.red; s.st = smem + L.st; s.scal = smem + L.scal;
     return s;
 }
 
+// frames[d][6][32]: world axis k and origin o of the joint carrying dof d; then EE R (9) + p (3).
+__device__ __forceinline__ float *ee_frame(const Smem &s, int D) { return s.frames + D * 6 * NC; }
+
 // Forward kinematics of the 32 slots (Alg. 7 / Table 6): warps 0..2 each own one row of the
 // 3x4 link transforms (the paper's "parallel threads per matrix"), lane = slot.  Writes
-// lt[l][12][32]; then every warp places its spheres: sw[m][3][32] = R_link c_m + t_link.
-__device__ __forceinline__ void fk_phase(const KParams &kp, const Smem &s) {
-    const RobotPack &rp = kp.rp;
+// lt[l][12][32] plus the compact joint frames / EE pose; then every warp places its spheres:
+// sw[m][3][32] = R_link c_m + t_link.
+__device__ __forceinline__ void fk_phase(const RobotPack rp, const Smem &s) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (warp < 3) {
         const int r = warp;
+        float *fee = ee_frame(s, rp.D);
         float4 cur = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int l = 0; l < rp.L; ++l) {
             const float *F = s.fw + rp.o_links + 16 * l;
@@ -316,15 +337,15 @@ __device__ __forceinline__ void fk_phase(const KParams &kp, const Smem &s) {
                     float sn, cs;
                     sincosf(v, &sn, &cs);
                     if (type == 4) {        // revolute x: col1' = c f1 + s f2, col2' = -s f1 + c f2
-                        float a0 = m01, a1 = m11, a2 = m21;
+                        const float a0 = m01, a1 = m11, a2 = m21;
                         m01 = cs * a0 + sn * m02; m11 = cs * a1 + sn * m12; m21 = cs * a2 + sn * m22;
                         m02 = -sn * a0 + cs * m02; m12 = -sn * a1 + cs * m12; m22 = -sn * a2 + cs * m22;
                     } else if (type == 5) { // revolute y: col0' = c f0 - s f2, col2' = s f0 + c f2
-                        float a0 = m00, a1 = m10, a2 = m20;
+                        const float a0 = m00, a1 = m10, a2 = m20;
                         m00 = cs * a0 - sn * m02; m10 = cs * a1 - sn * m12; m20 = cs * a2 - sn * m22;
                         m02 = sn * a0 + cs * m02; m12 = sn * a1 + cs * m12; m22 = sn * a2 + cs * m22;
                     } else {                // revolute z: col0' = c f0 + s f1, col1' = -s f0 + c f1
-                        float a0 = m00, a1 = m10, a2 = m20;
+                        const float a0 = m00, a1 = m10, a2 = m20;
                         m00 = cs * a0 + sn * m01; m10 = cs * a1 + sn * m11; m20 = cs * a2 + sn * m21;
                         m01 = -sn * a0 + cs * m01; m11 = -sn * a1 + cs * m11; m21 = -sn * a2 + cs * m21;
                     }
@@ -337,6 +358,16 @@ __device__ __forceinline__ void fk_phase(const KParams &kp, const Smem &s) {
             nr.w = pr.x * m03 + pr.y * m13 + pr.z * m23 + pr.w;
             float *dst = s.lt + (l * 12 + r * 4) * NC + lane;
             dst[0] = nr.x; dst[NC] = nr.y; dst[2 * NC] = nr.z; dst[3 * NC] = nr.w;
+            if (type != 0) {   // joint axis = column `ax` of R_l, origin = t_l (Table 7)
+                const int ax = type >= 4 ? type - 4 : type - 1;
+                float *fr = s.frames + dof * 6 * NC + lane;
+                fr[r * NC] = ax == 0 ? nr.x : (ax == 1 ? nr.y : nr.z);
+                fr[(3 + r) * NC] = nr.w;
+            }
+            if (l == rp.ee) {
+                fee[(3 * r + 0) * NC + lane] = nr.x; fee[(3 * r + 1) * NC + lane] = nr.y;
+                fee[(3 * r + 2) * NC + lane] = nr.z; fee[(9 + r) * NC + lane] = nr.w;
+            }
             cur = nr;
         }
     }
@@ -346,9 +377,9 @@ __device__ __forceinline__ void fk_phase(const KParams &kp, const Smem &s) {
         const int l = s.iw[rp.o_sphlink + m];
         const float4 c = sph[m];
         const float *T = s.lt + l * 12 * NC + lane;
-        float wx = T[0] * c.x + T[NC] * c.y + T[2 * NC] * c.z + T[3 * NC];
-        float wy = T[4 * NC] * c.x + T[5 * NC] * c.y + T[6 * NC] * c.z + T[7 * NC];
-        float wz = T[8 * NC] * c.x + T[9 * NC] * c.y + T[10 * NC] * c.z + T[11 * NC];
+        const float wx = T[0] * c.x + T[NC] * c.y + T[2 * NC] * c.z + T[3 * NC];
+        const float wy = T[4 * NC] * c.x + T[5 * NC] * c.y + T[6 * NC] * c.z + T[7 * NC];
+        const float wz = T[8 * NC] * c.x + T[9 * NC] * c.y + T[10 * NC] * c.z + T[11 * NC];
         float *dst = s.sw + m * 3 * NC + lane;
         dst[0] = wx; dst[NC] = wy; dst[2 * NC] = wz;
     }
@@ -358,100 +389,139 @@ __device__ __forceinline__ void fk_phase(const KParams &kp, const Smem &s) {
 // Matrix -> quaternion (Shepperd), canonical w >= 0 (A31).
 __device__ __forceinline__ void mat_to_quat(float r00, float r01, float r02, float r10, float r11, float r12,
                                             float r20, float r21, float r22, float q[4]) {
-    float tr = r00 + r11 + r22;
+    const float tr = r00 + r11 + r22;
     float w, x, y, z;
     if (tr >= r00 && tr >= r11 && tr >= r22) {
-        w = 0.5f * sqrtf(1.f + tr); float k = 0.25f / w;
+        w = 0.5f * sqrtf(1.f + tr); const float k = 0.25f / w;
         x = (r21 - r12) * k; y = (r02 - r20) * k; z = (r10 - r01) * k;
     } else if (r00 >= r11 && r00 >= r22) {
-        x = 0.5f * sqrtf(1.f + r00 - r11 - r22); float k = 0.25f / x;
+        x = 0.5f * sqrtf(1.f + r00 - r11 - r22); const float k = 0.25f / x;
         w = (r21 - r12) * k; y = (r01 + r10) * k; z = (r02 + r20) * k;
     } else if (r11 >= r22) {
-        y = 0.5f * sqrtf(1.f - r00 + r11 - r22); float k = 0.25f / y;
+        y = 0.5f * sqrtf(1.f - r00 + r11 - r22); const float k = 0.25f / y;
         w = (r02 - r20) * k; x = (r01 + r10) * k; z = (r12 + r21) * k;
     } else {
-        z = 0.5f * sqrtf(1.f - r00 - r11 + r22); float k = 0.25f / z;
+        z = 0.5f * sqrtf(1.f - r00 - r11 + r22); const float k = 0.25f / z;
         w = (r10 - r01) * k; x = (r02 + r20) * k; y = (r12 + r21) * k;
     }
     if (w < 0.f) { w = -w; x = -x; y = -y; z = -z; }
     q[0] = w; q[1] = x; q[2] = y; q[3] = z;
 }
 
-// World term of one sphere at one slot (Alg. 10 discrete + §3.4 / Algs. 11-12 swept under
-// readings A6-A12; O5 in DESIGN.md).  Accumulates E and dE/dc (before beta_2 * speed).
-__device__ __forceinline__ float sphere_world(const float *boxes, int K, float cx, float cy, float cz, float rp,
-                                              float eta, bool doB, float bx, float by, float bz, float LB,
-                                              bool doF, float fx, float fy, float fz, float LF, int steps,
-                                              float &Gx, float &Gy, float &Gz) {
-    float E = 0.f;
-    const float boundB = 0.5f * LB, boundF = 0.5f * LF;
-    float maxb = 0.f;
-    if (doB) maxb = boundB;
-    if (doF) maxb = fmaxf(maxb, boundF);
-    const float rp2 = rp * rp, maxb2 = maxb * maxb;
-    for (int k = 0; k < K; ++k) {
-        const BoxView b = load_box(boxes, k);
-        float lx, ly, lz;
-        box_local(b, cx, cy, cz, lx, ly, lz);
-        const float qx = fabsf(lx) - b.h.x, qy = fabsf(ly) - b.h.y, qz = fabsf(lz) - b.h.z;
-        const float qm = fmaxf(qx, fmaxf(qy, qz));
-        const float mx = fmaxf(qx, 0.f), my = fmaxf(qy, 0.f), mz = fmaxf(qz, 0.f);
-        const float s2 = mx * mx + my * my + mz * mz;
-        const bool hit = (qm <= 0.f) || (s2 < rp2);
-        const bool sweep = (doB || doF) && (hit || s2 < maxb2);
-        if (!hit && !sweep) continue;
-        float sd0 = 0.f;
-        if (hit) {
+// State of one sphere at one slot for the world term (Alg. 10 discrete + §3.4 / Algs. 11-12
+// swept under readings A6-A12; O5 in DESIGN.md).  Only what the per-cuboid screen needs lives in
+// registers; the sweep geometry is rebuilt from shared memory on the (rare) slow path.
+struct SphereWorld {
+    float cx, cy, cz, rp, rp2, thr2;         // centre, r' = r + eta, r'^2, screen threshold (-1 = off)
+    float E, Gx, Gy, Gz;                     // sum of phi and dE/dc
+    const float *p;                          // &sw[m][0][lane]
+    int dirs;                                // bit 0: backward sweep, bit 1: forward sweep
+};
+
+// Cheap screening test of one box: returns s2 = sd^2 outside (0 inside), no square root.  The
+// box matters iff s2 < thr2: a discrete hit (sd < r') or a possible sweep sample (sd < the larger
+// half-segment).
+__device__ __forceinline__ float box_screen(const SphereWorld &w, const BoxView &b) {
+    float lx, ly, lz;
+    box_local(b, w.cx, w.cy, w.cz, lx, ly, lz);
+    const float mx = fmaxf(fabsf(lx) - b.h.x, 0.f), my = fmaxf(fabsf(ly) - b.h.y, 0.f),
+                mz = fmaxf(fabsf(lz) - b.h.z, 0.f);
+    return fmaf(mx, mx, fmaf(my, my, mz * mz));
+}
+
+// Rare path: the hit's activation and gradient, then the backward / forward marches (A6-A12):
+// L = |n - c|, bound = L/2, j = J0 (r' on a hit, else sd), at most n_s samples p = c + (j/L)(n - c);
+// a hit adds phi and (1 - kappa) phi' (-grad sd) and jumps r', a miss jumps sd.
+__device__ __forceinline__ void box_slow(SphereWorld &w, const BoxView &b, float s2, float eta, float inv_eta,
+                                         int steps) {
+    const bool hit = s2 < w.rp2;                       // inside (s2 = 0) or within r'
+    float sd0;
+    if (hit) {
+        float gx, gy, gz;
+        sd0 = box_sdf_grad(b, w.cx, w.cy, w.cz, gx, gy, gz);
+        float dphi;
+        w.E += activation(w.rp - sd0, eta, inv_eta, dphi);
+        w.Gx -= dphi * gx; w.Gy -= dphi * gy; w.Gz -= dphi * gz;
+    } else {
+        sd0 = sqrtf(s2);
+    }
+    if (!w.dirs) return;
+    const float J0 = (w.rp - sd0 > 0.f) ? w.rp : sd0;
+#pragma unroll 1
+    for (int dir = 0; dir < 2; ++dir) {
+        if (!(w.dirs & (1 << dir))) continue;
+        const int o = dir == 0 ? -1 : 1;               // neighbouring slot (timestep)
+        const float vx = w.p[o] - w.cx, vy = w.p[NC + o] - w.cy, vz = w.p[2 * NC + o] - w.cz;
+        const float L = sqrtf(vx * vx + vy * vy + vz * vz);
+        const float iL = 1.f / L, bound = 0.5f * L;
+        float j = J0;
+        for (int st = 0; st < steps; ++st) {
+            if (j >= bound) break;
+            const float kap = j * iL;
+            const float px = fmaf(kap, vx, w.cx), py = fmaf(kap, vy, w.cy), pz = fmaf(kap, vz, w.cz);
             float gx, gy, gz;
-            sd0 = box_sdf_grad(b, cx, cy, cz, gx, gy, gz);
-            float dphi;
-            const float phi = activation(rp - sd0, eta, dphi);
-            E += phi;
-            Gx -= dphi * gx; Gy -= dphi * gy; Gz -= dphi * gz;
-        } else {
-            sd0 = sqrtf(s2);
-        }
-        if (!sweep) continue;
-        const float J0 = (rp - sd0 > 0.f) ? rp : sd0;
-#pragma unroll
-        for (int dir = 0; dir < 2; ++dir) {
-            const bool on = dir == 0 ? doB : doF;
-            if (!on) continue;
-            const float L = dir == 0 ? LB : LF, bound = dir == 0 ? boundB : boundF;
-            const float vx = dir == 0 ? bx : fx, vy = dir == 0 ? by : fy, vz = dir == 0 ? bz : fz;
-            float j = J0;
-            for (int st = 0; st < steps; ++st) {
-                if (j >= bound) break;
-                const float kap = j / L;
-                const float px = fmaf(kap, vx, cx), py = fmaf(kap, vy, cy), pz = fmaf(kap, vz, cz);
-                float gx, gy, gz;
-                const float sd = box_sdf_grad(b, px, py, pz, gx, gy, gz);
-                const float dp = rp - sd;
-                if (dp > 0.f) {
-                    float dphi;
-                    E += activation(dp, eta, dphi);
-                    const float w = (1.f - kap) * dphi;
-                    Gx -= w * gx; Gy -= w * gy; Gz -= w * gz;
-                    j += rp;
-                } else {
-                    j += sd;
-                }
+            const float sd = box_sdf_grad(b, px, py, pz, gx, gy, gz);
+            const float dp = w.rp - sd;
+            if (dp > 0.f) {
+                float dphi;
+                w.E += activation(dp, eta, inv_eta, dphi);
+                const float f = (1.f - kap) * dphi;
+                w.Gx -= f * gx; w.Gy -= f * gy; w.Gz -= f * gz;
+                j += w.rp;
+            } else {
+                j += sd;
             }
         }
     }
-    return E;
+}
+
+// Set up sphere m at this lane's slot: neighbours, speed metric (A13), sweep flags (A6: a
+// direction is swept iff its neighbour exists and gap = L - 2r' > 0).  Returns the speed factor.
+__device__ __forceinline__ float setup_sphere(SphereWorld &w, const Smem &s, int m, float r, int lane, bool hasp,
+                                              bool hasn, bool sweepf, bool speedf, float eta, float inv_2dt) {
+    const float *p = s.sw + m * 3 * NC + lane;
+    w.p = p;
+    w.cx = p[0]; w.cy = p[NC]; w.cz = p[2 * NC];
+    float px = w.cx, py = w.cy, pz = w.cz, nx = w.cx, ny = w.cy, nz = w.cz;
+    if (hasp) { px = p[-1]; py = p[NC - 1]; pz = p[2 * NC - 1]; }
+    if (hasn) { nx = p[1]; ny = p[NC + 1]; nz = p[2 * NC + 1]; }
+    float sp = 1.f;
+    if (speedf) {
+        const float dx = nx - px, dy = ny - py, dz = nz - pz;
+        sp = sqrtf(dx * dx + dy * dy + dz * dz) * inv_2dt;
+    }
+    w.rp = r + eta;                     // Alg. 10 "sph.radius += eta"
+    w.rp2 = w.rp * w.rp;
+    const float bx = px - w.cx, by = py - w.cy, bz = pz - w.cz;
+    const float fx = nx - w.cx, fy = ny - w.cy, fz = nz - w.cz;
+    const float LB = sqrtf(bx * bx + by * by + bz * bz), LF = sqrtf(fx * fx + fy * fy + fz * fz);
+    const bool doB = sweepf && hasp && (LB - 2.f * w.rp > 0.f);
+    const bool doF = sweepf && hasn && (LF - 2.f * w.rp > 0.f);
+    w.dirs = (doB ? 1 : 0) | (doF ? 2 : 0);
+    float maxb = 0.f;
+    if (doB) maxb = 0.5f * LB;
+    if (doF) maxb = fmaxf(maxb, 0.5f * LF);
+    // r < 0 disables the sphere; sp = 0 => C_w = 0 exactly
+    const bool on = (r >= 0.f) && (sp != 0.f);
+    w.thr2 = on ? fmaxf(w.rp2, maxb * maxb) : -1.f;
+    w.E = 0.f; w.Gx = 0.f; w.Gy = 0.f; w.Gz = 0.f;
+    return sp;
 }
 
 // One evaluation pass over the 32 slots.  Inputs already in shared memory:
-//   TO: s.gV is NOT an input; the candidate V[H][D] is in `thA`, start in s.st, goal in s.goal.
+//   TO: the candidate V[H][D] in `thA`, start in s.st, goal in s.goal[7][32].
 //   IK: configurations in s.q_cfg[D][32], goals in s.goal[7][32].
-// Outputs: s.cfg_cost[32], s.cfg_terms[5][32]; TO: s.gV[H][D] = dC/dV; IK: s.gV[D][32].
-// n_act = number of valid slots (TO: H, IK: active seeds).
+//   dvec (TO, optional): a direction in smem; the pass then also returns g.dvec in s.scal[1].
+// Outputs: s.cfg_cost[32], s.cfg_terms[5][32], s.scal[0] = sum of the slot costs;
+//   TO: s.gV[H][D] = dC/dV; IK: s.gV[D][32].  Ends with a barrier.
 template <int MODE>
-__device__ void eval_pass(const KParams &kp, const Smem &s, const float *thA, int K, int n_act) {
-    const RobotPack &rp = kp.rp;
+__device__ __noinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
+                                       const float *dvec) {
+    const Smem s = make_smem(kp, smem);   // one out-of-line copy per mode keeps the hot code in I-cache
+    const RobotPack rp = kp.rp;           // by value: registers, not generic loads of the parameter block
+    const CostP cf = kp.cp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int D = rp.D, H = kp.H, XS = kp.lay.XS;
+    const int D = rp.D, H = cf.H, XS = kp.lay.XS;
     const float *lim = s.fw + rp.o_lim;
 
     // ---- a2: state map (O2, Table 5 last row) into xs[D][H+5] and the slot configurations
@@ -476,73 +546,112 @@ __device__ void eval_pass(const KParams &kp, const Smem &s, const float *thA, in
         __syncthreads();
     }
 
-    // ---- a3: forward kinematics
-    fk_phase(kp, s);
+    // ---- a3: forward kinematics (after this, lt is dead and its space holds sg)
+    fk_phase(rp, s);
 
-    // ---- a4: self-collision (Eq. self-collision, Alg. 9): warp w scans pairs w, w+NW, ...;
-    // lane = slot; first maximal pair per warp (strict >), merged in pair order below (A28).
+    // ---- a4: self-collision (Eq. self-collision, Alg. 9).  S is stored as rectangular blocks of
+    // pairs {ia..ia+na-1} x {jb..jb+len-1} (spheres of one link share their partner ranges); each
+    // warp walks its blocks holding the na <= 4 first spheres in registers and streaming the
+    // partners, lane = slot.  Ties go to the lowest rank in S (first maximal pair, A28).
     {
         float best = 0.f;
-        int bidx = -1;
-        const uint2 *pairs = reinterpret_cast<const uint2 *>(s.iw + rp.o_pairs);
-        for (int p = warp; p < rp.P; p += NW) {
-            const uint2 pr = pairs[p];
-            const int i = pr.x & 0xffff, j = pr.x >> 16;
-            const float R = __uint_as_float(pr.y);
-            const float *wi = s.sw + i * 3 * NC + lane, *wj = s.sw + j * 3 * NC + lane;
-            const float dx = wi[0] - wj[0], dy = wi[NC] - wj[NC], dz = wi[2 * NC] - wj[2 * NC];
-            const float d2 = dx * dx + dy * dy + dz * dz;
-            if (d2 < R * R) {
-                const float pen = R - sqrtf(d2);
-                if (pen > best) { best = pen; bidx = p; }
+        int brank = 0x7fffffff, bij = -1;
+        const uint2 *blk = reinterpret_cast<const uint2 *>(s.iw + rp.o_blocks);
+        const float *rself = s.fw + rp.o_rself;
+        const unsigned short *rk = reinterpret_cast<const unsigned short *>(s.iw + rp.o_rank);
+        const int b0 = s.iw[rp.o_wblk + warp], b1 = s.iw[rp.o_wblk + warp + 1];
+        for (int bi = b0; bi < b1; ++bi) {
+            const uint2 B = blk[bi];
+            const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff,
+                      len = (B.x >> 20) & 0x1ff;
+            float wx[4], wy[4], wz[4], ri[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = u < na ? ia + u : ia;
+                const float *wi = s.sw + i * 3 * NC + lane;
+                wx[u] = wi[0]; wy[u] = wi[NC]; wz[u] = wi[2 * NC];
+                ri[u] = rself[i];
+            }
+            const float *wj = s.sw + jb * 3 * NC + lane;
+            for (int v = 0; v < len; ++v, wj += 3 * NC) {
+                const float jx = wj[0], jy = wj[NC], jz = wj[2 * NC];
+                const float rj = rself[jb + v];
+                float e2[4];
+                bool any = false;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {     // common path: d^2 - R^2 only
+                    const float R = ri[u] + rj;
+                    const float dx = wx[u] - jx, dy = wy[u] - jy, dz = wz[u] - jz;
+                    e2[u] = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -R * R)));
+                    any |= (u < na) && (e2[u] < 0.f);
+                }
+                if (any) {                        // rare path: a penetrating pair
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (!(u < na && e2[u] < 0.f)) continue;
+                        const float R = ri[u] + rj;
+                        const float dx = wx[u] - jx, dy = wy[u] - jy, dz = wz[u] - jz;
+                        const float pen = R - sqrtf(dx * dx + dy * dy + dz * dz);
+                        if (pen >= best && pen > 0.f) {
+                            const int rank = rk[B.y + u * len + v];
+                            if (pen > best || rank < brank) {
+                                best = pen; brank = rank; bij = (ia + u) | ((jb + v) << 9);
+                            }
+                        }
+                    }
+                }
             }
         }
         s.sbest[warp * NC + lane] = best;
-        s.sidx[warp * NC + lane] = bidx;
+        s.srank[warp * NC + lane] = brank;
+        s.sij[warp * NC + lane] = bij;
     }
 
-    // ---- a5/a6: world collision, discrete + swept + speed (Eq. world-collision-cost)
+    // ---- a5/a6: world collision, discrete + swept + speed (Eq. world-collision-cost).  Each thread
+    // carries two spheres (m, m + NW) of its slot through one scan of the cuboids.
     {
         float wsum = 0.f;
         const bool to = MODE == MODE_TO;
-        const bool sweepf = to && (kp.flags & F_SWEEP);
-        const bool speedf = to && (kp.flags & F_SPEED);
+        const bool sweepf = to && (cf.flags & F_SWEEP);
+        const bool speedf = to && (cf.flags & F_SPEED);
         const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
         const bool hasp = to && lane > 0 && lane < H;
         const bool hasn = to && lane + 1 < H;
-        for (int m = warp; m < rp.M; m += NW) {
-            float *g = s.sg + m * 3 * NC + lane;
-            const float r = sph[m].w;
-            float Gx = 0.f, Gy = 0.f, Gz = 0.f;
-            float Ew = 0.f;
-            if (r >= 0.f) {   // r < 0 disables the sphere (Alg. 10)
-                const float *w = s.sw + m * 3 * NC + lane;
-                const float cx = w[0], cy = w[NC], cz = w[2 * NC];
-                float px = cx, py = cy, pz = cz, nx = cx, ny = cy, nz = cz;
-                if (hasp) { px = w[-1]; py = w[NC - 1]; pz = w[2 * NC - 1]; }
-                if (hasn) { nx = w[1]; ny = w[NC + 1]; nz = w[2 * NC + 1]; }
-                float sp = 1.f;
-                if (speedf) {   // A13: central difference, missing neighbour -> w_h
-                    const float ddx = nx - px, ddy = ny - py, ddz = nz - pz;
-                    sp = sqrtf(ddx * ddx + ddy * ddy + ddz * ddz) / (2.f * kp.dt);
-                }
-                if (sp != 0.f) {
-                    const float rpr = r + kp.eta;   // Alg. 10 "sph.radius += eta"
-                    const float bx = px - cx, by = py - cy, bz = pz - cz;
-                    const float fx = nx - cx, fy = ny - cy, fz = nz - cz;
-                    const float LB = sqrtf(bx * bx + by * by + bz * bz);
-                    const float LF = sqrtf(fx * fx + fy * fy + fz * fz);
-                    const bool doB = sweepf && hasp && (LB - 2.f * rpr > 0.f);   // A6
-                    const bool doF = sweepf && hasn && (LF - 2.f * rpr > 0.f);
-                    const float E = sphere_world(s.boxes, K, cx, cy, cz, rpr, kp.eta, doB, bx, by, bz, LB, doF,
-                                                 fx, fy, fz, LF, kp.sweep_steps, Gx, Gy, Gz);
-                    const float sc = kp.beta_world * sp;
-                    Ew = sc * E;
-                    Gx *= sc; Gy *= sc; Gz *= sc;
+        for (int m0 = warp; m0 < rp.M; m0 += 2 * NW) {
+            const int m1 = m0 + NW;
+            const bool two = m1 < rp.M;
+            SphereWorld A, B;
+            const float spA = setup_sphere(A, s, m0, sph[m0].w, lane, hasp, hasn, sweepf, speedf, cf.eta, cf.inv_2dt);
+            float spB = 0.f;
+            if (two) spB = setup_sphere(B, s, m1, sph[m1].w, lane, hasp, hasn, sweepf, speedf, cf.eta, cf.inv_2dt);
+            else { B = A; B.thr2 = -1.f; }
+            if (__any_sync(FULL, A.thr2 > 0.f || B.thr2 > 0.f)) {
+                for (int k = 0; k < K; ++k) {
+                    const BoxView b = load_box(s.boxes, k);
+                    const float s2A = box_screen(A, b), s2B = box_screen(B, b);
+                    int todo = (s2A < A.thr2 ? 1 : 0) | (s2B < B.thr2 ? 2 : 0);
+                    while (todo) {                // rare path, one inlined copy for both spheres
+                        const bool useA = todo & 1;
+                        todo &= useA ? 2 : 0;
+                        SphereWorld W = useA ? A : B;
+                        box_slow(W, b, useA ? s2A : s2B, cf.eta, cf.inv_eta, cf.sweep_steps);
+                        if (useA) { A.E = W.E; A.Gx = W.Gx; A.Gy = W.Gy; A.Gz = W.Gz; }
+                        else { B.E = W.E; B.Gx = W.Gx; B.Gy = W.Gy; B.Gz = W.Gz; }
+                    }
                 }
             }
-            g[0] = Gx; g[NC] = Gy; g[2 * NC] = Gz;
-            wsum += Ew;
+            {
+                const float sc = cf.beta_world * spA;
+                float *g = s.sg + m0 * 3 * NC + lane;
+                g[0] = sc * A.Gx; g[NC] = sc * A.Gy; g[2 * NC] = sc * A.Gz;
+                wsum += sc * A.E;
+            }
+            if (two) {
+                const float sc = cf.beta_world * spB;
+                float *g = s.sg + m1 * 3 * NC + lane;
+                g[0] = sc * B.Gx; g[NC] = sc * B.Gy; g[2 * NC] = sc * B.Gz;
+                wsum += sc * B.E;
+            }
         }
         s.wpart[warp * NC + lane] = wsum;
     }
@@ -557,23 +666,23 @@ __device__ void eval_pass(const KParams &kp, const Smem &s, const float *thA, in
             if (MODE == MODE_TO) {
                 const float *x = s.xs + d * XS + c + 3;   // x_h with h = c + 1
                 const float xm2 = x[-2], xm1 = x[-1], x0 = x[0], xp1 = x[1], xp2 = x[2];
-                const float dt = kp.dt, dt2 = dt * dt, dt3 = dt2 * dt;
+                const float dt = cf.dt, dt2 = dt * dt, dt3 = dt2 * dt;
                 // O3 five-point stencil (§A.5, A15)
                 const float v = (-xp2 + 8.f * xp1 - 8.f * xm1 + xm2) / (12.f * dt);
                 const float a = (-xp2 + 16.f * xp1 - 30.f * x0 + 16.f * xm1 - xm2) / (12.f * dt2);
                 const float j = (xp2 - 2.f * xp1 + 2.f * xm1 - xm2) / (2.f * dt3);
                 const float vm = lim[2 * D + d], am = lim[3 * D + d], jm = lim[4 * D + d];
-                cb += kp.wb[0] * bound_cost(x0, lo, hi, kp.eta_bound, dd); gx = kp.wb[0] * dd;
-                cb += kp.wb[1] * bound_cost(v, -vm, vm, kp.eta_bound, dd); gv = kp.wb[1] * dd;
-                cb += kp.wb[2] * bound_cost(a, -am, am, kp.eta_bound, dd); ga = kp.wb[2] * dd;
-                cb += kp.wb[3] * bound_cost(j, -jm, jm, kp.eta_bound, dd); gj = kp.wb[3] * dd;
-                cs = kp.a8 * a * a;
-                ga += 2.f * kp.a8 * a;
-                if (kp.flags & F_JERK) { cs += kp.a9 * j * j; gj += 2.f * kp.a9 * j; }
+                cb += cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd); gx = cf.wb[0] * dd;
+                cb += cf.wb[1] * bound_cost(v, -vm, vm, cf.eta_bound, dd); gv = cf.wb[1] * dd;
+                cb += cf.wb[2] * bound_cost(a, -am, am, cf.eta_bound, dd); ga = cf.wb[2] * dd;
+                cb += cf.wb[3] * bound_cost(j, -jm, jm, cf.eta_bound, dd); gj = cf.wb[3] * dd;
+                cs = cf.a8 * a * a;
+                ga += 2.f * cf.a8 * a;
+                if (cf.flags & F_JERK) { cs += cf.a9 * j * j; gj += 2.f * cf.a9 * j; }
             } else {
                 const float x0 = s.q_cfg[d * NC + c];
-                cb = kp.wb[0] * bound_cost(x0, lo, hi, kp.eta_bound, dd);
-                gx = kp.wb[0] * dd;
+                cb = cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd);
+                gx = cf.wb[0] * dd;
             }
         }
         s.cbb[idx] = cb; s.csm[idx] = cs; s.gxd[idx] = gx;
@@ -586,22 +695,22 @@ __device__ void eval_pass(const KParams &kp, const Smem &s, const float *thA, in
         const bool on = (MODE == MODE_TO) ? (c == H - 1) : (c < n_act);
         float ft[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, C = 0.f;
         if (on) {
-            const float *T = s.lt + rp.ee * 12 * NC + c;
-            const float px = T[3 * NC], py = T[7 * NC], pz = T[11 * NC];
+            const float *E = ee_frame(s, D) + c;
+            const float px = E[9 * NC], py = E[10 * NC], pz = E[11 * NC];
             float q[4];
-            mat_to_quat(T[0], T[NC], T[2 * NC], T[4 * NC], T[5 * NC], T[6 * NC], T[8 * NC], T[9 * NC],
-                        T[10 * NC], q);
+            mat_to_quat(E[0], E[NC], E[2 * NC], E[3 * NC], E[4 * NC], E[5 * NC], E[6 * NC], E[7 * NC],
+                        E[8 * NC], q);
             const float *G = s.goal;   // [7][32]
             const float ex = G[0 * NC + c] - px, ey = G[1 * NC + c] - py, ez = G[2 * NC + c] - pz;
             const float n = sqrtf(ex * ex + ey * ey + ez * ez);
             const float gw = G[3 * NC + c], gxq = G[4 * NC + c], gyq = G[5 * NC + c], gzq = G[6 * NC + c];
             const float dq = gw * q[0] + gxq * q[1] + gyq * q[2] + gzq * q[3];
             const float er = 1.f - fabsf(dq);
-            C = kp.a0 * logcoshf(kp.a2 * n) + kp.a1 * logcoshf(kp.a3 * er);
-            const float f = (n > 1e-12f) ? tanhf(kp.a2 * n) / n : kp.a2;
-            const float kpo = -kp.a0 * kp.a2 * f;
+            C = cf.a0 * logcoshf(cf.a2 * n) + cf.a1 * logcoshf(cf.a3 * er);
+            const float f = (n > 1e-12f) ? tanhf(cf.a2 * n) / n : cf.a2;
+            const float kpo = -cf.a0 * cf.a2 * f;
             const float gpx = kpo * ex, gpy = kpo * ey, gpz = kpo * ez;
-            const float kq = -kp.a1 * kp.a3 * tanhf(kp.a3 * er) * (dq >= 0.f ? 1.f : -1.f);
+            const float kq = -cf.a1 * cf.a3 * tanhf(cf.a3 * er) * (dq >= 0.f ? 1.f : -1.f);
             const float gqw = kq * gw, gqx = kq * gxq, gqy = kq * gyq, gqz = kq * gzq;
             // torque of the quaternion gradient: tau = 1/2 (w g_v - g_w v + v x g_v)  (A27)
             const float tx = 0.5f * (q[0] * gqx - gqw * q[1] + (q[2] * gqz - q[3] * gqy));
@@ -618,26 +727,25 @@ __device__ void eval_pass(const KParams &kp, const Smem &s, const float *thA, in
     }
     __syncthreads();
 
-    // ---- a10 (per slot): merge self-collision, apply its gradient, per-slot costs
+    // ---- a10 (per slot): merge self-collision, apply its gradient, per-slot costs and the total
     if (warp == 0) {
         const int c = lane;
         float bp = 0.f;
-        int bi = -1;
+        int br = 0x7fffffff, bij = -1;
         for (int w = 0; w < NW; ++w) {
             const float p = s.sbest[w * NC + c];
-            const int i = s.sidx[w * NC + c];
-            if (i >= 0 && (p > bp || (p == bp && i < bi))) { bp = p; bi = i; }
+            const int r = s.srank[w * NC + c];
+            if (p > bp || (p == bp && p > 0.f && r < br)) { bp = p; br = r; bij = s.sij[w * NC + c]; }
         }
         float cself = 0.f;
-        if (bi >= 0 && bp > 0.f) {
-            const uint2 pr = reinterpret_cast<const uint2 *>(s.iw + rp.o_pairs)[bi];
-            const int i = pr.x & 0xffff, j = pr.x >> 16;
+        if (bij >= 0 && bp > 0.f) {
+            const int i = bij & 0x1ff, j = (bij >> 9) & 0x1ff;
             const float *wi = s.sw + i * 3 * NC + c, *wj = s.sw + j * 3 * NC + c;
             float ux = wi[0] - wj[0], uy = wi[NC] - wj[NC], uz = wi[2 * NC] - wj[2 * NC];
             const float nu = sqrtf(ux * ux + uy * uy + uz * uz);
             if (nu < 1e-12f) { ux = 1.f; uy = 0.f; uz = 0.f; }
             else { ux /= nu; uy /= nu; uz /= nu; }
-            const float b = kp.beta_self;
+            const float b = cf.beta_self;
             float *gi = s.sg + i * 3 * NC + c, *gj = s.sg + j * 3 * NC + c;
             gi[0] -= b * ux; gi[NC] -= b * uy; gi[2 * NC] -= b * uz;
             gj[0] += b * ux; gj[NC] += b * uy; gj[2 * NC] += b * uz;
@@ -648,34 +756,54 @@ __device__ void eval_pass(const KParams &kp, const Smem &s, const float *thA, in
         float cb = 0.f, cs = 0.f;
         for (int d = 0; d < D; ++d) { cb += s.cbb[d * NC + c]; cs += s.csm[d * NC + c]; }
         const bool valid = c < n_act;
-        const float cp = s.pose_c[c];
-        const float t0 = valid ? cp : 0.f, t1 = valid ? cb : 0.f, t2 = valid ? cs : 0.f,
+        const float t0 = valid ? s.pose_c[c] : 0.f, t1 = valid ? cb : 0.f, t2 = valid ? cs : 0.f,
                     t3 = valid ? cself : 0.f, t4 = valid ? cw : 0.f;
         s.cfg_terms[0 * NC + c] = t0; s.cfg_terms[1 * NC + c] = t1; s.cfg_terms[2 * NC + c] = t2;
         s.cfg_terms[3 * NC + c] = t3; s.cfg_terms[4 * NC + c] = t4;
-        s.cfg_cost[c] = (((t0 + t1) + t2) + t3) + t4;
+        const float cc = (((t0 + t1) + t2) + t3) + t4;
+        s.cfg_cost[c] = cc;
+        const float tot = warp_sum(cc);
+        if (c == 0) s.scal[0] = tot;
     }
     __syncthreads();
 
     // ---- a9: backward to joint space (Alg. 8 / Table 7 as subtree sums):
-    // per link: F_l = sum G_m, T_l = sum w_m x G_m over its spheres (+ the pose pseudo-sphere)
-    for (int idx = tid; idx < rp.L * NC; idx += NT) {
-        const int l = idx / NC, c = idx - l * NC;
-        float F0 = 0.f, F1 = 0.f, F2 = 0.f, T0 = 0.f, T1 = 0.f, T2 = 0.f;
-        const int b = s.iw[rp.o_sbeg + l], e = s.iw[rp.o_sbeg + l + 1];
-        for (int m = b; m < e; ++m) {
-            const float *g = s.sg + m * 3 * NC + c, *w = s.sw + m * 3 * NC + c;
-            const float gx = g[0], gy = g[NC], gz = g[2 * NC];
-            const float wx = w[0], wy = w[NC], wz = w[2 * NC];
-            F0 += gx; F1 += gy; F2 += gz;
-            T0 += wy * gz - wz * gy; T1 += wz * gx - wx * gz; T2 += wx * gy - wy * gx;
+    // per link: F_l = sum G_m, T_l = sum w_m x G_m over its spheres (+ the pose pseudo-sphere);
+    // computed into registers, then (after a barrier) written over the dead sphere positions.
+    {
+        float acc[4][6];   // L <= 32 links x 32 slots <= 4 items per thread
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int idx = tid + it * NT;
+            float F0 = 0.f, F1 = 0.f, F2 = 0.f, T0 = 0.f, T1 = 0.f, T2 = 0.f;
+            if (idx < rp.L * NC) {
+                const int l = idx / NC, c = idx - l * NC;
+                const int b = s.iw[rp.o_sbeg + l], e = s.iw[rp.o_sbeg + l + 1];
+                for (int m = b; m < e; ++m) {
+                    const float *g = s.sg + m * 3 * NC + c, *w = s.sw + m * 3 * NC + c;
+                    const float gx = g[0], gy = g[NC], gz = g[2 * NC];
+                    const float wx = w[0], wy = w[NC], wz = w[2 * NC];
+                    F0 += gx; F1 += gy; F2 += gz;
+                    T0 += wy * gz - wz * gy; T1 += wz * gx - wx * gz; T2 += wx * gy - wy * gx;
+                }
+                if (l == rp.ee) {
+                    F0 += s.pose_ft[0 * NC + c]; F1 += s.pose_ft[1 * NC + c]; F2 += s.pose_ft[2 * NC + c];
+                    T0 += s.pose_ft[3 * NC + c]; T1 += s.pose_ft[4 * NC + c]; T2 += s.pose_ft[5 * NC + c];
+                }
+            }
+            acc[it][0] = F0; acc[it][1] = F1; acc[it][2] = F2; acc[it][3] = T0; acc[it][4] = T1; acc[it][5] = T2;
         }
-        if (l == rp.ee) {
-            F0 += s.pose_ft[0 * NC + c]; F1 += s.pose_ft[1 * NC + c]; F2 += s.pose_ft[2 * NC + c];
-            T0 += s.pose_ft[3 * NC + c]; T1 += s.pose_ft[4 * NC + c]; T2 += s.pose_ft[5 * NC + c];
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int idx = tid + it * NT;
+            if (idx < rp.L * NC) {
+                const int l = idx / NC, c = idx - l * NC;
+                float *o = s.ls + l * 6 * NC + c;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) o[k * NC] = acc[it][k];
+            }
         }
-        float *o = s.ls + l * 6 * NC + c;
-        o[0] = F0; o[NC] = F1; o[2 * NC] = F2; o[3 * NC] = T0; o[4 * NC] = T1; o[5 * NC] = T2;
     }
     __syncthreads();
     // subtree accumulation, child -> parent in reverse topological order; warp k owns component k
@@ -688,19 +816,17 @@ __device__ void eval_pass(const KParams &kp, const Smem &s, const float *thA, in
     }
     __syncthreads();
     // joint gradient: revolute k . (T_l - o_l x F_l), prismatic k . F_l (Table 7), + bound_pos
-    float *gq = s.sbest;   // reuse [D][32] (self scratch is dead now)
     for (int idx = tid; idx < D * NC; idx += NT) {
         const int d = idx / NC, c = idx - d * NC;
         const int l = s.iw[rp.o_doflink + d];
         const int type = s.iw[rp.o_links + 16 * l + 13];
-        const int ax = type >= 4 ? type - 4 : type - 1;
-        const float *T = s.lt + l * 12 * NC + c;
-        const float kx = T[ax * NC], ky = T[(4 + ax) * NC], kz = T[(8 + ax) * NC];
+        const float *fr = s.frames + d * 6 * NC + c;
+        const float kx = fr[0], ky = fr[NC], kz = fr[2 * NC];
         const float *S6 = s.ls + l * 6 * NC + c;
         const float F0 = S6[0], F1 = S6[NC], F2 = S6[2 * NC];
         float g;
         if (type >= 4) {
-            const float ox = T[3 * NC], oy = T[7 * NC], oz = T[11 * NC];
+            const float ox = fr[3 * NC], oy = fr[4 * NC], oz = fr[5 * NC];
             const float t0 = S6[3 * NC] - (oy * F2 - oz * F1);
             const float t1 = S6[4 * NC] - (oz * F0 - ox * F2);
             const float t2 = S6[5 * NC] - (ox * F1 - oy * F0);
@@ -708,17 +834,17 @@ __device__ void eval_pass(const KParams &kp, const Smem &s, const float *thA, in
         } else {
             g = kx * F0 + ky * F1 + kz * F2;
         }
-        gq[idx] = (c < n_act) ? g + s.gxd[idx] : 0.f;
+        s.gq[idx] = (c < n_act) ? g + s.gxd[idx] : 0.f;
     }
     __syncthreads();
 
     // ---- transposed stencil + transposed state map (O2/O3 gradient routing) -> dC/dV
     if (MODE == MODE_TO) {
-        const float dt = kp.dt, dt2 = dt * dt, dt3 = dt2 * dt;
-        const float cv[5] = {1.f / (12.f * dt), -8.f / (12.f * dt), 0.f, 8.f / (12.f * dt), -1.f / (12.f * dt)};
-        const float ca[5] = {-1.f / (12.f * dt2), 16.f / (12.f * dt2), -30.f / (12.f * dt2), 16.f / (12.f * dt2),
-                             -1.f / (12.f * dt2)};
-        const float cj[5] = {-1.f / (2.f * dt3), 2.f / (2.f * dt3), 0.f, -2.f / (2.f * dt3), 1.f / (2.f * dt3)};
+        const float dt = cf.dt, dt2 = dt * dt, dt3 = dt2 * dt;
+        // O3 coefficients: v: (1, -8, 0, 8, -1)/(12 dt), a: (-1, 16, -30, 16, -1)/(12 dt^2),
+        // j: (-1, 2, 0, -2, 1)/(2 dt^3) for x_{h-2} .. x_{h+2}
+        const float iv = 1.f / (12.f * dt), ia = 1.f / (12.f * dt2), ij = 1.f / (2.f * dt3);
+        float gdp = 0.f;
         for (int idx = tid; idx < D * NC; idx += NT) {
             const int d = idx / NC, h = idx - d * NC;   // V_h <-> x_{h+1}
             if (h >= H) continue;
@@ -727,23 +853,37 @@ __device__ void eval_pass(const KParams &kp, const Smem &s, const float *thA, in
             if (hx >= 4 && hx <= H - 4) { xlo = hx; xhi = hx; }
             else if (hx == H) { xlo = H - 3; xhi = H + 2; }
             else { s.gV[h * D + d] = 0.f; continue; }
+            const float *gv = s.gva + d * NC - 1, *ga = gv + D * NC, *gj = ga + D * NC;   // [hp] for hp = 1..H
             float acc = 0.f;
             for (int xi = xlo; xi <= xhi; ++xi) {
-                float gx = (xi >= 1 && xi <= H) ? gq[d * NC + xi - 1] : 0.f;
-                const int h0 = xi - 2 > 1 ? xi - 2 : 1, h1 = xi + 2 < H ? xi + 2 : H;
-                for (int hp = h0; hp <= h1; ++hp) {
-                    const int o = xi - hp + 2;
-                    const int e = d * NC + hp - 1;
-                    gx += cv[o] * s.gva[e] + ca[o] * s.gva[D * NC + e] + cj[o] * s.gva[2 * D * NC + e];
-                }
+                float gx = (xi >= 1 && xi <= H) ? s.gq[d * NC + xi - 1] : 0.f;
+                // x_xi enters the stencil of hp = xi - o with the coefficient of offset o
+                if (xi + 2 <= H) { const int e = xi + 2; gx += iv * gv[e] - ia * ga[e] - ij * gj[e]; }             // o = -2
+                if (xi + 1 >= 1 && xi + 1 <= H) { const int e = xi + 1; gx += -8.f * iv * gv[e] + 16.f * ia * ga[e] + 2.f * ij * gj[e]; }  // o = -1
+                if (xi >= 1 && xi <= H) gx += -30.f * ia * ga[xi];                                             // o = 0
+                if (xi - 1 >= 1 && xi - 1 <= H) { const int e = xi - 1; gx += 8.f * iv * gv[e] + 16.f * ia * ga[e] - 2.f * ij * gj[e]; }   // o = 1
+                if (xi - 2 >= 1) { const int e = xi - 2; gx += -iv * gv[e] - ia * ga[e] + ij * gj[e]; }        // o = 2
                 acc += gx;
             }
             s.gV[h * D + d] = acc;
+            if (dvec) gdp += acc * dvec[h * D + d];
+        }
+        if (dvec) {
+            gdp = warp_sum(gdp);
+            if (lane == 0) s.red[2 * NW + warp] = gdp;   // third half of `red`: pass-private
         }
     } else {
-        for (int idx = tid; idx < D * NC; idx += NT) s.gV[idx] = gq[idx];
+        for (int idx = tid; idx < D * NC; idx += NT) s.gV[idx] = s.gq[idx];
     }
     __syncthreads();
+}
+
+// g . dvec of the last TO pass (fixed warp order).
+__device__ __forceinline__ float pass_gdot(const Smem &s) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) v += s.red[2 * NW + w];
+    return v;
 }
 
 }  // namespace crb

@@ -27,58 +27,48 @@ namespace {
 
 constexpr int SMEM_MAX = 232448;   // 227 KB opt-in per CTA
 
-__device__ __forceinline__ float cta_cost_total(const Smem &s, float *scal_out) {
-    // sum of the per-slot costs in a fixed (butterfly) order; every thread gets the value
-    float v = 0.f;
-    if ((threadIdx.x >> 5) == 0) {
-        v = warp_sum(s.cfg_cost[threadIdx.x & 31]);
-        if (threadIdx.x == 0) *scal_out = v;
-    }
-    __syncthreads();
-    v = *scal_out;
-    __syncthreads();
-    return v;
-}
-
-// Two-loop recursion (Alg. 6; A18/A19) over the ring `order` (oldest first), one
-// element per thread, every dot product a deterministic block reduction.
+// Two-loop recursion (Alg. 6; A18/A19) over the ring `order` (oldest first); each
+// thread owns elements t and t + NT (N <= 2 NT); every dot product a deterministic block sum.
 __device__ void two_loop_block(int N, int Np, int count, const int *order, const float *Sb, const float *Yb,
                                const float *rho, const float *syv, const float *yyv, const float *g, float *d,
-                               float *red) {
-    const int t = threadIdx.x;
+                               float *red, int &ph) {
+    const int t0 = threadIdx.x, t1 = threadIdx.x + NT;
     float al[16];
-    float q = t < N ? g[t] : 0.f;
+    float q0 = t0 < N ? g[t0] : 0.f, q1 = t1 < N ? g[t1] : 0.f;
 #pragma unroll 1
     for (int i = count - 1; i >= 0; --i) {
-        const int sl = order[i];
-        const float sv = t < N ? Sb[sl * Np + t] : 0.f;
-        const float a = rho[sl] * block_sum(sv * q, red);
+        const float *S = Sb + order[i] * Np, *Y = Yb + order[i] * Np;
+        const float part = (t0 < N ? S[t0] * q0 : 0.f) + (t1 < N ? S[t1] * q1 : 0.f);
+        const float a = rho[order[i]] * block_sum(part, red, ph);
         al[i] = a;
-        if (t < N) q -= a * Yb[sl * Np + t];
+        if (t0 < N) q0 -= a * Y[t0];
+        if (t1 < N) q1 -= a * Y[t1];
     }
     float gamma = 1.f;
     if (count > 0) {
         const int sl = order[count - 1];
         gamma = syv[sl] / yyv[sl];
     }
-    float r = gamma * q;
+    float r0 = gamma * q0, r1 = gamma * q1;
 #pragma unroll 1
     for (int i = 0; i < count; ++i) {
-        const int sl = order[i];
-        const float yv = t < N ? Yb[sl * Np + t] : 0.f;
-        const float b = rho[sl] * block_sum(yv * r, red);
-        if (t < N) r += (al[i] - b) * Sb[sl * Np + t];
+        const float *S = Sb + order[i] * Np, *Y = Yb + order[i] * Np;
+        const float part = (t0 < N ? Y[t0] * r0 : 0.f) + (t1 < N ? Y[t1] * r1 : 0.f);
+        const float b = rho[order[i]] * block_sum(part, red, ph);
+        if (t0 < N) r0 += (al[i] - b) * S[t0];
+        if (t1 < N) r1 += (al[i] - b) * S[t1];
     }
-    if (t < N) d[t] = -r;
+    if (t0 < N) d[t0] = -r0;
+    if (t1 < N) d[t1] = -r1;
 }
 
 // ------------------------------------------------------------------------------------------
 // persistent TO solver: one CTA per (problem, seed)
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 1) solve_to_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int unit = blockIdx.x;
-    const int p = unit / kp.S, sidx = unit - p * kp.S;
+    const int p = unit / kp.S;
     const int env = kp.env ? kp.env[p] : 0;
     const int K = stage_tables(kp, smem, env);
     const Smem s = make_smem(kp, smem);
@@ -89,96 +79,131 @@ __global__ void __launch_bounds__(NT, 1) solve_to_kernel(const __grid_constant__
           *thA = best + Np, *cg = thA + Np, *Sb = cg + A * Np, *Yb = Sb + (m + 1) * Np,
           *rho = Yb + (m + 1) * Np, *syv = rho + 20, *yyv = syv + 20;
     int *order = reinterpret_cast<int *>(yyv + 20);
-    float *scal = yyv + 40;           // [0..7] c_a, [8..15] gd_a, [16] cost, [17] i*
+    float *scal = yyv + 40;           // [0..7] c_a, [8..15] gd_a, [17] i*
     int *ring = reinterpret_cast<int *>(scal + 24);   // [0] count, [1] free slot
     const float *lim = s.fw + kp.rp.o_lim;
+    int ph = 0;
 
     if (t < D) s.st[t] = kp.start[p * D + t];
     if (t < 7 * NC) s.goal[t] = kp.goal[p * 7 + t / NC];
     const float *seed = kp.q_in + (size_t)unit * N;
-    if (t < N) { th[t] = seed[t]; thA[t] = seed[t]; }
+    float lo_e[2], hi_e[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int i = t + e * NT;
+        lo_e[e] = i < N ? lim[i % D] : 0.f;
+        hi_e[e] = i < N ? lim[D + i % D] : 0.f;
+        if (i < N) { th[i] = seed[i]; thA[i] = seed[i]; }
+    }
     if (t == 0) { ring[0] = 0; ring[1] = 0; }
-    const float lo_t = t < N ? lim[t % D] : 0.f, hi_t = t < N ? lim[D + t % D] : 0.f;
     __syncthreads();
 
     // evaluate at Theta_0 (O8 initialise)
-    eval_pass<MODE_TO>(kp, s, thA, K, H);
-    float c = cta_cost_total(s, scal + 16);
-    if (t < N) { g[t] = s.gV[t]; best[t] = th[t]; }
+    eval_pass<MODE_TO>(kp, smem, thA, K, H, nullptr);
+    float c = s.scal[0];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int i = t + e * NT;
+        if (i < N) { g[i] = s.gV[i]; best[i] = th[i]; }
+    }
     float cbest = c;
-    __syncthreads();
 
     for (int it = 0; it < kp.iters; ++it) {
         // ---- a13: L-BFGS buffers (Alg. 6 lines 1-5) -- push (s, y, rho) unless s^T y <= 1e-12 (A20)
         if (it > 0) {
             const int fs = ring[1];
-            float sv = 0.f, yv = 0.f;
-            if (t < N) {
-                sv = th[t] - thp[t];
-                yv = g[t] - gp[t];
-                Sb[fs * Np + t] = sv;
-                Yb[fs * Np + t] = yv;
+            float sy_p = 0.f, yy_p = 0.f;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) {
+                    const float sv = th[i] - thp[i], yv = g[i] - gp[i];
+                    Sb[fs * Np + i] = sv; Yb[fs * Np + i] = yv;
+                    sy_p += sv * yv; yy_p += yv * yv;
+                }
             }
-            const float sy = block_sum(sv * yv, s.red);
-            const float yy = block_sum(yv * yv, s.red);
-            if (sy > 1e-12f) {
-                if (t == 0) {
-                    rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
-                    int cnt = ring[0];
-                    if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
-                    else {
-                        const int ev = order[0];
-                        for (int i = 0; i < m - 1; ++i) order[i] = order[i + 1];
-                        order[m - 1] = fs;
-                        ring[1] = ev;
-                    }
+            const float sy = block_sum(sy_p, s.red, ph);
+            const float yy = block_sum(yy_p, s.red, ph);
+            if (sy > 1e-12f && t == 0) {
+                rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
+                const int cnt = ring[0];
+                if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
+                else {
+                    const int ev = order[0];
+                    for (int i = 0; i < m - 1; ++i) order[i] = order[i + 1];
+                    order[m - 1] = fs;
+                    ring[1] = ev;
                 }
             }
             __syncthreads();
         }
-        if (t < N) { thp[t] = th[t]; gp[t] = g[t]; }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            if (i < N) { thp[i] = th[i]; gp[i] = g[i]; }
+        }
         // ---- two-loop recursion -> d = -H g
-        two_loop_block(N, Np, ring[0], order, Sb, Yb, rho, syv, yyv, g, dd, s.red);
-        const float dt_ = t < N ? dd[t] : 0.f;
-        const float g0d = block_sum((t < N ? g[t] : 0.f) * dt_, s.red);
+        two_loop_block(N, Np, ring[0], order, Sb, Yb, rho, syv, yyv, g, dd, s.red, ph);
+        float d_e[2];
+        float gd_p = 0.f;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            d_e[e] = i < N ? dd[i] : 0.f;
+            if (i < N) gd_p += g[i] * d_e[e];
+        }
+        const float g0d = block_sum(gd_p, s.red, ph);   // also publishes dd to every thread
         // ---- a1 + a2..a10: the A line-search candidates, each one evaluation pass
         for (int a = 0; a < A; ++a) {
-            if (t < N) thA[t] = candidate(th[t], kp.alpha[a], dt_, lo_t, hi_t);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) thA[i] = candidate(th[i], kp.alpha[a], d_e[e], lo_e[e], hi_e[e]);
+            }
             __syncthreads();
-            eval_pass<MODE_TO>(kp, s, thA, K, H);
-            const float ca = cta_cost_total(s, scal + a);
-            (void)ca;
-            if (t < N) cg[a * Np + t] = s.gV[t];
-            const float gda = block_sum(t < N ? s.gV[t] * dt_ : 0.f, s.red);
-            if (t == 0) scal[8 + a] = gda;
-        }
-        // ---- a11: selection (Alg. 1 lines 4-9), fp32 mirror, then take candidate i*
-        if (t == 0) {
-            const int i = ls_select(A, kp.alpha, c, g0d, scal, scal + 8, kp.c1, kp.c2, kp.ls_mode);
-            reinterpret_cast<int *>(scal)[17] = i;
+            eval_pass<MODE_TO>(kp, smem, thA, K, H, dd);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) cg[a * Np + i] = s.gV[i];
+            }
+            if (t == 0) { scal[a] = s.scal[0]; scal[8 + a] = pass_gdot(s); }
         }
         __syncthreads();
-        const int istar = reinterpret_cast<const int *>(scal)[17];
-        if (t < N) {
-            th[t] = candidate(th[t], kp.alpha[istar], dt_, lo_t, hi_t);
-            g[t] = cg[istar * Np + t];
+        // ---- a11: selection (Alg. 1 lines 4-9), fp32 mirror, then take candidate i*
+        const int istar = ls_select(A, kp.alpha, c, g0d, scal, scal + 8, kp.c1, kp.c2, kp.ls_mode);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            if (i < N) {
+                th[i] = candidate(th[i], kp.alpha[istar], d_e[e], lo_e[e], hi_e[e]);
+                g[i] = cg[istar * Np + i];
+            }
         }
         c = scal[istar];
         // ---- a12: best update, strict < (A23)
         if (c < cbest) {
             cbest = c;
-            if (t < N) best[t] = th[t];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) best[i] = th[i];
+            }
         }
-        __syncthreads();
     }
+    __syncthreads();
     if (t == 0) kp.seed_best_cost[unit] = cbest;
-    if (t < N) kp.seed_best_traj[(size_t)unit * N + t] = best[t];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int i = t + e * NT;
+        if (i < N) kp.seed_best_traj[(size_t)unit * N + i] = best[i];
+    }
 }
 
 // ------------------------------------------------------------------------------------------
 // persistent IK solver: one CTA per (problem, group of 32 seeds); lane = seed
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 1) solve_ik_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int G = (kp.S + NC - 1) / NC;
     const int p = blockIdx.x / G, grp = blockIdx.x - p * G;
@@ -206,7 +231,7 @@ __global__ void __launch_bounds__(NT, 1) solve_ik_kernel(const __grid_constant__
             s.q_cfg[d * NC + lane] = v;
         }
     __syncthreads();
-    eval_pass<MODE_IK>(kp, s, nullptr, K, n_act);
+    eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
     float c = 0.f, cbest = 0.f;
     int cnt = 0, fs = 0;
     if (warp == 0) {
@@ -268,7 +293,7 @@ __global__ void __launch_bounds__(NT, 1) solve_ik_kernel(const __grid_constant__
                 for (int d = 0; d < D; ++d)
                     s.q_cfg[d * NC + lane] = candidate(th[d * NC + lane], kp.alpha[a], dd[d * NC + lane], lim[d], lim[D + d]);
             __syncthreads();
-            eval_pass<MODE_IK>(kp, s, nullptr, K, n_act);
+            eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
             if (warp == 0) {
                 cc[a * NC + lane] = s.cfg_cost[lane];
                 float gd = 0.f;
@@ -307,7 +332,7 @@ __global__ void __launch_bounds__(NT, 1) solve_ik_kernel(const __grid_constant__
 // ------------------------------------------------------------------------------------------
 // one-shot evaluation, FK, selection
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 1) eval_to_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b = blockIdx.x;
     const int env = kp.env ? kp.env[b] : 0;
@@ -315,27 +340,25 @@ __global__ void __launch_bounds__(NT, 1) eval_to_kernel(const __grid_constant__ 
     const Smem s = make_smem(kp, smem);
     const int D = kp.rp.D, H = kp.H, N = H * D, t = threadIdx.x;
     float *thA = smem + kp.lay.solver;
-    float *scal = thA + ((N + 3) & ~3);
     if (t < D) s.st[t] = kp.start[(size_t)b * D + t];
     if (t < 7 * NC) s.goal[t] = kp.goal[(size_t)b * 7 + t / NC];
-    if (t < N) thA[t] = kp.q_in[(size_t)b * N + t];
+    for (int i = t; i < N; i += NT) thA[i] = kp.q_in[(size_t)b * N + i];
     __syncthreads();
-    eval_pass<MODE_TO>(kp, s, thA, K, H);
+    eval_pass<MODE_TO>(kp, smem, thA, K, H, nullptr);
     if (t < 32) {
-        const float c = warp_sum(s.cfg_cost[t]);
         float tr[5];
         for (int k = 0; k < 5; ++k) tr[k] = warp_sum(s.cfg_terms[k * NC + t]);
         if (t == 0) {
-            kp.cost_out[b] = c;
+            kp.cost_out[b] = s.scal[0];
             if (kp.terms_out)
                 for (int k = 0; k < 5; ++k) kp.terms_out[(size_t)b * 5 + k] = tr[k];
         }
     }
-    (void)scal;
-    if (t < N && kp.grad_out) kp.grad_out[(size_t)b * N + t] = s.gV[t];
+    if (kp.grad_out)
+        for (int i = t; i < N; i += NT) kp.grad_out[(size_t)b * N + i] = s.gV[i];
 }
 
-__global__ void __launch_bounds__(NT, 1) eval_ik_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b0 = blockIdx.x * NC;
     const int n_act = min(NC, kp.B - b0);
@@ -350,7 +373,7 @@ __global__ void __launch_bounds__(NT, 1) eval_ik_kernel(const __grid_constant__ 
         for (int k = 0; k < 7; ++k) s.goal[k * NC + lane] = act ? kp.goal[(size_t)(b0 + lane) * 7 + k] : (k == 3 ? 1.f : 0.f);
     }
     __syncthreads();
-    eval_pass<MODE_IK>(kp, s, nullptr, K, n_act);
+    eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
     if (warp == 0 && lane < n_act) {
         const int b = b0 + lane;
         const bool ok = !kp.env || kp.env[b] == env0;
@@ -362,7 +385,7 @@ __global__ void __launch_bounds__(NT, 1) eval_ik_kernel(const __grid_constant__ 
     }
 }
 
-__global__ void __launch_bounds__(NT, 1) fk_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b0 = blockIdx.x * NC;
     const int n_act = min(NC, kp.B - b0);
@@ -373,7 +396,7 @@ __global__ void __launch_bounds__(NT, 1) fk_kernel(const __grid_constant__ KPara
     if (warp == 0)
         for (int d = 0; d < D; ++d) s.q_cfg[d * NC + lane] = lane < n_act ? kp.q_in[(size_t)(b0 + lane) * D + d] : 0.f;
     __syncthreads();
-    fk_phase(kp, s);
+    fk_phase(kp.rp, s);
     const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
     if (kp.spheres_out)
         for (int m = warp; m < rp.M; m += NW) {
@@ -442,30 +465,32 @@ __global__ void argmin_keys_kernel(int P, int S, const float *cost, long long ba
     if (out_idx) out_idx[p] = bi;
 }
 
-__global__ void __launch_bounds__(NT, 1) lbfgs_direction_kernel(int n, int count, const float *S, const float *Y,
+__global__ void __launch_bounds__(NT, 2) lbfgs_direction_kernel(int n, int count, const float *S, const float *Y,
                                                                 const float *g, float *d) {
     extern __shared__ __align__(16) float smem[];
     const int b = blockIdx.x, t = threadIdx.x, Np = (n + 3) & ~3;
     float *Sb = smem, *Yb = Sb + count * Np, *gg = Yb + count * Np, *dd = gg + Np, *rho = dd + Np,
           *syv = rho + 16, *yyv = syv + 16, *red = yyv + 16;
-    int *order = reinterpret_cast<int *>(red + 32);
+    int *order = reinterpret_cast<int *>(red + 3 * NW);
+    int ph = 0;
     for (int i = 0; i < count; ++i)
-        if (t < n) {
-            Sb[i * Np + t] = S[((size_t)b * count + i) * n + t];
-            Yb[i * Np + t] = Y[((size_t)b * count + i) * n + t];
+        for (int e = t; e < n; e += NT) {
+            Sb[i * Np + e] = S[((size_t)b * count + i) * n + e];
+            Yb[i * Np + e] = Y[((size_t)b * count + i) * n + e];
         }
-    if (t < n) gg[t] = g[(size_t)b * n + t];
+    for (int e = t; e < n; e += NT) gg[e] = g[(size_t)b * n + e];
     if (t < count) order[t] = t;
     __syncthreads();
     for (int i = 0; i < count; ++i) {   // same reductions as the solver's push
-        const float sv = t < n ? Sb[i * Np + t] : 0.f, yv = t < n ? Yb[i * Np + t] : 0.f;
-        const float sy = block_sum(sv * yv, red);
-        const float yy = block_sum(yv * yv, red);
+        float sy_p = 0.f, yy_p = 0.f;
+        for (int e = t; e < n; e += NT) { sy_p += Sb[i * Np + e] * Yb[i * Np + e]; yy_p += Yb[i * Np + e] * Yb[i * Np + e]; }
+        const float sy = block_sum(sy_p, red, ph);
+        const float yy = block_sum(yy_p, red, ph);
         if (t == 0) { rho[i] = 1.f / sy; syv[i] = sy; yyv[i] = yy; }
     }
     __syncthreads();
-    two_loop_block(n, Np, count, order, Sb, Yb, rho, syv, yyv, gg, dd, red);
-    if (t < n) d[(size_t)b * n + t] = dd[t];
+    two_loop_block(n, Np, count, order, Sb, Yb, rho, syv, yyv, gg, dd, red, ph);
+    for (int e = t; e < n; e += NT) d[(size_t)b * n + e] = dd[e];
 }
 
 }  // namespace
@@ -548,16 +573,17 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.XS = mode == MODE_TO ? H + 5 : 0;
     L.q_cfg = take(D * NC);
     L.xs = take(D * L.XS);
-    L.lt = take(rp.L * 12 * NC);
-    L.sw = take(rp.M * 3 * NC);
-    L.sg = take(rp.M * 3 * NC);
-    L.ls = take(rp.L * 6 * NC);
+    L.ltg = take(std::max(rp.L * 12, rp.M * 3) * NC);     // link transforms, then sphere gradients
+    L.frames = take((D * 6 + 12) * NC);
+    L.swl = take(std::max(rp.M * 3, rp.L * 6) * NC);      // sphere centres, then link sums
     L.sbest = take(NW * NC);
-    L.sidx = take(NW * NC);
+    L.srank = take(NW * NC);
+    L.sij = take(NW * NC);
     L.wpart = take(NW * NC);
     L.cbb = take(D * NC);
     L.csm = take(D * NC);
     L.gxd = take(D * NC);
+    L.gq = take(D * NC);
     L.gva = take(mode == MODE_TO ? 3 * D * NC : 4);
     L.pose_ft = take(6 * NC);
     L.pose_c = take(NC);
@@ -565,8 +591,9 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.cfg_cost = take(NC);
     L.cfg_terms = take(5 * NC);
     L.gV = take(std::max(H * D, D * NC));
-    L.red = take(NW * 2);
+    L.red = take(3 * NW);
     L.st = take(16);
+    L.scal = take(8);
     L.solver = w;
     const int N = H * D, Np = r4(N), DC = D * NC;
     if (mode == MODE_TO) {
@@ -589,10 +616,13 @@ KParams base_params(const crb_ctx *ctx) {
     kp.kmax = ctx->kmax;
     kp.n_env = ctx->n_env;
     const crb_cost_params &c = ctx->cp;
-    kp.a0 = c.a0; kp.a1 = c.a1; kp.a2 = c.a2; kp.a3 = c.a3; kp.a8 = c.a8; kp.a9 = c.a9;
-    for (int i = 0; i < 4; ++i) kp.wb[i] = c.w_bound[i];
-    kp.beta_self = c.beta_self; kp.beta_world = c.beta_world; kp.eta = c.eta; kp.eta_bound = c.eta_bound;
-    kp.dt = c.dt; kp.sweep_steps = c.sweep_steps; kp.flags = c.flags;
+    CostP &k = kp.cp;
+    k.a0 = c.a0; k.a1 = c.a1; k.a2 = c.a2; k.a3 = c.a3; k.a8 = c.a8; k.a9 = c.a9;
+    for (int i = 0; i < 4; ++i) k.wb[i] = c.w_bound[i];
+    k.beta_self = c.beta_self; k.beta_world = c.beta_world; k.eta = c.eta; k.eta_bound = c.eta_bound;
+    k.dt = c.dt; k.sweep_steps = c.sweep_steps; k.flags = c.flags;
+    k.inv_eta = 1.0f / c.eta;
+    k.inv_2dt = 1.0f / (2.0f * c.dt);
     return kp;
 }
 
@@ -653,7 +683,7 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         (r->n_spheres > 0 && (!r->spheres || !r->sphere_link)) || (r->n_pairs > 0 && !r->pairs))
         return fail(ctx, CRB_E_ARG, "null pointer in robot description");
     const int L = r->n_links, D = r->n_dof, M = r->n_spheres, P = r->n_pairs;
-    if (L < 1 || L > 32 || D < 1 || D > 16 || M < 0 || M > 512 || P < 0 || P > 16384)
+    if (L < 1 || L > 32 || D < 1 || D > 16 || M < 0 || M > 512 || P < 0 || P > 16383)
         return fail(ctx, CRB_E_LIMIT, "robot size outside limits (L<=32, D<=16, M<=512, pairs<=16384)");
     if (r->ee_link < 0 || r->ee_link >= L) return fail(ctx, CRB_E_ROBOT, "ee_link out of range");
     std::vector<int> doflink(D, -1);
@@ -701,20 +731,81 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
     rp.o_sph = w; w += 4 * M;
     rp.o_sphlink = w; w += r4(M);
     rp.o_sbeg = w; w += r4(L + 1);
-    std::vector<uint32_t> pk;
+    // self pairs (Eq. self-collision): drop r+o <= 0 (Alg. 9 "continue", P:2778 -- exact),
+    // remap to packed sphere indices a < b, then cover S with rectangular blocks
+    // {ia..ia+na-1} x {jb..jb+len-1} (na <= 4): consecutive first spheres with identical partner runs
+    // share a block.  Blocks are balanced over the NW warps (LPT); the rank of every pair in S is
+    // kept so arg-max ties resolve to the first maximal pair in S order (A28).
+    std::vector<float> rself(M);
+    for (int k = 0; k < M; ++k) {
+        const int m = ord[k];
+        rself[k] = (float)((double)r->spheres[4 * m + 3] + (r->self_offset ? r->self_offset[m] : 0.0));
+    }
+    std::vector<int> rank_of((size_t)M * M, -1);
+    int npairs = 0;
     for (int p = 0; p < P; ++p) {
         const int i = r->pairs[2 * p], j = r->pairs[2 * p + 1];
         const double ri = (double)r->spheres[4 * i + 3] + (r->self_offset ? r->self_offset[i] : 0.0);
         const double rj = (double)r->spheres[4 * j + 3] + (r->self_offset ? r->self_offset[j] : 0.0);
-        if (ri <= 0.0 || rj <= 0.0) continue;   // Alg. 9 "continue": exact to drop
-        const float R = (float)(ri + rj);
-        uint32_t rb;
-        memcpy(&rb, &R, 4);
-        pk.push_back((uint32_t)inv[i] | ((uint32_t)inv[j] << 16));
-        pk.push_back(rb);
+        if (ri <= 0.0 || rj <= 0.0) continue;
+        const int a = std::min(inv[i], inv[j]), b = std::max(inv[i], inv[j]);
+        if (rank_of[(size_t)a * M + b] < 0) ++npairs;
+        rank_of[(size_t)a * M + b] = rank_of[(size_t)a * M + b] < 0 ? p : std::min(rank_of[(size_t)a * M + b], p);
     }
-    rp.P = (int)pk.size() / 2;
-    rp.o_pairs = w; w += r4(2 * rp.P);
+    auto runs_of = [&](int a) {
+        std::vector<std::pair<int, int>> rr;
+        for (int b = a + 1; b < M;) {
+            if (rank_of[(size_t)a * M + b] < 0) { ++b; continue; }
+            int e = b;
+            while (e < M && rank_of[(size_t)a * M + e] >= 0) ++e;
+            rr.push_back({b, e});
+            b = e;
+        }
+        return rr;
+    };
+    struct Blk { int ia, na, jb, len; };
+    std::vector<Blk> blks;
+    for (int a = 0; a < M;) {
+        const auto ra = runs_of(a);
+        int na = 1;
+        while (na < 4 && a + na < M && runs_of(a + na) == ra) ++na;
+        for (const auto &rn : ra)
+            for (int jb = rn.first; jb < rn.second; jb += 511)
+                blks.push_back({a, na, jb, std::min(511, rn.second - jb)});
+        a += na;
+    }
+    // LPT balance of the blocks over the NW warps (cost ~ len * (2 + 9 na) instructions)
+    std::vector<int> bord(blks.size());
+    for (size_t i = 0; i < blks.size(); ++i) bord[i] = (int)i;
+    std::stable_sort(bord.begin(), bord.end(), [&](int x, int y) {
+        return blks[x].len * (2 + 9 * blks[x].na) > blks[y].len * (2 + 9 * blks[y].na);
+    });
+    std::vector<long> load(NW, 0);
+    std::vector<std::vector<int>> per_warp(NW);
+    for (int bi : bord) {
+        const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[w] += (long)blks[bi].len * (2 + 9 * blks[bi].na);
+        per_warp[w].push_back(bi);
+    }
+    std::vector<uint32_t> bk, wblk(NW + 1, 0);
+    std::vector<uint16_t> ranks;
+    for (int w = 0; w < NW; ++w) {
+        std::sort(per_warp[w].begin(), per_warp[w].end());
+        wblk[w] = (uint32_t)(bk.size() / 2);
+        for (int bi : per_warp[w]) {
+            const Blk &b = blks[bi];
+            bk.push_back((uint32_t)b.ia | ((uint32_t)(b.na - 1) << 9) | ((uint32_t)b.jb << 11) | ((uint32_t)b.len << 20));
+            bk.push_back((uint32_t)ranks.size());
+            for (int u = 0; u < b.na; ++u)
+                for (int v = 0; v < b.len; ++v) ranks.push_back((uint16_t)rank_of[(size_t)(b.ia + u) * M + b.jb + v]);
+        }
+    }
+    wblk[NW] = (uint32_t)(bk.size() / 2);
+    rp.P = npairs;
+    rp.o_rself = w; w += r4(M);
+    rp.o_blocks = w; w += r4((int)bk.size());
+    rp.o_wblk = w; w += r4(NW + 1);
+    rp.o_rank = w; w += r4(((int)ranks.size() + 1) / 2);
     rp.o_lim = w; w += r4(5 * D);
     rp.o_doflink = w; w += r4(D);
     rp.o_perm = w; w += r4(M);
@@ -737,7 +828,10 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         while (k < M && r->sphere_link[ord[k]] < l) ++k;
         blob[rp.o_sbeg + l] = (uint32_t)k;
     }
-    for (size_t i = 0; i < pk.size(); ++i) blob[rp.o_pairs + i] = pk[i];
+    for (int k = 0; k < M; ++k) fput(rp.o_rself + k, rself[k]);
+    for (size_t i = 0; i < bk.size(); ++i) blob[rp.o_blocks + i] = bk[i];
+    for (int i = 0; i <= NW; ++i) blob[rp.o_wblk + i] = wblk[i];
+    if (!ranks.empty()) memcpy(&blob[rp.o_rank], ranks.data(), ranks.size() * 2);
     for (int d = 0; d < D; ++d) {
         fput(rp.o_lim + d, r->pos_lo[d]); fput(rp.o_lim + D + d, r->pos_hi[d]);
         fput(rp.o_lim + 2 * D + d, r->vel_max[d]); fput(rp.o_lim + 3 * D + d, r->acc_max[d]);
@@ -829,7 +923,7 @@ crb_status crb_fk(crb_ctx *ctx, const float *q, int B, float *spheres_out, float
     if (!q || B < 0) return fail(ctx, CRB_E_ARG, "bad fk arguments");
     KParams kp = base_params(ctx);
     kp.kmax = 0;
-    kp.B = B; kp.H = 1; kp.mode = MODE_IK; kp.q_in = q; kp.spheres_out = spheres_out; kp.ee_out = ee_out;
+    kp.B = B; kp.H = 1; kp.cp.H = 1; kp.mode = MODE_IK; kp.q_in = q; kp.spheres_out = spheres_out; kp.ee_out = ee_out;
     const size_t bytes = make_layout(ctx->rp, 0, MODE_IK, 1, 1, 1, false, kp.lay);
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large");
     return launch(ctx, fk_kernel, (B + NC - 1) / NC, bytes, (cudaStream_t)stream, kp, "fk_kernel");
@@ -845,7 +939,7 @@ crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, co
     if (mode == MODE_TO && (H < 8 || H > 32 || H * ctx->rp.D > 512 || !start))
         return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 32, H*D <= 512 and start");
     KParams kp = base_params(ctx);
-    kp.B = B; kp.H = H; kp.mode = mode; kp.q_in = q; kp.env = env; kp.start = start; kp.goal = goal;
+    kp.B = B; kp.H = H; kp.cp.H = H; kp.mode = mode; kp.q_in = q; kp.env = env; kp.start = start; kp.goal = goal;
     kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs;
     const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
@@ -872,7 +966,7 @@ crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int
     if (!sbc) { if ((st = grow(ctx, &ctx->ws_cost, &ctx->cap_cost, (size_t)P * S)) != CRB_OK) return st; sbc = ctx->ws_cost; }
     if (!sbt) { if ((st = grow(ctx, &ctx->ws_traj, &ctx->cap_traj, (size_t)P * S * N)) != CRB_OK) return st; sbt = ctx->ws_traj; }
     KParams kp = base_params(ctx);
-    kp.P = P; kp.S = S; kp.H = H; kp.mode = mode; kp.q_in = seeds; kp.env = env; kp.start = start; kp.goal = goal;
+    kp.P = P; kp.S = S; kp.H = H; kp.cp.H = H; kp.mode = mode; kp.q_in = seeds; kp.env = env; kp.start = start; kp.goal = goal;
     kp.iters = sp->iters; kp.m = sp->history; kp.A = sp->n_alpha; kp.ls_mode = sp->ls_mode;
     for (int i = 0; i < 8; ++i) kp.alpha[i] = sp->alpha[i];
     kp.c1 = sp->c1; kp.c2 = sp->c2; kp.seed_base = sp->global_seed_base;
@@ -943,10 +1037,10 @@ crb_status crb_argmin_keys(int P, int S, const float *cost, int64_t seed_base, i
 
 crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const float *Y, const float *g, float *d,
                                void *stream) {
-    if (B < 0 || n < 1 || n > NT || count < 0 || count > 16 || !g || !d || (count > 0 && (!S || !Y))) return CRB_E_ARG;
+    if (B < 0 || n < 1 || n > 2 * NT || count < 0 || count > 16 || !g || !d || (count > 0 && (!S || !Y))) return CRB_E_ARG;
     if (B == 0) return CRB_OK;
     const int Np = (n + 3) & ~3;
-    const size_t bytes = (size_t)(2 * count * Np + 2 * Np + 48 + 32 + 16) * 4;
+    const size_t bytes = (size_t)(2 * count * Np + 2 * Np + 48 + 3 * NW + 16) * 4;
     if (cudaFuncSetAttribute(lbfgs_direction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
         return CRB_E_CUDA;
     lbfgs_direction_kernel<<<B, NT, bytes, (cudaStream_t)stream>>>(n, count, S, Y, g, d);
