@@ -219,7 +219,7 @@ __device__ __forceinline__ float box_sdf_grad(const BoxView &b, float px, float 
     if (qm > 0.f) {
         const float mx = fmaxf(qx, 0.f), my = fmaxf(qy, 0.f), mz = fmaxf(qz, 0.f);
         sd = sqrtf(mx * mx + my * my + mz * mz);
-        const float inv = __frcp_rn(sd);
+        const float inv = 1.f / sd;
         glx = (lx >= 0.f ? mx : -mx) * inv;
         gly = (ly >= 0.f ? my : -my) * inv;
         glz = (lz >= 0.f ? mz : -mz) * inv;
@@ -273,8 +273,10 @@ struct Smem {
     const int *iw;          // robot blob as ints
     const float *fw;        // robot blob as floats
     const float *boxes;
-    float *q_cfg, *xs, *lt, *sg, *frames, *sw, *ls, *sbest, *wpart, *cbb, *csm, *gxd, *gq, *gva, *pose_ft,
+    float *q_cfg, *xs, *lt, *frames, *ls, *sbest, *wpart, *cbb, *csm, *gxd, *gq, *gva, *pose_ft,
         *pose_c, *goal, *cfg_cost, *cfg_terms, *gV, *red, *st, *scal;
+    float4 *sw;             // [M][32] sphere centre (x, y, z) and hb = -(|w|^2 - r_self^2) / 2
+    float4 *sg;             // [M][32] dE/dw (x, y, z) and the world energy E (w)
     int *srank, *sij;
 };
 
@@ -285,9 +287,11 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     s.fw = smem + L.robot;
     s.boxes = smem + L.boxes;
     s.q_cfg = smem + L.q_cfg; s.xs = smem + L.xs;
-    s.lt = smem + L.ltg; s.sg = smem + L.ltg;          // sg aliases lt (lt dead after sphere placement)
+    s.lt = smem + L.ltg;                               // sg aliases lt (lt dead after sphere placement)
+    s.sg = reinterpret_cast<float4 *>(smem + L.ltg);
     s.frames = smem + L.frames;
-    s.sw = smem + L.swl; s.ls = smem + L.swl;          // ls aliases sw (written after a barrier)
+    s.sw = reinterpret_cast<float4 *>(smem + L.swl);   // ls aliases sw (written after a barrier)
+    s.ls = smem + L.swl;
     s.sbest = smem + L.sbest;
     s.srank = reinterpret_cast<int *>(smem + L.srank);
     s.sij = reinterpret_cast<int *>(smem + L.sij);
@@ -380,8 +384,8 @@ __device__ __forceinline__ void fk_phase(const RobotPack rp, const Smem &s) {
         const float wx = T[0] * c.x + T[NC] * c.y + T[2 * NC] * c.z + T[3 * NC];
         const float wy = T[4 * NC] * c.x + T[5 * NC] * c.y + T[6 * NC] * c.z + T[7 * NC];
         const float wz = T[8 * NC] * c.x + T[9 * NC] * c.y + T[10 * NC] * c.z + T[11 * NC];
-        float *dst = s.sw + m * 3 * NC + lane;
-        dst[0] = wx; dst[NC] = wy; dst[2 * NC] = wz;
+        const float rs = s.fw[rp.o_rself + m];
+        s.sw[m * NC + lane] = make_float4(wx, wy, wz, -0.5f * (wx * wx + wy * wy + wz * wz - rs * rs));
     }
     __syncthreads();
 }
@@ -408,22 +412,39 @@ __device__ __forceinline__ void mat_to_quat(float r00, float r01, float r02, flo
     q[0] = w; q[1] = x; q[2] = y; q[3] = z;
 }
 
-// State of one sphere at one slot for the world term (Alg. 10 discrete + §3.4 / Algs. 11-12
-// swept under readings A6-A12; O5 in DESIGN.md).  Only what the per-cuboid screen needs lives in
-// registers; the sweep geometry is rebuilt from shared memory on the (rare) slow path.
-struct SphereWorld {
-    float cx, cy, cz, rp, rp2, thr2;         // centre, r' = r + eta, r'^2, screen threshold (-1 = off)
-    float E, Gx, Gy, Gz;                     // sum of phi and dE/dc
-    const float *p;                          // &sw[m][0][lane]
-    int dirs;                                // bit 0: backward sweep, bit 1: forward sweep
-};
+// World term of one sphere at one slot (Alg. 10 discrete + §3.4 / Algs. 11-12 swept under
+// readings A6-A12; O5 in DESIGN.md).  The per-cuboid screen needs only the centre and a threshold
+// in registers; the rare slow path rebuilds the rest from shared memory and accumulates E and
+// dE/dw into sg[m][lane].
+
+// Sweep directions of sphere m at this slot (A6: a direction is swept iff its neighbour exists
+// and gap = L - 2r' > 0); also the larger half-segment.  One function for the screen set-up and
+// the slow path, so both take bitwise the same decisions.
+__device__ __forceinline__ int sweep_dirs(const float4 *p, float cx, float cy, float cz, float rp, bool hasp,
+                                          bool hasn, bool sweepf, float &maxb) {
+    int dirs = 0;
+    maxb = 0.f;
+    if (sweepf && hasp) {
+        const float4 q = p[-1];
+        const float vx = q.x - cx, vy = q.y - cy, vz = q.z - cz;
+        const float L = sqrtf(vx * vx + vy * vy + vz * vz);
+        if (L - 2.f * rp > 0.f) { dirs |= 1; maxb = 0.5f * L; }
+    }
+    if (sweepf && hasn) {
+        const float4 q = p[1];
+        const float vx = q.x - cx, vy = q.y - cy, vz = q.z - cz;
+        const float L = sqrtf(vx * vx + vy * vy + vz * vz);
+        if (L - 2.f * rp > 0.f) { dirs |= 2; maxb = fmaxf(maxb, 0.5f * L); }
+    }
+    return dirs;
+}
 
 // Cheap screening test of one box: returns s2 = sd^2 outside (0 inside), no square root.  The
 // box matters iff s2 < thr2: a discrete hit (sd < r') or a possible sweep sample (sd < the larger
 // half-segment).
-__device__ __forceinline__ float box_screen(const SphereWorld &w, const BoxView &b) {
+__device__ __forceinline__ float box_screen(float cx, float cy, float cz, const BoxView &b) {
     float lx, ly, lz;
-    box_local(b, w.cx, w.cy, w.cz, lx, ly, lz);
+    box_local(b, cx, cy, cz, lx, ly, lz);
     const float mx = fmaxf(fabsf(lx) - b.h.x, 0.f), my = fmaxf(fabsf(ly) - b.h.y, 0.f),
                 mz = fmaxf(fabsf(lz) - b.h.z, 0.f);
     return fmaf(mx, mx, fmaf(my, my, mz * mz));
@@ -432,80 +453,53 @@ __device__ __forceinline__ float box_screen(const SphereWorld &w, const BoxView 
 // Rare path: the hit's activation and gradient, then the backward / forward marches (A6-A12):
 // L = |n - c|, bound = L/2, j = J0 (r' on a hit, else sd), at most n_s samples p = c + (j/L)(n - c);
 // a hit adds phi and (1 - kappa) phi' (-grad sd) and jumps r', a miss jumps sd.
-__device__ __forceinline__ void box_slow(SphereWorld &w, const BoxView &b, float s2, float eta, float inv_eta,
-                                         int steps) {
-    const bool hit = s2 < w.rp2;                       // inside (s2 = 0) or within r'
+__device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const float *boxes, int k, float cx, float cy,
+                                      float cz, float s2, float rp, int dirs, float eta, float inv_eta, int steps) {
+    const BoxView b = load_box(boxes, k);              // reloaded here: keeps the screen loop spill-free
+    float E = 0.f, Gx = 0.f, Gy = 0.f, Gz = 0.f;
+    const bool hit = s2 < rp * rp;                     // inside (s2 = 0) or within r'
     float sd0;
     if (hit) {
         float gx, gy, gz;
-        sd0 = box_sdf_grad(b, w.cx, w.cy, w.cz, gx, gy, gz);
+        sd0 = box_sdf_grad(b, cx, cy, cz, gx, gy, gz);
         float dphi;
-        w.E += activation(w.rp - sd0, eta, inv_eta, dphi);
-        w.Gx -= dphi * gx; w.Gy -= dphi * gy; w.Gz -= dphi * gz;
+        E += activation(rp - sd0, eta, inv_eta, dphi);
+        Gx -= dphi * gx; Gy -= dphi * gy; Gz -= dphi * gz;
     } else {
         sd0 = sqrtf(s2);
     }
-    if (!w.dirs) return;
-    const float J0 = (w.rp - sd0 > 0.f) ? w.rp : sd0;
+    if (dirs) {
+        const float J0 = (rp - sd0 > 0.f) ? rp : sd0;
 #pragma unroll 1
-    for (int dir = 0; dir < 2; ++dir) {
-        if (!(w.dirs & (1 << dir))) continue;
-        const int o = dir == 0 ? -1 : 1;               // neighbouring slot (timestep)
-        const float vx = w.p[o] - w.cx, vy = w.p[NC + o] - w.cy, vz = w.p[2 * NC + o] - w.cz;
-        const float L = sqrtf(vx * vx + vy * vy + vz * vz);
-        const float iL = 1.f / L, bound = 0.5f * L;
-        float j = J0;
-        for (int st = 0; st < steps; ++st) {
-            if (j >= bound) break;
-            const float kap = j * iL;
-            const float px = fmaf(kap, vx, w.cx), py = fmaf(kap, vy, w.cy), pz = fmaf(kap, vz, w.cz);
-            float gx, gy, gz;
-            const float sd = box_sdf_grad(b, px, py, pz, gx, gy, gz);
-            const float dp = w.rp - sd;
-            if (dp > 0.f) {
-                float dphi;
-                w.E += activation(dp, eta, inv_eta, dphi);
-                const float f = (1.f - kap) * dphi;
-                w.Gx -= f * gx; w.Gy -= f * gy; w.Gz -= f * gz;
-                j += w.rp;
-            } else {
-                j += sd;
+        for (int dir = 0; dir < 2; ++dir) {
+            if (!(dirs & (1 << dir))) continue;
+            const float4 q = p[dir == 0 ? -1 : 1];      // neighbouring slot (timestep)
+            const float vx = q.x - cx, vy = q.y - cy, vz = q.z - cz;
+            const float L = sqrtf(vx * vx + vy * vy + vz * vz);
+            const float iL = 1.f / L, bound = 0.5f * L;
+            float j = J0;
+            for (int st = 0; st < steps; ++st) {
+                if (j >= bound) break;
+                const float kap = j * iL;
+                const float px = fmaf(kap, vx, cx), py = fmaf(kap, vy, cy), pz = fmaf(kap, vz, cz);
+                float gx, gy, gz;
+                const float sd = box_sdf_grad(b, px, py, pz, gx, gy, gz);
+                const float dp = rp - sd;
+                if (dp > 0.f) {
+                    float dphi;
+                    E += activation(dp, eta, inv_eta, dphi);
+                    const float f = (1.f - kap) * dphi;
+                    Gx -= f * gx; Gy -= f * gy; Gz -= f * gz;
+                    j += rp;
+                } else {
+                    j += sd;
+                }
             }
         }
     }
-}
-
-// Set up sphere m at this lane's slot: neighbours, speed metric (A13), sweep flags (A6: a
-// direction is swept iff its neighbour exists and gap = L - 2r' > 0).  Returns the speed factor.
-__device__ __forceinline__ float setup_sphere(SphereWorld &w, const Smem &s, int m, float r, int lane, bool hasp,
-                                              bool hasn, bool sweepf, bool speedf, float eta, float inv_2dt) {
-    const float *p = s.sw + m * 3 * NC + lane;
-    w.p = p;
-    w.cx = p[0]; w.cy = p[NC]; w.cz = p[2 * NC];
-    float px = w.cx, py = w.cy, pz = w.cz, nx = w.cx, ny = w.cy, nz = w.cz;
-    if (hasp) { px = p[-1]; py = p[NC - 1]; pz = p[2 * NC - 1]; }
-    if (hasn) { nx = p[1]; ny = p[NC + 1]; nz = p[2 * NC + 1]; }
-    float sp = 1.f;
-    if (speedf) {
-        const float dx = nx - px, dy = ny - py, dz = nz - pz;
-        sp = sqrtf(dx * dx + dy * dy + dz * dz) * inv_2dt;
-    }
-    w.rp = r + eta;                     // Alg. 10 "sph.radius += eta"
-    w.rp2 = w.rp * w.rp;
-    const float bx = px - w.cx, by = py - w.cy, bz = pz - w.cz;
-    const float fx = nx - w.cx, fy = ny - w.cy, fz = nz - w.cz;
-    const float LB = sqrtf(bx * bx + by * by + bz * bz), LF = sqrtf(fx * fx + fy * fy + fz * fz);
-    const bool doB = sweepf && hasp && (LB - 2.f * w.rp > 0.f);
-    const bool doF = sweepf && hasn && (LF - 2.f * w.rp > 0.f);
-    w.dirs = (doB ? 1 : 0) | (doF ? 2 : 0);
-    float maxb = 0.f;
-    if (doB) maxb = 0.5f * LB;
-    if (doF) maxb = fmaxf(maxb, 0.5f * LF);
-    // r < 0 disables the sphere; sp = 0 => C_w = 0 exactly
-    const bool on = (r >= 0.f) && (sp != 0.f);
-    w.thr2 = on ? fmaxf(w.rp2, maxb * maxb) : -1.f;
-    w.E = 0.f; w.Gx = 0.f; w.Gy = 0.f; w.Gz = 0.f;
-    return sp;
+    float4 a = *acc;
+    a.x += Gx; a.y += Gy; a.z += Gz; a.w += E;
+    *acc = a;
 }
 
 // One evaluation pass over the 32 slots.  Inputs already in shared memory:
@@ -514,12 +508,14 @@ __device__ __forceinline__ float setup_sphere(SphereWorld &w, const Smem &s, int
 //   dvec (TO, optional): a direction in smem; the pass then also returns g.dvec in s.scal[1].
 // Outputs: s.cfg_cost[32], s.cfg_terms[5][32], s.scal[0] = sum of the slot costs;
 //   TO: s.gV[H][D] = dC/dV; IK: s.gV[D][32].  Ends with a barrier.
+// Called from exactly one site per kernel (the solvers loop over passes), so it is inlined with
+// the kernel parameters left in the constant bank.
 template <int MODE>
-__device__ __noinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
-                                       const float *dvec) {
-    const Smem s = make_smem(kp, smem);   // one out-of-line copy per mode keeps the hot code in I-cache
-    const RobotPack rp = kp.rp;           // by value: registers, not generic loads of the parameter block
-    const CostP cf = kp.cp;
+__device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
+                                          const float *dvec) {
+    const Smem s = make_smem(kp, smem);
+    const RobotPack &rp = kp.rp;
+    const CostP &cf = kp.cp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = rp.D, H = cf.H, XS = kp.lay.XS;
     const float *lim = s.fw + rp.o_lim;
@@ -552,7 +548,10 @@ __device__ __noinline__ void eval_pass(const KParams &kp, float *smem, const flo
     // ---- a4: self-collision (Eq. self-collision, Alg. 9).  S is stored as rectangular blocks of
     // pairs {ia..ia+na-1} x {jb..jb+len-1} (spheres of one link share their partner ranges); each
     // warp walks its blocks holding the na <= 4 first spheres in registers and streaming the
-    // partners, lane = slot.  Ties go to the lowest rank in S (first maximal pair, A28).
+    // partners, lane = slot.  Screen: d^2 - R^2 = -2 (w_i.w_j + r_i r_j + hb_i + hb_j) with
+    // hb = -(|w|^2 - r^2)/2 precomputed per sphere (5 FMA per pair); it is conservative (slack
+    // 1e-5 m^2 >> fp32 rounding) and every flagged pair is re-tested exactly.  Ties go to the lowest
+    // rank in S (first maximal pair, A28).
     {
         float best = 0.f;
         int brank = 0x7fffffff, bij = -1;
@@ -564,34 +563,35 @@ __device__ __noinline__ void eval_pass(const KParams &kp, float *smem, const flo
             const uint2 B = blk[bi];
             const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff,
                       len = (B.x >> 20) & 0x1ff;
-            float wx[4], wy[4], wz[4], ri[4];
+            float4 wi[4];
+            float ri[4], ha[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int i = u < na ? ia + u : ia;
-                const float *wi = s.sw + i * 3 * NC + lane;
-                wx[u] = wi[0]; wy[u] = wi[NC]; wz[u] = wi[2 * NC];
+                wi[u] = s.sw[i * NC + lane];
                 ri[u] = rself[i];
+                ha[u] = u < na ? wi[u].w : -1e30f;
             }
-            const float *wj = s.sw + jb * 3 * NC + lane;
-            for (int v = 0; v < len; ++v, wj += 3 * NC) {
-                const float jx = wj[0], jy = wj[NC], jz = wj[2 * NC];
+            const float4 *wjp = s.sw + jb * NC + lane;
+            for (int v = 0; v < len; ++v) {
+                const float4 wj = wjp[v * NC];
                 const float rj = rself[jb + v];
-                float e2[4];
+                float g[4];
                 bool any = false;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {     // common path: d^2 - R^2 only
-                    const float R = ri[u] + rj;
-                    const float dx = wx[u] - jx, dy = wy[u] - jy, dz = wz[u] - jz;
-                    e2[u] = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -R * R)));
-                    any |= (u < na) && (e2[u] < 0.f);
+                for (int u = 0; u < 4; ++u) {     // common path: the screen only
+                    g[u] = fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, ha[u] + wj.w))));
+                    any |= g[u] > -1e-5f;
                 }
-                if (any) {                        // rare path: a penetrating pair
+                if (any) {                        // rare path: exact test of the flagged pairs
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        if (!(u < na && e2[u] < 0.f)) continue;
+                        if (!(g[u] > -1e-5f)) continue;
                         const float R = ri[u] + rj;
-                        const float dx = wx[u] - jx, dy = wy[u] - jy, dz = wz[u] - jz;
-                        const float pen = R - sqrtf(dx * dx + dy * dy + dz * dz);
+                        const float dx = wi[u].x - wj.x, dy = wi[u].y - wj.y, dz = wi[u].z - wj.z;
+                        const float d2 = dx * dx + dy * dy + dz * dz;
+                        if (!(d2 < R * R)) continue;
+                        const float pen = R - sqrtf(d2);
                         if (pen >= best && pen > 0.f) {
                             const int rank = rk[B.y + u * len + v];
                             if (pen > best || rank < brank) {
@@ -608,7 +608,7 @@ __device__ __noinline__ void eval_pass(const KParams &kp, float *smem, const flo
     }
 
     // ---- a5/a6: world collision, discrete + swept + speed (Eq. world-collision-cost).  Each thread
-    // carries two spheres (m, m + NW) of its slot through one scan of the cuboids.
+    // carries four spheres (m0 + u NW, u < 4) of its slot through one scan of the cuboids.
     {
         float wsum = 0.f;
         const bool to = MODE == MODE_TO;
@@ -617,40 +617,63 @@ __device__ __noinline__ void eval_pass(const KParams &kp, float *smem, const flo
         const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
         const bool hasp = to && lane > 0 && lane < H;
         const bool hasn = to && lane + 1 < H;
-        for (int m0 = warp; m0 < rp.M; m0 += 2 * NW) {
-            const int m1 = m0 + NW;
-            const bool two = m1 < rp.M;
-            SphereWorld A, B;
-            const float spA = setup_sphere(A, s, m0, sph[m0].w, lane, hasp, hasn, sweepf, speedf, cf.eta, cf.inv_2dt);
-            float spB = 0.f;
-            if (two) spB = setup_sphere(B, s, m1, sph[m1].w, lane, hasp, hasn, sweepf, speedf, cf.eta, cf.inv_2dt);
-            else { B = A; B.thr2 = -1.f; }
-            if (__any_sync(FULL, A.thr2 > 0.f || B.thr2 > 0.f)) {
+        for (int m0 = warp; m0 < rp.M; m0 += 4 * NW) {
+            float cx[4], cy[4], cz[4], th2[4], sp[4];
+            int dirs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int m = m0 + u * NW;
+                cx[u] = 0.f; cy[u] = 0.f; cz[u] = 0.f; th2[u] = -1.f; sp[u] = 0.f; dirs[u] = 0;
+                if (m < rp.M) {
+                    const float4 *p = s.sw + m * NC + lane;
+                    const float4 c = p[0];
+                    cx[u] = c.x; cy[u] = c.y; cz[u] = c.z;
+                    s.sg[m * NC + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    float spd = 1.f;
+                    if (speedf) {   // A13: central difference, missing neighbour -> w_h
+                        const float4 a = hasp ? p[-1] : c, z = hasn ? p[1] : c;
+                        const float dx = z.x - a.x, dy = z.y - a.y, dz = z.z - a.z;
+                        spd = sqrtf(dx * dx + dy * dy + dz * dz) * cf.inv_2dt;
+                    }
+                    sp[u] = spd;
+                    const float r = sph[m].w;
+                    const float rpr = r + cf.eta;   // Alg. 10 "sph.radius += eta"
+                    float maxb;
+                    dirs[u] = sweep_dirs(p, c.x, c.y, c.z, rpr, hasp, hasn, sweepf, maxb);
+                    // r < 0 disables the sphere; sp = 0 => C_w = 0 exactly
+                    if (r >= 0.f && spd != 0.f) th2[u] = fmaxf(rpr * rpr, maxb * maxb);
+                }
+            }
+            if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
                 for (int k = 0; k < K; ++k) {
                     const BoxView b = load_box(s.boxes, k);
-                    const float s2A = box_screen(A, b), s2B = box_screen(B, b);
-                    int todo = (s2A < A.thr2 ? 1 : 0) | (s2B < B.thr2 ? 2 : 0);
-                    while (todo) {                // rare path, one inlined copy for both spheres
-                        const bool useA = todo & 1;
-                        todo &= useA ? 2 : 0;
-                        SphereWorld W = useA ? A : B;
-                        box_slow(W, b, useA ? s2A : s2B, cf.eta, cf.inv_eta, cf.sweep_steps);
-                        if (useA) { A.E = W.E; A.Gx = W.Gx; A.Gy = W.Gy; A.Gz = W.Gz; }
-                        else { B.E = W.E; B.Gx = W.Gx; B.Gy = W.Gy; B.Gz = W.Gz; }
+                    float s2[4];
+                    bool any = false;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        s2[u] = box_screen(cx[u], cy[u], cz[u], b);
+                        any |= s2[u] < th2[u];
+                    }
+                    if (any) {                    // rare path, one out-of-line copy for all spheres
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (!(s2[u] < th2[u])) continue;
+                            const int m = m0 + u * NW;
+                            box_slow(s.sg + m * NC + lane, s.sw + m * NC + lane, s.boxes, k, cx[u], cy[u], cz[u],
+                                     s2[u], sph[m].w + cf.eta, dirs[u], cf.eta, cf.inv_eta, cf.sweep_steps);
+                        }
                     }
                 }
             }
-            {
-                const float sc = cf.beta_world * spA;
-                float *g = s.sg + m0 * 3 * NC + lane;
-                g[0] = sc * A.Gx; g[NC] = sc * A.Gy; g[2 * NC] = sc * A.Gz;
-                wsum += sc * A.E;
-            }
-            if (two) {
-                const float sc = cf.beta_world * spB;
-                float *g = s.sg + m1 * 3 * NC + lane;
-                g[0] = sc * B.Gx; g[NC] = sc * B.Gy; g[2 * NC] = sc * B.Gz;
-                wsum += sc * B.E;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int m = m0 + u * NW;
+                if (m < rp.M) {
+                    const float sc = cf.beta_world * sp[u];
+                    float4 g = s.sg[m * NC + lane];
+                    wsum += sc * g.w;
+                    s.sg[m * NC + lane] = make_float4(sc * g.x, sc * g.y, sc * g.z, 0.f);
+                }
             }
         }
         s.wpart[warp * NC + lane] = wsum;
@@ -740,15 +763,15 @@ __device__ __noinline__ void eval_pass(const KParams &kp, float *smem, const flo
         float cself = 0.f;
         if (bij >= 0 && bp > 0.f) {
             const int i = bij & 0x1ff, j = (bij >> 9) & 0x1ff;
-            const float *wi = s.sw + i * 3 * NC + c, *wj = s.sw + j * 3 * NC + c;
-            float ux = wi[0] - wj[0], uy = wi[NC] - wj[NC], uz = wi[2 * NC] - wj[2 * NC];
+            const float4 wi = s.sw[i * NC + c], wj = s.sw[j * NC + c];
+            float ux = wi.x - wj.x, uy = wi.y - wj.y, uz = wi.z - wj.z;
             const float nu = sqrtf(ux * ux + uy * uy + uz * uz);
             if (nu < 1e-12f) { ux = 1.f; uy = 0.f; uz = 0.f; }
             else { ux /= nu; uy /= nu; uz /= nu; }
             const float b = cf.beta_self;
-            float *gi = s.sg + i * 3 * NC + c, *gj = s.sg + j * 3 * NC + c;
-            gi[0] -= b * ux; gi[NC] -= b * uy; gi[2 * NC] -= b * uz;
-            gj[0] += b * ux; gj[NC] += b * uy; gj[2 * NC] += b * uz;
+            float4 &gi = s.sg[i * NC + c], &gj = s.sg[j * NC + c];
+            gi.x -= b * ux; gi.y -= b * uy; gi.z -= b * uz;
+            gj.x += b * ux; gj.y += b * uy; gj.z += b * uz;
             cself = b * bp;
         }
         float cw = 0.f;
@@ -780,9 +803,9 @@ __device__ __noinline__ void eval_pass(const KParams &kp, float *smem, const flo
                 const int l = idx / NC, c = idx - l * NC;
                 const int b = s.iw[rp.o_sbeg + l], e = s.iw[rp.o_sbeg + l + 1];
                 for (int m = b; m < e; ++m) {
-                    const float *g = s.sg + m * 3 * NC + c, *w = s.sw + m * 3 * NC + c;
-                    const float gx = g[0], gy = g[NC], gz = g[2 * NC];
-                    const float wx = w[0], wy = w[NC], wz = w[2 * NC];
+                    const float4 g = s.sg[m * NC + c], w = s.sw[m * NC + c];
+                    const float gx = g.x, gy = g.y, gz = g.z;
+                    const float wx = w.x, wy = w.y, wz = w.z;
                     F0 += gx; F1 += gy; F2 += gz;
                     T0 += wy * gz - wz * gy; T1 += wz * gx - wx * gz; T2 += wx * gy - wy * gx;
                 }

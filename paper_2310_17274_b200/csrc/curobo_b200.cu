@@ -98,96 +98,107 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
     if (t == 0) { ring[0] = 0; ring[1] = 0; }
     __syncthreads();
 
-    // evaluate at Theta_0 (O8 initialise)
-    eval_pass<MODE_TO>(kp, smem, thA, K, H, nullptr);
-    float c = s.scal[0];
+    // One loop over evaluation passes with a single eval_pass call site: pass 0 evaluates Theta_0
+    // (O8 initialise); then every iteration is an L-BFGS step followed by A candidate passes.
+    float c = 0.f, cbest = 0.f, g0d = 0.f;
+    float d_e[2] = {0.f, 0.f};
+    const int npass = 1 + kp.iters * A;
+    for (int pass = 0; pass < npass; ++pass) {
+        const int a = pass == 0 ? -1 : (pass - 1) % A;
+        if (a == 0) {
+            const int it = (pass - 1) / A;
+            // ---- a13: L-BFGS buffers (Alg. 6 lines 1-5): push (s, y, rho) unless s^T y <= 1e-12 (A20)
+            if (it > 0) {
+                const int fs = ring[1];
+                float sy_p = 0.f, yy_p = 0.f;
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const int i = t + e * NT;
-        if (i < N) { g[i] = s.gV[i]; best[i] = th[i]; }
-    }
-    float cbest = c;
-
-    for (int it = 0; it < kp.iters; ++it) {
-        // ---- a13: L-BFGS buffers (Alg. 6 lines 1-5) -- push (s, y, rho) unless s^T y <= 1e-12 (A20)
-        if (it > 0) {
-            const int fs = ring[1];
-            float sy_p = 0.f, yy_p = 0.f;
+                for (int e = 0; e < 2; ++e) {
+                    const int i = t + e * NT;
+                    if (i < N) {
+                        const float sv = th[i] - thp[i], yv = g[i] - gp[i];
+                        Sb[fs * Np + i] = sv; Yb[fs * Np + i] = yv;
+                        sy_p += sv * yv; yy_p += yv * yv;
+                    }
+                }
+                const float sy = block_sum(sy_p, s.red, ph);
+                const float yy = block_sum(yy_p, s.red, ph);
+                if (sy > 1e-12f && t == 0) {
+                    rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
+                    const int cnt = ring[0];
+                    if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
+                    else {
+                        const int ev = order[0];
+                        for (int i = 0; i < m - 1; ++i) order[i] = order[i + 1];
+                        order[m - 1] = fs;
+                        ring[1] = ev;
+                    }
+                }
+                __syncthreads();
+            }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int i = t + e * NT;
-                if (i < N) {
-                    const float sv = th[i] - thp[i], yv = g[i] - gp[i];
-                    Sb[fs * Np + i] = sv; Yb[fs * Np + i] = yv;
-                    sy_p += sv * yv; yy_p += yv * yv;
-                }
+                if (i < N) { thp[i] = th[i]; gp[i] = g[i]; }
             }
-            const float sy = block_sum(sy_p, s.red, ph);
-            const float yy = block_sum(yy_p, s.red, ph);
-            if (sy > 1e-12f && t == 0) {
-                rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
-                const int cnt = ring[0];
-                if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
-                else {
-                    const int ev = order[0];
-                    for (int i = 0; i < m - 1; ++i) order[i] = order[i + 1];
-                    order[m - 1] = fs;
-                    ring[1] = ev;
-                }
+            // ---- two-loop recursion -> d = -H g
+            two_loop_block(N, Np, ring[0], order, Sb, Yb, rho, syv, yyv, g, dd, s.red, ph);
+            float gd_p = 0.f;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                d_e[e] = i < N ? dd[i] : 0.f;
+                if (i < N) gd_p += g[i] * d_e[e];
             }
-            __syncthreads();
+            g0d = block_sum(gd_p, s.red, ph);   // also publishes dd to every thread
         }
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int i = t + e * NT;
-            if (i < N) { thp[i] = th[i]; gp[i] = g[i]; }
-        }
-        // ---- two-loop recursion -> d = -H g
-        two_loop_block(N, Np, ring[0], order, Sb, Yb, rho, syv, yyv, g, dd, s.red, ph);
-        float d_e[2];
-        float gd_p = 0.f;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int i = t + e * NT;
-            d_e[e] = i < N ? dd[i] : 0.f;
-            if (i < N) gd_p += g[i] * d_e[e];
-        }
-        const float g0d = block_sum(gd_p, s.red, ph);   // also publishes dd to every thread
-        // ---- a1 + a2..a10: the A line-search candidates, each one evaluation pass
-        for (int a = 0; a < A; ++a) {
+        // ---- a1: candidate a = clip(theta + alpha_a d) (pass 0: theta_0 is already in thA)
+        if (a >= 0) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int i = t + e * NT;
                 if (i < N) thA[i] = candidate(th[i], kp.alpha[a], d_e[e], lo_e[e], hi_e[e]);
             }
             __syncthreads();
-            eval_pass<MODE_TO>(kp, smem, thA, K, H, dd);
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int i = t + e * NT;
-                if (i < N) cg[a * Np + i] = s.gV[i];
-            }
-            if (t == 0) { scal[a] = s.scal[0]; scal[8 + a] = pass_gdot(s); }
         }
-        __syncthreads();
-        // ---- a11: selection (Alg. 1 lines 4-9), fp32 mirror, then take candidate i*
-        const int istar = ls_select(A, kp.alpha, c, g0d, scal, scal + 8, kp.c1, kp.c2, kp.ls_mode);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int i = t + e * NT;
-            if (i < N) {
-                th[i] = candidate(th[i], kp.alpha[istar], d_e[e], lo_e[e], hi_e[e]);
-                g[i] = cg[istar * Np + i];
-            }
-        }
-        c = scal[istar];
-        // ---- a12: best update, strict < (A23)
-        if (c < cbest) {
+        // ---- a2..a10: one evaluation pass
+        eval_pass<MODE_TO>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr);
+        if (a < 0) {
+            c = s.scal[0];
             cbest = c;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int i = t + e * NT;
-                if (i < N) best[i] = th[i];
+                if (i < N) { g[i] = s.gV[i]; best[i] = th[i]; }
+            }
+            continue;
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            if (i < N) cg[a * Np + i] = s.gV[i];
+        }
+        if (t == 0) { scal[a] = s.scal[0]; scal[8 + a] = pass_gdot(s); }
+        if (a == A - 1) {
+            __syncthreads();
+            // ---- a11: selection (Alg. 1 lines 4-9), fp32 mirror, then take candidate i*
+            const int istar = ls_select(A, kp.alpha, c, g0d, scal, scal + 8, kp.c1, kp.c2, kp.ls_mode);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) {
+                    th[i] = candidate(th[i], kp.alpha[istar], d_e[e], lo_e[e], hi_e[e]);
+                    g[i] = cg[istar * Np + i];
+                }
+            }
+            c = scal[istar];
+            // ---- a12: best update, strict < (A23)
+            if (c < cbest) {
+                cbest = c;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = t + e * NT;
+                    if (i < N) best[i] = th[i];
+                }
             }
         }
     }
@@ -231,18 +242,14 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             s.q_cfg[d * NC + lane] = v;
         }
     __syncthreads();
-    eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
-    float c = 0.f, cbest = 0.f;
+    // single eval_pass call site: pass 0 = Theta_0, then (L-BFGS step, A candidates) per iteration
+    float c = 0.f, cbest = 0.f, g0d = 0.f;
     int cnt = 0, fs = 0;
-    if (warp == 0) {
-        c = s.cfg_cost[lane];
-        cbest = c;
-        for (int d = 0; d < D; ++d) { g[d * NC + lane] = s.gV[d * NC + lane]; best[d * NC + lane] = th[d * NC + lane]; }
-    }
-    __syncthreads();
-    float g0d = 0.f;
-    for (int it = 0; it < kp.iters; ++it) {
-        if (warp == 0) {
+    const int npass = 1 + kp.iters * A;
+    for (int pass = 0; pass < npass; ++pass) {
+        const int a = pass == 0 ? -1 : (pass - 1) % A;
+        if (a == 0 && warp == 0) {
+            const int it = (pass - 1) / A;
             // ---- ring push (per seed, A20)
             if (it > 0) {
                 float sy = 0.f, yy = 0.f;
@@ -269,45 +276,50 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             for (int d = 0; d < D; ++d) q[d] = g[d * NC + lane];
             for (int i = cnt - 1; i >= 0; --i) {
                 const int sl = order[i * NC + lane];
-                float a = 0.f;
-                for (int d = 0; d < D; ++d) a += Sb[sl * DC + d * NC + lane] * q[d];
-                a *= rho[sl * NC + lane];
-                al[i] = a;
-                for (int d = 0; d < D; ++d) q[d] -= a * Yb[sl * DC + d * NC + lane];
+                float ai = 0.f;
+                for (int d = 0; d < D; ++d) ai += Sb[sl * DC + d * NC + lane] * q[d];
+                ai *= rho[sl * NC + lane];
+                al[i] = ai;
+                for (int d = 0; d < D; ++d) q[d] -= ai * Yb[sl * DC + d * NC + lane];
             }
             float gamma = 1.f;
             if (cnt > 0) { const int sl = order[(cnt - 1) * NC + lane]; gamma = syv[sl * NC + lane] / yyv[sl * NC + lane]; }
             for (int d = 0; d < D; ++d) q[d] *= gamma;
             for (int i = 0; i < cnt; ++i) {
                 const int sl = order[i * NC + lane];
-                float b = 0.f;
-                for (int d = 0; d < D; ++d) b += Yb[sl * DC + d * NC + lane] * q[d];
-                b *= rho[sl * NC + lane];
-                for (int d = 0; d < D; ++d) q[d] += (al[i] - b) * Sb[sl * DC + d * NC + lane];
+                float bi = 0.f;
+                for (int d = 0; d < D; ++d) bi += Yb[sl * DC + d * NC + lane] * q[d];
+                bi *= rho[sl * NC + lane];
+                for (int d = 0; d < D; ++d) q[d] += (al[i] - bi) * Sb[sl * DC + d * NC + lane];
             }
             g0d = 0.f;
             for (int d = 0; d < D; ++d) { dd[d * NC + lane] = -q[d]; g0d += g[d * NC + lane] * (-q[d]); }
         }
-        for (int a = 0; a < A; ++a) {
+        if (a >= 0) {
             if (warp == 0)
                 for (int d = 0; d < D; ++d)
                     s.q_cfg[d * NC + lane] = candidate(th[d * NC + lane], kp.alpha[a], dd[d * NC + lane], lim[d], lim[D + d]);
             __syncthreads();
-            eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
-            if (warp == 0) {
-                cc[a * NC + lane] = s.cfg_cost[lane];
-                float gd = 0.f;
-                for (int d = 0; d < D; ++d) {
-                    const float v = s.gV[d * NC + lane];
-                    cg[a * DC + d * NC + lane] = v;
-                    gd += v * dd[d * NC + lane];
-                }
-                cgd[a * NC + lane] = gd;
-            }
         }
-        if (warp == 0) {
+        eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
+        if (warp != 0) continue;
+        if (a < 0) {
+            c = s.cfg_cost[lane];
+            cbest = c;
+            for (int d = 0; d < D; ++d) { g[d * NC + lane] = s.gV[d * NC + lane]; best[d * NC + lane] = th[d * NC + lane]; }
+            continue;
+        }
+        cc[a * NC + lane] = s.cfg_cost[lane];
+        float gd = 0.f;
+        for (int d = 0; d < D; ++d) {
+            const float v = s.gV[d * NC + lane];
+            cg[a * DC + d * NC + lane] = v;
+            gd += v * dd[d * NC + lane];
+        }
+        cgd[a * NC + lane] = gd;
+        if (a == A - 1) {
             float ca[8], gda[8];
-            for (int a = 0; a < A; ++a) { ca[a] = cc[a * NC + lane]; gda[a] = cgd[a * NC + lane]; }
+            for (int k = 0; k < A; ++k) { ca[k] = cc[k * NC + lane]; gda[k] = cgd[k * NC + lane]; }
             const int i = ls_select(A, kp.alpha, c, g0d, ca, gda, kp.c1, kp.c2, kp.ls_mode);
             for (int d = 0; d < D; ++d) {
                 const int e = d * NC + lane;
@@ -320,8 +332,8 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
                 for (int d = 0; d < D; ++d) best[d * NC + lane] = th[d * NC + lane];
             }
         }
-        __syncthreads();
     }
+    __syncthreads();
     if (warp == 0 && active) {
         const size_t u = (size_t)p * kp.S + sd;
         kp.seed_best_cost[u] = cbest;
@@ -403,8 +415,8 @@ __global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KPara
             if (lane >= n_act) continue;
             const int um = s.iw[rp.o_perm + m];
             float *o = kp.spheres_out + ((size_t)(b0 + lane) * rp.M + um) * 4;
-            const float *w = s.sw + m * 3 * NC + lane;
-            o[0] = w[0]; o[1] = w[NC]; o[2] = w[2 * NC]; o[3] = sph[m].w;
+            const float4 w = s.sw[m * NC + lane];
+            o[0] = w.x; o[1] = w.y; o[2] = w.z; o[3] = sph[m].w;
         }
     if (kp.ee_out && warp == 0 && lane < n_act) {
         const float *T = s.lt + rp.ee * 12 * NC + lane;
@@ -573,9 +585,9 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.XS = mode == MODE_TO ? H + 5 : 0;
     L.q_cfg = take(D * NC);
     L.xs = take(D * L.XS);
-    L.ltg = take(std::max(rp.L * 12, rp.M * 3) * NC);     // link transforms, then sphere gradients
+    L.ltg = take(std::max(rp.L * 12, rp.M * 4) * NC);     // link transforms, then sphere gradients + E
     L.frames = take((D * 6 + 12) * NC);
-    L.swl = take(std::max(rp.M * 3, rp.L * 6) * NC);      // sphere centres, then link sums
+    L.swl = take(std::max(rp.M * 4, rp.L * 6) * NC);      // sphere centres (+hb), then link sums
     L.sbest = take(NW * NC);
     L.srank = take(NW * NC);
     L.sij = take(NW * NC);
