@@ -65,7 +65,7 @@ def test_seed_sharded_merge_matches_single_process(world):
     rng = np.random.default_rng(0)
     P, S = 9, 8
     costs = rng.uniform(0, 10, (P, S)).astype(np.float32)
-    costs[0, 2] = costs[0, 5] = 0.25   # minimal tie across ranks -> lowest global seed (2)
+    costs[0, 2] = costs[0, 5] = 0.01   # minimal tie across ranks -> lowest global seed (2)
     costs[1, :] = np.nan               # all NaN -> seed 0
     costs[2, 6] = np.nan
     trajs = rng.normal(size=(P, S, 4, 3)).astype(np.float32)
