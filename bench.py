@@ -214,6 +214,7 @@ def run_native(args):
     start = torch.tensor(wl.start, device=dev)
     env = torch.tensor(wl.env, device=dev)
     sp = wl.solver
+    ctas_per_sm, smem_per_cta = ctx.solver_occupancy(32, sp.history, len(sp.alpha))
     evals_per_step = wl.evals_per_solve()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
@@ -297,6 +298,7 @@ def run_native(args):
                            "seeds": 32, "timesteps": 32, "dof": 7, "spheres": 64, "self_pairs": int(len(wl.robot.pairs)),
                            "boxes": 20, "iters": args.iters, "line_search": list(sp.alpha), "history": sp.history,
                            "flags": "sweep+speed", "evals_per_step_per_gpu": evals_per_step,
+                           "ctas_per_sm": ctas_per_sm, "smem_bytes_per_cta": smem_per_cta,
                            "l2": "flushed between timed steps (256 MB write, outside the events)",
                            "parallelism": f"problem-sharded x{world}, no data-path collective"},
                 "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",

@@ -192,6 +192,11 @@ crb_status crb_argmin_keys(int P, int S, const float *cost, int64_t seed_base, i
 crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const float *Y,
                                const float *g, float *d, void *stream);
 
+/* Shared-memory footprint (bytes per CTA) and resident CTAs per SM of the persistent solver for
+ * horizon H (1 = IK) with the current robot and world (diagnostics; needs robot, world, params). */
+crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, int *ctas_per_sm,
+                                int *smem_bytes);
+
 /* Number of kernel launches this context issued since creation (bench accounting). */
 int64_t crb_launch_count(const crb_ctx *ctx);
 

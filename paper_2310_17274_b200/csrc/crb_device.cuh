@@ -40,6 +40,7 @@ struct RobotPack {
     int o_rank;     // u16 ranks in S of the block pairs, [block][u][v] from the block's rank base
     int o_lim;      // 5 x D floats: lo, hi, vmax, amax, jmax
     int o_doflink;  // D ints: link carrying dof d
+    int o_desc;     // L ints: bit l' set iff link l' is in the subtree of link l (l itself included)
     int o_perm;     // M ints: packed sphere index -> caller's sphere index
     int words;      // total (multiple of 4)
 };
@@ -47,7 +48,7 @@ struct RobotPack {
 // Shared-memory layout (offsets in 4-byte words from the dynamic smem base).
 struct Layout {
     int robot, boxes, mbar;
-    int q_cfg, xs, ltg, frames, swl, sbest, srank, sij, wpart, cbb, csm, gxd, gq, gva, pose_ft, pose_c,
+    int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, wpart, cbb, csm, gxd, gq, gva, pose_ft, pose_c,
         goal, cfg_cost, cfg_terms, gV, red, st, scal;
     int solver;      // start of the solver region
     int total;       // words
@@ -273,7 +274,7 @@ struct Smem {
     const int *iw;          // robot blob as ints
     const float *fw;        // robot blob as floats
     const float *boxes;
-    float *q_cfg, *xs, *lt, *frames, *ls, *sbest, *wpart, *cbb, *csm, *gxd, *gq, *gva, *pose_ft,
+    float *q_cfg, *scs, *xs, *lt, *frames, *ls, *sbest, *wpart, *cbb, *csm, *gxd, *gq, *gva, *pose_ft,
         *pose_c, *goal, *cfg_cost, *cfg_terms, *gV, *red, *st, *scal;
     float4 *sw;             // [M][32] sphere centre (x, y, z) and hb = -(|w|^2 - r_self^2) / 2
     float4 *sg;             // [M][32] dE/dw (x, y, z) and the world energy E (w)
@@ -286,7 +287,7 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     s.iw = reinterpret_cast<const int *>(smem + L.robot);
     s.fw = smem + L.robot;
     s.boxes = smem + L.boxes;
-    s.q_cfg = smem + L.q_cfg; s.xs = smem + L.xs;
+    s.q_cfg = smem + L.q_cfg; s.scs = smem + L.scs; s.xs = smem + L.xs;
     s.lt = smem + L.ltg;                               // sg aliases lt (lt dead after sphere placement)
     s.sg = reinterpret_cast<float4 *>(smem + L.ltg);
     s.frames = smem + L.frames;
@@ -300,6 +301,17 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     s.goal = smem + L.goal; s.cfg_cost = smem + L.cfg_cost; s.cfg_terms = smem + L.cfg_terms;
     s.gV = smem + L.gV; s.red = smem + L.red; s.st = smem + L.st; s.scal = smem + L.scal;
     return s;
+}
+
+// sin / cos of every joint value of the 32 slots, computed by all threads before the serial FK
+// chain (scs[0..D) = sin, scs[D..2D) = cos).
+__device__ __forceinline__ void prep_sincos(const Smem &s, int D) {
+    for (int idx = threadIdx.x; idx < D * NC; idx += NT) {
+        float sn, cs;
+        sincosf(s.q_cfg[idx], &sn, &cs);
+        s.scs[idx] = sn;
+        s.scs[D * NC + idx] = cs;
+    }
 }
 
 // frames[d][6][32]: world axis k and origin o of the joint carrying dof d; then EE R (9) + p (3).
@@ -338,8 +350,7 @@ __device__ __forceinline__ void fk_phase(const RobotPack rp, const Smem &s) {
                     else if (type == 2) { m03 = fmaf(m01, v, m03); m13 = fmaf(m11, v, m13); m23 = fmaf(m21, v, m23); }
                     else { m03 = fmaf(m02, v, m03); m13 = fmaf(m12, v, m13); m23 = fmaf(m22, v, m23); }
                 } else {
-                    float sn, cs;
-                    sincosf(v, &sn, &cs);
+                    const float sn = s.scs[dof * NC + lane], cs = s.scs[(rp.D + dof) * NC + lane];
                     if (type == 4) {        // revolute x: col1' = c f1 + s f2, col2' = -s f1 + c f2
                         const float a0 = m01, a1 = m11, a2 = m21;
                         m01 = cs * a0 + sn * m02; m11 = cs * a1 + sn * m12; m21 = cs * a2 + sn * m22;
@@ -538,7 +549,14 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             else if (h >= H - 3) v = thA[(H - 1) * D + d];
             else v = thA[(h - 1) * D + d];
             s.q_cfg[idx] = v;
+            float sn, cs;
+            sincosf(v, &sn, &cs);
+            s.scs[idx] = sn;
+            s.scs[D * NC + idx] = cs;
         }
+        __syncthreads();
+    } else {
+        prep_sincos(s, D);
         __syncthreads();
     }
 
@@ -829,30 +847,28 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         }
     }
     __syncthreads();
-    // subtree accumulation, child -> parent in reverse topological order; warp k owns component k
-    if (warp < 6) {
-        const int k = warp;
-        for (int l = rp.L - 1; l >= 1; --l) {
-            const int p = s.iw[rp.o_links + 16 * l + 12];
-            if (p >= 0) s.ls[(p * 6 + k) * NC + lane] += s.ls[(l * 6 + k) * NC + lane];
-        }
-    }
-    __syncthreads();
-    // joint gradient: revolute k . (T_l - o_l x F_l), prismatic k . F_l (Table 7), + bound_pos
+    // joint gradient: the subtree sums of the joint's link (independent loads over the host-built
+    // descendant mask), then revolute k . (T - o x F), prismatic k . F (Table 7), + bound_pos
     for (int idx = tid; idx < D * NC; idx += NT) {
         const int d = idx / NC, c = idx - d * NC;
         const int l = s.iw[rp.o_doflink + d];
         const int type = s.iw[rp.o_links + 16 * l + 13];
+        unsigned mask = (unsigned)s.iw[rp.o_desc + l];
+        float F0 = 0.f, F1 = 0.f, F2 = 0.f, T0 = 0.f, T1 = 0.f, T2 = 0.f;
+        while (mask) {
+            const int l2 = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float *S6 = s.ls + l2 * 6 * NC + c;
+            F0 += S6[0]; F1 += S6[NC]; F2 += S6[2 * NC]; T0 += S6[3 * NC]; T1 += S6[4 * NC]; T2 += S6[5 * NC];
+        }
         const float *fr = s.frames + d * 6 * NC + c;
         const float kx = fr[0], ky = fr[NC], kz = fr[2 * NC];
-        const float *S6 = s.ls + l * 6 * NC + c;
-        const float F0 = S6[0], F1 = S6[NC], F2 = S6[2 * NC];
         float g;
         if (type >= 4) {
             const float ox = fr[3 * NC], oy = fr[4 * NC], oz = fr[5 * NC];
-            const float t0 = S6[3 * NC] - (oy * F2 - oz * F1);
-            const float t1 = S6[4 * NC] - (oz * F0 - ox * F2);
-            const float t2 = S6[5 * NC] - (ox * F1 - oy * F0);
+            const float t0 = T0 - (oy * F2 - oz * F1);
+            const float t1 = T1 - (oz * F0 - ox * F2);
+            const float t2 = T2 - (ox * F1 - oy * F0);
             g = kx * t0 + ky * t1 + kz * t2;
         } else {
             g = kx * F0 + ky * F1 + kz * F2;

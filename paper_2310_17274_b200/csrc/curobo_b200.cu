@@ -408,6 +408,8 @@ __global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KPara
     if (warp == 0)
         for (int d = 0; d < D; ++d) s.q_cfg[d * NC + lane] = lane < n_act ? kp.q_in[(size_t)(b0 + lane) * D + d] : 0.f;
     __syncthreads();
+    prep_sincos(s, D);
+    __syncthreads();
     fk_phase(kp.rp, s);
     const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
     if (kp.spheres_out)
@@ -587,7 +589,8 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.xs = take(D * L.XS);
     L.ltg = take(std::max(rp.L * 12, rp.M * 4) * NC);     // link transforms, then sphere gradients + E
     L.frames = take((D * 6 + 12) * NC);
-    L.swl = take(std::max(rp.M * 4, rp.L * 6) * NC);      // sphere centres (+hb), then link sums
+    L.swl = take(std::max(std::max(rp.M * 4, rp.L * 6), 2 * D) * NC);   // joint sin/cos (before the chain),
+    L.scs = L.swl;                                                      // then sphere centres (+hb), then link sums
     L.sbest = take(NW * NC);
     L.srank = take(NW * NC);
     L.sij = take(NW * NC);
@@ -820,6 +823,7 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
     rp.o_rank = w; w += r4(((int)ranks.size() + 1) / 2);
     rp.o_lim = w; w += r4(5 * D);
     rp.o_doflink = w; w += r4(D);
+    rp.o_desc = w; w += r4(L);
     rp.o_perm = w; w += r4(M);
     rp.words = r4(w);
     std::vector<uint32_t> blob(rp.words, 0);
@@ -849,6 +853,15 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         fput(rp.o_lim + 2 * D + d, r->vel_max[d]); fput(rp.o_lim + 3 * D + d, r->acc_max[d]);
         fput(rp.o_lim + 4 * D + d, r->jerk_max[d]);
         blob[rp.o_doflink + d] = (uint32_t)doflink[d];
+    }
+    for (int l = 0; l < L; ++l) {   // descendant masks: walk every later link up towards l
+        uint32_t m = 1u << l;
+        for (int c2 = l + 1; c2 < L; ++c2) {
+            int a = c2;
+            while (a > l) a = r->links[a].parent;
+            if (a == l) m |= 1u << c2;
+        }
+        blob[rp.o_desc + l] = m;
     }
     cudaFree(ctx->d_robot);
     ctx->d_robot = nullptr;
@@ -1026,6 +1039,24 @@ crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P
     if (st == CRB_OK && best_key) st = cuda_check(ctx, cudaMemcpyAsync(best_key, ctx->h_key, (size_t)P * 8, cudaMemcpyDeviceToHost, s), "D2H key");
     if (st != CRB_OK) return st;
     return cuda_check(ctx, cudaStreamSynchronize(s), "solve_host synchronize");
+}
+
+crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, int *ctas_per_sm,
+                                 int *smem_bytes) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if ((st = ready(ctx, true)) != CRB_OK) return st;
+    KParams kp = base_params(ctx);
+    const int mode = H == 1 ? MODE_IK : MODE_TO;
+    const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, history, n_alpha, true, kp.lay);
+    if (smem_bytes) *smem_bytes = (int)bytes;
+    if (bytes > SMEM_MAX) { if (ctas_per_sm) *ctas_per_sm = 0; return CRB_OK; }
+    int n = 0;
+    const void *fn = mode == MODE_TO ? (const void *)solve_to_kernel : (const void *)solve_ik_kernel;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    st = cuda_check(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, NT, bytes), "occupancy");
+    if (ctas_per_sm) *ctas_per_sm = n;
+    return st;
 }
 
 crb_status crb_ls_select(int n, int A, const float *alpha_host, const float *c0, const float *g0d, const float *ca,

@@ -82,12 +82,13 @@ _lib.crb_lbfgs_solve_host.argtypes = [_V, C.POINTER(crb_solver_params), C.c_int,
 _lib.crb_ls_select.argtypes = [C.c_int, C.c_int, F_P, _V, _V, _V, _V, C.c_float, C.c_float, C.c_int, _V, _V]
 _lib.crb_argmin_keys.argtypes = [C.c_int, C.c_int, _V, C.c_int64, _V, _V, _V]
 _lib.crb_lbfgs_direction.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, _V, _V, _V]
+_lib.crb_solver_occupancy.argtypes = [_V, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
 _lib.crb_launch_count.argtypes = [_V]
 _lib.crb_launch_count.restype = C.c_int64
 
 SYMBOLS = ["crb_create", "crb_destroy", "crb_last_error", "crb_version", "crb_set_robot", "crb_set_world",
            "crb_set_cost_params", "crb_fk", "crb_evaluate_cost_grad", "crb_lbfgs_solve", "crb_lbfgs_solve_host",
-           "crb_ls_select", "crb_argmin_keys", "crb_lbfgs_direction", "crb_launch_count"]
+           "crb_ls_select", "crb_argmin_keys", "crb_lbfgs_direction", "crb_launch_count", "crb_solver_occupancy"]
 
 
 def _ptr(t):
@@ -146,6 +147,12 @@ class Context:
     def _chk(self, code):
         if code != 0:
             raise CrbError(code, _lib.crb_last_error(self.h).decode())
+
+    def solver_occupancy(self, H: int, history: int = 4, n_alpha: int = 4):
+        """(CTAs resident per SM, shared-memory bytes per CTA) of the persistent solver."""
+        n, b = C.c_int(), C.c_int()
+        self._chk(_lib.crb_solver_occupancy(self.h, int(H), int(history), int(n_alpha), C.byref(n), C.byref(b)))
+        return n.value, b.value
 
     @property
     def launches(self) -> int:

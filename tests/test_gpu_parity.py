@@ -444,3 +444,59 @@ def test_error_statuses(native):
         ctx.evaluate(T(np.zeros((2, 5, 7))), T(np.zeros((2, 7))), start=T(np.zeros((2, 7))))
     assert e.value.code == -2                       # H < 8 in TO mode
     ctx.close()
+
+
+# ------------------------------------------------------------------------------------------ config 5 / full size
+
+def test_eval_to_parity_dense_k1000(native, O):
+    """Config 5 geometry: 1000 small cuboids per environment, swept + speed (cuboid table 64 KB in
+    shared memory, so one CTA per SM)."""
+    B, H = 6, 32
+    rb, starts, goals_cfg, trajs = franka_trajs(555, B, H, noise=0.4)
+    worlds = [inputs.dense_scene(4, e, 1000) for e in range(2)]
+    cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED, dt=0.25)
+    ctx = make(native, rb, worlds, cp)
+    R = O.Robot(rb)
+    Ws = [O.World(w) for w in worlds]
+    env = (np.arange(B) % 2).astype(np.int32)
+    goals = np.array([O.fk(R, q)[2] for q in goals_cfg])
+    V, st, gl = f32(trajs), f32(starts), f32(goals)
+    cost, grad, terms = ctx.evaluate(T(V), T(gl), start=T(st), env=T(env, torch.int32))
+    cost, grad = cost.cpu().numpy(), grad.cpu().numpy()
+    stats = Stats()
+    active = 0
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin, cnt = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"dense {b}")
+        active += t_ref[4] > 0
+    stats.done(0.34)
+    assert active >= 2
+    ctx.close()
+
+
+def test_full_size_solve_sampled_against_oracle(native, O):
+    """BASELINE configs[1] at the bench size (64 problems x 32 seeds x 32 timesteps, K = 20,
+    100 iterations) in the launch configuration bench.py times; for sampled problems the oracle
+    re-evaluates the returned winner: its cost must equal the reported best cost, and the winner
+    must be the argmin of the per-seed results."""
+    from paper_2310_17274_b200 import workload
+    wl = workload.franka_to(0, list(range(64)), S=32, H=32, iters=100)
+    ctx = make(native, wl.robot, wl.worlds, wl.cost)
+    out = ctx.solve(wl.solver, T(wl.seeds), T(wl.goal), start=T(wl.start), env=T(wl.env, torch.int32),
+                    seed_outputs=True)
+    bt = out["best_traj"].cpu().numpy().astype(np.float64)
+    bc = out["best_cost"].cpu().numpy()
+    sbc = out["seed_best_cost"].cpu().numpy()
+    R = O.Robot(wl.robot)
+    stats = Stats()
+    for p in (0, 17, 38, 63):
+        c_ref, g_ref, _, margin, _ = O.eval_traj(R, O.World(wl.worlds[p]), wl.cost, f32(wl.start[p]),
+                                                 f32(wl.goal[p]), bt[p])
+        stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"winner {p}")
+        assert bc[p] == sbc[p].min()
+    stats.done(0.5)
+    # every seed improved on its initial cost
+    c0, _, _ = ctx.evaluate(T(wl.seeds.reshape(-1, 32, 7)), T(np.repeat(wl.goal, 32, 0)),
+                            start=T(np.repeat(wl.start, 32, 0)), env=T(np.repeat(wl.env, 32), torch.int32))
+    assert np.all(sbc.reshape(-1) <= c0.cpu().numpy() * (1 + 1e-6))
+    ctx.close()
