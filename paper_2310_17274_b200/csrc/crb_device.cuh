@@ -321,9 +321,9 @@ __device__ __forceinline__ float *ee_frame(const Smem &s, int D) { return s.fram
 // 3x4 link transforms (the paper's "parallel threads per matrix"), lane = slot.  Writes
 // lt[l][12][32] plus the compact joint frames / EE pose; then every warp places its spheres:
 // sw[m][3][32] = R_link c_m + t_link.
-__device__ __forceinline__ void fk_phase(const RobotPack rp, const Smem &s) {
+__device__ __forceinline__ void fk_chain(const RobotPack &rp, const Smem &s) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp < 3) {
+    {
         const int r = warp;
         float *fee = ee_frame(s, rp.D);
         float4 cur = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -386,7 +386,11 @@ __device__ __forceinline__ void fk_phase(const RobotPack rp, const Smem &s) {
             cur = nr;
         }
     }
-    __syncthreads();
+}
+
+// Sphere placement (all warps), after the chain: sw[m][lane] = (R_link c_m + t_link, hb).
+__device__ __forceinline__ void fk_place(const RobotPack &rp, const Smem &s) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
     for (int m = warp; m < rp.M; m += NW) {
         const int l = s.iw[rp.o_sphlink + m];
@@ -398,6 +402,12 @@ __device__ __forceinline__ void fk_phase(const RobotPack rp, const Smem &s) {
         const float rs = s.fw[rp.o_rself + m];
         s.sw[m * NC + lane] = make_float4(wx, wy, wz, -0.5f * (wx * wx + wy * wy + wz * wz - rs * rs));
     }
+}
+
+__device__ __forceinline__ void fk_phase(const RobotPack &rp, const Smem &s) {
+    if ((threadIdx.x >> 5) < 3) fk_chain(rp, s);
+    __syncthreads();
+    fk_place(rp, s);
     __syncthreads();
 }
 
@@ -432,20 +442,22 @@ __device__ __forceinline__ void mat_to_quat(float r00, float r01, float r02, flo
 // and gap = L - 2r' > 0); also the larger half-segment.  One function for the screen set-up and
 // the slow path, so both take bitwise the same decisions.
 __device__ __forceinline__ int sweep_dirs(const float4 *p, float cx, float cy, float cz, float rp, bool hasp,
-                                          bool hasn, bool sweepf, float &maxb) {
+                                          bool hasn, bool sweepf, float &maxb2) {
+    // gap = L - 2r' > 0  <=>  L^2 > 4 r'^2 ;  (L/2)^2 = L^2 / 4  (no square root on this path)
     int dirs = 0;
-    maxb = 0.f;
+    maxb2 = 0.f;
+    const float four_rp2 = 4.f * rp * rp;
     if (sweepf && hasp) {
         const float4 q = p[-1];
         const float vx = q.x - cx, vy = q.y - cy, vz = q.z - cz;
-        const float L = sqrtf(vx * vx + vy * vy + vz * vz);
-        if (L - 2.f * rp > 0.f) { dirs |= 1; maxb = 0.5f * L; }
+        const float L2 = vx * vx + vy * vy + vz * vz;
+        if (L2 > four_rp2) { dirs |= 1; maxb2 = 0.25f * L2; }
     }
     if (sweepf && hasn) {
         const float4 q = p[1];
         const float vx = q.x - cx, vy = q.y - cy, vz = q.z - cz;
-        const float L = sqrtf(vx * vx + vy * vy + vz * vz);
-        if (L - 2.f * rp > 0.f) { dirs |= 2; maxb = fmaxf(maxb, 0.5f * L); }
+        const float L2 = vx * vx + vy * vy + vz * vz;
+        if (L2 > four_rp2) { dirs |= 2; maxb2 = fmaxf(maxb2, 0.25f * L2); }
     }
     return dirs;
 }
@@ -560,8 +572,47 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         __syncthreads();
     }
 
-    // ---- a3: forward kinematics (after this, lt is dead and its space holds sg)
-    fk_phase(rp, s);
+    // ---- a3: forward kinematics: warps 0..2 walk the chain (after this, lt is dead and holds sg)
+    if (warp < 3) {
+        fk_chain(rp, s);
+    } else {
+        // ---- a8 runs on warps 3.. while warps 0..2 walk the kinematic chain (it needs only xs / q)
+        //      a8: bound (Eq. bound_cost) on pos/vel/acc/jerk and smoothness (Eq. smooth_cost)
+        for (int idx = tid - 3 * NC; idx < D * NC; idx += NT - 3 * NC) {
+            const int d = idx / NC, c = idx - d * NC;
+            float cb = 0.f, cs = 0.f, gx = 0.f, gv = 0.f, ga = 0.f, gj = 0.f;
+            if (c < n_act) {
+                const float lo = lim[d], hi = lim[D + d];
+                float dd;
+                if (MODE == MODE_TO) {
+                    const float *x = s.xs + d * XS + c + 3;   // x_h with h = c + 1
+                    const float xm2 = x[-2], xm1 = x[-1], x0 = x[0], xp1 = x[1], xp2 = x[2];
+                    const float dt = cf.dt, dt2 = dt * dt, dt3 = dt2 * dt;
+                    // O3 five-point stencil (§A.5, A15)
+                    const float v = (-xp2 + 8.f * xp1 - 8.f * xm1 + xm2) / (12.f * dt);
+                    const float a = (-xp2 + 16.f * xp1 - 30.f * x0 + 16.f * xm1 - xm2) / (12.f * dt2);
+                    const float j = (xp2 - 2.f * xp1 + 2.f * xm1 - xm2) / (2.f * dt3);
+                    const float vm = lim[2 * D + d], am = lim[3 * D + d], jm = lim[4 * D + d];
+                    cb += cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd); gx = cf.wb[0] * dd;
+                    cb += cf.wb[1] * bound_cost(v, -vm, vm, cf.eta_bound, dd); gv = cf.wb[1] * dd;
+                    cb += cf.wb[2] * bound_cost(a, -am, am, cf.eta_bound, dd); ga = cf.wb[2] * dd;
+                    cb += cf.wb[3] * bound_cost(j, -jm, jm, cf.eta_bound, dd); gj = cf.wb[3] * dd;
+                    cs = cf.a8 * a * a;
+                    ga += 2.f * cf.a8 * a;
+                    if (cf.flags & F_JERK) { cs += cf.a9 * j * j; gj += 2.f * cf.a9 * j; }
+                } else {
+                    const float x0 = s.q_cfg[d * NC + c];
+                    cb = cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd);
+                    gx = cf.wb[0] * dd;
+                }
+            }
+            s.cbb[idx] = cb; s.csm[idx] = cs; s.gxd[idx] = gx;
+            if (MODE == MODE_TO) { s.gva[idx] = gv; s.gva[D * NC + idx] = ga; s.gva[2 * D * NC + idx] = gj; }
+        }
+    }
+    __syncthreads();
+    fk_place(rp, s);
+    __syncthreads();
 
     // ---- a4: self-collision (Eq. self-collision, Alg. 9).  S is stored as rectangular blocks of
     // pairs {ia..ia+na-1} x {jb..jb+len-1} (spheres of one link share their partner ranges); each
@@ -591,6 +642,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 ha[u] = u < na ? wi[u].w : -1e30f;
             }
             const float4 *wjp = s.sw + jb * NC + lane;
+#pragma unroll 2
             for (int v = 0; v < len; ++v) {
                 const float4 wj = wjp[v * NC];
                 const float rj = rself[jb + v];
@@ -656,10 +708,10 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     sp[u] = spd;
                     const float r = sph[m].w;
                     const float rpr = r + cf.eta;   // Alg. 10 "sph.radius += eta"
-                    float maxb;
-                    dirs[u] = sweep_dirs(p, c.x, c.y, c.z, rpr, hasp, hasn, sweepf, maxb);
+                    float maxb2;
+                    dirs[u] = sweep_dirs(p, c.x, c.y, c.z, rpr, hasp, hasn, sweepf, maxb2);
                     // r < 0 disables the sphere; sp = 0 => C_w = 0 exactly
-                    if (r >= 0.f && spd != 0.f) th2[u] = fmaxf(rpr * rpr, maxb * maxb);
+                    if (r >= 0.f && spd != 0.f) th2[u] = fmaxf(rpr * rpr, maxb2);
                 }
             }
             if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
@@ -695,39 +747,6 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             }
         }
         s.wpart[warp * NC + lane] = wsum;
-    }
-
-    // ---- a8: bound (Eq. bound_cost) on pos/vel/acc/jerk and smoothness (Eq. smooth_cost)
-    for (int idx = tid; idx < D * NC; idx += NT) {
-        const int d = idx / NC, c = idx - d * NC;
-        float cb = 0.f, cs = 0.f, gx = 0.f, gv = 0.f, ga = 0.f, gj = 0.f;
-        if (c < n_act) {
-            const float lo = lim[d], hi = lim[D + d];
-            float dd;
-            if (MODE == MODE_TO) {
-                const float *x = s.xs + d * XS + c + 3;   // x_h with h = c + 1
-                const float xm2 = x[-2], xm1 = x[-1], x0 = x[0], xp1 = x[1], xp2 = x[2];
-                const float dt = cf.dt, dt2 = dt * dt, dt3 = dt2 * dt;
-                // O3 five-point stencil (§A.5, A15)
-                const float v = (-xp2 + 8.f * xp1 - 8.f * xm1 + xm2) / (12.f * dt);
-                const float a = (-xp2 + 16.f * xp1 - 30.f * x0 + 16.f * xm1 - xm2) / (12.f * dt2);
-                const float j = (xp2 - 2.f * xp1 + 2.f * xm1 - xm2) / (2.f * dt3);
-                const float vm = lim[2 * D + d], am = lim[3 * D + d], jm = lim[4 * D + d];
-                cb += cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd); gx = cf.wb[0] * dd;
-                cb += cf.wb[1] * bound_cost(v, -vm, vm, cf.eta_bound, dd); gv = cf.wb[1] * dd;
-                cb += cf.wb[2] * bound_cost(a, -am, am, cf.eta_bound, dd); ga = cf.wb[2] * dd;
-                cb += cf.wb[3] * bound_cost(j, -jm, jm, cf.eta_bound, dd); gj = cf.wb[3] * dd;
-                cs = cf.a8 * a * a;
-                ga += 2.f * cf.a8 * a;
-                if (cf.flags & F_JERK) { cs += cf.a9 * j * j; gj += 2.f * cf.a9 * j; }
-            } else {
-                const float x0 = s.q_cfg[d * NC + c];
-                cb = cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd);
-                gx = cf.wb[0] * dd;
-            }
-        }
-        s.cbb[idx] = cb; s.csm[idx] = cs; s.gxd[idx] = gx;
-        if (MODE == MODE_TO) { s.gva[idx] = gv; s.gva[D * NC + idx] = ga; s.gva[2 * D * NC + idx] = gj; }
     }
 
     // ---- a7: pose cost (Eq. pose_cost_term, A1) at the terminal slot (TO) / every slot (IK)
