@@ -28,8 +28,9 @@ enum { MODE_TO = 0, MODE_IK = 1 };
 // Packed robot tables (built by the host in crb_set_robot).  Offsets are in 4-byte words from
 // the start of the blob; every section starts on a 16-byte boundary.
 struct RobotPack {
-    int L, D, M, P, ee;
-    int o_links;    // L x 16 words: F[12] (3x4 row-major), parent, type, dof, pad
+    int L, D, M, P, ee;  // L = number of FRAMES (root + actuated links, fixed links folded); ee = EE frame
+    int o_links;    // L x 16 words: C[12] (3x4 row-major fixed part), parent frame, type, dof, pad
+    int o_eeoff;    // 12 floats: EE pose in its frame (3x4)
     int o_sph;      // M float4 (centre in link frame, radius), spheres grouped by link
     int o_sphlink;  // M ints
     int o_sbeg;     // L+1 ints: spheres of link l are [sbeg[l], sbeg[l+1])
@@ -379,9 +380,12 @@ __device__ __forceinline__ void fk_chain(const RobotPack &rp, const Smem &s) {
                 fr[r * NC] = ax == 0 ? nr.x : (ax == 1 ? nr.y : nr.z);
                 fr[(3 + r) * NC] = nr.w;
             }
-            if (l == rp.ee) {
-                fee[(3 * r + 0) * NC + lane] = nr.x; fee[(3 * r + 1) * NC + lane] = nr.y;
-                fee[(3 * r + 2) * NC + lane] = nr.z; fee[(9 + r) * NC + lane] = nr.w;
+            if (l == rp.ee) {   // EE = T_frame * C_ee (the folded fixed offset)
+                const float *E = s.fw + rp.o_eeoff;
+                fee[(3 * r + 0) * NC + lane] = nr.x * E[0] + nr.y * E[4] + nr.z * E[8];
+                fee[(3 * r + 1) * NC + lane] = nr.x * E[1] + nr.y * E[5] + nr.z * E[9];
+                fee[(3 * r + 2) * NC + lane] = nr.x * E[2] + nr.y * E[6] + nr.z * E[10];
+                fee[(9 + r) * NC + lane] = nr.x * E[3] + nr.y * E[7] + nr.z * E[11] + nr.w;
             }
             cur = nr;
         }

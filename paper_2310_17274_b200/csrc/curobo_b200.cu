@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -421,11 +422,11 @@ __global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KPara
             o[0] = w.x; o[1] = w.y; o[2] = w.z; o[3] = sph[m].w;
         }
     if (kp.ee_out && warp == 0 && lane < n_act) {
-        const float *T = s.lt + rp.ee * 12 * NC + lane;
+        const float *E = ee_frame(s, D) + lane;   // R (9, row-major) then p (3)
         float q[4];
-        mat_to_quat(T[0], T[NC], T[2 * NC], T[4 * NC], T[5 * NC], T[6 * NC], T[8 * NC], T[9 * NC], T[10 * NC], q);
+        mat_to_quat(E[0], E[NC], E[2 * NC], E[3 * NC], E[4 * NC], E[5 * NC], E[6 * NC], E[7 * NC], E[8 * NC], q);
         float *o = kp.ee_out + (size_t)(b0 + lane) * 7;
-        o[0] = T[3 * NC]; o[1] = T[7 * NC]; o[2] = T[11 * NC];
+        o[0] = E[9 * NC]; o[1] = E[10 * NC]; o[2] = E[11 * NC];
         o[3] = q[0]; o[4] = q[1]; o[5] = q[2]; o[6] = q[3];
     }
 }
@@ -733,19 +734,74 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         const int i = r->pairs[2 * p], j = r->pairs[2 * p + 1];
         if (i < 0 || j >= M || i >= j) return fail(ctx, CRB_E_ROBOT, "self-collision pair with i >= j or out of range");
     }
-    // ---- pack: spheres grouped by link (stable), pairs remapped, disabled pairs dropped
+    // ---- kinematic folding (exact algebra, fp64 on the host): every fixed link l is rigidly
+    // attached to its nearest actuated ancestor b(l), T_l = T_b(l) * C_l with C_l the product of the
+    // fixed transforms on the path (Table 6: full link = F * J, J = I for fixed joints).  The
+    // device chain then runs over frame 0 (the root, identity) and the D actuated links only;
+    // spheres and the end effector are re-expressed in their frame.
+    typedef std::array<double, 12> M34;
+    auto compose = [](const M34 &A, const M34 &B) {   // [A|a] * [B|b] (3x4 homogeneous)
+        M34 C{};
+        for (int i = 0; i < 3; ++i) {
+            for (int j = 0; j < 4; ++j) {
+                double v = 0.0;
+                for (int k = 0; k < 3; ++k) v += A[i * 4 + k] * B[k * 4 + j];
+                C[i * 4 + j] = v + (j == 3 ? A[i * 4 + 3] : 0.0);
+            }
+        }
+        return C;
+    };
+    std::vector<int> bl(L), frame_of(L, -1);
+    std::vector<M34> Cl(L);
+    for (int l = 0; l < L; ++l) {
+        M34 F;
+        for (int i = 0; i < 12; ++i) F[i] = r->links[l].fixed[i];
+        const int p = r->links[l].parent;
+        if (p < 0) { bl[l] = -1; Cl[l] = F; }
+        else if (r->links[p].type != 0) { bl[l] = p; Cl[l] = F; }
+        else { bl[l] = bl[p]; Cl[l] = compose(Cl[p], F); }
+    }
+    const int NF = D + 1;
+    std::vector<int> fparent(NF, -1), ftype(NF, 0), fdof(NF, -1);
+    std::vector<M34> fC(NF);
+    fC[0] = M34{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+    for (int l = 0, f = 1; l < L; ++l)
+        if (r->links[l].type != 0) {
+            frame_of[l] = f;
+            fparent[f] = bl[l] < 0 ? 0 : frame_of[bl[l]];
+            ftype[f] = r->links[l].type; fdof[f] = r->links[l].dof; fC[f] = Cl[l];
+            ++f;
+        }
+    auto frame_and_offset = [&](int l, M34 &off) {   // frame carrying link l, offset of l in it
+        if (r->links[l].type != 0) { off = M34{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0}; return frame_of[l]; }
+        off = Cl[l];
+        return bl[l] < 0 ? 0 : frame_of[bl[l]];
+    };
+    std::vector<int> sframe(M);
+    std::vector<std::array<double, 3>> scen(M);
+    for (int m = 0; m < M; ++m) {
+        M34 off;
+        sframe[m] = frame_and_offset(r->sphere_link[m], off);
+        for (int i = 0; i < 3; ++i)
+            scen[m][i] = off[i * 4 + 0] * r->spheres[4 * m + 0] + off[i * 4 + 1] * r->spheres[4 * m + 1] +
+                         off[i * 4 + 2] * r->spheres[4 * m + 2] + off[i * 4 + 3];
+    }
+    M34 eeoff;
+    const int fee = frame_and_offset(r->ee_link, eeoff);
+    // ---- pack: spheres grouped by frame (stable), pairs remapped, disabled pairs dropped
     std::vector<int> ord(M);
     for (int m = 0; m < M; ++m) ord[m] = m;
-    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return r->sphere_link[a] < r->sphere_link[b]; });
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return sframe[a] < sframe[b]; });
     std::vector<int> inv(M);
     for (int k = 0; k < M; ++k) inv[ord[k]] = k;
     RobotPack rp{};
-    rp.L = L; rp.D = D; rp.M = M; rp.ee = r->ee_link;
+    rp.L = NF; rp.D = D; rp.M = M; rp.ee = fee;
     int w = 0;
-    rp.o_links = w; w += 16 * L;
+    rp.o_links = w; w += 16 * NF;
+    rp.o_eeoff = w; w += 12 + 4;
     rp.o_sph = w; w += 4 * M;
     rp.o_sphlink = w; w += r4(M);
-    rp.o_sbeg = w; w += r4(L + 1);
+    rp.o_sbeg = w; w += r4(NF + 1);
     // self pairs (Eq. self-collision): drop r+o <= 0 (Alg. 9 "continue", P:2778 -- exact),
     // remap to packed sphere indices a < b, then cover S with rectangular blocks
     // {ia..ia+na-1} x {jb..jb+len-1} (na <= 4): consecutive first spheres with identical partner runs
@@ -823,26 +879,28 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
     rp.o_rank = w; w += r4(((int)ranks.size() + 1) / 2);
     rp.o_lim = w; w += r4(5 * D);
     rp.o_doflink = w; w += r4(D);
-    rp.o_desc = w; w += r4(L);
+    rp.o_desc = w; w += r4(NF);
     rp.o_perm = w; w += r4(M);
     rp.words = r4(w);
     std::vector<uint32_t> blob(rp.words, 0);
     auto fput = [&](int o, float v) { memcpy(&blob[o], &v, 4); };
-    for (int l = 0; l < L; ++l) {
-        for (int i = 0; i < 12; ++i) fput(rp.o_links + 16 * l + i, r->links[l].fixed[i]);
-        blob[rp.o_links + 16 * l + 12] = (uint32_t)r->links[l].parent;
-        blob[rp.o_links + 16 * l + 13] = (uint32_t)r->links[l].type;
-        blob[rp.o_links + 16 * l + 14] = (uint32_t)r->links[l].dof;
+    for (int f = 0; f < NF; ++f) {
+        for (int i = 0; i < 12; ++i) fput(rp.o_links + 16 * f + i, (float)fC[f][i]);
+        blob[rp.o_links + 16 * f + 12] = (uint32_t)fparent[f];
+        blob[rp.o_links + 16 * f + 13] = (uint32_t)ftype[f];
+        blob[rp.o_links + 16 * f + 14] = (uint32_t)fdof[f];
     }
+    for (int i = 0; i < 12; ++i) fput(rp.o_eeoff + i, (float)eeoff[i]);
     for (int k = 0; k < M; ++k) {
         const int m = ord[k];
-        for (int i = 0; i < 4; ++i) fput(rp.o_sph + 4 * k + i, r->spheres[4 * m + i]);
-        blob[rp.o_sphlink + k] = (uint32_t)r->sphere_link[m];
+        for (int i = 0; i < 3; ++i) fput(rp.o_sph + 4 * k + i, (float)scen[m][i]);
+        fput(rp.o_sph + 4 * k + 3, r->spheres[4 * m + 3]);
+        blob[rp.o_sphlink + k] = (uint32_t)sframe[m];
         blob[rp.o_perm + k] = (uint32_t)m;
     }
-    for (int l = 0, k = 0; l <= L; ++l) {
-        while (k < M && r->sphere_link[ord[k]] < l) ++k;
-        blob[rp.o_sbeg + l] = (uint32_t)k;
+    for (int f = 0, k = 0; f <= NF; ++f) {
+        while (k < M && sframe[ord[k]] < f) ++k;
+        blob[rp.o_sbeg + f] = (uint32_t)k;
     }
     for (int k = 0; k < M; ++k) fput(rp.o_rself + k, rself[k]);
     for (size_t i = 0; i < bk.size(); ++i) blob[rp.o_blocks + i] = bk[i];
@@ -852,16 +910,16 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         fput(rp.o_lim + d, r->pos_lo[d]); fput(rp.o_lim + D + d, r->pos_hi[d]);
         fput(rp.o_lim + 2 * D + d, r->vel_max[d]); fput(rp.o_lim + 3 * D + d, r->acc_max[d]);
         fput(rp.o_lim + 4 * D + d, r->jerk_max[d]);
-        blob[rp.o_doflink + d] = (uint32_t)doflink[d];
+        blob[rp.o_doflink + d] = (uint32_t)frame_of[doflink[d]];
     }
-    for (int l = 0; l < L; ++l) {   // descendant masks: walk every later link up towards l
-        uint32_t m = 1u << l;
-        for (int c2 = l + 1; c2 < L; ++c2) {
+    for (int f = 0; f < NF; ++f) {   // descendant masks over frames: walk every later frame up towards f
+        uint32_t m = 1u << f;
+        for (int c2 = f + 1; c2 < NF; ++c2) {
             int a = c2;
-            while (a > l) a = r->links[a].parent;
-            if (a == l) m |= 1u << c2;
+            while (a > f) a = fparent[a];
+            if (a == f) m |= 1u << c2;
         }
-        blob[rp.o_desc + l] = m;
+        blob[rp.o_desc + f] = m;
     }
     cudaFree(ctx->d_robot);
     ctx->d_robot = nullptr;
