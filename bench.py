@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config-3 (IK) and config-5 (dense) side metrics")
     return ap.parse_args()
 
 
@@ -191,6 +192,66 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _timed_solves(ctx, sp, seeds, goal, start, env, steps, flush, world, dev):
+    import torch
+    import torch.distributed as dist
+    from paper_2310_17274_b200 import parallel
+    ctx.solve(sp, seeds, goal, start=start, env=env)          # warm-up
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ctx.solve(sp, seeds, goal, start=start, env=env)
+        b.record()
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    if world > 1:
+        tot = parallel.max_over_ranks(tot, dev)
+    return tot / steps
+
+
+def side_metrics(local, rank, world, dev, flush, steps=2):
+    """The other metrics of BASELINE.json on their own configs (device-timed, max over ranks):
+    config 3 -- collision-free IK, 1000 goals x 30 Halton seeds, 100 iterations, one shared K = 20
+    scene (IK queries/s = goals / solve time); config 5 sample -- Franka vs K = 1000 dense cuboids,
+    swept + speed, 16 problems x 32 seeds x 32 timesteps x 100 iterations per GPU."""
+    import torch
+    from paper_2310_17274_b200 import native, workload
+    out = {}
+    n_ik = 1000
+    lo = rank * n_ik
+    wl = workload.franka_ik(local, list(range(lo, lo + n_ik)), S=30, iters=100)
+    ctx = native.Context(local)
+    ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
+    ms = _timed_solves(ctx, wl.solver, torch.tensor(wl.seeds, device=dev), torch.tensor(wl.goal, device=dev), None,
+                       torch.tensor(wl.env, device=dev), steps, flush, world, dev)
+    out["cfg3_ik"] = {"goals_per_gpu": n_ik, "seeds": 30, "iters": 100, "ms_per_solve": ms,
+                      "ik_queries_per_s": n_ik * world / (ms * 1e-3),
+                      "evals_per_s": wl.evals_per_solve() * world / (ms * 1e-3),
+                      "ctas_per_sm": ctx.solver_occupancy(1)[0]}
+    ctx.close()
+    n_dense = 16
+    lo = rank * n_dense
+    wl = workload.franka_to(local, list(range(lo, lo + n_dense)), S=32, H=32, n_boxes=1000, iters=100, dense=True)
+    ctx = native.Context(local)
+    ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
+    ms = _timed_solves(ctx, wl.solver, torch.tensor(wl.seeds, device=dev), torch.tensor(wl.goal, device=dev),
+                       torch.tensor(wl.start, device=dev), torch.tensor(wl.env, device=dev), steps, flush, world, dev)
+    fl = workload.nominal_flops_per_eval(wl)
+    ev = wl.evals_per_solve() * world / (ms * 1e-3)
+    out["cfg5_dense_sample"] = {"problems_per_gpu": n_dense, "seeds": 32, "timesteps": 32, "boxes": 1000,
+                                "iters": 100, "ms_per_solve": ms, "evals_per_s": ev,
+                                "problems_per_s": n_dense * world / (ms * 1e-3), "flops_per_eval": fl,
+                                "achieved_tflops": ev / world * fl / 1e12,
+                                "ctas_per_sm": ctx.solver_occupancy(32)[0]}
+    ctx.close()
+    return out
+
+
 def run_native(args):
     import torch
     import torch.distributed as dist
@@ -290,6 +351,11 @@ def run_native(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl)
 
+    extras = None
+    if not args.no_extras:
+        extras = {"to_problems_per_s": P * world / (total_ms / args.steps * 1e-3)}
+        extras.update(side_metrics(local, rank, world, dev, flush))
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -307,7 +373,8 @@ def run_native(args):
                              "peak_basis": f"register-operand FFMA: 148 SMs x 64 FFMA/clk x 2 flops x {sm_max:.0f} MHz "
                                            "(sm_max_mhz of MEASURED_PEAKS.json); measured 37.3 TF by tools/ffma_peak.cu; "
                                            "the 128-lane unit count (74.4 TF) needs immediate-operand FFMA"},
-                "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches}
+                "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+                "extras": extras}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
