@@ -37,7 +37,7 @@ struct RobotPack {
     int o_rself;    // M floats: self-collision radius r + o (Alg. 9)
     int o_blocks;   // NB x uint2: pair block (ia | (na-1) << 9 | jb << 11 | len << 20, rank base):
                     //   the pairs {ia..ia+na-1} x {jb..jb+len-1}, all in S (na <= 4)
-    int o_wblk;     // NW+1 ints: blocks of warp w are [wblk[w], wblk[w+1]) (balanced on the host)
+    int NB;         // number of pair blocks (stored in decreasing cost order: a work queue)
     int o_rank;     // u16 ranks in S of the block pairs, [block][u][v] from the block's rank base
     int o_lim;      // 5 x D floats: lo, hi, vmax, amax, jmax
     int o_doflink;  // D ints: link carrying dof d
@@ -546,6 +546,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = rp.D, H = cf.H, XS = kp.lay.XS;
     const float *lim = s.fw + rp.o_lim;
+    if (tid == 0) reinterpret_cast<int *>(s.scal + 4)[0] = 0;   // work-queue counter (read after 2 barriers)
 
     // ---- a2: state map (O2, Table 5 last row) into xs[D][H+5] and the slot configurations
     if (MODE == MODE_TO) {
@@ -572,8 +573,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         }
         __syncthreads();
     } else {
-        prep_sincos(s, D);
-        __syncthreads();
+        __syncthreads();   // IK: the caller filled q_cfg and its sin / cos (prep_sincos or fused)
     }
 
     // ---- a3: forward kinematics: warps 0..2 walk the chain (after this, lt is dead and holds sg)
@@ -618,142 +618,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     fk_place(rp, s);
     __syncthreads();
 
-    // ---- a4: self-collision (Eq. self-collision, Alg. 9).  S is stored as rectangular blocks of
-    // pairs {ia..ia+na-1} x {jb..jb+len-1} (spheres of one link share their partner ranges); each
-    // warp walks its blocks holding the na <= 4 first spheres in registers and streaming the
-    // partners, lane = slot.  Screen: d^2 - R^2 = -2 (w_i.w_j + r_i r_j + hb_i + hb_j) with
-    // hb = -(|w|^2 - r^2)/2 precomputed per sphere (5 FMA per pair); it is conservative (slack
-    // 1e-5 m^2 >> fp32 rounding) and every flagged pair is re-tested exactly.  Ties go to the lowest
-    // rank in S (first maximal pair, A28).
-    {
-        float best = 0.f;
-        int brank = 0x7fffffff, bij = -1;
-        const uint2 *blk = reinterpret_cast<const uint2 *>(s.iw + rp.o_blocks);
-        const float *rself = s.fw + rp.o_rself;
-        const unsigned short *rk = reinterpret_cast<const unsigned short *>(s.iw + rp.o_rank);
-        const int b0 = s.iw[rp.o_wblk + warp], b1 = s.iw[rp.o_wblk + warp + 1];
-        for (int bi = b0; bi < b1; ++bi) {
-            const uint2 B = blk[bi];
-            const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff,
-                      len = (B.x >> 20) & 0x1ff;
-            float4 wi[4];
-            float ri[4], ha[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = u < na ? ia + u : ia;
-                wi[u] = s.sw[i * NC + lane];
-                ri[u] = rself[i];
-                ha[u] = u < na ? wi[u].w : -1e30f;
-            }
-            const float4 *wjp = s.sw + jb * NC + lane;
-#pragma unroll 2
-            for (int v = 0; v < len; ++v) {
-                const float4 wj = wjp[v * NC];
-                const float rj = rself[jb + v];
-                float g[4];
-                bool any = false;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {     // common path: the screen only
-                    g[u] = fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, ha[u] + wj.w))));
-                    any |= g[u] > -1e-5f;
-                }
-                if (any) {                        // rare path: exact test of the flagged pairs
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        if (!(g[u] > -1e-5f)) continue;
-                        const float R = ri[u] + rj;
-                        const float dx = wi[u].x - wj.x, dy = wi[u].y - wj.y, dz = wi[u].z - wj.z;
-                        const float d2 = dx * dx + dy * dy + dz * dz;
-                        if (!(d2 < R * R)) continue;
-                        const float pen = R - sqrtf(d2);
-                        if (pen >= best && pen > 0.f) {
-                            const int rank = rk[B.y + u * len + v];
-                            if (pen > best || rank < brank) {
-                                best = pen; brank = rank; bij = (ia + u) | ((jb + v) << 9);
-                            }
-                        }
-                    }
-                }
-            }
-        }
-        s.sbest[warp * NC + lane] = best;
-        s.srank[warp * NC + lane] = brank;
-        s.sij[warp * NC + lane] = bij;
-    }
-
-    // ---- a5/a6: world collision, discrete + swept + speed (Eq. world-collision-cost).  Each thread
-    // carries four spheres (m0 + u NW, u < 4) of its slot through one scan of the cuboids.
-    {
-        float wsum = 0.f;
-        const bool to = MODE == MODE_TO;
-        const bool sweepf = to && (cf.flags & F_SWEEP);
-        const bool speedf = to && (cf.flags & F_SPEED);
-        const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
-        const bool hasp = to && lane > 0 && lane < H;
-        const bool hasn = to && lane + 1 < H;
-        for (int m0 = warp; m0 < rp.M; m0 += 4 * NW) {
-            float cx[4], cy[4], cz[4], th2[4], sp[4];
-            int dirs[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int m = m0 + u * NW;
-                cx[u] = 0.f; cy[u] = 0.f; cz[u] = 0.f; th2[u] = -1.f; sp[u] = 0.f; dirs[u] = 0;
-                if (m < rp.M) {
-                    const float4 *p = s.sw + m * NC + lane;
-                    const float4 c = p[0];
-                    cx[u] = c.x; cy[u] = c.y; cz[u] = c.z;
-                    s.sg[m * NC + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    float spd = 1.f;
-                    if (speedf) {   // A13: central difference, missing neighbour -> w_h
-                        const float4 a = hasp ? p[-1] : c, z = hasn ? p[1] : c;
-                        const float dx = z.x - a.x, dy = z.y - a.y, dz = z.z - a.z;
-                        spd = sqrtf(dx * dx + dy * dy + dz * dz) * cf.inv_2dt;
-                    }
-                    sp[u] = spd;
-                    const float r = sph[m].w;
-                    const float rpr = r + cf.eta;   // Alg. 10 "sph.radius += eta"
-                    float maxb2;
-                    dirs[u] = sweep_dirs(p, c.x, c.y, c.z, rpr, hasp, hasn, sweepf, maxb2);
-                    // r < 0 disables the sphere; sp = 0 => C_w = 0 exactly
-                    if (r >= 0.f && spd != 0.f) th2[u] = fmaxf(rpr * rpr, maxb2);
-                }
-            }
-            if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
-                for (int k = 0; k < K; ++k) {
-                    const BoxView b = load_box(s.boxes, k);
-                    float s2[4];
-                    bool any = false;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        s2[u] = box_screen(cx[u], cy[u], cz[u], b);
-                        any |= s2[u] < th2[u];
-                    }
-                    if (any) {                    // rare path, one out-of-line copy for all spheres
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            if (!(s2[u] < th2[u])) continue;
-                            const int m = m0 + u * NW;
-                            box_slow(s.sg + m * NC + lane, s.sw + m * NC + lane, s.boxes, k, cx[u], cy[u], cz[u],
-                                     s2[u], sph[m].w + cf.eta, dirs[u], cf.eta, cf.inv_eta, cf.sweep_steps);
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int m = m0 + u * NW;
-                if (m < rp.M) {
-                    const float sc = cf.beta_world * sp[u];
-                    float4 g = s.sg[m * NC + lane];
-                    wsum += sc * g.w;
-                    s.sg[m * NC + lane] = make_float4(sc * g.x, sc * g.y, sc * g.z, 0.f);
-                }
-            }
-        }
-        s.wpart[warp * NC + lane] = wsum;
-    }
-
-    // ---- a7: pose cost (Eq. pose_cost_term, A1) at the terminal slot (TO) / every slot (IK)
+    // ---- a7: pose cost (Eq. pose_cost_term, A1) at the terminal slot (TO) / every slot (IK); the
+    // last warp does it before joining the work queue below
     if (warp == NW - 1) {
         const int c = lane;
         const bool on = (MODE == MODE_TO) ? (c == H - 1) : (c < n_act);
@@ -789,6 +655,150 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         for (int k = 0; k < 6; ++k) s.pose_ft[k * NC + c] = ft[k];
         s.pose_c[c] = C;
     }
+
+    // ---- a4 + a5/a6: self-collision and world collision as ONE dynamic work queue.  Items are the
+    // world groups (4 consecutive spheres, all cuboids) followed by the self-collision pair blocks
+    // in decreasing cost order; warps take items from a shared counter, so data-dependent costs
+    // (hits, sweeps, penetrating pairs) balance across warps.  Each warp keeps its own partial
+    // (self best, world sum) and the merge below combines them in fixed warp order: the result
+    // does not depend on which warp took which item.
+    {
+        // self (Eq. self-collision, Alg. 9): block {ia..ia+na-1} x {jb..jb+len-1} of S, na <= 4
+        // first spheres in registers, partners streamed, lane = slot.  Screen: d^2 - R^2 =
+        // -2 (w_i.w_j + r_i r_j + hb_i + hb_j), hb = -(|w|^2 - r^2)/2 per sphere (5 FMA per pair),
+        // conservative (slack 1e-5 m^2 >> fp32 rounding); flagged pairs are re-tested exactly.  Ties
+        // go to the lowest rank in S (first maximal pair, A28).
+        float best = 0.f;
+        int brank = 0x7fffffff, bij = -1;
+        const uint2 *blk = reinterpret_cast<const uint2 *>(s.iw + rp.o_blocks);
+        const float *rself = s.fw + rp.o_rself;
+        const unsigned short *rk = reinterpret_cast<const unsigned short *>(s.iw + rp.o_rank);
+        // world (Alg. 10 + Algs. 11-12, Eq. world-collision-cost): each thread carries the 4
+        // spheres of a group at its slot through one scan of the cuboids
+        float wsum = 0.f;
+        const bool to = MODE == MODE_TO;
+        const bool sweepf = to && (cf.flags & F_SWEEP);
+        const bool speedf = to && (cf.flags & F_SPEED);
+        const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
+        const bool hasp = to && lane > 0 && lane < H;
+        const bool hasn = to && lane + 1 < H;
+        const int nwg = (rp.M + 3) >> 2, nitems = nwg + rp.NB;
+        int *qctr = reinterpret_cast<int *>(s.scal + 4);
+        for (;;) {
+            int item = 0;
+            if (lane == 0) item = atomicAdd(qctr, 1);
+            item = __shfl_sync(FULL, item, 0);
+            if (item >= nitems) break;
+            if (item < nwg) {
+                const int m0 = item << 2;
+                float cx[4], cy[4], cz[4], th2[4], sp[4];
+                int dirs[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int m = m0 + u;
+                    cx[u] = 0.f; cy[u] = 0.f; cz[u] = 0.f; th2[u] = -1.f; sp[u] = 0.f; dirs[u] = 0;
+                    if (m < rp.M) {
+                        const float4 *p = s.sw + m * NC + lane;
+                        const float4 c = p[0];
+                        cx[u] = c.x; cy[u] = c.y; cz[u] = c.z;
+                        s.sg[m * NC + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        float spd = 1.f;
+                        if (speedf) {   // A13: central difference, missing neighbour -> w_h
+                            const float4 a = hasp ? p[-1] : c, z = hasn ? p[1] : c;
+                            const float dx = z.x - a.x, dy = z.y - a.y, dz = z.z - a.z;
+                            spd = sqrtf(dx * dx + dy * dy + dz * dz) * cf.inv_2dt;
+                        }
+                        sp[u] = spd;
+                        const float r = sph[m].w;
+                        const float rpr = r + cf.eta;   // Alg. 10 "sph.radius += eta"
+                        float maxb2;
+                        dirs[u] = sweep_dirs(p, c.x, c.y, c.z, rpr, hasp, hasn, sweepf, maxb2);
+                        // r < 0 disables the sphere; sp = 0 => C_w = 0 exactly
+                        if (r >= 0.f && spd != 0.f) th2[u] = fmaxf(rpr * rpr, maxb2);
+                    }
+                }
+                if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
+                    for (int k = 0; k < K; ++k) {
+                        const BoxView b = load_box(s.boxes, k);
+                        float s2[4];
+                        bool any = false;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            s2[u] = box_screen(cx[u], cy[u], cz[u], b);
+                            any |= s2[u] < th2[u];
+                        }
+                        if (any) {                    // rare path, one out-of-line copy for all spheres
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                if (!(s2[u] < th2[u])) continue;
+                                const int m = m0 + u;
+                                box_slow(s.sg + m * NC + lane, s.sw + m * NC + lane, s.boxes, k, cx[u], cy[u], cz[u],
+                                         s2[u], sph[m].w + cf.eta, dirs[u], cf.eta, cf.inv_eta, cf.sweep_steps);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int m = m0 + u;
+                    if (m < rp.M) {
+                        const float sc = cf.beta_world * sp[u];
+                        float4 g = s.sg[m * NC + lane];
+                        wsum += sc * g.w;
+                        s.sg[m * NC + lane] = make_float4(sc * g.x, sc * g.y, sc * g.z, 0.f);
+                    }
+                }
+            } else {
+                const uint2 B = blk[item - nwg];
+                const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff,
+                          len = (B.x >> 20) & 0x1ff;
+                float4 wi[4];
+                float ri[4], ha[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = u < na ? ia + u : ia;
+                    wi[u] = s.sw[i * NC + lane];
+                    ri[u] = rself[i];
+                    ha[u] = u < na ? wi[u].w : -1e30f;
+                }
+                const float4 *wjp = s.sw + jb * NC + lane;
+#pragma unroll 2
+                for (int v = 0; v < len; ++v) {
+                    const float4 wj = wjp[v * NC];
+                    const float rj = rself[jb + v];
+                    float g[4];
+                    bool any = false;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {     // common path: the screen only
+                        g[u] = fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, ha[u] + wj.w))));
+                        any |= g[u] > -1e-5f;
+                    }
+                    if (any) {                        // rare path: exact test of the flagged pairs
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (!(g[u] > -1e-5f)) continue;
+                            const float R = ri[u] + rj;
+                            const float dx = wi[u].x - wj.x, dy = wi[u].y - wj.y, dz = wi[u].z - wj.z;
+                            const float d2 = dx * dx + dy * dy + dz * dz;
+                            if (!(d2 < R * R)) continue;
+                            const float pen = R - sqrtf(d2);
+                            if (pen >= best && pen > 0.f) {
+                                const int rank = rk[B.y + u * len + v];
+                                if (pen > best || rank < brank) {
+                                    best = pen; brank = rank; bij = (ia + u) | ((jb + v) << 9);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        s.sbest[warp * NC + lane] = best;
+        s.srank[warp * NC + lane] = brank;
+        s.sij[warp * NC + lane] = bij;
+        s.wpart[warp * NC + lane] = wsum;
+    }
+
     __syncthreads();
 
     // ---- a10 (per slot): merge self-collision, apply its gradient, per-slot costs and the total

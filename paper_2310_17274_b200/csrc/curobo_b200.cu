@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             s.q_cfg[d * NC + lane] = v;
         }
     __syncthreads();
+    prep_sincos(s, D);
     // single eval_pass call site: pass 0 = Theta_0, then (L-BFGS step, A candidates) per iteration
     float c = 0.f, cbest = 0.f, g0d = 0.f;
     int cnt = 0, fs = 0;
@@ -297,10 +298,16 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             for (int d = 0; d < D; ++d) { dd[d * NC + lane] = -q[d]; g0d += g[d * NC + lane] * (-q[d]); }
         }
         if (a >= 0) {
-            if (warp == 0)
-                for (int d = 0; d < D; ++d)
-                    s.q_cfg[d * NC + lane] = candidate(th[d * NC + lane], kp.alpha[a], dd[d * NC + lane], lim[d], lim[D + d]);
-            __syncthreads();
+            if (a == 0) __syncthreads();   // the L-BFGS step (warp 0) wrote the directions
+            for (int idx = t; idx < DC; idx += NT) {   // all threads: candidate + its sin / cos
+                const int d = idx / NC;
+                const float v = candidate(th[idx], kp.alpha[a], dd[idx], lim[d], lim[D + d]);
+                s.q_cfg[idx] = v;
+                float sn, cs;
+                sincosf(v, &sn, &cs);
+                s.scs[idx] = sn;
+                s.scs[DC + idx] = cs;
+            }
         }
         eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
         if (warp != 0) continue;
@@ -386,6 +393,7 @@ __global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ 
         for (int k = 0; k < 7; ++k) s.goal[k * NC + lane] = act ? kp.goal[(size_t)(b0 + lane) * 7 + k] : (k == 3 ? 1.f : 0.f);
     }
     __syncthreads();
+    prep_sincos(s, D);
     eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
     if (warp == 0 && lane < n_act) {
         const int b = b0 + lane;
@@ -845,37 +853,25 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
                 blks.push_back({a, na, jb, std::min(511, rn.second - jb)});
         a += na;
     }
-    // LPT balance of the blocks over the NW warps (cost ~ len * (2 + 9 na) instructions)
+    // work-queue order: decreasing cost (~ len * (2 + 9 na) instructions), ties by position
     std::vector<int> bord(blks.size());
     for (size_t i = 0; i < blks.size(); ++i) bord[i] = (int)i;
     std::stable_sort(bord.begin(), bord.end(), [&](int x, int y) {
         return blks[x].len * (2 + 9 * blks[x].na) > blks[y].len * (2 + 9 * blks[y].na);
     });
-    std::vector<long> load(NW, 0);
-    std::vector<std::vector<int>> per_warp(NW);
-    for (int bi : bord) {
-        const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-        load[w] += (long)blks[bi].len * (2 + 9 * blks[bi].na);
-        per_warp[w].push_back(bi);
-    }
-    std::vector<uint32_t> bk, wblk(NW + 1, 0);
+    std::vector<uint32_t> bk;
     std::vector<uint16_t> ranks;
-    for (int w = 0; w < NW; ++w) {
-        std::sort(per_warp[w].begin(), per_warp[w].end());
-        wblk[w] = (uint32_t)(bk.size() / 2);
-        for (int bi : per_warp[w]) {
-            const Blk &b = blks[bi];
-            bk.push_back((uint32_t)b.ia | ((uint32_t)(b.na - 1) << 9) | ((uint32_t)b.jb << 11) | ((uint32_t)b.len << 20));
-            bk.push_back((uint32_t)ranks.size());
-            for (int u = 0; u < b.na; ++u)
-                for (int v = 0; v < b.len; ++v) ranks.push_back((uint16_t)rank_of[(size_t)(b.ia + u) * M + b.jb + v]);
-        }
+    for (int bi : bord) {
+        const Blk &b = blks[bi];
+        bk.push_back((uint32_t)b.ia | ((uint32_t)(b.na - 1) << 9) | ((uint32_t)b.jb << 11) | ((uint32_t)b.len << 20));
+        bk.push_back((uint32_t)ranks.size());
+        for (int u = 0; u < b.na; ++u)
+            for (int v = 0; v < b.len; ++v) ranks.push_back((uint16_t)rank_of[(size_t)(b.ia + u) * M + b.jb + v]);
     }
-    wblk[NW] = (uint32_t)(bk.size() / 2);
+    rp.NB = (int)blks.size();
     rp.P = npairs;
     rp.o_rself = w; w += r4(M);
     rp.o_blocks = w; w += r4((int)bk.size());
-    rp.o_wblk = w; w += r4(NW + 1);
     rp.o_rank = w; w += r4(((int)ranks.size() + 1) / 2);
     rp.o_lim = w; w += r4(5 * D);
     rp.o_doflink = w; w += r4(D);
@@ -904,7 +900,6 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
     }
     for (int k = 0; k < M; ++k) fput(rp.o_rself + k, rself[k]);
     for (size_t i = 0; i < bk.size(); ++i) blob[rp.o_blocks + i] = bk[i];
-    for (int i = 0; i <= NW; ++i) blob[rp.o_wblk + i] = wblk[i];
     if (!ranks.empty()) memcpy(&blob[rp.o_rank], ranks.data(), ranks.size() * 2);
     for (int d = 0; d < D; ++d) {
         fput(rp.o_lim + d, r->pos_lo[d]); fput(rp.o_lim + D + d, r->pos_hi[d]);
