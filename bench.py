@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the config-3 (IK) and config-5 (dense) side metrics")
+    ap.add_argument("--shard", default="problem", choices=["problem", "seed"],
+                    help="problem: each rank owns its own problems (weak scaling, no collective); seed: every rank "
+                         "solves its seed block of the SAME problems, then C1 all_reduce(MIN) of packed keys + C2 "
+                         "all_gather of winners (strong scaling)")
     return ap.parse_args()
 
 
@@ -264,8 +268,16 @@ def run_native(args):
     from paper_2310_17274_b200 import native, parallel, workload
 
     P = args.problems
-    lo = rank * P
-    wl = workload.franka_to(local, list(range(lo, lo + P)), S=32, H=32, iters=args.iters)
+    S_total = 32
+    seed_mode = args.shard == "seed"
+    if seed_mode:
+        s_lo, s_hi = parallel.seed_block(S_total, world, rank)
+        wl = workload.franka_to(local, list(range(P)), S=S_total, H=32, iters=args.iters)
+        wl.seeds = np.ascontiguousarray(wl.seeds[:, s_lo:s_hi])
+    else:
+        s_lo = 0
+        lo = rank * P
+        wl = workload.franka_to(local, list(range(lo, lo + P)), S=S_total, H=32, iters=args.iters)
     ctx = native.Context(local)
     ctx.set_robot(wl.robot)
     ctx.set_world(wl.worlds)
@@ -279,8 +291,15 @@ def run_native(args):
     evals_per_step = wl.evals_per_solve()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
+    def step():
+        out = ctx.solve(sp, seeds, goal, start=start, env=env, seed_base=s_lo)
+        if seed_mode:   # the real exchange step of seed sharding: C1 + C2
+            out["best_key"], out["best_traj"], out["best_cost"] = parallel.merge_seed_sharded(
+                out["best_key"], out["best_traj"], S_total)
+        return out
+
     for _ in range(args.warmup):
-        ctx.solve(sp, seeds, goal, start=start, env=env)
+        step()
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
@@ -293,7 +312,7 @@ def run_native(args):
         for k in range(args.steps):
             flush.zero_()                       # L2 flush, outside the timed events
             evs[k][0].record(stream)
-            out = ctx.solve(sp, seeds, goal, start=start, env=env)
+            out = step()
             evs[k][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -303,7 +322,7 @@ def run_native(args):
     total_ms = sum(step_ms)
     if world > 1:
         total_ms = parallel.max_over_ranks(total_ms, dev)
-    evals_all = evals_per_step * args.steps * world
+    evals_all = evals_per_step * args.steps * world   # seed mode: evals_per_step counts this rank's seeds
     value = evals_all / (total_ms * 1e-3)
 
     # ---- roofline of the dominant kernel (solve_to_kernel; the select kernel is ~us).  FP32 peak for
@@ -331,7 +350,18 @@ def run_native(args):
         he = env.cpu().pin_memory()
         hb = torch.empty(P, 32, 7).pin_memory(); hc = torch.empty(P).pin_memory()
         hk = torch.empty(P, dtype=torch.int64).pin_memory()
-        ctx.solve_host(sp, hs, hg, start=hst, env=he, best_traj=hb, best_cost=hc, best_key=hk)
+
+        def e2e_step():
+            if not seed_mode:   # one C-ABI call: H2D, solve, D2H, synchronise
+                ctx.solve_host(sp, hs, hg, start=hst, env=he, best_traj=hb, best_cost=hc, best_key=hk)
+                return
+            seeds.copy_(hs, non_blocking=True); goal.copy_(hg, non_blocking=True)
+            start.copy_(hst, non_blocking=True); env.copy_(he, non_blocking=True)
+            out = step()
+            hb.copy_(out["best_traj"]); hc.copy_(out["best_cost"]); hk.copy_(out["best_key"])
+            torch.cuda.synchronize()
+
+        e2e_step()
         tt = 0.0
         for k in range(args.steps):
             flush.zero_()
@@ -339,7 +369,7 @@ def run_native(args):
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            ctx.solve_host(sp, hs, hg, start=hst, env=he, best_traj=hb, best_cost=hc, best_key=hk)
+            e2e_step()
             tt += time.perf_counter() - t0
         if world > 1:
             tt = parallel.max_over_ranks(tt, dev)
@@ -359,14 +389,18 @@ def run_native(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": "cfg2_franka_to_batched", "problems_per_gpu": P, "global_problems": P * world,
+                "scaling": "strong" if seed_mode else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "cfg2_franka_to_batched", "problems_per_gpu": P,
+                           "global_problems": P if seed_mode else P * world,
+                           "seeds_per_gpu": int(wl.seeds.shape[1]),
                            "seeds": 32, "timesteps": 32, "dof": 7, "spheres": 64, "self_pairs": int(len(wl.robot.pairs)),
                            "boxes": 20, "iters": args.iters, "line_search": list(sp.alpha), "history": sp.history,
                            "flags": "sweep+speed", "evals_per_step_per_gpu": evals_per_step,
                            "ctas_per_sm": ctas_per_sm, "smem_bytes_per_cta": smem_per_cta,
                            "l2": "flushed between timed steps (256 MB write, outside the events)",
-                           "parallelism": f"problem-sharded x{world}, no data-path collective"},
+                           "parallelism": (f"seed-sharded x{world}: C1 all_reduce(MIN) of packed keys + C2 all_gather "
+                                           f"of winners inside the timed step") if seed_mode else
+                                          f"problem-sharded x{world}, no data-path collective"},
                 "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                              "frac": achieved_tf / peak_tf, "traffic": traffic,
                              "kernel": "solve_to_kernel", "flops_per_eval": flops_eval,
