@@ -263,7 +263,7 @@ def run_native(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    if world > 1:
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:   # launched by torchrun (any world size)
         dist.init_process_group("nccl", device_id=dev)
     from paper_2310_17274_b200 import native, parallel, workload
 
@@ -293,7 +293,7 @@ def run_native(args):
 
     def step():
         out = ctx.solve(sp, seeds, goal, start=start, env=env, seed_base=s_lo)
-        if seed_mode:   # the real exchange step of seed sharding: C1 + C2
+        if seed_mode and dist.is_initialized():   # the real exchange step of seed sharding: C1 + C2
             out["best_key"], out["best_traj"], out["best_cost"] = parallel.merge_seed_sharded(
                 out["best_key"], out["best_traj"], S_total)
         return out
@@ -411,7 +411,7 @@ def run_native(args):
                 "extras": extras}
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
