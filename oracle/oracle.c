@@ -701,6 +701,107 @@ int orc_argmin_f32(int n, const float *c) {
     return best;
 }
 
+/* ------------------------------------------------------------------------------------------ */
+/* O11 particle-based warm-up (§4.2 "Particle-Based Optimization"; Alg. 5,          */
+/* P:2130-2144; two iterations before L-BFGS)                                          */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Counter-based generator for the particle draws (reading B9).  Philox4x32-10 as published by
+ * Salmon et al. (SC'11): 10 rounds of two 32x32->64 multiplies with M0 = 0xD2511F53,
+ * M1 = 0xCD9E8D57, the key bumped by the Weyl constants W0 = 0x9E3779B9, W1 = 0xBB67AE85 after
+ * every round.  Pinned by the published known-answer vectors (tests/test_oracle_particle.py). */
+void orc_philox4x32(const unsigned key[2], const unsigned ctr[4], unsigned out[4]) {
+    unsigned k0 = key[0], k1 = key[1];
+    unsigned x0 = ctr[0], x1 = ctr[1], x2 = ctr[2], x3 = ctr[3];
+    for (int r = 0; r < 10; ++r) {
+        unsigned long long p0 = (unsigned long long)0xD2511F53u * x0;
+        unsigned long long p1 = (unsigned long long)0xCD9E8D57u * x2;
+        unsigned hi0 = (unsigned)(p0 >> 32), lo0 = (unsigned)p0;
+        unsigned hi1 = (unsigned)(p1 >> 32), lo1 = (unsigned)p1;
+        unsigned y0 = hi1 ^ x1 ^ k0, y1 = lo1, y2 = hi0 ^ x3 ^ k1, y3 = lo0;
+        x0 = y0; x1 = y1; x2 = y2; x3 = y3;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+/* theta_s ~ N(0, 1) for variable `var` of particle `particle` in iteration `iter` of a seed
+ * (B9): Philox(key = (key0, key1), ctr = (var / 4, particle, iter, seed)) gives 4 words; words
+ * (0,1) and (2,3) are two Box-Muller pairs with 24-bit uniforms u1 = (w_a >> 8 + 1) 2^-24 in
+ * (0, 1], u2 = (w_b >> 8) 2^-24 in [0, 1): z = sqrt(-2 ln u1) (cos | sin)(2 pi u2); variable
+ * var takes output var % 4 (cos for even, sin for odd). */
+double orc_normal(unsigned key0, unsigned key1, unsigned var, unsigned particle, unsigned iter,
+                  unsigned seed) {
+    unsigned key[2] = {key0, key1}, ctr[4] = {var >> 2, particle, iter, seed}, w[4];
+    orc_philox4x32(key, ctr, w);
+    int j = (int)(var & 3u), a = (j >> 1) * 2;
+    double u1 = ((double)(w[a] >> 8) + 1.0) / 16777216.0;
+    double u2 = (double)(w[a + 1] >> 8) / 16777216.0;
+    double r = sqrt(-2.0 * log(u1));
+    const double two_pi = 6.283185307179586476925286766559;
+    return (j & 1) ? r * sin(two_pi * u2) : r * cos(two_pi * u2);
+}
+
+/* Alg. 5: mu <- Theta_init, sigma <- sigma_0; for each iteration: Theta_l <- SAMPLE(mu, sigma)
+ * (theta_l = mu + sqrt(Theta_sigma) * theta_s, clipped to the box constraints, B7);
+ * c_l <- C(Theta_l) (cost only); UPDATE: c = -C/beta, w = e^{c_i} / sum e^{c_i} (the max is
+ * subtracted first: the same ratio), Eq. particle_1 mu = (1-k_mu) mu + k_mu sum_i w_i theta_i,
+ * Eq. particle_2 as read in B6: sigma = (1-k_sigma) sigma + k_sigma sum_i w_i (theta_i - mu_prev)^2
+ * (diagonal covariance).  A non-finite cost gets weight 0; if every weight is 0 the iteration
+ * leaves (mu, sigma) unchanged (B10).  cost_trace[it * n + l] = c_l (may be NULL). */
+void orc_particle_solve(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
+                        const double *hi, const orc_particle *pp, unsigned problem,
+                        unsigned seed, double *mu, double *var, double *cost_trace) {
+    int L = pp->n;
+    double *theta = malloc(sizeof(double) * (size_t)L * n);
+    double *C = malloc(sizeof(double) * L), *w = malloc(sizeof(double) * L);
+    for (int v = 0; v < n; ++v) {
+        double s0 = pp->sigma0_frac * (hi[v] - lo[v]);
+        mu[v] = x0[v];
+        var[v] = s0 * s0;
+    }
+    for (int it = 0; it < pp->iters; ++it) {
+        /* SAMPLE */
+        for (int l = 0; l < L; ++l)
+            for (int v = 0; v < n; ++v) {
+                double z = orc_normal(pp->key, problem, (unsigned)v, (unsigned)l, (unsigned)it, seed);
+                double x = mu[v] + sqrt(var[v]) * z;
+                if (x < lo[v]) x = lo[v];
+                if (x > hi[v]) x = hi[v];
+                theta[(size_t)l * n + v] = x;
+            }
+        /* C(Theta_l), cost only */
+        for (int l = 0; l < L; ++l) {
+            C[l] = f(ctx, theta + (size_t)l * n, NULL);
+            if (cost_trace) cost_trace[(size_t)it * L + l] = C[l];
+        }
+        /* UPDATE: exponential utility */
+        double cmax = -ORC_INF;
+        for (int l = 0; l < L; ++l) {
+            double cl = -C[l] / pp->beta;
+            if (isfinite(C[l]) && cl > cmax) cmax = cl;
+        }
+        if (!(cmax > -ORC_INF)) continue;            /* B10: no finite particle */
+        double Z = 0.0;
+        for (int l = 0; l < L; ++l) {
+            w[l] = isfinite(C[l]) ? exp(-C[l] / pp->beta - cmax) : 0.0;
+            Z += w[l];
+        }
+        for (int l = 0; l < L; ++l) w[l] /= Z;
+        for (int v = 0; v < n; ++v) {
+            double m1 = 0.0, m2 = 0.0;
+            for (int l = 0; l < L; ++l) {
+                double x = theta[(size_t)l * n + v];
+                m1 += w[l] * x;                                   /* w * theta (Eq. particle_1) */
+                m2 += w[l] * (x - mu[v]) * (x - mu[v]);   /* B6: mu[v] is still Theta_mu-1 here */
+            }
+            mu[v] = (1.0 - pp->k_mu) * mu[v] + pp->k_mu * m1;
+            var[v] = (1.0 - pp->k_sigma) * var[v] + pp->k_sigma * m2;
+        }
+    }
+    free(theta); free(C); free(w);
+}
+
 /* O8 per-seed solver in fp64: evaluate at x0, then `iters` iterations of
  * L-BFGS step -> clipped candidates -> batched evaluation -> selection -> best update. */
 void orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
@@ -796,8 +897,18 @@ static void *solve_worker(void *arg) {
         int p = u / jb->S;
         traj_ctx ctx = {jb->rb, jb->worlds + (jb->env ? jb->env[p] : 0), jb->pr,
                         jb->start ? jb->start + (size_t)p * D : NULL, jb->goal + (size_t)p * 7, jb->H};
-        orc_lbfgs_solve(jb->ik ? ik_fun : traj_fun, &ctx, N, jb->seeds + (size_t)u * N, lo, hi, jb->sp,
+        const double *x0 = jb->seeds + (size_t)u * N;
+        double *mu = NULL, *var = NULL;
+        if (jb->sp->pt.iters > 0) {                   /* O11 warm-up, then L-BFGS from its mean */
+            mu = malloc(sizeof(double) * N); var = malloc(sizeof(double) * N);
+            orc_particle_solve(jb->ik ? ik_fun : traj_fun, &ctx, N, x0, lo, hi, &jb->sp->pt,
+                               (unsigned)(jb->sp->problem_base + p),
+                               (unsigned)(jb->sp->seed_base + (u - p * jb->S)), mu, var, NULL);
+            x0 = mu;
+        }
+        orc_lbfgs_solve(jb->ik ? ik_fun : traj_fun, &ctx, N, x0, lo, hi, jb->sp,
                         jb->out_x + (size_t)u * N, jb->out_c + u, NULL);
+        free(mu); free(var);
     }
     free(lo); free(hi);
     return NULL;

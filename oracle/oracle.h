@@ -50,11 +50,22 @@ typedef struct {
     int flags;                       /* ORC_SWEEP | ORC_SPEED | ORC_JERK                               */
 } orc_params;
 
+/* O11 particle warm-up (Alg. 5; Eqs. particle_1/2 P:192-199; readings B6-B10). */
+typedef struct {
+    int iters;                       /* Alg. 5 N: 2 before L-BFGS; 0 = off               */
+    int n;                           /* particles per iteration (SPEC default 64, no paper value) */
+    double beta, k_mu, k_sigma;      /* c = -C/beta; step sizes of Eqs. particle_1/2              */
+    double sigma0_frac;              /* Theta_sigma0 = (frac * (hi - lo))^2 per variable (B8)     */
+    unsigned key;                    /* Philox4x32-10 key word 0 (word 1 = problem index, B9)     */
+} orc_particle;
+
 typedef struct {
     int iters, history, n_alpha;
     double alpha[8];
     double c1, c2;
     int ls_mode;                     /* 0 armijo, 1 wolfe, 2 strong wolfe (Alg. 1) */
+    orc_particle pt;                 /* warm-up run before L-BFGS by orc_solve_to / orc_solve_ik  */
+    long long problem_base, seed_base;   /* global indices of problem 0 / seed 0 (RNG counters) */
 } orc_solver;
 
 /* O10 instrumentation.  `margin` = the minimum distance of any quantity to a branch point where
@@ -106,6 +117,13 @@ int    orc_ls_select(int A, const double *alpha, double c0, double g0d, const do
 int    orc_ls_select_f32(int A, const float *alpha, float c0, float g0d, const float *ca,
                          const float *gda, float c1, float c2, int mode);
 int    orc_argmin_f32(int n, const float *c);
+/* O11: counter-based generator (Philox4x32-10) and the particle warm-up */
+void   orc_philox4x32(const unsigned key[2], const unsigned ctr[4], unsigned out[4]);
+double orc_normal(unsigned key0, unsigned key1, unsigned var, unsigned particle, unsigned iter,
+                  unsigned seed);
+void   orc_particle_solve(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
+                          const double *hi, const orc_particle *pp, unsigned problem,
+                          unsigned seed, double *mu, double *var, double *cost_trace);
 void   orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
                        const double *hi, const orc_solver *sp, double *best_x, double *best_c,
                        double *trace);

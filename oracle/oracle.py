@@ -56,10 +56,16 @@ class _Params(C.Structure):
                 ("flags", C.c_int)]
 
 
+class _Particle(C.Structure):
+    _fields_ = [("iters", C.c_int), ("n", C.c_int), ("beta", C.c_double), ("k_mu", C.c_double),
+                ("k_sigma", C.c_double), ("sigma0_frac", C.c_double), ("key", C.c_uint)]
+
+
 class _Solver(C.Structure):
     _fields_ = [("iters", C.c_int), ("history", C.c_int), ("n_alpha", C.c_int),
                 ("alpha", C.c_double * 8), ("c1", C.c_double), ("c2", C.c_double),
-                ("ls_mode", C.c_int)]
+                ("ls_mode", C.c_int), ("pt", _Particle), ("problem_base", C.c_longlong),
+                ("seed_base", C.c_longlong)]
 
 
 _FUN = C.CFUNCTYPE(C.c_double, C.c_void_p, D_P, D_P)
@@ -149,10 +155,16 @@ def params(cp):
                    int(cp.flags))
 
 
-def solver(sp):
+def particle(sp):
+    return _Particle(int(sp.particle_iters), int(sp.n_particles), float(sp.particle_beta),
+                     float(sp.k_mu), float(sp.k_sigma), float(sp.sigma0_frac), int(sp.rng_key) & 0xFFFFFFFF)
+
+
+def solver(sp, problem_base=0, seed_base=0):
     al = list(sp.alpha) + [0.0] * (8 - len(sp.alpha))
     return _Solver(int(sp.iters), int(sp.history), len(sp.alpha), (C.c_double * 8)(*al),
-                   float(sp.c1), float(sp.c2), int(sp.ls_mode))
+                   float(sp.c1), float(sp.c2), int(sp.ls_mode), particle(sp), int(problem_base),
+                   int(seed_base))
 
 
 # ---------------------------------------------------------------------------------------------
@@ -328,17 +340,52 @@ def lbfgs_solve(fun, x0, sp, lo=None, hi=None):
     return bx, bc.value, trace
 
 
+def philox4x32(key, ctr):
+    k = (C.c_uint * 2)(*[int(v) & 0xFFFFFFFF for v in key])
+    c = (C.c_uint * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+    o = (C.c_uint * 4)()
+    lib().orc_philox4x32(k, c, o)
+    return [int(v) for v in o]
+
+
+def normal(key0, key1, var, particle_, it, seed):
+    L = lib()
+    L.orc_normal.restype = C.c_double
+    L.orc_normal.argtypes = [C.c_uint] * 6
+    return L.orc_normal(key0 & 0xFFFFFFFF, key1 & 0xFFFFFFFF, var, particle_, it, seed & 0xFFFFFFFF)
+
+
+def particle_solve(fun, x0, sp, lo, hi, problem=0, seed=0):
+    """O11 warm-up. fun(x) -> cost (fp64); returns (mu, var, costs[iters][n])."""
+    x0 = _d(x0)
+    n = x0.shape[0]
+
+    def cb(_ctx, xp, gp):
+        x = np.ctypeslib.as_array(xp, shape=(n,)).copy()
+        return float(fun(x))
+
+    cfun = _FUN(cb)
+    mu = np.zeros(n); var = np.zeros(n)
+    trace = np.zeros((max(sp.particle_iters, 1), sp.n_particles))
+    pp = particle(sp)
+    lib().orc_particle_solve(cfun, None, n, _dp(x0), _dp(_d(np.broadcast_to(lo, (n,)))),
+                             _dp(_d(np.broadcast_to(hi, (n,)))), C.byref(pp), C.c_uint(problem & 0xFFFFFFFF),
+                             C.c_uint(seed & 0xFFFFFFFF), _dp(mu), _dp(var), _dp(trace))
+    return mu, var, trace[:sp.particle_iters]
+
+
 def _worlds_array(worlds):
     arr = (_World * len(worlds))(*[w.s for w in worlds])
     return arr
 
 
-def solve_to(robot: Robot, worlds, env, cp, sp, seeds, start, goal, nthreads=1):
+def solve_to(robot: Robot, worlds, env, cp, sp, seeds, start, goal, nthreads=1, problem_base=0,
+             seed_base=0):
     seeds = _d(seeds)
     P, S, H, D = seeds.shape
     out = np.zeros_like(seeds); cost = np.zeros((P, S))
     warr = _worlds_array(worlds)
-    pr, so = params(cp), solver(sp)
+    pr, so = params(cp), solver(sp, problem_base, seed_base)
     envc = _i(env)
     lib().orc_solve_to.argtypes = [C.POINTER(_Robot), C.POINTER(_World), I_P, C.POINTER(_Params),
                                    C.POINTER(_Solver), C.c_int, C.c_int, C.c_int, D_P, D_P, D_P,
@@ -348,12 +395,12 @@ def solve_to(robot: Robot, worlds, env, cp, sp, seeds, start, goal, nthreads=1):
     return out, cost
 
 
-def solve_ik(robot: Robot, worlds, env, cp, sp, seeds, goal, nthreads=1):
+def solve_ik(robot: Robot, worlds, env, cp, sp, seeds, goal, nthreads=1, problem_base=0, seed_base=0):
     seeds = _d(seeds)
     P, S, D = seeds.shape
     out = np.zeros_like(seeds); cost = np.zeros((P, S))
     warr = _worlds_array(worlds)
-    pr, so = params(cp), solver(sp)
+    pr, so = params(cp), solver(sp, problem_base, seed_base)
     envc = _i(env)
     lib().orc_solve_ik.argtypes = [C.POINTER(_Robot), C.POINTER(_World), I_P, C.POINTER(_Params),
                                    C.POINTER(_Solver), C.c_int, C.c_int, D_P, D_P, C.c_int, D_P, D_P]

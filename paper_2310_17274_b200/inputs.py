@@ -106,6 +106,16 @@ class SolverParams:
     c1: float = 1e-4
     c2: float = 0.9
     ls_mode: int = 2
+    # particle warm-up before L-BFGS (Alg. 5, Eqs. particle_1/2).  The paper runs
+    # 2 iterations but gives no n / beta / k_mu / k_sigma / sigma_0: SPEC defaults
+    # (S:368), non-paper values.  particle_iters = 0 disables the warm-up.
+    particle_iters: int = 0
+    n_particles: int = 64
+    particle_beta: float = 1.0
+    k_mu: float = 0.9
+    k_sigma: float = 0.5
+    sigma0_frac: float = 0.1
+    rng_key: int = 0
 
 
 # --------------------------------------------------------------------------------------------
