@@ -111,7 +111,21 @@ typedef struct {
     float alpha[8];            /* ascending; alpha[0] is the noisy fallback    */
     float c1, c2;              /* Armijo / Wolfe constants (A17: 1e-4, 0.9)                    */
     int ls_mode;               /* 0 Armijo, 1 Armijo+Wolfe, 2 Armijo+strong Wolfe (Alg. 1)     */
-    int64_t global_seed_base;  /* added to the local seed index in the packed selection key     */
+    int64_t global_seed_base;  /* added to the local seed index in the packed selection key and
+                                  the particle RNG counter                                       */
+    /* Particle warm-up before L-BFGS (§4.2, Alg. 5, Eqs. particle_1/2;
+     * DESIGN.md readings B6-B10).  The paper runs 2 iterations and gives no values for
+     * the rest; the SPEC defaults are n = 64, beta = 1, k_mu = 0.9, k_sigma = 0.5,
+     * sigma0_frac = 0.1.  Each iteration draws n particles theta = clip(mu + sqrt(sigma) z) with
+     * z from Philox4x32-10(key = (rng_key, global problem), ctr = (var/4, particle, iteration,
+     * global seed)), evaluates their cost only, and updates mu, sigma with w = softmax(-C/beta). */
+    int particle_iters;        /* 0 = off; >= 0                                                  */
+    int n_particles;           /* n >= 1 when particle_iters > 0                                  */
+    float particle_beta;       /* beta > 0                                                        */
+    float k_mu, k_sigma;       /* step sizes in [0, 1]                                            */
+    float sigma0_frac;         /* initial Theta_sigma = (sigma0_frac (hi - lo))^2 per variable    */
+    uint32_t rng_key;          /* Philox key word 0                                               */
+    int64_t global_problem_base;   /* added to the local problem index: Philox key word 1        */
 } crb_solver_params;
 
 crb_status crb_create(int cuda_device, crb_ctx **out);
@@ -191,6 +205,12 @@ crb_status crb_argmin_keys(int P, int S, const float *cost, int64_t seed_base, i
  * S[B][count][n], Y[B][count][n], g[B][n], d[B][n].  n <= 512, count <= 16. */
 crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const float *Y,
                                const float *g, float *d, void *stream);
+
+/* The particle warm-up's draws (Alg. 5 SAMPLE, reading B9) exactly as the solver makes them:
+ * out[l][v] = theta_s for variable v of particle l in iteration `iter` of global seed `seed`,
+ * key (key0, key1 = global problem).  Device pointer out[n_particles][n_var]. */
+crb_status crb_particle_normals(uint32_t key0, uint32_t key1, int n_var, int n_particles, int iter,
+                                uint32_t seed, float *out, void *stream);
 
 /* Shared-memory footprint (bytes per CTA) and resident CTAs per SM of the persistent solver for
  * horizon H (1 = IK) with the current robot and world (diagnostics; needs robot, world, params). */

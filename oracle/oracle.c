@@ -22,6 +22,18 @@ static void upd_margin(double *margin, double v) {
     if (margin && fabs(v) < *margin) *margin = fabs(v);
 }
 
+/* Margin kinds: upd_margin for branches where the COST jumps (a sweep sample that appears or
+ * disappears while in contact), upd_margin_grad where only the gradient does (the cost is
+ * continuous there).  With cost-only margins on (orc_set_margin_mode(1), per thread) the latter
+ * are not recorded: what a cost-only evaluation (the particle warm-up) needs. */
+static _Thread_local int g_cost_only_margins = 0;
+
+void orc_set_margin_mode(int cost_only) { g_cost_only_margins = cost_only; }
+
+static void upd_margin_grad(double *margin, double v) {
+    if (!g_cost_only_margins) upd_margin(margin, v);
+}
+
 /* ------------------------------------------------------------------------------------------ */
 /* 4x4 homogeneous matrices, Table 6                                              */
 /* ------------------------------------------------------------------------------------------ */
@@ -259,7 +271,7 @@ static double box_sdf_impl(const double *p, const double *pos, const double *qua
             double second = -ORC_INF;
             for (int i = 0; i < 3; ++i)
                 if (i != imax && qv[i] > second) second = qv[i];
-            upd_margin(margin, qmax - second);
+            upd_margin_grad(margin, qmax - second);
         }
     }
     if (grad)
@@ -334,7 +346,15 @@ double orc_sphere_world(const orc_world *w, const double *c, const double *cprev
             double bound = 0.5 * L;
             double j = (rp - sd0 > 0) ? rp : sd0;
             for (int s = 0; s < steps; ++s) {
-                upd_margin(margin, j - bound);
+                if (margin && fabs(j - bound) < 1e-3) {
+                    /* the sample at the exit exists on one side of j = bound only: a cost and
+                     * gradient jump iff it is in contact (a free sample adds nothing and ends
+                     * the sweep either way) */
+                    double kb = j / L;
+                    double pb[3] = {c[0] + kb * dv[0], c[1] + kb * dv[1], c[2] + kb * dv[2]};
+                    double sdb = box_sdf_impl(pb, w->pos + 3 * k, w->quat + 4 * k, w->half + 3 * k, NULL, NULL);
+                    if (rp - sdb > -1e-6) upd_margin(margin, j - bound);
+                }
                 if (j >= bound) break;
                 double kappa = j / L;
                 double p[3] = {c[0] + kappa * dv[0], c[1] + kappa * dv[1], c[2] + kappa * dv[2]};
@@ -376,9 +396,9 @@ double orc_self_collision(const orc_robot *rb, const double *spheres, double bet
     }
     if (arg_pair) *arg_pair = -1;
     if (ibest < 0) return 0.0;
-    upd_margin(margin, best);
+    upd_margin_grad(margin, best);
     if (best <= 0) return 0.0;
-    if (margin && second > -ORC_INF) upd_margin(margin, best - second);
+    if (margin && second > -ORC_INF) upd_margin_grad(margin, best - second);
     if (arg_pair) *arg_pair = ibest;
     int i = rb->pairs[2 * ibest], j = rb->pairs[2 * ibest + 1];
     double u[3] = {spheres[i * 4] - spheres[j * 4], spheres[i * 4 + 1] - spheres[j * 4 + 1],
@@ -555,7 +575,7 @@ double orc_eval_traj(const orc_robot *rb, const orc_world *w, const orc_params *
     /* pose at x_H (Eq. pose_cost_term) */
     double gp[3], gq[4];
     tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
-    if (margin) upd_margin(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
+    if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
     /* backward (O6) per evaluated configuration */
     for (int h = 1; h <= H; ++h) {
         orc_fk_backward(rb, XR(h), gs + h * M * 3, (h == H) ? gp : NULL, (h == H) ? gq : NULL, tmp);
@@ -613,7 +633,7 @@ double orc_eval_ik(const orc_robot *rb, const orc_world *w, const orc_params *pr
     }
     double gp[3], gq[4];
     tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
-    if (margin) upd_margin(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
+    if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
     if (grad) {
         orc_fk_backward(rb, q, gs, gp, gq, grad);
         for (int d = 0; d < D; ++d) grad[d] += gb[d];

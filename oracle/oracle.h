@@ -71,10 +71,12 @@ typedef struct {
 /* O10 instrumentation.  `margin` = the minimum distance of any quantity to a branch point where
  * the cost or its gradient is DISCONTINUOUS: the self-collision max(0, P*) switch and the top-2
  * gap of the arg-max pair, the inside-box nearest-face tie, a sweep exit |j - bound| (a sample
- * appears or disappears) and |<q_g, q>| (sign switch of the orientation gradient).  The
+ * in contact appears or disappears; a free boundary sample changes nothing) and |<q_g, q>| (sign
+ * switch of the orientation gradient).  Only the sweep exit makes the COST jump.  The
  * activation (Eq. smooth-distance-cases), the bound cost (Eq. bound_cost), the hit/free jump
  * switch (j += r' vs j += sd: equal at sd = r') and the gap test are C1 there and need no margin.
  * counters[] layout: */
+void orc_set_margin_mode(int cost_only);   /* 1: record cost-discontinuity margins only (this thread) */
 enum { ORC_CNT_BOX_TESTS = 0, ORC_CNT_BOX_HITS, ORC_CNT_SWEEP_SAMPLES, ORC_CNT_SWEEP_HITS,
        ORC_CNT_PAIR_TESTS, ORC_CNT_PAIR_PEN, ORC_CNT_ACTIVE_SPHERES, ORC_CNT_N };
 

@@ -340,6 +340,19 @@ def lbfgs_solve(fun, x0, sp, lo=None, hi=None):
     return bx, bc.value, trace
 
 
+class cost_only_margins:
+    """Context manager: while active, evaluation margins count only branches where the COST is
+    discontinuous (a sweep sample in contact appearing / disappearing) -- for cost-only passes."""
+
+    def __enter__(self):
+        lib().orc_set_margin_mode(1)
+        return self
+
+    def __exit__(self, *exc):
+        lib().orc_set_margin_mode(0)
+        return False
+
+
 def philox4x32(key, ctr):
     k = (C.c_uint * 2)(*[int(v) & 0xFFFFFFFF for v in key])
     c = (C.c_uint * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])

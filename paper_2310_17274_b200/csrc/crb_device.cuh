@@ -49,7 +49,7 @@ struct RobotPack {
 // Shared-memory layout (offsets in 4-byte words from the dynamic smem base).
 struct Layout {
     int robot, boxes, mbar;
-    int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, wpart, cbb, csm, gxd, gq, gva, pose_ft, pose_c,
+    int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, cbb, csm, gxd, gq, gva, pose_ft, pose_c,
         goal, cfg_cost, cfg_terms, gV, red, st, scal;
     int solver;      // start of the solver region
     int total;       // words
@@ -76,6 +76,11 @@ struct KParams {
     int iters, m, A, ls_mode;
     float alpha[8], c1, c2;
     long long seed_base;
+    // particle warm-up (Alg. 5; f1)
+    int pn_iters, pn;
+    float p_inv_beta, k_mu, k_sigma, s0_frac;
+    unsigned rng_key;
+    long long prob_base;
     // problem
     int mode, H, S, P, B;
     const float *q_in;
@@ -268,6 +273,47 @@ __device__ __forceinline__ float candidate(float th, float alpha, float d, float
     return fminf(fmaxf(__fmaf_rn(alpha, d, th), lo), hi);
 }
 
+// Particle warm-up draws (§4.2, Alg. 5 SAMPLE; reading B9): Philox4x32-10 keyed by
+// (rng_key, global problem), counter (var / 4, particle, iteration, global seed); words (0,1) and
+// (2,3) are Box-Muller pairs on 24-bit uniforms, var % 4 picks (cos, sin, cos, sin).
+__device__ __forceinline__ float particle_normal(unsigned k0, unsigned k1, unsigned var, unsigned l,
+                                                 unsigned it, unsigned seed) {
+    unsigned x0 = var >> 2, x1 = l, x2 = it, x3 = seed;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const unsigned hi0 = __umulhi(0xD2511F53u, x0), lo0 = 0xD2511F53u * x0;
+        const unsigned hi1 = __umulhi(0xCD9E8D57u, x2), lo1 = 0xCD9E8D57u * x2;
+        x0 = hi1 ^ x1 ^ k0; x1 = lo1; x2 = hi0 ^ x3 ^ k1; x3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    const int j = var & 3;
+    const unsigned wa = j < 2 ? x0 : x2, wb = j < 2 ? x1 : x3;
+    const float u1 = (float)((wa >> 8) + 1u) * 5.9604644775390625e-8f;   // 2^-24, exact
+    const float u2 = (float)(wb >> 8) * 5.9604644775390625e-8f;
+    const float r = sqrtf(-2.f * logf(u1));
+    float sn, cs;
+    sincospif(2.f * u2, &sn, &cs);
+    return r * ((j & 1) ? sn : cs);
+}
+
+// Streaming form of UPDATE (Alg. 5; Eqs. particle_1/2 with B6): per variable the running
+// max-shifted exponential utility sums Z, S1 = sum e theta, S2 = sum e (theta - mu)^2, rescaled
+// when a particle raises the running max; non-finite costs get weight 0 (B10).
+struct ParticleAcc {
+    float m, Z;
+    __device__ __forceinline__ void reset() { m = -INFINITY; Z = 0.f; }
+    // returns the weight factor e of this particle and the rescale factor r of earlier sums
+    __device__ __forceinline__ float add(float C, float inv_beta, float &r) {
+        r = 1.f;
+        const float c = -C * inv_beta;
+        if (!(fabsf(C) <= 3.4e38f)) return 0.f;       // NaN / inf: weight 0
+        if (c > m) { r = expf(m - c); Z *= r; m = c; }
+        const float e = expf(c - m);
+        Z += e;
+        return e;
+    }
+};
+
 // ------------------------------------------------------------------------------------------
 // the fused evaluation pass over 32 configuration slots
 // ------------------------------------------------------------------------------------------
@@ -275,7 +321,7 @@ struct Smem {
     const int *iw;          // robot blob as ints
     const float *fw;        // robot blob as floats
     const float *boxes;
-    float *q_cfg, *scs, *xs, *lt, *frames, *ls, *sbest, *wpart, *cbb, *csm, *gxd, *gq, *gva, *pose_ft,
+    float *q_cfg, *scs, *xs, *lt, *frames, *ls, *sbest, *cbb, *csm, *gxd, *gq, *gva, *pose_ft,
         *pose_c, *goal, *cfg_cost, *cfg_terms, *gV, *red, *st, *scal;
     float4 *sw;             // [M][32] sphere centre (x, y, z) and hb = -(|w|^2 - r_self^2) / 2
     float4 *sg;             // [M][32] dE/dw (x, y, z) and the world energy E (w)
@@ -297,7 +343,7 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     s.sbest = smem + L.sbest;
     s.srank = reinterpret_cast<int *>(smem + L.srank);
     s.sij = reinterpret_cast<int *>(smem + L.sij);
-    s.wpart = smem + L.wpart; s.cbb = smem + L.cbb; s.csm = smem + L.csm; s.gxd = smem + L.gxd;
+    s.cbb = smem + L.cbb; s.csm = smem + L.csm; s.gxd = smem + L.gxd;
     s.gq = smem + L.gq; s.gva = smem + L.gva; s.pose_ft = smem + L.pose_ft; s.pose_c = smem + L.pose_c;
     s.goal = smem + L.goal; s.cfg_cost = smem + L.cfg_cost; s.cfg_terms = smem + L.cfg_terms;
     s.gV = smem + L.gV; s.red = smem + L.red; s.st = smem + L.st; s.scal = smem + L.scal;
@@ -539,7 +585,7 @@ __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const float 
 // the kernel parameters left in the constant bank.
 template <int MODE>
 __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
-                                          const float *dvec) {
+                                          const float *dvec, bool grad = true) {
     const Smem s = make_smem(kp, smem);
     const RobotPack &rp = kp.rp;
     const CostP &cf = kp.cp;
@@ -659,9 +705,10 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     // ---- a4 + a5/a6: self-collision and world collision as ONE dynamic work queue.  Items are the
     // world groups (4 consecutive spheres, all cuboids) followed by the self-collision pair blocks
     // in decreasing cost order; warps take items from a shared counter, so data-dependent costs
-    // (hits, sweeps, penetrating pairs) balance across warps.  Each warp keeps its own partial
-    // (self best, world sum) and the merge below combines them in fixed warp order: the result
-    // does not depend on which warp took which item.
+    // (hits, sweeps, penetrating pairs) balance across warps.  Each warp keeps its own self best
+    // (max with rank ties: partition-independent) and each world group stores its own cost sum;
+    // the merge below combines them in a fixed order, so the result does not depend on which warp
+    // took which item (bitwise deterministic).
     {
         // self (Eq. self-collision, Alg. 9): block {ia..ia+na-1} x {jb..jb+len-1} of S, na <= 4
         // first spheres in registers, partners streamed, lane = slot.  Screen: d^2 - R^2 =
@@ -675,7 +722,6 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         const unsigned short *rk = reinterpret_cast<const unsigned short *>(s.iw + rp.o_rank);
         // world (Alg. 10 + Algs. 11-12, Eq. world-collision-cost): each thread carries the 4
         // spheres of a group at its slot through one scan of the cuboids
-        float wsum = 0.f;
         const bool to = MODE == MODE_TO;
         const bool sweepf = to && (cf.flags & F_SWEEP);
         const bool speedf = to && (cf.flags & F_SPEED);
@@ -738,16 +784,20 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         }
                     }
                 }
+                // the group's cost goes to the .w of its first sphere (unused by the backward):
+                // the merge sums the groups in index order, whichever warp took them
+                float gsum = 0.f;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int m = m0 + u;
                     if (m < rp.M) {
                         const float sc = cf.beta_world * sp[u];
                         float4 g = s.sg[m * NC + lane];
-                        wsum += sc * g.w;
+                        gsum += sc * g.w;
                         s.sg[m * NC + lane] = make_float4(sc * g.x, sc * g.y, sc * g.z, 0.f);
                     }
                 }
+                s.sg[m0 * NC + lane].w = gsum;
             } else {
                 const uint2 B = blk[item - nwg];
                 const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff,
@@ -796,7 +846,6 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         s.sbest[warp * NC + lane] = best;
         s.srank[warp * NC + lane] = brank;
         s.sij[warp * NC + lane] = bij;
-        s.wpart[warp * NC + lane] = wsum;
     }
 
     __syncthreads();
@@ -826,7 +875,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             cself = b * bp;
         }
         float cw = 0.f;
-        for (int w = 0; w < NW; ++w) cw += s.wpart[w * NC + c];
+        for (int q = 0; q < ((rp.M + 3) >> 2); ++q) cw += s.sg[(q << 2) * NC + c].w;   // fixed order
         float cb = 0.f, cs = 0.f;
         for (int d = 0; d < D; ++d) { cb += s.cbb[d * NC + c]; cs += s.csm[d * NC + c]; }
         const bool valid = c < n_act;
@@ -840,6 +889,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         if (c == 0) s.scal[0] = tot;
     }
     __syncthreads();
+    if (!grad) return;   // cost-only pass (particle warm-up, f1): no backward
 
     // ---- a9: backward to joint space (Alg. 8 / Table 7 as subtree sums):
     // per link: F_l = sum G_m, T_l = sum w_m x G_m over its spheres (+ the pose pseudo-sphere);

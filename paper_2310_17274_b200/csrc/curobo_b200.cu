@@ -99,15 +99,43 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
     if (t == 0) { ring[0] = 0; ring[1] = 0; }
     __syncthreads();
 
-    // One loop over evaluation passes with a single eval_pass call site: pass 0 evaluates Theta_0
-    // (O8 initialise); then every iteration is an L-BFGS step followed by A candidate passes.
+    // One loop over evaluation passes with a single eval_pass call site: first the particle
+    // warm-up (f1: pn_iters x pn cost-only passes, Alg. 5), then pass 0 evaluates Theta_0 (O8
+    // initialise) and every iteration is an L-BFGS step followed by A candidate passes.
+    // During the warm-up th holds mu, g holds Theta_sigma, dd / thp the UPDATE sums S1 / S2.
     float c = 0.f, cbest = 0.f, g0d = 0.f;
     float d_e[2] = {0.f, 0.f};
-    const int npass = 1 + kp.iters * A;
+    const int npart = kp.pn_iters * kp.pn;
+    const int npass = npart + 1 + kp.iters * A;
+    const unsigned pk1 = (unsigned)(kp.prob_base + p), psd = (unsigned)(kp.seed_base + (unit - p * kp.S));
+    ParticleAcc pacc;
+    pacc.reset();
+    if (npart > 0) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            if (i < N) { const float s0 = kp.s0_frac * (hi_e[e] - lo_e[e]); g[i] = s0 * s0; }   // B8
+        }
+    }
     for (int pass = 0; pass < npass; ++pass) {
-        const int a = pass == 0 ? -1 : (pass - 1) % A;
+        const bool part = pass < npart;
+        const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
+        const int lpass = pass - npart;
+        const int a = part ? -2 : (lpass == 0 ? -1 : (lpass - 1) % A);
+        if (part) {
+            // ---- f1 SAMPLE (Alg. 5): theta_l = clip(mu + sqrt(Theta_sigma) theta_s) (B7)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) {
+                    const float z = particle_normal(kp.rng_key, pk1, (unsigned)i, (unsigned)pl, (unsigned)pit, psd);
+                    thA[i] = fminf(fmaxf(fmaf(sqrtf(g[i]), z, th[i]), lo_e[e]), hi_e[e]);
+                }
+            }
+            __syncthreads();
+        }
         if (a == 0) {
-            const int it = (pass - 1) / A;
+            const int it = (lpass - 1) / A;
             // ---- a13: L-BFGS buffers (Alg. 6 lines 1-5): push (s, y, rho) unless s^T y <= 1e-12 (A20)
             if (it > 0) {
                 const int fs = ring[1];
@@ -161,8 +189,40 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             }
             __syncthreads();
         }
-        // ---- a2..a10: one evaluation pass
-        eval_pass<MODE_TO>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr);
+        // ---- a2..a10: one evaluation pass (cost only for particles)
+        eval_pass<MODE_TO>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr, !part);
+        if (part) {
+            // ---- f1 UPDATE, streamed over the particles (Eqs. particle_1/2, B6)
+            float r;
+            const float w = pacc.add(s.scal[0], kp.p_inv_beta, r);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) {
+                    const float x = thA[i], dx = x - th[i];
+                    dd[i] = (pl == 0 ? 0.f : dd[i] * r) + w * x;
+                    thp[i] = (pl == 0 ? 0.f : thp[i] * r) + w * dx * dx;
+                }
+            }
+            if (pl == kp.pn - 1) {
+                const bool upd = pacc.Z > 0.f;
+                const float iz = upd ? 1.f / pacc.Z : 0.f;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = t + e * NT;
+                    if (i < N) {
+                        if (upd) {
+                            th[i] = (1.f - kp.k_mu) * th[i] + kp.k_mu * (dd[i] * iz);
+                            g[i] = (1.f - kp.k_sigma) * g[i] + kp.k_sigma * (thp[i] * iz);
+                        }
+                        if (pass == npart - 1) thA[i] = th[i];   // Theta_0 of L-BFGS = mu
+                    }
+                }
+                pacc.reset();
+                __syncthreads();
+            }
+            continue;
+        }
         if (a < 0) {
             c = s.scal[0];
             cbest = c;
@@ -244,14 +304,40 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
         }
     __syncthreads();
     prep_sincos(s, D);
-    // single eval_pass call site: pass 0 = Theta_0, then (L-BFGS step, A candidates) per iteration
+    // single eval_pass call site: the particle warm-up (f1, cost only: thread t < D*32 owns
+    // element t with mu in th, Theta_sigma in g, the UPDATE sums in dd / thp), then pass 0 =
+    // Theta_0 and (L-BFGS step, A candidates) per iteration
     float c = 0.f, cbest = 0.f, g0d = 0.f;
     int cnt = 0, fs = 0;
-    const int npass = 1 + kp.iters * A;
+    const int npart = kp.pn_iters * kp.pn;
+    const int npass = npart + 1 + kp.iters * A;
+    const unsigned pk1 = (unsigned)(kp.prob_base + p);
+    const unsigned psd = (unsigned)(kp.seed_base + grp * NC + (t & 31));
+    ParticleAcc pacc;
+    pacc.reset();
+    if (npart > 0 && t < DC) {
+        const int d = t / NC;
+        const float s0 = kp.s0_frac * (lim[D + d] - lim[d]);   // B8
+        g[t] = s0 * s0;
+    }
     for (int pass = 0; pass < npass; ++pass) {
-        const int a = pass == 0 ? -1 : (pass - 1) % A;
+        const bool part = pass < npart;
+        const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
+        const int lpass = pass - npart;
+        const int a = part ? -2 : (lpass == 0 ? -1 : (lpass - 1) % A);
+        if (part && t < DC) {
+            // ---- f1 SAMPLE (Alg. 5) for every seed of the group: variable d of seed lane
+            const int d = t / NC;
+            const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
+            const float v = fminf(fmaxf(fmaf(sqrtf(g[t]), z, th[t]), lim[d]), lim[D + d]);
+            s.q_cfg[t] = v;
+            float sn, cs;
+            sincosf(v, &sn, &cs);
+            s.scs[t] = sn;
+            s.scs[DC + t] = cs;
+        }
         if (a == 0 && warp == 0) {
-            const int it = (pass - 1) / A;
+            const int it = (lpass - 1) / A;
             // ---- ring push (per seed, A20)
             if (it > 0) {
                 float sy = 0.f, yy = 0.f;
@@ -309,7 +395,36 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
                 s.scs[DC + idx] = cs;
             }
         }
-        eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
+        eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr, !part);
+        if (part) {
+            // ---- f1 UPDATE, streamed over the particles (Eqs. particle_1/2, B6), per seed
+            float r;
+            const float w = pacc.add(s.cfg_cost[t & 31], kp.p_inv_beta, r);
+            if (t < DC) {
+                const float x = s.q_cfg[t], dx = x - th[t];
+                dd[t] = (pl == 0 ? 0.f : dd[t] * r) + w * x;
+                thp[t] = (pl == 0 ? 0.f : thp[t] * r) + w * dx * dx;
+            }
+            if (pl == kp.pn - 1) {
+                if (t < DC) {
+                    if (pacc.Z > 0.f) {
+                        const float iz = 1.f / pacc.Z;
+                        th[t] = (1.f - kp.k_mu) * th[t] + kp.k_mu * (dd[t] * iz);
+                        g[t] = (1.f - kp.k_sigma) * g[t] + kp.k_sigma * (thp[t] * iz);
+                    }
+                    if (pass == npart - 1) {   // Theta_0 of L-BFGS = mu
+                        const float v = th[t];
+                        s.q_cfg[t] = v;
+                        float sn, cs;
+                        sincosf(v, &sn, &cs);
+                        s.scs[t] = sn;
+                        s.scs[DC + t] = cs;
+                    }
+                }
+                pacc.reset();
+            }
+            continue;
+        }
         if (warp != 0) continue;
         if (a < 0) {
             c = s.cfg_cost[lane];
@@ -488,6 +603,14 @@ __global__ void argmin_keys_kernel(int P, int S, const float *cost, long long ba
     if (out_idx) out_idx[p] = bi;
 }
 
+__global__ void particle_normals_kernel(unsigned k0, unsigned k1, int n_var, int n, int it, unsigned seed,
+                                        float *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * n_var) return;
+    const int l = i / n_var, v = i - l * n_var;
+    out[i] = particle_normal(k0, k1, (unsigned)v, (unsigned)l, (unsigned)it, seed);
+}
+
 __global__ void __launch_bounds__(NT, 2) lbfgs_direction_kernel(int n, int count, const float *S, const float *Y,
                                                                 const float *g, float *d) {
     extern __shared__ __align__(16) float smem[];
@@ -603,7 +726,6 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.sbest = take(NW * NC);
     L.srank = take(NW * NC);
     L.sij = take(NW * NC);
-    L.wpart = take(NW * NC);
     L.cbb = take(D * NC);
     L.csm = take(D * NC);
     L.gxd = take(D * NC);
@@ -1034,6 +1156,11 @@ crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int
     if (!sp || !seeds || !goal || P < 0 || S < 1) return fail(ctx, CRB_E_ARG, "bad solve arguments");
     if (sp->history < 1 || sp->history > 16 || sp->n_alpha < 1 || sp->n_alpha > 8 || sp->iters < 0)
         return fail(ctx, CRB_E_LIMIT, "history must be in [1,16], n_alpha in [1,8], iters >= 0");
+    if (sp->particle_iters < 0 ||
+        (sp->particle_iters > 0 && (sp->n_particles < 1 || !(sp->particle_beta > 0.f) || !(sp->k_mu >= 0.f) ||
+                                    !(sp->k_mu <= 1.f) || !(sp->k_sigma >= 0.f) || !(sp->k_sigma <= 1.f) ||
+                                    !(sp->sigma0_frac >= 0.f))))
+        return fail(ctx, CRB_E_ARG, "particle warm-up: iters >= 0, n >= 1, beta > 0, k_mu/k_sigma in [0,1], sigma0_frac >= 0");
     const int mode = H == 1 ? MODE_IK : MODE_TO;
     const int D = ctx->rp.D;
     if (mode == MODE_TO && (H < 8 || H > 32 || H * D > 512 || !start))
@@ -1048,6 +1175,10 @@ crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int
     kp.iters = sp->iters; kp.m = sp->history; kp.A = sp->n_alpha; kp.ls_mode = sp->ls_mode;
     for (int i = 0; i < 8; ++i) kp.alpha[i] = sp->alpha[i];
     kp.c1 = sp->c1; kp.c2 = sp->c2; kp.seed_base = sp->global_seed_base;
+    kp.pn_iters = sp->particle_iters; kp.pn = sp->particle_iters > 0 ? sp->n_particles : 1;
+    kp.p_inv_beta = sp->particle_iters > 0 ? 1.f / sp->particle_beta : 0.f;
+    kp.k_mu = sp->k_mu; kp.k_sigma = sp->k_sigma; kp.s0_frac = sp->sigma0_frac;
+    kp.rng_key = sp->rng_key; kp.prob_base = sp->global_problem_base;
     kp.seed_best_cost = sbc; kp.seed_best_traj = sbt;
     const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids + solver)");
@@ -1140,6 +1271,16 @@ crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const fl
     if (cudaFuncSetAttribute(lbfgs_direction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
         return CRB_E_CUDA;
     lbfgs_direction_kernel<<<B, NT, bytes, (cudaStream_t)stream>>>(n, count, S, Y, g, d);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_particle_normals(uint32_t key0, uint32_t key1, int n_var, int n_particles, int iter, uint32_t seed,
+                                float *out, void *stream) {
+    if (n_var < 0 || n_particles < 0 || iter < 0 || (!out && n_var * n_particles > 0)) return CRB_E_ARG;
+    const int total = n_var * n_particles;
+    if (total == 0) return CRB_OK;
+    particle_normals_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(key0, key1, n_var, n_particles,
+                                                                                  iter, seed, out);
     return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
 }
 

@@ -61,7 +61,10 @@ class crb_cost_params(C.Structure):
 
 class crb_solver_params(C.Structure):
     _fields_ = [("iters", C.c_int), ("history", C.c_int), ("n_alpha", C.c_int), ("alpha", C.c_float * 8),
-                ("c1", C.c_float), ("c2", C.c_float), ("ls_mode", C.c_int), ("global_seed_base", C.c_int64)]
+                ("c1", C.c_float), ("c2", C.c_float), ("ls_mode", C.c_int), ("global_seed_base", C.c_int64),
+                ("particle_iters", C.c_int), ("n_particles", C.c_int), ("particle_beta", C.c_float),
+                ("k_mu", C.c_float), ("k_sigma", C.c_float), ("sigma0_frac", C.c_float),
+                ("rng_key", C.c_uint32), ("global_problem_base", C.c_int64)]
 
 
 _V = C.c_void_p
@@ -83,12 +86,14 @@ _lib.crb_ls_select.argtypes = [C.c_int, C.c_int, F_P, _V, _V, _V, _V, C.c_float,
 _lib.crb_argmin_keys.argtypes = [C.c_int, C.c_int, _V, C.c_int64, _V, _V, _V]
 _lib.crb_lbfgs_direction.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, _V, _V, _V]
 _lib.crb_solver_occupancy.argtypes = [_V, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+_lib.crb_particle_normals.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_uint32, _V, _V]
 _lib.crb_launch_count.argtypes = [_V]
 _lib.crb_launch_count.restype = C.c_int64
 
 SYMBOLS = ["crb_create", "crb_destroy", "crb_last_error", "crb_version", "crb_set_robot", "crb_set_world",
            "crb_set_cost_params", "crb_fk", "crb_evaluate_cost_grad", "crb_lbfgs_solve", "crb_lbfgs_solve_host",
-           "crb_ls_select", "crb_argmin_keys", "crb_lbfgs_direction", "crb_launch_count", "crb_solver_occupancy"]
+           "crb_ls_select", "crb_argmin_keys", "crb_lbfgs_direction", "crb_launch_count", "crb_solver_occupancy",
+           "crb_particle_normals"]
 
 
 def _ptr(t):
@@ -115,10 +120,12 @@ def cost_params_struct(cp: inputs.CostParams) -> crb_cost_params:
                            int(cp.flags))
 
 
-def solver_params_struct(sp: inputs.SolverParams, seed_base: int = 0) -> crb_solver_params:
+def solver_params_struct(sp: inputs.SolverParams, seed_base: int = 0, problem_base: int = 0) -> crb_solver_params:
     al = list(sp.alpha) + [0.0] * (8 - len(sp.alpha))
     return crb_solver_params(int(sp.iters), int(sp.history), len(sp.alpha), (C.c_float * 8)(*al), float(sp.c1),
-                             float(sp.c2), int(sp.ls_mode), int(seed_base))
+                             float(sp.c2), int(sp.ls_mode), int(seed_base), int(sp.particle_iters),
+                             int(sp.n_particles), float(sp.particle_beta), float(sp.k_mu), float(sp.k_sigma),
+                             float(sp.sigma0_frac), int(sp.rng_key) & 0xFFFFFFFF, int(problem_base))
 
 
 class Context:
@@ -223,7 +230,7 @@ class Context:
         return cost, g, tc
 
     def solve(self, sp: inputs.SolverParams, seeds, goal, start=None, env=None, seed_base: int = 0,
-              seed_outputs: bool = False):
+              seed_outputs: bool = False, problem_base: int = 0):
         """seeds [P,S,H,D] (TO) or [P,S,D] (IK).  Returns dict of device tensors."""
         import torch
         P, S = seeds.shape[0], seeds.shape[1]
@@ -236,19 +243,19 @@ class Context:
         if seed_outputs:
             out["seed_best_cost"] = torch.empty(P, S, device=dev, dtype=torch.float32)
             out["seed_best_traj"] = torch.empty_like(seeds)
-        s = solver_params_struct(sp, seed_base)
+        s = solver_params_struct(sp, seed_base, problem_base)
         self._chk(_lib.crb_lbfgs_solve(self.h, C.byref(s), P, S, H, _ptr(seeds), _ptr(env), _ptr(start), _ptr(goal),
                                        _ptr(out["best_traj"]), _ptr(out["best_cost"]), _ptr(out["best_key"]),
                                        _ptr(out.get("seed_best_cost")), _ptr(out.get("seed_best_traj")), _stream()))
         return out
 
     def solve_host(self, sp: inputs.SolverParams, seeds, goal, start=None, env=None, seed_base: int = 0,
-                   best_traj=None, best_cost=None, best_key=None):
+                   best_traj=None, best_cost=None, best_key=None, problem_base: int = 0):
         """Host (ideally pinned) torch CPU tensors in and out; H2D + solve + D2H + sync in the library."""
         P, S = seeds.shape[0], seeds.shape[1]
         H = 1 if seeds.dim() == 3 else seeds.shape[2]
         hp = lambda t: None if t is None else C.c_void_p(t.data_ptr())
-        s = solver_params_struct(sp, seed_base)
+        s = solver_params_struct(sp, seed_base, problem_base)
         self._chk(_lib.crb_lbfgs_solve_host(self.h, C.byref(s), P, S, H, hp(seeds), hp(env), hp(start), hp(goal),
                                             hp(best_traj), hp(best_cost), hp(best_key), _stream()))
 
@@ -282,6 +289,15 @@ def lbfgs_direction(S, Y, g):
     d = torch.empty_like(g)
     _check_free(_lib.crb_lbfgs_direction(B, n, count, _ptr(S), _ptr(Y), _ptr(g), _ptr(d), _stream()))
     return d
+
+
+def particle_normals(key0, key1, n_var, n_particles, it, seed):
+    """[n_particles, n_var] device fp32: the warm-up's draws as the solver makes them (B9)."""
+    import torch
+    out = torch.empty(n_particles, n_var, device="cuda", dtype=torch.float32)
+    _check_free(_lib.crb_particle_normals(C.c_uint32(key0 & 0xFFFFFFFF), C.c_uint32(key1 & 0xFFFFFFFF), n_var,
+                                          n_particles, it, C.c_uint32(seed & 0xFFFFFFFF), _ptr(out), _stream()))
+    return out
 
 
 def version() -> str:

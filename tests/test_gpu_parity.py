@@ -348,6 +348,27 @@ def test_solve_to_invariants_and_determinism(native, O):
     ctx.close()
 
 
+def test_solve_bitwise_deterministic_franka(native, O):
+    """Franka + 20 cuboids: 16 world groups + ~100 self blocks per pass go through the dynamic
+    work queue, so warps take different items from run to run; costs, trajectories and keys must
+    still be bitwise identical (fixed-order merge)."""
+    rb, starts, goals_cfg, trajs = franka_trajs(77, 8, 16)
+    R = O.Robot(rb)
+    worlds = [inputs.tabletop_scene(2, 0, 20)]
+    ctx = make(native, rb, worlds, inputs.CostParams(dt=0.25))
+    gl = f32(np.array([O.fk(R, q)[2] for q in goals_cfg]))
+    seeds = f32(trajs.reshape(2, 4, 16, 7))
+    sp = inputs.SolverParams(iters=15)
+    outs = [ctx.solve(sp, T(seeds), T(gl[:2]), start=T(f32(starts[:2])), seed_outputs=True) for _ in range(4)]
+    ik_seeds = f32(np.stack([inputs.ik_seeds(rb, p, 64) for p in range(2)]))
+    iks = [ctx.solve(sp, T(ik_seeds), T(gl[:2]), seed_outputs=True) for _ in range(4)]
+    for runs in (outs, iks):
+        for o in runs[1:]:
+            for k in o:
+                assert torch.equal(o[k], runs[0][k]), k
+    ctx.close()
+
+
 def test_solve_seed_base_and_host_api(native, O):
     rb, starts, goals = planar_problems(O, 3)
     P, S, H = 3, 5, 16
