@@ -15,6 +15,7 @@ bounded sample of the same workload on the host cores.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -237,6 +238,34 @@ def side_metrics(local, rank, world, dev, flush, steps=2):
                       "ik_queries_per_s": n_ik * world / (ms * 1e-3),
                       "evals_per_s": wl.evals_per_solve() * world / (ms * 1e-3),
                       "ctas_per_sm": ctx.solver_occupancy(1)[0]}
+    # f1: the paper's IK pipeline = 2 particle iterations, then L-BFGS
+    spp = dataclasses.replace(wl.solver, particle_iters=2, n_particles=64)
+    msp = _timed_solves(ctx, spp, torch.tensor(wl.seeds, device=dev), torch.tensor(wl.goal, device=dev), None,
+                        torch.tensor(wl.env, device=dev), steps, flush, world, dev)
+    out["cfg3_ik"]["with_particles"] = {"particle_iters": 2, "n_particles": 64, "ms_per_solve": msp,
+                                        "ik_queries_per_s": n_ik * world / (msp * 1e-3),
+                                        "added_ms": msp - ms}
+    ctx.close()
+    # f1 on the headline TO workload (config 2 shape): 2 x 64 cost-only particle passes per seed
+    # before the same 100 L-BFGS iterations; the paper reports +2 ms for this warm-up
+    n_f1 = 64
+    lo = rank * n_f1
+    wl = workload.franka_to(local, list(range(lo, lo + n_f1)), S=32, H=32, iters=100)
+    ctx = native.Context(local)
+    ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
+    args_ = (torch.tensor(wl.seeds, device=dev), torch.tensor(wl.goal, device=dev),
+             torch.tensor(wl.start, device=dev), torch.tensor(wl.env, device=dev))
+    ms0 = _timed_solves(ctx, wl.solver, *args_, steps, flush, world, dev)
+    spp = dataclasses.replace(wl.solver, particle_iters=2, n_particles=64)
+    msp = _timed_solves(ctx, spp, *args_, steps, flush, world, dev)
+    sp0 = dataclasses.replace(wl.solver, iters=0, particle_iters=2, n_particles=64)
+    msw = _timed_solves(ctx, sp0, *args_, steps, flush, world, dev)
+    n_part = n_f1 * 32 * 2 * 64 * 32     # cost-only seed-timestep evaluations of the warm-up
+    out["f1_particle_to"] = {"problems_per_gpu": n_f1, "seeds": 32, "timesteps": 32, "particle_iters": 2,
+                             "n_particles": 64, "ms_lbfgs_only": ms0, "ms_particle_plus_lbfgs": msp,
+                             "added_ms": msp - ms0, "ms_warmup_only": msw,
+                             "warmup_cost_only_evals_per_s": n_part * world / (msw * 1e-3),
+                             "to_problems_per_s_with_particles": n_f1 * world / (msp * 1e-3)}
     ctx.close()
     n_dense = 16
     lo = rank * n_dense

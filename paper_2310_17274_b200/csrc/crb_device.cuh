@@ -773,13 +773,31 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                             s2[u] = box_screen(cx[u], cy[u], cz[u], b);
                             any |= s2[u] < th2[u];
                         }
-                        if (any) {                    // rare path, one out-of-line copy for all spheres
+                        // rare path, compacted: the flagged (sphere u, slot) entries of this cuboid
+                        // are dealt one per lane, so a few hits do not serialise the warp.  Each
+                        // entry is a distinct sg[m][slot] and cuboids are flushed in order, so
+                        // every accumulator sees the same sequence of additions as a per-lane loop.
+                        if (__any_sync(FULL, any)) {
+                            unsigned bal[4];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                if (!(s2[u] < th2[u])) continue;
+                            for (int u = 0; u < 4; ++u) bal[u] = __ballot_sync(FULL, s2[u] < th2[u]);
+                            const int n0 = __popc(bal[0]), n1 = __popc(bal[1]), n2 = __popc(bal[2]);
+                            const int tot = n0 + n1 + n2 + __popc(bal[3]);
+                            for (int e = lane; e - lane < tot; e += 32) {
+                                if (e >= tot) continue;
+                                int u = 0, r = e;
+                                if (r >= n0) { r -= n0; u = 1; if (r >= n1) { r -= n1; u = 2; if (r >= n2) { r -= n2; u = 3; } } }
+                                const unsigned bm = u == 0 ? bal[0] : u == 1 ? bal[1] : u == 2 ? bal[2] : bal[3];
+                                const int src = __fns(bm, 0, r + 1);          // the r-th flagged slot
                                 const int m = m0 + u;
-                                box_slow(s.sg + m * NC + lane, s.sw + m * NC + lane, s.boxes, k, cx[u], cy[u], cz[u],
-                                         s2[u], sph[m].w + cf.eta, dirs[u], cf.eta, cf.inv_eta, cf.sweep_steps);
+                                const float4 *pc = s.sw + m * NC + src;
+                                const float4 c = pc[0];
+                                const float rpr = sph[m].w + cf.eta;
+                                float maxb2;
+                                const bool hp = to && src > 0 && src < H, hn = to && src + 1 < H;
+                                const int dr = sweep_dirs(pc, c.x, c.y, c.z, rpr, hp, hn, sweepf, maxb2);
+                                box_slow(s.sg + m * NC + src, pc, s.boxes, k, c.x, c.y, c.z, box_screen(c.x, c.y, c.z, b),
+                                         rpr, dr, cf.eta, cf.inv_eta, cf.sweep_steps);
                             }
                         }
                     }
