@@ -60,6 +60,7 @@ struct Layout {
 struct CostP {
     float a0, a1, a2, a3, a8, a9, wb[4], beta_self, beta_world, eta, eta_bound, dt;
     float inv_eta, inv_2dt;   // host-computed reciprocals (no divisions in the hot loops)
+    float inv_12dt, inv_12dt2, inv_2dt3;   // five-point stencil scales 1/(12 dt), 1/(12 dt^2), 1/(2 dt^3)
     int sweep_steps, H;
     unsigned flags;
 };
@@ -442,13 +443,26 @@ __device__ __forceinline__ void fk_chain(const RobotPack &rp, const Smem &s) {
 __device__ __forceinline__ void fk_place(const RobotPack &rp, const Smem &s) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
-    for (int m = warp; m < rp.M; m += NW) {
+    // each warp places a contiguous run of the link-sorted spheres, so the link transform is
+    // loaded into registers once per link change instead of once per sphere
+    const int per = (rp.M + NW - 1) / NW;
+    const int me = min(rp.M, (warp + 1) * per);
+    int lc = -1;
+    float T[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) T[i] = 0.f;
+    for (int m = warp * per; m < me; ++m) {
         const int l = s.iw[rp.o_sphlink + m];
+        if (l != lc) {
+            lc = l;
+            const float *Tl = s.lt + l * 12 * NC + lane;
+#pragma unroll
+            for (int i = 0; i < 12; ++i) T[i] = Tl[i * NC];
+        }
         const float4 c = sph[m];
-        const float *T = s.lt + l * 12 * NC + lane;
-        const float wx = T[0] * c.x + T[NC] * c.y + T[2 * NC] * c.z + T[3 * NC];
-        const float wy = T[4 * NC] * c.x + T[5 * NC] * c.y + T[6 * NC] * c.z + T[7 * NC];
-        const float wz = T[8 * NC] * c.x + T[9 * NC] * c.y + T[10 * NC] * c.z + T[11 * NC];
+        const float wx = T[0] * c.x + T[1] * c.y + T[2] * c.z + T[3];
+        const float wy = T[4] * c.x + T[5] * c.y + T[6] * c.z + T[7];
+        const float wz = T[8] * c.x + T[9] * c.y + T[10] * c.z + T[11];
         const float rs = s.fw[rp.o_rself + m];
         s.sw[m * NC + lane] = make_float4(wx, wy, wz, -0.5f * (wx * wx + wy * wy + wz * wz - rs * rs));
     }
@@ -637,11 +651,10 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 if (MODE == MODE_TO) {
                     const float *x = s.xs + d * XS + c + 3;   // x_h with h = c + 1
                     const float xm2 = x[-2], xm1 = x[-1], x0 = x[0], xp1 = x[1], xp2 = x[2];
-                    const float dt = cf.dt, dt2 = dt * dt, dt3 = dt2 * dt;
                     // O3 five-point stencil (§A.5, A15)
-                    const float v = (-xp2 + 8.f * xp1 - 8.f * xm1 + xm2) / (12.f * dt);
-                    const float a = (-xp2 + 16.f * xp1 - 30.f * x0 + 16.f * xm1 - xm2) / (12.f * dt2);
-                    const float j = (xp2 - 2.f * xp1 + 2.f * xm1 - xm2) / (2.f * dt3);
+                    const float v = (-xp2 + 8.f * xp1 - 8.f * xm1 + xm2) * cf.inv_12dt;
+                    const float a = (-xp2 + 16.f * xp1 - 30.f * x0 + 16.f * xm1 - xm2) * cf.inv_12dt2;
+                    const float j = (xp2 - 2.f * xp1 + 2.f * xm1 - xm2) * cf.inv_2dt3;
                     const float vm = lim[2 * D + d], am = lim[3 * D + d], jm = lim[4 * D + d];
                     cb += cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd); gx = cf.wb[0] * dd;
                     cb += cf.wb[1] * bound_cost(v, -vm, vm, cf.eta_bound, dd); gv = cf.wb[1] * dd;
@@ -980,10 +993,9 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
 
     // ---- transposed stencil + transposed state map (O2/O3 gradient routing) -> dC/dV
     if (MODE == MODE_TO) {
-        const float dt = cf.dt, dt2 = dt * dt, dt3 = dt2 * dt;
         // O3 coefficients: v: (1, -8, 0, 8, -1)/(12 dt), a: (-1, 16, -30, 16, -1)/(12 dt^2),
         // j: (-1, 2, 0, -2, 1)/(2 dt^3) for x_{h-2} .. x_{h+2}
-        const float iv = 1.f / (12.f * dt), ia = 1.f / (12.f * dt2), ij = 1.f / (2.f * dt3);
+        const float iv = cf.inv_12dt, ia = cf.inv_12dt2, ij = cf.inv_2dt3;
         float gdp = 0.f;
         for (int idx = tid; idx < D * NC; idx += NT) {
             const int d = idx / NC, h = idx - d * NC;   // V_h <-> x_{h+1}

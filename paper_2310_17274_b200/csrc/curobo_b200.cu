@@ -769,6 +769,9 @@ KParams base_params(const crb_ctx *ctx) {
     k.dt = c.dt; k.sweep_steps = c.sweep_steps; k.flags = c.flags;
     k.inv_eta = 1.0f / c.eta;
     k.inv_2dt = 1.0f / (2.0f * c.dt);
+    k.inv_12dt = (float)(1.0 / (12.0 * c.dt));
+    k.inv_12dt2 = (float)(1.0 / (12.0 * (double)c.dt * c.dt));
+    k.inv_2dt3 = (float)(1.0 / (2.0 * (double)c.dt * c.dt * c.dt));
     return kp;
 }
 

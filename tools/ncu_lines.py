@@ -22,6 +22,7 @@ for r in rows:
         continue
     if r[0]:
         line_no = r[0]; src_line = r[1]
+        continue                  # source rows repeat the sum of their SASS rows: count SASS only
     try:
         ins = int(r[ii] or 0); smp = int(r[si] or 0)
     except ValueError:

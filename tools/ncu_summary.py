@@ -19,7 +19,8 @@ for r in rows:
         hdr = r; ii = hdr.index("Instructions Executed"); si = hdr.index("Warp Stall Sampling (All Samples)")
         sidx = [i for i, h in enumerate(hdr) if h.startswith('stall_') and 'Not Issued' not in h]; continue
     if hdr is None or len(r) < len(hdr): continue
-    if r[0]: ln = int(r[0])
+    if r[0]:
+        ln = int(r[0]); continue        # source rows repeat the sum of their SASS rows
     try: n = int(r[ii] or 0); sm = int(r[si] or 0)
     except ValueError: continue
     agg[(cur, ln)] += n; smp[(cur, ln)] += sm
@@ -28,7 +29,7 @@ for r in rows:
         except ValueError: pass
 ts = sum(stall.values())
 print("  stalls: " + " ".join(f"{k}={100*v/ts:.1f}%" for k, v in stall.most_common(8)))
-srcf = open('/root/repo/paper_2310_17274_b200/csrc/crb_device.cuh').read().split('\n')
+srcf = open(sys.argv[2] if len(sys.argv) > 2 else '/root/repo/paper_2310_17274_b200/csrc/crb_device.cuh').read().split('\n')
 marks = []
 for i, l in enumerate(srcf):
     m = re.match(r'^__device__ .*?(\w+)\(', l)
