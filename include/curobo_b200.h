@@ -20,7 +20,7 @@
  *   - Non-finite inputs are not scanned: a NaN propagates into the cost, a NaN cost packs to the
  *     +inf key and never wins a selection (SURVEY §8(b) deviation).
  *   - Capacity limits (CRB_E_LIMIT): D <= 16, L <= 32, M <= 512, pairs <= 16384, H*D <= 512,
- *     history <= 16, n_alpha <= 8, TO mode requires 8 <= H <= 32, IK mode has H == 1, and the
+ *     history <= 32, n_alpha <= 8, TO mode requires 8 <= H <= 32, IK mode has H == 1, and the
  *     per-CTA shared memory (robot tables + one environment's cuboids + solver state) must fit
  *     in 227 KB.
  */
@@ -54,7 +54,9 @@ enum { CRB_FIXED = 0, CRB_PRISMATIC_X = 1, CRB_PRISMATIC_Y = 2, CRB_PRISMATIC_Z 
 /* Cost flags. */
 enum { CRB_SWEEP = 1u,   /* continuous collision checking, §3.4 / Algs. 11-12     */
        CRB_SPEED = 2u,   /* speed metric d_s = sdot * d_c, §3.3                    */
-       CRB_JERK = 4u };  /* alpha_9 jerk term of Eq. smooth_cost (off in the 1st TO) */
+       CRB_JERK = 4u,    /* alpha_9 jerk term of Eq. smooth_cost (off in the 1st TO) */
+       CRB_CSPACE = 8u };/* goal term = Eq. cspace-cost on a joint-space goal
+                            theta_g[D] instead of Eq. pose_cost_term on a pose[7]             */
 
 /* One link of the kinematic tree (Alg. 7 kinematic data). */
 typedef struct {
@@ -100,13 +102,14 @@ typedef struct {
     float eta_bound;           /* eta_2 of Eq. bound_cost: 0.1                        */
     float dt;                  /* timestep of the five-point stencil (§A.5) and speed metric   */
     int sweep_steps;           /* n_s of Alg. 12 (never given in the paper; 4, A11)            */
-    unsigned flags;            /* CRB_SWEEP | CRB_SPEED | CRB_JERK                             */
+    unsigned flags;            /* CRB_SWEEP | CRB_SPEED | CRB_JERK | CRB_CSPACE                */
+    float a4, a5;              /* Eq. cspace-cost: 5000, 50                            */
 } crb_cost_params;
 
 /* L-BFGS + parallel noisy line search (Alg. 6, Alg. 1). */
 typedef struct {
     int iters;                 /* L-BFGS iterations after the initial evaluation (100) */
-    int history;               /* m (4), <= 16                                         */
+    int history;               /* m (4), 0..32; 0 = gradient descent d = -g  */
     int n_alpha;               /* number of magnitudes, <= 8                                    */
     float alpha[8];            /* ascending; alpha[0] is the noisy fallback    */
     float c1, c2;              /* Armijo / Wolfe constants (A17: 1e-4, 0.9)                    */
@@ -158,7 +161,8 @@ crb_status crb_fk(crb_ctx *ctx, const float *q, int B, float *spheres_out, float
  *   H == 1 (IK mode): q[B][D] configurations; pose + self + discrete world + position bound.
  *     The env index must be constant inside each aligned group of 32 rows (rows that violate it
  *     get a NaN cost).  start may be NULL.
- *   env[B] (may be NULL = all 0), goal[B][7] (position, quaternion w,x,y,z).
+ *   env[B] (may be NULL = all 0), goal[B][7] (position, quaternion w,x,y,z), or goal[B][D]
+ *   (joint configuration) when the cost flags include CRB_CSPACE.
  *   term_costs[B][5] (pose, bound, smooth, self, world) may be NULL. */
 crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, const int *env,
                                   const float *start, const float *goal, float *cost,
@@ -167,7 +171,7 @@ crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, co
 /* Per-seed L-BFGS solve (§4.1, Alg. 6 + Alg. 1), one persistent CTA per seed trajectory (TO) or
  * per 32 seeds of one problem (IK), all `iters` iterations inside one launch.
  *   seeds[P][S][H][D] (TO, H >= 8) or [P][S][D] (IK, H == 1); env[P] (may be NULL);
- *   start[P][D] (TO only); goal[P][7].
+ *   start[P][D] (TO only); goal[P][7] (pose) or goal[P][D] (CRB_CSPACE).
  * Outputs (any may be NULL): best_traj[P][H][D] and best_cost[P] of the winning seed per
  * problem; best_key[P] = (float_bits(cost) << 32) | (global_seed_base + s), the packed key the
  * multi-GPU argmin reduces with MIN (NaN -> +inf bits); seed_best_cost[P][S] and
@@ -202,7 +206,7 @@ crb_status crb_argmin_keys(int P, int S, const float *cost, int64_t seed_base, i
 
 /* Two-loop recursion (Alg. 6) exactly as run inside the solver: for each of B problems with n
  * variables and `count` stored pairs (oldest first), d = -H g.  Device pointers:
- * S[B][count][n], Y[B][count][n], g[B][n], d[B][n].  n <= 512, count <= 16. */
+ * S[B][count][n], Y[B][count][n], g[B][n], d[B][n].  n <= 512, count <= 32. */
 crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const float *Y,
                                const float *g, float *d, void *stream);
 

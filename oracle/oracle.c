@@ -440,6 +440,18 @@ double orc_logcosh(double x) {
     return ax + log1p(exp(-2.0 * ax)) - log(2.0);
 }
 
+/* Eq. cspace-cost, the goal cost "for tasks that require reaching a joint
+ * configuration": C = a4 logcosh(a5 ||theta_g - theta_T||_2^2);
+ * dC/dtheta_T = a4 a5 tanh(a5 ||.||^2) * 2 (theta_T - theta_g). */
+double orc_cspace_cost(const orc_params *pr, int D, const double *q, const double *goal, double *g) {
+    double s = 0.0;
+    for (int d = 0; d < D; ++d) s += (goal[d] - q[d]) * (goal[d] - q[d]);
+    double C = pr->a4 * orc_logcosh(pr->a5 * s);
+    if (g)
+        for (int d = 0; d < D; ++d) g[d] = pr->a4 * pr->a5 * tanh(pr->a5 * s) * 2.0 * (q[d] - goal[d]);
+    return C;
+}
+
 /* Eq. pose_cost_term with reading A1: e_r = 1 - |<q_g, q>|. */
 double orc_pose_cost(const orc_params *pr, const double *ee, const double *goal, double *gp,
                      double *gq) {
@@ -572,13 +584,20 @@ double orc_eval_traj(const orc_robot *rb, const orc_world *w, const orc_params *
             tm[4] += pr->beta_world * sp * E;
             for (int i = 0; i < 3; ++i) gs[(h * M + m) * 3 + i] += pr->beta_world * sp * G[i];
         }
-    /* pose at x_H (Eq. pose_cost_term) */
+    /* goal term at x_H: Eq. pose_cost_term, or Eq. cspace-cost (goal = theta_g[D]) */
     double gp[3], gq[4];
-    tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
-    if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
+    int cspace = (pr->flags & ORC_CSPACE) != 0;
+    if (cspace) {
+        tm[0] = orc_cspace_cost(pr, D, XR(H), goal, tmp);
+        for (int d = 0; d < D; ++d) GX(H)[d] += tmp[d];
+    } else {
+        tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
+        if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
+    }
     /* backward (O6) per evaluated configuration */
     for (int h = 1; h <= H; ++h) {
-        orc_fk_backward(rb, XR(h), gs + h * M * 3, (h == H) ? gp : NULL, (h == H) ? gq : NULL, tmp);
+        int pose = (h == H) && !cspace;
+        orc_fk_backward(rb, XR(h), gs + h * M * 3, pose ? gp : NULL, pose ? gq : NULL, tmp);
         for (int d = 0; d < D; ++d) GX(h)[d] += tmp[d];
     }
     /* transposed stencil: chain rule through O3 */
@@ -632,12 +651,19 @@ double orc_eval_ik(const orc_robot *rb, const orc_world *w, const orc_params *pr
         for (int i = 0; i < 3; ++i) gs[m * 3 + i] += pr->beta_world * G[i];
     }
     double gp[3], gq[4];
-    tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
-    if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
-    if (grad) {
-        orc_fk_backward(rb, q, gs, gp, gq, grad);
-        for (int d = 0; d < D; ++d) grad[d] += gb[d];
+    int cspace = (pr->flags & ORC_CSPACE) != 0;
+    double *gc = calloc(D, sizeof(double));
+    if (cspace) {
+        tm[0] = orc_cspace_cost(pr, D, q, goal, gc);          /* Eq. cspace-cost */
+    } else {
+        tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
+        if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
     }
+    if (grad) {
+        orc_fk_backward(rb, q, gs, cspace ? NULL : gp, cspace ? NULL : gq, grad);
+        for (int d = 0; d < D; ++d) grad[d] += gb[d] + gc[d];
+    }
+    free(gc);
     if (terms) memcpy(terms, tm, sizeof(tm));
     free(sph); free(gs); free(gb);
     return tm[0] + tm[1] + tm[2] + tm[3] + tm[4];
@@ -846,7 +872,7 @@ void orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double
             double *s = malloc(sizeof(double) * n), *y = malloc(sizeof(double) * n);
             for (int t = 0; t < n; ++t) { s[t] = x[t] - xp[t]; y[t] = g[t] - gpv[t]; }
             double sy = dot(n, s, y);
-            if (sy > 1e-12) {                             /* A20 */
+            if (m > 0 && sy > 1e-12) {                    /* A20; m = 0 is gradient descent */
                 if (count == m) {                         /* shift buffers (Alg. 6 line 1) */
                     memmove(S, S + n, sizeof(double) * (size_t)(m - 1) * n);
                     memmove(Y, Y + n, sizeof(double) * (size_t)(m - 1) * n);

@@ -39,7 +39,7 @@ typedef struct {
     const int *enabled;      /* [K]                                                  */
 } orc_world;
 
-enum { ORC_SWEEP = 1, ORC_SPEED = 2, ORC_JERK = 4 };
+enum { ORC_SWEEP = 1, ORC_SPEED = 2, ORC_JERK = 4, ORC_CSPACE = 8 };
 
 typedef struct {
     double a0, a1, a2, a3, a8, a9;   /* Eq. pose_cost_term, Eq. smooth_cost */
@@ -47,7 +47,9 @@ typedef struct {
     double beta_self, beta_world;    /* beta_1 (Eq. self-collision), beta_2 (Eq. world-collision-cost) */
     double eta, eta_bound, dt;       /* eta, eta_2, timestep                        */
     int sweep_steps;                 /* n_s (A11)                                                      */
-    int flags;                       /* ORC_SWEEP | ORC_SPEED | ORC_JERK                               */
+    int flags;                       /* ORC_SWEEP | ORC_SPEED | ORC_JERK | ORC_CSPACE                  */
+    double a4, a5;                   /* Eq. cspace-cost: 5000, 50; goal = theta_g[D] when
+                                        ORC_CSPACE is set, else the pose (p, q) [7]                  */
 } orc_params;
 
 /* O11 particle warm-up (Alg. 5; Eqs. particle_1/2 P:192-199; readings B6-B10). */
@@ -91,6 +93,7 @@ double orc_box_sdf(const double *p, const double *pos, const double *quat, const
 double orc_activation(double dprime, double eta, double *dphi);
 double orc_bound(double x, double lo, double hi, double eta2, double *dx);
 double orc_logcosh(double x);
+double orc_cspace_cost(const orc_params *pr, int D, const double *q, const double *goal, double *g);
 double orc_pose_cost(const orc_params *pr, const double *ee, const double *goal, double *gp,
                      double *gq);
 double orc_self_collision(const orc_robot *rb, const double *spheres, double beta, double *g,

@@ -53,7 +53,7 @@ class _Params(C.Structure):
                 ("a8", C.c_double), ("a9", C.c_double), ("w_bound", C.c_double * 4),
                 ("beta_self", C.c_double), ("beta_world", C.c_double), ("eta", C.c_double),
                 ("eta_bound", C.c_double), ("dt", C.c_double), ("sweep_steps", C.c_int),
-                ("flags", C.c_int)]
+                ("flags", C.c_int), ("a4", C.c_double), ("a5", C.c_double)]
 
 
 class _Particle(C.Structure):
@@ -152,7 +152,7 @@ class World:
 def params(cp):
     return _Params(cp.a0, cp.a1, cp.a2, cp.a3, cp.a8, cp.a9, (C.c_double * 4)(*cp.w_bound),
                    cp.beta_self, cp.beta_world, cp.eta, cp.eta_bound, cp.dt, int(cp.sweep_steps),
-                   int(cp.flags))
+                   int(cp.flags), cp.a4, cp.a5)
 
 
 def particle(sp):
@@ -257,6 +257,17 @@ def derivs(x, H, dt):
     lib().orc_derivs.argtypes = [D_P, C.c_int, C.c_int, C.c_double, D_P, D_P, D_P]
     lib().orc_derivs(_dp(x), H, D, float(dt), _dp(v), _dp(a), _dp(j))
     return v, a, j
+
+
+def cspace_cost(cp, q, goal):
+    q = _d(q); goal = _d(goal)
+    g = np.zeros_like(q)
+    L = lib()
+    L.orc_cspace_cost.restype = C.c_double
+    L.orc_cspace_cost.argtypes = [C.POINTER(_Params), C.c_int, D_P, D_P, D_P]
+    pr = params(cp)
+    c = L.orc_cspace_cost(C.byref(pr), q.shape[0], _dp(q), _dp(goal), _dp(g))
+    return c, g
 
 
 def eval_traj(robot: Robot, world: World, cp, start, goal, V):

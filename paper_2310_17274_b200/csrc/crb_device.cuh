@@ -22,7 +22,7 @@ constexpr int NW = NT / 32;      // warps per CTA
 constexpr int NC = 32;           // configuration slots per pass (= lanes)
 constexpr unsigned FULL = 0xffffffffu;
 
-enum : unsigned { F_SWEEP = 1u, F_SPEED = 2u, F_JERK = 4u };
+enum : unsigned { F_SWEEP = 1u, F_SPEED = 2u, F_JERK = 4u, F_CSPACE = 8u };
 enum { MODE_TO = 0, MODE_IK = 1 };
 
 // Packed robot tables (built by the host in crb_set_robot).  Offsets are in 4-byte words from
@@ -61,7 +61,9 @@ struct CostP {
     float a0, a1, a2, a3, a8, a9, wb[4], beta_self, beta_world, eta, eta_bound, dt;
     float inv_eta, inv_2dt;   // host-computed reciprocals (no divisions in the hot loops)
     float inv_12dt, inv_12dt2, inv_2dt3;   // five-point stencil scales 1/(12 dt), 1/(12 dt^2), 1/(2 dt^3)
+    float a4, a5;             // Eq. cspace-cost
     int sweep_steps, H;
+    int gw;                   // goal row width: 7 (pose) or D (F_CSPACE)
     unsigned flags;
 };
 
@@ -683,7 +685,20 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         const int c = lane;
         const bool on = (MODE == MODE_TO) ? (c == H - 1) : (c < n_act);
         float ft[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, C = 0.f;
-        if (on) {
+        if (on && (cf.flags & F_CSPACE)) {
+            // Eq. cspace-cost: C = a4 logcosh(a5 |theta_g - theta_T|^2); its joint-space gradient
+            // a4 a5 tanh(a5 s) 2 (theta_T - theta_g) joins the position-bound gradient gxd (a8
+            // finished before the placement barrier), so it skips the FK backward
+            float sq = 0.f;
+            for (int d = 0; d < D; ++d) {
+                const float e = s.q_cfg[d * NC + c] - s.goal[d * NC + c];
+                sq = fmaf(e, e, sq);
+            }
+            C = cf.a4 * logcoshf(cf.a5 * sq);
+            const float k2 = 2.f * cf.a4 * cf.a5 * tanhf(cf.a5 * sq);
+            for (int d = 0; d < D; ++d)
+                s.gxd[d * NC + c] += k2 * (s.q_cfg[d * NC + c] - s.goal[d * NC + c]);
+        } else if (on) {
             const float *E = ee_frame(s, D) + c;
             const float px = E[9 * NC], py = E[10 * NC], pz = E[11 * NC];
             float q[4];

@@ -34,7 +34,7 @@ __device__ void two_loop_block(int N, int Np, int count, const int *order, const
                                const float *rho, const float *syv, const float *yyv, const float *g, float *d,
                                float *red, int &ph) {
     const int t0 = threadIdx.x, t1 = threadIdx.x + NT;
-    float al[16];
+    float al[32];
     float q0 = t0 < N ? g[t0] : 0.f, q1 = t1 < N ? g[t1] : 0.f;
 #pragma unroll 1
     for (int i = count - 1; i >= 0; --i) {
@@ -78,15 +78,15 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
     float *base = smem + kp.lay.solver;
     float *th = base, *g = th + Np, *dd = g + Np, *thp = dd + Np, *gp = thp + Np, *best = gp + Np,
           *thA = best + Np, *cg = thA + Np, *Sb = cg + A * Np, *Yb = Sb + (m + 1) * Np,
-          *rho = Yb + (m + 1) * Np, *syv = rho + 20, *yyv = syv + 20;
-    int *order = reinterpret_cast<int *>(yyv + 20);
-    float *scal = yyv + 40;           // [0..7] c_a, [8..15] gd_a, [17] i*
+          *rho = Yb + (m + 1) * Np, *syv = rho + 40, *yyv = syv + 40;   // m + 1 <= 33 slots each
+    int *order = reinterpret_cast<int *>(yyv + 40);
+    float *scal = yyv + 80;           // [0..7] c_a, [8..15] gd_a, [17] i*
     int *ring = reinterpret_cast<int *>(scal + 24);   // [0] count, [1] free slot
     const float *lim = s.fw + kp.rp.o_lim;
     int ph = 0;
 
     if (t < D) s.st[t] = kp.start[p * D + t];
-    if (t < 7 * NC) s.goal[t] = kp.goal[p * 7 + t / NC];
+    if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[p * kp.cp.gw + t / NC];
     const float *seed = kp.q_in + (size_t)unit * N;
     float lo_e[2], hi_e[2];
 #pragma unroll
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
                 }
                 const float sy = block_sum(sy_p, s.red, ph);
                 const float yy = block_sum(yy_p, s.red, ph);
-                if (sy > 1e-12f && t == 0) {
+                if (m > 0 && sy > 1e-12f && t == 0) {   // m = 0: gradient descent
                     rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
                     const int cnt = ring[0];
                     if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
     const int sd = grp * NC + lane;
     const bool active = lane < n_act;
 
-    if (t < 7 * NC) s.goal[t] = kp.goal[p * 7 + t / NC];
+    if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[p * kp.cp.gw + t / NC];
     if (warp == 0)
         for (int d = 0; d < D; ++d) {
             const float v = active ? kp.q_in[((size_t)p * kp.S + sd) * D + d] : lim[d];
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
                     Sb[fs * DC + e] = sv; Yb[fs * DC + e] = yv;
                     sy += sv * yv; yy += yv * yv;
                 }
-                if (sy > 1e-12f) {
+                if (m > 0 && sy > 1e-12f) {
                     rho[fs * NC + lane] = 1.f / sy; syv[fs * NC + lane] = sy; yyv[fs * NC + lane] = yy;
                     if (cnt < m) { order[cnt * NC + lane] = fs; ++cnt; fs = cnt; }
                     else {
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             }
             for (int d = 0; d < D; ++d) { thp[d * NC + lane] = th[d * NC + lane]; gp[d * NC + lane] = g[d * NC + lane]; }
             // ---- two-loop recursion per seed (Alg. 6)
-            float q[16], al[16];
+            float q[16], al[32];
             for (int d = 0; d < D; ++d) q[d] = g[d * NC + lane];
             for (int i = cnt - 1; i >= 0; --i) {
                 const int sl = order[i * NC + lane];
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ 
     const int D = kp.rp.D, H = kp.H, N = H * D, t = threadIdx.x;
     float *thA = smem + kp.lay.solver;
     if (t < D) s.st[t] = kp.start[(size_t)b * D + t];
-    if (t < 7 * NC) s.goal[t] = kp.goal[(size_t)b * 7 + t / NC];
+    if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[(size_t)b * kp.cp.gw + t / NC];
     for (int i = t; i < N; i += NT) thA[i] = kp.q_in[(size_t)b * N + i];
     __syncthreads();
     eval_pass<MODE_TO>(kp, smem, thA, K, H, nullptr);
@@ -505,7 +505,9 @@ __global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ 
     if (warp == 0) {
         const bool act = lane < n_act;
         for (int d = 0; d < D; ++d) s.q_cfg[d * NC + lane] = act ? kp.q_in[(size_t)(b0 + lane) * D + d] : lim[d];
-        for (int k = 0; k < 7; ++k) s.goal[k * NC + lane] = act ? kp.goal[(size_t)(b0 + lane) * 7 + k] : (k == 3 ? 1.f : 0.f);
+        const int gw = kp.cp.gw;
+        for (int k = 0; k < gw; ++k)
+            s.goal[k * NC + lane] = act ? kp.goal[(size_t)(b0 + lane) * gw + k] : (k == 3 && gw == 7 ? 1.f : 0.f);
     }
     __syncthreads();
     prep_sincos(s, D);
@@ -733,7 +735,7 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.gva = take(mode == MODE_TO ? 3 * D * NC : 4);
     L.pose_ft = take(6 * NC);
     L.pose_c = take(NC);
-    L.goal = take(7 * NC);
+    L.goal = take(std::max(7, D) * NC);   // pose [7][32] or joint-space goal [D][32] (CRB_CSPACE)
     L.cfg_cost = take(NC);
     L.cfg_terms = take(5 * NC);
     L.gV = take(std::max(H * D, D * NC));
@@ -743,7 +745,7 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.solver = w;
     const int N = H * D, Np = r4(N), DC = D * NC;
     if (mode == MODE_TO) {
-        if (solver) w += 7 * Np + A * Np + 2 * (m + 1) * Np + 128;   // + rho/syv/yyv/order/scal/ring tail
+        if (solver) w += 7 * Np + A * Np + 2 * (m + 1) * Np + 192;   // + rho/syv/yyv/order/scal/ring tail
         else w += Np + 8;
     } else if (solver) {
         w += 6 * DC + 2 * (m + 1) * DC + 3 * (m + 1) * NC + A * DC + 2 * A * NC + (m + 1) * NC;
@@ -767,6 +769,8 @@ KParams base_params(const crb_ctx *ctx) {
     for (int i = 0; i < 4; ++i) k.wb[i] = c.w_bound[i];
     k.beta_self = c.beta_self; k.beta_world = c.beta_world; k.eta = c.eta; k.eta_bound = c.eta_bound;
     k.dt = c.dt; k.sweep_steps = c.sweep_steps; k.flags = c.flags;
+    k.a4 = c.a4; k.a5 = c.a5;
+    k.gw = (c.flags & CRB_CSPACE) ? ctx->rp.D : 7;
     k.inv_eta = 1.0f / c.eta;
     k.inv_2dt = 1.0f / (2.0f * c.dt);
     k.inv_12dt = (float)(1.0 / (12.0 * c.dt));
@@ -1157,8 +1161,8 @@ crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int
     if (st != CRB_OK) return st;
     if ((st = ready(ctx, true)) != CRB_OK) return st;
     if (!sp || !seeds || !goal || P < 0 || S < 1) return fail(ctx, CRB_E_ARG, "bad solve arguments");
-    if (sp->history < 1 || sp->history > 16 || sp->n_alpha < 1 || sp->n_alpha > 8 || sp->iters < 0)
-        return fail(ctx, CRB_E_LIMIT, "history must be in [1,16], n_alpha in [1,8], iters >= 0");
+    if (sp->history < 0 || sp->history > 32 || sp->n_alpha < 1 || sp->n_alpha > 8 || sp->iters < 0)
+        return fail(ctx, CRB_E_LIMIT, "history must be in [0,32] (0 = gradient descent), n_alpha in [1,8], iters >= 0");
     if (sp->particle_iters < 0 ||
         (sp->particle_iters > 0 && (sp->n_particles < 1 || !(sp->particle_beta > 0.f) || !(sp->k_mu >= 0.f) ||
                                     !(sp->k_mu <= 1.f) || !(sp->k_sigma >= 0.f) || !(sp->k_sigma <= 1.f) ||
@@ -1207,14 +1211,15 @@ crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P
     const int D = ctx->rp.D, N = H * D;
     cudaStream_t s = (cudaStream_t)stream;
     if ((st = grow(ctx, &ctx->h_seeds, &ctx->cap_h_seeds, (size_t)P * S * N)) != CRB_OK) return st;
-    if ((st = grow(ctx, &ctx->h_goal, &ctx->cap_h_goal, (size_t)P * 7)) != CRB_OK) return st;
+    const int gw = (ctx->cp.flags & CRB_CSPACE) ? D : 7;
+    if ((st = grow(ctx, &ctx->h_goal, &ctx->cap_h_goal, (size_t)P * gw)) != CRB_OK) return st;
     if ((st = grow(ctx, &ctx->h_best, &ctx->cap_h_best, (size_t)P * N)) != CRB_OK) return st;
     if ((st = grow(ctx, &ctx->h_bcost, &ctx->cap_h_bcost, (size_t)P)) != CRB_OK) return st;
     if ((st = grow(ctx, &ctx->h_key, &ctx->cap_h_key, (size_t)P)) != CRB_OK) return st;
     if (start && (st = grow(ctx, &ctx->h_start, &ctx->cap_h_start, (size_t)P * D)) != CRB_OK) return st;
     if (env && (st = grow(ctx, &ctx->h_env, &ctx->cap_h_env, (size_t)P)) != CRB_OK) return st;
     st = cuda_check(ctx, cudaMemcpyAsync(ctx->h_seeds, seeds, (size_t)P * S * N * 4, cudaMemcpyHostToDevice, s), "H2D seeds");
-    if (st == CRB_OK) st = cuda_check(ctx, cudaMemcpyAsync(ctx->h_goal, goal, (size_t)P * 7 * 4, cudaMemcpyHostToDevice, s), "H2D goal");
+    if (st == CRB_OK) st = cuda_check(ctx, cudaMemcpyAsync(ctx->h_goal, goal, (size_t)P * gw * 4, cudaMemcpyHostToDevice, s), "H2D goal");
     if (st == CRB_OK && start) st = cuda_check(ctx, cudaMemcpyAsync(ctx->h_start, start, (size_t)P * D * 4, cudaMemcpyHostToDevice, s), "H2D start");
     if (st == CRB_OK && env) st = cuda_check(ctx, cudaMemcpyAsync(ctx->h_env, env, (size_t)P * 4, cudaMemcpyHostToDevice, s), "H2D env");
     if (st != CRB_OK) return st;
@@ -1267,7 +1272,7 @@ crb_status crb_argmin_keys(int P, int S, const float *cost, int64_t seed_base, i
 
 crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const float *Y, const float *g, float *d,
                                void *stream) {
-    if (B < 0 || n < 1 || n > 2 * NT || count < 0 || count > 16 || !g || !d || (count > 0 && (!S || !Y))) return CRB_E_ARG;
+    if (B < 0 || n < 1 || n > 2 * NT || count < 0 || count > 32 || !g || !d || (count > 0 && (!S || !Y))) return CRB_E_ARG;
     if (B == 0) return CRB_OK;
     const int Np = (n + 3) & ~3;
     const size_t bytes = (size_t)(2 * count * Np + 2 * Np + 48 + 3 * NW + 16) * 4;

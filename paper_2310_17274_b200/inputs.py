@@ -18,7 +18,7 @@ from typing import Callable, Optional, Sequence
 import numpy as np
 
 # flags (same bit meaning in the oracle and the C-ABI; each side defines its own constants)
-SWEEP, SPEED, JERK = 1, 2, 4
+SWEEP, SPEED, JERK, CSPACE = 1, 2, 4, 8
 
 STREAM_SCENE, STREAM_CONFIG, STREAM_SEED, STREAM_IK, STREAM_TEST = 1, 2, 3, 4, 5
 
@@ -94,6 +94,8 @@ class CostParams:
     dt: float = 0.25
     sweep_steps: int = 4
     flags: int = SWEEP | SPEED
+    a4: float = 5000.0        # Eq. cspace-cost, used when flags & CSPACE
+    a5: float = 50.0
 
 
 @dataclasses.dataclass

@@ -56,7 +56,8 @@ class crb_cost_params(C.Structure):
     _fields_ = [("a0", C.c_float), ("a1", C.c_float), ("a2", C.c_float), ("a3", C.c_float),
                 ("a8", C.c_float), ("a9", C.c_float), ("w_bound", C.c_float * 4),
                 ("beta_self", C.c_float), ("beta_world", C.c_float), ("eta", C.c_float),
-                ("eta_bound", C.c_float), ("dt", C.c_float), ("sweep_steps", C.c_int), ("flags", C.c_uint)]
+                ("eta_bound", C.c_float), ("dt", C.c_float), ("sweep_steps", C.c_int), ("flags", C.c_uint),
+                ("a4", C.c_float), ("a5", C.c_float)]
 
 
 class crb_solver_params(C.Structure):
@@ -117,7 +118,7 @@ def _check_free(code):
 def cost_params_struct(cp: inputs.CostParams) -> crb_cost_params:
     return crb_cost_params(cp.a0, cp.a1, cp.a2, cp.a3, cp.a8, cp.a9, (C.c_float * 4)(*cp.w_bound),
                            cp.beta_self, cp.beta_world, cp.eta, cp.eta_bound, cp.dt, int(cp.sweep_steps),
-                           int(cp.flags))
+                           int(cp.flags), cp.a4, cp.a5)
 
 
 def solver_params_struct(sp: inputs.SolverParams, seed_base: int = 0, problem_base: int = 0) -> crb_solver_params:

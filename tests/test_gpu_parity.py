@@ -290,7 +290,7 @@ def test_argmin_keys_bit_exact(native, O):
 
 # ------------------------------------------------------------------------------------------ two-loop
 
-@pytest.mark.parametrize("n,count", [(224, 0), (224, 1), (224, 4), (7, 4), (512, 16), (100, 3)])
+@pytest.mark.parametrize("n,count", [(224, 0), (224, 1), (224, 4), (7, 4), (512, 16), (100, 3), (224, 25), (512, 32)])
 def test_two_loop_teacher_forced(native, O, n, count):
     """The solver's two-loop routine on the GPU vs the oracle on identical fp32 inputs."""
     g = np.random.default_rng(n + count)
