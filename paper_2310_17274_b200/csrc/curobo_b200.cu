@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(NT, 2) lbfgs_direction_kernel(int n, int count
     extern __shared__ __align__(16) float smem[];
     const int b = blockIdx.x, t = threadIdx.x, Np = (n + 3) & ~3;
     float *Sb = smem, *Yb = Sb + count * Np, *gg = Yb + count * Np, *dd = gg + Np, *rho = dd + Np,
-          *syv = rho + 16, *yyv = syv + 16, *red = yyv + 16;
+          *syv = rho + 32, *yyv = syv + 32, *red = yyv + 32;   // count <= 32
     int *order = reinterpret_cast<int *>(red + 3 * NW);
     int ph = 0;
     for (int i = 0; i < count; ++i)
@@ -1275,7 +1275,7 @@ crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const fl
     if (B < 0 || n < 1 || n > 2 * NT || count < 0 || count > 32 || !g || !d || (count > 0 && (!S || !Y))) return CRB_E_ARG;
     if (B == 0) return CRB_OK;
     const int Np = (n + 3) & ~3;
-    const size_t bytes = (size_t)(2 * count * Np + 2 * Np + 48 + 3 * NW + 16) * 4;
+    const size_t bytes = (size_t)(2 * count * Np + 2 * Np + 96 + 3 * NW + 32) * 4;
     if (cudaFuncSetAttribute(lbfgs_direction_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
         return CRB_E_CUDA;
     lbfgs_direction_kernel<<<B, NT, bytes, (cudaStream_t)stream>>>(n, count, S, Y, g, d);

@@ -31,13 +31,15 @@ def test_cspace_eval_to_parity(native, O, H):
     cost, grad, terms = ctx.evaluate(T(V), T(gl), start=T(st), env=T(env, torch.int32))
     cost, grad, terms = cost.cpu().numpy(), grad.cpu().numpy(), terms.cpu().numpy()
     stats = Stats()
+    active = 0
     for b in range(B):
         c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"traj {b}")
         if margin >= 2e-5:
             assert terms[b, 0] == pytest.approx(t_ref[0], rel=1e-4, abs=1e-3)
-        assert t_ref[0] > 0
+        active += t_ref[0] > 0
     stats.done()
+    assert active >= B // 2            # the goal term is live (seed 0 of each pair ends on the goal)
     ctx.close()
 
 
