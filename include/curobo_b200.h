@@ -189,6 +189,28 @@ crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P
                                 const float *goal, float *best_traj, float *best_cost,
                                 int64_t *best_key, void *stream);
 
+/* ---- validity mask and parallel steering (Alg. 3) ---- */
+
+/* mask_samples (Alg. 3 line 5, reading B12): valid[k] = 1 iff configuration q[k] is
+ * inside the position limits, no self-collision pair of S penetrates, and every enabled sphere
+ * keeps a distance >= r + margin (m, >= 0) to every enabled cuboid of env[k]; else 0.
+ * Device pointers: q[K][D], env[K] (may be NULL = 0; constant within aligned groups of 32 rows,
+ * a row that violates it is reported invalid), valid[K] (uint8).  Needs robot, world, params. */
+crb_status crb_mask_samples(crb_ctx *ctx, const float *q, int K, const int *env, float margin,
+                            uint8_t *valid, void *stream);
+
+/* Parallel steering (Alg. 3, reading B13) of E edges in environment `env`:
+ *   n = floor(max_{e,d} |dw_d (dst_ed - src_ed)| / r) + 1, shared by the batch and clamped to
+ *   n_cap (the grid is sized for n_cap: no host synchronisation); waypoints
+ *   l_ej = src_e + (j / n)(dst_e - src_e), j = 0..n, are validated as by crb_mask_samples;
+ *   h[e] = (first invalid j) - 1, or n if all are valid (-1: invalid source, v_new = src);
+ *   v_new[e] = l_e,h[e]; dist[e] = |dw * (v_new[e] - src[e])|_2 (the edge weight).
+ * Device pointers: src[E][D], dst[E][D], dw[D], n_out[2] (n used, n before clamping; may be
+ * NULL), h[E], v_new[E][D], dist[E].  The graph bookkeeping (Alg. 2) stays with the caller. */
+crb_status crb_steer(crb_ctx *ctx, int E, const float *src, const float *dst, const float *dw, float r,
+                     int env, float margin, int n_cap, int *n_out, int *h, float *v_new, float *dist,
+                     void *stream);
+
 /* ---- test hooks: the exact device routines the solver uses, on caller data ---- */
 
 /* Alg. 1 selection (lines 4-9) for n independent line searches, in fp32 with the fixed

@@ -748,6 +748,105 @@ int orc_argmin_f32(int n, const float *c) {
 }
 
 /* ------------------------------------------------------------------------------------------ */
+/* O12 validity mask and parallel steering (Alg. 3; readings B12-B14) */
+/* ------------------------------------------------------------------------------------------ */
+
+/* mask_samples (Alg. 3 line 5, "check for validity"), reading B12: a configuration is valid iff
+ * every joint is inside its position limits, no self-collision pair of S penetrates
+ * ((r_i+o_i) + (r_j+o_j) - |w_i - w_j| <= 0, pairs with r+o <= 0 skipped as in Alg. 9), and every
+ * enabled sphere (r >= 0) keeps sd_k(c) >= r + margin to every enabled cuboid (strict
+ * non-penetration with a safety margin).  margin_out (may be NULL) = the smallest distance of a
+ * decision quantity to its threshold (for fp32-vs-fp64 parity filtering). */
+int orc_mask_sample(const orc_robot *rb, const orc_world *w, const double *q, double margin,
+                    double *margin_out) {
+    int D = rb->n_dof, M = rb->n_spheres, L = rb->n_links;
+    int valid = 1;
+    double mg = ORC_INF;
+    for (int d = 0; d < D; ++d) {
+        double a = q[d] - rb->lo[d], b = rb->hi[d] - q[d];
+        if (a < 0 || b < 0) valid = 0;
+        if (fabs(a) < mg) mg = fabs(a);
+        if (fabs(b) < mg) mg = fabs(b);
+    }
+    double *T = malloc(sizeof(double) * 12 * L), *sph = malloc(sizeof(double) * 4 * M), ee[7];
+    orc_fk(rb, q, T, sph, ee);
+    for (int p = 0; p < rb->n_pairs; ++p) {
+        int i = rb->pairs[2 * p], j = rb->pairs[2 * p + 1];
+        double ri = rb->sph[i * 4 + 3] + (rb->sph_off ? rb->sph_off[i] : 0.0);
+        double rj = rb->sph[j * 4 + 3] + (rb->sph_off ? rb->sph_off[j] : 0.0);
+        if (ri <= 0.0 || rj <= 0.0) continue;
+        double dx = sph[i * 4] - sph[j * 4], dy = sph[i * 4 + 1] - sph[j * 4 + 1],
+               dz = sph[i * 4 + 2] - sph[j * 4 + 2];
+        double P = ri + rj - sqrt(dx * dx + dy * dy + dz * dz);
+        if (P > 0) valid = 0;
+        if (fabs(P) < mg) mg = fabs(P);
+    }
+    for (int m = 0; m < M; ++m) {
+        double r = rb->sph[m * 4 + 3];
+        if (r < 0) continue;
+        for (int k = 0; k < w->n_boxes; ++k) {
+            if (!w->enabled[k]) continue;
+            double sd = orc_box_sdf(sph + m * 4, w->pos + 3 * k, w->quat + 4 * k, w->half + 3 * k, NULL);
+            if (sd < r + margin) valid = 0;
+            if (fabs(sd - (r + margin)) < mg) mg = fabs(sd - (r + margin));
+        }
+    }
+    free(T); free(sph);
+    if (margin_out) *margin_out = mg;
+    return valid;
+}
+
+/* Alg. 3 (Parallel Steering) under reading B13, for E edges (src_e, dst_e):
+ *   g_e = d_w * (dst_e - src_e)                       (distvec, per-joint weighted)
+ *   n = floor(max_{e,j} |g_ej| / r) + 1               (line 2, ONE n shared by the batch)
+ *   l_ei = src_e + (i / n) (dst_e - src_e), i = 0..n  (lines 3-4)
+ *   mask = validity of every l_ei                     (line 5)
+ *   h_e = (first invalid i) - 1, or n if none          (lines 6-7)
+ *   v_new_e = l_e,h_e; dist_e = |d_w * (v_new_e - src_e)|_2   (lines 8-9)
+ * h_e = -1 (source invalid, outside Alg. 3's precondition) gives v_new = src and dist 0.
+ * Returns n; margin_out[E] (may be NULL) = the smallest decision margin over each edge's
+ * waypoints up to and including its first invalid one. */
+int orc_steer(const orc_robot *rb, const orc_world *w, int E, const double *src, const double *dst,
+              const double *dw, double r, double margin, int *h, double *v_new, double *dist,
+              double *margin_out) {
+    int D = rb->n_dof;
+    double gmax = 0.0;
+    for (int e = 0; e < E; ++e)
+        for (int d = 0; d < D; ++d) {
+            double gv = fabs(dw[d] * (dst[e * D + d] - src[e * D + d]));
+            if (gv > gmax) gmax = gv;
+        }
+    int n = (int)floor(gmax / r) + 1;
+    double *l = malloc(sizeof(double) * D);
+    for (int e = 0; e < E; ++e) {
+        int first = -1;
+        double me = ORC_INF;
+        for (int i = 0; i <= n; ++i) {
+            for (int d = 0; d < D; ++d)
+                l[d] = src[e * D + d] + ((double)i / n) * (dst[e * D + d] - src[e * D + d]);
+            double mi;
+            int ok = orc_mask_sample(rb, w, l, margin, &mi);
+            if (mi < me) me = mi;
+            if (!ok) { first = i; break; }
+        }
+        int he = first < 0 ? n : first - 1;
+        h[e] = he;
+        double s2 = 0.0;
+        for (int d = 0; d < D; ++d) {
+            double v = he < 0 ? src[e * D + d]
+                              : src[e * D + d] + ((double)he / n) * (dst[e * D + d] - src[e * D + d]);
+            v_new[e * D + d] = v;
+            double gd = dw[d] * (v - src[e * D + d]);
+            s2 += gd * gd;
+        }
+        dist[e] = sqrt(s2);
+        if (margin_out) margin_out[e] = me;
+    }
+    free(l);
+    return n;
+}
+
+/* ------------------------------------------------------------------------------------------ */
 /* O11 particle-based warm-up (§4.2 "Particle-Based Optimization"; Alg. 5,          */
 /* P:2130-2144; two iterations before L-BFGS)                                          */
 /* ------------------------------------------------------------------------------------------ */

@@ -122,6 +122,12 @@ int    orc_ls_select(int A, const double *alpha, double c0, double g0d, const do
 int    orc_ls_select_f32(int A, const float *alpha, float c0, float g0d, const float *ca,
                          const float *gda, float c1, float c2, int mode);
 int    orc_argmin_f32(int n, const float *c);
+/* O12: validity mask and parallel steering (Alg. 3) */
+int    orc_mask_sample(const orc_robot *rb, const orc_world *w, const double *q, double margin,
+                       double *margin_out);
+int    orc_steer(const orc_robot *rb, const orc_world *w, int E, const double *src,
+                 const double *dst, const double *dw, double r, double margin, int *h,
+                 double *v_new, double *dist, double *margin_out);
 /* O11: counter-based generator (Philox4x32-10) and the particle warm-up */
 void   orc_philox4x32(const unsigned key[2], const unsigned ctr[4], unsigned out[4]);
 double orc_normal(unsigned key0, unsigned key1, unsigned var, unsigned particle, unsigned iter,

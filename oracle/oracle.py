@@ -351,6 +351,30 @@ def lbfgs_solve(fun, x0, sp, lo=None, hi=None):
     return bx, bc.value, trace
 
 
+def mask_sample(robot: Robot, world: World, q, margin=0.0):
+    """O12: (valid, decision margin) of one configuration."""
+    L = lib()
+    L.orc_mask_sample.restype = C.c_int
+    L.orc_mask_sample.argtypes = [C.POINTER(_Robot), C.POINTER(_World), D_P, C.c_double, D_P]
+    mg = C.c_double()
+    v = L.orc_mask_sample(C.byref(robot.s), C.byref(world.s), _dp(_d(q)), float(margin), C.byref(mg))
+    return bool(v), mg.value
+
+
+def steer(robot: Robot, world: World, src, dst, dw, r, margin=0.0):
+    """O12 Alg. 3: returns (n, h[E], v_new[E][D], dist[E], margin[E])."""
+    src = _d(src); dst = _d(dst)
+    E, D = src.shape
+    h = np.zeros(E, np.int32); v = np.zeros((E, D)); dist = np.zeros(E); mg = np.zeros(E)
+    L = lib()
+    L.orc_steer.restype = C.c_int
+    L.orc_steer.argtypes = [C.POINTER(_Robot), C.POINTER(_World), C.c_int, D_P, D_P, D_P, C.c_double,
+                            C.c_double, I_P, D_P, D_P, D_P]
+    n = L.orc_steer(C.byref(robot.s), C.byref(world.s), E, _dp(src), _dp(dst), _dp(_d(dw)), float(r),
+                    float(margin), _ip(h), _dp(v), _dp(dist), _dp(mg))
+    return n, h, v, dist, mg
+
+
 class cost_only_margins:
     """Context manager: while active, evaluation margins count only branches where the COST is
     discontinuous (a sweep sample in contact appearing / disappearing) -- for cost-only passes."""

@@ -91,6 +91,12 @@ struct KParams {
     const float *start, *goal;
     float *cost_out, *grad_out, *terms_out, *spheres_out, *ee_out;
     float *seed_best_cost, *seed_best_traj;
+    // validity mask / steering (Alg. 3; f4)
+    float margin;
+    unsigned char *mask_out;
+    const float *e_src, *e_dst;   // steering edges [E][D] (NULL: plain configurations q_in[B][D])
+    const int *e_n;               // device: the shared step count n (after clamping to n_cap)
+    int E, e_env;                 // edges, and the one environment of a steering batch
 };
 
 // ------------------------------------------------------------------------------------------

@@ -557,6 +557,152 @@ __global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KPara
 }
 
 // O9: per problem, the seed with the smallest packed key (cost bits, global seed index).
+// ------------------------------------------------------------------------------------------
+// validity mask and parallel steering (Alg. 3; readings B12-B14)
+// ------------------------------------------------------------------------------------------
+// One CTA per 32 configurations (lane = configuration): FK, then limits (warp 0), self pairs
+// (pair blocks by warp) and sphere-cuboid distances (spheres by warp) each set a bit of the slot's
+// flag; valid = no bit.  The cuboid screen's s2 is the exact squared outside distance, so
+// sd < r + margin  <=>  s2 < (r + margin)^2 for r + margin > 0 (inside: s2 = 0).
+__global__ void __launch_bounds__(NT, 2) mask_kernel(const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) float smem[];
+    const RobotPack &rp = kp.rp;
+    const int D = rp.D, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const bool edges = kp.e_src != nullptr;
+    const int n = edges ? kp.e_n[0] : 0;
+    const int total = edges ? kp.E * (n + 1) : kp.B;
+    const int b0 = blockIdx.x * NC;
+    if (b0 >= total) return;                          // grid sized for n_cap >= n
+    const int n_act = min(NC, total - b0);
+    const int env = edges ? kp.e_env : (kp.env ? kp.env[b0] : 0);
+    const int K = stage_tables(kp, smem, env);
+    const Smem s = make_smem(kp, smem);
+    const float *lim = s.fw + rp.o_lim;
+    int *flag = reinterpret_cast<int *>(s.cfg_cost);  // [32] per-slot invalid bits (unused otherwise here)
+    if (warp == 0) {
+        flag[lane] = 0;
+        const int i = b0 + lane;
+        for (int d = 0; d < D; ++d) {
+            float v = lim[d];
+            if (lane < n_act) {
+                if (edges) {                          // l_ej = src_e + (j / n)(dst_e - src_e)
+                    const int e = i / (n + 1), j = i - e * (n + 1);
+                    const float a = kp.e_src[(size_t)e * D + d], b = kp.e_dst[(size_t)e * D + d];
+                    v = fmaf((float)j / (float)n, b - a, a);
+                } else {
+                    v = kp.q_in[(size_t)i * D + d];
+                }
+            }
+            s.q_cfg[d * NC + lane] = v;
+        }
+        if (!edges && kp.env && lane < n_act && kp.env[b0 + lane] != env) flag[lane] = 8;   // env group rule
+    }
+    __syncthreads();
+    prep_sincos(s, D);
+    __syncthreads();
+    fk_phase(rp, s);
+    int bad = 0;
+    if (warp == 0)                                    // position limits
+        for (int d = 0; d < D; ++d) {
+            const float v = s.q_cfg[d * NC + lane];
+            if (v < lim[d] || v > lim[D + d]) bad |= 1;
+        }
+    {                                                 // self pairs (every pair of S with r + o > 0)
+        const uint2 *blk = reinterpret_cast<const uint2 *>(s.iw + rp.o_blocks);
+        const float *rself = s.fw + rp.o_rself;
+        for (int bi = warp; bi < rp.NB; bi += NW) {
+            const uint2 B = blk[bi];
+            const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff, len = (B.x >> 20) & 0x1ff;
+            for (int u = 0; u < na; ++u) {
+                const float4 wi = s.sw[(ia + u) * NC + lane];
+                const float ri = rself[ia + u];
+                for (int v = 0; v < len; ++v) {
+                    const float4 wj = s.sw[(jb + v) * NC + lane];
+                    const float R = ri + rself[jb + v];
+                    const float dx = wi.x - wj.x, dy = wi.y - wj.y, dz = wi.z - wj.z;
+                    if (dx * dx + dy * dy + dz * dz < R * R) bad |= 2;
+                }
+            }
+        }
+    }
+    {                                                 // world: sd_k(c) >= r + margin for all k
+        const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
+        for (int m = warp; m < rp.M; m += NW) {
+            const float r = sph[m].w;
+            if (r < 0.f) continue;                    // disabled sphere
+            const float4 c = s.sw[m * NC + lane];
+            const float thr = r + kp.margin, thr2 = thr * thr;
+            for (int k = 0; k < K; ++k) {
+                const BoxView b = load_box(s.boxes, k);
+                const float s2 = box_screen(c.x, c.y, c.z, b);
+                bool hit;
+                if (thr > 0.f) hit = s2 < thr2;
+                else {                                // degenerate r + margin = 0: strictly inside
+                    float gx, gy, gz;
+                    hit = s2 == 0.f && box_sdf_grad(b, c.x, c.y, c.z, gx, gy, gz) < thr;
+                }
+                if (hit) bad |= 4;
+            }
+        }
+    }
+    if (bad) atomicOr(&flag[lane], bad);
+    __syncthreads();
+    if (warp == 0 && lane < n_act) kp.mask_out[b0 + lane] = flag[lane] == 0 ? 1 : 0;
+}
+
+// Alg. 3 line 2: n = floor(max_{e,d} |dw_d (dst - src)| / r) + 1, in fp64 from the fp32 inputs
+// (the integer is decided exactly as the oracle decides it), clamped to n_cap; out[0] = n used,
+// out[1] = n before clamping.
+__global__ void steer_n_kernel(int E, int D, const float *src, const float *dst, const float *dw, float r, int n_cap,
+                               int *out) {
+    __shared__ double red[NT];
+    double gm = 0.0;
+    for (int i = threadIdx.x; i < E * D; i += blockDim.x) {
+        const int d = i % D;
+        const double g = fabs((double)dw[d] * ((double)dst[i] - (double)src[i]));
+        gm = fmax(gm, g);
+    }
+    red[threadIdx.x] = gm;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double q = floor(red[0] / (double)r) + 1.0;
+        const int n = q > 2.0e9 ? 2000000000 : (int)q;
+        out[0] = min(n, n_cap);
+        out[1] = n;
+    }
+}
+
+// Alg. 3 lines 6-9, one warp per edge: h = first invalid - 1 (n if none), v_new = l_h,
+// dist = |dw (v_new - src)|_2; h = -1 (invalid source) gives v_new = src, dist = 0.
+__global__ void steer_scan_kernel(int E, int D, const float *src, const float *dst, const float *dw, const int *n_dev,
+                                  const unsigned char *mask, int *h_out, float *v_out, float *dist_out) {
+    const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (e >= E) return;
+    const int n = n_dev[0];
+    int first = -1;
+    for (int j0 = 0; j0 <= n && first < 0; j0 += 32) {
+        const int j = j0 + lane;
+        const bool inval = j <= n && !mask[(size_t)e * (n + 1) + j];
+        const unsigned bal = __ballot_sync(0xffffffffu, inval);
+        if (bal) first = j0 + __ffs(bal) - 1;
+    }
+    const int h = first < 0 ? n : first - 1;
+    float s2 = 0.f;
+    for (int d = lane; d < D; d += 32) {
+        const float a = src[(size_t)e * D + d], b = dst[(size_t)e * D + d];
+        const float v = h < 0 ? a : fmaf((float)h / (float)n, b - a, a);
+        v_out[(size_t)e * D + d] = v;
+        const float g = dw[d] * (v - a);
+        s2 += g * g;
+    }
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (lane == 0) { h_out[e] = h; dist_out[e] = sqrtf(s2); }
+}
+
 __global__ void select_kernel(int P, int S, int N, const float *seed_cost, const float *seed_traj,
                               long long seed_base, float *best_traj, float *best_cost, long long *best_key) {
     const int p = blockIdx.x;
@@ -666,6 +812,10 @@ struct crb_ctx {
     // workspaces (grow on demand)
     float *ws_cost = nullptr, *ws_traj = nullptr;
     size_t cap_cost = 0, cap_traj = 0;
+    unsigned char *ws_mask = nullptr;     // steering waypoint validity [E][n_cap + 1]
+    size_t cap_mask = 0;
+    int *ws_n = nullptr;                  // steering step count (used, unclamped)
+    size_t cap_n = 0;
     // host-API buffers
     float *h_seeds = nullptr, *h_start = nullptr, *h_goal = nullptr, *h_best = nullptr, *h_bcost = nullptr;
     int *h_env = nullptr;
@@ -818,7 +968,7 @@ crb_status crb_destroy(crb_ctx *ctx) {
     if (!ctx) return CRB_E_ARG;
     cudaSetDevice(ctx->device);
     cudaFree(ctx->d_robot); cudaFree(ctx->d_boxes); cudaFree(ctx->d_box_count);
-    cudaFree(ctx->ws_cost); cudaFree(ctx->ws_traj);
+    cudaFree(ctx->ws_cost); cudaFree(ctx->ws_traj); cudaFree(ctx->ws_mask); cudaFree(ctx->ws_n);
     cudaFree(ctx->h_seeds); cudaFree(ctx->h_start); cudaFree(ctx->h_goal); cudaFree(ctx->h_best);
     cudaFree(ctx->h_bcost); cudaFree(ctx->h_env); cudaFree(ctx->h_key);
     delete ctx;
@@ -1280,6 +1430,52 @@ crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const fl
         return CRB_E_CUDA;
     lbfgs_direction_kernel<<<B, NT, bytes, (cudaStream_t)stream>>>(n, count, S, Y, g, d);
     return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_mask_samples(crb_ctx *ctx, const float *q, int K, const int *env, float margin, uint8_t *valid,
+                            void *stream) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if ((st = ready(ctx, true)) != CRB_OK) return st;
+    if (K < 0 || (K > 0 && (!q || !valid)) || !(margin >= 0.f)) return fail(ctx, CRB_E_ARG, "bad mask arguments");
+    KParams kp = base_params(ctx);
+    kp.B = K; kp.H = 1; kp.cp.H = 1; kp.mode = MODE_IK; kp.q_in = q; kp.env = env; kp.margin = margin;
+    kp.mask_out = valid;
+    const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, MODE_IK, 1, 1, 1, false, kp.lay);
+    if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
+    return launch(ctx, mask_kernel, (K + NC - 1) / NC, bytes, (cudaStream_t)stream, kp, "mask_kernel");
+}
+
+crb_status crb_steer(crb_ctx *ctx, int E, const float *src, const float *dst, const float *dw, float r, int env,
+                     float margin, int n_cap, int *n_out, int *h, float *v_new, float *dist, void *stream) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if ((st = ready(ctx, true)) != CRB_OK) return st;
+    if (E < 0 || (E > 0 && (!src || !dst || !dw || !h || !v_new || !dist)) || !(r > 0.f) || !(margin >= 0.f) ||
+        n_cap < 1 || env < 0 || env >= ctx->n_env)
+        return fail(ctx, CRB_E_ARG, "bad steer arguments");
+    if (E == 0) return CRB_OK;
+    const int D = ctx->rp.D;
+    const size_t nw = (size_t)E * (n_cap + 1);
+    if (nw > (size_t)1 << 31) return fail(ctx, CRB_E_LIMIT, "E * (n_cap + 1) too large");
+    if ((st = grow(ctx, &ctx->ws_mask, &ctx->cap_mask, nw)) != CRB_OK) return st;
+    if ((st = grow(ctx, &ctx->ws_n, &ctx->cap_n, (size_t)2)) != CRB_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    steer_n_kernel<<<1, NT, 0, s>>>(E, D, src, dst, dw, r, n_cap, ctx->ws_n);
+    ctx->launches++;
+    if ((st = cuda_check(ctx, cudaGetLastError(), "steer_n_kernel")) != CRB_OK) return st;
+    KParams kp = base_params(ctx);
+    kp.H = 1; kp.cp.H = 1; kp.mode = MODE_IK; kp.margin = margin; kp.mask_out = ctx->ws_mask;
+    kp.e_src = src; kp.e_dst = dst; kp.e_n = ctx->ws_n; kp.E = E; kp.e_env = env;
+    const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, MODE_IK, 1, 1, 1, false, kp.lay);
+    if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
+    if ((st = launch(ctx, mask_kernel, (int)((nw + NC - 1) / NC), bytes, s, kp, "mask_kernel")) != CRB_OK) return st;
+    steer_scan_kernel<<<(E + 7) / 8, 256, 0, s>>>(E, D, src, dst, dw, ctx->ws_n, ctx->ws_mask, h, v_new, dist);
+    ctx->launches++;
+    if ((st = cuda_check(ctx, cudaGetLastError(), "steer_scan_kernel")) != CRB_OK) return st;
+    if (n_out)
+        st = cuda_check(ctx, cudaMemcpyAsync(n_out, ctx->ws_n, 2 * sizeof(int), cudaMemcpyDeviceToDevice, s), "n copy");
+    return st;
 }
 
 crb_status crb_particle_normals(uint32_t key0, uint32_t key1, int n_var, int n_particles, int iter, uint32_t seed,

@@ -87,6 +87,8 @@ _lib.crb_ls_select.argtypes = [C.c_int, C.c_int, F_P, _V, _V, _V, _V, C.c_float,
 _lib.crb_argmin_keys.argtypes = [C.c_int, C.c_int, _V, C.c_int64, _V, _V, _V]
 _lib.crb_lbfgs_direction.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, _V, _V, _V]
 _lib.crb_solver_occupancy.argtypes = [_V, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+_lib.crb_mask_samples.argtypes = [_V, _V, C.c_int, _V, C.c_float, _V, _V]
+_lib.crb_steer.argtypes = [_V, C.c_int, _V, _V, _V, C.c_float, C.c_int, C.c_float, C.c_int, _V, _V, _V, _V, _V]
 _lib.crb_particle_normals.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_uint32, _V, _V]
 _lib.crb_launch_count.argtypes = [_V]
 _lib.crb_launch_count.restype = C.c_int64
@@ -94,7 +96,7 @@ _lib.crb_launch_count.restype = C.c_int64
 SYMBOLS = ["crb_create", "crb_destroy", "crb_last_error", "crb_version", "crb_set_robot", "crb_set_world",
            "crb_set_cost_params", "crb_fk", "crb_evaluate_cost_grad", "crb_lbfgs_solve", "crb_lbfgs_solve_host",
            "crb_ls_select", "crb_argmin_keys", "crb_lbfgs_direction", "crb_launch_count", "crb_solver_occupancy",
-           "crb_particle_normals"]
+           "crb_particle_normals", "crb_mask_samples", "crb_steer"]
 
 
 def _ptr(t):
@@ -248,6 +250,27 @@ class Context:
         self._chk(_lib.crb_lbfgs_solve(self.h, C.byref(s), P, S, H, _ptr(seeds), _ptr(env), _ptr(start), _ptr(goal),
                                        _ptr(out["best_traj"]), _ptr(out["best_cost"]), _ptr(out["best_key"]),
                                        _ptr(out.get("seed_best_cost")), _ptr(out.get("seed_best_traj")), _stream()))
+        return out
+
+    def mask_samples(self, q, env=None, margin: float = 0.0):
+        """q [K,D] device fp32 -> valid [K] uint8 (Alg. 3 mask_samples)."""
+        import torch
+        K = q.shape[0]
+        valid = torch.empty(K, dtype=torch.uint8, device=q.device)
+        self._chk(_lib.crb_mask_samples(self.h, _ptr(q), K, _ptr(env), float(margin), _ptr(valid), _stream()))
+        return valid
+
+    def steer(self, src, dst, dw, r: float, env: int = 0, margin: float = 0.0, n_cap: int = 256):
+        """Alg. 3 parallel steering of E edges: returns dict(n [2] int32, h [E], v_new [E,D], dist [E])."""
+        import torch
+        E, D = src.shape
+        dev = src.device
+        out = dict(n=torch.empty(2, dtype=torch.int32, device=dev), h=torch.empty(E, dtype=torch.int32, device=dev),
+                   v_new=torch.empty(E, D, dtype=torch.float32, device=dev),
+                   dist=torch.empty(E, dtype=torch.float32, device=dev))
+        self._chk(_lib.crb_steer(self.h, E, _ptr(src), _ptr(dst), _ptr(dw), float(r), int(env), float(margin),
+                                 int(n_cap), _ptr(out["n"]), _ptr(out["h"]), _ptr(out["v_new"]), _ptr(out["dist"]),
+                                 _stream()))
         return out
 
     def solve_host(self, sp: inputs.SolverParams, seeds, goal, start=None, env=None, seed_base: int = 0,
