@@ -49,7 +49,7 @@ struct RobotPack {
 // Shared-memory layout (offsets in 4-byte words from the dynamic smem base).
 struct Layout {
     int robot, boxes, mbar;
-    int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, cbb, csm, gxd, gq, gva, pose_ft, pose_c,
+    int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, cbb, csm, gxd, gq, gva, pose_ft,
         goal, cfg_cost, cfg_terms, gV, red, st, scal;
     int solver;      // start of the solver region
     int total;       // words
@@ -331,7 +331,7 @@ struct Smem {
     const float *fw;        // robot blob as floats
     const float *boxes;
     float *q_cfg, *scs, *xs, *lt, *frames, *ls, *sbest, *cbb, *csm, *gxd, *gq, *gva, *pose_ft,
-        *pose_c, *goal, *cfg_cost, *cfg_terms, *gV, *red, *st, *scal;
+        *goal, *cfg_cost, *cfg_terms, *gV, *red, *st, *scal;
     float4 *sw;             // [M][32] sphere centre (x, y, z) and hb = -(|w|^2 - r_self^2) / 2
     float4 *sg;             // [M][32] dE/dw (x, y, z) and the world energy E (w)
     int *srank, *sij;
@@ -353,7 +353,7 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     s.srank = reinterpret_cast<int *>(smem + L.srank);
     s.sij = reinterpret_cast<int *>(smem + L.sij);
     s.cbb = smem + L.cbb; s.csm = smem + L.csm; s.gxd = smem + L.gxd;
-    s.gq = smem + L.gq; s.gva = smem + L.gva; s.pose_ft = smem + L.pose_ft; s.pose_c = smem + L.pose_c;
+    s.gq = smem + L.gq; s.gva = smem + L.gva; s.pose_ft = smem + L.pose_ft;
     s.goal = smem + L.goal; s.cfg_cost = smem + L.cfg_cost; s.cfg_terms = smem + L.cfg_terms;
     s.gV = smem + L.gV; s.red = smem + L.red; s.st = smem + L.st; s.scal = smem + L.scal;
     return s;
@@ -513,20 +513,21 @@ __device__ __forceinline__ void mat_to_quat(float r00, float r01, float r02, flo
 // Sweep directions of sphere m at this slot (A6: a direction is swept iff its neighbour exists
 // and gap = L - 2r' > 0); also the larger half-segment.  One function for the screen set-up and
 // the slow path, so both take bitwise the same decisions.
-__device__ __forceinline__ int sweep_dirs(const float4 *p, float cx, float cy, float cz, float rp, bool hasp,
+__device__ __forceinline__ int sweep_dirs(float4 qp, float4 qn, float cx, float cy, float cz, float rp, bool hasp,
                                           bool hasn, bool sweepf, float &maxb2) {
     // gap = L - 2r' > 0  <=>  L^2 > 4 r'^2 ;  (L/2)^2 = L^2 / 4  (no square root on this path)
+    // qp / qn: the sphere at the previous / next slot (loaded once by the caller)
     int dirs = 0;
     maxb2 = 0.f;
     const float four_rp2 = 4.f * rp * rp;
     if (sweepf && hasp) {
-        const float4 q = p[-1];
+        const float4 q = qp;
         const float vx = q.x - cx, vy = q.y - cy, vz = q.z - cz;
         const float L2 = vx * vx + vy * vy + vz * vz;
         if (L2 > four_rp2) { dirs |= 1; maxb2 = 0.25f * L2; }
     }
     if (sweepf && hasn) {
-        const float4 q = p[1];
+        const float4 q = qn;
         const float vx = q.x - cx, vy = q.y - cy, vz = q.z - cz;
         const float L2 = vx * vx + vy * vy + vz * vz;
         if (L2 > four_rp2) { dirs |= 2; maxb2 = fmaxf(maxb2, 0.25f * L2); }
@@ -733,7 +734,14 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         }
 #pragma unroll
         for (int k = 0; k < 6; ++k) s.pose_ft[k * NC + c] = ft[k];
-        s.pose_c[c] = C;
+        // per-slot goal, bound and smoothness terms here (a8 finished before the placement
+        // barrier), off the merge's critical path
+        float cb = 0.f, cs = 0.f;
+        for (int d = 0; d < D; ++d) { cb += s.cbb[d * NC + c]; cs += s.csm[d * NC + c]; }
+        const bool valid = c < n_act;
+        s.cfg_terms[0 * NC + c] = valid ? C : 0.f;
+        s.cfg_terms[1 * NC + c] = valid ? cb : 0.f;
+        s.cfg_terms[2 * NC + c] = valid ? cs : 0.f;
     }
 
     // ---- a4 + a5/a6: self-collision and world collision as ONE dynamic work queue.  Items are the
@@ -780,11 +788,13 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     if (m < rp.M) {
                         const float4 *p = s.sw + m * NC + lane;
                         const float4 c = p[0];
+                        // neighbours at the previous / next slot, loaded once (speed and sweep);
+                        // a missing neighbour reads as the sphere itself (A13)
+                        const float4 a = hasp ? p[-1] : c, z = hasn ? p[1] : c;
                         cx[u] = c.x; cy[u] = c.y; cz[u] = c.z;
                         s.sg[m * NC + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
                         float spd = 1.f;
                         if (speedf) {   // A13: central difference, missing neighbour -> w_h
-                            const float4 a = hasp ? p[-1] : c, z = hasn ? p[1] : c;
                             const float dx = z.x - a.x, dy = z.y - a.y, dz = z.z - a.z;
                             spd = sqrtf(dx * dx + dy * dy + dz * dz) * cf.inv_2dt;
                         }
@@ -792,7 +802,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         const float r = sph[m].w;
                         const float rpr = r + cf.eta;   // Alg. 10 "sph.radius += eta"
                         float maxb2;
-                        dirs[u] = sweep_dirs(p, c.x, c.y, c.z, rpr, hasp, hasn, sweepf, maxb2);
+                        dirs[u] = sweep_dirs(a, z, c.x, c.y, c.z, rpr, hasp, hasn, sweepf, maxb2);
                         // r < 0 disables the sphere; sp = 0 => C_w = 0 exactly
                         if (r >= 0.f && spd != 0.f) th2[u] = fmaxf(rpr * rpr, maxb2);
                     }
@@ -829,7 +839,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                 const float rpr = sph[m].w + cf.eta;
                                 float maxb2;
                                 const bool hp = to && src > 0 && src < H, hn = to && src + 1 < H;
-                                const int dr = sweep_dirs(pc, c.x, c.y, c.z, rpr, hp, hn, sweepf, maxb2);
+                                const int dr = sweep_dirs(hp ? pc[-1] : c, hn ? pc[1] : c, c.x, c.y, c.z, rpr, hp, hn,
+                                                          sweepf, maxb2);
                                 box_slow(s.sg + m * NC + src, pc, s.boxes, k, c.x, c.y, c.z, box_screen(c.x, c.y, c.z, b),
                                          rpr, dr, cf.eta, cf.inv_eta, cf.sweep_steps);
                             }
@@ -902,7 +913,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
 
     __syncthreads();
 
-    // ---- a10 (per slot): merge self-collision, apply its gradient, per-slot costs and the total
+    // ---- a10 (per slot): warp 0 merges self-collision and applies its gradient (x, y, z only);
+    // warp 1 sums the world groups in index order; then warp 0 forms the slot costs and the total
     if (warp == 0) {
         const int c = lane;
         float bp = 0.f;
@@ -921,27 +933,32 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             if (nu < 1e-12f) { ux = 1.f; uy = 0.f; uz = 0.f; }
             else { ux /= nu; uy /= nu; uz /= nu; }
             const float b = cf.beta_self;
-            float4 &gi = s.sg[i * NC + c], &gj = s.sg[j * NC + c];
-            gi.x -= b * ux; gi.y -= b * uy; gi.z -= b * uz;
-            gj.x += b * ux; gj.y += b * uy; gj.z += b * uz;
+            float *gi = reinterpret_cast<float *>(s.sg + i * NC + c), *gj = reinterpret_cast<float *>(s.sg + j * NC + c);
+            gi[0] -= b * ux; gi[1] -= b * uy; gi[2] -= b * uz;   // .w (group cost) is read by warp 1
+            gj[0] += b * ux; gj[1] += b * uy; gj[2] += b * uz;
             cself = b * bp;
         }
+        s.cfg_terms[3 * NC + c] = c < n_act ? cself : 0.f;
+    } else if (warp == 1) {
+        const int c = lane;
         float cw = 0.f;
         for (int q = 0; q < ((rp.M + 3) >> 2); ++q) cw += s.sg[(q << 2) * NC + c].w;   // fixed order
-        float cb = 0.f, cs = 0.f;
-        for (int d = 0; d < D; ++d) { cb += s.cbb[d * NC + c]; cs += s.csm[d * NC + c]; }
-        const bool valid = c < n_act;
-        const float t0 = valid ? s.pose_c[c] : 0.f, t1 = valid ? cb : 0.f, t2 = valid ? cs : 0.f,
-                    t3 = valid ? cself : 0.f, t4 = valid ? cw : 0.f;
-        s.cfg_terms[0 * NC + c] = t0; s.cfg_terms[1 * NC + c] = t1; s.cfg_terms[2 * NC + c] = t2;
-        s.cfg_terms[3 * NC + c] = t3; s.cfg_terms[4 * NC + c] = t4;
+        s.cfg_terms[4 * NC + c] = c < n_act ? cw : 0.f;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int c = lane;
+        const float t0 = s.cfg_terms[0 * NC + c], t1 = s.cfg_terms[1 * NC + c], t2 = s.cfg_terms[2 * NC + c],
+                    t3 = s.cfg_terms[3 * NC + c], t4 = s.cfg_terms[4 * NC + c];
         const float cc = (((t0 + t1) + t2) + t3) + t4;
         s.cfg_cost[c] = cc;
         const float tot = warp_sum(cc);
         if (c == 0) s.scal[0] = tot;
     }
-    __syncthreads();
-    if (!grad) return;   // cost-only pass (particle warm-up, f1): no backward
+    if (!grad) {          // cost-only pass (particle warm-up, f1): no backward
+        __syncthreads();
+        return;
+    }
 
     // ---- a9: backward to joint space (Alg. 8 / Table 7 as subtree sums):
     // per link: F_l = sum G_m, T_l = sum w_m x G_m over its spheres (+ the pose pseudo-sphere);

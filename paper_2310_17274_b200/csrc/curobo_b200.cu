@@ -884,7 +884,6 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.gq = take(D * NC);
     L.gva = take(mode == MODE_TO ? 3 * D * NC : 4);
     L.pose_ft = take(6 * NC);
-    L.pose_c = take(NC);
     L.goal = take(std::max(7, D) * NC);   // pose [7][32] or joint-space goal [D][32] (CRB_CSPACE)
     L.cfg_cost = take(NC);
     L.cfg_terms = take(5 * NC);
