@@ -748,6 +748,93 @@ int orc_argmin_f32(int n, const float *c) {
 }
 
 /* ------------------------------------------------------------------------------------------ */
+/* O13 motion-generation pipeline pieces (§2 / Fig. 2, Alg. 4, App. B; */
+/* readings B15-B18)                                                                           */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Alg. 4 retime ("find dt that pushes trajectory to robot limits (velocity, acceleration or
+ * jerk)"), reading B15 after SPEC S:515: with v, a, j the five-point-stencil derivatives (O3) of
+ * the state sequence (O2 state map of V with `start`) at dt, over h = 1..H and every joint,
+ *   s = max(1e-3, max(|v|/vmax, sqrt(|a|/amax), cbrt(|j|/jmax)));  dt_opt = s dt.
+ * Time scaling by s divides v, a, j by s, s^2, s^3, so at dt_opt every derivative is within its
+ * limit and the binding one sits on it.  ratio_out[3] (may be NULL) = the three maxima at dt. */
+double orc_retime(const orc_robot *rb, const double *start, const double *V, int H, double dt,
+                  double *ratio_out) {
+    int D = rb->n_dof;
+    double *x = malloc(sizeof(double) * (H + 5) * D), *v = malloc(sizeof(double) * H * D),
+           *a = malloc(sizeof(double) * H * D), *j = malloc(sizeof(double) * H * D);
+    orc_state_map(start, V, H, D, x);
+    orc_derivs(x, H, D, dt, v, a, j);
+    double rv = 0.0, ra = 0.0, rj = 0.0;
+    for (int h = 0; h < H; ++h)
+        for (int d = 0; d < D; ++d) {
+            double qv = fabs(v[h * D + d]) / rb->vmax[d];
+            double qa = sqrt(fabs(a[h * D + d]) / rb->amax[d]);
+            double qj = cbrt(fabs(j[h * D + d]) / rb->jmax[d]);
+            if (qv > rv) rv = qv;
+            if (qa > ra) ra = qa;
+            if (qj > rj) rj = qj;
+        }
+    double sc = rv;
+    if (ra > sc) sc = ra;
+    if (rj > sc) sc = rj;
+    if (sc < 1e-3) sc = 1e-3;
+    if (ratio_out) { ratio_out[0] = rv; ratio_out[1] = ra; ratio_out[2] = rj; }
+    free(x); free(v); free(a); free(j);
+    return sc;
+}
+
+/* Alg. 4 "scale_traj_opt(dt_opt)" + "enable_jerk_cost()", reading B15: the smoothness weights are
+ * rescaled so that the terms keep their magnitude when the same path is re-timed from dt_ref to
+ * dt (a ~ dt^-2, j ~ dt^-3): a8 (dt/dt_ref)^4, a9 (dt/dt_ref)^6; the limit (bound) weights are
+ * physical constraints and stay. */
+void orc_scale_params(const orc_params *in, double dt, double dt_ref, int jerk_on, orc_params *out) {
+    *out = *in;
+    double r = dt / dt_ref;
+    out->dt = dt;
+    out->a8 = in->a8 * r * r * r * r;
+    out->a9 = in->a9 * r * r * r * r * r * r;
+    if (jerk_on) out->flags |= ORC_JERK;
+}
+
+/* Goal errors of a configuration (App. B P:2190 "pose error"): position |p_g - p|_2 and
+ * orientation 1 - |<q_g, q>| (reading A1). */
+void orc_goal_error(const orc_robot *rb, const double *q, const double *goal, double *pos_err,
+                    double *rot_err) {
+    int L = rb->n_links, M = rb->n_spheres;
+    double *T = malloc(sizeof(double) * 12 * L), *sph = malloc(sizeof(double) * 4 * M), ee[7];
+    orc_fk(rb, q, T, sph, ee);
+    double dx = goal[0] - ee[0], dy = goal[1] - ee[1], dz = goal[2] - ee[2];
+    *pos_err = sqrt(dx * dx + dy * dy + dz * dz);
+    *rot_err = 1.0 - fabs(goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
+    free(T); free(sph);
+}
+
+/* Linear TO seed ("linear interpolation from the start configuration to the solved terminal
+ * configuration"), reading B17: V_h = start + (h / (H-1)) (q_T - start), h = 0..H-1. */
+void orc_linear_seed(const double *start, const double *qT, int H, int D, double *V) {
+    for (int h = 0; h < H; ++h)
+        for (int d = 0; d < D; ++d) V[h * D + d] = start[d] + ((double)h / (H - 1)) * (qT[d] - start[d]);
+}
+
+/* Scores (App. B, reading B18).  IK: "a lowest weighted sum of pose error and the
+ * distance of the solution to the current joint configuration":
+ *   w_pose (pos_err + rot_err) + w_dist |q - q_0|_2.
+ * TO: "a blended sum of the pose error, maximum jerk, and motion time":
+ *   w_pose (pos_err + rot_err) + w_jerk max|j| + w_time (H - 1) dt  (after retiming). */
+double orc_ik_score(int D, const double *q, const double *q0, double pos_err, double rot_err,
+                    double w_pose, double w_dist) {
+    double s2 = 0.0;
+    for (int d = 0; d < D; ++d) s2 += (q[d] - q0[d]) * (q[d] - q0[d]);
+    return w_pose * (pos_err + rot_err) + w_dist * sqrt(s2);
+}
+
+double orc_blended_score(double pos_err, double rot_err, double max_jerk, double motion_time,
+                         double w_pose, double w_jerk, double w_time) {
+    return w_pose * (pos_err + rot_err) + w_jerk * max_jerk + w_time * motion_time;
+}
+
+/* ------------------------------------------------------------------------------------------ */
 /* O12 validity mask and parallel steering (Alg. 3; readings B12-B14) */
 /* ------------------------------------------------------------------------------------------ */
 

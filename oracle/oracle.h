@@ -122,6 +122,17 @@ int    orc_ls_select(int A, const double *alpha, double c0, double g0d, const do
 int    orc_ls_select_f32(int A, const float *alpha, float c0, float g0d, const float *ca,
                          const float *gda, float c1, float c2, int mode);
 int    orc_argmin_f32(int n, const float *c);
+/* O13: motion-generation pipeline pieces (Alg. 4 retime, weight scaling, goal errors, seeds, scores) */
+double orc_retime(const orc_robot *rb, const double *start, const double *V, int H, double dt,
+                  double *ratio_out);
+void   orc_scale_params(const orc_params *in, double dt, double dt_ref, int jerk_on, orc_params *out);
+void   orc_goal_error(const orc_robot *rb, const double *q, const double *goal, double *pos_err,
+                      double *rot_err);
+void   orc_linear_seed(const double *start, const double *qT, int H, int D, double *V);
+double orc_ik_score(int D, const double *q, const double *q0, double pos_err, double rot_err,
+                    double w_pose, double w_dist);
+double orc_blended_score(double pos_err, double rot_err, double max_jerk, double motion_time,
+                         double w_pose, double w_jerk, double w_time);
 /* O12: validity mask and parallel steering (Alg. 3) */
 int    orc_mask_sample(const orc_robot *rb, const orc_world *w, const double *q, double margin,
                        double *margin_out);

@@ -351,6 +351,68 @@ def lbfgs_solve(fun, x0, sp, lo=None, hi=None):
     return bx, bc.value, trace
 
 
+def retime(robot: Robot, start, V, dt):
+    """O13 Alg. 4 retime: returns (s, dt_opt, (max |v|/vmax, max sqrt(|a|/amax), max cbrt(|j|/jmax)))."""
+    V = _d(V)
+    H = V.shape[0]
+    L = lib()
+    L.orc_retime.restype = C.c_double
+    L.orc_retime.argtypes = [C.POINTER(_Robot), D_P, D_P, C.c_int, C.c_double, D_P]
+    r = np.zeros(3)
+    s = L.orc_retime(C.byref(robot.s), _dp(_d(start)), _dp(V), H, float(dt), _dp(r))
+    return s, s * dt, r
+
+
+def scale_params(cp, dt, dt_ref=0.25, jerk_on=True):
+    """O13 Alg. 4 weight scaling (reading B15) on an inputs.CostParams; returns a new CostParams."""
+    import dataclasses
+    r = dt / dt_ref
+    return dataclasses.replace(cp, dt=dt, a8=cp.a8 * r ** 4, a9=cp.a9 * r ** 6,
+                               flags=cp.flags | (4 if jerk_on else 0))
+
+
+def scale_params_c(cp, dt, dt_ref=0.25, jerk_on=True):
+    """The same scaling done by the C oracle (orc_scale_params), returned as (dt, a8, a9, flags)."""
+    L = lib()
+    L.orc_scale_params.argtypes = [C.POINTER(_Params), C.c_double, C.c_double, C.c_int, C.POINTER(_Params)]
+    pin = params(cp); pout = _Params()
+    L.orc_scale_params(C.byref(pin), float(dt), float(dt_ref), int(jerk_on), C.byref(pout))
+    return pout.dt, pout.a8, pout.a9, pout.flags
+
+
+def goal_error(robot: Robot, q, goal):
+    L = lib()
+    L.orc_goal_error.argtypes = [C.POINTER(_Robot), D_P, D_P, D_P, D_P]
+    pe, re = C.c_double(), C.c_double()
+    L.orc_goal_error(C.byref(robot.s), _dp(_d(q)), _dp(_d(goal)), C.byref(pe), C.byref(re))
+    return pe.value, re.value
+
+
+def linear_seed(start, qT, H):
+    start = _d(start); qT = _d(qT)
+    D = start.shape[0]
+    V = np.zeros((H, D))
+    L = lib()
+    L.orc_linear_seed.argtypes = [D_P, D_P, C.c_int, C.c_int, D_P]
+    L.orc_linear_seed(_dp(start), _dp(qT), H, D, _dp(V))
+    return V
+
+
+def ik_score(q, q0, pos_err, rot_err, w_pose, w_dist):
+    q = _d(q)
+    L = lib()
+    L.orc_ik_score.restype = C.c_double
+    L.orc_ik_score.argtypes = [C.c_int, D_P, D_P, C.c_double, C.c_double, C.c_double, C.c_double]
+    return L.orc_ik_score(q.shape[0], _dp(q), _dp(_d(q0)), pos_err, rot_err, w_pose, w_dist)
+
+
+def blended_score(pos_err, rot_err, max_jerk, motion_time, w_pose, w_jerk, w_time):
+    L = lib()
+    L.orc_blended_score.restype = C.c_double
+    L.orc_blended_score.argtypes = [C.c_double] * 7
+    return L.orc_blended_score(pos_err, rot_err, max_jerk, motion_time, w_pose, w_jerk, w_time)
+
+
 def mask_sample(robot: Robot, world: World, q, margin=0.0):
     """O12: (valid, decision margin) of one configuration."""
     L = lib()
