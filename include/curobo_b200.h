@@ -168,6 +168,15 @@ crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, co
                                   const float *start, const float *goal, float *cost,
                                   float *grad, float *term_costs, void *stream);
 
+/* Same with a per-row timestep (Alg. 4 "run trajectory optimization with new dt", reading B15):
+ * dt[B] (device, > 0; NULL = the cost params' dt).  The five-point stencil and the speed metric
+ * use dt[b]; the smoothness weights are rescaled relative to dt_ref = the cost params' dt:
+ * alpha_8 (dt/dt_ref)^4, alpha_9 (dt/dt_ref)^6 (the terms keep their magnitude when the same
+ * path is re-timed); the bound weights are physical limits and stay.  IK rows ignore dt. */
+crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H, const int *env,
+                                     const float *start, const float *goal, const float *dt,
+                                     float *cost, float *grad, float *term_costs, void *stream);
+
 /* Per-seed L-BFGS solve (§4.1, Alg. 6 + Alg. 1), one persistent CTA per seed trajectory (TO) or
  * per 32 seeds of one problem (IK), all `iters` iterations inside one launch.
  *   seeds[P][S][H][D] (TO, H >= 8) or [P][S][D] (IK, H == 1); env[P] (may be NULL);
@@ -182,6 +191,14 @@ crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int
                            int64_t *best_key, float *seed_best_cost, float *seed_best_traj,
                            void *stream);
 
+/* crb_lbfgs_solve with a per-problem timestep dt[P] (device, > 0; NULL = the cost params' dt),
+ * weights rescaled as in crb_evaluate_cost_grad_dt (the second trajectory optimisation of Alg. 4). */
+crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H,
+                              const float *seeds, const int *env, const float *start,
+                              const float *goal, const float *dt, float *best_traj, float *best_cost,
+                              int64_t *best_key, float *seed_best_cost, float *seed_best_traj,
+                              void *stream);
+
 /* Same as crb_lbfgs_solve with HOST buffers: copies inputs to context-owned device buffers,
  * solves, copies outputs back and synchronises `stream`. */
 crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H,
@@ -194,10 +211,11 @@ crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P
 /* mask_samples (Alg. 3 line 5, reading B12): valid[k] = 1 iff configuration q[k] is
  * inside the position limits, no self-collision pair of S penetrates, and every enabled sphere
  * keeps a distance >= r + margin (m, >= 0) to every enabled cuboid of env[k]; else 0.
- * Device pointers: q[K][D], env[K] (may be NULL = 0; constant within aligned groups of 32 rows,
- * a row that violates it is reported invalid), valid[K] (uint8).  Needs robot, world, params. */
-crb_status crb_mask_samples(crb_ctx *ctx, const float *q, int K, const int *env, float margin,
-                            uint8_t *valid, void *stream);
+ * Device pointers: q[K][D], env[K / env_div] (row k uses env[k / env_div]; may be NULL = 0; the
+ * env must be constant within aligned groups of 32 rows, a row that violates it is reported
+ * invalid), valid[K] (uint8).  Needs robot, world, params. */
+crb_status crb_mask_samples(crb_ctx *ctx, const float *q, int K, const int *env, int env_div,
+                            float margin, uint8_t *valid, void *stream);
 
 /* Parallel steering (Alg. 3, reading B13) of E edges in environment `env`:
  *   n = floor(max_{e,d} |dw_d (dst_ed - src_ed)| / r) + 1, shared by the batch and clamped to
@@ -210,6 +228,62 @@ crb_status crb_mask_samples(crb_ctx *ctx, const float *q, int K, const int *env,
 crb_status crb_steer(crb_ctx *ctx, int E, const float *src, const float *dst, const float *dw, float r,
                      int env, float margin, int n_cap, int *n_out, int *h, float *v_new, float *dist,
                      void *stream);
+
+/* ---- motion-generation pipeline pieces (§2 / Fig. 2, Alg. 4, App. B P:2189-2190;
+ *      SURVEY §8(f) f2; readings B15-B18).  The calls without a context are plain
+ *      arithmetic on device arrays. ---- */
+
+/* Alg. 4 retime ("find dt that pushes trajectory to robot limits"): for each of B trajectories
+ * V[B][H][D] with its start row start[b / start_div][D] and timestep dt[b] (NULL = the cost
+ * params' dt), the five-point-stencil v, a, j of the Table 5 state sequence give
+ *   scale[b] = max(1e-3, max |v|/vmax, sqrt(|a|/amax), cbrt(|j|/jmax)),
+ *   dt_opt[b] = scale[b] dt[b]  (may be NULL),  max_jerk[b] = max |j| at dt_opt (may be NULL).
+ * Needs the robot (limits).  H >= 8. */
+crb_status crb_retime(crb_ctx *ctx, int B, int H, const float *V, const float *start, int start_div,
+                      const float *dt, float *scale, float *dt_opt, float *max_jerk, void *stream);
+
+/* Goal errors of B configurations q (row b at q + b * q_stride, q_stride >= D floats; e.g. the
+ * terminal state V[b][H-1] with q = V + (H-1) D, q_stride = H D): pos_err[b] = |p_g - p|_2,
+ * rot_err[b] = 1 - |<q_g, q>| (reading A1), goal[B / goal_div][7] (row b uses goal[b / goal_div]).
+ * Needs the robot. */
+crb_status crb_goal_error(crb_ctx *ctx, int B, const float *q, int q_stride, const float *goal,
+                          int goal_div, float *pos_err, float *rot_err, void *stream);
+
+/* IK ranking score (App. B: "lowest weighted sum of pose error and the distance of the solution to
+ * the current joint configuration"): score[p][s] = w_pose (pe + re) + w_dist |q[p][s] - q0[p]|_2,
+ * plus `penalty` (e.g. +inf) unless pe < pos_thr, re < rot_thr and valid[p][s] (uint8 mask, may
+ * be NULL). */
+crb_status crb_ik_scores(int P, int S, int D, const float *q, const float *q0, const float *pos_err,
+                         const float *rot_err, const uint8_t *valid, float pos_thr, float rot_thr,
+                         float w_pose, float w_dist, float penalty, float *score, void *stream);
+
+/* TO blended score (App. B: "a blended sum of the pose error, maximum jerk, and motion time"):
+ * score[p][s] = w_pose (pe + re) + w_jerk max_jerk + w_time (H-1) dt_opt, plus `penalty` unless
+ * the pose thresholds hold and all H states are valid (valid[p][s][H], uint8, may be NULL). */
+crb_status crb_to_scores(int P, int S, int H, const float *pos_err, const float *rot_err,
+                         const float *max_jerk, const float *dt_opt, const uint8_t *valid,
+                         float pos_thr, float rot_thr, float w_pose, float w_jerk, float w_time,
+                         float penalty, float *score, void *stream);
+
+/* Per problem, the k lowest finite scores in ascending order (ties -> lower index): idx[p][j] =
+ * seed index of rank j; for j >= count[p] the ranked list repeats cyclically; idx = -1 when
+ * count[p] = 0 (no valid seed).  score[P][S]. */
+crb_status crb_rank_seeds(int P, int S, const float *score, int k, int *idx, int *count, void *stream);
+
+/* Linear TO seeds (reading B17): seeds[p][s][h] = q0[p] + (h/(H-1)) (qT[p][j] - q0[p]) with
+ * j = idx[p][s] (idx may be NULL: j = s, then Sq >= S), qT[P][Sq][D]; j < 0 gives a still seed. */
+crb_status crb_linear_seeds(int P, int S, int H, int D, const float *q0, const float *qT, int Sq,
+                            const int *idx, float *seeds, void *stream);
+
+/* The trajectory states of optimisation variables (Table 5 last row): x[b][h-1] = x_h for
+ * h = 1..H with x_1..x_3 = start[b / start_div], x_{H-3..H} = V[b][H-1], else V[b][h-1] (the
+ * pinned V_0..V_2 and aliased V_{H-4..H-2} are not states).  V[B][H][D] -> x[B][H][D]. */
+crb_status crb_trajectory_states(int B, int H, int D, const float *V, const float *start, int start_div,
+                                 float *x, void *stream);
+
+/* dst[p][:] = src[p][idx[p * idx_stride]][:] for rows of n floats, src[P][S][n] (idx < 0: zeros). */
+crb_status crb_gather_rows(int P, int S, int n, const float *src, const int *idx, int idx_stride,
+                           float *dst, void *stream);
 
 /* ---- test hooks: the exact device routines the solver uses, on caller data ---- */
 

@@ -49,7 +49,7 @@ struct RobotPack {
 // Shared-memory layout (offsets in 4-byte words from the dynamic smem base).
 struct Layout {
     int robot, boxes, mbar;
-    int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, cbb, csm, gxd, gq, gva, pose_ft,
+    int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, cbb, csm, gxd, gq, gva, pose_ft, tdp,
         goal, cfg_cost, cfg_terms, gV, red, st, scal;
     int solver;      // start of the solver region
     int total;       // words
@@ -91,6 +91,10 @@ struct KParams {
     const float *start, *goal;
     float *cost_out, *grad_out, *terms_out, *spheres_out, *ee_out;
     float *seed_best_cost, *seed_best_traj;
+    const float *dt_arr;          // per-problem (solve) / per-row (evaluate) dt, or NULL (Alg. 4, B15)
+    int q_stride;                 // fk / goal-error rows: floats between consecutive configurations
+    int goal_div, env_div;        // goal-error / mask rows: row b uses goal[b / goal_div], env[b / env_div]
+    float *pos_err_out, *rot_err_out;
     // validity mask / steering (Alg. 3; f4)
     float margin;
     unsigned char *mask_out;
@@ -331,7 +335,7 @@ struct Smem {
     const float *fw;        // robot blob as floats
     const float *boxes;
     float *q_cfg, *scs, *xs, *lt, *frames, *ls, *sbest, *cbb, *csm, *gxd, *gq, *gva, *pose_ft,
-        *goal, *cfg_cost, *cfg_terms, *gV, *red, *st, *scal;
+        *goal, *cfg_cost, *cfg_terms, *gV, *red, *st, *scal, *tdp;
     float4 *sw;             // [M][32] sphere centre (x, y, z) and hb = -(|w|^2 - r_self^2) / 2
     float4 *sg;             // [M][32] dE/dw (x, y, z) and the world energy E (w)
     int *srank, *sij;
@@ -353,7 +357,7 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     s.srank = reinterpret_cast<int *>(smem + L.srank);
     s.sij = reinterpret_cast<int *>(smem + L.sij);
     s.cbb = smem + L.cbb; s.csm = smem + L.csm; s.gxd = smem + L.gxd;
-    s.gq = smem + L.gq; s.gva = smem + L.gva; s.pose_ft = smem + L.pose_ft;
+    s.gq = smem + L.gq; s.gva = smem + L.gva; s.pose_ft = smem + L.pose_ft; s.tdp = smem + L.tdp;
     s.goal = smem + L.goal; s.cfg_cost = smem + L.cfg_cost; s.cfg_terms = smem + L.cfg_terms;
     s.gV = smem + L.gV; s.red = smem + L.red; s.st = smem + L.st; s.scal = smem + L.scal;
     return s;
@@ -606,6 +610,27 @@ __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const float 
 //   TO: s.gV[H][D] = dC/dV; IK: s.gV[D][32].  Ends with a barrier.
 // Called from exactly one site per kernel (the solvers loop over passes), so it is inlined with
 // the kernel parameters left in the constant bank.
+// The dt-dependent scalars of one problem into s.tdp (thread 0; the caller synchronises):
+// [0] 1/(2 dt) (speed metric), [1..3] 1/(12 dt), 1/(12 dt^2), 1/(2 dt^3) (five-point stencil),
+// [4] a8, [5] a9.  With a per-problem dt the smoothness weights follow reading B15 relative to the
+// context's dt_ref = cp.dt: a8 (dt/dt_ref)^4, a9 (dt/dt_ref)^6 (Alg. 4 "scale weights by new dt").
+__device__ __forceinline__ void stage_dt(const KParams &kp, const Smem &s, int row) {
+    if (threadIdx.x != 0) return;
+    const CostP &cf = kp.cp;
+    if (!kp.dt_arr) {
+        s.tdp[0] = cf.inv_2dt; s.tdp[1] = cf.inv_12dt; s.tdp[2] = cf.inv_12dt2; s.tdp[3] = cf.inv_2dt3;
+        s.tdp[4] = cf.a8; s.tdp[5] = cf.a9;
+        return;
+    }
+    const double dt = kp.dt_arr[row], r = dt / (double)cf.dt, r2 = r * r;
+    s.tdp[0] = (float)(1.0 / (2.0 * dt));
+    s.tdp[1] = (float)(1.0 / (12.0 * dt));
+    s.tdp[2] = (float)(1.0 / (12.0 * dt * dt));
+    s.tdp[3] = (float)(1.0 / (2.0 * dt * dt * dt));
+    s.tdp[4] = (float)(cf.a8 * (r2 * r2));
+    s.tdp[5] = (float)(cf.a9 * (r2 * r2 * r2));
+}
+
 template <int MODE>
 __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
                                           const float *dvec, bool grad = true) {
@@ -661,17 +686,18 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     const float *x = s.xs + d * XS + c + 3;   // x_h with h = c + 1
                     const float xm2 = x[-2], xm1 = x[-1], x0 = x[0], xp1 = x[1], xp2 = x[2];
                     // O3 five-point stencil (§A.5, A15)
-                    const float v = (-xp2 + 8.f * xp1 - 8.f * xm1 + xm2) * cf.inv_12dt;
-                    const float a = (-xp2 + 16.f * xp1 - 30.f * x0 + 16.f * xm1 - xm2) * cf.inv_12dt2;
-                    const float j = (xp2 - 2.f * xp1 + 2.f * xm1 - xm2) * cf.inv_2dt3;
+                    const float v = (-xp2 + 8.f * xp1 - 8.f * xm1 + xm2) * s.tdp[1];
+                    const float a = (-xp2 + 16.f * xp1 - 30.f * x0 + 16.f * xm1 - xm2) * s.tdp[2];
+                    const float j = (xp2 - 2.f * xp1 + 2.f * xm1 - xm2) * s.tdp[3];
                     const float vm = lim[2 * D + d], am = lim[3 * D + d], jm = lim[4 * D + d];
                     cb += cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd); gx = cf.wb[0] * dd;
                     cb += cf.wb[1] * bound_cost(v, -vm, vm, cf.eta_bound, dd); gv = cf.wb[1] * dd;
                     cb += cf.wb[2] * bound_cost(a, -am, am, cf.eta_bound, dd); ga = cf.wb[2] * dd;
                     cb += cf.wb[3] * bound_cost(j, -jm, jm, cf.eta_bound, dd); gj = cf.wb[3] * dd;
-                    cs = cf.a8 * a * a;
-                    ga += 2.f * cf.a8 * a;
-                    if (cf.flags & F_JERK) { cs += cf.a9 * j * j; gj += 2.f * cf.a9 * j; }
+                    const float a8 = s.tdp[4], a9 = s.tdp[5];
+                    cs = a8 * a * a;
+                    ga += 2.f * a8 * a;
+                    if (cf.flags & F_JERK) { cs += a9 * j * j; gj += 2.f * a9 * j; }
                 } else {
                     const float x0 = s.q_cfg[d * NC + c];
                     cb = cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd);
@@ -796,7 +822,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         float spd = 1.f;
                         if (speedf) {   // A13: central difference, missing neighbour -> w_h
                             const float dx = z.x - a.x, dy = z.y - a.y, dz = z.z - a.z;
-                            spd = sqrtf(dx * dx + dy * dy + dz * dz) * cf.inv_2dt;
+                            spd = sqrtf(dx * dx + dy * dy + dz * dz) * s.tdp[0];
                         }
                         sp[u] = spd;
                         const float r = sph[m].w;
@@ -1033,7 +1059,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     if (MODE == MODE_TO) {
         // O3 coefficients: v: (1, -8, 0, 8, -1)/(12 dt), a: (-1, 16, -30, 16, -1)/(12 dt^2),
         // j: (-1, 2, 0, -2, 1)/(2 dt^3) for x_{h-2} .. x_{h+2}
-        const float iv = cf.inv_12dt, ia = cf.inv_12dt2, ij = cf.inv_2dt3;
+        const float iv = s.tdp[1], ia = s.tdp[2], ij = s.tdp[3];
         float gdp = 0.f;
         for (int idx = tid; idx < D * NC; idx += NT) {
             const int d = idx / NC, h = idx - d * NC;   // V_h <-> x_{h+1}

@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
 
     if (t < D) s.st[t] = kp.start[p * D + t];
     if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[p * kp.cp.gw + t / NC];
+    stage_dt(kp, s, p);
     const float *seed = kp.q_in + (size_t)unit * N;
     float lo_e[2], hi_e[2];
 #pragma unroll
@@ -477,6 +478,7 @@ __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ 
     float *thA = smem + kp.lay.solver;
     if (t < D) s.st[t] = kp.start[(size_t)b * D + t];
     if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[(size_t)b * kp.cp.gw + t / NC];
+    stage_dt(kp, s, b);
     for (int i = t; i < N; i += NT) thA[i] = kp.q_in[(size_t)b * N + i];
     __syncthreads();
     eval_pass<MODE_TO>(kp, smem, thA, K, H, nullptr);
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KPara
     const RobotPack &rp = kp.rp;
     const int D = rp.D, t = threadIdx.x, lane = t & 31, warp = t >> 5;
     if (warp == 0)
-        for (int d = 0; d < D; ++d) s.q_cfg[d * NC + lane] = lane < n_act ? kp.q_in[(size_t)(b0 + lane) * D + d] : 0.f;
+        for (int d = 0; d < D; ++d) s.q_cfg[d * NC + lane] = lane < n_act ? kp.q_in[(size_t)(b0 + lane) * kp.q_stride + d] : 0.f;
     __syncthreads();
     prep_sincos(s, D);
     __syncthreads();
@@ -546,13 +548,21 @@ __global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KPara
             const float4 w = s.sw[m * NC + lane];
             o[0] = w.x; o[1] = w.y; o[2] = w.z; o[3] = sph[m].w;
         }
-    if (kp.ee_out && warp == 0 && lane < n_act) {
+    if ((kp.ee_out || kp.pos_err_out) && warp == 0 && lane < n_act) {
         const float *E = ee_frame(s, D) + lane;   // R (9, row-major) then p (3)
         float q[4];
         mat_to_quat(E[0], E[NC], E[2 * NC], E[3 * NC], E[4 * NC], E[5 * NC], E[6 * NC], E[7 * NC], E[8 * NC], q);
-        float *o = kp.ee_out + (size_t)(b0 + lane) * 7;
-        o[0] = E[9 * NC]; o[1] = E[10 * NC]; o[2] = E[11 * NC];
-        o[3] = q[0]; o[4] = q[1]; o[5] = q[2]; o[6] = q[3];
+        if (kp.ee_out) {
+            float *o = kp.ee_out + (size_t)(b0 + lane) * 7;
+            o[0] = E[9 * NC]; o[1] = E[10 * NC]; o[2] = E[11 * NC];
+            o[3] = q[0]; o[4] = q[1]; o[5] = q[2]; o[6] = q[3];
+        }
+        if (kp.pos_err_out) {   // goal errors (App. B "pose error"): |p_g - p|, 1 - |<q_g, q>| (A1)
+            const float *G = kp.goal + (size_t)((b0 + lane) / kp.goal_div) * 7;
+            const float ex = G[0] - E[9 * NC], ey = G[1] - E[10 * NC], ez = G[2] - E[11 * NC];
+            kp.pos_err_out[b0 + lane] = sqrtf(ex * ex + ey * ey + ez * ez);
+            kp.rot_err_out[b0 + lane] = 1.f - fabsf(G[3] * q[0] + G[4] * q[1] + G[5] * q[2] + G[6] * q[3]);
+        }
     }
 }
 
@@ -574,7 +584,7 @@ __global__ void __launch_bounds__(NT, 2) mask_kernel(const __grid_constant__ KPa
     const int b0 = blockIdx.x * NC;
     if (b0 >= total) return;                          // grid sized for n_cap >= n
     const int n_act = min(NC, total - b0);
-    const int env = edges ? kp.e_env : (kp.env ? kp.env[b0] : 0);
+    const int env = edges ? kp.e_env : (kp.env ? kp.env[b0 / kp.env_div] : 0);
     const int K = stage_tables(kp, smem, env);
     const Smem s = make_smem(kp, smem);
     const float *lim = s.fw + rp.o_lim;
@@ -595,7 +605,7 @@ __global__ void __launch_bounds__(NT, 2) mask_kernel(const __grid_constant__ KPa
             }
             s.q_cfg[d * NC + lane] = v;
         }
-        if (!edges && kp.env && lane < n_act && kp.env[b0 + lane] != env) flag[lane] = 8;   // env group rule
+        if (!edges && kp.env && lane < n_act && kp.env[(b0 + lane) / kp.env_div] != env) flag[lane] = 8;   // env group rule
     }
     __syncthreads();
     prep_sincos(s, D);
@@ -701,6 +711,146 @@ __global__ void steer_scan_kernel(int E, int D, const float *src, const float *d
     }
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     if (lane == 0) { h_out[e] = h; dist_out[e] = sqrtf(s2); }
+}
+
+// ------------------------------------------------------------------------------------------
+// motion-generation pipeline pieces (§8(f) f2; Alg. 4, App. B; readings B15-B18)
+// ------------------------------------------------------------------------------------------
+// Alg. 4 retime, one warp per trajectory: the five-point-stencil v, a, j of the state sequence
+// (O2 map of V with the start) at dt[b]; s = max(1e-3, max |v|/vmax, sqrt(|a|/amax),
+// cbrt(|j|/jmax)); dt_opt = s dt; max_jerk = max |j| / s^3 (the jerk at dt_opt).
+__global__ void retime_kernel(int B, int H, int D, const float *V, const float *start, int start_div, const float *dt,
+                              float dt_default, const float *lim, float *s_out, float *dt_out, float *jerk_out) {
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (b >= B) return;
+    const float *Vb = V + (size_t)b * H * D, *st = start + (size_t)(b / start_div) * D;
+    const float h_dt = dt ? dt[b] : dt_default;
+    const float i12 = 1.f / (12.f * h_dt), i12b = 1.f / (12.f * h_dt * h_dt), i2c = 1.f / (2.f * h_dt * h_dt * h_dt);
+    float rv = 0.f, ra = 0.f, rj = 0.f, jm = 0.f;
+    for (int e = lane; e < H * D; e += 32) {
+        const int h = e / D + 1, d = e - (h - 1) * D;     // state x_h, h = 1..H
+        float x[5];
+#pragma unroll
+        for (int o = 0; o < 5; ++o) {
+            const int k = h - 2 + o;                        // Table 5 map: pin / alias / V
+            x[o] = k <= 3 ? st[d] : (k >= H - 3 ? Vb[(H - 1) * D + d] : Vb[(k - 1) * D + d]);
+        }
+        const float v = (-x[4] + 8.f * x[3] - 8.f * x[1] + x[0]) * i12;
+        const float a = (-x[4] + 16.f * x[3] - 30.f * x[2] + 16.f * x[1] - x[0]) * i12b;
+        const float j = (x[4] - 2.f * x[3] + 2.f * x[1] - x[0]) * i2c;
+        rv = fmaxf(rv, fabsf(v) / lim[2 * D + d]);
+        ra = fmaxf(ra, sqrtf(fabsf(a) / lim[3 * D + d]));
+        rj = fmaxf(rj, cbrtf(fabsf(j) / lim[4 * D + d]));
+        jm = fmaxf(jm, fabsf(j));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        rv = fmaxf(rv, __shfl_xor_sync(0xffffffffu, rv, o));
+        ra = fmaxf(ra, __shfl_xor_sync(0xffffffffu, ra, o));
+        rj = fmaxf(rj, __shfl_xor_sync(0xffffffffu, rj, o));
+        jm = fmaxf(jm, __shfl_xor_sync(0xffffffffu, jm, o));
+    }
+    if (lane == 0) {
+        const float sc = fmaxf(fmaxf(fmaxf(rv, ra), rj), 1e-3f);
+        s_out[b] = sc;
+        if (dt_out) dt_out[b] = sc * h_dt;
+        if (jerk_out) jerk_out[b] = jm / (sc * sc * sc);
+    }
+}
+
+// App. B scores (reading B18); +inf marks an invalid seed.  IK: w_pose (pe + re) + w_dist |q - q0|
+// for seeds inside the pose thresholds whose configuration is valid (mask).  TO: the blended
+// w_pose (pe + re) + w_jerk max|j| + w_time (H-1) dt_opt for seeds inside the pose thresholds whose
+// H states are all valid.
+__global__ void ik_scores_kernel(int P, int S, int D, const float *q, const float *q0, const float *pe, const float *re,
+                                 const unsigned char *valid, float pos_thr, float rot_thr, float w_pose, float w_dist,
+                                 float penalty, float *score) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P * S) return;
+    const int p = i / S;
+    float d2 = 0.f;
+    for (int d = 0; d < D; ++d) {
+        const float e = q[(size_t)i * D + d] - q0[(size_t)p * D + d];
+        d2 = fmaf(e, e, d2);
+    }
+    const bool ok = (!valid || valid[i]) && pe[i] < pos_thr && re[i] < rot_thr;
+    score[i] = w_pose * (pe[i] + re[i]) + w_dist * sqrtf(d2) + (ok ? 0.f : penalty);
+}
+
+__global__ void to_scores_kernel(int P, int S, int H, const float *pe, const float *re, const float *max_jerk,
+                                 const float *dt_opt, const unsigned char *valid, float pos_thr, float rot_thr,
+                                 float w_pose, float w_jerk, float w_time, float penalty, float *score) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P * S) return;
+    bool ok = pe[i] < pos_thr && re[i] < rot_thr;
+    if (valid)
+        for (int h = 0; h < H && ok; ++h) ok = valid[(size_t)i * H + h] != 0;
+    score[i] = w_pose * (pe[i] + re[i]) + w_jerk * max_jerk[i] + w_time * (float)(H - 1) * dt_opt[i] + (ok ? 0.f : penalty);
+}
+
+// Per problem: the k lowest finite scores in ascending order (ties -> lower seed index), one warp
+// per problem; idx[p][j] for j >= count repeats the ranked list cyclically (-1 if count = 0).
+__global__ void rank_kernel(int P, int S, const float *score, int k, int *idx, int *count) {
+    const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (p >= P) return;
+    const float *sc = score + (size_t)p * S;
+    int cnt = 0;
+    for (int s0 = 0; s0 < S; s0 += 32) {
+        const int sidx = s0 + lane;
+        const bool fin = sidx < S && sc[sidx] < INFINITY;
+        cnt += __popc(__ballot_sync(0xffffffffu, fin));
+    }
+    for (int s0 = 0; s0 < S; s0 += 32) {
+        const int si = s0 + lane;
+        if (si < S) {
+            const float v = sc[si];
+            if (v < INFINITY) {
+                int r = 0;                                     // rank = #(finite entries before it)
+                for (int t = 0; t < S; ++t) {
+                    const float w = sc[t];
+                    r += (w < v) || (w == v && t < si);
+                }
+                for (int j = r; j < k; j += cnt) idx[(size_t)p * k + j] = si;
+            }
+        }
+    }
+    if (cnt == 0)
+        for (int j = lane; j < k; j += 32) idx[(size_t)p * k + j] = -1;
+    if (lane == 0) count[p] = cnt;
+}
+
+// Linear TO seeds (reading B17): V_h = q0 + (h / (H-1)) (qT - q0) from the ranked terminal
+// configurations qT[p][idx[p][s]] (idx may be NULL = s; idx < 0 -> the start, a still seed).
+__global__ void linear_seeds_kernel(int P, int S, int H, int D, const float *q0, const float *qT, int Sq, const int *idx,
+                                    float *seeds) {
+    const size_t n = (size_t)P * S * H * D;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        const int d = (int)(e % D), h = (int)((e / D) % H), s = (int)((e / ((size_t)D * H)) % S), p = (int)(e / ((size_t)D * H * S));
+        const int j = idx ? idx[(size_t)p * S + s] : s;
+        const float a = q0[(size_t)p * D + d];
+        const float b = j >= 0 ? qT[((size_t)p * Sq + j) * D + d] : a;
+        seeds[e] = a + ((float)h / (float)(H - 1)) * (b - a);
+    }
+}
+
+// The trajectory states x_1..x_H of optimisation variables V (Table 5 last row, O2): x_h = start for
+// h <= 3, x_h = V_{H-1} for h >= H-3, else V_{h-1} (V_0..V_2 and V_{H-4..H-2} are not states).
+__global__ void states_kernel(int B, int H, int D, const float *V, const float *start, int start_div, float *x) {
+    const size_t n = (size_t)B * H * D;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        const int d = (int)(e % D), h = (int)((e / D) % H) + 1, b = (int)(e / ((size_t)D * H));
+        const float *Vb = V + (size_t)b * H * D;
+        x[e] = h <= 3 ? start[(size_t)(b / start_div) * D + d] : (h >= H - 3 ? Vb[(H - 1) * D + d] : Vb[(h - 1) * D + d]);
+    }
+}
+
+// dst[p][:] = src[p][idx[p]][:] (rows of n floats; idx < 0 -> zeros)
+__global__ void gather_kernel(int P, int S, int n, const float *src, const int *idx, int idx_stride, float *dst) {
+    const size_t tot = (size_t)P * n;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+        const int p = (int)(e / n), c = (int)(e % n);
+        const int j = idx[(size_t)p * idx_stride];
+        dst[e] = j >= 0 ? src[((size_t)p * S + j) * n + c] : 0.f;
+    }
 }
 
 __global__ void select_kernel(int P, int S, int N, const float *seed_cost, const float *seed_traj,
@@ -884,6 +1034,7 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.gq = take(D * NC);
     L.gva = take(mode == MODE_TO ? 3 * D * NC : 4);
     L.pose_ft = take(6 * NC);
+    L.tdp = take(8);
     L.goal = take(std::max(7, D) * NC);   // pose [7][32] or joint-space goal [D][32] (CRB_CSPACE)
     L.cfg_cost = take(NC);
     L.cfg_terms = take(5 * NC);
@@ -1280,6 +1431,7 @@ crb_status crb_fk(crb_ctx *ctx, const float *q, int B, float *spheres_out, float
     KParams kp = base_params(ctx);
     kp.kmax = 0;
     kp.B = B; kp.H = 1; kp.cp.H = 1; kp.mode = MODE_IK; kp.q_in = q; kp.spheres_out = spheres_out; kp.ee_out = ee_out;
+    kp.q_stride = ctx->rp.D;
     const size_t bytes = make_layout(ctx->rp, 0, MODE_IK, 1, 1, 1, false, kp.lay);
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large");
     return launch(ctx, fk_kernel, (B + NC - 1) / NC, bytes, (cudaStream_t)stream, kp, "fk_kernel");
@@ -1287,6 +1439,12 @@ crb_status crb_fk(crb_ctx *ctx, const float *q, int B, float *spheres_out, float
 
 crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, const int *env, const float *start,
                                   const float *goal, float *cost, float *grad, float *term_costs, void *stream) {
+    return crb_evaluate_cost_grad_dt(ctx, q, B, H, env, start, goal, nullptr, cost, grad, term_costs, stream);
+}
+
+crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H, const int *env, const float *start,
+                                     const float *goal, const float *dt, float *cost, float *grad, float *term_costs,
+                                     void *stream) {
     crb_status st = enter(ctx);
     if (st != CRB_OK) return st;
     if ((st = ready(ctx, true)) != CRB_OK) return st;
@@ -1296,7 +1454,7 @@ crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, co
         return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 32, H*D <= 512 and start");
     KParams kp = base_params(ctx);
     kp.B = B; kp.H = H; kp.cp.H = H; kp.mode = mode; kp.q_in = q; kp.env = env; kp.start = start; kp.goal = goal;
-    kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs;
+    kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs; kp.dt_arr = dt;
     const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
     if (mode == MODE_TO) return launch(ctx, eval_to_kernel, B, bytes, (cudaStream_t)stream, kp, "eval_to_kernel");
@@ -1306,6 +1464,14 @@ crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, co
 crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H, const float *seeds,
                            const int *env, const float *start, const float *goal, float *best_traj, float *best_cost,
                            int64_t *best_key, float *seed_best_cost, float *seed_best_traj, void *stream) {
+    return crb_lbfgs_solve_dt(ctx, sp, P, S, H, seeds, env, start, goal, nullptr, best_traj, best_cost, best_key,
+                              seed_best_cost, seed_best_traj, stream);
+}
+
+crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H, const float *seeds,
+                              const int *env, const float *start, const float *goal, const float *dt,
+                              float *best_traj, float *best_cost, int64_t *best_key, float *seed_best_cost,
+                              float *seed_best_traj, void *stream) {
     crb_status st = enter(ctx);
     if (st != CRB_OK) return st;
     if ((st = ready(ctx, true)) != CRB_OK) return st;
@@ -1328,6 +1494,7 @@ crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int
     if (!sbt) { if ((st = grow(ctx, &ctx->ws_traj, &ctx->cap_traj, (size_t)P * S * N)) != CRB_OK) return st; sbt = ctx->ws_traj; }
     KParams kp = base_params(ctx);
     kp.P = P; kp.S = S; kp.H = H; kp.cp.H = H; kp.mode = mode; kp.q_in = seeds; kp.env = env; kp.start = start; kp.goal = goal;
+    kp.dt_arr = mode == MODE_TO ? dt : nullptr;
     kp.iters = sp->iters; kp.m = sp->history; kp.A = sp->n_alpha; kp.ls_mode = sp->ls_mode;
     for (int i = 0; i < 8; ++i) kp.alpha[i] = sp->alpha[i];
     kp.c1 = sp->c1; kp.c2 = sp->c2; kp.seed_base = sp->global_seed_base;
@@ -1431,15 +1598,16 @@ crb_status crb_lbfgs_direction(int B, int n, int count, const float *S, const fl
     return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
 }
 
-crb_status crb_mask_samples(crb_ctx *ctx, const float *q, int K, const int *env, float margin, uint8_t *valid,
-                            void *stream) {
+crb_status crb_mask_samples(crb_ctx *ctx, const float *q, int K, const int *env, int env_div, float margin,
+                            uint8_t *valid, void *stream) {
     crb_status st = enter(ctx);
     if (st != CRB_OK) return st;
     if ((st = ready(ctx, true)) != CRB_OK) return st;
-    if (K < 0 || (K > 0 && (!q || !valid)) || !(margin >= 0.f)) return fail(ctx, CRB_E_ARG, "bad mask arguments");
+    if (K < 0 || (K > 0 && (!q || !valid)) || !(margin >= 0.f) || env_div < 1)
+        return fail(ctx, CRB_E_ARG, "bad mask arguments");
     KParams kp = base_params(ctx);
     kp.B = K; kp.H = 1; kp.cp.H = 1; kp.mode = MODE_IK; kp.q_in = q; kp.env = env; kp.margin = margin;
-    kp.mask_out = valid;
+    kp.mask_out = valid; kp.env_div = env_div;
     const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, MODE_IK, 1, 1, 1, false, kp.lay);
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
     return launch(ctx, mask_kernel, (K + NC - 1) / NC, bytes, (cudaStream_t)stream, kp, "mask_kernel");
@@ -1475,6 +1643,97 @@ crb_status crb_steer(crb_ctx *ctx, int E, const float *src, const float *dst, co
     if (n_out)
         st = cuda_check(ctx, cudaMemcpyAsync(n_out, ctx->ws_n, 2 * sizeof(int), cudaMemcpyDeviceToDevice, s), "n copy");
     return st;
+}
+
+crb_status crb_retime(crb_ctx *ctx, int B, int H, const float *V, const float *start, int start_div, const float *dt,
+                      float *scale, float *dt_opt, float *max_jerk, void *stream) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if ((st = ready(ctx, false)) != CRB_OK) return st;
+    if (B < 0 || H < 8 || (B > 0 && (!V || !start || !scale)) || start_div < 1)
+        return fail(ctx, CRB_E_ARG, "bad retime arguments (H >= 8, start_div >= 1)");
+    if (B == 0) return CRB_OK;
+    const float *lim = reinterpret_cast<const float *>(ctx->d_robot) + ctx->rp.o_lim;
+    retime_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(B, H, ctx->rp.D, V, start, start_div, dt,
+                                                                   ctx->params_ok ? ctx->cp.dt : 0.25f, lim, scale,
+                                                                   dt_opt, max_jerk);
+    ctx->launches++;
+    return cuda_check(ctx, cudaGetLastError(), "retime_kernel");
+}
+
+crb_status crb_goal_error(crb_ctx *ctx, int B, const float *q, int q_stride, const float *goal, int goal_div,
+                          float *pos_err, float *rot_err, void *stream) {
+    crb_status st = enter(ctx);
+    if (st != CRB_OK) return st;
+    if ((st = ready(ctx, false)) != CRB_OK) return st;
+    if (B < 0 || (B > 0 && (!q || !goal || !pos_err || !rot_err)) || q_stride < ctx->rp.D || goal_div < 1)
+        return fail(ctx, CRB_E_ARG, "bad goal_error arguments");
+    KParams kp = base_params(ctx);
+    kp.kmax = 0;
+    kp.B = B; kp.H = 1; kp.cp.H = 1; kp.mode = MODE_IK; kp.q_in = q; kp.q_stride = q_stride; kp.goal = goal;
+    kp.pos_err_out = pos_err; kp.rot_err_out = rot_err; kp.goal_div = goal_div;
+    const size_t bytes = make_layout(ctx->rp, 0, MODE_IK, 1, 1, 1, false, kp.lay);
+    if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large");
+    return launch(ctx, fk_kernel, (B + NC - 1) / NC, bytes, (cudaStream_t)stream, kp, "fk_kernel(goal_error)");
+}
+
+crb_status crb_ik_scores(int P, int S, int D, const float *q, const float *q0, const float *pos_err, const float *rot_err,
+                         const uint8_t *valid, float pos_thr, float rot_thr, float w_pose, float w_dist, float penalty,
+                         float *score, void *stream) {
+    if (P < 0 || S < 1 || D < 1 || (P > 0 && (!q || !q0 || !pos_err || !rot_err || !score))) return CRB_E_ARG;
+    if (P == 0) return CRB_OK;
+    ik_scores_kernel<<<(P * S + 255) / 256, 256, 0, (cudaStream_t)stream>>>(P, S, D, q, q0, pos_err, rot_err, valid, pos_thr,
+                                                                          rot_thr, w_pose, w_dist, penalty, score);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_to_scores(int P, int S, int H, const float *pos_err, const float *rot_err, const float *max_jerk,
+                         const float *dt_opt, const uint8_t *valid, float pos_thr, float rot_thr, float w_pose,
+                         float w_jerk, float w_time, float penalty, float *score, void *stream) {
+    if (P < 0 || S < 1 || H < 1 || (P > 0 && (!pos_err || !rot_err || !max_jerk || !dt_opt || !score))) return CRB_E_ARG;
+    if (P == 0) return CRB_OK;
+    to_scores_kernel<<<(P * S + 255) / 256, 256, 0, (cudaStream_t)stream>>>(P, S, H, pos_err, rot_err, max_jerk, dt_opt,
+                                                                          valid, pos_thr, rot_thr, w_pose, w_jerk, w_time,
+                                                                          penalty, score);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_rank_seeds(int P, int S, const float *score, int k, int *idx, int *count, void *stream) {
+    if (P < 0 || S < 1 || k < 1 || (P > 0 && (!score || !idx || !count))) return CRB_E_ARG;
+    if (P == 0) return CRB_OK;
+    rank_kernel<<<(P + 7) / 8, 256, 0, (cudaStream_t)stream>>>(P, S, score, k, idx, count);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_linear_seeds(int P, int S, int H, int D, const float *q0, const float *qT, int Sq, const int *idx,
+                            float *seeds, void *stream) {
+    if (P < 0 || S < 1 || H < 2 || D < 1 || Sq < 1 || (P > 0 && (!q0 || !qT || !seeds)) || (!idx && Sq < S))
+        return CRB_E_ARG;
+    if (P == 0) return CRB_OK;
+    const size_t n = (size_t)P * S * H * D;
+    const int grid = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+    linear_seeds_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(P, S, H, D, q0, qT, Sq, idx, seeds);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_trajectory_states(int B, int H, int D, const float *V, const float *start, int start_div, float *x,
+                                 void *stream) {
+    if (B < 0 || H < 8 || D < 1 || start_div < 1 || (B > 0 && (!V || !start || !x))) return CRB_E_ARG;
+    if (B == 0) return CRB_OK;
+    const size_t n = (size_t)B * H * D;
+    const int grid = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+    states_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(B, H, D, V, start, start_div, x);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_gather_rows(int P, int S, int n, const float *src, const int *idx, int idx_stride, float *dst,
+                           void *stream) {
+    if (P < 0 || S < 1 || n < 1 || idx_stride < 1 || (P > 0 && (!src || !idx || !dst))) return CRB_E_ARG;
+    if (P == 0) return CRB_OK;
+    const size_t tot = (size_t)P * n;
+    const int grid = (int)std::min<size_t>((tot + 255) / 256, 148 * 16);
+    gather_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(P, S, n, src, idx, idx_stride, dst);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
 }
 
 crb_status crb_particle_normals(uint32_t key0, uint32_t key1, int n_var, int n_particles, int iter, uint32_t seed,

@@ -87,8 +87,21 @@ _lib.crb_ls_select.argtypes = [C.c_int, C.c_int, F_P, _V, _V, _V, _V, C.c_float,
 _lib.crb_argmin_keys.argtypes = [C.c_int, C.c_int, _V, C.c_int64, _V, _V, _V]
 _lib.crb_lbfgs_direction.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, _V, _V, _V]
 _lib.crb_solver_occupancy.argtypes = [_V, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
-_lib.crb_mask_samples.argtypes = [_V, _V, C.c_int, _V, C.c_float, _V, _V]
+_lib.crb_mask_samples.argtypes = [_V, _V, C.c_int, _V, C.c_int, C.c_float, _V, _V]
 _lib.crb_steer.argtypes = [_V, C.c_int, _V, _V, _V, C.c_float, C.c_int, C.c_float, C.c_int, _V, _V, _V, _V, _V]
+_lib.crb_evaluate_cost_grad_dt.argtypes = [_V, _V, C.c_int, C.c_int, _V, _V, _V, _V, _V, _V, _V, _V]
+_lib.crb_lbfgs_solve_dt.argtypes = [_V, C.POINTER(crb_solver_params), C.c_int, C.c_int, C.c_int, _V, _V, _V, _V,
+                                    _V, _V, _V, _V, _V, _V, _V]
+_lib.crb_retime.argtypes = [_V, C.c_int, C.c_int, _V, _V, C.c_int, _V, _V, _V, _V, _V]
+_lib.crb_goal_error.argtypes = [_V, C.c_int, _V, C.c_int, _V, C.c_int, _V, _V, _V]
+_lib.crb_ik_scores.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, _V, _V, _V, C.c_float, C.c_float, C.c_float,
+                               C.c_float, C.c_float, _V, _V]
+_lib.crb_to_scores.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, _V, _V, _V, C.c_float, C.c_float, C.c_float,
+                               C.c_float, C.c_float, C.c_float, _V, _V]
+_lib.crb_rank_seeds.argtypes = [C.c_int, C.c_int, _V, C.c_int, _V, _V, _V]
+_lib.crb_linear_seeds.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _V, _V, C.c_int, _V, _V, _V]
+_lib.crb_trajectory_states.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, C.c_int, _V, _V]
+_lib.crb_gather_rows.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, C.c_int, _V, _V]
 _lib.crb_particle_normals.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_uint32, _V, _V]
 _lib.crb_launch_count.argtypes = [_V]
 _lib.crb_launch_count.restype = C.c_int64
@@ -96,7 +109,9 @@ _lib.crb_launch_count.restype = C.c_int64
 SYMBOLS = ["crb_create", "crb_destroy", "crb_last_error", "crb_version", "crb_set_robot", "crb_set_world",
            "crb_set_cost_params", "crb_fk", "crb_evaluate_cost_grad", "crb_lbfgs_solve", "crb_lbfgs_solve_host",
            "crb_ls_select", "crb_argmin_keys", "crb_lbfgs_direction", "crb_launch_count", "crb_solver_occupancy",
-           "crb_particle_normals", "crb_mask_samples", "crb_steer"]
+           "crb_particle_normals", "crb_mask_samples", "crb_steer", "crb_evaluate_cost_grad_dt",
+           "crb_lbfgs_solve_dt", "crb_retime", "crb_goal_error", "crb_ik_scores", "crb_to_scores",
+           "crb_rank_seeds", "crb_linear_seeds", "crb_gather_rows", "crb_trajectory_states"]
 
 
 def _ptr(t):
@@ -220,20 +235,43 @@ class Context:
         self._chk(_lib.crb_fk(self.h, _ptr(q), B, _ptr(spheres_out), _ptr(ee_out), _stream()))
         return spheres_out, ee_out
 
-    def evaluate(self, q, goal, start=None, env=None, grad=True, terms=True):
-        """q [B,H,D] (TO) or [B,D] (IK); returns (cost [B], grad, terms [B,5])."""
+    def evaluate(self, q, goal, start=None, env=None, grad=True, terms=True, dt=None):
+        """q [B,H,D] (TO) or [B,D] (IK); dt [B] per-row timestep (None = the params' dt);
+        returns (cost [B], grad, terms [B,5])."""
         import torch
         B = q.shape[0]
         H = 1 if q.dim() == 2 else q.shape[1]
         cost = torch.empty(B, device=q.device, dtype=torch.float32)
         g = torch.empty_like(q) if grad else None
         tc = torch.empty(B, 5, device=q.device, dtype=torch.float32) if terms else None
-        self._chk(_lib.crb_evaluate_cost_grad(self.h, _ptr(q), B, H, _ptr(env), _ptr(start), _ptr(goal), _ptr(cost),
-                                              _ptr(g), _ptr(tc), _stream()))
+        self._chk(_lib.crb_evaluate_cost_grad_dt(self.h, _ptr(q), B, H, _ptr(env), _ptr(start), _ptr(goal), _ptr(dt),
+                                                 _ptr(cost), _ptr(g), _ptr(tc), _stream()))
         return cost, g, tc
 
+    def retime(self, V, start, dt=None):
+        """Alg. 4 retime of V [B,H,D] (start [B or P, D]): returns (scale, dt_opt, max_jerk) [B]."""
+        import torch
+        B, H, _ = V.shape
+        div = B // start.shape[0]
+        out = [torch.empty(B, device=V.device, dtype=torch.float32) for _ in range(3)]
+        self._chk(_lib.crb_retime(self.h, B, H, _ptr(V), _ptr(start), div, _ptr(dt), _ptr(out[0]), _ptr(out[1]),
+                                  _ptr(out[2]), _stream()))
+        return tuple(out)
+
+    def goal_error(self, q, goal, B=None, stride=None, goal_div: int = 1):
+        """Goal errors of B configurations (rows of `stride` floats from q's start, e.g. the terminal
+        states of trajectories); goal [B // goal_div, 7].  Returns (pos_err, rot_err) [B]."""
+        import torch
+        B = goal.shape[0] * goal_div if B is None else B
+        pe = torch.empty(B, device=goal.device, dtype=torch.float32)
+        re = torch.empty(B, device=goal.device, dtype=torch.float32)
+        stride = q.shape[-1] if stride is None else stride
+        self._chk(_lib.crb_goal_error(self.h, B, _ptr(q), int(stride), _ptr(goal), int(goal_div), _ptr(pe), _ptr(re),
+                                      _stream()))
+        return pe, re
+
     def solve(self, sp: inputs.SolverParams, seeds, goal, start=None, env=None, seed_base: int = 0,
-              seed_outputs: bool = False, problem_base: int = 0):
+              seed_outputs: bool = False, problem_base: int = 0, dt=None):
         """seeds [P,S,H,D] (TO) or [P,S,D] (IK).  Returns dict of device tensors."""
         import torch
         P, S = seeds.shape[0], seeds.shape[1]
@@ -247,17 +285,19 @@ class Context:
             out["seed_best_cost"] = torch.empty(P, S, device=dev, dtype=torch.float32)
             out["seed_best_traj"] = torch.empty_like(seeds)
         s = solver_params_struct(sp, seed_base, problem_base)
-        self._chk(_lib.crb_lbfgs_solve(self.h, C.byref(s), P, S, H, _ptr(seeds), _ptr(env), _ptr(start), _ptr(goal),
-                                       _ptr(out["best_traj"]), _ptr(out["best_cost"]), _ptr(out["best_key"]),
-                                       _ptr(out.get("seed_best_cost")), _ptr(out.get("seed_best_traj")), _stream()))
+        self._chk(_lib.crb_lbfgs_solve_dt(self.h, C.byref(s), P, S, H, _ptr(seeds), _ptr(env), _ptr(start), _ptr(goal),
+                                          _ptr(dt), _ptr(out["best_traj"]), _ptr(out["best_cost"]),
+                                          _ptr(out["best_key"]), _ptr(out.get("seed_best_cost")),
+                                          _ptr(out.get("seed_best_traj")), _stream()))
         return out
 
-    def mask_samples(self, q, env=None, margin: float = 0.0):
-        """q [K,D] device fp32 -> valid [K] uint8 (Alg. 3 mask_samples)."""
+    def mask_samples(self, q, env=None, margin: float = 0.0, env_div: int = 1):
+        """q [K,D] device fp32 (env row k // env_div) -> valid [K] uint8 (Alg. 3 mask_samples)."""
         import torch
         K = q.shape[0]
         valid = torch.empty(K, dtype=torch.uint8, device=q.device)
-        self._chk(_lib.crb_mask_samples(self.h, _ptr(q), K, _ptr(env), float(margin), _ptr(valid), _stream()))
+        self._chk(_lib.crb_mask_samples(self.h, _ptr(q), K, _ptr(env), int(env_div), float(margin), _ptr(valid),
+                                        _stream()))
         return valid
 
     def steer(self, src, dst, dw, r: float, env: int = 0, margin: float = 0.0, n_cap: int = 256):
@@ -313,6 +353,68 @@ def lbfgs_direction(S, Y, g):
     d = torch.empty_like(g)
     _check_free(_lib.crb_lbfgs_direction(B, n, count, _ptr(S), _ptr(Y), _ptr(g), _ptr(d), _stream()))
     return d
+
+
+def ik_scores(q, q0, pos_err, rot_err, valid, pos_thr, rot_thr, w_pose, w_dist, penalty=float("inf")):
+    """q [P,S,D], q0 [P,D], errors [P,S], valid [P,S] uint8 (or None) -> score [P,S]."""
+    import torch
+    P, S, D = q.shape
+    score = torch.empty(P, S, device=q.device, dtype=torch.float32)
+    _check_free(_lib.crb_ik_scores(P, S, D, _ptr(q), _ptr(q0), _ptr(pos_err), _ptr(rot_err), _ptr(valid),
+                                   float(pos_thr), float(rot_thr), float(w_pose), float(w_dist), float(penalty),
+                                   _ptr(score), _stream()))
+    return score
+
+
+def to_scores(pos_err, rot_err, max_jerk, dt_opt, valid, H, pos_thr, rot_thr, w_pose, w_jerk, w_time,
+              penalty=float("inf")):
+    """errors / max_jerk / dt_opt [P,S], valid [P,S,H] uint8 (or None) -> blended score [P,S]."""
+    import torch
+    P, S = pos_err.shape
+    score = torch.empty(P, S, device=pos_err.device, dtype=torch.float32)
+    _check_free(_lib.crb_to_scores(P, S, int(H), _ptr(pos_err), _ptr(rot_err), _ptr(max_jerk), _ptr(dt_opt),
+                                   _ptr(valid), float(pos_thr), float(rot_thr), float(w_pose), float(w_jerk),
+                                   float(w_time), float(penalty), _ptr(score), _stream()))
+    return score
+
+
+def rank_seeds(score, k):
+    """score [P,S] -> (idx [P,k] int32, count [P] int32)."""
+    import torch
+    P, S = score.shape
+    idx = torch.empty(P, k, device=score.device, dtype=torch.int32)
+    cnt = torch.empty(P, device=score.device, dtype=torch.int32)
+    _check_free(_lib.crb_rank_seeds(P, S, _ptr(score), int(k), _ptr(idx), _ptr(cnt), _stream()))
+    return idx, cnt
+
+
+def linear_seeds(q0, qT, H, idx=None, S=None):
+    """q0 [P,D], qT [P,Sq,D], idx [P,S] (or None) -> seeds [P,S,H,D]."""
+    import torch
+    P, Sq, D = qT.shape
+    S = idx.shape[1] if idx is not None else (S or Sq)
+    seeds = torch.empty(P, S, H, D, device=qT.device, dtype=torch.float32)
+    _check_free(_lib.crb_linear_seeds(P, S, int(H), D, _ptr(q0), _ptr(qT), Sq, _ptr(idx), _ptr(seeds), _stream()))
+    return seeds
+
+
+def trajectory_states(V, start):
+    """V [B,H,D] optimisation variables, start [B or P, D] -> the states x_1..x_H [B,H,D]."""
+    import torch
+    B, H, D = V.shape
+    x = torch.empty_like(V)
+    _check_free(_lib.crb_trajectory_states(B, H, D, _ptr(V), _ptr(start), B // start.shape[0], _ptr(x), _stream()))
+    return x
+
+
+def gather_rows(src, idx, idx_stride=1):
+    """src [P,S,...], idx [P*idx_stride] int32 -> dst [P,...] = src[p, idx[p*idx_stride]]."""
+    import torch
+    P, S = src.shape[0], src.shape[1]
+    n = int(src[0, 0].numel())
+    dst = torch.empty((P,) + tuple(src.shape[2:]), device=src.device, dtype=torch.float32)
+    _check_free(_lib.crb_gather_rows(P, S, n, _ptr(src), _ptr(idx), int(idx_stride), _ptr(dst), _stream()))
+    return dst
 
 
 def particle_normals(key0, key1, n_var, n_particles, it, seed):
