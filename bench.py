@@ -219,6 +219,45 @@ def _timed_solves(ctx, sp, seeds, goal, start, env, steps, flush, world, dev):
     return tot / steps
 
 
+def motion_gen_metrics(local, rank, world, dev, steps):
+    """Device-timed (CUDA events around the whole pipeline call, host launches included) motion
+    generation: P = 64 problems per GPU in one batch, and P = 1 (latency)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2310_17274_b200 import motion_gen, native, parallel, workload
+    res = {}
+    for P in (64, 1):
+        lo = rank * P
+        wl = workload.franka_to(local, list(range(lo, lo + P)), S=12, H=32, iters=100)
+        ctx = native.Context(local)
+        ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
+        mg = motion_gen.MotionGen(ctx, wl.robot, wl.cost)
+        args = (torch.tensor(wl.start, device=dev), torch.tensor(wl.goal, device=dev),
+                torch.tensor(wl.env, device=dev), torch.tensor(mg.ik_seed_batch(wl.robot, range(lo, lo + P), 32),
+                                                               device=dev))
+        mg.plan(*args)
+        torch.cuda.synchronize()
+        tot, succ = 0.0, 0
+        for _ in range(steps):
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            out = mg.plan(*args)
+            b.record()
+            torch.cuda.synchronize()
+            tot += a.elapsed_time(b)
+            succ = int(out["success"].sum().item())
+        ms = tot / steps
+        if world > 1:
+            ms = parallel.max_over_ranks(ms, dev)
+        res[f"P{P}"] = {"problems_per_gpu": P, "ms_per_batch": ms, "problems_per_s": P * world / (ms * 1e-3),
+                        "success": succ, "ik_seeds": 32, "to_seeds": 12, "timesteps": 32,
+                        "iters": "IK 2p+100, TO 2p+100, refine 300"}
+        ctx.close()
+    return res
+
+
 def side_metrics(local, rank, world, dev, flush, steps=2):
     """The other metrics of BASELINE.json on their own configs (device-timed, max over ranks):
     config 3 -- collision-free IK, 1000 goals x 30 Halton seeds, 100 iterations, one shared K = 20
@@ -267,6 +306,22 @@ def side_metrics(local, rank, world, dev, flush, steps=2):
                              "warmup_cost_only_evals_per_s": n_part * world / (msw * 1e-3),
                              "to_problems_per_s_with_particles": n_f1 * world / (msp * 1e-3)}
     ctx.close()
+    # config 4: batched TO, 1024 problems x 12 seeds x 32 timesteps over 8 GPUs = 128 problems per
+    # GPU, each with its own K = 20 scene, 100 iterations
+    n4 = 128
+    lo = rank * n4
+    wl = workload.franka_to(local, list(range(lo, lo + n4)), S=12, H=32, iters=100)
+    ctx = native.Context(local)
+    ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
+    ms = _timed_solves(ctx, wl.solver, torch.tensor(wl.seeds, device=dev), torch.tensor(wl.goal, device=dev),
+                       torch.tensor(wl.start, device=dev), torch.tensor(wl.env, device=dev), steps, flush, world, dev)
+    out["cfg4_batched_to"] = {"problems_per_gpu": n4, "seeds": 12, "timesteps": 32, "iters": 100,
+                              "ms_per_solve": ms, "problems_per_s": n4 * world / (ms * 1e-3),
+                              "evals_per_s": wl.evals_per_solve() * world / (ms * 1e-3)}
+    ctx.close()
+    # f2: the whole motion-generation pipeline (IK -> seeds -> TO -> retime -> TO at dt_opt ->
+    # retime -> success), batched and for one problem (the paper's ~50 ms figure)
+    out["f2_motion_gen"] = motion_gen_metrics(local, rank, world, dev, steps)
     n_dense = 16
     lo = rank * n_dense
     wl = workload.franka_to(local, list(range(lo, lo + n_dense)), S=32, H=32, n_boxes=1000, iters=100, dense=True)

@@ -33,8 +33,8 @@ class MotionGenConfig:
     """Pipeline parameters.  Paper values: 30 IK seeds (P:1248, 32 here so IK rows stay in aligned
     warp groups for the mask), 12 TO seeds and 32 timesteps (Table 9 / P:2204 "Bookshelf"),
     dt_i = 0.25 s (Alg. 4 / P:2054), 2 particle iterations before L-BFGS, 100 TO
-    iterations and up to 300 for the single-seed re-optimisation.  Thresholds and
-    score weights are readings (B18)."""
+    iterations and up to 300 for the single-seed re-optimisation; the success
+    thresholds are the paper's; the score weights are readings (B18)."""
     ik_seeds: int = 32
     to_seeds: int = 12
     horizon: int = 32
@@ -43,8 +43,8 @@ class MotionGenConfig:
     to_iters: int = 100
     refine_iters: int = 300
     particle_iters: int = 2
-    pos_thr: float = 5e-3           # m
-    rot_thr: float = 1e-3           # 1 - |<q_g, q>|  (~5 deg)
+    pos_thr: float = 5e-3           # m: "within 5mm ... of desired position"
+    rot_thr: float = 0.05           # "5% of desired ... orientation" in the A1 metric 1 - |<q_g, q>|
     w_pose: float = 1.0
     w_dist: float = 0.01
     w_jerk: float = 1e-4

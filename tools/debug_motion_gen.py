@@ -13,7 +13,7 @@ import dataclasses, os
 cost = dataclasses.replace(wl.cost, a1=wl.cost.a1 * float(os.environ.get("A1X", "1")),
                            a0=wl.cost.a0 * float(os.environ.get("A0X", "1")))
 ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(cost)
-cfg = motion_gen.MotionGenConfig(rot_thr=float(os.environ.get("ROT", "1e-3")))
+cfg = motion_gen.MotionGenConfig(**({"rot_thr": float(os.environ["ROT"])} if "ROT" in os.environ else {}))
 mg = motion_gen.MotionGen(ctx, wl.robot, cost, cfg)
 T = lambda a, dt=torch.float32: torch.tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
 out = mg.plan(T(wl.start), T(wl.goal), T(wl.env, torch.int32), T(mg.ik_seed_batch(wl.robot, range(P), 32)))
