@@ -68,57 +68,74 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
-    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
-              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap"]
+    """SM clock + throttle reasons polled through NVML every 10 ms during the timed region (the
+    recipe's clocks line; nvidia-smi -lms as a fallback when NVML is unavailable)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.stop = threading.Event()
+        self.th = None
 
-    def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
-            self.th.start()
-        except Exception:
-            self.proc = None
-        return self
+    def _poll_nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+        self.mx.append(float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)))
+        while not self.stop.is_set():
+            self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for n, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(n)
+            time.sleep(0.01)
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
-
-    def summary(self):
-        sm, mx, reasons = [], [], set()
+    def _poll_smi(self):
+        fields = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+                  "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+                  "clocks_event_reasons.sw_power_cap"]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(fields),
+                                 "--format=csv,noheader,nounits", "-lms", "50"],
+                                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        threading.Thread(target=lambda: (self.stop.wait(), proc.terminate()), daemon=True).start()
+        for ln in proc.stdout:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
             try:
-                sm.append(float(parts[0])); mx.append(float(parts[1]))
-            except ValueError:
+                self.sm.append(float(parts[0])); self.mx.append(float(parts[1]))
+            except (ValueError, IndexError):
                 continue
             for n, v in zip(names, parts[2:6]):
                 if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
+                    self.reasons.add(n)
+
+    def _run(self):
+        try:
+            self._poll_nvml()
+        except Exception:
+            try:
+                self._poll_smi()
+            except Exception:
+                pass
+
+    def __enter__(self):
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        time.sleep(0.02)
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(3)
+
+    def summary(self):
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_min_mhz": min(self.sm),
+                "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
 def oracle_sample_rate(wl, problem: int, iters: int, nthreads: int):

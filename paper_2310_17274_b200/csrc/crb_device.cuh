@@ -14,6 +14,29 @@
 // P:n = line n of the paper; A* = readings listed in DESIGN.md.
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
+
+// Work counters of the world screen (tools/world_stats.py builds a separate library with 1).
+#ifndef CRB_STATS
+#define CRB_STATS 0
+#endif
+#if CRB_STATS
+__device__ unsigned long long g_crb_stats[8];
+#define CRB_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_crb_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define CRB_STAT(i, v) do { } while (0)
+#endif
+
+// World pre-screen on the tensor cores: 1 = the affine cuboid-frame
+// transform of a world group runs as HMMA.16816 on an fp16 hi/lo split, 0 = the FFMA screen only.
+#ifndef CRB_WORLD_MMA
+#define CRB_WORLD_MMA 1
+#endif
+// ... used when the environment has at least this many cuboids (below it the FFMA screen is as
+// fast and its smaller code keeps the instruction cache warm: DESIGN.md "World screen")
+#ifndef CRB_MMA_MIN_K
+#define CRB_MMA_MIN_K 32
+#endif
 
 namespace crb {
 
@@ -60,6 +83,7 @@ struct Layout {
 struct CostP {
     float a0, a1, a2, a3, a8, a9, wb[4], beta_self, beta_world, eta, eta_bound, dt;
     float inv_eta, inv_2dt;   // host-computed reciprocals (no divisions in the hot loops)
+    float inv_eta_bound;
     float inv_12dt, inv_12dt2, inv_2dt3;   // five-point stencil scales 1/(12 dt), 1/(12 dt^2), 1/(2 dt^3)
     float a4, a5;             // Eq. cspace-cost
     int sweep_steps, H;
@@ -190,14 +214,17 @@ __device__ __forceinline__ float activation(float dp, float eta, float inv_eta, 
     return dp - 0.5f * eta;
 }
 
-// Eq. bound_cost, the five branches in the paper's order.
-__device__ __forceinline__ float bound_cost(float x, float lo, float hi, float e2, float &dx) {
-    if (x < lo) { dx = -1.f; return lo - x + 0.5f * e2; }
-    if (lo + e2 > x && x >= lo) { float t = lo - x + e2; dx = -t / e2; return 0.5f / e2 * t * t; }
-    if (x > hi) { dx = 1.f; return x - hi + 0.5f * e2; }
-    if (hi - e2 < x && x <= hi) { float t = x - hi + e2; dx = t / e2; return 0.5f / e2 * t * t; }
-    dx = 0.f;
-    return 0.f;
+// Eq. bound_cost, branch-free.  The paper's cases in order: x < lo and
+// lo <= x < lo + e2 (the lower side, t = lo - x + e2), then x > hi and hi - e2 < x <= hi (the upper
+// side, t = x - hi + e2), else 0.  On the selected side, with c = clamp(t, 0, e2):
+// cost = c^2 / (2 e2) + max(t - e2, 0) (= t - e2/2 beyond the limit), d cost / dx = -+c / e2.
+// Taking the lower side iff x < lo + e2 keeps the printed case order when the bands overlap.
+__device__ __forceinline__ float bound_cost(float x, float lo, float hi, float e2, float ie2, float &dx) {
+    const bool low = lo + e2 > x;
+    const float t = low ? lo - x + e2 : x - hi + e2;
+    const float c = fminf(fmaxf(t, 0.f), e2);
+    dx = (low ? -c : c) * ie2;
+    return 0.5f * ie2 * c * c + fmaxf(t - e2, 0.f);
 }
 
 // log cosh accurate in fp32 for all x: log1p(2 sinh^2(x/2)) for |x| < 5, else the
@@ -550,6 +577,36 @@ __device__ __forceinline__ float box_screen(float cx, float cy, float cz, const 
     return fmaf(mx, mx, fmaf(my, my, mz * mz));
 }
 
+// ---- tensor-core pre-screen of the cuboid test.  For a world group
+// (4 spheres x 32 slots = 128 rows) and 8 cuboids, the cuboid-frame coordinates
+// p_loc_c = col_c . w + off_c are a dense [128 x 4] x [4 x 8] product per coordinate c.  One
+// mma.m16n8k16 (fp16 in, fp32 accumulate) per 16 rows, 8 cuboids and coordinate computes it on
+// an fp16 hi/lo split of both operands:
+//   A row = (wh, 1 | wh, 1 | wl, 0 | 0),  B col = (Bh | Bl | Bh | 0)  =>  A.B = wh.(Bh + Bl) + wl.Bh,
+// i.e. (wh + wl).(Bh + Bl) without the wl.Bl term: |error| <= ~5e-6 (1 + |w|)(1 + |B|) m, covered
+// by the per-cuboid slack in h.w (set_world).  The result only decides which cuboids go through
+// the exact fp32 test below, so the world term is bitwise the FFMA path's.
+__device__ __forceinline__ void split_h2(float x, float y, unsigned &hi, unsigned &lo) {
+    const __half2 h = __floats2half2_rn(x, y);
+    const float2 f = __half22float2(h);
+    const __half2 l = __floats2half2_rn(x - f.x, y - f.y);
+    hi = *reinterpret_cast<const unsigned *>(&h);
+    lo = *reinterpret_cast<const unsigned *>(&l);
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%10,%10,%10};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
+}
+
+// inside the cuboid expanded by e along every axis (Chebyshev bound of the Euclidean test);
+// written as !(|p| >= e) so a NaN coordinate is flagged and left to the exact test
+__device__ __forceinline__ bool in_ebox(float px, float py, float pz, float ex, float ey, float ez) {
+    return !(fabsf(px) >= ex) && !(fabsf(py) >= ey) && !(fabsf(pz) >= ez);
+}
+
 // Rare path: the hit's activation and gradient, then the backward / forward marches (A6-A12):
 // L = |n - c|, bound = L/2, j = J0 (r' on a hit, else sd), at most n_s samples p = c + (j/L)(n - c);
 // a hit adds phi and (1 - kappa) phi' (-grad sd) and jumps r', a miss jumps sd.
@@ -631,7 +688,7 @@ __device__ __forceinline__ void stage_dt(const KParams &kp, const Smem &s, int r
     s.tdp[5] = (float)(cf.a9 * (r2 * r2 * r2));
 }
 
-template <int MODE>
+template <int MODE, bool WMMA>
 __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
                                           const float *dvec, bool grad = true) {
     const Smem s = make_smem(kp, smem);
@@ -690,17 +747,17 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     const float a = (-xp2 + 16.f * xp1 - 30.f * x0 + 16.f * xm1 - xm2) * s.tdp[2];
                     const float j = (xp2 - 2.f * xp1 + 2.f * xm1 - xm2) * s.tdp[3];
                     const float vm = lim[2 * D + d], am = lim[3 * D + d], jm = lim[4 * D + d];
-                    cb += cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd); gx = cf.wb[0] * dd;
-                    cb += cf.wb[1] * bound_cost(v, -vm, vm, cf.eta_bound, dd); gv = cf.wb[1] * dd;
-                    cb += cf.wb[2] * bound_cost(a, -am, am, cf.eta_bound, dd); ga = cf.wb[2] * dd;
-                    cb += cf.wb[3] * bound_cost(j, -jm, jm, cf.eta_bound, dd); gj = cf.wb[3] * dd;
+                    cb += cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, cf.inv_eta_bound, dd); gx = cf.wb[0] * dd;
+                    cb += cf.wb[1] * bound_cost(v, -vm, vm, cf.eta_bound, cf.inv_eta_bound, dd); gv = cf.wb[1] * dd;
+                    cb += cf.wb[2] * bound_cost(a, -am, am, cf.eta_bound, cf.inv_eta_bound, dd); ga = cf.wb[2] * dd;
+                    cb += cf.wb[3] * bound_cost(j, -jm, jm, cf.eta_bound, cf.inv_eta_bound, dd); gj = cf.wb[3] * dd;
                     const float a8 = s.tdp[4], a9 = s.tdp[5];
                     cs = a8 * a * a;
                     ga += 2.f * a8 * a;
                     if (cf.flags & F_JERK) { cs += a9 * j * j; gj += 2.f * a9 * j; }
                 } else {
                     const float x0 = s.q_cfg[d * NC + c];
-                    cb = cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, dd);
+                    cb = cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, cf.inv_eta_bound, dd);
                     gx = cf.wb[0] * dd;
                 }
             }
@@ -833,14 +890,19 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         if (r >= 0.f && spd != 0.f) th2[u] = fmaxf(rpr * rpr, maxb2);
                     }
                 }
-                if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
-                    for (int k = 0; k < K; ++k) {
+                // exact fp32 test of cuboid k for the group (the screen of record)
+                auto exact_box = [&](int k, bool reload) {
                         const BoxView b = load_box(s.boxes, k);
                         float s2[4];
                         bool any = false;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            s2[u] = box_screen(cx[u], cy[u], cz[u], b);
+                            if (reload) {   // after the tensor-core screen: reload instead of holding it
+                                const float4 c = m0 + u < rp.M ? s.sw[(m0 + u) * NC + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+                                s2[u] = box_screen(c.x, c.y, c.z, b);
+                            } else {
+                                s2[u] = box_screen(cx[u], cy[u], cz[u], b);
+                            }
                             any |= s2[u] < th2[u];
                         }
                         // rare path, compacted: the flagged (sphere u, slot) entries of this cuboid
@@ -849,10 +911,12 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         // every accumulator sees the same sequence of additions as a per-lane loop.
                         if (__any_sync(FULL, any)) {
                             unsigned bal[4];
+                            CRB_STAT(2, 1);
 #pragma unroll
                             for (int u = 0; u < 4; ++u) bal[u] = __ballot_sync(FULL, s2[u] < th2[u]);
                             const int n0 = __popc(bal[0]), n1 = __popc(bal[1]), n2 = __popc(bal[2]);
                             const int tot = n0 + n1 + n2 + __popc(bal[3]);
+                            CRB_STAT(3, tot);
                             for (int e = lane; e - lane < tot; e += 32) {
                                 if (e >= tot) continue;
                                 int u = 0, r = e;
@@ -871,7 +935,95 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                          rpr, dr, cf.eta, cf.inv_eta, cf.sweep_steps);
                             }
                         }
+                };
+                if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
+                    CRB_STAT(0, K);
+#if CRB_WORLD_MMA
+                    if (WMMA) {
+                    // tensor-core pre-screen, 8 cuboids per step; only cuboids with a flagged row
+                    // go through exact_box, in increasing k (the accumulation order of the FFMA path)
+                    const int g8 = lane >> 2, t4 = lane & 3;
+                    const bool odd = t4 & 1, hi_only = t4 >= 2;
+                    unsigned thb = 0u, wb = 0u;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        thb = max(thb, th2[u] > 0.f ? __float_as_uint(th2[u]) : 0u);
+                        wb = max(wb, max(__float_as_uint(fabsf(cx[u])),
+                                         max(__float_as_uint(fabsf(cy[u])), __float_as_uint(fabsf(cz[u])))));
                     }
+                    // group threshold: the largest sqrt(th2) (>= every row's), and the |w| factor of the
+                    // rounding slack (NaN bits order above inf: a NaN makes every cuboid flagged)
+                    const float thg = sqrtf(__uint_as_float(__reduce_max_sync(FULL, thb)));
+                    // (|w| >= 3e4 m would overflow fp16: the NaN factor then flags every cuboid)
+                    const float wm = __uint_as_float(__reduce_max_sync(FULL, wb));
+                    const float wfac = wm < 3e4f ? 1.f + wm : __uint_as_float(0x7fc00000u);
+                    unsigned af[8][4];   // A fragments: m-tile mt = (sphere mt>>1, slots 16(mt&1) + 0..15)
+#pragma unroll
+                    for (int mt = 0; mt < 8; ++mt) {
+                        const int m = min(m0 + (mt >> 1), rp.M - 1), sl = ((mt & 1) << 4) + g8;
+                        const float4 w0 = s.sw[m * NC + sl], w1 = s.sw[m * NC + sl + 8];
+                        unsigned h0, l0, h1, l1;
+                        split_h2(odd ? w0.z : w0.x, odd ? 1.f : w0.y, h0, l0);
+                        split_h2(odd ? w1.z : w1.x, odd ? 1.f : w1.y, h1, l1);
+                        af[mt][0] = h0; af[mt][1] = h1;
+                        af[mt][2] = hi_only ? 0u : l0; af[mt][3] = hi_only ? 0u : l1;
+                    }
+                    const float4 *bx4 = reinterpret_cast<const float4 *>(s.boxes);
+                    for (int kb = 0; kb < K; kb += 8) {
+                        // B fragments of cuboid kb + g8 (column g8), one per coordinate
+                        const float4 *bk = bx4 + 4 * min(kb + g8, K - 1);
+                        unsigned b0[3], b1[3];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const float2 v = reinterpret_cast<const float2 *>(bk + c)[odd];
+                            unsigned hi, lo;
+                            split_h2(v.x, v.y, hi, lo);
+                            b0[c] = hi_only ? lo : hi;
+                            b1[c] = hi_only ? 0u : hi;
+                        }
+                        // expanded half extents of this thread's C columns: cuboids kb + 2 t4 + j
+                        float ex[2], ey[2], ez[2];
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            const int kk = kb + 2 * t4 + j;
+                            const float4 h = bx4[4 * min(kk, K - 1) + 3];
+                            const float e = fmaf(h.w, wfac, thg);
+                            const bool ok = kk < K;
+                            ex[j] = ok ? h.x + e : -1.f; ey[j] = ok ? h.y + e : -1.f; ez[j] = ok ? h.z + e : -1.f;
+                        }
+                        bool f0 = false, f1 = false;
+#pragma unroll
+                        for (int mt = 0; mt < 8; ++mt) {
+                            float px[4], py[4], pz[4];
+                            mma16816(px, af[mt], b0[0], b1[0]);
+                            mma16816(py, af[mt], b0[1], b1[1]);
+                            mma16816(pz, af[mt], b0[2], b1[2]);
+                            f0 |= in_ebox(px[0], py[0], pz[0], ex[0], ey[0], ez[0]) |
+                                  in_ebox(px[2], py[2], pz[2], ex[0], ey[0], ez[0]);
+                            f1 |= in_ebox(px[1], py[1], pz[1], ex[1], ey[1], ez[1]) |
+                                  in_ebox(px[3], py[3], pz[3], ex[1], ey[1], ez[1]);
+                        }
+                        const unsigned q0 = __ballot_sync(FULL, f0), q1 = __ballot_sync(FULL, f1);
+                        if (q0 | q1) {
+                            // column 2t + j is flagged iff a lane with lane & 3 == t has its bit
+                            unsigned n0 = q0 | (q0 >> 16), n1 = q1 | (q1 >> 16);
+                            n0 |= n0 >> 8; n1 |= n1 >> 8;
+                            n0 = (n0 | (n0 >> 4)) & 0xfu; n1 = (n1 | (n1 >> 4)) & 0xfu;
+                            unsigned mask = 0u;
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) mask |= ((n0 >> t) & 1u) << (2 * t) | ((n1 >> t) & 1u) << (2 * t + 1);
+                            if (K - kb < 8) mask &= (1u << (K - kb)) - 1u;
+                            CRB_STAT(1, __popc(mask));
+                            while (mask) {
+                                const int b = __ffs(mask) - 1;
+                                mask &= mask - 1u;
+                                exact_box(kb + b, true);
+                            }
+                        }
+                    }
+                    } else
+#endif
+                    for (int k = 0; k < K; ++k) exact_box(k, false);
                 }
                 // the group's cost goes to the .w of its first sphere (unused by the backward):
                 // the merge sums the groups in index order, whichever warp took them

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -66,6 +67,7 @@ __device__ void two_loop_block(int N, int Np, int count, const int *order, const
 // ------------------------------------------------------------------------------------------
 // persistent TO solver: one CTA per (problem, seed)
 // ------------------------------------------------------------------------------------------
+template <bool WMMA>
 __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int unit = blockIdx.x;
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             __syncthreads();
         }
         // ---- a2..a10: one evaluation pass (cost only for particles)
-        eval_pass<MODE_TO>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr, !part);
+        eval_pass<MODE_TO, WMMA>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr, !part);
         if (part) {
             // ---- f1 UPDATE, streamed over the particles (Eqs. particle_1/2, B6)
             float r;
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
 // ------------------------------------------------------------------------------------------
 // persistent IK solver: one CTA per (problem, group of 32 seeds); lane = seed
 // ------------------------------------------------------------------------------------------
+template <bool WMMA>
 __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int G = (kp.S + NC - 1) / NC;
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
                 s.scs[DC + idx] = cs;
             }
         }
-        eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr, !part);
+        eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
         if (part) {
             // ---- f1 UPDATE, streamed over the particles (Eqs. particle_1/2, B6), per seed
             float r;
@@ -468,6 +471,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
 // ------------------------------------------------------------------------------------------
 // one-shot evaluation, FK, selection
 // ------------------------------------------------------------------------------------------
+template <bool WMMA>
 __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b = blockIdx.x;
@@ -481,7 +485,7 @@ __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ 
     stage_dt(kp, s, b);
     for (int i = t; i < N; i += NT) thA[i] = kp.q_in[(size_t)b * N + i];
     __syncthreads();
-    eval_pass<MODE_TO>(kp, smem, thA, K, H, nullptr);
+    eval_pass<MODE_TO, WMMA>(kp, smem, thA, K, H, nullptr);
     if (t < 32) {
         float tr[5];
         for (int k = 0; k < 5; ++k) tr[k] = warp_sum(s.cfg_terms[k * NC + t]);
@@ -495,6 +499,7 @@ __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ 
         for (int i = t; i < N; i += NT) kp.grad_out[(size_t)b * N + i] = s.gV[i];
 }
 
+template <bool WMMA>
 __global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b0 = blockIdx.x * NC;
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ 
     }
     __syncthreads();
     prep_sincos(s, D);
-    eval_pass<MODE_IK>(kp, smem, nullptr, K, n_act, nullptr);
+    eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr);
     if (warp == 0 && lane < n_act) {
         const int b = b0 + lane;
         const bool ok = !kp.env || kp.env[b] == env0;
@@ -1072,6 +1077,7 @@ KParams base_params(const crb_ctx *ctx) {
     k.a4 = c.a4; k.a5 = c.a5;
     k.gw = (c.flags & CRB_CSPACE) ? ctx->rp.D : 7;
     k.inv_eta = 1.0f / c.eta;
+    k.inv_eta_bound = 1.0f / c.eta_bound;
     k.inv_2dt = 1.0f / (2.0f * c.dt);
     k.inv_12dt = (float)(1.0 / (12.0 * c.dt));
     k.inv_12dt2 = (float)(1.0 / (12.0 * (double)c.dt * c.dt));
@@ -1085,6 +1091,11 @@ crb_status ready(crb_ctx *ctx, bool need_world) {
     if (need_world && !ctx->params_ok) return fail(ctx, CRB_E_NOT_READY, "cost params not set");
     return CRB_OK;
 }
+
+// The solver / evaluation kernels come in two builds of the world screen (crb_device.cuh "tensor-
+// core pre-screen"): with it when some environment holds >= CRB_MMA_MIN_K enabled cuboids, else
+// the FFMA-only build (its smaller register footprint is faster on small worlds).
+bool use_world_mma(const crb_ctx *ctx) { return CRB_WORLD_MMA && ctx->kmax_enabled >= CRB_MMA_MIN_K; }
 
 template <typename Kern>
 crb_status launch(crb_ctx *ctx, Kern k, int grid, size_t smem, cudaStream_t st, const KParams &kp, const char *nm) {
@@ -1388,7 +1399,12 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
                 o[4 * i2 + 2] = (float)R[2][i2];
                 o[4 * i2 + 3] = (float)(-(R[0][i2] * b.pos[0] + R[1][i2] * b.pos[1] + R[2][i2] * b.pos[2]));
             }
-            o[12] = 0.5f * b.dims[0]; o[13] = 0.5f * b.dims[1]; o[14] = 0.5f * b.dims[2]; o[15] = 0.f;
+            o[12] = 0.5f * b.dims[0]; o[13] = 0.5f * b.dims[1]; o[14] = 0.5f * b.dims[2];
+            // rounding slack factor of the tensor-core pre-screen (crb_device.cuh split_h2): the
+            // hi/lo fp16 product is within ~5e-6 (1 + |w|)(1 + |B|) m of the fp32 one; 4x margin.
+            // Offsets beyond the fp16 range get NaN: every sphere is then sent to the exact test.
+            const double om = std::max({1.0, std::fabs((double)o[3]), std::fabs((double)o[7]), std::fabs((double)o[11])});
+            o[15] = om < 3e4 ? (float)(2e-5 * (1.0 + om)) : std::numeric_limits<float>::quiet_NaN();
             ++k;
         }
         count[e] = k;
@@ -1457,8 +1473,12 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
     kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs; kp.dt_arr = dt;
     const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
-    if (mode == MODE_TO) return launch(ctx, eval_to_kernel, B, bytes, (cudaStream_t)stream, kp, "eval_to_kernel");
-    return launch(ctx, eval_ik_kernel, (B + NC - 1) / NC, bytes, (cudaStream_t)stream, kp, "eval_ik_kernel");
+    const bool wm = use_world_mma(ctx);
+    if (mode == MODE_TO)
+        return launch(ctx, wm ? eval_to_kernel<true> : eval_to_kernel<false>, B, bytes, (cudaStream_t)stream, kp,
+                      "eval_to_kernel");
+    return launch(ctx, wm ? eval_ik_kernel<true> : eval_ik_kernel<false>, (B + NC - 1) / NC, bytes,
+                  (cudaStream_t)stream, kp, "eval_ik_kernel");
 }
 
 crb_status crb_lbfgs_solve(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H, const float *seeds,
@@ -1505,8 +1525,12 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     kp.seed_best_cost = sbc; kp.seed_best_traj = sbt;
     const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids + solver)");
-    if (mode == MODE_TO) st = launch(ctx, solve_to_kernel, P * S, bytes, stream_, kp, "solve_to_kernel");
-    else st = launch(ctx, solve_ik_kernel, P * ((S + NC - 1) / NC), bytes, stream_, kp, "solve_ik_kernel");
+    const bool wm = use_world_mma(ctx);
+    if (mode == MODE_TO)
+        st = launch(ctx, wm ? solve_to_kernel<true> : solve_to_kernel<false>, P * S, bytes, stream_, kp, "solve_to_kernel");
+    else
+        st = launch(ctx, wm ? solve_ik_kernel<true> : solve_ik_kernel<false>, P * ((S + NC - 1) / NC), bytes, stream_,
+                    kp, "solve_ik_kernel");
     if (st != CRB_OK) return st;
     if (P > 0 && (best_traj || best_cost || best_key)) {
         select_kernel<<<P, 128, 0, stream_>>>(P, S, N, sbc, sbt, (long long)sp->global_seed_base, best_traj,
@@ -1560,7 +1584,9 @@ crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, i
     if (smem_bytes) *smem_bytes = (int)bytes;
     if (bytes > SMEM_MAX) { if (ctas_per_sm) *ctas_per_sm = 0; return CRB_OK; }
     int n = 0;
-    const void *fn = mode == MODE_TO ? (const void *)solve_to_kernel : (const void *)solve_ik_kernel;
+    const bool wm = use_world_mma(ctx);
+    const void *fn = mode == MODE_TO ? (wm ? (const void *)solve_to_kernel<true> : (const void *)solve_to_kernel<false>)
+                                     : (wm ? (const void *)solve_ik_kernel<true> : (const void *)solve_ik_kernel<false>);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     st = cuda_check(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, NT, bytes), "occupancy");
     if (ctas_per_sm) *ctas_per_sm = n;
@@ -1747,3 +1773,16 @@ crb_status crb_particle_normals(uint32_t key0, uint32_t key1, int n_var, int n_p
 }
 
 }  // extern "C"
+
+#if CRB_STATS
+// world-screen work counters (tools/world_stats.py only; not part of the product ABI)
+extern "C" int crb_debug_stats(unsigned long long *out, int reset) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out, ::g_crb_stats, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(::g_crb_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

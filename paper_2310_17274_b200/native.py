@@ -15,7 +15,8 @@ import numpy as np
 from . import inputs
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcurobo_b200.so")
+# CRB_LIB: an alternative build of the same library (tools/world_stats.py); default the in-tree one
+LIB_PATH = os.environ.get("CRB_LIB") or os.path.join(HERE, "libcurobo_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "

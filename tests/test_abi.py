@@ -48,7 +48,14 @@ def test_sass_is_sm100a(lib_path):
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True).stdout
     assert "UBLKCP" in sass            # TMA bulk copy of the robot / cuboid tables
-    assert "HMMA" not in sass          # no legacy tensor-core path (the path is not a contraction)
+    # the cuboid pre-screen's [rows x 4] x [4 x 8] products run on the tensor cores (HMMA.16816) in
+    # the large-world build (template argument true) only; the FFMA build has no HMMA
+    funcs = re.split(r"\n\s+Function : ", sass)
+    for kern in ("solve_to_kernel", "solve_ik_kernel", "eval_to_kernel", "eval_ik_kernel"):
+        body = {("ILb1E" in f.split("\n", 1)[0]): f for f in funcs if kern in f.split("\n", 1)[0]}
+        assert set(body) == {False, True}, kern
+        assert "HMMA.16816.F32" in body[True], kern
+        assert "HMMA" not in body[False], kern
 
 
 def test_create_fails_loudly_without_gpu(lib_path):

@@ -1,0 +1,139 @@
+"""GPU: the tensor-core cuboid pre-screen (crb_device.cuh "tensor-core pre-screen", DESIGN.md
+"World screen").
+
+The library builds its solver / evaluation kernels twice: with the HMMA pre-screen when some
+environment holds >= CRB_MMA_MIN_K (32) enabled cuboids, else FFMA only.  The pre-screen only
+chooses which cuboids go through the exact fp32 test, so on the SAME environments both builds must
+return bitwise the same costs, gradients and solves; a context whose world list includes one large
+environment runs the HMMA build for all of them.  Parity against the fp64 oracle at K in the HMMA
+range (ragged K, far and huge cuboids) uses the tolerances of test_gpu_parity.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2310_17274_b200 import inputs, robots
+
+from test_gpu_parity import MARGIN, Stats, T, f32, franka_trajs, make  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+MMA_MIN_K = 32
+
+
+@pytest.fixture(scope="module")
+def native():
+    from paper_2310_17274_b200 import native as N
+    return N
+
+
+def _pair(native, rb, small, cp, big_k=64):
+    """(FFMA context over `small`, HMMA context over `small` + one big environment)."""
+    big = inputs.random_world(9, 0, big_k, lo=-0.9, hi=0.9, disabled_frac=0.0)
+    return make(native, rb, small, cp), make(native, rb, list(small) + [big], cp)
+
+
+@pytest.mark.parametrize("flags", [inputs.SWEEP | inputs.SPEED, inputs.SPEED | inputs.JERK, 0])
+def test_mma_and_ffma_builds_bitwise_equal_eval_to(native, O, flags):
+    B, H = 48, 32
+    rb, starts, goals_cfg, trajs = franka_trajs(70 + flags, B, H, noise=0.4)
+    small = [inputs.tabletop_scene(1, e, 20) for e in range(2)] + [inputs.random_world(3, 0, 30, lo=-0.8, hi=0.8)]
+    cp = inputs.CostParams(flags=flags, dt=0.25)
+    ffma, mma = _pair(native, rb, small, cp)
+    R = O.Robot(rb)
+    goals = np.array([O.fk(R, q)[2] for q in goals_cfg])
+    env = T((np.arange(B) % 3).astype(np.int32), torch.int32)
+    a = ffma.evaluate(T(f32(trajs)), T(f32(goals)), start=T(f32(starts)), env=env)
+    b = mma.evaluate(T(f32(trajs)), T(f32(goals)), start=T(f32(starts)), env=env)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    assert (a[2][:, 4] > 0).sum() >= B // 4          # the world term is active on many trajectories
+    ffma.close(); mma.close()
+
+
+def test_mma_and_ffma_builds_bitwise_equal_ik_and_solves(native, O):
+    from paper_2310_17274_b200 import workload
+    wl = workload.franka_to(0, list(range(4)), S=8, H=32, iters=15)
+    ffma, mma = _pair(native, wl.robot, wl.worlds, wl.cost)
+    outs = []
+    for ctx in (ffma, mma):
+        outs.append(ctx.solve(wl.solver, T(wl.seeds), T(wl.goal), start=T(wl.start), env=T(wl.env, torch.int32),
+                              seed_outputs=True))
+    for k in ("best_cost", "best_traj", "best_key", "seed_best_cost"):
+        assert torch.equal(outs[0][k], outs[1][k]), k
+    ik = workload.franka_ik(0, list(range(40)), S=30, iters=20)
+    outs = []
+    for ctx in (ffma, mma):
+        ctx.set_cost_params(ik.cost)
+        ctx.set_world(ik.worlds if ctx is ffma else list(ik.worlds) + [inputs.random_world(9, 0, 64)])
+        outs.append(ctx.solve(ik.solver, T(ik.seeds), T(ik.goal), env=T(ik.env, torch.int32), seed_outputs=True))
+    for k in ("best_cost", "best_traj", "seed_best_cost"):
+        assert torch.equal(outs[0][k], outs[1][k]), k
+    ffma.close(); mma.close()
+
+
+@pytest.mark.parametrize("K,lo,hi,dmax", [(48, -0.8, 0.8, 0.4), (61, -0.7, 0.7, 0.3), (203, -0.9, 0.9, 0.15)])
+def test_eval_to_parity_mma_range(native, O, K, lo, hi, dmax):
+    """Oracle parity with the HMMA build: K = 48, 61 (ragged last 8-cuboid tile),
+    203; rotated cuboids, some disabled."""
+    B, H = 16, 32
+    rb, starts, goals_cfg, trajs = franka_trajs(300 + K, B, H, noise=0.4)
+    worlds = [inputs.random_world(11, e, K, lo=lo, hi=hi, dmax=dmax) for e in range(2)]
+    cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED, dt=0.25)
+    ctx = make(native, rb, worlds, cp)
+    R = O.Robot(rb)
+    Ws = [O.World(w) for w in worlds]
+    env = (np.arange(B) % 2).astype(np.int32)
+    goals = np.array([O.fk(R, q)[2] for q in goals_cfg])
+    V, st, gl = f32(trajs), f32(starts), f32(goals)
+    cost, grad, terms = ctx.evaluate(T(V), T(gl), start=T(st), env=T(env, torch.int32))
+    cost, grad = cost.cpu().numpy(), grad.cpu().numpy()
+    stats = Stats()
+    active = 0
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"K={K} traj {b}")
+        active += t_ref[4] > 0
+    stats.done(0.34)
+    assert active >= B // 4
+    ctx.close()
+
+
+def test_mma_far_and_huge_cuboids(native, O):
+    """Cuboids far outside the workspace (large offsets, still inside the fp16 range) and one
+    beyond it (|offset| > 3e4 m: the pre-screen flags it and the exact test decides) next to a
+    cuboid the arm penetrates: costs equal the FFMA build and the oracle."""
+    B, H = 8, 32
+    rb, starts, goals_cfg, trajs = franka_trajs(808, B, H, noise=0.3)
+    base = inputs.random_world(12, 0, 56, lo=-0.8, hi=0.8, disabled_frac=0.0)
+    pos = base.pos.copy(); dims = base.dims.copy()
+    pos[3] = [2.0e3, -1.0e3, 5.0]                    # far, inside fp16 range
+    pos[7] = [5.0e4, 0.0, 0.0]; dims[7] = [1.0, 1.0, 1.0]   # beyond the fp16 range
+    pos[9] = [9.0e4, 0.0, 0.0]; dims[9] = [1.9e5, 2.0, 2.0]  # huge: contains the base of the arm
+    pos[11] = [0.3, 0.0, 0.3]; dims[11] = [0.2, 0.2, 0.2]    # in the arm's way
+    quat = base.quat.copy()
+    quat[[7, 9]] = [1.0, 0.0, 0.0, 0.0]              # axis-aligned: the active faces stay exact in fp32
+    w = inputs.World(pos, quat, dims, base.enabled)
+    small = inputs.World(pos[:20].copy(), quat[:20].copy(), dims[:20].copy(), base.enabled[:20].copy())
+    cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED, dt=0.25)
+    R = O.Robot(rb)
+    goals = np.array([O.fk(R, q)[2] for q in goals_cfg])
+    V, st, gl = f32(trajs), f32(starts), f32(goals)
+    ctx = make(native, rb, [w], cp)
+    cost, grad, _ = ctx.evaluate(T(V), T(gl), start=T(st), env=T(np.zeros(B, np.int32), torch.int32))
+    cost, grad = cost.cpu().numpy(), grad.cpu().numpy()
+    Wo = O.World(w)
+    stats = Stats()
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Wo, cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"far {b}")
+        assert t_ref[4] > 0                          # the huge cuboid contains the base spheres
+    stats.done(0.34)
+    # the 20-cuboid prefix through both builds: bitwise equal
+    ffma, mma = _pair(native, rb, [small], cp)
+    env = T(np.zeros(B, np.int32), torch.int32)
+    a = ffma.evaluate(T(V), T(gl), start=T(st), env=env)
+    b2 = mma.evaluate(T(V), T(gl), start=T(st), env=env)
+    for x, y in zip(a, b2):
+        assert torch.equal(x, y)
+    ctx.close(); ffma.close(); mma.close()

@@ -1,0 +1,64 @@
+"""World-screen work counters (analysis tool, not the product path).
+
+Builds a CRB_STATS=1 variant of the library next to this file (tools/libcurobo_stats.so, optionally
+with -DCRB_WORLD_MMA=0) and runs the bench workloads through it:
+  [0] (group, cuboid) pairs examined, [1] pairs flagged by the tensor-core pre-screen,
+  [2] pairs with an exact flag (some entry needs the slow path), [3] flagged entries (slow calls).
+usage: python tools/world_stats.py [--mma 0|1]
+"""
+import argparse
+import ctypes as C
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--mma", type=int, default=1)
+ap.add_argument("--problems", type=int, default=16)
+args = ap.parse_args()
+
+from paper_2310_17274_b200 import build as B  # noqa: E402
+
+lib = os.path.join(ROOT, "tools", f"libcurobo_stats{args.mma}.so")
+cmd = [B.NVCC, *B.FLAGS, "-DCRB_STATS=1", f"-DCRB_WORLD_MMA={args.mma}", "-o", lib, B.SRC]
+i = cmd.index("-v")
+del cmd[i - 1:i + 1]   # drop "-Xptxas -v"
+if not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(d) for d in B.DEPS):
+    subprocess.run(cmd, check=True)
+os.environ["CRB_LIB"] = lib
+
+import torch  # noqa: E402
+from paper_2310_17274_b200 import native, workload  # noqa: E402
+
+so = C.CDLL(lib)
+so.crb_debug_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+
+
+def stats(reset=True):
+    a = (C.c_ulonglong * 8)()
+    so.crb_debug_stats(a, int(reset))
+    return list(a)
+
+
+def run(name, wl):
+    ctx = native.Context(0)
+    ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
+    stats()
+    kw = {"env": torch.tensor(wl.env, device="cuda")}
+    if wl.start is not None:
+        kw["start"] = torch.tensor(wl.start, device="cuda")
+    ctx.solve(wl.solver, torch.tensor(wl.seeds, device="cuda"), torch.tensor(wl.goal, device="cuda"), **kw)
+    s = stats()
+    ctx.close()
+    ex = max(s[0], 1)
+    print(f"{name}: pairs {s[0]}  mma-flagged {s[1] / ex:.3f}  exact-flagged {s[2] / ex:.3f}  "
+          f"entries/pair {s[3] / ex:.3f}", flush=True)
+
+
+P = args.problems
+run("cfg2 K=20 TO", workload.franka_to(0, list(range(P)), S=32, H=32, iters=100))
+run("cfg3 K=20 IK", workload.franka_ik(0, list(range(300)), S=30, iters=100))
+run("cfg5 K=1000 TO", workload.franka_to(0, list(range(4)), S=32, H=32, n_boxes=1000, iters=20, dense=True))
