@@ -837,7 +837,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     {
         // self (Eq. self-collision, Alg. 9): block {ia..ia+na-1} x {jb..jb+len-1} of S, na <= 4
         // first spheres in registers, partners streamed, lane = slot.  Screen: d^2 - R^2 =
-        // -2 (w_i.w_j + r_i r_j + hb_i + hb_j), hb = -(|w|^2 - r^2)/2 per sphere (5 FMA per pair),
+        // -2 (w_i.w_j + r_i r_j + hb_i + hb_j), hb = -(|w|^2 - r^2)/2 per sphere (4 FMA per pair
+        // against a per-first-sphere threshold),
         // conservative (slack 1e-5 m^2 >> fp32 rounding); flagged pairs are re-tested exactly.  Ties
         // go to the lowest rank in S (first maximal pair, A28).
         float best = 0.f;
@@ -1044,30 +1045,32 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff,
                           len = (B.x >> 20) & 0x1ff;
                 float4 wi[4];
-                float ri[4], ha[4];
+                float ri[4], thr[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int i = u < na ? ia + u : ia;
                     wi[u] = s.sw[i * NC + lane];
                     ri[u] = rself[i];
-                    ha[u] = u < na ? wi[u].w : -1e30f;
+                    // flag iff w_i.w_j + r_i r_j + hb_j > -slack - hb_i  (u >= na never flags)
+                    thr[u] = u < na ? -1e-5f - wi[u].w : 1e30f;
                 }
                 const float4 *wjp = s.sw + jb * NC + lane;
-#pragma unroll 2
-                for (int v = 0; v < len; ++v) {
-                    const float4 wj = wjp[v * NC];
-                    const float rj = rself[jb + v];
+                const float *rjp = rself + jb;
+#pragma unroll 4
+                for (int v = 0; v < len; ++v, wjp += NC, ++rjp) {
+                    const float4 wj = *wjp;
+                    const float rj = *rjp;
                     float g[4];
                     bool any = false;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {     // common path: the screen only
-                        g[u] = fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, ha[u] + wj.w))));
-                        any |= g[u] > -1e-5f;
+                    for (int u = 0; u < 4; ++u) {     // common path: the screen only (4 FFMA + 1 compare)
+                        g[u] = fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, wj.w))));
+                        any |= g[u] > thr[u];
                     }
                     if (any) {                        // rare path: exact test of the flagged pairs
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            if (!(g[u] > -1e-5f)) continue;
+                            if (!(g[u] > thr[u])) continue;
                             const float R = ri[u] + rj;
                             const float dx = wi[u].x - wj.x, dy = wi[u].y - wj.y, dz = wi[u].z - wj.z;
                             const float d2 = dx * dx + dy * dy + dz * dz;
