@@ -27,6 +27,12 @@ __device__ unsigned long long g_crb_stats[8];
 #define CRB_STAT(i, v) do { } while (0)
 #endif
 
+// Small-world pre-screen in packed fp16 (HFMA2, two cuboids per instruction) ahead of the exact
+// fp32 test; 0 = the fp32 screen of every (sphere, cuboid).
+#ifndef CRB_WORLD_H2
+#define CRB_WORLD_H2 1
+#endif
+
 // World pre-screen on the tensor cores: 1 = the affine cuboid-frame
 // transform of a world group runs as HMMA.16816 on an fp16 hi/lo split, 0 = the FFMA screen only.
 #ifndef CRB_WORLD_MMA
@@ -100,7 +106,9 @@ struct KParams {
     Layout lay;
     CostP cp;
     const float4 *robot;     // packed robot blob (global)
-    const float4 *boxes;     // [n_env][kmax][4] float4: (R col i, -col_i . t) x3, (h, 0)
+    const float4 *boxes;     // [n_env][kmax][4] float4: (R col i, -col_i . t) x3, (h, M)
+    const uint4 *boxes_h2;   // [n_env][kpairs][4] uint4: fp16x2 cuboid pairs (set_world)
+    int kpairs;
     const int *box_count;    // [n_env] enabled (compacted) boxes
     int kmax, n_env;
     // solver parameters (Alg. 6, Alg. 1)
@@ -194,6 +202,7 @@ __device__ __forceinline__ int stage_tables(const KParams &kp, float *smem, int 
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + kp.lay.mbar);
     const int K = (env >= 0 && env < kp.n_env) ? kp.box_count[env] : 0;
     if (threadIdx.x == 0) {
+        reinterpret_cast<int *>(smem + kp.lay.mbar)[2] = env;   // for the fp16x2 cuboid table
         mbar_init(bar, 1);
         const uint32_t rbytes = (uint32_t)kp.rp.words * 4u;
         const uint32_t bbytes = (uint32_t)K * 64u;
@@ -588,8 +597,9 @@ __device__ __forceinline__ float box_screen(float cx, float cy, float cz, const 
 // an fp16 hi/lo split of both operands:
 //   A row = (wh, 1 | wh, 1 | wl, 0 | 0),  B col = (Bh | Bl | Bh | 0)  =>  A.B = wh.(Bh + Bl) + wl.Bh,
 // i.e. (wh + wl).(Bh + Bl) without the wl.Bl term: |error| <= ~5e-6 (1 + |w|)(1 + |B|) m, covered
-// by the per-cuboid slack in h.w (set_world).  The result only decides which cuboids go through
-// the exact fp32 test below, so the world term is bitwise the FFMA path's.
+// by the slack 2e-5 (2 + M)(1 + max|w|), M = max(|off|, h) in h.w (set_world).  The result only
+// decides which cuboids go through the exact fp32 test below, so the world term is bitwise the
+// FFMA path's.
 __device__ __forceinline__ void split_h2(float x, float y, unsigned &hi, unsigned &lo) {
     const __half2 h = __floats2half2_rn(x, y);
     const float2 f = __half22float2(h);
@@ -992,7 +1002,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         for (int j = 0; j < 2; ++j) {
                             const int kk = kb + 2 * t4 + j;
                             const float4 h = bx4[4 * min(kk, K - 1) + 3];
-                            const float e = fmaf(h.w, wfac, thg);
+                            const float e = fmaf(2e-5f * (2.f + h.w), wfac, thg);   // NaN h.w: always flagged
                             const bool ok = kk < K;
                             ex[j] = ok ? h.x + e : -1.f; ey[j] = ok ? h.y + e : -1.f; ez[j] = ok ? h.z + e : -1.f;
                         }
@@ -1028,7 +1038,66 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     }
                     } else
 #endif
+#if CRB_WORLD_H2
+                    {
+                    // fp16x2 pre-screen, cuboids k, k+1 in the two halves, each thread's 4 spheres
+                    // broadcast.  Chebyshev test max_i(|l_i| - (h_i + delta)) < th per sphere, with
+                    // l = R^T (w - t) in fp16: |error| <= 2^-11 (5 S + 4 |off| + 3 h + th), S the
+                    // group's largest |w|_1 (HFMA2 rounds each partial sum; 1.5x margin in delta).
+                    // Only the cuboids a lane flags go through the exact fp32 test, in increasing k:
+                    // the world term is bitwise the all-fp32 screen's.
+                    unsigned sb = 0u, tb = 0u;
+                    __half2 hx[4], hy[4], hz[4], hth[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        sb = max(sb, __float_as_uint(fabsf(cx[u]) + fabsf(cy[u]) + fabsf(cz[u])));
+                        const float th = th2[u] > 0.f ? sqrtf(th2[u]) : -6e4f;   // disabled: never flags
+                        tb = max(tb, th > 0.f ? __float_as_uint(th) : 0u);
+                        hx[u] = __float2half2_rn(cx[u]); hy[u] = __float2half2_rn(cy[u]);
+                        hz[u] = __float2half2_rn(cz[u]); hth[u] = __float2half2_rn(th);
+                    }
+                    // delta_k = U (5 S + th_max + 7 M_k), U = 1.5 * 2^-11
+                    const float U = 1.5f * 4.8828125e-4f;
+                    const float d0r = U * fmaf(5.f, __uint_as_float(__reduce_max_sync(FULL, sb)),
+                                               __uint_as_float(__reduce_max_sync(FULL, tb)));
+                    const float d0 = d0r < 6e4f ? d0r : 6e4f;   // NaN / huge |w|: every cuboid flagged
+                    const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
+                    const uint4 *bh = kp.boxes_h2 + (size_t)envc * kp.kpairs * 4;
+                    const __half2 u7 = __float2half2_rn(7.f * U), dd = __float2half2_rn(d0);
+                    for (int kb = 0; kb < K; kb += 2) {
+                        const uint4 w0 = __ldg(bh), w1 = __ldg(bh + 1), w2 = __ldg(bh + 2), w3 = __ldg(bh + 3);
+                        bh += 4;
+                        const __half2 *W0 = reinterpret_cast<const __half2 *>(&w0), *W1 = reinterpret_cast<const __half2 *>(&w1),
+                                      *W2 = reinterpret_cast<const __half2 *>(&w2), *W3 = reinterpret_cast<const __half2 *>(&w3);
+                        const __half2 r00 = W0[0], r01 = W0[1], r02 = W0[2], o0 = W0[3];
+                        const __half2 r10 = W1[0], r11 = W1[1], r12 = W1[2], o1 = W1[3];
+                        const __half2 r20 = W2[0], r21 = W2[1], r22 = W2[2], o2 = W2[3];
+                        const __half2 e = __hfma2(u7, W3[3], dd);   // delta of each cuboid
+                        const __half2 ex = __hadd2(W3[0], e), ey = __hadd2(W3[1], e), ez = __hadd2(W3[2], e);
+                        __half2 mn = __float2half2_rn(1.f);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const __half2 lx = __hfma2(r00, hx[u], __hfma2(r01, hy[u], __hfma2(r02, hz[u], o0)));
+                            const __half2 ly = __hfma2(r10, hx[u], __hfma2(r11, hy[u], __hfma2(r12, hz[u], o1)));
+                            const __half2 lz = __hfma2(r20, hx[u], __hfma2(r21, hy[u], __hfma2(r22, hz[u], o2)));
+                            const __half2 q = __hmax2(__hsub2(__habs2(lx), ex),
+                                                      __hmax2(__hsub2(__habs2(ly), ey), __hsub2(__habs2(lz), ez)));
+                            mn = __hmin2(mn, __hsub2(q, hth[u]));
+                        }
+                        // sign bit of a half: that cuboid is within reach of some sphere of this lane
+                        const unsigned fl = *reinterpret_cast<const unsigned *>(&mn) & 0x80008000u;
+                        const unsigned f = __reduce_or_sync(FULL, fl);
+                        if (f) {
+                            CRB_STAT(1, ((f & 0x8000u) ? 1 : 0) + ((f & 0x80000000u) ? 1 : 0));
+#pragma unroll 1   // one copy of the exact path (instruction cache)
+                            for (int j = 0; j < 2; ++j)
+                                if (f & (0x8000u << (16 * j))) exact_box(kb + j, true);
+                        }
+                    }
+                    }
+#else
                     for (int k = 0; k < K; ++k) exact_box(k, false);
+#endif
                 }
                 // the group's cost goes to the .w of its first sphere (unused by the backward):
                 // the merge sums the groups in index order, whichever warp took them
@@ -1060,30 +1129,38 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 }
                 const float4 *wjp = s.sw + jb * NC + lane;
                 const float *rjp = rself + jb;
-#pragma unroll 4
-                for (int v = 0; v < len; ++v, wjp += NC, ++rjp) {
-                    const float4 wj = *wjp;
-                    const float rj = *rjp;
-                    float g[4];
+                // 4 partners per step: the screen only (4 FFMA + 1 compare per pair); a partner
+                // beyond len gets hb = -1e30 and never flags.  The rare exact test sits out of the
+                // loop body, one copy (instruction cache)
+                for (int v0 = 0; v0 < len; v0 += 4, wjp += 4 * NC, rjp += 4) {
                     bool any = false;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {     // common path: the screen only (4 FFMA + 1 compare)
-                        g[u] = fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, wj.w))));
-                        any |= g[u] > thr[u];
-                    }
-                    if (any) {                        // rare path: exact test of the flagged pairs
+                    for (int vv = 0; vv < 4; ++vv) {
+                        const float4 wj = wjp[vv * NC];
+                        const float rj = rjp[vv];
+                        const float hbj = v0 + vv < len ? wj.w : -1e30f;
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            if (!(g[u] > thr[u])) continue;
-                            const float R = ri[u] + rj;
-                            const float dx = wi[u].x - wj.x, dy = wi[u].y - wj.y, dz = wi[u].z - wj.z;
-                            const float d2 = dx * dx + dy * dy + dz * dz;
-                            if (!(d2 < R * R)) continue;
-                            const float pen = R - sqrtf(d2);
-                            if (pen >= best && pen > 0.f) {
-                                const int rank = rk[B.y + u * len + v];
-                                if (pen > best || rank < brank) {
-                                    best = pen; brank = rank; bij = (ia + u) | ((jb + v) << 9);
+                        for (int u = 0; u < 4; ++u)
+                            any |= fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, hbj)))) > thr[u];
+                    }
+                    if (any) {   // rare: exact test of these (up to) 4 x 4 pairs, Eq. self-collision
+#pragma unroll 1
+                        for (int v = v0; v < min(v0 + 4, len); ++v) {
+                            const float4 wj = s.sw[(jb + v) * NC + lane];
+                            const float rj = rself[jb + v];
+#pragma unroll 1
+                            for (int u = 0; u < na; ++u) {
+                                const float4 w = s.sw[(ia + u) * NC + lane];
+                                const float R = rself[ia + u] + rj;
+                                const float dx = w.x - wj.x, dy = w.y - wj.y, dz = w.z - wj.z;
+                                const float d2 = dx * dx + dy * dy + dz * dz;
+                                if (!(d2 < R * R)) continue;
+                                const float pen = R - sqrtf(d2);
+                                if (pen >= best && pen > 0.f) {
+                                    const int rank = rk[B.y + u * len + v];
+                                    if (pen > best || rank < brank) {
+                                        best = pen; brank = rank; bij = (ia + u) | ((jb + v) << 9);
+                                    }
                                 }
                             }
                         }

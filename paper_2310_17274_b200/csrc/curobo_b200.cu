@@ -959,6 +959,8 @@ struct crb_ctx {
     // world
     bool world_ok = false;
     float4 *d_boxes = nullptr;
+    uint4 *d_boxes_h2 = nullptr;          // fp16x2 cuboid pairs of the small-world pre-screen
+    int kpairs = 1;                       // pairs per environment in d_boxes_h2
     int *d_box_count = nullptr;
     int n_env = 0, kmax = 0, kmax_enabled = 0;
     // params
@@ -1065,6 +1067,8 @@ KParams base_params(const crb_ctx *ctx) {
     kp.rp = ctx->rp;
     kp.robot = ctx->d_robot;
     kp.boxes = ctx->d_boxes;
+    kp.boxes_h2 = ctx->d_boxes_h2;
+    kp.kpairs = ctx->kpairs;
     kp.box_count = ctx->d_box_count;
     kp.kmax = ctx->kmax;
     kp.n_env = ctx->n_env;
@@ -1128,7 +1132,7 @@ crb_status crb_create(int cuda_device, crb_ctx **out) {
 crb_status crb_destroy(crb_ctx *ctx) {
     if (!ctx) return CRB_E_ARG;
     cudaSetDevice(ctx->device);
-    cudaFree(ctx->d_robot); cudaFree(ctx->d_boxes); cudaFree(ctx->d_box_count);
+    cudaFree(ctx->d_robot); cudaFree(ctx->d_boxes); cudaFree(ctx->d_boxes_h2); cudaFree(ctx->d_box_count);
     cudaFree(ctx->ws_cost); cudaFree(ctx->ws_traj); cudaFree(ctx->ws_mask); cudaFree(ctx->ws_n);
     cudaFree(ctx->h_seeds); cudaFree(ctx->h_start); cudaFree(ctx->h_goal); cudaFree(ctx->h_best);
     cudaFree(ctx->h_bcost); cudaFree(ctx->h_env); cudaFree(ctx->h_key);
@@ -1400,21 +1404,47 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
                 o[4 * i2 + 3] = (float)(-(R[0][i2] * b.pos[0] + R[1][i2] * b.pos[1] + R[2][i2] * b.pos[2]));
             }
             o[12] = 0.5f * b.dims[0]; o[13] = 0.5f * b.dims[1]; o[14] = 0.5f * b.dims[2];
-            // rounding slack factor of the tensor-core pre-screen (crb_device.cuh split_h2): the
-            // hi/lo fp16 product is within ~5e-6 (1 + |w|)(1 + |B|) m of the fp32 one; 4x margin.
-            // Offsets beyond the fp16 range get NaN: every sphere is then sent to the exact test.
-            const double om = std::max({1.0, std::fabs((double)o[3]), std::fabs((double)o[7]), std::fabs((double)o[11])});
-            o[15] = om < 3e4 ? (float)(2e-5 * (1.0 + om)) : std::numeric_limits<float>::quiet_NaN();
+            // cuboid magnitude M = max(|off_i|, h_i) for the rounding slack of the reduced-precision
+            // pre-screens (crb_device.cuh: HMMA hi/lo split, fp16x2 screen); NaN beyond the fp16
+            // range, which makes both screens send every sphere to the exact fp32 test
+            const double om = std::max({std::fabs((double)o[3]), std::fabs((double)o[7]), std::fabs((double)o[11]),
+                                        (double)o[12], (double)o[13], (double)o[14]});
+            o[15] = om < 3e4 ? (float)om : std::numeric_limits<float>::quiet_NaN();
             ++k;
         }
         count[e] = k;
         kmax_en = std::max(kmax_en, k);
     }
-    cudaFree(ctx->d_boxes); cudaFree(ctx->d_box_count);
-    ctx->d_boxes = nullptr; ctx->d_box_count = nullptr;
+    // fp16x2 pairs (2p, 2p+1) of each environment's enabled cuboids for the small-world pre-screen
+    // (crb_device.cuh "fp16x2 pre-screen"): words 0-11 = rows of R^T with -col . t as (k0, k1)
+    // half pairs, 12-14 = half extents, 15 = magnitude M.  A cuboid beyond the fp16 range gets zero
+    // rows and h = +6e4 (always flagged), a missing second cuboid h = -6e4 (never flagged).
+    const int kpairs = std::max(1, (kmax_en + 1) / 2);
+    std::vector<__half2> ph((size_t)n_env * kpairs * 16, __floats2half2_rn(0.f, 0.f));
+    for (int e = 0; e < n_env; ++e)
+        for (int p2 = 0; p2 < kpairs; ++p2) {
+            float v[2][16];
+            for (int j = 0; j < 2; ++j) {
+                const int k = 2 * p2 + j;
+                const float *o = &packed[((size_t)e * k_max + std::min(k, std::max(k_max - 1, 0))) * 16];
+                const bool have = k < count[e], ok = have && o[15] < 3e4f;
+                for (int i = 0; i < 12; ++i) v[j][i] = ok ? o[i] : 0.f;
+                for (int i = 12; i < 15; ++i) v[j][i] = ok ? o[i] : (have ? 6e4f : -6e4f);
+                v[j][15] = ok ? o[15] : 0.f;
+            }
+            for (int i = 0; i < 16; ++i) ph[((size_t)e * kpairs + p2) * 16 + i] = __floats2half2_rn(v[0][i], v[1][i]);
+        }
+    cudaFree(ctx->d_boxes); cudaFree(ctx->d_boxes_h2); cudaFree(ctx->d_box_count);
+    ctx->d_boxes = nullptr; ctx->d_boxes_h2 = nullptr; ctx->d_box_count = nullptr;
     ctx->world_ok = false;
     st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes, packed.size() * 4), "cudaMalloc boxes");
     if (st != CRB_OK) return st;
+    st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes_h2, ph.size() * sizeof(__half2)), "cudaMalloc boxes h2");
+    if (st != CRB_OK) return st;
+    st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes_h2, ph.data(), ph.size() * sizeof(__half2), cudaMemcpyHostToDevice),
+                    "upload boxes h2");
+    if (st != CRB_OK) return st;
+    ctx->kpairs = kpairs;
     st = cuda_check(ctx, cudaMalloc(&ctx->d_box_count, n_env * sizeof(int)), "cudaMalloc box count");
     if (st != CRB_OK) return st;
     st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "upload boxes");

@@ -23,7 +23,7 @@ args = ap.parse_args()
 from paper_2310_17274_b200 import build as B  # noqa: E402
 
 lib = os.path.join(ROOT, "tools", f"libcurobo_stats{args.mma}.so")
-cmd = [B.NVCC, *B.FLAGS, "-DCRB_STATS=1", f"-DCRB_WORLD_MMA={args.mma}", "-o", lib, B.SRC]
+cmd = [B.NVCC, *B.FLAGS, "-DCRB_STATS=1", f"-DCRB_WORLD_MMA={args.mma}", "-DCRB_MMA_MIN_K=0" if args.mma else "-DCRB_MMA_MIN_K=100000", "-o", lib, B.SRC]
 i = cmd.index("-v")
 del cmd[i - 1:i + 1]   # drop "-Xptxas -v"
 if not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(d) for d in B.DEPS):
