@@ -41,7 +41,7 @@ __device__ unsigned long long g_crb_stats[8];
 // ... used when the environment has at least this many cuboids (below it the FFMA screen is as
 // fast and its smaller code keeps the instruction cache warm: DESIGN.md "World screen")
 #ifndef CRB_MMA_MIN_K
-#define CRB_MMA_MIN_K 32
+#define CRB_MMA_MIN_K 64
 #endif
 
 namespace crb {

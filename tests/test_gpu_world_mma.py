@@ -2,7 +2,7 @@
 "World screen").
 
 The library builds its solver / evaluation kernels twice: with the HMMA pre-screen when some
-environment holds >= CRB_MMA_MIN_K (32) enabled cuboids, else FFMA only.  The pre-screen only
+environment holds >= CRB_MMA_MIN_K (64) enabled cuboids, else FFMA only.  The pre-screen only
 chooses which cuboids go through the exact fp32 test, so on the SAME environments both builds must
 return bitwise the same costs, gradients and solves; a context whose world list includes one large
 environment runs the HMMA build for all of them.  Parity against the fp64 oracle at K in the HMMA
@@ -18,7 +18,7 @@ from test_gpu_parity import MARGIN, Stats, T, f32, franka_trajs, make  # noqa: F
 
 pytestmark = pytest.mark.gpu
 
-MMA_MIN_K = 32
+MMA_MIN_K = 64
 
 
 @pytest.fixture(scope="module")
@@ -27,7 +27,7 @@ def native():
     return N
 
 
-def _pair(native, rb, small, cp, big_k=64):
+def _pair(native, rb, small, cp, big_k=80):
     """(FFMA context over `small`, HMMA context over `small` + one big environment)."""
     big = inputs.random_world(9, 0, big_k, lo=-0.9, hi=0.9, disabled_frac=0.0)
     return make(native, rb, small, cp), make(native, rb, list(small) + [big], cp)
@@ -65,20 +65,21 @@ def test_mma_and_ffma_builds_bitwise_equal_ik_and_solves(native, O):
     outs = []
     for ctx in (ffma, mma):
         ctx.set_cost_params(ik.cost)
-        ctx.set_world(ik.worlds if ctx is ffma else list(ik.worlds) + [inputs.random_world(9, 0, 64)])
+        ctx.set_world(ik.worlds if ctx is ffma else list(ik.worlds) + [inputs.random_world(9, 0, 80, disabled_frac=0.0)])
         outs.append(ctx.solve(ik.solver, T(ik.seeds), T(ik.goal), env=T(ik.env, torch.int32), seed_outputs=True))
     for k in ("best_cost", "best_traj", "seed_best_cost"):
         assert torch.equal(outs[0][k], outs[1][k]), k
     ffma.close(); mma.close()
 
 
-@pytest.mark.parametrize("K,lo,hi,dmax", [(48, -0.8, 0.8, 0.4), (61, -0.7, 0.7, 0.3), (203, -0.9, 0.9, 0.15)])
+@pytest.mark.parametrize("K,lo,hi,dmax", [(72, -0.8, 0.8, 0.4), (77, -0.7, 0.7, 0.3), (203, -0.9, 0.9, 0.15)])
 def test_eval_to_parity_mma_range(native, O, K, lo, hi, dmax):
-    """Oracle parity with the HMMA build: K = 48, 61 (ragged last 8-cuboid tile),
-    203; rotated cuboids, some disabled."""
+    """Oracle parity with the HMMA build: K = 72, 77 (ragged last 8-cuboid tile), 203 (~10 %
+    disabled, so the enabled counts stay >= 64); rotated cuboids."""
     B, H = 16, 32
     rb, starts, goals_cfg, trajs = franka_trajs(300 + K, B, H, noise=0.4)
     worlds = [inputs.random_world(11, e, K, lo=lo, hi=hi, dmax=dmax) for e in range(2)]
+    assert max(int(w.enabled.sum()) for w in worlds) >= MMA_MIN_K     # the HMMA build runs
     cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED, dt=0.25)
     ctx = make(native, rb, worlds, cp)
     R = O.Robot(rb)
@@ -105,7 +106,7 @@ def test_mma_far_and_huge_cuboids(native, O):
     cuboid the arm penetrates: costs equal the FFMA build and the oracle."""
     B, H = 8, 32
     rb, starts, goals_cfg, trajs = franka_trajs(808, B, H, noise=0.3)
-    base = inputs.random_world(12, 0, 56, lo=-0.8, hi=0.8, disabled_frac=0.0)
+    base = inputs.random_world(12, 0, 70, lo=-0.8, hi=0.8, disabled_frac=0.0)
     pos = base.pos.copy(); dims = base.dims.copy()
     pos[3] = [2.0e3, -1.0e3, 5.0]                    # far, inside fp16 range
     pos[7] = [5.0e4, 0.0, 0.0]; dims[7] = [1.0, 1.0, 1.0]   # beyond the fp16 range

@@ -22,3 +22,13 @@ for K in [int(k) for k in (sys.argv[1] if len(sys.argv) > 1 else "20,32,48,64,96
     out[K] = round(wl.evals_per_solve() / (ms * 1e-3) / 1e6, 1)
     ctx.close()
 print(os.environ.get("CRB_LIB", "default"), json.dumps(out))
+if len(sys.argv) > 2 and sys.argv[2] == "dense":
+    wl = workload.franka_to(0, list(range(16)), S=32, H=32, n_boxes=1000, iters=30, dense=True)
+    ctx = native.Context(0)
+    ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
+    args = (wl.solver, torch.tensor(wl.seeds, device="cuda"), torch.tensor(wl.goal, device="cuda"))
+    kw = dict(start=torch.tensor(wl.start, device="cuda"), env=torch.tensor(wl.env, device="cuda"))
+    ctx.solve(*args, **kw); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); ctx.solve(*args, **kw); e1.record(); torch.cuda.synchronize()
+    print("dense1000", round(wl.evals_per_solve() / (e0.elapsed_time(e1) * 1e-3) / 1e6, 2), "M evals/s")
