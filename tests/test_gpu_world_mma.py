@@ -138,3 +138,34 @@ def test_mma_far_and_huge_cuboids(native, O):
     for x, y in zip(a, b2):
         assert torch.equal(x, y)
     ctx.close(); ffma.close(); mma.close()
+
+
+def test_fp16x2_screen_far_and_huge_cuboids_against_oracle(native, O):
+    """The small-world build (fp16x2 pre-screen, K < 64) on cuboids far outside the workspace, one
+    beyond the fp16 range (forced to the exact test), one huge cuboid containing the arm's base,
+    and one in the arm's way: oracle parity."""
+    B, H = 16, 32
+    rb, starts, goals_cfg, trajs = franka_trajs(809, B, H, noise=0.3)
+    base = inputs.random_world(13, 0, 24, lo=-0.8, hi=0.8, disabled_frac=0.0)
+    pos = base.pos.copy(); dims = base.dims.copy(); quat = base.quat.copy()
+    pos[3] = [2.0e3, -1.0e3, 5.0]
+    pos[7] = [5.0e4, 0.0, 0.0]; dims[7] = [1.0, 1.0, 1.0]
+    pos[9] = [9.0e4, 0.0, 0.0]; dims[9] = [1.9e5, 2.0, 2.0]
+    pos[11] = [0.3, 0.0, 0.3]; dims[11] = [0.2, 0.2, 0.2]
+    quat[[7, 9]] = [1.0, 0.0, 0.0, 0.0]
+    w = inputs.World(pos, quat, dims, base.enabled)
+    cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED, dt=0.25)
+    R = O.Robot(rb)
+    goals = np.array([O.fk(R, q)[2] for q in goals_cfg])
+    V, st, gl = f32(trajs), f32(starts), f32(goals)
+    ctx = make(native, rb, [w], cp)
+    cost, grad, _ = ctx.evaluate(T(V), T(gl), start=T(st), env=T(np.zeros(B, np.int32), torch.int32))
+    cost, grad = cost.cpu().numpy(), grad.cpu().numpy()
+    Wo = O.World(w)
+    stats = Stats()
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Wo, cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"h2 far {b}")
+        assert t_ref[4] > 0
+    stats.done(0.5)        # deep inside the huge cuboid: many nearest-face ties (margin exclusions)
+    ctx.close()
