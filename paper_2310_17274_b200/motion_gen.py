@@ -50,6 +50,8 @@ class MotionGenConfig:
     w_jerk: float = 1e-4
     w_time: float = 1.0
     invalid_penalty: float = 1e6    # TO selection: an invalid seed still ranks after every valid one
+    attempts: int = 1               # plan_retry: the paper re-attempts with new linear seeds up to 3x
+                                    # before its graph planner (the planner is not built)
 
 
 class MotionGen:
@@ -61,7 +63,34 @@ class MotionGen:
         self.sp_to = inputs.SolverParams(iters=cfg.to_iters, particle_iters=cfg.particle_iters)
         self.sp_refine = inputs.SolverParams(iters=cfg.refine_iters)
 
-    def plan(self, start, goal, env, ik_seeds):
+    def plan_retry(self, start, goal, env, problems, attempts=None):
+        """plan() on the batch, then again on the problems that failed, with fresh IK seeds (the
+        Halton sequence offset by 7919 per attempt) and particle draws (rng_key = attempt), up to
+        `attempts` times in all (three attempts with linear seeds before the geometric
+        planner).  Returns plan()'s dict for the whole batch (each problem's last attempt) plus
+        `attempt` [P] int32 (1-based attempt of the returned result)."""
+        import torch
+        n = self.cfg.attempts if attempts is None else attempts
+        problems = np.asarray(list(problems))
+        S = self.cfg.ik_seeds
+        seeds = torch.tensor(self.ik_seed_batch(self.robot, problems, S), device=start.device)
+        out = self.plan(start, goal, env, seeds)
+        out["attempt"] = torch.ones(start.shape[0], dtype=torch.int32, device=start.device)
+        keys = ("traj", "variables", "dt", "final_score", "success", "pos_err", "rot_err", "max_jerk")
+        for a in range(1, n):
+            fail = torch.nonzero(~out["success"]).flatten()
+            if fail.numel() == 0:
+                break
+            fi = fail.cpu().numpy()
+            seeds = torch.tensor(self.ik_seed_batch(self.robot, problems[fi] + 7919 * a, S), device=start.device)
+            r = self.plan(start[fail].contiguous(), goal[fail].contiguous(), env[fail].contiguous(), seeds,
+                          rng_key=a)
+            for k in keys:
+                out[k][fail] = r[k].view(out[k][fail].shape)
+            out["attempt"][fail] = a + 1
+        return out
+
+    def plan(self, start, goal, env, ik_seeds, rng_key: int = 0):
         """start [P,D], goal [P,7] (device fp32), env [P] int32 (device), ik_seeds [P,S_ik,D]
         (device, e.g. inputs.ik_seeds).  Returns a dict of device tensors: traj [P,H,D] (the states
         x_1..x_H; `variables` holds the solver's V), dt [P],
@@ -73,7 +102,9 @@ class MotionGen:
         Sik, Sto = ik_seeds.shape[1], c.to_seeds
         # 1-2: collision-free IK and the S_to best solutions
         ctx.set_cost_params(self.cost_to1)
-        ik = ctx.solve(self.sp_ik, ik_seeds, goal, env=env, seed_outputs=True)
+        sp_ik = dataclasses.replace(self.sp_ik, rng_key=rng_key)
+        sp_to = dataclasses.replace(self.sp_to, rng_key=rng_key)
+        ik = ctx.solve(sp_ik, ik_seeds, goal, env=env, seed_outputs=True)
         q_ik = ik["seed_best_traj"]                                            # [P,Sik,D]
         pe, re = ctx.goal_error(q_ik, goal, B=P * Sik, goal_div=Sik)
         valid = ctx.mask_samples(q_ik.view(P * Sik, D), env=env, env_div=Sik)
@@ -82,7 +113,7 @@ class MotionGen:
         ik_idx, ik_count = N.rank_seeds(score, Sto)
         # 3-4: linear seeds and the first trajectory optimisation (dt_i, jerk off)
         seeds = N.linear_seeds(start, q_ik, H, idx=ik_idx)                   # [P,Sto,H,D]
-        to1 = ctx.solve(self.sp_to, seeds, goal, start=start, env=env, seed_outputs=True)
+        to1 = ctx.solve(sp_to, seeds, goal, start=start, env=env, seed_outputs=True)
         tr1 = to1["seed_best_traj"]                                            # [P,Sto,H,D]
         # 5: retime every seed, score it, pick the best
         _, dt1, jerk1 = ctx.retime(tr1.view(P * Sto, H, D), start)

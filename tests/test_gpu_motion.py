@@ -158,3 +158,33 @@ def test_motion_gen_pipeline_end_to_end(native, O):
         assert s == pytest.approx(1.0, rel=1e-3)
     assert np.all(out["ik_count"].cpu().numpy() > 0)
     ctx.close()
+
+
+def test_motion_gen_retries_keep_successes_and_recheck(native, O):
+    """plan_retry (up to three attempts with fresh linear seeds): first-attempt successes
+    are kept bit for bit, the success count never drops, and every success is re-checked against
+    the oracle (pose thresholds, every state valid)."""
+    from paper_2310_17274_b200 import motion_gen, workload
+    P = 8
+    wl = workload.franka_to(0, list(range(P)), S=12, H=32, iters=100)
+    ctx = native.Context(0)
+    ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
+    mg = motion_gen.MotionGen(ctx, wl.robot, wl.cost)
+    args = (T(wl.start), T(wl.goal), T(wl.env, torch.int32))
+    one = mg.plan(*args, T(mg.ik_seed_batch(wl.robot, range(P), 32)))
+    three = mg.plan_retry(*args, range(P), attempts=3)
+    s1, s3 = one["success"].cpu().numpy(), three["success"].cpu().numpy()
+    att = three["attempt"].cpu().numpy()
+    assert s3.sum() >= s1.sum()
+    assert np.all(att[s1] == 1)
+    assert torch.equal(three["traj"][torch.tensor(s1)], one["traj"][torch.tensor(s1)])
+    assert np.all((att >= 1) & (att <= 3))
+    R = O.Robot(wl.robot)
+    traj = three["traj"].cpu().numpy().astype(np.float64)
+    for p in np.nonzero(s3)[0]:
+        W = O.World(wl.worlds[wl.env[p]])
+        pe, re = O.goal_error(R, traj[p, -1], wl.goal[p])
+        assert pe < 5.5e-3 and re < 0.051
+        ok = [O.mask_sample(R, W, traj[p, h]) for h in range(32)]
+        assert sum(v for v, mg_ in ok if mg_ > 2e-5) == sum(1 for v, mg_ in ok if mg_ > 2e-5)
+    ctx.close()
