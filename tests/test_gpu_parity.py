@@ -51,12 +51,15 @@ class Stats:
         self.worst_c = 0.0
         self.worst_g = 0.0
 
-    def check(self, c_gpu, g_gpu, c_ref, g_ref, margin, label):
+    def check(self, c_gpu, g_gpu, c_ref, g_ref, margin, label, grad_slack=0.0):
+        # grad_slack (converged solutions only): the cost there is an O(n^2) residual of an fp32
+        # position, so its fp32 error is ~ |grad c| x the fp32 rounding of the kinematics (a
+        # config-space equivalent of ~1e-6 m at the end effector), not a fraction of c itself
         self.n += 1
         if margin < MARGIN:
             self.excluded += 1
             return
-        ec = abs(c_gpu - c_ref) / (abs(c_ref) * COST_RTOL + COST_ATOL)
+        ec = abs(c_gpu - c_ref) / (abs(c_ref) * COST_RTOL + COST_ATOL + grad_slack * np.linalg.norm(g_ref))
         eg = np.linalg.norm(g_gpu - g_ref) / (np.linalg.norm(g_ref) * GRAD_RTOL + GRAD_ATOL * np.sqrt(g_ref.size))
         self.worst_c = max(self.worst_c, ec)
         self.worst_g = max(self.worst_g, eg)
@@ -517,6 +520,57 @@ def test_full_size_solve_sampled_against_oracle(native, O):
         assert bc[p] == sbc[p].min()
     stats.done(0.5)
     # every seed improved on its initial cost
+    c0, _, _ = ctx.evaluate(T(wl.seeds.reshape(-1, 32, 7)), T(np.repeat(wl.goal, 32, 0)),
+                            start=T(np.repeat(wl.start, 32, 0)), env=T(np.repeat(wl.env, 32), torch.int32))
+    assert np.all(sbc.reshape(-1) <= c0.cpu().numpy() * (1 + 1e-6))
+    ctx.close()
+
+
+def test_full_size_ik_solve_sampled_against_oracle(native, O):
+    """BASELINE configs[2] at the bench size (1000 goals x 30 seeds, shared K = 20 scene, 100
+    iterations, IK mode) in the launch configuration bench.py times: for sampled goals the oracle
+    re-evaluates the returned winner (cost equals the reported best), the winner is the argmin of
+    the per-seed results, and every seed improved on its initial cost."""
+    from paper_2310_17274_b200 import workload
+    wl = workload.franka_ik(0, list(range(1000)), S=30, iters=100)
+    ctx = make(native, wl.robot, wl.worlds, wl.cost)
+    out = ctx.solve(wl.solver, T(wl.seeds), T(wl.goal), env=T(wl.env, torch.int32), seed_outputs=True)
+    bq = out["best_traj"].cpu().numpy().astype(np.float64)
+    bc = out["best_cost"].cpu().numpy()
+    sbc = out["seed_best_cost"].cpu().numpy()
+    R, W = O.Robot(wl.robot), O.World(wl.worlds[0])
+    stats = Stats()
+    for p in (0, 1, 257, 511, 768, 999):
+        c_ref, g_ref, _, margin, _ = O.eval_ik(R, W, wl.cost, f32(wl.goal[p]), bq[p].reshape(-1))
+        stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"ik winner {p}", grad_slack=2e-6)
+        assert bc[p] == sbc[p].min()
+    stats.done(0.5)
+    c0, _, _ = ctx.evaluate(T(wl.seeds.reshape(-1, 7)), T(np.repeat(wl.goal, 30, 0)))
+    assert np.all(sbc.reshape(-1) <= c0.cpu().numpy() * (1 + 1e-6))
+    ctx.close()
+
+
+def test_full_size_dense_solve_sampled_against_oracle(native, O):
+    """BASELINE configs[4] per GPU at the bench's sample size (16 problems x 32 seeds x 32
+    timesteps, K = 1000 per problem, swept + speed, 100 iterations; the HMMA pre-screen build):
+    sampled winners re-evaluated by the oracle, argmin of the per-seed results, every seed
+    improved on its initial cost."""
+    from paper_2310_17274_b200 import workload
+    wl = workload.franka_to(0, list(range(16)), S=32, H=32, n_boxes=1000, iters=100, dense=True)
+    ctx = make(native, wl.robot, wl.worlds, wl.cost)
+    out = ctx.solve(wl.solver, T(wl.seeds), T(wl.goal), start=T(wl.start), env=T(wl.env, torch.int32),
+                    seed_outputs=True)
+    bt = out["best_traj"].cpu().numpy().astype(np.float64)
+    bc = out["best_cost"].cpu().numpy()
+    sbc = out["seed_best_cost"].cpu().numpy()
+    R = O.Robot(wl.robot)
+    stats = Stats()
+    for p in (0, 7, 15):
+        c_ref, g_ref, _, margin, _ = O.eval_traj(R, O.World(wl.worlds[p]), wl.cost, f32(wl.start[p]),
+                                                 f32(wl.goal[p]), bt[p])
+        stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"dense winner {p}")
+        assert bc[p] == sbc[p].min()
+    stats.done(0.67)
     c0, _, _ = ctx.evaluate(T(wl.seeds.reshape(-1, 32, 7)), T(np.repeat(wl.goal, 32, 0)),
                             start=T(np.repeat(wl.start, 32, 0)), env=T(np.repeat(wl.env, 32), torch.int32))
     assert np.all(sbc.reshape(-1) <= c0.cpu().numpy() * (1 + 1e-6))
