@@ -1143,16 +1143,19 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         for (int u = 0; u < 4; ++u)
                             any |= fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, hbj)))) > thr[u];
                     }
-                    if (any) {   // rare: exact test of these (up to) 4 x 4 pairs, Eq. self-collision
+                    if (any) {   // rare: exact test of the flagged pairs among these 4 x 4, Eq. self-collision
 #pragma unroll 1
                         for (int v = v0; v < min(v0 + 4, len); ++v) {
                             const float4 wj = s.sw[(jb + v) * NC + lane];
                             const float rj = rself[jb + v];
-#pragma unroll 1
-                            for (int u = 0; u < na; ++u) {
-                                const float4 w = s.sw[(ia + u) * NC + lane];
-                                const float R = rself[ia + u] + rj;
-                                const float dx = w.x - wj.x, dy = w.y - wj.y, dz = w.z - wj.z;
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                // the screen again (same expression): only its flagged pairs
+                                if (!(fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, wj.w)))) >
+                                      thr[u]))
+                                    continue;
+                                const float R = ri[u] + rj;
+                                const float dx = wi[u].x - wj.x, dy = wi[u].y - wj.y, dz = wi[u].z - wj.z;
                                 const float d2 = dx * dx + dy * dy + dz * dz;
                                 if (!(d2 < R * R)) continue;
                                 const float pen = R - sqrtf(d2);
