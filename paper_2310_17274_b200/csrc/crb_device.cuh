@@ -21,7 +21,7 @@
 #define CRB_STATS 0
 #endif
 #if CRB_STATS
-__device__ unsigned long long g_crb_stats[8];
+__device__ unsigned long long g_crb_stats[16];
 #define CRB_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_crb_stats[i], (unsigned long long)(v)); } while (0)
 #else
 #define CRB_STAT(i, v) do { } while (0)
@@ -870,11 +870,21 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         const bool hasn = to && lane + 1 < H;
         const int nwg = (rp.M + 3) >> 2, nitems = nwg + rp.NB;
         int *qctr = reinterpret_cast<int *>(s.scal + 4);
+#if CRB_STATS
+        const long long t_q0 = clock64();
+#endif
         for (;;) {
             int item = 0;
             if (lane == 0) item = atomicAdd(qctr, 1);
             item = __shfl_sync(FULL, item, 0);
             if (item >= nitems) break;
+#if CRB_STATS
+            const long long t_start = clock64();
+            struct StatT {
+                long long t0; int w;
+                __device__ ~StatT() { CRB_STAT(w ? 4 : 5, clock64() - t0); CRB_STAT(w ? 8 : 9, 1); }
+            } stat_t{t_start, item < nwg};
+#endif
             if (item < nwg) {
                 const int m0 = item << 2;
                 float cx[4], cy[4], cz[4], th2[4], sp[4];
@@ -1174,6 +1184,13 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         s.sbest[warp * NC + lane] = best;
         s.srank[warp * NC + lane] = brank;
         s.sij[warp * NC + lane] = bij;
+#if CRB_STATS
+        const long long t_done = clock64();
+        __syncthreads();
+        CRB_STAT(6, clock64() - t_done);    // wait at the queue barrier
+        CRB_STAT(7, t_done - t_q0);         // time in the queue
+        CRB_STAT(10, 1);                    // warp-passes
+#endif
     }
 
     __syncthreads();

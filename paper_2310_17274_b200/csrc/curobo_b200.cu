@@ -23,6 +23,10 @@
 #include "curobo_b200.h"
 #include "crb_device.cuh"
 
+#ifndef CRB_SELF_LEN
+#define CRB_SELF_LEN 16   // partners per self-collision work item (<= 511)
+#endif
+
 using namespace crb;
 
 namespace {
@@ -1292,9 +1296,11 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         const auto ra = runs_of(a);
         int na = 1;
         while (na < 4 && a + na < M && runs_of(a + na) == ra) ++na;
+        // runs are cut into pieces of at most CRB_SELF_LEN partners: finer work-queue items keep the
+        // warps' queue times balanced (uneven penetrations, e.g. IK seeds)
         for (const auto &rn : ra)
-            for (int jb = rn.first; jb < rn.second; jb += 511)
-                blks.push_back({a, na, jb, std::min(511, rn.second - jb)});
+            for (int jb = rn.first; jb < rn.second; jb += CRB_SELF_LEN)
+                blks.push_back({a, na, jb, std::min(CRB_SELF_LEN, rn.second - jb)});
         a += na;
     }
     // work-queue order: decreasing cost (~ len * (2 + 9 na) instructions), ties by position
@@ -1808,9 +1814,9 @@ crb_status crb_particle_normals(uint32_t key0, uint32_t key1, int n_var, int n_p
 // world-screen work counters (tools/world_stats.py only; not part of the product ABI)
 extern "C" int crb_debug_stats(unsigned long long *out, int reset) {
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-    if (cudaMemcpyFromSymbol(out, ::g_crb_stats, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out, ::g_crb_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
     if (reset) {
-        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long z[16] = {};
         cudaMemcpyToSymbol(::g_crb_stats, z, sizeof(z));
     }
     return 0;

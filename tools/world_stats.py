@@ -38,7 +38,7 @@ so.crb_debug_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 
 
 def stats(reset=True):
-    a = (C.c_ulonglong * 8)()
+    a = (C.c_ulonglong * 16)()
     so.crb_debug_stats(a, int(reset))
     return list(a)
 
@@ -54,8 +54,12 @@ def run(name, wl):
     s = stats()
     ctx.close()
     ex = max(s[0], 1)
-    print(f"{name}: pairs {s[0]}  mma-flagged {s[1] / ex:.3f}  exact-flagged {s[2] / ex:.3f}  "
+    print(f"{name}: pairs {s[0]}  pre-screen-flagged {s[1] / ex:.3f}  exact-flagged {s[2] / ex:.3f}  "
           f"entries/pair {s[3] / ex:.3f}", flush=True)
+    wp = max(s[10], 1)
+    print(f"   queue: world item {s[4] / max(s[8], 1):.0f} cyc x {s[8] / wp * 8:.1f}/pass, self item "
+          f"{s[5] / max(s[9], 1):.0f} cyc x {s[9] / wp * 8:.1f}/pass; per warp-pass: in queue {s[7] / wp:.0f} cyc, "
+          f"barrier wait {s[6] / wp:.0f} cyc", flush=True)
 
 
 P = args.problems
