@@ -83,7 +83,7 @@ struct RobotPack {
 struct Layout {
     int robot, boxes, mbar;
     int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, cbb, csm, gxd, gq, gva, pose_ft, tdp,
-        goal, cfg_cost, cfg_terms, gV, red, st, scal;
+        goal, cfg_cost, cfg_terms, gV, red, st, scal, wq;
     int solver;      // start of the solver region
     int total;       // words
     int XS;          // row length of xs (H + 5)
@@ -209,6 +209,11 @@ __device__ __forceinline__ int stage_tables(const KParams &kp, float *smem, int 
         mbar_expect_tx(bar, rbytes + bbytes);
         bulk_g2s(smem + kp.lay.robot, kp.robot, rbytes, bar);
         if (K > 0) bulk_g2s(smem + kp.lay.boxes, kp.boxes + (size_t)env * kp.kmax * 4, bbytes, bar);
+    }
+    {   // world work-queue order: identity, no cost history yet
+        const int nwg = (kp.rp.M + 3) >> 2;
+        int *wq = reinterpret_cast<int *>(smem + kp.lay.wq);
+        for (int i = threadIdx.x; i < 2 * nwg; i += blockDim.x) wq[i] = i < nwg ? i : 0;
     }
     __syncthreads();
     mbar_wait(bar, 0);
@@ -379,6 +384,7 @@ struct Smem {
     float4 *sw;             // [M][32] sphere centre (x, y, z) and hb = -(|w|^2 - r_self^2) / 2
     float4 *sg;             // [M][32] dE/dw (x, y, z) and the world energy E (w)
     int *srank, *sij;
+    int *wq;                // [nwg] world-item order (largest last-pass cost first), [nwg] those costs
 };
 
 __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
@@ -400,6 +406,7 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     s.gq = smem + L.gq; s.gva = smem + L.gva; s.pose_ft = smem + L.pose_ft; s.tdp = smem + L.tdp;
     s.goal = smem + L.goal; s.cfg_cost = smem + L.cfg_cost; s.cfg_terms = smem + L.cfg_terms;
     s.gV = smem + L.gV; s.red = smem + L.red; s.st = smem + L.st; s.scal = smem + L.scal;
+    s.wq = reinterpret_cast<int *>(smem + L.wq);
     return s;
 }
 
@@ -711,7 +718,22 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = rp.D, H = cf.H, XS = kp.lay.XS;
     const float *lim = s.fw + rp.o_lim;
-    if (tid == 0) reinterpret_cast<int *>(s.scal + 4)[0] = 0;   // work-queue counter (read after 2 barriers)
+    if (tid == 0) {
+        reinterpret_cast<int *>(s.scal + 4)[0] = 0;   // work-queue counter (read after 2 barriers)
+        // world items in decreasing cost of the previous pass (longest first: the queue's tail is
+        // then the short self items); ties keep index order.  Which warp takes which item never
+        // changes a result (fixed-order merges).
+        const int nwg = (rp.M + 3) >> 2;
+        if (WMMA && nwg <= 32) {   // large worlds only: few, long world items
+            int *ord = s.wq, *cost = s.wq + nwg;
+            for (int i = 1; i < nwg; ++i) {
+                const int g = ord[i], cg = cost[g];
+                int j = i - 1;
+                while (j >= 0 && (cost[ord[j]] < cg || (cost[ord[j]] == cg && ord[j] > g))) { ord[j + 1] = ord[j]; --j; }
+                ord[j + 1] = g;
+            }
+        }
+    }
 
     // ---- a2: state map (O2, Table 5 last row) into xs[D][H+5] and the slot configurations
     if (MODE == MODE_TO) {
@@ -886,7 +908,14 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             } stat_t{t_start, item < nwg};
 #endif
             if (item < nwg) {
-                const int m0 = item << 2;
+                const int grp = WMMA ? s.wq[item] : item;
+                const int m0 = grp << 2;
+                struct ItemCost {   // large worlds: the group's cost for the next pass's order (lane 0)
+                    int *dst; long long t0;
+                    __device__ ~ItemCost() {
+                        if (WMMA && (threadIdx.x & 31) == 0) *dst = (int)min(clock64() - t0, (long long)0x3fffffff);
+                    }
+                } item_cost{s.wq + nwg + grp, WMMA ? clock64() : 0ll};
                 float cx[4], cy[4], cz[4], th2[4], sp[4];
                 int dirs[4];
 #pragma unroll
