@@ -206,8 +206,9 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg2_franka_to", "problems_per_step": 1, "seeds": 32, "timesteps": 32,
-                       "iters_per_step": iters, "boxes": 20, "spheres": 64, "dof": 7},
+            "config": {"workload": "cfg2_franka_to_batched", "sample_of_step": "problem 0 of the 64-problem step",
+                       "problems_per_step": 1, "seeds": 32, "timesteps": 32, "iters_per_step": iters, "boxes": 20,
+                       "spheres": 64, "dof": 7, "flags": "sweep+speed"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "oracle",
                              "sample": f"1 problem x 32 seeds x {iters} iterations per step (fp64 C oracle)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
