@@ -60,7 +60,7 @@ def _worker(rank, world, port, costs, trajs, S, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_seed_sharded_merge_matches_single_process(world):
     rng = np.random.default_rng(0)
     P, S = 9, 8
