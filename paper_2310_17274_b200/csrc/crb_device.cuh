@@ -41,7 +41,7 @@ __device__ unsigned long long g_crb_stats[16];
 // ... used when the environment has at least this many cuboids (below it the FFMA screen is as
 // fast and its smaller code keeps the instruction cache warm: DESIGN.md "World screen")
 #ifndef CRB_MMA_MIN_K
-#define CRB_MMA_MIN_K 64
+#define CRB_MMA_MIN_K 60
 #endif
 
 namespace crb {
@@ -87,6 +87,7 @@ struct Layout {
     int solver;      // start of the solver region
     int total;       // words
     int XS;          // row length of xs (H + 5)
+    int boxes_gmem;  // 1: the cuboid table is read from global memory (large-world build), not staged
 };
 
 // Cost parameters (App. A), copied by value into registers by eval_pass.
@@ -205,10 +206,10 @@ __device__ __forceinline__ int stage_tables(const KParams &kp, float *smem, int 
         reinterpret_cast<int *>(smem + kp.lay.mbar)[2] = env;   // for the fp16x2 cuboid table
         mbar_init(bar, 1);
         const uint32_t rbytes = (uint32_t)kp.rp.words * 4u;
-        const uint32_t bbytes = (uint32_t)K * 64u;
+        const uint32_t bbytes = kp.lay.boxes_gmem ? 0u : (uint32_t)K * 64u;
         mbar_expect_tx(bar, rbytes + bbytes);
         bulk_g2s(smem + kp.lay.robot, kp.robot, rbytes, bar);
-        if (K > 0) bulk_g2s(smem + kp.lay.boxes, kp.boxes + (size_t)env * kp.kmax * 4, bbytes, bar);
+        if (bbytes > 0) bulk_g2s(smem + kp.lay.boxes, kp.boxes + (size_t)env * kp.kmax * 4, bbytes, bar);
     }
     {   // world work-queue order: identity, no cost history yet
         const int nwg = (kp.rp.M + 3) >> 2;
@@ -392,7 +393,11 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     Smem s;
     s.iw = reinterpret_cast<const int *>(smem + L.robot);
     s.fw = smem + L.robot;
-    s.boxes = smem + L.boxes;
+    // large worlds: the cuboid table stays in global memory (L1 / L2), so the CTA keeps its
+    // shared-memory footprint and two CTAs fit per SM; env from stage_tables
+    s.boxes = L.boxes_gmem ? reinterpret_cast<const float *>(
+                                 kp.boxes + (size_t)reinterpret_cast<const int *>(smem + L.mbar)[2] * kp.kmax * 4)
+                           : smem + L.boxes;
     s.q_cfg = smem + L.q_cfg; s.scs = smem + L.scs; s.xs = smem + L.xs;
     s.lt = smem + L.ltg;                               // sg aliases lt (lt dead after sphere placement)
     s.sg = reinterpret_cast<float4 *>(smem + L.ltg);

@@ -1508,7 +1508,8 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
     KParams kp = base_params(ctx);
     kp.B = B; kp.H = H; kp.cp.H = H; kp.mode = mode; kp.q_in = q; kp.env = env; kp.start = start; kp.goal = goal;
     kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs; kp.dt_arr = dt;
-    const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
+    const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
+    kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
     const bool wm = use_world_mma(ctx);
     if (mode == MODE_TO)
@@ -1560,7 +1561,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     kp.k_mu = sp->k_mu; kp.k_sigma = sp->k_sigma; kp.s0_frac = sp->sigma0_frac;
     kp.rng_key = sp->rng_key; kp.prob_base = sp->global_problem_base;
     kp.seed_best_cost = sbc; kp.seed_best_traj = sbt;
-    const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
+    const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
+    kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids + solver)");
     const bool wm = use_world_mma(ctx);
     if (mode == MODE_TO)
@@ -1617,7 +1619,8 @@ crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, i
     if ((st = ready(ctx, true)) != CRB_OK) return st;
     KParams kp = base_params(ctx);
     const int mode = H == 1 ? MODE_IK : MODE_TO;
-    const size_t bytes = make_layout(ctx->rp, ctx->kmax_enabled, mode, H, history, n_alpha, true, kp.lay);
+    const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, history, n_alpha, true, kp.lay);
+    kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
     if (smem_bytes) *smem_bytes = (int)bytes;
     if (bytes > SMEM_MAX) { if (ctas_per_sm) *ctas_per_sm = 0; return CRB_OK; }
     int n = 0;

@@ -2,7 +2,7 @@
 "World screen").
 
 The library builds its solver / evaluation kernels twice: with the HMMA pre-screen when some
-environment holds >= CRB_MMA_MIN_K (64) enabled cuboids, else FFMA only.  The pre-screen only
+environment holds >= CRB_MMA_MIN_K (60) enabled cuboids, else FFMA only.  The pre-screen only
 chooses which cuboids go through the exact fp32 test, so on the SAME environments both builds must
 return bitwise the same costs, gradients and solves; a context whose world list includes one large
 environment runs the HMMA build for all of them.  Parity against the fp64 oracle at K in the HMMA
@@ -18,7 +18,7 @@ from test_gpu_parity import MARGIN, Stats, T, f32, franka_trajs, make  # noqa: F
 
 pytestmark = pytest.mark.gpu
 
-MMA_MIN_K = 64
+MMA_MIN_K = 60
 
 
 @pytest.fixture(scope="module")
