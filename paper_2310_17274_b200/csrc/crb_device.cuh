@@ -393,11 +393,7 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     Smem s;
     s.iw = reinterpret_cast<const int *>(smem + L.robot);
     s.fw = smem + L.robot;
-    // large worlds: the cuboid table stays in global memory (L1 / L2), so the CTA keeps its
-    // shared-memory footprint and two CTAs fit per SM; env from stage_tables
-    s.boxes = L.boxes_gmem ? reinterpret_cast<const float *>(
-                                 kp.boxes + (size_t)reinterpret_cast<const int *>(smem + L.mbar)[2] * kp.kmax * 4)
-                           : smem + L.boxes;
+    s.boxes = smem + L.boxes;   // eval_pass of the large-world build re-points it to global memory
     s.q_cfg = smem + L.q_cfg; s.scs = smem + L.scs; s.xs = smem + L.xs;
     s.lt = smem + L.ltg;                               // sg aliases lt (lt dead after sphere placement)
     s.sg = reinterpret_cast<float4 *>(smem + L.ltg);
@@ -717,7 +713,13 @@ __device__ __forceinline__ void stage_dt(const KParams &kp, const Smem &s, int r
 template <int MODE, bool WMMA>
 __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
                                           const float *dvec, bool grad = true) {
-    const Smem s = make_smem(kp, smem);
+    Smem s = make_smem(kp, smem);
+    // large worlds: the cuboid table stays in global memory (L1 / L2), so the CTA keeps its
+    // shared-memory footprint and two CTAs fit per SM (kp.lay.boxes_gmem == WMMA); env from
+    // stage_tables
+    if (WMMA)
+        s.boxes = reinterpret_cast<const float *>(
+            kp.boxes + (size_t)reinterpret_cast<const int *>(smem + kp.lay.mbar)[2] * kp.kmax * 4);
     const RobotPack &rp = kp.rp;
     const CostP &cf = kp.cp;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
