@@ -71,7 +71,8 @@ struct RobotPack {
     int o_blocks;   // NB x uint2: pair block (ia | (na-1) << 9 | jb << 11 | len << 20, rank base):
                     //   the pairs {ia..ia+na-1} x {jb..jb+len-1}, all in S (na <= 4)
     int NB;         // number of pair blocks (stored in decreasing cost order: a work queue)
-    int o_rank;     // u16 ranks in S of the block pairs, [block][u][v] from the block's rank base
+    int o_blocks_ik, NB_ik;   // the same pairs in pieces of <= CRB_SELF_LEN partners (IK passes)
+    int o_rank;     // u16 ranks in S of the block pairs, [v][u] from the block's rank base
     int o_lim;      // 5 x D floats: lo, hi, vmax, amax, jmax
     int o_doflink;  // D ints: link carrying dof d
     int o_desc;     // L ints: bit l' set iff link l' is in the subtree of link l (l itself included)
@@ -886,7 +887,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         // go to the lowest rank in S (first maximal pair, A28).
         float best = 0.f;
         int brank = 0x7fffffff, bij = -1;
-        const uint2 *blk = reinterpret_cast<const uint2 *>(s.iw + rp.o_blocks);
+        const uint2 *blk = reinterpret_cast<const uint2 *>(s.iw + (MODE == MODE_IK ? rp.o_blocks_ik : rp.o_blocks));
         const float *rself = s.fw + rp.o_rself;
         const unsigned short *rk = reinterpret_cast<const unsigned short *>(s.iw + rp.o_rank);
         // world (Alg. 10 + Algs. 11-12, Eq. world-collision-cost): each thread carries the 4
@@ -897,7 +898,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
         const bool hasp = to && lane > 0 && lane < H;
         const bool hasn = to && lane + 1 < H;
-        const int nwg = (rp.M + 3) >> 2, nitems = nwg + rp.NB;
+        const int nwg = (rp.M + 3) >> 2, nitems = nwg + (MODE == MODE_IK ? rp.NB_ik : rp.NB);
         int *qctr = reinterpret_cast<int *>(s.scal + 4);
 #if CRB_STATS
         const long long t_q0 = clock64();
@@ -1206,7 +1207,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                 if (!(d2 < R * R)) continue;
                                 const float pen = R - sqrtf(d2);
                                 if (pen >= best && pen > 0.f) {
-                                    const int rank = rk[B.y + u * len + v];
+                                    const int rank = rk[B.y + v * na + u];
                                     if (pen > best || rank < brank) {
                                         best = pen; brank = rank; bij = (ia + u) | ((jb + v) << 9);
                                     }

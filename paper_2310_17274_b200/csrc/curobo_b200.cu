@@ -1291,38 +1291,49 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         }
         return rr;
     };
-    struct Blk { int ia, na, jb, len; };
-    std::vector<Blk> blks;
+    // Two work-item tables over the same pairs: TO passes take whole runs (<= 511 partners: fewer,
+    // longer items), IK passes runs cut into pieces of at most CRB_SELF_LEN partners (the random IK
+    // seeds make penetrations uneven: finer items keep the warps' queue times balanced).  Ranks are
+    // stored v-major per run ([v][u]), so a piece of a run indexes the same array: rank of pair
+    // (u, v) of a block = rank[B.y + v * na + u].
+    struct Blk { int ia, na, jb, len, rbase; };
+    std::vector<Blk> full, cut;
+    std::vector<uint16_t> ranks;
     for (int a = 0; a < M;) {
         const auto ra = runs_of(a);
         int na = 1;
         while (na < 4 && a + na < M && runs_of(a + na) == ra) ++na;
-        // runs are cut into pieces of at most CRB_SELF_LEN partners: finer work-queue items keep the
-        // warps' queue times balanced (uneven penetrations, e.g. IK seeds)
-        for (const auto &rn : ra)
-            for (int jb = rn.first; jb < rn.second; jb += CRB_SELF_LEN)
-                blks.push_back({a, na, jb, std::min(CRB_SELF_LEN, rn.second - jb)});
+        for (const auto &rn : ra) {
+            const int base = (int)ranks.size(), len = rn.second - rn.first;
+            for (int v = 0; v < len; ++v)
+                for (int u = 0; u < na; ++u) ranks.push_back((uint16_t)rank_of[(size_t)(a + u) * M + rn.first + v]);
+            for (int j0 = 0; j0 < len; j0 += 511)
+                full.push_back({a, na, rn.first + j0, std::min(511, len - j0), base + j0 * na});
+            for (int j0 = 0; j0 < len; j0 += CRB_SELF_LEN)
+                cut.push_back({a, na, rn.first + j0, std::min(CRB_SELF_LEN, len - j0), base + j0 * na});
+        }
         a += na;
     }
     // work-queue order: decreasing cost (~ len * (2 + 9 na) instructions), ties by position
-    std::vector<int> bord(blks.size());
-    for (size_t i = 0; i < blks.size(); ++i) bord[i] = (int)i;
-    std::stable_sort(bord.begin(), bord.end(), [&](int x, int y) {
-        return blks[x].len * (2 + 9 * blks[x].na) > blks[y].len * (2 + 9 * blks[y].na);
-    });
-    std::vector<uint32_t> bk;
-    std::vector<uint16_t> ranks;
-    for (int bi : bord) {
-        const Blk &b = blks[bi];
-        bk.push_back((uint32_t)b.ia | ((uint32_t)(b.na - 1) << 9) | ((uint32_t)b.jb << 11) | ((uint32_t)b.len << 20));
-        bk.push_back((uint32_t)ranks.size());
-        for (int u = 0; u < b.na; ++u)
-            for (int v = 0; v < b.len; ++v) ranks.push_back((uint16_t)rank_of[(size_t)(b.ia + u) * M + b.jb + v]);
-    }
+    auto emit = [&](std::vector<Blk> &blks, std::vector<uint32_t> &bk) {
+        std::stable_sort(blks.begin(), blks.end(), [&](const Blk &x, const Blk &y) {
+            return x.len * (2 + 9 * x.na) > y.len * (2 + 9 * y.na);
+        });
+        for (const Blk &b : blks) {
+            bk.push_back((uint32_t)b.ia | ((uint32_t)(b.na - 1) << 9) | ((uint32_t)b.jb << 11) | ((uint32_t)b.len << 20));
+            bk.push_back((uint32_t)b.rbase);
+        }
+    };
+    std::vector<uint32_t> bk, bk_ik;
+    emit(full, bk);
+    emit(cut, bk_ik);
+    const std::vector<Blk> &blks = full;
     rp.NB = (int)blks.size();
+    rp.NB_ik = (int)cut.size();
     rp.P = npairs;
     rp.o_rself = w; w += r4(M);
     rp.o_blocks = w; w += r4((int)bk.size());
+    rp.o_blocks_ik = w; w += r4((int)bk_ik.size());
     rp.o_rank = w; w += r4(((int)ranks.size() + 1) / 2);
     rp.o_lim = w; w += r4(5 * D);
     rp.o_doflink = w; w += r4(D);
@@ -1351,6 +1362,7 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
     }
     for (int k = 0; k < M; ++k) fput(rp.o_rself + k, rself[k]);
     for (size_t i = 0; i < bk.size(); ++i) blob[rp.o_blocks + i] = bk[i];
+    for (size_t i = 0; i < bk_ik.size(); ++i) blob[rp.o_blocks_ik + i] = bk_ik[i];
     if (!ranks.empty()) memcpy(&blob[rp.o_rank], ranks.data(), ranks.size() * 2);
     for (int d = 0; d < D; ++d) {
         fput(rp.o_lim + d, r->pos_lo[d]); fput(rp.o_lim + D + d, r->pos_hi[d]);
