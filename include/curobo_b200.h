@@ -16,13 +16,16 @@
  *   - crb_lbfgs_solve_host takes HOST pointers (pinned memory recommended), performs the
  *     host->device copies, the solve and the device->host copies on `stream`, and synchronises.
  *   - A context is bound to one CUDA device and used by one host thread at a time.
- *   - Numeric types: all arithmetic on the device is fp32 (the paper's kernels are fp32).
+ *   - Numeric types: all results are fp32 arithmetic (the paper's kernels are fp32).  The
+ *     sphere-cuboid screen runs a conservative reduced-precision pre-screen (packed fp16 below 60
+ *     enabled cuboids per environment, tensor-core fp16 hi/lo products from 60) that only selects
+ *     the cuboids given the exact fp32 test: results are bitwise those of the all-fp32 screen.
  *   - Non-finite inputs are not scanned: a NaN propagates into the cost, a NaN cost packs to the
  *     +inf key and never wins a selection (SURVEY §8(b) deviation).
  *   - Capacity limits (CRB_E_LIMIT): D <= 16, L <= 32, M <= 512, pairs <= 16384, H*D <= 512,
  *     history <= 32, n_alpha <= 8, TO mode requires 8 <= H <= 32, IK mode has H == 1, and the
- *     per-CTA shared memory (robot tables + one environment's cuboids + solver state) must fit
- *     in 227 KB.
+ *     per-CTA shared memory (robot tables + solver state, plus one environment's cuboids below
+ *     60 cuboids; from 60 the cuboids are read from global memory) must fit in 227 KB.
  */
 #ifndef CUROBO_B200_H
 #define CUROBO_B200_H
@@ -141,8 +144,11 @@ const char *crb_version(void);
 crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *robot);
 
 /* Upload n_env environments of cuboids: boxes[n_env * k_max], env e using its first
- * boxes_per_env[e] entries.  Disabled cuboids are compacted away (Alg. 10 skips them).
- * Stream-ordered on the legacy stream: synchronises before returning. */
+ * boxes_per_env[e] entries.  Disabled cuboids are compacted away (Alg. 10 skips them).  Also
+ * builds the fp16 pair table of the small-world pre-screen and each cuboid's magnitude
+ * max(|R^T t|, h) that sizes both pre-screens' rounding slack (cuboids beyond the fp16 range,
+ * 3e4 m, always get the exact test).  Stream-ordered on the legacy stream: synchronises before
+ * returning. */
 crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_per_env,
                          const crb_cuboid *boxes);
 
