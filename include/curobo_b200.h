@@ -132,6 +132,13 @@ typedef struct {
     float sigma0_frac;         /* initial Theta_sigma = (sigma0_frac (hi - lo))^2 per variable    */
     uint32_t rng_key;          /* Philox key word 0                                               */
     int64_t global_problem_base;   /* added to the local problem index: Philox key word 1        */
+    /* "up to" an iteration count (the single-seed re-optimisation runs "for upto 300"
+     * iterations) in chunks of check_every iterations (25-iteration CUDA-graph chunks):
+     * after each chunk a TO seed stops when its best cost improved by at most conv_rtol x |best
+     * at the chunk start| (reading B20).  check_every = 0 runs exactly `iters` (the default); IK
+     * solves ignore it. */
+    int check_every;           /* >= 0                                                            */
+    float conv_rtol;           /* >= 0                                                            */
 } crb_solver_params;
 
 crb_status crb_create(int cuda_device, crb_ctx **out);

@@ -118,6 +118,8 @@ struct KParams {
     float alpha[8], c1, c2;
     long long seed_base;
     // particle warm-up (Alg. 5; f1)
+    int check_every;              // chunked convergence exit of TO solves (0: off; reading B20)
+    float conv_rtol;
     int pn_iters, pn;
     float p_inv_beta, k_mu, k_sigma, s0_frac;
     unsigned rng_key;

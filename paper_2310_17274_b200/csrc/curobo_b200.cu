@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
     // warm-up (f1: pn_iters x pn cost-only passes, Alg. 5), then pass 0 evaluates Theta_0 (O8
     // initialise) and every iteration is an L-BFGS step followed by A candidate passes.
     // During the warm-up th holds mu, g holds Theta_sigma, dd / thp the UPDATE sums S1 / S2.
-    float c = 0.f, cbest = 0.f, g0d = 0.f;
+    float c = 0.f, cbest = 0.f, g0d = 0.f, chunk_best = 0.f;
     float d_e[2] = {0.f, 0.f};
     const int npart = kp.pn_iters * kp.pn;
     const int npass = npart + 1 + kp.iters * A;
@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
         if (a < 0) {
             c = s.scal[0];
             cbest = c;
+            chunk_best = c;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int i = t + e * NT;
@@ -266,6 +267,15 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
                 for (int e = 0; e < 2; ++e) {
                     const int i = t + e * NT;
                     if (i < N) best[i] = th[i];
+                }
+            }
+            // ---- a14: "up to" iters in chunks (B20): every thread holds the same cbest, so the
+            // exit is CTA-uniform
+            if (kp.check_every > 0) {
+                const int it = (lpass - 1) / A + 1;   // iterations done
+                if (it % kp.check_every == 0) {
+                    if (!(cbest < chunk_best - kp.conv_rtol * fabsf(chunk_best))) break;
+                    chunk_best = cbest;
                 }
             }
         }
@@ -1553,6 +1563,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
                                     !(sp->k_mu <= 1.f) || !(sp->k_sigma >= 0.f) || !(sp->k_sigma <= 1.f) ||
                                     !(sp->sigma0_frac >= 0.f))))
         return fail(ctx, CRB_E_ARG, "particle warm-up: iters >= 0, n >= 1, beta > 0, k_mu/k_sigma in [0,1], sigma0_frac >= 0");
+    if (sp->check_every < 0 || !(sp->conv_rtol >= 0.f))
+        return fail(ctx, CRB_E_ARG, "check_every >= 0 and conv_rtol >= 0");
     const int mode = H == 1 ? MODE_IK : MODE_TO;
     const int D = ctx->rp.D;
     if (mode == MODE_TO && (H < 8 || H > 32 || H * D > 512 || !start))
@@ -1572,6 +1584,7 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     kp.p_inv_beta = sp->particle_iters > 0 ? 1.f / sp->particle_beta : 0.f;
     kp.k_mu = sp->k_mu; kp.k_sigma = sp->k_sigma; kp.s0_frac = sp->sigma0_frac;
     kp.rng_key = sp->rng_key; kp.prob_base = sp->global_problem_base;
+    kp.check_every = sp->check_every; kp.conv_rtol = sp->conv_rtol;
     kp.seed_best_cost = sbc; kp.seed_best_traj = sbt;
     const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
     kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;

@@ -118,6 +118,10 @@ class SolverParams:
     k_sigma: float = 0.5
     sigma0_frac: float = 0.1
     rng_key: int = 0
+    # "up to" iters in chunks of check_every iterations: a TO seed stops when
+    # its best cost improved by at most conv_rtol x |best| over a chunk (reading B20); 0 = off
+    check_every: int = 0
+    conv_rtol: float = 0.0
 
 
 # --------------------------------------------------------------------------------------------

@@ -42,6 +42,8 @@ class MotionGenConfig:
     ik_iters: int = 100
     to_iters: int = 100
     refine_iters: int = 300
+    refine_check: int = 25          # the re-optimisation runs "for upto 300" in 25-iteration
+    refine_rtol: float = 1e-3       # chunks; stop when a chunk improves the best < 0.1 % (B20)
     particle_iters: int = 2
     pos_thr: float = 5e-3           # m: "within 5mm ... of desired position"
     rot_thr: float = 0.05           # "5% of desired ... orientation" in the A1 metric 1 - |<q_g, q>|
@@ -61,7 +63,8 @@ class MotionGen:
         self.cost_to2 = dataclasses.replace(cost, dt=cfg.dt_init, flags=cost.flags | inputs.JERK)
         self.sp_ik = inputs.SolverParams(iters=cfg.ik_iters, particle_iters=cfg.particle_iters)
         self.sp_to = inputs.SolverParams(iters=cfg.to_iters, particle_iters=cfg.particle_iters)
-        self.sp_refine = inputs.SolverParams(iters=cfg.refine_iters)
+        self.sp_refine = inputs.SolverParams(iters=cfg.refine_iters, check_every=cfg.refine_check,
+                                             conv_rtol=cfg.refine_rtol)
 
     def plan_retry(self, start, goal, env, problems, attempts=None):
         """plan() on the batch, then again on the problems that failed, with fresh IK seeds (the

@@ -66,7 +66,8 @@ class crb_solver_params(C.Structure):
                 ("c1", C.c_float), ("c2", C.c_float), ("ls_mode", C.c_int), ("global_seed_base", C.c_int64),
                 ("particle_iters", C.c_int), ("n_particles", C.c_int), ("particle_beta", C.c_float),
                 ("k_mu", C.c_float), ("k_sigma", C.c_float), ("sigma0_frac", C.c_float),
-                ("rng_key", C.c_uint32), ("global_problem_base", C.c_int64)]
+                ("rng_key", C.c_uint32), ("global_problem_base", C.c_int64), ("check_every", C.c_int),
+                ("conv_rtol", C.c_float)]
 
 
 _V = C.c_void_p
@@ -144,7 +145,8 @@ def solver_params_struct(sp: inputs.SolverParams, seed_base: int = 0, problem_ba
     return crb_solver_params(int(sp.iters), int(sp.history), len(sp.alpha), (C.c_float * 8)(*al), float(sp.c1),
                              float(sp.c2), int(sp.ls_mode), int(seed_base), int(sp.particle_iters),
                              int(sp.n_particles), float(sp.particle_beta), float(sp.k_mu), float(sp.k_sigma),
-                             float(sp.sigma0_frac), int(sp.rng_key) & 0xFFFFFFFF, int(problem_base))
+                             float(sp.sigma0_frac), int(sp.rng_key) & 0xFFFFFFFF, int(problem_base),
+                             int(sp.check_every), float(sp.conv_rtol))
 
 
 class Context:

@@ -575,3 +575,41 @@ def test_full_size_dense_solve_sampled_against_oracle(native, O):
                             start=T(np.repeat(wl.start, 32, 0)), env=T(np.repeat(wl.env, 32), torch.int32))
     assert np.all(sbc.reshape(-1) <= c0.cpu().numpy() * (1 + 1e-6))
     ctx.close()
+
+
+def test_solve_to_chunked_convergence_exit(native, O):
+    """check_every / conv_rtol (reading B20, "upto 300", P:2381 25-iteration chunks): each
+    seed's result equals, bit for bit, the fixed-iteration solve stopped at some multiple of the
+    chunk, at the first chunk whose improvement is <= conv_rtol |best|; check_every = 0 is the
+    plain fixed-iteration solve."""
+    import dataclasses
+    from paper_2310_17274_b200 import workload
+    wl = workload.franka_to(0, list(range(3)), S=6, H=32, iters=150)
+    ctx = make(native, wl.robot, wl.worlds, wl.cost)
+    args = (T(wl.seeds), T(wl.goal))
+    kw = dict(start=T(wl.start), env=T(wl.env, torch.int32), seed_outputs=True)
+    fixed = {}
+    for k in range(0, 151, 25):
+        sp = dataclasses.replace(wl.solver, iters=k)
+        o = ctx.solve(sp, *args, **kw)
+        fixed[k] = (o["seed_best_cost"].cpu().numpy(), o["seed_best_traj"].cpu().numpy())
+    plain = ctx.solve(dataclasses.replace(wl.solver, check_every=0, conv_rtol=0.5), *args, **kw)
+    assert np.array_equal(plain["seed_best_cost"].cpu().numpy(), fixed[150][0])
+    rtol = 0.2                  # large enough that the rule fires within 150 iterations here
+    early = ctx.solve(dataclasses.replace(wl.solver, check_every=25, conv_rtol=rtol), *args, **kw)
+    ec, et = early["seed_best_cost"].cpu().numpy(), early["seed_best_traj"].cpu().numpy()
+    stopped = 0
+    for idx in np.ndindex(ec.shape):
+        # the rule, replayed on the fixed-iteration results: stop after the first chunk k whose
+        # improvement over the previous chunk end is <= rtol |best at k - 25|
+        k_stop = 150
+        for k in range(25, 151, 25):
+            prev, cur = fixed[k - 25][0][idx], fixed[k][0][idx]
+            if not (cur < prev - rtol * abs(prev)):
+                k_stop = k
+                break
+        assert ec[idx] == fixed[k_stop][0][idx], (idx, k_stop)
+        assert np.array_equal(et[idx], fixed[k_stop][1][idx])
+        stopped += k_stop < 150
+    assert stopped > 0          # the rule fired for some seeds
+    ctx.close()
