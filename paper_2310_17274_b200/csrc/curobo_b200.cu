@@ -9,6 +9,7 @@
 //   fk_kernel         forward kinematics only (crb_fk)
 //   select_kernel     per-problem packed-key argmin over seeds (O9)
 //   + the test-hook kernels (ls_select, argmin_keys, lbfgs_direction)
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -292,6 +293,222 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
 // ------------------------------------------------------------------------------------------
 // persistent IK solver: one CTA per (problem, group of 32 seeds); lane = seed
 // ------------------------------------------------------------------------------------------
+// latency mode of the TO solver (small batches): the A line-search candidates of an iteration are
+// evaluated by the A CTAs of a thread-block cluster, one candidate each, instead of one after the
+// other by one CTA.  Every CTA of the cluster holds the whole solver state and runs the identical
+// L-BFGS step; after the candidate passes each reads the A costs / directional derivatives and the
+// winner's gradient from the owners' shared memory (DSMEM), so every step is bitwise the
+// sequential kernel's.  The particle warm-up and pass 0 run redundantly in every CTA.
+// ------------------------------------------------------------------------------------------
+template <bool WMMA>
+__global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) float smem[];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int A = kp.A;
+    const int rank = (int)cluster.block_rank();
+    const int unit = blockIdx.x / A;
+    const int p = unit / kp.S;
+    const int env = kp.env ? kp.env[p] : 0;
+    const int K = stage_tables(kp, smem, env);
+    const Smem s = make_smem(kp, smem);
+    const int D = kp.rp.D, H = kp.H, N = H * D, Np = (N + 3) & ~3, m = kp.m;
+    const int t = threadIdx.x;
+    float *base = smem + kp.lay.solver;
+    float *th = base, *g = th + Np, *dd = g + Np, *thp = dd + Np, *gp = thp + Np, *best = gp + Np,
+          *thA = best + Np, *cg_ = thA + Np, *Sb = cg_ + A * Np, *Yb = Sb + (m + 1) * Np,
+          *rho = Yb + (m + 1) * Np, *syv = rho + 40, *yyv = syv + 40;
+    int *order = reinterpret_cast<int *>(yyv + 40);
+    float *scal = yyv + 80;           // [0] this CTA's candidate cost, [8] its g . d
+    int *ring = reinterpret_cast<int *>(scal + 24);
+    const float *lim = s.fw + kp.rp.o_lim;
+    int ph = 0;
+
+    if (t < D) s.st[t] = kp.start[p * D + t];
+    if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[p * kp.cp.gw + t / NC];
+    stage_dt(kp, s, p);
+    const float *seed = kp.q_in + (size_t)unit * N;
+    float lo_e[2], hi_e[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int i = t + e * NT;
+        lo_e[e] = i < N ? lim[i % D] : 0.f;
+        hi_e[e] = i < N ? lim[D + i % D] : 0.f;
+        if (i < N) { th[i] = seed[i]; thA[i] = seed[i]; }
+    }
+    if (t == 0) { ring[0] = 0; ring[1] = 0; }
+    __syncthreads();
+
+    float c = 0.f, cbest = 0.f, g0d = 0.f, chunk_best = 0.f;
+    float d_e[2] = {0.f, 0.f};
+    const int npart = kp.pn_iters * kp.pn;
+    const int npass = npart + 1 + kp.iters;   // warm-up, pass 0, then one candidate pass per iteration
+    const unsigned pk1 = (unsigned)(kp.prob_base + p), psd = (unsigned)(kp.seed_base + (unit - p * kp.S));
+    ParticleAcc pacc;
+    pacc.reset();
+    if (npart > 0) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            if (i < N) { const float s0 = kp.s0_frac * (hi_e[e] - lo_e[e]); g[i] = s0 * s0; }   // B8
+        }
+    }
+    for (int pass = 0; pass < npass; ++pass) {
+        const bool part = pass < npart;
+        const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
+        const int lpass = pass - npart;        // 0: Theta_0, it + 1: iteration it
+        if (part) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) {
+                    const float z = particle_normal(kp.rng_key, pk1, (unsigned)i, (unsigned)pl, (unsigned)pit, psd);
+                    thA[i] = fminf(fmaxf(fmaf(sqrtf(g[i]), z, th[i]), lo_e[e]), hi_e[e]);
+                }
+            }
+            __syncthreads();
+        }
+        if (lpass > 0) {
+            const int it = lpass - 1;
+            // ---- a13 (identical in every CTA of the cluster)
+            if (it > 0) {
+                const int fs = ring[1];
+                float sy_p = 0.f, yy_p = 0.f;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = t + e * NT;
+                    if (i < N) {
+                        const float sv = th[i] - thp[i], yv = g[i] - gp[i];
+                        Sb[fs * Np + i] = sv; Yb[fs * Np + i] = yv;
+                        sy_p += sv * yv; yy_p += yv * yv;
+                    }
+                }
+                const float sy = block_sum(sy_p, s.red, ph);
+                const float yy = block_sum(yy_p, s.red, ph);
+                if (m > 0 && sy > 1e-12f && t == 0) {
+                    rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
+                    const int cnt = ring[0];
+                    if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
+                    else {
+                        const int ev = order[0];
+                        for (int i = 0; i < m - 1; ++i) order[i] = order[i + 1];
+                        order[m - 1] = fs;
+                        ring[1] = ev;
+                    }
+                }
+                __syncthreads();
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) { thp[i] = th[i]; gp[i] = g[i]; }
+            }
+            two_loop_block(N, Np, ring[0], order, Sb, Yb, rho, syv, yyv, g, dd, s.red, ph);
+            float gd_p = 0.f;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                d_e[e] = i < N ? dd[i] : 0.f;
+                if (i < N) gd_p += g[i] * d_e[e];
+            }
+            g0d = block_sum(gd_p, s.red, ph);
+            // ---- a1: this CTA's candidate
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) thA[i] = candidate(th[i], kp.alpha[rank], d_e[e], lo_e[e], hi_e[e]);
+            }
+            __syncthreads();
+        }
+        eval_pass<MODE_TO, WMMA>(kp, smem, thA, K, H, lpass > 0 ? dd : nullptr, !part);
+        if (part) {
+            float r;
+            const float w = pacc.add(s.scal[0], kp.p_inv_beta, r);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) {
+                    const float x = thA[i], dx = x - th[i];
+                    dd[i] = (pl == 0 ? 0.f : dd[i] * r) + w * x;
+                    thp[i] = (pl == 0 ? 0.f : thp[i] * r) + w * dx * dx;
+                }
+            }
+            if (pl == kp.pn - 1) {
+                const bool upd = pacc.Z > 0.f;
+                const float iz = upd ? 1.f / pacc.Z : 0.f;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = t + e * NT;
+                    if (i < N) {
+                        if (upd) {
+                            th[i] = (1.f - kp.k_mu) * th[i] + kp.k_mu * (dd[i] * iz);
+                            g[i] = (1.f - kp.k_sigma) * g[i] + kp.k_sigma * (thp[i] * iz);
+                        }
+                        if (pass == npart - 1) thA[i] = th[i];
+                    }
+                }
+                pacc.reset();
+                __syncthreads();
+            }
+            continue;
+        }
+        if (lpass == 0) {
+            c = s.scal[0];
+            cbest = c;
+            chunk_best = c;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) { g[i] = s.gV[i]; best[i] = th[i]; }
+            }
+            continue;
+        }
+        // ---- publish this candidate, then a11 over all of them (DSMEM)
+        if (t == 0) { scal[0] = s.scal[0]; scal[8] = pass_gdot(s); }
+        cluster.sync();
+        float ca[8], gda[8];
+        for (int a = 0; a < A; ++a) {
+            const float *ps = cluster.map_shared_rank(scal, a);
+            ca[a] = ps[0];
+            gda[a] = ps[8];
+        }
+        const int istar = ls_select(A, kp.alpha, c, g0d, ca, gda, kp.c1, kp.c2, kp.ls_mode);
+        const float *gsrc = cluster.map_shared_rank(s.gV, istar);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            if (i < N) {
+                th[i] = candidate(th[i], kp.alpha[istar], d_e[e], lo_e[e], hi_e[e]);
+                g[i] = gsrc[i];
+            }
+        }
+        c = ca[istar];
+        if (c < cbest) {                       // a12 (A23)
+            cbest = c;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = t + e * NT;
+                if (i < N) best[i] = th[i];
+            }
+        }
+        cluster.sync();                        // peers have read this CTA's candidate before it is overwritten
+        if (kp.check_every > 0 && lpass % kp.check_every == 0) {   // a14 chunk exit (B20), cluster-uniform
+            if (!(cbest < chunk_best - kp.conv_rtol * fabsf(chunk_best))) break;
+            chunk_best = cbest;
+        }
+    }
+    __syncthreads();
+    if (rank == 0) {
+        if (t == 0) kp.seed_best_cost[unit] = cbest;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            if (i < N) kp.seed_best_traj[(size_t)unit * N + i] = best[i];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 template <bool WMMA>
 __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
@@ -476,6 +693,206 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
     }
     __syncthreads();
     if (warp == 0 && active) {
+        const size_t u = (size_t)p * kp.S + sd;
+        kp.seed_best_cost[u] = cbest;
+        for (int d = 0; d < D; ++d) kp.seed_best_traj[u * D + d] = best[d * NC + lane];
+    }
+}
+
+// latency mode of the IK solver: the A candidates of an iteration on the A CTAs of a cluster (as
+// solve_to_cluster_kernel; per-seed selection on warp 0 from the peers' costs and gradients)
+template <bool WMMA>
+__global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) float smem[];
+    cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int G = (kp.S + NC - 1) / NC;
+    const int cid = blockIdx.x / kp.A;   // cluster = one 32-seed group, A CTAs
+    const int p = cid / G, grp = cid - p * G;
+    const int env = kp.env ? kp.env[p] : 0;
+    const int K = stage_tables(kp, smem, env);
+    const Smem s = make_smem(kp, smem);
+    const int D = kp.rp.D, m = kp.m, A = kp.A;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n_act = min(NC, kp.S - grp * NC);
+    const int DC = D * NC;
+    float *base = smem + kp.lay.solver;
+    float *th = base, *g = th + DC, *dd = g + DC, *thp = dd + DC, *gp = thp + DC, *best = gp + DC,
+          *Sb = best + DC, *Yb = Sb + (m + 1) * DC, *rho = Yb + (m + 1) * DC, *syv = rho + (m + 1) * NC,
+          *yyv = syv + (m + 1) * NC, *cg = yyv + (m + 1) * NC, *cc = cg + A * DC, *cgd = cc + A * NC;
+    int *order = reinterpret_cast<int *>(cgd + A * NC);   // [m][32]
+    const float *lim = s.fw + kp.rp.o_lim;
+    const int sd = grp * NC + lane;
+    const bool active = lane < n_act;
+
+    if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[p * kp.cp.gw + t / NC];
+    if (warp == 0)
+        for (int d = 0; d < D; ++d) {
+            const float v = active ? kp.q_in[((size_t)p * kp.S + sd) * D + d] : lim[d];
+            th[d * NC + lane] = v;
+            s.q_cfg[d * NC + lane] = v;
+        }
+    __syncthreads();
+    prep_sincos(s, D);
+    // single eval_pass call site: the particle warm-up (f1, cost only: thread t < D*32 owns
+    // element t with mu in th, Theta_sigma in g, the UPDATE sums in dd / thp), then pass 0 =
+    // Theta_0 and (L-BFGS step, A candidates) per iteration
+    float c = 0.f, cbest = 0.f, g0d = 0.f;
+    int cnt = 0, fs = 0;
+    const int npart = kp.pn_iters * kp.pn;
+    const int npass = npart + 1 + kp.iters;   // one candidate pass per iteration (this CTA's rank)
+    const unsigned pk1 = (unsigned)(kp.prob_base + p);
+    const unsigned psd = (unsigned)(kp.seed_base + grp * NC + (t & 31));
+    ParticleAcc pacc;
+    pacc.reset();
+    if (npart > 0 && t < DC) {
+        const int d = t / NC;
+        const float s0 = kp.s0_frac * (lim[D + d] - lim[d]);   // B8
+        g[t] = s0 * s0;
+    }
+    for (int pass = 0; pass < npass; ++pass) {
+        const bool part = pass < npart;
+        const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
+        const int lpass = pass - npart;
+        const int a = part ? -2 : (lpass == 0 ? -1 : rank);
+        if (part && t < DC) {
+            // ---- f1 SAMPLE (Alg. 5) for every seed of the group: variable d of seed lane
+            const int d = t / NC;
+            const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
+            const float v = fminf(fmaxf(fmaf(sqrtf(g[t]), z, th[t]), lim[d]), lim[D + d]);
+            s.q_cfg[t] = v;
+            float sn, cs;
+            sincosf(v, &sn, &cs);
+            s.scs[t] = sn;
+            s.scs[DC + t] = cs;
+        }
+        if (a >= 0 && warp == 0) {
+            const int it = lpass - 1;
+            // ---- ring push (per seed, A20)
+            if (it > 0) {
+                float sy = 0.f, yy = 0.f;
+                for (int d = 0; d < D; ++d) {
+                    const int e = d * NC + lane;
+                    const float sv = th[e] - thp[e], yv = g[e] - gp[e];
+                    Sb[fs * DC + e] = sv; Yb[fs * DC + e] = yv;
+                    sy += sv * yv; yy += yv * yv;
+                }
+                if (m > 0 && sy > 1e-12f) {
+                    rho[fs * NC + lane] = 1.f / sy; syv[fs * NC + lane] = sy; yyv[fs * NC + lane] = yy;
+                    if (cnt < m) { order[cnt * NC + lane] = fs; ++cnt; fs = cnt; }
+                    else {
+                        const int ev = order[lane];
+                        for (int i = 0; i < m - 1; ++i) order[i * NC + lane] = order[(i + 1) * NC + lane];
+                        order[(m - 1) * NC + lane] = fs;
+                        fs = ev;
+                    }
+                }
+            }
+            for (int d = 0; d < D; ++d) { thp[d * NC + lane] = th[d * NC + lane]; gp[d * NC + lane] = g[d * NC + lane]; }
+            // ---- two-loop recursion per seed (Alg. 6)
+            float q[16], al[32];
+            for (int d = 0; d < D; ++d) q[d] = g[d * NC + lane];
+            for (int i = cnt - 1; i >= 0; --i) {
+                const int sl = order[i * NC + lane];
+                float ai = 0.f;
+                for (int d = 0; d < D; ++d) ai += Sb[sl * DC + d * NC + lane] * q[d];
+                ai *= rho[sl * NC + lane];
+                al[i] = ai;
+                for (int d = 0; d < D; ++d) q[d] -= ai * Yb[sl * DC + d * NC + lane];
+            }
+            float gamma = 1.f;
+            if (cnt > 0) { const int sl = order[(cnt - 1) * NC + lane]; gamma = syv[sl * NC + lane] / yyv[sl * NC + lane]; }
+            for (int d = 0; d < D; ++d) q[d] *= gamma;
+            for (int i = 0; i < cnt; ++i) {
+                const int sl = order[i * NC + lane];
+                float bi = 0.f;
+                for (int d = 0; d < D; ++d) bi += Yb[sl * DC + d * NC + lane] * q[d];
+                bi *= rho[sl * NC + lane];
+                for (int d = 0; d < D; ++d) q[d] += (al[i] - bi) * Sb[sl * DC + d * NC + lane];
+            }
+            g0d = 0.f;
+            for (int d = 0; d < D; ++d) { dd[d * NC + lane] = -q[d]; g0d += g[d * NC + lane] * (-q[d]); }
+        }
+        if (a >= 0) {
+            __syncthreads();               // the L-BFGS step (warp 0) wrote the directions
+            for (int idx = t; idx < DC; idx += NT) {   // all threads: candidate + its sin / cos
+                const int d = idx / NC;
+                const float v = candidate(th[idx], kp.alpha[a], dd[idx], lim[d], lim[D + d]);
+                s.q_cfg[idx] = v;
+                float sn, cs;
+                sincosf(v, &sn, &cs);
+                s.scs[idx] = sn;
+                s.scs[DC + idx] = cs;
+            }
+        }
+        eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
+        if (part) {
+            // ---- f1 UPDATE, streamed over the particles (Eqs. particle_1/2, B6), per seed
+            float r;
+            const float w = pacc.add(s.cfg_cost[t & 31], kp.p_inv_beta, r);
+            if (t < DC) {
+                const float x = s.q_cfg[t], dx = x - th[t];
+                dd[t] = (pl == 0 ? 0.f : dd[t] * r) + w * x;
+                thp[t] = (pl == 0 ? 0.f : thp[t] * r) + w * dx * dx;
+            }
+            if (pl == kp.pn - 1) {
+                if (t < DC) {
+                    if (pacc.Z > 0.f) {
+                        const float iz = 1.f / pacc.Z;
+                        th[t] = (1.f - kp.k_mu) * th[t] + kp.k_mu * (dd[t] * iz);
+                        g[t] = (1.f - kp.k_sigma) * g[t] + kp.k_sigma * (thp[t] * iz);
+                    }
+                    if (pass == npart - 1) {   // Theta_0 of L-BFGS = mu
+                        const float v = th[t];
+                        s.q_cfg[t] = v;
+                        float sn, cs;
+                        sincosf(v, &sn, &cs);
+                        s.scs[t] = sn;
+                        s.scs[DC + t] = cs;
+                    }
+                }
+                pacc.reset();
+            }
+            continue;
+        }
+        if (a < 0) {
+            if (warp != 0) continue;
+            c = s.cfg_cost[lane];
+            cbest = c;
+            for (int d = 0; d < D; ++d) { g[d * NC + lane] = s.gV[d * NC + lane]; best[d * NC + lane] = th[d * NC + lane]; }
+            continue;
+        }
+        // ---- publish this CTA's candidate (per seed), then a11 over all of them (DSMEM)
+        if (warp == 0) {
+            float gd = 0.f;
+            for (int d = 0; d < D; ++d) gd += s.gV[d * NC + lane] * dd[d * NC + lane];
+            cc[lane] = s.cfg_cost[lane];
+            cgd[lane] = gd;
+        }
+        cluster.sync();
+        if (warp == 0) {
+            float ca[8], gda[8];
+            for (int k = 0; k < A; ++k) {
+                ca[k] = cluster.map_shared_rank(cc, k)[lane];
+                gda[k] = cluster.map_shared_rank(cgd, k)[lane];
+            }
+            const int i = ls_select(A, kp.alpha, c, g0d, ca, gda, kp.c1, kp.c2, kp.ls_mode);
+            const float *gsrc = cluster.map_shared_rank(s.gV, i);
+            for (int d = 0; d < D; ++d) {
+                const int e = d * NC + lane;
+                th[e] = candidate(th[e], kp.alpha[i], dd[e], lim[d], lim[D + d]);
+                g[e] = gsrc[e];
+            }
+            c = ca[i];
+            if (c < cbest) {
+                cbest = c;
+                for (int d = 0; d < D; ++d) best[d * NC + lane] = th[d * NC + lane];
+            }
+        }
+        cluster.sync();                        // peers have read this CTA's candidate
+    }
+    __syncthreads();
+    if (rank == 0 && warp == 0 && active) {
         const size_t u = (size_t)p * kp.S + sd;
         kp.seed_best_cost[u] = cbest;
         for (int d = 0; d < D; ++d) kp.seed_best_traj[u * D + d] = best[d * NC + lane];
@@ -977,6 +1394,7 @@ struct crb_ctx {
     int kpairs = 1;                       // pairs per environment in d_boxes_h2
     int *d_box_count = nullptr;
     int n_env = 0, kmax = 0, kmax_enabled = 0;
+    int sm_count = 148;
     // params
     bool params_ok = false;
     crb_cost_params cp{};
@@ -1140,6 +1558,7 @@ crb_status crb_create(int cuda_device, crb_ctx **out) {
     crb_ctx *c = new crb_ctx();
     c->device = cuda_device;
     if (cudaSetDevice(cuda_device) != cudaSuccess) { delete c; return CRB_E_CUDA; }
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
     *out = c;
     return CRB_OK;
 }
@@ -1563,8 +1982,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
                                     !(sp->k_mu <= 1.f) || !(sp->k_sigma >= 0.f) || !(sp->k_sigma <= 1.f) ||
                                     !(sp->sigma0_frac >= 0.f))))
         return fail(ctx, CRB_E_ARG, "particle warm-up: iters >= 0, n >= 1, beta > 0, k_mu/k_sigma in [0,1], sigma0_frac >= 0");
-    if (sp->check_every < 0 || !(sp->conv_rtol >= 0.f))
-        return fail(ctx, CRB_E_ARG, "check_every >= 0 and conv_rtol >= 0");
+    if (sp->check_every < 0 || !(sp->conv_rtol >= 0.f) || sp->cluster < -1 || sp->cluster > 1)
+        return fail(ctx, CRB_E_ARG, "check_every >= 0, conv_rtol >= 0, cluster in {-1, 0, 1}");
     const int mode = H == 1 ? MODE_IK : MODE_TO;
     const int D = ctx->rp.D;
     if (mode == MODE_TO && (H < 8 || H > 32 || H * D > 512 || !start))
@@ -1590,7 +2009,32 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids + solver)");
     const bool wm = use_world_mma(ctx);
-    if (mode == MODE_TO)
+    // latency mode: A CTAs per seed in a cluster when the whole batch fits one wave (2 CTAs / SM)
+    const long long units = mode == MODE_TO ? (long long)P * S : (long long)P * ((S + NC - 1) / NC);
+    const bool clus = sp->n_alpha >= 2 &&
+                      (sp->cluster == 1 || (sp->cluster == -1 && units * sp->n_alpha <= 2LL * ctx->sm_count));
+    if (clus && units > 0) {
+        auto kern = mode == MODE_TO ? (wm ? solve_to_cluster_kernel<true> : solve_to_cluster_kernel<false>)
+                                    : (wm ? solve_ik_cluster_kernel<true> : solve_ik_cluster_kernel<false>);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return cuda_check(ctx, e, "solve_cluster_kernel");
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(units * sp->n_alpha));
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = bytes;
+        cfg.stream = stream_;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)sp->n_alpha;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, kp);
+        ctx->launches++;
+        if (e != cudaSuccess) return cuda_check(ctx, e, "solve_cluster_kernel");
+        st = cuda_check(ctx, cudaGetLastError(), "solve_cluster_kernel");
+    } else if (mode == MODE_TO)
         st = launch(ctx, wm ? solve_to_kernel<true> : solve_to_kernel<false>, P * S, bytes, stream_, kp, "solve_to_kernel");
     else
         st = launch(ctx, wm ? solve_ik_kernel<true> : solve_ik_kernel<false>, P * ((S + NC - 1) / NC), bytes, stream_,

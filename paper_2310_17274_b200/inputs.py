@@ -122,6 +122,9 @@ class SolverParams:
     # its best cost improved by at most conv_rtol x |best| over a chunk (reading B20); 0 = off
     check_every: int = 0
     conv_rtol: float = 0.0
+    # latency mode: the line-search candidates of an iteration on the CTAs of a cluster
+    # (-1 automatic for batches that fit one wave, 0 off, 1 on); bitwise identical results
+    cluster: int = -1
 
 
 # --------------------------------------------------------------------------------------------

@@ -67,7 +67,7 @@ class crb_solver_params(C.Structure):
                 ("particle_iters", C.c_int), ("n_particles", C.c_int), ("particle_beta", C.c_float),
                 ("k_mu", C.c_float), ("k_sigma", C.c_float), ("sigma0_frac", C.c_float),
                 ("rng_key", C.c_uint32), ("global_problem_base", C.c_int64), ("check_every", C.c_int),
-                ("conv_rtol", C.c_float)]
+                ("conv_rtol", C.c_float), ("cluster", C.c_int)]
 
 
 _V = C.c_void_p
@@ -146,7 +146,7 @@ def solver_params_struct(sp: inputs.SolverParams, seed_base: int = 0, problem_ba
                              float(sp.c2), int(sp.ls_mode), int(seed_base), int(sp.particle_iters),
                              int(sp.n_particles), float(sp.particle_beta), float(sp.k_mu), float(sp.k_sigma),
                              float(sp.sigma0_frac), int(sp.rng_key) & 0xFFFFFFFF, int(problem_base),
-                             int(sp.check_every), float(sp.conv_rtol))
+                             int(sp.check_every), float(sp.conv_rtol), int(sp.cluster))
 
 
 class Context:

@@ -613,3 +613,49 @@ def test_solve_to_chunked_convergence_exit(native, O):
         stopped += k_stop < 150
     assert stopped > 0          # the rule fired for some seeds
     ctx.close()
+
+
+@pytest.mark.parametrize("variant", ["default", "particles", "chunked", "gd_a2", "armijo_a8"])
+def test_solve_to_cluster_mode_bitwise(native, O, variant):
+    """Latency mode (the line-search candidates of an iteration on the CTAs of a thread-block
+    cluster, DSMEM exchange) against the sequential one-CTA solver: bitwise identical per-seed
+    results, with the particle warm-up, the chunked exit, gradient descent with 2 magnitudes and
+    an 8-magnitude Armijo search."""
+    import dataclasses
+    from paper_2310_17274_b200 import workload
+    wl = workload.franka_to(0, list(range(3)), S=5, H=32, iters=60)
+    sp = wl.solver
+    if variant == "particles":
+        sp = dataclasses.replace(sp, particle_iters=2, n_particles=16)
+    elif variant == "chunked":
+        sp = dataclasses.replace(sp, check_every=10, conv_rtol=0.05)
+    elif variant == "gd_a2":
+        sp = dataclasses.replace(sp, history=0, alpha=(0.01, 0.5))
+    elif variant == "armijo_a8":
+        sp = dataclasses.replace(sp, ls_mode=0, alpha=(0.01, 0.05, 0.1, 0.2, 0.3, 0.5, 0.7, 1.0))
+    ctx = make(native, wl.robot, wl.worlds, wl.cost)
+    args = (T(wl.seeds), T(wl.goal))
+    kw = dict(start=T(wl.start), env=T(wl.env, torch.int32), seed_outputs=True)
+    seq = ctx.solve(dataclasses.replace(sp, cluster=0), *args, **kw)
+    clu = ctx.solve(dataclasses.replace(sp, cluster=1), *args, **kw)
+    for k in ("seed_best_cost", "seed_best_traj", "best_cost", "best_traj", "best_key"):
+        assert torch.equal(seq[k], clu[k]), k
+    ctx.close()
+
+
+@pytest.mark.parametrize("particles", [0, 2])
+def test_solve_ik_cluster_mode_bitwise(native, O, particles):
+    """IK latency mode (candidates on the CTAs of a cluster, per-seed selection from the peers'
+    costs and gradients) against the sequential IK solver: bitwise identical."""
+    import dataclasses
+    from paper_2310_17274_b200 import workload
+    wl = workload.franka_ik(0, list(range(7)), S=30, iters=40)
+    sp = dataclasses.replace(wl.solver, particle_iters=particles, n_particles=16)
+    ctx = make(native, wl.robot, wl.worlds, wl.cost)
+    args = (T(wl.seeds), T(wl.goal))
+    kw = dict(env=T(wl.env, torch.int32), seed_outputs=True)
+    seq = ctx.solve(dataclasses.replace(sp, cluster=0), *args, **kw)
+    clu = ctx.solve(dataclasses.replace(sp, cluster=1), *args, **kw)
+    for k in ("seed_best_cost", "seed_best_traj", "best_cost", "best_traj", "best_key"):
+        assert torch.equal(seq[k], clu[k]), k
+    ctx.close()
