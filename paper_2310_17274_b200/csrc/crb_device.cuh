@@ -376,6 +376,27 @@ struct ParticleAcc {
     }
 };
 
+// The particles of an iteration are accumulated in nch contiguous chunks (nch = the number of
+// line-search magnitudes A when A >= 2, so the latency-mode cluster can give one chunk to each
+// CTA): particles [c n / nch, (c + 1) n / nch) stream into a fresh (m, Z, S1, S2), and the chunks
+// are merged in order c = 0, 1, ... into the total.  chunk_merge gives the factors of that merge,
+// S_total = S_total * ft + S_chunk * fc; an empty chunk (no finite cost) leaves the total as is.
+__device__ __forceinline__ void chunk_merge(float &mt, float &Zt, float mc, float Zc, float &ft, float &fc) {
+    if (!(Zc > 0.f)) { ft = 1.f; fc = 0.f; return; }
+    if (!(Zt > 0.f)) { ft = 0.f; fc = 1.f; mt = mc; Zt = Zc; return; }
+    const float mm = fmaxf(mt, mc);
+    ft = expf(mt - mm);
+    fc = expf(mc - mm);
+    Zt = Zt * ft + Zc * fc;
+    mt = mm;
+}
+
+__device__ __forceinline__ int particle_chunk(int l, int n, int nch) {
+    int c = 0;
+    while (c + 1 < nch && (c + 1) * n / nch <= l) ++c;
+    return c;
+}
+
 // ------------------------------------------------------------------------------------------
 // the fused evaluation pass over 32 configuration slots
 // ------------------------------------------------------------------------------------------

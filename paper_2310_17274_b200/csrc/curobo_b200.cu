@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
     const unsigned pk1 = (unsigned)(kp.prob_base + p), psd = (unsigned)(kp.seed_base + (unit - p * kp.S));
     ParticleAcc pacc;
     pacc.reset();
+    float tm = -INFINITY, tZ = 0.f;   // merged particle chunks of the current warm-up iteration
     if (npart > 0) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -200,7 +201,11 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
         // ---- a2..a10: one evaluation pass (cost only for particles)
         eval_pass<MODE_TO, WMMA>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr, !part);
         if (part) {
-            // ---- f1 UPDATE, streamed over the particles (Eqs. particle_1/2, B6)
+            // ---- f1 UPDATE, streamed over the particles of a chunk (Eqs. particle_1/2, B6), the
+            // chunks merged in order (chunk_merge; totals in cg, unused during the warm-up)
+            const int nch = A >= 2 ? A : 1, ch = particle_chunk(pl, kp.pn, nch);
+            const int clo = ch * kp.pn / nch, chi = (ch + 1) * kp.pn / nch;
+            float *S1t = cg, *S2t = cg + Np;
             float r;
             const float w = pacc.add(s.scal[0], kp.p_inv_beta, r);
 #pragma unroll
@@ -208,20 +213,36 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
                 const int i = t + e * NT;
                 if (i < N) {
                     const float x = thA[i], dx = x - th[i];
-                    dd[i] = (pl == 0 ? 0.f : dd[i] * r) + w * x;
-                    thp[i] = (pl == 0 ? 0.f : thp[i] * r) + w * dx * dx;
+                    dd[i] = (pl == clo ? 0.f : dd[i] * r) + w * x;
+                    thp[i] = (pl == clo ? 0.f : thp[i] * r) + w * dx * dx;
                 }
             }
+            if (pl == chi - 1 && nch > 1) {
+                if (ch == 0) { tm = -INFINITY; tZ = 0.f; }
+                float ft, fc;
+                chunk_merge(tm, tZ, pacc.m, pacc.Z, ft, fc);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = t + e * NT;
+                    if (i < N) {
+                        S1t[i] = (ch == 0 ? 0.f : S1t[i]) * ft + dd[i] * fc;
+                        S2t[i] = (ch == 0 ? 0.f : S2t[i]) * ft + thp[i] * fc;
+                    }
+                }
+                pacc.reset();
+            }
             if (pl == kp.pn - 1) {
-                const bool upd = pacc.Z > 0.f;
-                const float iz = upd ? 1.f / pacc.Z : 0.f;
+                const float Zs = nch > 1 ? tZ : pacc.Z;
+                const float *S1 = nch > 1 ? S1t : dd, *S2 = nch > 1 ? S2t : thp;
+                const bool upd = Zs > 0.f;
+                const float iz = upd ? 1.f / Zs : 0.f;
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int i = t + e * NT;
                     if (i < N) {
                         if (upd) {
-                            th[i] = (1.f - kp.k_mu) * th[i] + kp.k_mu * (dd[i] * iz);
-                            g[i] = (1.f - kp.k_sigma) * g[i] + kp.k_sigma * (thp[i] * iz);
+                            th[i] = (1.f - kp.k_mu) * th[i] + kp.k_mu * (S1[i] * iz);
+                            g[i] = (1.f - kp.k_sigma) * g[i] + kp.k_sigma * (S2[i] * iz);
                         }
                         if (pass == npart - 1) thA[i] = th[i];   // Theta_0 of L-BFGS = mu
                     }
@@ -341,8 +362,12 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
 
     float c = 0.f, cbest = 0.f, g0d = 0.f, chunk_best = 0.f;
     float d_e[2] = {0.f, 0.f};
-    const int npart = kp.pn_iters * kp.pn;
+    // particle warm-up: this CTA evaluates chunk `rank` of every iteration's particles (the
+    // sequential kernel's chunks), the chunks are merged in order through DSMEM
+    const int clo = rank * kp.pn / A, chi = (rank + 1) * kp.pn / A, csz = chi - clo;   // csz >= 1 (host)
+    const int npart = kp.pn_iters * csz;
     const int npass = npart + 1 + kp.iters;   // warm-up, pass 0, then one candidate pass per iteration
+    float tm = -INFINITY, tZ = 0.f;
     const unsigned pk1 = (unsigned)(kp.prob_base + p), psd = (unsigned)(kp.seed_base + (unit - p * kp.S));
     ParticleAcc pacc;
     pacc.reset();
@@ -355,7 +380,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
     }
     for (int pass = 0; pass < npass; ++pass) {
         const bool part = pass < npart;
-        const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
+        const int pit = part ? pass / csz : 0, pl = part ? clo + (pass - pit * csz) : 0;
         const int lpass = pass - npart;        // 0: Theta_0, it + 1: iteration it
         if (part) {
 #pragma unroll
@@ -429,20 +454,40 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
                 const int i = t + e * NT;
                 if (i < N) {
                     const float x = thA[i], dx = x - th[i];
-                    dd[i] = (pl == 0 ? 0.f : dd[i] * r) + w * x;
-                    thp[i] = (pl == 0 ? 0.f : thp[i] * r) + w * dx * dx;
+                    dd[i] = (pl == clo ? 0.f : dd[i] * r) + w * x;
+                    thp[i] = (pl == clo ? 0.f : thp[i] * r) + w * dx * dx;
                 }
             }
-            if (pl == kp.pn - 1) {
-                const bool upd = pacc.Z > 0.f;
-                const float iz = upd ? 1.f / pacc.Z : 0.f;
+            if (pl == chi - 1) {
+                // publish this chunk, merge all chunks in order (identical in every CTA)
+                if (t == 0) { scal[0] = pacc.m; scal[1] = pacc.Z; }
+                cluster.sync();
+                float *S1t = cg_, *S2t = cg_ + Np;
+                tm = -INFINITY; tZ = 0.f;
+                for (int c = 0; c < A; ++c) {
+                    const float *pc = cluster.map_shared_rank(scal, c);
+                    const float *pd = cluster.map_shared_rank(dd, c), *pq = cluster.map_shared_rank(thp, c);
+                    float ft, fc;
+                    chunk_merge(tm, tZ, pc[0], pc[1], ft, fc);
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int i = t + e * NT;
+                        if (i < N) {
+                            S1t[i] = (c == 0 ? 0.f : S1t[i]) * ft + pd[i] * fc;
+                            S2t[i] = (c == 0 ? 0.f : S2t[i]) * ft + pq[i] * fc;
+                        }
+                    }
+                }
+                cluster.sync();                // peers have read this chunk before it is overwritten
+                const bool upd = tZ > 0.f;
+                const float iz = upd ? 1.f / tZ : 0.f;
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int i = t + e * NT;
                     if (i < N) {
                         if (upd) {
-                            th[i] = (1.f - kp.k_mu) * th[i] + kp.k_mu * (dd[i] * iz);
-                            g[i] = (1.f - kp.k_sigma) * g[i] + kp.k_sigma * (thp[i] * iz);
+                            th[i] = (1.f - kp.k_mu) * th[i] + kp.k_mu * (S1t[i] * iz);
+                            g[i] = (1.f - kp.k_sigma) * g[i] + kp.k_sigma * (S2t[i] * iz);
                         }
                         if (pass == npart - 1) thA[i] = th[i];
                     }
@@ -550,6 +595,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
     const unsigned psd = (unsigned)(kp.seed_base + grp * NC + (t & 31));
     ParticleAcc pacc;
     pacc.reset();
+    float tm = -INFINITY, tZ = 0.f;   // merged particle chunks of the current warm-up iteration
     if (npart > 0 && t < DC) {
         const int d = t / NC;
         const float s0 = kp.s0_frac * (lim[D + d] - lim[d]);   // B8
@@ -632,20 +678,36 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
         }
         eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
         if (part) {
-            // ---- f1 UPDATE, streamed over the particles (Eqs. particle_1/2, B6), per seed
+            // ---- f1 UPDATE, streamed over the particles of a chunk (Eqs. particle_1/2, B6), per
+            // seed; the chunks merged in order (chunk_merge; totals in cg, unused during the warm-up)
+            const int nch = A >= 2 ? A : 1, ch = particle_chunk(pl, kp.pn, nch);
+            const int clo = ch * kp.pn / nch, chi = (ch + 1) * kp.pn / nch;
+            float *S1t = cg, *S2t = cg + DC;
             float r;
             const float w = pacc.add(s.cfg_cost[t & 31], kp.p_inv_beta, r);
             if (t < DC) {
                 const float x = s.q_cfg[t], dx = x - th[t];
-                dd[t] = (pl == 0 ? 0.f : dd[t] * r) + w * x;
-                thp[t] = (pl == 0 ? 0.f : thp[t] * r) + w * dx * dx;
+                dd[t] = (pl == clo ? 0.f : dd[t] * r) + w * x;
+                thp[t] = (pl == clo ? 0.f : thp[t] * r) + w * dx * dx;
+            }
+            if (pl == chi - 1 && nch > 1) {
+                if (ch == 0) { tm = -INFINITY; tZ = 0.f; }
+                float ft, fc;
+                chunk_merge(tm, tZ, pacc.m, pacc.Z, ft, fc);
+                if (t < DC) {
+                    S1t[t] = (ch == 0 ? 0.f : S1t[t]) * ft + dd[t] * fc;
+                    S2t[t] = (ch == 0 ? 0.f : S2t[t]) * ft + thp[t] * fc;
+                }
+                pacc.reset();
             }
             if (pl == kp.pn - 1) {
                 if (t < DC) {
-                    if (pacc.Z > 0.f) {
-                        const float iz = 1.f / pacc.Z;
-                        th[t] = (1.f - kp.k_mu) * th[t] + kp.k_mu * (dd[t] * iz);
-                        g[t] = (1.f - kp.k_sigma) * g[t] + kp.k_sigma * (thp[t] * iz);
+                    const float Zs = nch > 1 ? tZ : pacc.Z;
+                    const float *S1 = nch > 1 ? S1t : dd, *S2 = nch > 1 ? S2t : thp;
+                    if (Zs > 0.f) {
+                        const float iz = 1.f / Zs;
+                        th[t] = (1.f - kp.k_mu) * th[t] + kp.k_mu * (S1[t] * iz);
+                        g[t] = (1.f - kp.k_sigma) * g[t] + kp.k_sigma * (S2[t] * iz);
                     }
                     if (pass == npart - 1) {   // Theta_0 of L-BFGS = mu
                         const float v = th[t];
@@ -739,8 +801,11 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
     // Theta_0 and (L-BFGS step, A candidates) per iteration
     float c = 0.f, cbest = 0.f, g0d = 0.f;
     int cnt = 0, fs = 0;
-    const int npart = kp.pn_iters * kp.pn;
+    // particle warm-up: this CTA evaluates chunk `rank` of every iteration's particles
+    const int clo = rank * kp.pn / A, chi = (rank + 1) * kp.pn / A, csz = chi - clo;   // csz >= 1 (host)
+    const int npart = kp.pn_iters * csz;
     const int npass = npart + 1 + kp.iters;   // one candidate pass per iteration (this CTA's rank)
+    float tm = -INFINITY, tZ = 0.f;
     const unsigned pk1 = (unsigned)(kp.prob_base + p);
     const unsigned psd = (unsigned)(kp.seed_base + grp * NC + (t & 31));
     ParticleAcc pacc;
@@ -752,7 +817,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
     }
     for (int pass = 0; pass < npass; ++pass) {
         const bool part = pass < npart;
-        const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
+        const int pit = part ? pass / csz : 0, pl = part ? clo + (pass - pit * csz) : 0;
         const int lpass = pass - npart;
         const int a = part ? -2 : (lpass == 0 ? -1 : rank);
         if (part && t < DC) {
@@ -827,15 +892,34 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
         }
         eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
         if (part) {
-            // ---- f1 UPDATE, streamed over the particles (Eqs. particle_1/2, B6), per seed
+            // ---- f1 UPDATE over this CTA's chunk, then all chunks merged in order (DSMEM)
             float r;
             const float w = pacc.add(s.cfg_cost[t & 31], kp.p_inv_beta, r);
             if (t < DC) {
                 const float x = s.q_cfg[t], dx = x - th[t];
-                dd[t] = (pl == 0 ? 0.f : dd[t] * r) + w * x;
-                thp[t] = (pl == 0 ? 0.f : thp[t] * r) + w * dx * dx;
+                dd[t] = (pl == clo ? 0.f : dd[t] * r) + w * x;
+                thp[t] = (pl == clo ? 0.f : thp[t] * r) + w * dx * dx;
             }
-            if (pl == kp.pn - 1) {
+            if (pl == chi - 1) {
+                if (t < NC) { cc[t] = pacc.m; cgd[t] = pacc.Z; }   // this chunk's per-seed (m, Z)
+                cluster.sync();
+                float *S1t = cg, *S2t = cg + DC;
+                tm = -INFINITY; tZ = 0.f;
+                for (int c = 0; c < A; ++c) {
+                    const float mc = cluster.map_shared_rank(cc, c)[t & 31], Zc = cluster.map_shared_rank(cgd, c)[t & 31];
+                    float ft, fc;
+                    chunk_merge(tm, tZ, mc, Zc, ft, fc);
+                    if (t < DC) {
+                        const float *pd = cluster.map_shared_rank(dd, c), *pq = cluster.map_shared_rank(thp, c);
+                        S1t[t] = (c == 0 ? 0.f : S1t[t]) * ft + pd[t] * fc;
+                        S2t[t] = (c == 0 ? 0.f : S2t[t]) * ft + pq[t] * fc;
+                    }
+                }
+                cluster.sync();                // peers have read this chunk before it is overwritten
+                pacc.m = tm; pacc.Z = tZ;      // the merged totals feed the update below
+                if (t < DC) { dd[t] = S1t[t]; thp[t] = S2t[t]; }
+            }
+            if (pl == chi - 1) {
                 if (t < DC) {
                     if (pacc.Z > 0.f) {
                         const float iz = 1.f / pacc.Z;
@@ -2011,7 +2095,7 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     const bool wm = use_world_mma(ctx);
     // latency mode: A CTAs per seed in a cluster when the whole batch fits one wave (2 CTAs / SM)
     const long long units = mode == MODE_TO ? (long long)P * S : (long long)P * ((S + NC - 1) / NC);
-    const bool clus = sp->n_alpha >= 2 &&
+    const bool clus = sp->n_alpha >= 2 && (sp->particle_iters == 0 || sp->n_particles >= sp->n_alpha) &&
                       (sp->cluster == 1 || (sp->cluster == -1 && units * sp->n_alpha <= 2LL * ctx->sm_count));
     if (clus && units > 0) {
         auto kern = mode == MODE_TO ? (wm ? solve_to_cluster_kernel<true> : solve_to_cluster_kernel<false>)
