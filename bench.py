@@ -319,6 +319,11 @@ def side_metrics(local, rank, world, dev, flush, steps=2):
     out["cfg3_ik"]["with_particles"] = {"particle_iters": 2, "n_particles": 64, "ms_per_solve": msp,
                                         "ik_queries_per_s": n_ik * world / (msp * 1e-3),
                                         "added_ms": msp - ms}
+    # single-query latency (batch size 1, "2.7ms"): the cluster latency mode runs it
+    one = (torch.tensor(wl.seeds[:1], device=dev), torch.tensor(wl.goal[:1], device=dev), None,
+           torch.tensor(wl.env[:1], device=dev))
+    out["cfg3_ik"]["single_query_ms"] = _timed_solves(ctx, wl.solver, *one, steps, flush, 1, dev)
+    out["cfg3_ik"]["single_query_ms_with_particles"] = _timed_solves(ctx, spp, *one, steps, flush, 1, dev)
     ctx.close()
     # f1 on the headline TO workload (config 2 shape): 2 x 64 cost-only particle passes per seed
     # before the same 100 L-BFGS iterations; the paper reports +2 ms for this warm-up
