@@ -69,6 +69,58 @@ __device__ void two_loop_block(int N, int Np, int count, const int *order, const
     if (t1 < N) d[t1] = -r1;
 }
 
+// L-BFGS step of a TO seed by the whole CTA (Alg. 6): push (s, y, rho) of the last
+// move unless s^T y <= 1e-12 (A20), then the two-loop recursion d = -H g; returns g^T d.  One
+// definition for the sequential and the cluster solver (identical arithmetic).
+__device__ __forceinline__ float lbfgs_step_to(int it, int N, int Np, int m, const float *th, const float *g, float *thp,
+                                               float *gp, float *dd, float *Sb, float *Yb, float *rho, float *syv,
+                                               float *yyv, int *order, int *ring, float *red, int &ph, float (&d_e)[2]) {
+    const int t = threadIdx.x;
+    // ---- a13: L-BFGS buffers (Alg. 6 lines 1-5): push (s, y, rho) unless s^T y <= 1e-12 (A20)
+    if (it > 0) {
+        const int fs = ring[1];
+        float sy_p = 0.f, yy_p = 0.f;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            if (i < N) {
+                const float sv = th[i] - thp[i], yv = g[i] - gp[i];
+                Sb[fs * Np + i] = sv; Yb[fs * Np + i] = yv;
+                sy_p += sv * yv; yy_p += yv * yv;
+            }
+        }
+        const float sy = block_sum(sy_p, red, ph);
+        const float yy = block_sum(yy_p, red, ph);
+        if (m > 0 && sy > 1e-12f && t == 0) {   // m = 0: gradient descent
+            rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
+            const int cnt = ring[0];
+            if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
+            else {
+                const int ev = order[0];
+                for (int i = 0; i < m - 1; ++i) order[i] = order[i + 1];
+                order[m - 1] = fs;
+                ring[1] = ev;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int i = t + e * NT;
+        if (i < N) { thp[i] = th[i]; gp[i] = g[i]; }
+    }
+    // ---- two-loop recursion -> d = -H g
+    two_loop_block(N, Np, ring[0], order, Sb, Yb, rho, syv, yyv, g, dd, red, ph);
+    float gd_p = 0.f;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int i = t + e * NT;
+        d_e[e] = i < N ? dd[i] : 0.f;
+        if (i < N) gd_p += g[i] * d_e[e];
+    }
+    return block_sum(gd_p, red, ph);   // also publishes dd to every thread
+}
+
 // ------------------------------------------------------------------------------------------
 // persistent TO solver: one CTA per (problem, seed)
 // ------------------------------------------------------------------------------------------
@@ -145,49 +197,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
         }
         if (a == 0) {
             const int it = (lpass - 1) / A;
-            // ---- a13: L-BFGS buffers (Alg. 6 lines 1-5): push (s, y, rho) unless s^T y <= 1e-12 (A20)
-            if (it > 0) {
-                const int fs = ring[1];
-                float sy_p = 0.f, yy_p = 0.f;
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int i = t + e * NT;
-                    if (i < N) {
-                        const float sv = th[i] - thp[i], yv = g[i] - gp[i];
-                        Sb[fs * Np + i] = sv; Yb[fs * Np + i] = yv;
-                        sy_p += sv * yv; yy_p += yv * yv;
-                    }
-                }
-                const float sy = block_sum(sy_p, s.red, ph);
-                const float yy = block_sum(yy_p, s.red, ph);
-                if (m > 0 && sy > 1e-12f && t == 0) {   // m = 0: gradient descent
-                    rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
-                    const int cnt = ring[0];
-                    if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
-                    else {
-                        const int ev = order[0];
-                        for (int i = 0; i < m - 1; ++i) order[i] = order[i + 1];
-                        order[m - 1] = fs;
-                        ring[1] = ev;
-                    }
-                }
-                __syncthreads();
-            }
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int i = t + e * NT;
-                if (i < N) { thp[i] = th[i]; gp[i] = g[i]; }
-            }
-            // ---- two-loop recursion -> d = -H g
-            two_loop_block(N, Np, ring[0], order, Sb, Yb, rho, syv, yyv, g, dd, s.red, ph);
-            float gd_p = 0.f;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int i = t + e * NT;
-                d_e[e] = i < N ? dd[i] : 0.f;
-                if (i < N) gd_p += g[i] * d_e[e];
-            }
-            g0d = block_sum(gd_p, s.red, ph);   // also publishes dd to every thread
+            g0d = lbfgs_step_to(it, N, Np, m, th, g, thp, gp, dd, Sb, Yb, rho, syv, yyv, order, ring, s.red, ph, d_e);
         }
         // ---- a1: candidate a = clip(theta + alpha_a d) (pass 0: theta_0 is already in thA)
         if (a >= 0) {
@@ -396,47 +406,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
         if (lpass > 0) {
             const int it = lpass - 1;
             // ---- a13 (identical in every CTA of the cluster)
-            if (it > 0) {
-                const int fs = ring[1];
-                float sy_p = 0.f, yy_p = 0.f;
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int i = t + e * NT;
-                    if (i < N) {
-                        const float sv = th[i] - thp[i], yv = g[i] - gp[i];
-                        Sb[fs * Np + i] = sv; Yb[fs * Np + i] = yv;
-                        sy_p += sv * yv; yy_p += yv * yv;
-                    }
-                }
-                const float sy = block_sum(sy_p, s.red, ph);
-                const float yy = block_sum(yy_p, s.red, ph);
-                if (m > 0 && sy > 1e-12f && t == 0) {
-                    rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
-                    const int cnt = ring[0];
-                    if (cnt < m) { order[cnt] = fs; ring[0] = cnt + 1; ring[1] = cnt + 1; }
-                    else {
-                        const int ev = order[0];
-                        for (int i = 0; i < m - 1; ++i) order[i] = order[i + 1];
-                        order[m - 1] = fs;
-                        ring[1] = ev;
-                    }
-                }
-                __syncthreads();
-            }
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int i = t + e * NT;
-                if (i < N) { thp[i] = th[i]; gp[i] = g[i]; }
-            }
-            two_loop_block(N, Np, ring[0], order, Sb, Yb, rho, syv, yyv, g, dd, s.red, ph);
-            float gd_p = 0.f;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int i = t + e * NT;
-                d_e[e] = i < N ? dd[i] : 0.f;
-                if (i < N) gd_p += g[i] * d_e[e];
-            }
-            g0d = block_sum(gd_p, s.red, ph);
+            g0d = lbfgs_step_to(it, N, Np, m, th, g, thp, gp, dd, Sb, Yb, rho, syv, yyv, order, ring, s.red, ph, d_e);
             // ---- a1: this CTA's candidate
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
