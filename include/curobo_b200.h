@@ -142,8 +142,9 @@ typedef struct {
     /* Latency mode: the n_alpha line-search candidates of each iteration are evaluated in
      * parallel by the n_alpha CTAs of a thread-block cluster (DSMEM exchange of the candidates'
      * costs and the winner's gradient) instead of one after the other by one CTA; results are
-     * bitwise identical.  -1 = automatic (when the batch's CTAs x n_alpha fit in one wave of two
-     * CTAs per SM), 0 = off, 1 = on.  TO and IK solves. */
+     * bitwise identical.  -1 = automatic (the batch's CTAs x n_alpha fit in one wave of two CTAs
+     * per SM; or a particle warm-up on at most 3 waves; or a better-filled last wave), 0 = off,
+     * 1 = on.  TO and IK solves. */
     int cluster;
 } crb_solver_params;
 

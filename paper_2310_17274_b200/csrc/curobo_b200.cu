@@ -2065,8 +2065,16 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     const bool wm = use_world_mma(ctx);
     // latency mode: A CTAs per seed in a cluster when the whole batch fits one wave (2 CTAs / SM)
     const long long units = mode == MODE_TO ? (long long)P * S : (long long)P * ((S + NC - 1) / NC);
+    // automatic choice (tools/cluster_vs_seq.py): the batch fits one wave in cluster mode; or the
+    // particle warm-up (split A ways, not repeated) runs on at most 3 waves of units; or the
+    // predicted wave count, ceil(A units / W) / A with ~15 % cluster overhead, beats the
+    // sequential one by 5 % (a poorly filled last wave).  W = two CTAs per SM.
+    const long long W = 2LL * ctx->sm_count, A_ = sp->n_alpha;
+    const bool fits = units * A_ <= W;
+    const bool parts = sp->particle_iters > 0 && units <= 3 * W;
+    const bool waves = (double)((units * A_ + W - 1) / W) / (double)A_ * 1.15 < 0.95 * (double)((units + W - 1) / W);
     const bool clus = sp->n_alpha >= 2 && (sp->particle_iters == 0 || sp->n_particles >= sp->n_alpha) &&
-                      (sp->cluster == 1 || (sp->cluster == -1 && units * sp->n_alpha <= 2LL * ctx->sm_count));
+                      (sp->cluster == 1 || (sp->cluster == -1 && (fits || parts || waves)));
     if (clus && units > 0) {
         auto kern = mode == MODE_TO ? (wm ? solve_to_cluster_kernel<true> : solve_to_cluster_kernel<false>)
                                     : (wm ? solve_ik_cluster_kernel<true> : solve_ik_cluster_kernel<false>);
