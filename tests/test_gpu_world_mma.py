@@ -169,3 +169,65 @@ def test_fp16x2_screen_far_and_huge_cuboids_against_oracle(native, O):
         assert t_ref[4] > 0
     stats.done(0.5)        # deep inside the huge cuboid: many nearest-face ties (margin exclusions)
     ctx.close()
+
+
+def _random_robot(seed, n_links=9, n_spheres=23):
+    """A random tree (every Table 6 joint type, fixed links in the middle of the chain), an odd
+    sphere count, 3 disabled spheres, a random pair list: the general paths of the kernels."""
+    from test_oracle_kinematics import random_chain
+    rb = random_chain(seed, n_links, n_spheres)
+    g = np.random.default_rng(seed + 1)
+    sph = rb.spheres.copy()
+    sph[:, 3] = g.uniform(0.03, 0.09, n_spheres)
+    sph[[2, 9, 17], 3] = -1.0                                    # disabled (P:2842)
+    pairs = [(i, j) for i in range(n_spheres) for j in range(i + 1, n_spheres) if g.random() < 0.35]
+    import dataclasses
+    D = rb.n_dof
+    return dataclasses.replace(rb, spheres=sph, pairs=np.array(pairs, np.int32), lo=-np.ones(D) * 2.5,
+                               hi=np.ones(D) * 2.5, vmax=np.ones(D) * 2.0, amax=np.ones(D) * 15.0,
+                               jmax=np.ones(D) * 500.0)
+
+
+@pytest.mark.parametrize("seed,big", [(3, False), (4, False), (5, True)])
+def test_random_robot_eval_parity_both_builds(native, O, seed, big):
+    """Random robots (prismatic and revolute x/y/z joints, folded fixed links, 23 spheres of which
+    3 disabled, random self pairs) through the TO and IK evaluations against the oracle, in the
+    fp16x2 build (K = 30) and the HMMA build (an extra 70-cuboid environment), plus an empty
+    environment."""
+    rb = _random_robot(seed)
+    D, H, B = rb.n_dof, 16, 12
+    g = np.random.default_rng(seed)
+    worlds = [inputs.random_world(20 + seed, 0, 30, lo=-0.9, hi=0.9, dmax=0.3),
+              inputs.World(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros(0, np.int32))]
+    if big:
+        worlds.append(inputs.random_world(30 + seed, 0, 70, lo=-0.9, hi=0.9, dmax=0.2, disabled_frac=0.0))
+    cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED | inputs.JERK, dt=0.1)
+    ctx = make(native, rb, worlds, cp)
+    R = O.Robot(rb)
+    Ws = [O.World(w) for w in worlds]
+    V = f32(g.uniform(-1.5, 1.5, (B, H, D)))
+    st = f32(g.uniform(-1.0, 1.0, (B, D)))
+    gl = f32(np.array([O.fk(R, g.uniform(-1, 1, D))[2] for _ in range(B)]))
+    env = (np.arange(B) % len(worlds)).astype(np.int32)
+    cost, grad, terms = ctx.evaluate(T(V), T(gl), start=T(st), env=T(env, torch.int32))
+    cost, grad, terms = cost.cpu().numpy(), grad.cpu().numpy(), terms.cpu().numpy()
+    stats = Stats()
+    active_w = active_s = 0
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"rand TO {b}")
+        active_w += t_ref[4] > 0
+        active_s += t_ref[3] > 0
+    stats.done(0.34)
+    assert active_w >= 2 and active_s >= 2
+    # IK mode (one configuration per row, all in the first environment)
+    Q = f32(g.uniform(-1.5, 1.5, (40, D)))
+    glq = f32(np.repeat(gl[:1], 40, 0))
+    cq, gq, _ = ctx.evaluate(T(Q), T(glq), env=T(np.zeros(40, np.int32), torch.int32))
+    cq, gq = cq.cpu().numpy(), gq.cpu().numpy()
+    stats = Stats()
+    for b in range(40):
+        c_ref, g_ref, _, margin, _ = O.eval_ik(R, Ws[0], cp, glq[b], Q[b])
+        stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, margin, f"rand IK {b}")
+    stats.done(0.34)
+    ctx.close()
