@@ -60,6 +60,9 @@ def run(name, wl):
     print(f"   queue: world item {s[4] / max(s[8], 1):.0f} cyc x {s[8] / wp * 8:.1f}/pass, self item "
           f"{s[5] / max(s[9], 1):.0f} cyc x {s[9] / wp * 8:.1f}/pass; per warp-pass: in queue {s[7] / wp:.0f} cyc, "
           f"barrier wait {s[6] / wp:.0f} cyc", flush=True)
+    fp = max(s[12], 1)
+    print(f"   FK chain {s[11] / fp:.0f} cyc per pass, warp 0 waits {s[13] / fp:.0f} cyc at the placement barrier",
+          flush=True)
 
 
 P = args.problems
