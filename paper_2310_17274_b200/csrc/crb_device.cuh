@@ -795,8 +795,14 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     }
 
     // ---- a3: forward kinematics: the last three warps walk the chain (after this, lt is dead and holds sg)
+#if CRB_STATS
+    const long long t_fk0 = clock64();
+#endif
     if (warp >= FK_W0) {
         fk_chain(rp, s);
+#if CRB_STATS
+        if (warp == FK_W0) { CRB_STAT(11, clock64() - t_fk0); CRB_STAT(12, 1); }
+#endif
     } else {
         // ---- a8 runs on warps 0..FK_W0-1 while the last three walk the kinematic chain (it needs only xs / q)
         //      a8: bound (Eq. bound_cost) on pos/vel/acc/jerk and smoothness (Eq. smooth_cost)
@@ -832,7 +838,13 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             if (MODE == MODE_TO) { s.gva[idx] = gv; s.gva[D * NC + idx] = ga; s.gva[2 * D * NC + idx] = gj; }
         }
     }
+#if CRB_STATS
+    const long long t_a8 = clock64();
+#endif
     __syncthreads();
+#if CRB_STATS
+    if (warp == 0) { CRB_STAT(13, clock64() - t_a8); }
+#endif
     fk_place(rp, s);
     __syncthreads();
 
