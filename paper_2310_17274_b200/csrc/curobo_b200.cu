@@ -1347,7 +1347,6 @@ __global__ void select_kernel(int P, int S, int N, const float *seed_cost, const
                               long long seed_base, float *best_traj, float *best_cost, long long *best_key) {
     const int p = blockIdx.x;
     __shared__ int sbest;
-    __shared__ unsigned long long skey;
     if (threadIdx.x == 0) {
         unsigned long long k = ~0ull;
         int bi = 0;
@@ -1355,7 +1354,7 @@ __global__ void select_kernel(int P, int S, int N, const float *seed_cost, const
             const unsigned long long ks = pack_key(seed_cost[(size_t)p * S + s], seed_base + s);
             if (ks < k) { k = ks; bi = s; }
         }
-        sbest = bi; skey = k;
+        sbest = bi;
         if (best_cost) best_cost[p] = seed_cost[(size_t)p * S + bi];
         if (best_key) best_key[p] = (long long)k;
     }
