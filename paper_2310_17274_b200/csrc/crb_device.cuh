@@ -987,6 +987,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         if (r >= 0.f && spd != 0.f) th2[u] = fmaxf(rpr * rpr, maxb2);
                     }
                 }
+                __syncwarp();   // the zeroed accumulators are visible to the lanes that flush into them
                 // exact fp32 test of cuboid k for the group (the screen of record)
                 auto exact_box = [&](int k, bool reload) {
                         const BoxView b = load_box(s.boxes, k);
@@ -1031,6 +1032,9 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                 box_slow(s.sg + m * NC + src, pc, s.boxes, k, c.x, c.y, c.z, box_screen(c.x, c.y, c.z, b),
                                          rpr, dr, cf.eta, cf.inv_eta, cf.sweep_steps);
                             }
+                            // lanes wrote other lanes' accumulators: order those writes before any
+                            // later access to them (the next cuboid's flush, the group's own reads)
+                            __syncwarp();
                         }
                 };
                 if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
