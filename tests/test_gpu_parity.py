@@ -615,7 +615,7 @@ def test_solve_to_chunked_convergence_exit(native, O):
     ctx.close()
 
 
-@pytest.mark.parametrize("variant", ["default", "particles", "chunked", "gd_a2", "armijo_a8"])
+@pytest.mark.parametrize("variant", ["default", "particles", "chunked", "gd_a2", "armijo_a8", "big_world"])
 def test_solve_to_cluster_mode_bitwise(native, O, variant):
     """Latency mode (the line-search candidates of an iteration on the CTAs of a thread-block
     cluster, DSMEM exchange) against the sequential one-CTA solver: bitwise identical per-seed
@@ -623,8 +623,10 @@ def test_solve_to_cluster_mode_bitwise(native, O, variant):
     an 8-magnitude Armijo search."""
     import dataclasses
     from paper_2310_17274_b200 import workload
-    wl = workload.franka_to(0, list(range(3)), S=5, H=32, iters=60)
+    wl = workload.franka_to(0, list(range(3)), S=5, H=32, iters=60, n_boxes=80 if variant == "big_world" else 20)
     sp = wl.solver
+    if variant == "big_world":     # the HMMA build (cuboids in global memory, longest-first world items)
+        sp = dataclasses.replace(sp, particle_iters=1, n_particles=8)
     if variant == "particles":
         sp = dataclasses.replace(sp, particle_iters=2, n_particles=16)
     elif variant == "chunked":
