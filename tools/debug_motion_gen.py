@@ -36,9 +36,9 @@ print("to1 rot_err", re1.view(P, 12).cpu().numpy())
 v1 = ctx.mask_samples(tr1.view(P * 12 * H, D), env=T(wl.env, torch.int32), env_div=12 * H).view(P, 12, H).cpu().numpy()
 print("to1 valid states", v1.sum(2))
 envt = T(wl.env, torch.int32)
-print("start valid", ctx.mask_samples(T(wl.start), env=envt).cpu().numpy())
-if hasattr(wl, "goal_cfg") and wl.goal_cfg is not None:
-    print("goal cfg valid", ctx.mask_samples(T(wl.goal_cfg), env=envt).cpu().numpy())
+# mask_samples evaluates 32 rows per CTA against ONE environment (rows of a group share env[row //
+# env_div]): one call per problem here, since every problem has its own scene
+print("start valid", [int(ctx.mask_samples(T(wl.start[p:p + 1]), env=envt[p:p + 1]).item()) for p in range(P)])
 b1 = out["best1"].cpu().numpy().ravel()
 for p in range(P):
     print("p", p, "to1 best state validity", v1[p, b1[p]].astype(int))
