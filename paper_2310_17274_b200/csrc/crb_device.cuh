@@ -1392,6 +1392,24 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         // O3 coefficients: v: (1, -8, 0, 8, -1)/(12 dt), a: (-1, 16, -30, 16, -1)/(12 dt^2),
         // j: (-1, 2, 0, -2, 1)/(2 dt^3) for x_{h-2} .. x_{h+2}
         const float iv = s.tdp[1], ia = s.tdp[2], ij = s.tdp[3];
+        // (1) every state's full gradient gx (x_xi for xi = 4..H+2, the ones that reach a
+        // variable), one per thread, into xs (dead after a8): the aliased end state no longer
+        // makes one lane per dof loop over six states while the others wait
+        for (int idx = tid; idx < D * (H - 1); idx += NT) {
+            const int d = idx / (H - 1), xi = idx - d * (H - 1) + 4;
+            const float *gv = s.gva + d * NC - 1, *ga = gv + D * NC, *gj = ga + D * NC;   // [hp] for hp = 1..H
+            float gx = (xi >= 1 && xi <= H) ? s.gq[d * NC + xi - 1] : 0.f;
+            // x_xi enters the stencil of hp = xi - o with the coefficient of offset o
+            if (xi + 2 <= H) { const int e = xi + 2; gx += iv * gv[e] - ia * ga[e] - ij * gj[e]; }             // o = -2
+            if (xi + 1 >= 1 && xi + 1 <= H) { const int e = xi + 1; gx += -8.f * iv * gv[e] + 16.f * ia * ga[e] + 2.f * ij * gj[e]; }  // o = -1
+            if (xi >= 1 && xi <= H) gx += -30.f * ia * ga[xi];                                             // o = 0
+            if (xi - 1 >= 1 && xi - 1 <= H) { const int e = xi - 1; gx += 8.f * iv * gv[e] + 16.f * ia * ga[e] - 2.f * ij * gj[e]; }   // o = 1
+            if (xi - 2 >= 1) { const int e = xi - 2; gx += -iv * gv[e] - ia * ga[e] + ij * gj[e]; }        // o = 2
+            s.xs[d * XS + xi] = gx;
+        }
+        __syncthreads();
+        // (2) the transposed state map: a free variable takes its state, V_{H-1} the sum of the
+        // aliased states x_{H-3..H} and the pads x_{H+1}, x_{H+2} (in that order), the rest 0
         float gdp = 0.f;
         for (int idx = tid; idx < D * NC; idx += NT) {
             const int d = idx / NC, h = idx - d * NC;   // V_h <-> x_{h+1}
@@ -1401,18 +1419,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             if (hx >= 4 && hx <= H - 4) { xlo = hx; xhi = hx; }
             else if (hx == H) { xlo = H - 3; xhi = H + 2; }
             else { s.gV[h * D + d] = 0.f; continue; }
-            const float *gv = s.gva + d * NC - 1, *ga = gv + D * NC, *gj = ga + D * NC;   // [hp] for hp = 1..H
             float acc = 0.f;
-            for (int xi = xlo; xi <= xhi; ++xi) {
-                float gx = (xi >= 1 && xi <= H) ? s.gq[d * NC + xi - 1] : 0.f;
-                // x_xi enters the stencil of hp = xi - o with the coefficient of offset o
-                if (xi + 2 <= H) { const int e = xi + 2; gx += iv * gv[e] - ia * ga[e] - ij * gj[e]; }             // o = -2
-                if (xi + 1 >= 1 && xi + 1 <= H) { const int e = xi + 1; gx += -8.f * iv * gv[e] + 16.f * ia * ga[e] + 2.f * ij * gj[e]; }  // o = -1
-                if (xi >= 1 && xi <= H) gx += -30.f * ia * ga[xi];                                             // o = 0
-                if (xi - 1 >= 1 && xi - 1 <= H) { const int e = xi - 1; gx += 8.f * iv * gv[e] + 16.f * ia * ga[e] - 2.f * ij * gj[e]; }   // o = 1
-                if (xi - 2 >= 1) { const int e = xi - 2; gx += -iv * gv[e] - ia * ga[e] + ij * gj[e]; }        // o = 2
-                acc += gx;
-            }
+            for (int xi = xlo; xi <= xhi; ++xi) acc += s.xs[d * XS + xi];
             s.gV[h * D + d] = acc;
             if (dvec) gdp += acc * dvec[h * D + d];
         }
