@@ -37,7 +37,7 @@ FFMA_PER_CLK_PER_SM, SMS = 64, 148
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--problems", type=int, default=64, help="problems per GPU (32 seeds each)")
@@ -78,11 +78,19 @@ class ClockSampler:
         self.sm, self.mx, self.reasons = [], [], set()
         self.stop = threading.Event()
         self.th = None
+        self.h = None
+        try:   # NVML set up before the timed region, so polling starts at once
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        except Exception:
+            self.h = None
 
     def _poll_nvml(self):
         import pynvml
-        pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+        if self.h is None:
+            raise RuntimeError("no NVML")
+        h = self.h
         self.mx.append(float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)))
         while not self.stop.is_set():
             self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
