@@ -51,15 +51,14 @@ class Stats:
         self.worst_c = 0.0
         self.worst_g = 0.0
 
-    def check(self, c_gpu, g_gpu, c_ref, g_ref, margin, label, grad_slack=0.0):
-        # grad_slack (converged solutions only): the cost there is an O(n^2) residual of an fp32
-        # position, so its fp32 error is ~ |grad c| x the fp32 rounding of the kinematics (a
-        # config-space equivalent of ~1e-6 m at the end effector), not a fraction of c itself
+    def check(self, c_gpu, g_gpu, c_ref, g_ref, margin, label, cost_slack=0.0):
+        # cost_slack (converged solutions only, reading B19): an absolute allowance for a cost that
+        # is a small residual of fp32 kinematics (see pose_cost_slack)
         self.n += 1
         if margin < MARGIN:
             self.excluded += 1
             return
-        ec = abs(c_gpu - c_ref) / (abs(c_ref) * COST_RTOL + COST_ATOL + grad_slack * np.linalg.norm(g_ref))
+        ec = abs(c_gpu - c_ref) / (abs(c_ref) * COST_RTOL + COST_ATOL + cost_slack)
         eg = np.linalg.norm(g_gpu - g_ref) / (np.linalg.norm(g_ref) * GRAD_RTOL + GRAD_ATOL * np.sqrt(g_ref.size))
         self.worst_c = max(self.worst_c, ec)
         self.worst_g = max(self.worst_g, eg)
@@ -526,6 +525,16 @@ def test_full_size_solve_sampled_against_oracle(native, O):
     ctx.close()
 
 
+def pose_cost_slack(O, R, cp, goal, q, dp=1e-6, dq=1e-6):
+    """Reading B19: at a converged solution the pose term a0 l(a2 n) + a1 l(a3 e_r) is a residual
+    of the fp32 end-effector pose; its fp32 error is its sensitivity to that pose times the fp32
+    rounding of the kinematics (dp ~ 1e-6 m in position, dq ~ 1e-6 in the quaternion metric)."""
+    ee = O.fk(R, q)[2]
+    n = np.linalg.norm(np.asarray(goal[:3]) - ee[:3])
+    er = 1.0 - abs(float(np.dot(goal[3:], ee[3:])))
+    return cp.a0 * cp.a2 * np.tanh(cp.a2 * n) * dp + cp.a1 * cp.a3 * np.tanh(cp.a3 * er) * dq
+
+
 def test_full_size_ik_solve_sampled_against_oracle(native, O):
     """BASELINE configs[2] at the bench size (1000 goals x 30 seeds, shared K = 20 scene, 100
     iterations, IK mode) in the launch configuration bench.py times: for sampled goals the oracle
@@ -542,7 +551,8 @@ def test_full_size_ik_solve_sampled_against_oracle(native, O):
     stats = Stats()
     for p in (0, 1, 257, 511, 768, 999):
         c_ref, g_ref, _, margin, _ = O.eval_ik(R, W, wl.cost, f32(wl.goal[p]), bq[p].reshape(-1))
-        stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"ik winner {p}", grad_slack=2e-6)
+        stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"ik winner {p}",
+                    cost_slack=pose_cost_slack(O, R, wl.cost, f32(wl.goal[p]), bq[p].reshape(-1)))
         assert bc[p] == sbc[p].min()
     stats.done(0.5)
     c0, _, _ = ctx.evaluate(T(wl.seeds.reshape(-1, 7)), T(np.repeat(wl.goal, 30, 0)))
