@@ -228,15 +228,15 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
                 }
             }
             if (pl == chi - 1 && nch > 1) {
-                if (ch == 0) { tm = -INFINITY; tZ = 0.f; }
+                if (clo == 0) { tm = -INFINITY; tZ = 0.f; }   // the iteration's first (non-empty) chunk
                 float ft, fc;
                 chunk_merge(tm, tZ, pacc.m, pacc.Z, ft, fc);
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int i = t + e * NT;
                     if (i < N) {
-                        S1t[i] = (ch == 0 ? 0.f : S1t[i]) * ft + dd[i] * fc;
-                        S2t[i] = (ch == 0 ? 0.f : S2t[i]) * ft + thp[i] * fc;
+                        S1t[i] = (clo == 0 ? 0.f : S1t[i]) * ft + dd[i] * fc;
+                        S2t[i] = (clo == 0 ? 0.f : S2t[i]) * ft + thp[i] * fc;
                     }
                 }
                 pacc.reset();
@@ -661,12 +661,12 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
                 thp[t] = (pl == clo ? 0.f : thp[t] * r) + w * dx * dx;
             }
             if (pl == chi - 1 && nch > 1) {
-                if (ch == 0) { tm = -INFINITY; tZ = 0.f; }
+                if (clo == 0) { tm = -INFINITY; tZ = 0.f; }   // the iteration's first (non-empty) chunk
                 float ft, fc;
                 chunk_merge(tm, tZ, pacc.m, pacc.Z, ft, fc);
                 if (t < DC) {
-                    S1t[t] = (ch == 0 ? 0.f : S1t[t]) * ft + dd[t] * fc;
-                    S2t[t] = (ch == 0 ? 0.f : S2t[t]) * ft + thp[t] * fc;
+                    S1t[t] = (clo == 0 ? 0.f : S1t[t]) * ft + dd[t] * fc;
+                    S2t[t] = (clo == 0 ? 0.f : S2t[t]) * ft + thp[t] * fc;
                 }
                 pacc.reset();
             }

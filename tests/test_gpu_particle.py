@@ -73,8 +73,10 @@ def _to_case(O, P=3, S=4, H=16):
     return rb, R, worlds, env, st, gl, seeds
 
 
-@pytest.mark.parametrize("beta_mode", ["smooth", "onehot"])
-def test_particle_warmup_to_parity(native, O, beta_mode):
+@pytest.mark.parametrize("beta_mode,n_particles", [("smooth", 32), ("onehot", 32), ("smooth", 3)])
+def test_particle_warmup_to_parity(native, O, beta_mode, n_particles):
+    """n_particles = 3 < A = 4: the first of the A accumulation chunks is empty (and the solver
+    runs sequentially: the latency mode needs a particle per CTA)."""
     P, S, H = 3, 4, 16
     rb, R, worlds, env, st, gl, seeds = _to_case(O, P, S, H)
     Ws = [O.World(w) for w in worlds]
@@ -83,7 +85,7 @@ def test_particle_warmup_to_parity(native, O, beta_mode):
     beta = 0.25 * float(np.median(c0)) if beta_mode == "smooth" else 1.0
     # sigma_0 = 0.03 (hi - lo): iid per-step draws at the SPEC's 0.1 put most particles deep in
     # contact, where sweep samples cross their exit bound in nearly every evaluation
-    sp = inputs.SolverParams(iters=0, particle_iters=2, n_particles=32, particle_beta=beta, rng_key=77,
+    sp = inputs.SolverParams(iters=0, particle_iters=2, n_particles=n_particles, particle_beta=beta, rng_key=77,
                              sigma0_frac=0.03)
     ctx = make(native, rb, worlds, cp)
     out = ctx.solve(sp, T(seeds), T(gl), start=T(st), env=T(env, torch.int32), seed_outputs=True,
