@@ -16,6 +16,8 @@
  *   - crb_lbfgs_solve_host takes HOST pointers (pinned memory recommended), performs the
  *     host->device copies, the solve and the device->host copies on `stream`, and synchronises.
  *   - A context is bound to one CUDA device and used by one host thread at a time.
+ *   - An empty batch (B == 0 or P == 0) is validated like any other and returns CRB_OK without a
+ *     launch; its batch pointers may then be NULL.
  *   - Numeric types: all results are fp32 arithmetic (the paper's kernels are fp32).  The
  *     sphere-cuboid screen runs a conservative reduced-precision pre-screen (packed fp16 below 60
  *     enabled cuboids per environment, tensor-core fp16 hi/lo products from 60) that only selects

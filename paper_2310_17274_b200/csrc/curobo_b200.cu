@@ -1974,7 +1974,8 @@ crb_status crb_fk(crb_ctx *ctx, const float *q, int B, float *spheres_out, float
     crb_status st = enter(ctx);
     if (st != CRB_OK) return st;
     if ((st = ready(ctx, false)) != CRB_OK) return st;
-    if (!q || B < 0) return fail(ctx, CRB_E_ARG, "bad fk arguments");
+    if (B < 0 || (B > 0 && !q)) return fail(ctx, CRB_E_ARG, "bad fk arguments");
+    if (B == 0) return CRB_OK;
     KParams kp = base_params(ctx);
     kp.kmax = 0;
     kp.B = B; kp.H = 1; kp.cp.H = 1; kp.mode = MODE_IK; kp.q_in = q; kp.spheres_out = spheres_out; kp.ee_out = ee_out;
@@ -1995,9 +1996,9 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
     crb_status st = enter(ctx);
     if (st != CRB_OK) return st;
     if ((st = ready(ctx, true)) != CRB_OK) return st;
-    if (!q || !goal || !cost || B < 0) return fail(ctx, CRB_E_ARG, "bad evaluate arguments");
+    if (B < 0 || (B > 0 && (!q || !goal || !cost))) return fail(ctx, CRB_E_ARG, "bad evaluate arguments");
     const int mode = H == 1 ? MODE_IK : MODE_TO;
-    if (mode == MODE_TO && (H < 8 || H > 32 || H * ctx->rp.D > 512 || !start))
+    if (mode == MODE_TO && (H < 8 || H > 32 || H * ctx->rp.D > 512 || (B > 0 && !start)))
         return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 32, H*D <= 512 and start");
     KParams kp = base_params(ctx);
     kp.B = B; kp.H = H; kp.cp.H = H; kp.mode = mode; kp.q_in = q; kp.env = env; kp.start = start; kp.goal = goal;
@@ -2027,7 +2028,7 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     crb_status st = enter(ctx);
     if (st != CRB_OK) return st;
     if ((st = ready(ctx, true)) != CRB_OK) return st;
-    if (!sp || !seeds || !goal || P < 0 || S < 1) return fail(ctx, CRB_E_ARG, "bad solve arguments");
+    if (!sp || P < 0 || S < 1 || (P > 0 && (!seeds || !goal))) return fail(ctx, CRB_E_ARG, "bad solve arguments");
     if (sp->history < 0 || sp->history > 32 || sp->n_alpha < 1 || sp->n_alpha > 8 || sp->iters < 0)
         return fail(ctx, CRB_E_LIMIT, "history must be in [0,32] (0 = gradient descent), n_alpha in [1,8], iters >= 0");
     if (sp->particle_iters < 0 ||
@@ -2039,8 +2040,9 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
         return fail(ctx, CRB_E_ARG, "check_every >= 0, conv_rtol >= 0, cluster in {-1, 0, 1}");
     const int mode = H == 1 ? MODE_IK : MODE_TO;
     const int D = ctx->rp.D;
-    if (mode == MODE_TO && (H < 8 || H > 32 || H * D > 512 || !start))
+    if (mode == MODE_TO && (H < 8 || H > 32 || H * D > 512 || (P > 0 && !start)))
         return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 32, H*D <= 512 and start");
+    if (P == 0) return CRB_OK;   // empty batch: validated, nothing launched
     const int N = H * D;
     cudaStream_t stream_ = (cudaStream_t)stream;
     float *sbc = seed_best_cost, *sbt = seed_best_traj;
@@ -2116,7 +2118,10 @@ crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P
     crb_status st = enter(ctx);
     if (st != CRB_OK) return st;
     if ((st = ready(ctx, true)) != CRB_OK) return st;
-    if (!seeds || !goal || P < 0 || S < 1 || H < 1) return fail(ctx, CRB_E_ARG, "bad solve arguments");
+    if (!sp || P < 0 || S < 1 || H < 1 || (P > 0 && (!seeds || !goal))) return fail(ctx, CRB_E_ARG, "bad solve arguments");
+    if (P == 0)   // validate the parameters, copy nothing
+        return crb_lbfgs_solve(ctx, sp, 0, S, H, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                               nullptr, stream);
     const int D = ctx->rp.D, N = H * D;
     cudaStream_t s = (cudaStream_t)stream;
     if ((st = grow(ctx, &ctx->h_seeds, &ctx->cap_h_seeds, (size_t)P * S * N)) != CRB_OK) return st;

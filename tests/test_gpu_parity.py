@@ -8,6 +8,7 @@ decision can actually differ between fp32 and fp64 are excluded (DESIGN.md "Pari
 excluded fraction is asserted small.  Line-search selection and the packed-key argmin are
 bit-exact on identical fp32 inputs.
 """
+import dataclasses
 import struct
 
 import numpy as np
@@ -387,6 +388,55 @@ def test_solve_seed_base_and_host_api(native, O):
                    best_traj=hb, best_cost=hc, best_key=hk)
     assert torch.equal(hb, dev["best_traj"].cpu()) and torch.equal(hc, dev["best_cost"].cpu())
     assert torch.equal(hk, dev["best_key"].cpu())
+    ctx.close()
+
+
+def test_solve_degenerate_shapes(native, O):
+    """Edge cases of the solve / evaluate / FK calls on the Franka + 20-cuboid scene:
+    - empty batches (P = 0, B = 0) validate and return without a launch;
+    - iters = 0 returns the seeds themselves with the cost of Theta_0 (Alg. 6 before its loop);
+    - seeds are independent (per-seed L-BFGS, §4.1): a TO seed solved alone, and an IK seed in a
+      ragged 33-seed batch (second 32-seed group with one active lane), give bitwise the result
+      it has inside the full batch;
+    - one line-search candidate (n_alpha = 1) never returns a seed worse than its start."""
+    rb, starts, goals_cfg, trajs = franka_trajs(91, 8, 16)
+    R = O.Robot(rb)
+    ctx = make(native, rb, [inputs.tabletop_scene(2, 0, 20)], inputs.CostParams(dt=0.25))
+    gl = f32(np.array([O.fk(R, q)[2] for q in goals_cfg]))
+    sp = inputs.SolverParams(iters=12)
+    # empty batches
+    out = ctx.solve(sp, T(np.zeros((0, 4, 16, 7))), T(np.zeros((0, 7))), start=T(np.zeros((0, 7))), seed_outputs=True)
+    assert out["best_cost"].shape == (0,) and out["seed_best_traj"].shape == (0, 4, 16, 7)
+    out = ctx.solve(sp, T(np.zeros((0, 30, 7))), T(np.zeros((0, 7))))
+    assert out["best_traj"].shape == (0, 7)
+    c, g, _ = ctx.evaluate(T(np.zeros((0, 16, 7))), T(np.zeros((0, 7))), start=T(np.zeros((0, 7))))
+    assert c.shape == (0,) and g.shape == (0, 16, 7)
+    torch.cuda.synchronize()
+    # iters = 0: the seeds and their own costs
+    seeds = f32(trajs.reshape(2, 4, 16, 7))
+    st, gg = T(f32(starts[:2])), T(gl[:2])
+    o0 = ctx.solve(inputs.SolverParams(iters=0), T(seeds), gg, start=st, seed_outputs=True)
+    assert torch.equal(o0["seed_best_traj"], T(seeds))
+    c0, _, _ = ctx.evaluate(T(seeds.reshape(8, 16, 7)), T(np.repeat(gl[:2], 4, 0)), start=T(np.repeat(f32(starts[:2]), 4, 0)))
+    np.testing.assert_allclose(o0["seed_best_cost"].cpu().numpy().reshape(-1), c0.cpu().numpy(), rtol=1e-6)
+    # TO seed independence: seed 2 of problem 1 alone
+    full = ctx.solve(sp, T(seeds), gg, start=st, seed_outputs=True)
+    one = ctx.solve(sp, T(seeds[1:2, 2:3]), gg[1:2], start=st[1:2], seed_outputs=True)
+    assert torch.equal(one["seed_best_cost"][0, 0], full["seed_best_cost"][1, 2])
+    assert torch.equal(one["seed_best_traj"][0, 0], full["seed_best_traj"][1, 2])
+    # IK: 33 seeds (a ragged second group) against the same seeds alone
+    iks = f32(np.stack([inputs.ik_seeds(rb, p, 33) for p in range(2)]))
+    fk = ctx.solve(sp, T(iks), gg, seed_outputs=True)
+    for s in (0, 31, 32):
+        alone = ctx.solve(sp, T(iks[:, s:s + 1]), gg, seed_outputs=True)
+        assert torch.equal(alone["seed_best_cost"][:, 0], fk["seed_best_cost"][:, s]), s
+        assert torch.equal(alone["seed_best_traj"][:, 0], fk["seed_best_traj"][:, s]), s
+    # one candidate per iteration
+    for hist in (0, 6):
+        o1 = ctx.solve(dataclasses.replace(sp, history=hist, alpha=(0.1,)), T(seeds), gg, start=st,
+                       seed_outputs=True)
+        sbc = o1["seed_best_cost"].cpu().numpy().reshape(-1)
+        assert np.all(np.isfinite(sbc)) and np.all(sbc <= c0.cpu().numpy() * (1 + 1e-6))
     ctx.close()
 
 
