@@ -21,7 +21,7 @@
 #define CRB_STATS 0
 #endif
 #if CRB_STATS
-__device__ unsigned long long g_crb_stats[16];
+static __device__ unsigned long long g_crb_stats[16];   // one copy per translation unit
 #define CRB_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_crb_stats[i], (unsigned long long)(v)); } while (0)
 #else
 #define CRB_STAT(i, v) do { } while (0)
@@ -656,7 +656,7 @@ __device__ __forceinline__ bool in_ebox(float px, float py, float pz, float ex, 
 // Rare path: the hit's activation and gradient, then the backward / forward marches (A6-A12):
 // L = |n - c|, bound = L/2, j = J0 (r' on a hit, else sd), at most n_s samples p = c + (j/L)(n - c);
 // a hit adds phi and (1 - kappa) phi' (-grad sd) and jumps r', a miss jumps sd.
-__device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const float *boxes, int k, float cx, float cy,
+static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const float *boxes, int k, float cx, float cy,
                                       float cz, float s2, float rp, int dirs, float eta, float inv_eta, int steps) {
     const BoxView b = load_box(boxes, k);              // reloaded here: keeps the screen loop spill-free
     float E = 0.f, Gx = 0.f, Gy = 0.f, Gz = 0.f;

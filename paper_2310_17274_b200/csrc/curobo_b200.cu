@@ -1,6 +1,6 @@
 // curobo_b200.cu -- kernels and host side of the C-ABI declared in include/curobo_b200.h.
 //
-// Kernels (all sm_100a, NT = 512 threads, 1 CTA per SM by shared-memory footprint):
+// Kernels (all sm_100a, NT = 256 threads, 2 CTAs per SM by shared-memory footprint):
 //   solve_to_kernel   persistent per-seed L-BFGS for trajectory optimisation: one CTA = one seed
 //                     trajectory, all iterations in one launch (replaces the paper's ~20 kernels
 //                     x 25-iteration CUDA graph)
@@ -9,6 +9,15 @@
 //   fk_kernel         forward kinematics only (crb_fk)
 //   select_kernel     per-problem packed-key argmin over seeds (O9)
 //   + the test-hook kernels (ls_select, argmin_keys, lbfgs_direction)
+//
+// Two translation units: this file (CRB_PART 0: every kernel except the tensor-core-screen
+// builds, plus the host side) is compiled with -ftz=true; curobo_b200_wmma.cu includes it with
+// CRB_PART 1 and instantiates only the <WMMA = true> kernels, compiled without -ftz
+// (build.py; measured: flush-to-zero speeds the small-world builds by 2-3 % but slows the
+// tensor-core build by 9 %).  crb_wmma_kernel() hands those kernels to the host side.
+#ifndef CRB_PART
+#define CRB_PART 0
+#endif
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -1428,6 +1437,39 @@ __global__ void __launch_bounds__(NT, 2) lbfgs_direction_kernel(int n, int count
 
 }  // namespace
 
+// the <WMMA = true> kernels, instantiated in CRB_PART 1 (no flush-to-zero)
+enum { KW_EVAL_TO, KW_EVAL_IK, KW_SOLVE_TO, KW_SOLVE_IK, KW_SOLVE_TO_CLUSTER, KW_SOLVE_IK_CLUSTER };
+const void *crb_wmma_kernel(int k);
+
+#if CRB_STATS
+static int stats_copy(unsigned long long *out, int reset) {   // this translation unit's counters
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out, ::g_crb_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(::g_crb_stats, z, sizeof(z));
+    }
+    return 0;
+}
+int crb_wmma_stats(unsigned long long *out, int reset);
+#endif
+
+#if CRB_PART == 1
+#if CRB_STATS
+int crb_wmma_stats(unsigned long long *out, int reset) { return stats_copy(out, reset); }
+#endif
+const void *crb_wmma_kernel(int k) {
+    switch (k) {
+    case KW_EVAL_TO: return (const void *)eval_to_kernel<true>;
+    case KW_EVAL_IK: return (const void *)eval_ik_kernel<true>;
+    case KW_SOLVE_TO: return (const void *)solve_to_kernel<true>;
+    case KW_SOLVE_IK: return (const void *)solve_ik_kernel<true>;
+    case KW_SOLVE_TO_CLUSTER: return (const void *)solve_to_cluster_kernel<true>;
+    case KW_SOLVE_IK_CLUSTER: return (const void *)solve_ik_cluster_kernel<true>;
+    }
+    return nullptr;
+}
+#else
 // ==========================================================================================
 // host side
 // ==========================================================================================
@@ -1586,6 +1628,18 @@ crb_status ready(crb_ctx *ctx, bool need_world) {
 // core pre-screen"): with it when some environment holds >= CRB_MMA_MIN_K enabled cuboids, else
 // the FFMA-only build (its smaller register footprint is faster on small worlds).
 bool use_world_mma(const crb_ctx *ctx) { return CRB_WORLD_MMA && ctx->kmax_enabled >= CRB_MMA_MIN_K; }
+
+crb_status launch_fn(crb_ctx *ctx, const void *fn, int grid, size_t smem, cudaStream_t st, const KParams &kp,
+                     const char *nm) {
+    if (grid <= 0) return CRB_OK;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_check(ctx, e, nm);
+    void *args[] = {(void *)&kp};
+    e = cudaLaunchKernel(fn, dim3(grid), dim3(NT), args, smem, st);
+    ctx->launches++;
+    if (e != cudaSuccess) return cuda_check(ctx, e, nm);
+    return cuda_check(ctx, cudaGetLastError(), nm);
+}
 
 template <typename Kern>
 crb_status launch(crb_ctx *ctx, Kern k, int grid, size_t smem, cudaStream_t st, const KParams &kp, const char *nm) {
@@ -2008,9 +2062,10 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
     const bool wm = use_world_mma(ctx);
     if (mode == MODE_TO)
-        return launch(ctx, wm ? eval_to_kernel<true> : eval_to_kernel<false>, B, bytes, (cudaStream_t)stream, kp,
+        return launch_fn(ctx, wm ? crb_wmma_kernel(KW_EVAL_TO) : (const void *)eval_to_kernel<false>, B, bytes,
+                         (cudaStream_t)stream, kp,
                       "eval_to_kernel");
-    return launch(ctx, wm ? eval_ik_kernel<true> : eval_ik_kernel<false>, (B + NC - 1) / NC, bytes,
+    return launch_fn(ctx, wm ? crb_wmma_kernel(KW_EVAL_IK) : (const void *)eval_ik_kernel<false>, (B + NC - 1) / NC, bytes,
                   (cudaStream_t)stream, kp, "eval_ik_kernel");
 }
 
@@ -2077,8 +2132,9 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     const bool clus = sp->n_alpha >= 2 && (sp->particle_iters == 0 || sp->n_particles >= sp->n_alpha) &&
                       (sp->cluster == 1 || (sp->cluster == -1 && (fits || parts || waves)));
     if (clus && units > 0) {
-        auto kern = mode == MODE_TO ? (wm ? solve_to_cluster_kernel<true> : solve_to_cluster_kernel<false>)
-                                    : (wm ? solve_ik_cluster_kernel<true> : solve_ik_cluster_kernel<false>);
+        const void *kern = mode == MODE_TO
+                               ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_CLUSTER) : (const void *)solve_to_cluster_kernel<false>)
+                               : (wm ? crb_wmma_kernel(KW_SOLVE_IK_CLUSTER) : (const void *)solve_ik_cluster_kernel<false>);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         if (e != cudaSuccess) return cuda_check(ctx, e, "solve_cluster_kernel");
         cudaLaunchConfig_t cfg = {};
@@ -2093,14 +2149,17 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, kp);
+        void *args[] = {(void *)&kp};
+        e = cudaLaunchKernelExC(&cfg, kern, args);
         ctx->launches++;
         if (e != cudaSuccess) return cuda_check(ctx, e, "solve_cluster_kernel");
         st = cuda_check(ctx, cudaGetLastError(), "solve_cluster_kernel");
     } else if (mode == MODE_TO)
-        st = launch(ctx, wm ? solve_to_kernel<true> : solve_to_kernel<false>, P * S, bytes, stream_, kp, "solve_to_kernel");
+        st = launch_fn(ctx, wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false>, P * S, bytes, stream_,
+                       kp, "solve_to_kernel");
     else
-        st = launch(ctx, wm ? solve_ik_kernel<true> : solve_ik_kernel<false>, P * ((S + NC - 1) / NC), bytes, stream_,
+        st = launch_fn(ctx, wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false>, P * ((S + NC - 1) / NC),
+                       bytes, stream_,
                     kp, "solve_ik_kernel");
     if (st != CRB_OK) return st;
     if (P > 0 && (best_traj || best_cost || best_key)) {
@@ -2160,8 +2219,8 @@ crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, i
     if (bytes > SMEM_MAX) { if (ctas_per_sm) *ctas_per_sm = 0; return CRB_OK; }
     int n = 0;
     const bool wm = use_world_mma(ctx);
-    const void *fn = mode == MODE_TO ? (wm ? (const void *)solve_to_kernel<true> : (const void *)solve_to_kernel<false>)
-                                     : (wm ? (const void *)solve_ik_kernel<true> : (const void *)solve_ik_kernel<false>);
+    const void *fn = mode == MODE_TO ? (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false>)
+                                     : (wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false>);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     st = cuda_check(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, NT, bytes), "occupancy");
     if (ctas_per_sm) *ctas_per_sm = n;
@@ -2352,12 +2411,11 @@ crb_status crb_particle_normals(uint32_t key0, uint32_t key1, int n_var, int n_p
 #if CRB_STATS
 // world-screen work counters (tools/world_stats.py only; not part of the product ABI)
 extern "C" int crb_debug_stats(unsigned long long *out, int reset) {
-    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-    if (cudaMemcpyFromSymbol(out, ::g_crb_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
-    if (reset) {
-        unsigned long long z[16] = {};
-        cudaMemcpyToSymbol(::g_crb_stats, z, sizeof(z));
-    }
+    unsigned long long w[16];
+    if (stats_copy(out, reset) != 0 || crb_wmma_stats(w, reset) != 0) return -1;
+    for (int i = 0; i < 16; ++i) out[i] += w[i];   // the counters of both translation units
     return 0;
 }
 #endif
+
+#endif  // CRB_PART == 0

@@ -18,16 +18,15 @@ sys.path.insert(0, ROOT)
 ap = argparse.ArgumentParser()
 ap.add_argument("--mma", type=int, default=1)
 ap.add_argument("--problems", type=int, default=16)
+ap.add_argument("--ftz", type=int, default=1, help="0: build without -ftz=true (A/B of the flag)")
 args = ap.parse_args()
 
 from paper_2310_17274_b200 import build as B  # noqa: E402
 
-lib = os.path.join(ROOT, "tools", f"libcurobo_stats{args.mma}.so")
-cmd = [B.NVCC, *B.FLAGS, "-DCRB_STATS=1", f"-DCRB_WORLD_MMA={args.mma}", "-DCRB_MMA_MIN_K=0" if args.mma else "-DCRB_MMA_MIN_K=100000", "-o", lib, B.SRC]
-i = cmd.index("-v")
-del cmd[i - 1:i + 1]   # drop "-Xptxas -v"
+lib = os.path.join(ROOT, "tools", f"libcurobo_stats{args.mma}{'' if args.ftz else '_noftz'}.so")
 if not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(d) for d in B.DEPS):
-    subprocess.run(cmd, check=True)
+    B.compile_lib(lib, ["-DCRB_STATS=1", f"-DCRB_WORLD_MMA={args.mma}",
+                        "-DCRB_MMA_MIN_K=0" if args.mma else "-DCRB_MMA_MIN_K=100000"], ftz=bool(args.ftz))
 os.environ["CRB_LIB"] = lib
 
 import torch  # noqa: E402
