@@ -22,6 +22,8 @@
  *     sphere-cuboid screen runs a conservative reduced-precision pre-screen (packed fp16 below 60
  *     enabled cuboids per environment, tensor-core fp16 hi/lo products from 60) that only selects
  *     the cuboids given the exact fp32 test: results are bitwise those of the all-fp32 screen.
+ *     The small-world kernels flush fp32 subnormals to zero (-ftz); the tensor-core-screen
+ *     kernels keep them, so the two builds agree bitwise unless an intermediate falls below 2^-126.
  *   - Non-finite inputs are not scanned: a NaN propagates into the cost, a NaN cost packs to the
  *     +inf key and never wins a selection (SURVEY §8(b) deviation).
  *   - Capacity limits (CRB_E_LIMIT): D <= 16, L <= 32, M <= 512, pairs <= 16384, H*D <= 512,

@@ -4,8 +4,9 @@
 The library builds its solver / evaluation kernels twice: with the HMMA pre-screen when some
 environment holds >= CRB_MMA_MIN_K (60) enabled cuboids, else FFMA only.  The pre-screen only
 chooses which cuboids go through the exact fp32 test, so on the SAME environments both builds must
-return bitwise the same costs, gradients and solves; a context whose world list includes one large
-environment runs the HMMA build for all of them.  Parity against the fp64 oracle at K in the HMMA
+return bitwise the same costs, gradients and solves (the FFMA build flushes subnormals, the HMMA
+build keeps them: no intermediate of these inputs falls below 2^-126); a context whose world list
+includes one large environment runs the HMMA build for all of them.  Parity against the fp64 oracle at K in the HMMA
 range (ragged K, far and huge cuboids) uses the tolerances of test_gpu_parity.py.
 """
 import numpy as np
