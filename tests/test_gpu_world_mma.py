@@ -232,3 +232,72 @@ def test_random_robot_eval_parity_both_builds(native, O, seed, big):
         stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, margin, f"rand IK {b}")
     stats.done(0.34)
     ctx.close()
+
+
+@pytest.mark.parametrize("big", [False, True])
+def test_capacity_robot_parity(native, O, big):
+    """The capacity corner of the header: D = 16 joints on L = 32 links (every other link fixed,
+    all revolute / prismatic types), H = 32 so H·D = 512, 96 spheres with a dense pair list.  TO
+    and IK evaluations against the oracle in both world builds; short solves are bitwise
+    repeatable and never worse than their seeds."""
+    from test_oracle_kinematics import random_chain
+    import dataclasses
+    M = 96
+    rb = random_chain(41, 32, M, types=[0, 4, 0, 5, 0, 6, 0, 1, 0, 4, 0, 2, 0, 5, 0, 3])
+    D, H, B = rb.n_dof, 32, 10
+    assert D == 16
+    g = np.random.default_rng(42)
+    sph = rb.spheres.copy()
+    sph[:, 3] = g.uniform(0.02, 0.06, M)
+    pairs = [(i, j) for i in range(M) for j in range(i + 1, M) if g.random() < 0.25]
+    rb = dataclasses.replace(rb, spheres=sph, pairs=np.array(pairs, np.int32), lo=-np.ones(D) * 2.0,
+                             hi=np.ones(D) * 2.0, vmax=np.ones(D) * 2.0, amax=np.ones(D) * 15.0,
+                             jmax=np.ones(D) * 500.0)
+    worlds = [inputs.random_world(61, 0, 24, lo=-1.2, hi=1.2, dmax=0.3)]
+    if big:
+        worlds.append(inputs.random_world(62, 0, 70, lo=-1.2, hi=1.2, dmax=0.2, disabled_frac=0.0))
+    cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED | inputs.JERK, dt=0.1)
+    ctx = make(native, rb, worlds, cp)
+    n_cta, smem = ctx.solver_occupancy(H)
+    assert n_cta >= 1 and smem <= 227 * 1024
+    R = O.Robot(rb)
+    Ws = [O.World(w) for w in worlds]
+    st = f32(g.uniform(-1.0, 1.0, (B, D)))
+    V = f32(np.clip(st[:, None, :] + np.cumsum(g.normal(0, 0.05, (B, H, D)), axis=1), -2.0, 2.0))
+    gl = f32(np.array([O.fk(R, g.uniform(-1, 1, D))[2] for _ in range(B)]))
+    env = (np.arange(B) % len(worlds)).astype(np.int32)
+    cost, grad, _ = ctx.evaluate(T(V), T(gl), start=T(st), env=T(env, torch.int32))
+    cost, grad = cost.cpu().numpy(), grad.cpu().numpy()
+    stats = Stats()
+    active_w = active_s = 0
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"cap TO {b}")
+        active_w += t_ref[4] > 0
+        active_s += t_ref[3] > 0
+    stats.done(0.34)
+    assert active_w >= 2 and active_s >= 2, (active_w, active_s)   # not vacuous
+    Q = f32(g.uniform(-1.5, 1.5, (40, D)))
+    glq = f32(np.repeat(gl[:1], 40, 0))
+    cq, gq, _ = ctx.evaluate(T(Q), T(glq), env=T(np.zeros(40, np.int32), torch.int32))
+    cq, gq = cq.cpu().numpy(), gq.cpu().numpy()
+    stats = Stats()
+    for b in range(40):
+        c_ref, g_ref, _, margin, _ = O.eval_ik(R, Ws[0], cp, glq[b], Q[b])
+        stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, margin, f"cap IK {b}")
+    stats.done(0.34)
+    sp = inputs.SolverParams(iters=8)
+    seeds = V.reshape(2, 5, H, D)
+    runs = [ctx.solve(sp, T(seeds), T(gl[:2]), start=T(st[:2]), env=T(env[:2], torch.int32), seed_outputs=True)
+            for _ in range(2)]
+    for k in runs[0]:
+        assert torch.equal(runs[0][k], runs[1][k]), k
+    sbc = runs[0]["seed_best_cost"].cpu().numpy().reshape(-1)
+    # seeds of problem p were evaluated above with env[p * 5 + s]; re-evaluate with the problem's env
+    ce, _, _ = ctx.evaluate(T(V), T(np.repeat(gl[:2], 5, 0)), start=T(np.repeat(st[:2], 5, 0)),
+                            env=T(np.repeat(env[:2], 5), torch.int32))
+    assert np.all(sbc <= ce.cpu().numpy() * (1 + 1e-6))
+    ik = ctx.solve(sp, T(f32(g.uniform(-1.5, 1.5, (2, 33, D)))), T(gl[:2]), env=T(env[:2], torch.int32),
+                   seed_outputs=True)
+    assert torch.isfinite(ik["seed_best_cost"]).all()
+    ctx.close()
