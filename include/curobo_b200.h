@@ -45,7 +45,7 @@ typedef struct crb_ctx crb_ctx;
 typedef enum {
     CRB_OK = 0,
     CRB_E_ARG = -1,        /* NULL pointer / invalid scalar argument                         */
-    CRB_E_SHAPE = -2,      /* inconsistent sizes (e.g. env index outside [0, n_env))         */
+    CRB_E_SHAPE = -2,      /* inconsistent sizes (H, D, batch shapes)                        */
     CRB_E_ROBOT = -3,      /* robot description fails validation (see crb_set_robot)       */
     CRB_E_WORLD = -4,      /* cuboid description fails validation                           */
     CRB_E_NOT_READY = -5,  /* robot / world / cost params not set                           */
@@ -185,7 +185,9 @@ crb_status crb_fk(crb_ctx *ctx, const float *q, int B, float *spheres_out, float
  *   H == 1 (IK mode): q[B][D] configurations; pose + self + discrete world + position bound.
  *     The env index must be constant inside each aligned group of 32 rows (rows that violate it
  *     get a NaN cost).  start may be NULL.
- *   env[B] (may be NULL = all 0), goal[B][7] (position, quaternion w,x,y,z), or goal[B][D]
+ *   env[B] (may be NULL = all 0; device memory, so an index outside [0, n_env) is not checked
+ *   on the host: such a row gets a NaN cost, never an obstacle-free one), goal[B][7] (position,
+ *   quaternion w,x,y,z), or goal[B][D]
  *   (joint configuration) when the cost flags include CRB_CSPACE.
  *   term_costs[B][5] (pose, bound, smooth, self, world) may be NULL. */
 crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, const int *env,
@@ -203,7 +205,9 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
 
 /* Per-seed L-BFGS solve (§4.1, Alg. 6 + Alg. 1), one persistent CTA per seed trajectory (TO) or
  * per 32 seeds of one problem (IK), all `iters` iterations inside one launch.
- *   seeds[P][S][H][D] (TO, H >= 8) or [P][S][D] (IK, H == 1); env[P] (may be NULL);
+ *   seeds[P][S][H][D] (TO, H >= 8) or [P][S][D] (IK, H == 1); env[P] (may be NULL; a problem
+ *   whose env index is outside [0, n_env) evaluates to NaN costs: its best_cost is NaN and its
+ *   best_key the +inf bits);
  *   start[P][D] (TO only); goal[P][7] (pose) or goal[P][D] (CRB_CSPACE).
  * Outputs (any may be NULL): best_traj[P][H][D] and best_cost[P] of the winning seed per
  * problem; best_key[P] = (float_bits(cost) << 32) | (global_seed_base + s), the packed key the
@@ -224,7 +228,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
                               void *stream);
 
 /* Same as crb_lbfgs_solve with HOST buffers: copies inputs to context-owned device buffers,
- * solves, copies outputs back and synchronises `stream`. */
+ * solves, copies outputs back and synchronises `stream`.  The env indices are host data here, so
+ * one outside [0, n_env) returns CRB_E_SHAPE before anything is copied. */
 crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P, int S, int H,
                                 const float *seeds, const int *env, const float *start,
                                 const float *goal, float *best_traj, float *best_cost,
@@ -236,8 +241,8 @@ crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P
  * inside the position limits, no self-collision pair of S penetrates, and every enabled sphere
  * keeps a distance >= r + margin (m, >= 0) to every enabled cuboid of env[k]; else 0.
  * Device pointers: q[K][D], env[K / env_div] (row k uses env[k / env_div]; may be NULL = 0; the
- * env must be constant within aligned groups of 32 rows, a row that violates it is reported
- * invalid), valid[K] (uint8).  Needs robot, world, params. */
+ * env must be constant within aligned groups of 32 rows, a row that violates it, or whose env
+ * index is outside [0, n_env), is reported invalid), valid[K] (uint8).  Needs robot, world, params. */
 crb_status crb_mask_samples(crb_ctx *ctx, const float *q, int K, const int *env, int env_div,
                             float margin, uint8_t *valid, void *stream);
 

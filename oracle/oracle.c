@@ -17,6 +17,7 @@
 #include <string.h>
 
 #define ORC_INF (1.0 / 0.0)
+#define ORC_NAN (0.0 / 0.0)
 
 static void upd_margin(double *margin, double v) {
     if (margin && fabs(v) < *margin) *margin = fabs(v);
@@ -1034,17 +1035,60 @@ void orc_particle_solve(orc_fun f, void *ctx, int n, const double *x0, const dou
     free(theta); free(C); free(w);
 }
 
+/* O8 steps 1-2, Alg. 6 lines 1-5 ("Shift Buffers"): the pair of the last move,
+ * s = x - xp, y = g - gp, joins the history ring S, Y [m][n] (oldest first), rho [m] holding
+ * `count` pairs, unless s'y <= 1e-12 (A20, the pair is skipped); a full ring drops its oldest
+ * pair first.  Returns the new count; *sy_out = s'y (O10: |s'y - 1e-12| is the skip margin).
+ * m = 0 is gradient descent: nothing is ever stored. */
+int orc_lbfgs_push(int n, int m, double *S, double *Y, double *rho, int count, const double *x,
+                   const double *xp, const double *g, const double *gp, double *sy_out) {
+    double *s = malloc(sizeof(double) * (size_t)n), *y = malloc(sizeof(double) * (size_t)n);
+    for (int t = 0; t < n; ++t) { s[t] = x[t] - xp[t]; y[t] = g[t] - gp[t]; }
+    double sy = dot(n, s, y);
+    if (sy_out) *sy_out = sy;
+    if (m > 0 && sy > 1e-12) {                    /* A20 */
+        if (count == m) {                         /* shift buffers: drop the oldest pair */
+            memmove(S, S + n, sizeof(double) * (size_t)(m - 1) * n);
+            memmove(Y, Y + n, sizeof(double) * (size_t)(m - 1) * n);
+            memmove(rho, rho + 1, sizeof(double) * (m - 1));
+            count = m - 1;
+        }
+        memcpy(S + (size_t)count * n, s, sizeof(double) * n);
+        memcpy(Y + (size_t)count * n, y, sizeof(double) * n);
+        rho[count] = 1.0 / sy;
+        count++;
+    }
+    free(s); free(y);
+    return count;
+}
+
+/* O10 solver margin of one line search (Alg. 1 lines 4-9): the smallest distance of an active
+ * condition to its decision point, over the A candidates: |c_a - (c0 + c1 alpha_a g0d)| (Armijo),
+ * |g_a'd - c2 g0d| (Wolfe, mode 1), ||g_a'd| - c2 |g0d|| (strong Wolfe, mode 2). */
+double orc_ls_margin(int A, const double *alpha, double c0, double g0d, const double *ca,
+                     const double *gda, double c1, double c2, int mode) {
+    double mg = ORC_INF;
+    for (int a = 0; a < A; ++a) {
+        mg = fmin(mg, fabs(ca[a] - (c0 + (c1 * alpha[a]) * g0d)));
+        if (mode == 1) mg = fmin(mg, fabs(gda[a] - c2 * g0d));
+        if (mode == 2) mg = fmin(mg, fabs(fabs(gda[a]) - c2 * fabs(g0d)));
+    }
+    return mg;
+}
+
 /* O8 per-seed solver in fp64: evaluate at x0, then `iters` iterations of
- * L-BFGS step -> clipped candidates -> batched evaluation -> selection -> best update. */
-void orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
-                     const double *hi, const orc_solver *sp, double *best_x, double *best_c,
-                     double *trace) {
+ * L-BFGS step -> clipped candidates -> batched evaluation -> selection -> best update.
+ * tr (may be NULL; every member may be NULL) records each iteration (O10 instrumentation). */
+void orc_lbfgs_solve_traced(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
+                            const double *hi, const orc_solver *sp, double *best_x, double *best_c,
+                            orc_solver_trace *tr) {
     int m = sp->history, A = sp->n_alpha;
     double *x = malloc(sizeof(double) * n), *g = malloc(sizeof(double) * n);
     double *xp = malloc(sizeof(double) * n), *gpv = malloc(sizeof(double) * n);
     double *d = malloc(sizeof(double) * n);
-    double *S = malloc(sizeof(double) * (size_t)m * n), *Y = malloc(sizeof(double) * (size_t)m * n);
-    double *rho = malloc(sizeof(double) * m);
+    size_t mm = m > 0 ? (size_t)m : 1;
+    double *S = malloc(sizeof(double) * mm * n), *Y = malloc(sizeof(double) * mm * n);
+    double *rho = malloc(sizeof(double) * mm);
     double *xa = malloc(sizeof(double) * (size_t)A * n), *ga = malloc(sizeof(double) * (size_t)A * n);
     double ca[8], gda[8];
     int count = 0;
@@ -1052,26 +1096,16 @@ void orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double
     double c = f(ctx, x, g);
     double bc = c;
     memcpy(best_x, x, sizeof(double) * n);
-    if (trace) trace[0] = bc;
-    for (int it = 0; it < sp->iters; ++it) {
-        if (it > 0) {
-            double *s = malloc(sizeof(double) * n), *y = malloc(sizeof(double) * n);
-            for (int t = 0; t < n; ++t) { s[t] = x[t] - xp[t]; y[t] = g[t] - gpv[t]; }
-            double sy = dot(n, s, y);
-            if (m > 0 && sy > 1e-12) {                    /* A20; m = 0 is gradient descent */
-                if (count == m) {                         /* shift buffers (Alg. 6 line 1) */
-                    memmove(S, S + n, sizeof(double) * (size_t)(m - 1) * n);
-                    memmove(Y, Y + n, sizeof(double) * (size_t)(m - 1) * n);
-                    memmove(rho, rho + 1, sizeof(double) * (m - 1));
-                    count = m - 1;
-                }
-                memcpy(S + (size_t)count * n, s, sizeof(double) * n);
-                memcpy(Y + (size_t)count * n, y, sizeof(double) * n);
-                rho[count] = 1.0 / sy;
-                count++;
-            }
-            free(s); free(y);
+    for (int it = 0; it <= sp->iters; ++it) {
+        if (tr) {                                     /* the iterate entering iteration it */
+            if (tr->x) memcpy(tr->x + (size_t)it * n, x, sizeof(double) * n);
+            if (tr->g) memcpy(tr->g + (size_t)it * n, g, sizeof(double) * n);
+            if (tr->c) tr->c[it] = c;
+            if (tr->best_c) tr->best_c[it] = bc;
         }
+        if (it == sp->iters) break;
+        double sy = ORC_NAN;
+        if (it > 0) count = orc_lbfgs_push(n, m, S, Y, rho, count, x, xp, g, gpv, &sy);   /* A21: none at 0 */
         memcpy(xp, x, sizeof(double) * n);
         memcpy(gpv, g, sizeof(double) * n);
         orc_lbfgs_direction(n, count, S, Y, rho, g, d);
@@ -1088,14 +1122,35 @@ void orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double
             gda[a] = dot(n, ga + (size_t)a * n, d);
         }
         int i = orc_ls_select(A, sp->alpha, c, g0d, ca, gda, sp->c1, sp->c2, sp->ls_mode);
+        if (tr) {
+            if (tr->d) memcpy(tr->d + (size_t)it * n, d, sizeof(double) * n);
+            if (tr->g0d) tr->g0d[it] = g0d;
+            for (int a = 0; a < A; ++a) {
+                if (tr->ca) tr->ca[it * 8 + a] = ca[a];
+                if (tr->gda) tr->gda[it * 8 + a] = gda[a];
+            }
+            if (tr->istar) tr->istar[it] = i;
+            if (tr->count) tr->count[it] = count;
+            if (tr->sy) tr->sy[it] = sy;
+            if (tr->ls_margin)
+                tr->ls_margin[it] = orc_ls_margin(A, sp->alpha, c, g0d, ca, gda, sp->c1, sp->c2, sp->ls_mode);
+        }
         memcpy(x, xa + (size_t)i * n, sizeof(double) * n);
         memcpy(g, ga + (size_t)i * n, sizeof(double) * n);
         c = ca[i];
         if (c < bc) { bc = c; memcpy(best_x, x, sizeof(double) * n); }   /* A23 strict < */
-        if (trace) trace[it + 1] = bc;
     }
     *best_c = bc;
     free(x); free(g); free(xp); free(gpv); free(d); free(S); free(Y); free(rho); free(xa); free(ga);
+}
+
+void orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
+                     const double *hi, const orc_solver *sp, double *best_x, double *best_c,
+                     double *trace) {
+    orc_solver_trace tr;
+    memset(&tr, 0, sizeof(tr));
+    tr.best_c = trace;                                /* best cost after each iteration */
+    orc_lbfgs_solve_traced(f, ctx, n, x0, lo, hi, sp, best_x, best_c, trace ? &tr : NULL);
 }
 
 /* ---- rollout objectives and threaded multi-seed solves (timing harness for cpu_baseline) ---- */

@@ -149,6 +149,26 @@ void   orc_particle_solve(orc_fun f, void *ctx, int n, const double *x0, const d
 void   orc_lbfgs_solve(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
                        const double *hi, const orc_solver *sp, double *best_x, double *best_c,
                        double *trace);
+/* O8 steps 1-2 (Alg. 6 lines 1-5): push (x - xp, g - gp) into the ring S, Y [m][n] (oldest
+ * first), rho [m] of `count` pairs unless s'y <= 1e-12 (A20), dropping the oldest when full;
+ * returns the new count, *sy_out = s'y. */
+int    orc_lbfgs_push(int n, int m, double *S, double *Y, double *rho, int count, const double *x,
+                      const double *xp, const double *g, const double *gp, double *sy_out);
+/* O10 solver margin: distance of the active Armijo / (strong) Wolfe tests to their thresholds. */
+double orc_ls_margin(int A, const double *alpha, double c0, double g0d, const double *ca,
+                     const double *gda, double c1, double c2, int mode);
+/* O10 per-iteration record of orc_lbfgs_solve_traced; every pointer may be NULL.  Row k of
+ * x / g / c / best_c is the iterate entering iteration k (k = iters: the final one); rows of the
+ * others are iteration k's L-BFGS step and line search (ca / gda rows have 8 slots). */
+typedef struct {
+    double *x, *g, *c, *best_c;          /* [iters+1][n], [iters+1][n], [iters+1], [iters+1] */
+    double *d, *g0d, *ca, *gda;          /* [iters][n], [iters], [iters][8], [iters][8]        */
+    int *istar, *count;                  /* [iters] selected candidate, ring size used for d  */
+    double *sy, *ls_margin;              /* [iters] s'y offered at k (NaN at 0), O10 margin    */
+} orc_solver_trace;
+void   orc_lbfgs_solve_traced(orc_fun f, void *ctx, int n, const double *x0, const double *lo,
+                              const double *hi, const orc_solver *sp, double *best_x,
+                              double *best_c, orc_solver_trace *tr);
 void   orc_solve_to(const orc_robot *rb, const orc_world *worlds, const int *env,
                     const orc_params *pr, const orc_solver *sp, int P, int S, int H,
                     const double *seeds, const double *start, const double *goal, int nthreads,

@@ -330,8 +330,16 @@ def argmin_f32(c):
     return lib().orc_argmin_f32(len(c), c.ctypes.data_as(F_P))
 
 
-def lbfgs_solve(fun, x0, sp, lo=None, hi=None):
-    """fun(x) -> (cost, grad) in numpy fp64; returns (best_x, best_c, trace)."""
+class _Trace(C.Structure):
+    _fields_ = [("x", D_P), ("g", D_P), ("c", D_P), ("best_c", D_P), ("d", D_P), ("g0d", D_P),
+                ("ca", D_P), ("gda", D_P), ("istar", I_P), ("count", I_P), ("sy", D_P),
+                ("ls_margin", D_P)]
+
+
+def lbfgs_solve(fun, x0, sp, lo=None, hi=None, traced=False):
+    """fun(x) -> (cost, grad) in numpy fp64; returns (best_x, best_c, trace) with trace the best
+    cost entering each iteration, or with traced=True a dict of the O10 per-iteration record
+    (orc_solver_trace: x, g, c, best_c [iters+1], d, g0d, ca, gda, istar, count, sy, ls_margin)."""
     x0 = _d(x0)
     n = x0.shape[0]
 
@@ -342,13 +350,54 @@ def lbfgs_solve(fun, x0, sp, lo=None, hi=None):
         return float(c)
 
     cfun = _FUN(cb)
-    bx = np.zeros(n); bc = C.c_double(); trace = np.zeros(sp.iters + 1)
+    bx = np.zeros(n); bc = C.c_double()
     so = solver(sp)
     lo = None if lo is None else _d(np.broadcast_to(lo, (n,)))
     hi = None if hi is None else _d(np.broadcast_to(hi, (n,)))
-    lib().orc_lbfgs_solve(cfun, None, n, _dp(x0), _dp(lo), _dp(hi), C.byref(so), _dp(bx),
-                          C.byref(bc), _dp(trace))
-    return bx, bc.value, trace
+    K = sp.iters
+    tr = dict(x=np.zeros((K + 1, n)), g=np.zeros((K + 1, n)), c=np.zeros(K + 1), best_c=np.zeros(K + 1),
+              d=np.zeros((max(K, 1), n)), g0d=np.zeros(max(K, 1)), ca=np.zeros((max(K, 1), 8)),
+              gda=np.zeros((max(K, 1), 8)), istar=np.zeros(max(K, 1), np.int32),
+              count=np.zeros(max(K, 1), np.int32), sy=np.zeros(max(K, 1)), ls_margin=np.zeros(max(K, 1)))
+    ts = _Trace(*[tr[k].ctypes.data_as(I_P if tr[k].dtype == np.int32 else D_P) for k, _ in _Trace._fields_])
+    L = lib()
+    L.orc_lbfgs_solve_traced.argtypes = [_FUN, C.c_void_p, C.c_int, D_P, D_P, D_P, C.POINTER(_Solver), D_P, D_P,
+                                         C.POINTER(_Trace)]
+    L.orc_lbfgs_solve_traced(cfun, None, n, _dp(x0), _dp(lo), _dp(hi), C.byref(so), _dp(bx), C.byref(bc),
+                             C.byref(ts))
+    if not traced:
+        return bx, bc.value, tr["best_c"]
+    A = len(sp.alpha)
+    for k in ("d", "g0d", "ca", "gda", "istar", "count", "sy", "ls_margin"):
+        tr[k] = tr[k][:K]
+    tr["ca"] = tr["ca"][:, :A]; tr["gda"] = tr["gda"][:, :A]
+    return bx, bc.value, tr
+
+
+def lbfgs_push(S, Y, rho, count, m, x, xp, g, gp):
+    """O8 steps 1-2 on a ring S, Y [m][n] (oldest first), rho [m] with `count` pairs; returns
+    (S, Y, rho, count, s'y) after the push (copies: the inputs are left unchanged)."""
+    x = _d(x)
+    n = x.shape[0]
+    S = _d(np.array(S, dtype=np.float64).reshape(max(m, 1), n)).copy()
+    Y = _d(np.array(Y, dtype=np.float64).reshape(max(m, 1), n)).copy()
+    rho = _d(np.array(rho, dtype=np.float64).reshape(max(m, 1))).copy()
+    sy = C.c_double()
+    L = lib()
+    L.orc_lbfgs_push.restype = C.c_int
+    L.orc_lbfgs_push.argtypes = [C.c_int, C.c_int, D_P, D_P, D_P, C.c_int, D_P, D_P, D_P, D_P, D_P]
+    cnt = L.orc_lbfgs_push(n, int(m), _dp(S), _dp(Y), _dp(rho), int(count), _dp(x), _dp(_d(xp)), _dp(_d(g)),
+                           _dp(_d(gp)), C.byref(sy))
+    return S, Y, rho, cnt, sy.value
+
+
+def ls_margin(alpha, c0, g0d, ca, gda, c1=1e-4, c2=0.9, mode=2):
+    al = _d(alpha)
+    L = lib()
+    L.orc_ls_margin.restype = C.c_double
+    L.orc_ls_margin.argtypes = [C.c_int, D_P, C.c_double, C.c_double, D_P, D_P, C.c_double, C.c_double, C.c_int]
+    return L.orc_ls_margin(len(al), _dp(al), float(c0), float(g0d), _dp(_d(ca)), _dp(_d(gda)), float(c1),
+                           float(c2), int(mode))
 
 
 def retime(robot: Robot, start, V, dt):

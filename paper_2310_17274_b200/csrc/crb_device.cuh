@@ -1308,7 +1308,10 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         const int c = lane;
         const float t0 = s.cfg_terms[0 * NC + c], t1 = s.cfg_terms[1 * NC + c], t2 = s.cfg_terms[2 * NC + c],
                     t3 = s.cfg_terms[3 * NC + c], t4 = s.cfg_terms[4 * NC + c];
-        const float cc = (((t0 + t1) + t2) + t3) + t4;
+        // an env index outside [0, n_env) (staged as an empty world) poisons the cost: NaN, so the
+        // row never looks collision-free and its seeds never win (packed key +inf)
+        const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
+        const float cc = (envc >= 0 && envc < kp.n_env) ? (((t0 + t1) + t2) + t3) + t4 : __int_as_float(0x7fc00000);
         s.cfg_cost[c] = cc;
         const float tot = warp_sum(cc);
         if (c == 0) s.scal[0] = tot;

@@ -575,27 +575,30 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
     ParticleAcc pacc;
     pacc.reset();
     float tm = -INFINITY, tZ = 0.f;   // merged particle chunks of the current warm-up iteration
-    if (npart > 0 && t < DC) {
-        const int d = t / NC;
-        const float s0 = kp.s0_frac * (lim[D + d] - lim[d]);   // B8
-        g[t] = s0 * s0;
-    }
+    if (npart > 0)
+        for (int idx = t; idx < DC; idx += NT) {   // D * 32 elements: D > 8 needs more than one per thread
+            const int d = idx / NC;
+            const float s0 = kp.s0_frac * (lim[D + d] - lim[d]);   // B8
+            g[idx] = s0 * s0;
+        }
     for (int pass = 0; pass < npass; ++pass) {
         const bool part = pass < npart;
         const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
         const int lpass = pass - npart;
         const int a = part ? -2 : (lpass == 0 ? -1 : (lpass - 1) % A);
-        if (part && t < DC) {
-            // ---- f1 SAMPLE (Alg. 5) for every seed of the group: variable d of seed lane
-            const int d = t / NC;
-            const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
-            const float v = fminf(fmaxf(fmaf(sqrtf(g[t]), z, th[t]), lim[d]), lim[D + d]);
-            s.q_cfg[t] = v;
-            float sn, cs;
-            sincosf(v, &sn, &cs);
-            s.scs[t] = sn;
-            s.scs[DC + t] = cs;
-        }
+        if (part)
+            for (int idx = t; idx < DC; idx += NT) {
+                // ---- f1 SAMPLE (Alg. 5) for every seed of the group: variable d of seed idx & 31
+                // (idx & 31 == t & 31: psd is this thread's seed for all its elements)
+                const int d = idx / NC;
+                const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
+                const float v = fminf(fmaxf(fmaf(sqrtf(g[idx]), z, th[idx]), lim[d]), lim[D + d]);
+                s.q_cfg[idx] = v;
+                float sn, cs;
+                sincosf(v, &sn, &cs);
+                s.scs[idx] = sn;
+                s.scs[DC + idx] = cs;
+            }
         if (a == 0 && warp == 0) {
             const int it = (lpass - 1) / A;
             // ---- ring push (per seed, A20)
@@ -664,37 +667,37 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             float *S1t = cg, *S2t = cg + DC;
             float r;
             const float w = pacc.add(s.cfg_cost[t & 31], kp.p_inv_beta, r);
-            if (t < DC) {
-                const float x = s.q_cfg[t], dx = x - th[t];
-                dd[t] = (pl == clo ? 0.f : dd[t] * r) + w * x;
-                thp[t] = (pl == clo ? 0.f : thp[t] * r) + w * dx * dx;
+            for (int idx = t; idx < DC; idx += NT) {   // w, r: seed idx & 31 == t & 31
+                const float x = s.q_cfg[idx], dx = x - th[idx];
+                dd[idx] = (pl == clo ? 0.f : dd[idx] * r) + w * x;
+                thp[idx] = (pl == clo ? 0.f : thp[idx] * r) + w * dx * dx;
             }
             if (pl == chi - 1 && nch > 1) {
                 if (clo == 0) { tm = -INFINITY; tZ = 0.f; }   // the iteration's first (non-empty) chunk
                 float ft, fc;
                 chunk_merge(tm, tZ, pacc.m, pacc.Z, ft, fc);
-                if (t < DC) {
-                    S1t[t] = (clo == 0 ? 0.f : S1t[t]) * ft + dd[t] * fc;
-                    S2t[t] = (clo == 0 ? 0.f : S2t[t]) * ft + thp[t] * fc;
+                for (int idx = t; idx < DC; idx += NT) {
+                    S1t[idx] = (clo == 0 ? 0.f : S1t[idx]) * ft + dd[idx] * fc;
+                    S2t[idx] = (clo == 0 ? 0.f : S2t[idx]) * ft + thp[idx] * fc;
                 }
                 pacc.reset();
             }
             if (pl == kp.pn - 1) {
-                if (t < DC) {
-                    const float Zs = nch > 1 ? tZ : pacc.Z;
-                    const float *S1 = nch > 1 ? S1t : dd, *S2 = nch > 1 ? S2t : thp;
+                const float Zs = nch > 1 ? tZ : pacc.Z;
+                const float *S1 = nch > 1 ? S1t : dd, *S2 = nch > 1 ? S2t : thp;
+                for (int idx = t; idx < DC; idx += NT) {
                     if (Zs > 0.f) {
                         const float iz = 1.f / Zs;
-                        th[t] = (1.f - kp.k_mu) * th[t] + kp.k_mu * (S1[t] * iz);
-                        g[t] = (1.f - kp.k_sigma) * g[t] + kp.k_sigma * (S2[t] * iz);
+                        th[idx] = (1.f - kp.k_mu) * th[idx] + kp.k_mu * (S1[idx] * iz);
+                        g[idx] = (1.f - kp.k_sigma) * g[idx] + kp.k_sigma * (S2[idx] * iz);
                     }
                     if (pass == npart - 1) {   // Theta_0 of L-BFGS = mu
-                        const float v = th[t];
-                        s.q_cfg[t] = v;
+                        const float v = th[idx];
+                        s.q_cfg[idx] = v;
                         float sn, cs;
                         sincosf(v, &sn, &cs);
-                        s.scs[t] = sn;
-                        s.scs[DC + t] = cs;
+                        s.scs[idx] = sn;
+                        s.scs[DC + idx] = cs;
                     }
                 }
                 pacc.reset();
@@ -789,27 +792,30 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
     const unsigned psd = (unsigned)(kp.seed_base + grp * NC + (t & 31));
     ParticleAcc pacc;
     pacc.reset();
-    if (npart > 0 && t < DC) {
-        const int d = t / NC;
-        const float s0 = kp.s0_frac * (lim[D + d] - lim[d]);   // B8
-        g[t] = s0 * s0;
-    }
+    if (npart > 0)
+        for (int idx = t; idx < DC; idx += NT) {   // D * 32 elements: D > 8 needs more than one per thread
+            const int d = idx / NC;
+            const float s0 = kp.s0_frac * (lim[D + d] - lim[d]);   // B8
+            g[idx] = s0 * s0;
+        }
     for (int pass = 0; pass < npass; ++pass) {
         const bool part = pass < npart;
         const int pit = part ? pass / csz : 0, pl = part ? clo + (pass - pit * csz) : 0;
         const int lpass = pass - npart;
         const int a = part ? -2 : (lpass == 0 ? -1 : rank);
-        if (part && t < DC) {
-            // ---- f1 SAMPLE (Alg. 5) for every seed of the group: variable d of seed lane
-            const int d = t / NC;
-            const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
-            const float v = fminf(fmaxf(fmaf(sqrtf(g[t]), z, th[t]), lim[d]), lim[D + d]);
-            s.q_cfg[t] = v;
-            float sn, cs;
-            sincosf(v, &sn, &cs);
-            s.scs[t] = sn;
-            s.scs[DC + t] = cs;
-        }
+        if (part)
+            for (int idx = t; idx < DC; idx += NT) {
+                // ---- f1 SAMPLE (Alg. 5) for every seed of the group: variable d of seed idx & 31
+                // (idx & 31 == t & 31: psd is this thread's seed for all its elements)
+                const int d = idx / NC;
+                const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
+                const float v = fminf(fmaxf(fmaf(sqrtf(g[idx]), z, th[idx]), lim[d]), lim[D + d]);
+                s.q_cfg[idx] = v;
+                float sn, cs;
+                sincosf(v, &sn, &cs);
+                s.scs[idx] = sn;
+                s.scs[DC + idx] = cs;
+            }
         if (a >= 0 && warp == 0) {
             const int it = lpass - 1;
             // ---- ring push (per seed, A20)
@@ -874,10 +880,10 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
             // ---- f1 UPDATE over this CTA's chunk, then all chunks merged in order (DSMEM)
             float r;
             const float w = pacc.add(s.cfg_cost[t & 31], kp.p_inv_beta, r);
-            if (t < DC) {
-                const float x = s.q_cfg[t], dx = x - th[t];
-                dd[t] = (pl == clo ? 0.f : dd[t] * r) + w * x;
-                thp[t] = (pl == clo ? 0.f : thp[t] * r) + w * dx * dx;
+            for (int idx = t; idx < DC; idx += NT) {   // w, r: seed idx & 31 == t & 31
+                const float x = s.q_cfg[idx], dx = x - th[idx];
+                dd[idx] = (pl == clo ? 0.f : dd[idx] * r) + w * x;
+                thp[idx] = (pl == clo ? 0.f : thp[idx] * r) + w * dx * dx;
             }
             if (pl == chi - 1) {
                 if (t < NC) { cc[t] = pacc.m; cgd[t] = pacc.Z; }   // this chunk's per-seed (m, Z)
@@ -888,30 +894,30 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
                     const float mc = cluster.map_shared_rank(cc, c)[t & 31], Zc = cluster.map_shared_rank(cgd, c)[t & 31];
                     float ft, fc;
                     chunk_merge(tm, tZ, mc, Zc, ft, fc);
-                    if (t < DC) {
-                        const float *pd = cluster.map_shared_rank(dd, c), *pq = cluster.map_shared_rank(thp, c);
-                        S1t[t] = (c == 0 ? 0.f : S1t[t]) * ft + pd[t] * fc;
-                        S2t[t] = (c == 0 ? 0.f : S2t[t]) * ft + pq[t] * fc;
+                    const float *pd = cluster.map_shared_rank(dd, c), *pq = cluster.map_shared_rank(thp, c);
+                    for (int idx = t; idx < DC; idx += NT) {
+                        S1t[idx] = (c == 0 ? 0.f : S1t[idx]) * ft + pd[idx] * fc;
+                        S2t[idx] = (c == 0 ? 0.f : S2t[idx]) * ft + pq[idx] * fc;
                     }
                 }
                 cluster.sync();                // peers have read this chunk before it is overwritten
                 pacc.m = tm; pacc.Z = tZ;      // the merged totals feed the update below
-                if (t < DC) { dd[t] = S1t[t]; thp[t] = S2t[t]; }
+                for (int idx = t; idx < DC; idx += NT) { dd[idx] = S1t[idx]; thp[idx] = S2t[idx]; }
             }
             if (pl == chi - 1) {
-                if (t < DC) {
+                for (int idx = t; idx < DC; idx += NT) {
                     if (pacc.Z > 0.f) {
                         const float iz = 1.f / pacc.Z;
-                        th[t] = (1.f - kp.k_mu) * th[t] + kp.k_mu * (dd[t] * iz);
-                        g[t] = (1.f - kp.k_sigma) * g[t] + kp.k_sigma * (thp[t] * iz);
+                        th[idx] = (1.f - kp.k_mu) * th[idx] + kp.k_mu * (dd[idx] * iz);
+                        g[idx] = (1.f - kp.k_sigma) * g[idx] + kp.k_sigma * (thp[idx] * iz);
                     }
                     if (pass == npart - 1) {   // Theta_0 of L-BFGS = mu
-                        const float v = th[t];
-                        s.q_cfg[t] = v;
+                        const float v = th[idx];
+                        s.q_cfg[idx] = v;
                         float sn, cs;
                         sincosf(v, &sn, &cs);
-                        s.scs[t] = sn;
-                        s.scs[DC + t] = cs;
+                        s.scs[idx] = sn;
+                        s.scs[DC + idx] = cs;
                     }
                 }
                 pacc.reset();
@@ -1110,7 +1116,7 @@ __global__ void __launch_bounds__(NT, 2) mask_kernel(const __grid_constant__ KPa
     prep_sincos(s, D);
     __syncthreads();
     fk_phase(rp, s);
-    int bad = 0;
+    int bad = (env < 0 || env >= kp.n_env) ? 16 : 0;  // env index outside [0, n_env): invalid
     if (warp == 0)                                    // position limits
         for (int d = 0; d < D; ++d) {
             const float v = s.q_cfg[d * NC + lane];
@@ -2182,6 +2188,9 @@ crb_status crb_lbfgs_solve_host(crb_ctx *ctx, const crb_solver_params *sp, int P
         return crb_lbfgs_solve(ctx, sp, 0, S, H, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                                nullptr, stream);
     const int D = ctx->rp.D, N = H * D;
+    if (env)   // host buffer: the env indices can be checked here (the device path poisons them with NaN)
+        for (int p = 0; p < P; ++p)
+            if (env[p] < 0 || env[p] >= ctx->n_env) return fail(ctx, CRB_E_SHAPE, "env index outside [0, n_env)");
     cudaStream_t s = (cudaStream_t)stream;
     if ((st = grow(ctx, &ctx->h_seeds, &ctx->cap_h_seeds, (size_t)P * S * N)) != CRB_OK) return st;
     const int gw = (ctx->cp.flags & CRB_CSPACE) ? D : 7;

@@ -234,6 +234,46 @@ def test_ik_env_group_violation_is_loud(native, O):
     ctx.close()
 
 
+@pytest.mark.parametrize("big", [False, True])
+def test_env_index_out_of_range_is_loud(native, O, big):
+    """an env index outside [0, n_env) must never read as an empty world.
+    Device batches get NaN costs (evaluate TO / IK, solve: NaN best cost, +inf key), the mask
+    reports the row invalid, and the host solve API refuses it with CRB_E_SHAPE."""
+    rb = robots.franka64()
+    worlds = [inputs.tabletop_scene(0, e, 80 if big else 5) for e in range(2)]
+    cp = inputs.CostParams(dt=0.25)
+    ctx = make(native, rb, worlds, cp)
+    H = 16
+    st = np.tile(rb.ready, (4, 1))
+    V = np.tile(rb.ready, (4, H, 1))
+    gl = np.tile([0.3, 0, 0.5, 1, 0, 0, 0], (4, 1))
+    env = np.array([0, 2, -1, 1], np.int32)
+    cost, _, _ = ctx.evaluate(T(V), T(gl), start=T(st), env=T(env, torch.int32))
+    c = cost.cpu().numpy()
+    assert np.isfinite(c[[0, 3]]).all() and np.isnan(c[[1, 2]]).all(), c
+    for e in (2, -1, 7):   # IK: a whole 32-row group in a bad env
+        cq, _, _ = ctx.evaluate(T(np.tile(rb.ready, (3, 1))), T(gl[:3]), env=T(np.full(3, e, np.int32), torch.int32))
+        assert np.isnan(cq.cpu().numpy()).all()
+    out = ctx.solve(inputs.SolverParams(iters=3), T(V.reshape(4, 1, H, 7)), T(gl), start=T(st),
+                    env=T(env, torch.int32), seed_outputs=True)
+    bc = out["best_cost"].cpu().numpy()
+    assert np.isfinite(bc[[0, 3]]).all() and np.isnan(bc[[1, 2]]).all(), bc
+    keys = out["best_key"].cpu().numpy()
+    assert (keys[[1, 2]] >> 32 == 0x7f800000).all()
+    ik = ctx.solve(inputs.SolverParams(iters=3), T(np.tile(rb.ready, (4, 5, 1))), T(gl), env=T(env, torch.int32))
+    bc = ik["best_cost"].cpu().numpy()
+    assert np.isfinite(bc[[0, 3]]).all() and np.isnan(bc[[1, 2]]).all(), bc
+    valid = ctx.mask_samples(T(np.tile(rb.ready, (64, 1))), env=T(np.array([0, 5], np.int32), torch.int32), env_div=32)
+    v = valid.cpu().numpy()
+    assert not v[32:].any()
+    with pytest.raises(native.CrbError) as e:
+        ctx.solve_host(inputs.SolverParams(iters=1), torch.tensor(V.reshape(4, 1, H, 7), dtype=torch.float32),
+                       torch.tensor(gl, dtype=torch.float32), start=torch.tensor(st, dtype=torch.float32),
+                       env=torch.tensor(env), best_cost=torch.empty(4))
+    assert e.value.code == -2
+    ctx.close()
+
+
 # ------------------------------------------------------------------------------------------ selection
 
 def test_line_search_selection_bit_exact(native, O):

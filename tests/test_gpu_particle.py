@@ -144,6 +144,44 @@ def test_particle_warmup_ik_parity(native, O):
     ctx.close()
 
 
+@pytest.mark.parametrize("cluster", [0, 1])
+def test_particle_warmup_ik_parity_d16(native, O, cluster):
+    """D = 16 makes D * 32 = 512 particle elements per 32-seed group, two per
+    thread of the 256-thread CTA.  Every dof (not only the first 8) must be sampled, updated and
+    given fresh sin / cos; sequential and latency-mode (cluster) kernels against the oracle."""
+    from test_gpu_world_mma import capacity_robot
+    rb = capacity_robot()
+    D = rb.n_dof
+    R = O.Robot(rb)
+    world = inputs.random_world(61, 0, 24, lo=-1.2, hi=1.2, dmax=0.3)
+    W = O.World(world)
+    cp = inputs.CostParams()
+    P, S = 1, 33
+    g = np.random.default_rng(16)
+    goals = f32(np.array([O.fk(R, g.uniform(-1.0, 1.0, D))[2] for _ in range(P)]))
+    seeds = f32(g.uniform(-1.5, 1.5, (P, S, D)))
+    c0 = [O.eval_ik(R, W, cp, goals[p], seeds[p, s])[0] for p in range(P) for s in range(S)]
+    sp = inputs.SolverParams(iters=0, particle_iters=2, n_particles=16,
+                             particle_beta=0.25 * float(np.median(c0)), rng_key=21, cluster=cluster)
+    ctx = make(native, rb, [world], cp)
+    out = ctx.solve(sp, T(seeds), T(goals), seed_outputs=True)
+    mu_gpu = out["seed_best_traj"].cpu().numpy().astype(np.float64)
+    ref = _oracle_means(O, R, [W], np.zeros(P, np.int32), cp, sp, seeds, None, goals, rb.lo, rb.hi, 0, 0)
+    checked, worst = 0, 0.0
+    for u, (mu, margin, _) in enumerate(ref):
+        p, s = divmod(u, S)
+        if margin < MARGIN:
+            continue
+        err = np.abs(mu_gpu[p, s] - mu).max()
+        worst = max(worst, err)
+        assert err <= MU_ATOL_SMOOTH, (u, err, np.abs(mu_gpu[p, s] - mu))
+        assert np.abs(mu[8:] - seeds[p, s, 8:]).max() > 1e-3, "dofs 8..15 did not move: vacuous"
+        checked += 1
+    assert checked >= 0.8 * P * S
+    print(f"particle IK parity D=16 (cluster={cluster}): {checked} seeds, worst |dmu| = {worst:.2e}")
+    ctx.close()
+
+
 def test_particle_sharding_is_bit_exact(native, O):
     """The draws are keyed by GLOBAL problem / seed indices (B9): solving a slice with
     problem_base / seed_base reproduces the full solve bit for bit (the multi-GPU seed and

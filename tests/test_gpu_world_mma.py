@@ -234,25 +234,33 @@ def test_random_robot_eval_parity_both_builds(native, O, seed, big):
     ctx.close()
 
 
+def capacity_robot():
+    """D = 16 joints on L = 32 links (every other link fixed, all revolute / prismatic types), 96
+    spheres with a dense pair list (the capacity corner of the header)."""
+    from test_oracle_kinematics import random_chain
+    import dataclasses
+    M = 96
+    rb = random_chain(41, 32, M, types=[0, 4, 0, 5, 0, 6, 0, 1, 0, 4, 0, 2, 0, 5, 0, 3])
+    D = rb.n_dof
+    assert D == 16
+    g = np.random.default_rng(42)
+    sph = rb.spheres.copy()
+    sph[:, 3] = g.uniform(0.02, 0.06, M)
+    pairs = [(i, j) for i in range(M) for j in range(i + 1, M) if g.random() < 0.25]
+    return dataclasses.replace(rb, spheres=sph, pairs=np.array(pairs, np.int32), lo=-np.ones(D) * 2.0,
+                               hi=np.ones(D) * 2.0, vmax=np.ones(D) * 2.0, amax=np.ones(D) * 15.0,
+                               jmax=np.ones(D) * 500.0)
+
+
 @pytest.mark.parametrize("big", [False, True])
 def test_capacity_robot_parity(native, O, big):
     """The capacity corner of the header: D = 16 joints on L = 32 links (every other link fixed,
     all revolute / prismatic types), H = 32 so H·D = 512, 96 spheres with a dense pair list.  TO
     and IK evaluations against the oracle in both world builds; short solves are bitwise
     repeatable and never worse than their seeds."""
-    from test_oracle_kinematics import random_chain
-    import dataclasses
-    M = 96
-    rb = random_chain(41, 32, M, types=[0, 4, 0, 5, 0, 6, 0, 1, 0, 4, 0, 2, 0, 5, 0, 3])
+    rb = capacity_robot()
     D, H, B = rb.n_dof, 32, 10
-    assert D == 16
-    g = np.random.default_rng(42)
-    sph = rb.spheres.copy()
-    sph[:, 3] = g.uniform(0.02, 0.06, M)
-    pairs = [(i, j) for i in range(M) for j in range(i + 1, M) if g.random() < 0.25]
-    rb = dataclasses.replace(rb, spheres=sph, pairs=np.array(pairs, np.int32), lo=-np.ones(D) * 2.0,
-                             hi=np.ones(D) * 2.0, vmax=np.ones(D) * 2.0, amax=np.ones(D) * 15.0,
-                             jmax=np.ones(D) * 500.0)
+    g = np.random.default_rng(43)
     worlds = [inputs.random_world(61, 0, 24, lo=-1.2, hi=1.2, dmax=0.3)]
     if big:
         worlds.append(inputs.random_world(62, 0, 70, lo=-1.2, hi=1.2, dmax=0.2, disabled_frac=0.0))

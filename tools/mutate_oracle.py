@@ -1,0 +1,111 @@
+"""Mutation check of the oracle's pins (VERDICT r1 "What's weak" 1; ③ "a plausible mistake anywhere
+in it ... fails one of them").
+
+Each mutation is one plausible bug written into a scratch copy of oracle/oracle.c.  The copy of the
+repo (oracle/, tests/, the package sources, no built libraries) is put under a temp directory, the
+mutated oracle is built there, and `pytest -m "not gpu" -x` runs against it.  A mutation is KILLED
+when some test fails.  Usage:  python tools/mutate_oracle.py [name ...]   (default: all).  Writes
+one JSON line per mutation and a summary; exits 1 if any mutation survives.
+"""
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# (name, what it breaks, old text, new text): old must occur exactly once in oracle.c
+MUTATIONS = [
+    ("speed_not_in_world_grad", "Eq. world-collision-cost: sp dropped from the world gradient (P:121)",
+     "gs[(h * M + m) * 3 + i] += pr->beta_world * sp * G[i];",
+     "gs[(h * M + m) * 3 + i] += pr->beta_world * G[i];"),
+    ("speed_forward_difference", "A13 / P:118: speed as a one-sided difference",
+     "const double *pa = cp ? cp : c, *pb = cn ? cn : c;\n"
+     "                double dx = pb[0] - pa[0], dy = pb[1] - pa[1], dz = pb[2] - pa[2];\n"
+     "                sp = sqrt(dx * dx + dy * dy + dz * dz) / (2.0 * pr->dt);",
+     "const double *pa = c, *pb = cn ? cn : c;\n"
+     "                double dx = pb[0] - pa[0], dy = pb[1] - pa[1], dz = pb[2] - pa[2];\n"
+     "                sp = sqrt(dx * dx + dy * dy + dz * dz) / (pr->dt);"),
+    ("ring_evicts_newest", "Alg. 6 'Shift Buffers' (P:2153): the newest pair dropped instead of the oldest",
+     "            memmove(S, S + n, sizeof(double) * (size_t)(m - 1) * n);\n"
+     "            memmove(Y, Y + n, sizeof(double) * (size_t)(m - 1) * n);\n"
+     "            memmove(rho, rho + 1, sizeof(double) * (m - 1));\n",
+     ""),
+    ("no_sy_skip", "A20: pairs with s'y <= 1e-12 pushed anyway",
+     "if (m > 0 && sy > 1e-12) {                    /* A20 */",
+     "if (m > 0) {                    /* A20 */"),
+    ("no_candidate_clip", "Alg. 1 line 1 / A35: candidates not clipped to [lo, hi]",
+     "                if (lo && v < lo[t]) v = lo[t];\n                if (hi && v > hi[t]) v = hi[t];\n",
+     ""),
+    ("best_update_not_strict", "A23: ties replace the best iterate",
+     "if (c < bc) { bc = c; memcpy(best_x, x, sizeof(double) * n); }",
+     "if (c <= bc) { bc = c; memcpy(best_x, x, sizeof(double) * n); }"),
+    # further plausible slips, beyond the six the round-1 review recorded
+    ("sweep_grad_no_one_minus_kappa", "A12: the sweep sample's gradient not scaled by (1 - kappa)",
+     "double phis = box_term(w, k, p, rp, eta, 1.0 - kappa, G, &sdp, margin);",
+     "double phis = box_term(w, k, p, rp, eta, 1.0, G, &sdp, margin);"),
+    ("armijo_sign", "Alg. 1 / A17: Armijo with + instead of the descent term",
+     "int ok = ca[a] <= c0 + (c1 * alpha[a]) * g0d;",
+     "int ok = ca[a] <= c0 - (c1 * alpha[a]) * g0d;"),
+    ("strong_wolfe_no_abs", "A17: strong Wolfe without |.| on g_a'd",
+     "if (mode == 2) ok = ok && (fabs(gda[a]) <= c2 * fabs(g0d));\n        if (ok) best = a;",
+     "if (mode == 2) ok = ok && (gda[a] <= c2 * fabs(g0d));\n        if (ok) best = a;"),
+    ("largest_true_first", "A22: the first (not the largest) satisfying candidate",
+     "if (mode == 2) ok = ok && (fabs(gda[a]) <= c2 * fabs(g0d));\n        if (ok) best = a;",
+     "if (mode == 2) ok = ok && (fabs(gda[a]) <= c2 * fabs(g0d));\n        if (ok && best == 0) best = a;"),
+    ("gamma_oldest_pair", "A19: H0 scaling from the oldest instead of the newest pair",
+     "const double *s = S + (size_t)(count - 1) * n, *y = Y + (size_t)(count - 1) * n;",
+     "const double *s = S, *y = Y;"),
+    ("direction_not_negated", "A18: d = r instead of -r",
+     "for (int t = 0; t < n; ++t) d[t] = -q[t];",
+     "for (int t = 0; t < n; ++t) d[t] = q[t];"),
+]
+
+
+def run(name, old, new, keep=False):
+    src = open(os.path.join(ROOT, "oracle", "oracle.c")).read()
+    assert src.count(old) == 1, f"{name}: anchor text found {src.count(old)} times"
+    tmp = tempfile.mkdtemp(prefix=f"mut_{name}_")
+    try:
+        for d in ("oracle", "tests", "paper_2310_17274_b200", "include"):
+            shutil.copytree(os.path.join(ROOT, d), os.path.join(tmp, d),
+                            ignore=shutil.ignore_patterns("*.so", "__pycache__", "*.o"))
+        for f in ("pytest.ini", "__graft_entry__.py"):
+            shutil.copy(os.path.join(ROOT, f), tmp)
+        # the ABI tests load the CUDA library: give the copy the built one (unchanged product code)
+        lib = os.path.join(ROOT, "paper_2310_17274_b200", "libcurobo_b200.so")
+        if os.path.exists(lib):
+            shutil.copy(lib, os.path.join(tmp, "paper_2310_17274_b200"))
+        with open(os.path.join(tmp, "oracle", "oracle.c"), "w") as f:
+            f.write(src.replace(old, new))
+        t0 = time.time()
+        r = subprocess.run([sys.executable, "-m", "pytest", "tests", "-x", "-q", "-m", "not gpu", "-p", "no:randomly"],
+                           cwd=tmp, capture_output=True, text=True)
+        failed = [ln.split(" ")[1] for ln in r.stdout.splitlines() if ln.startswith("FAILED ")]
+        return dict(mutation=name, killed=r.returncode != 0, by=failed[:3], seconds=round(time.time() - t0, 1),
+                    rc=r.returncode)
+    finally:
+        if not keep:
+            shutil.rmtree(tmp, ignore_errors=True)
+
+
+def main():
+    want = set(sys.argv[1:])
+    results = []
+    for name, what, old, new in MUTATIONS:
+        if want and name not in want:
+            continue
+        res = run(name, old, new)
+        res["what"] = what
+        print(json.dumps(res), flush=True)
+        results.append(res)
+    surv = [r["mutation"] for r in results if not r["killed"]]
+    print(json.dumps({"mutations": len(results), "killed": len(results) - len(surv), "survivors": surv}))
+    sys.exit(1 if surv else 0)
+
+
+if __name__ == "__main__":
+    main()
