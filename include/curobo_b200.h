@@ -150,7 +150,27 @@ typedef struct {
      * per SM; or a particle warm-up on at most 3 waves; or a better-filled last wave), 0 = off,
      * 1 = on.  TO and IK solves. */
     int cluster;
+    /* Solver trace for teacher-forced parity tests (SURVEY §8(c).4 "the oracle recomputes d from
+     * the GPU's (Theta, g, ring)"; O10).  trace = NULL (the default) records nothing.  Otherwise
+     * a DEVICE buffer of P * S * n_trace records of CRB_TRACE_REC(N, history) floats, N = H * D
+     * (TO) or D (IK); record (p * S + s) * n_trace + j is seed s of problem p at iteration
+     * trace_iter[j] (0-based, ascending not required; an iteration never reached, e.g. after a
+     * chunked exit, leaves its record untouched).  Tracing runs the sequential kernels (the
+     * latency-mode clusters are bitwise identical, see `cluster`).  Record layout, in floats:
+     *   [0, N) Theta_k entering iteration k    [N, 2N) g_k    [2N, 3N) Theta_{k-1}    [3N, 4N) g_{k-1}
+     *     (Theta_{k-1}, g_{k-1} are 0 at k = 0)    [4N, 5N) the L-BFGS direction d_k
+     *   ring BEFORE the push of iteration k: S [m][N], Y [m][N] (oldest first, zero rows beyond
+     *     the count), rho [m], count
+     *   ring AFTER the push: S [m][N], Y [m][N], rho [m], count
+     *   24 scalars: g_k.d_k, c_k, i*, s'y of the offered pair (0 at k = 0), c_a [8], g_a.d [8],
+     *     k, best cost after the iteration's update, 2 unused */
+    float *trace;
+    int n_trace;               /* 0..8                                                            */
+    int trace_iter[8];
 } crb_solver_params;
+
+/* Size in floats of one solver trace record (crb_solver_params.trace). */
+#define CRB_TRACE_REC(N, m) (5 * (N) + 2 * (2 * (m) * (N) + (m) + 1) + 24)
 
 crb_status crb_create(int cuda_device, crb_ctx **out);
 crb_status crb_destroy(crb_ctx *ctx);

@@ -118,6 +118,8 @@ struct KParams {
     float alpha[8], c1, c2;
     long long seed_base;
     // particle warm-up (Alg. 5; f1)
+    float *trace;                 // solver trace for teacher-forced parity (NULL: off; header)
+    int n_trace, trace_iter[8];
     int check_every;              // chunked convergence exit of TO solves (0: off; reading B20)
     float conv_rtol;
     int pn_iters, pn;

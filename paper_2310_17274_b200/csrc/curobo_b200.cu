@@ -83,8 +83,10 @@ __device__ void two_loop_block(int N, int Np, int count, const int *order, const
 // definition for the sequential and the cluster solver (identical arithmetic).
 __device__ __forceinline__ float lbfgs_step_to(int it, int N, int Np, int m, const float *th, const float *g, float *thp,
                                                float *gp, float *dd, float *Sb, float *Yb, float *rho, float *syv,
-                                               float *yyv, int *order, int *ring, float *red, int &ph, float (&d_e)[2]) {
+                                               float *yyv, int *order, int *ring, float *red, int &ph, float (&d_e)[2],
+                                               float &sy_out) {
     const int t = threadIdx.x;
+    sy_out = 0.f;
     // ---- a13: L-BFGS buffers (Alg. 6 lines 1-5): push (s, y, rho) unless s^T y <= 1e-12 (A20)
     if (it > 0) {
         const int fs = ring[1];
@@ -100,6 +102,7 @@ __device__ __forceinline__ float lbfgs_step_to(int it, int N, int Np, int m, con
         }
         const float sy = block_sum(sy_p, red, ph);
         const float yy = block_sum(yy_p, red, ph);
+        sy_out = sy;
         if (m > 0 && sy > 1e-12f && t == 0) {   // m = 0: gradient descent
             rho[fs] = 1.f / sy; syv[fs] = sy; yyv[fs] = yy;
             const int cnt = ring[0];
@@ -128,6 +131,106 @@ __device__ __forceinline__ float lbfgs_step_to(int it, int N, int Np, int m, con
         if (i < N) gd_p += g[i] * d_e[e];
     }
     return block_sum(gd_p, red, ph);   // also publishes dd to every thread
+}
+
+// ------------------------------------------------------------------------------------------
+// solver trace for the teacher-forced parity tests (crb_solver_params.trace; record layout in
+// the header).  Out of line, behind one uniform branch: the hot loop keeps its code size.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ int trace_slot(const KParams &kp, int it) {
+    if (kp.trace == nullptr) return -1;
+    for (int j = 0; j < kp.n_trace; ++j)
+        if (kp.trace_iter[j] == it) return j;
+    return -1;
+}
+
+__device__ __forceinline__ float *trace_rec(const KParams &kp, size_t seed_unit, int j, int N) {
+    return kp.trace + (seed_unit * (size_t)kp.n_trace + (size_t)j) * (size_t)CRB_TRACE_REC(N, kp.m);
+}
+
+// TO: the ring (slots via order[], oldest first) as S [m][N], Y [m][N], rho [m], count; every
+// element is read by the thread that wrote it in the push (e = t, t + NT)
+__device__ __forceinline__ void trace_to_ring(float *dst, int N, int Np, int m, const float *Sb, const float *Yb,
+                                              const float *rho, const int *order, int cnt) {
+    for (int i = 0; i < m; ++i)
+        for (int e = threadIdx.x; e < N; e += NT) {
+            dst[i * N + e] = i < cnt ? Sb[order[i] * Np + e] : 0.f;
+            dst[(m + i) * N + e] = i < cnt ? Yb[order[i] * Np + e] : 0.f;
+        }
+    for (int i = threadIdx.x; i < m; i += NT) dst[2 * m * N + i] = i < cnt ? rho[order[i]] : 0.f;
+    if (threadIdx.x == 0) dst[2 * m * N + m] = (float)cnt;
+}
+
+// One TO trace phase (all threads; few scalar arguments, the solver arrays are re-derived from
+// the shared-memory layout of solve_to_kernel): 0 = entering iteration `it` (before the push),
+// 1 = after the L-BFGS step, 2 = after the selection (thread 0 only writes).
+static __device__ __noinline__ void trace_to(const KParams &kp, int phase, int unit, int it, int tj, float c, float g0d,
+                                             float sy, int istar, float cbest) {
+    extern __shared__ __align__(16) float smem[];
+    const int D = kp.rp.D, N = kp.H * D, Np = (N + 3) & ~3, m = kp.m, A = kp.A;
+    float *th = smem + kp.lay.solver, *g = th + Np, *dd = g + Np, *thp = dd + Np, *gp = thp + Np, *best = gp + Np,
+          *thA = best + Np, *cg = thA + Np, *Sb = cg + A * Np, *Yb = Sb + (m + 1) * Np, *rho = Yb + (m + 1) * Np,
+          *syv = rho + 40, *yyv = syv + 40;
+    const int *order = reinterpret_cast<const int *>(yyv + 40);
+    const float *scal = yyv + 80;
+    const int *ring = reinterpret_cast<const int *>(scal + 24);
+    float *rec = trace_rec(kp, (size_t)unit, tj, N), *sc = rec + CRB_TRACE_REC(N, m) - 24;
+    if (phase == 0) {
+        for (int e = threadIdx.x; e < N; e += NT) {
+            rec[e] = th[e]; rec[N + e] = g[e];
+            rec[2 * N + e] = it > 0 ? thp[e] : 0.f; rec[3 * N + e] = it > 0 ? gp[e] : 0.f;
+        }
+        trace_to_ring(rec + 5 * N, N, Np, m, Sb, Yb, rho, order, ring[0]);
+        if (threadIdx.x == 0) { sc[1] = c; sc[20] = (float)it; }
+    } else if (phase == 1) {
+        for (int e = threadIdx.x; e < N; e += NT) rec[4 * N + e] = dd[e];
+        trace_to_ring(rec + 5 * N + 2 * m * N + m + 1, N, Np, m, Sb, Yb, rho, order, ring[0]);
+        if (threadIdx.x == 0) { sc[0] = g0d; sc[3] = sy; }
+    } else if (threadIdx.x == 0) {
+        sc[2] = (float)istar;
+        for (int a = 0; a < 8; ++a) { sc[4 + a] = a < A ? scal[a] : 0.f; sc[12 + a] = a < A ? scal[8 + a] : 0.f; }
+        sc[21] = cbest;
+    }
+}
+
+// One IK trace phase for seed `lane` of the CTA's group (warp 0, per lane; arrays re-derived from
+// the shared-memory layout of solve_ik_kernel; cnt = the lane's ring count).
+static __device__ __noinline__ void trace_ik(const KParams &kp, int phase, size_t seed_unit, int it, int tj, int cnt,
+                                             float c, float g0d, float sy, int istar, float cbest) {
+    extern __shared__ __align__(16) float smem[];
+    const int D = kp.rp.D, m = kp.m, A = kp.A, DC = D * NC, lane = threadIdx.x & 31;
+    float *th = smem + kp.lay.solver, *g = th + DC, *dd = g + DC, *thp = dd + DC, *gp = thp + DC, *best = gp + DC,
+          *Sb = best + DC, *Yb = Sb + (m + 1) * DC, *rho = Yb + (m + 1) * DC, *syv = rho + (m + 1) * NC,
+          *yyv = syv + (m + 1) * NC, *cg = yyv + (m + 1) * NC, *cc = cg + A * DC, *cgd = cc + A * NC;
+    const int *order = reinterpret_cast<const int *>(cgd + A * NC);
+    float *rec = trace_rec(kp, seed_unit, tj, D), *sc = rec + CRB_TRACE_REC(D, m) - 24;
+    if (phase == 2) {
+        sc[2] = (float)istar;
+        for (int a = 0; a < 8; ++a) { sc[4 + a] = a < A ? cc[a * NC + lane] : 0.f; sc[12 + a] = a < A ? cgd[a * NC + lane] : 0.f; }
+        sc[21] = cbest;
+        return;
+    }
+    float *dst = rec + 5 * D + (phase == 1 ? 2 * m * D + m + 1 : 0);
+    for (int i = 0; i < m; ++i) {
+        const int sl = i < cnt ? order[i * NC + lane] : 0;
+        for (int d = 0; d < D; ++d) {
+            dst[i * D + d] = i < cnt ? Sb[sl * DC + d * NC + lane] : 0.f;
+            dst[(m + i) * D + d] = i < cnt ? Yb[sl * DC + d * NC + lane] : 0.f;
+        }
+        dst[2 * m * D + i] = i < cnt ? rho[sl * NC + lane] : 0.f;
+    }
+    dst[2 * m * D + m] = (float)cnt;
+    if (phase == 0) {
+        for (int d = 0; d < D; ++d) {
+            const int e = d * NC + lane;
+            rec[d] = th[e]; rec[D + d] = g[e];
+            rec[2 * D + d] = it > 0 ? thp[e] : 0.f; rec[3 * D + d] = it > 0 ? gp[e] : 0.f;
+        }
+        sc[1] = c; sc[20] = (float)it;
+    } else {
+        for (int d = 0; d < D; ++d) rec[4 * D + d] = dd[d * NC + lane];
+        sc[0] = g0d; sc[3] = sy;
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -206,7 +309,11 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
         }
         if (a == 0) {
             const int it = (lpass - 1) / A;
-            g0d = lbfgs_step_to(it, N, Np, m, th, g, thp, gp, dd, Sb, Yb, rho, syv, yyv, order, ring, s.red, ph, d_e);
+            const int tj = trace_slot(kp, it);
+            if (tj >= 0) trace_to(kp, 0, unit, it, tj, c, 0.f, 0.f, 0, 0.f);
+            float sy;
+            g0d = lbfgs_step_to(it, N, Np, m, th, g, thp, gp, dd, Sb, Yb, rho, syv, yyv, order, ring, s.red, ph, d_e, sy);
+            if (tj >= 0) trace_to(kp, 1, unit, it, tj, c, g0d, sy, 0, 0.f);
         }
         // ---- a1: candidate a = clip(theta + alpha_a d) (pass 0: theta_0 is already in thA)
         if (a >= 0) {
@@ -309,6 +416,10 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
                     const int i = t + e * NT;
                     if (i < N) best[i] = th[i];
                 }
+            }
+            if (kp.trace) {
+                const int tj = trace_slot(kp, (lpass - 1) / A);
+                if (tj >= 0) trace_to(kp, 2, unit, 0, tj, c, 0.f, 0.f, istar, cbest);
             }
             // ---- a14: "up to" iters in chunks (B20): every thread holds the same cbest, so the
             // exit is CTA-uniform
@@ -415,7 +526,8 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
         if (lpass > 0) {
             const int it = lpass - 1;
             // ---- a13 (identical in every CTA of the cluster)
-            g0d = lbfgs_step_to(it, N, Np, m, th, g, thp, gp, dd, Sb, Yb, rho, syv, yyv, order, ring, s.red, ph, d_e);
+            float sy;
+            g0d = lbfgs_step_to(it, N, Np, m, th, g, thp, gp, dd, Sb, Yb, rho, syv, yyv, order, ring, s.red, ph, d_e, sy);
             // ---- a1: this CTA's candidate
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
@@ -601,9 +713,12 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             }
         if (a == 0 && warp == 0) {
             const int it = (lpass - 1) / A;
+            const int tj = active ? trace_slot(kp, it) : -1;
+            if (tj >= 0) trace_ik(kp, 0, (size_t)p * kp.S + sd, it, tj, cnt, c, 0.f, 0.f, 0, 0.f);
+            float sy = 0.f;
             // ---- ring push (per seed, A20)
             if (it > 0) {
-                float sy = 0.f, yy = 0.f;
+                float yy = 0.f;
                 for (int d = 0; d < D; ++d) {
                     const int e = d * NC + lane;
                     const float sv = th[e] - thp[e], yv = g[e] - gp[e];
@@ -645,6 +760,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             }
             g0d = 0.f;
             for (int d = 0; d < D; ++d) { dd[d * NC + lane] = -q[d]; g0d += g[d * NC + lane] * (-q[d]); }
+            if (tj >= 0) trace_ik(kp, 1, (size_t)p * kp.S + sd, it, tj, cnt, c, g0d, sy, 0, 0.f);
         }
         if (a >= 0) {
             if (a == 0) __syncthreads();   // the L-BFGS step (warp 0) wrote the directions
@@ -732,6 +848,10 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             if (c < cbest) {
                 cbest = c;
                 for (int d = 0; d < D; ++d) best[d * NC + lane] = th[d * NC + lane];
+            }
+            if (kp.trace && active) {
+                const int tj = trace_slot(kp, (lpass - 1) / A);
+                if (tj >= 0) trace_ik(kp, 2, (size_t)p * kp.S + sd, 0, tj, cnt, c, 0.f, 0.f, i, cbest);
             }
         }
     }
@@ -2099,6 +2219,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
         return fail(ctx, CRB_E_ARG, "particle warm-up: iters >= 0, n >= 1, beta > 0, k_mu/k_sigma in [0,1], sigma0_frac >= 0");
     if (sp->check_every < 0 || !(sp->conv_rtol >= 0.f) || sp->cluster < -1 || sp->cluster > 1)
         return fail(ctx, CRB_E_ARG, "check_every >= 0, conv_rtol >= 0, cluster in {-1, 0, 1}");
+    if (sp->trace && (sp->n_trace < 0 || sp->n_trace > 8))
+        return fail(ctx, CRB_E_ARG, "trace: 0 <= n_trace <= 8");
     const int mode = H == 1 ? MODE_IK : MODE_TO;
     const int D = ctx->rp.D;
     if (mode == MODE_TO && (H < 8 || H > 32 || H * D > 512 || (P > 0 && !start)))
@@ -2120,6 +2242,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     kp.k_mu = sp->k_mu; kp.k_sigma = sp->k_sigma; kp.s0_frac = sp->sigma0_frac;
     kp.rng_key = sp->rng_key; kp.prob_base = sp->global_problem_base;
     kp.check_every = sp->check_every; kp.conv_rtol = sp->conv_rtol;
+    kp.trace = sp->n_trace > 0 ? sp->trace : nullptr; kp.n_trace = sp->n_trace;
+    for (int j = 0; j < 8; ++j) kp.trace_iter[j] = j < sp->n_trace ? sp->trace_iter[j] : -1;
     kp.seed_best_cost = sbc; kp.seed_best_traj = sbt;
     const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
     kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
@@ -2135,7 +2259,7 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     const bool fits = units * A_ <= W;
     const bool parts = sp->particle_iters > 0 && units <= 3 * W;
     const bool waves = (double)((units * A_ + W - 1) / W) / (double)A_ * 1.15 < 0.95 * (double)((units + W - 1) / W);
-    const bool clus = sp->n_alpha >= 2 && (sp->particle_iters == 0 || sp->n_particles >= sp->n_alpha) &&
+    const bool clus = sp->n_alpha >= 2 && (sp->particle_iters == 0 || sp->n_particles >= sp->n_alpha) && !kp.trace &&
                       (sp->cluster == 1 || (sp->cluster == -1 && (fits || parts || waves)));
     if (clus && units > 0) {
         const void *kern = mode == MODE_TO

@@ -67,7 +67,8 @@ class crb_solver_params(C.Structure):
                 ("particle_iters", C.c_int), ("n_particles", C.c_int), ("particle_beta", C.c_float),
                 ("k_mu", C.c_float), ("k_sigma", C.c_float), ("sigma0_frac", C.c_float),
                 ("rng_key", C.c_uint32), ("global_problem_base", C.c_int64), ("check_every", C.c_int),
-                ("conv_rtol", C.c_float), ("cluster", C.c_int)]
+                ("conv_rtol", C.c_float), ("cluster", C.c_int), ("trace", C.c_void_p), ("n_trace", C.c_int),
+                ("trace_iter", C.c_int * 8)]
 
 
 _V = C.c_void_p
@@ -140,13 +141,36 @@ def cost_params_struct(cp: inputs.CostParams) -> crb_cost_params:
                            int(cp.flags), cp.a4, cp.a5)
 
 
-def solver_params_struct(sp: inputs.SolverParams, seed_base: int = 0, problem_base: int = 0) -> crb_solver_params:
+def solver_params_struct(sp: inputs.SolverParams, seed_base: int = 0, problem_base: int = 0, trace=None,
+                         trace_iters=()) -> crb_solver_params:
     al = list(sp.alpha) + [0.0] * (8 - len(sp.alpha))
+    ti = list(trace_iters) + [-1] * (8 - len(trace_iters))
     return crb_solver_params(int(sp.iters), int(sp.history), len(sp.alpha), (C.c_float * 8)(*al), float(sp.c1),
                              float(sp.c2), int(sp.ls_mode), int(seed_base), int(sp.particle_iters),
                              int(sp.n_particles), float(sp.particle_beta), float(sp.k_mu), float(sp.k_sigma),
                              float(sp.sigma0_frac), int(sp.rng_key) & 0xFFFFFFFF, int(problem_base),
-                             int(sp.check_every), float(sp.conv_rtol), int(sp.cluster))
+                             int(sp.check_every), float(sp.conv_rtol), int(sp.cluster),
+                             None if trace is None else C.c_void_p(trace.data_ptr()), len(trace_iters),
+                             (C.c_int * 8)(*ti))
+
+
+def trace_rec(N: int, m: int) -> int:
+    """CRB_TRACE_REC(N, m): floats per solver trace record (include/curobo_b200.h)."""
+    return 5 * N + 2 * (2 * m * N + m + 1) + 24
+
+
+def parse_trace(rec, N: int, m: int) -> dict:
+    """One record (numpy float array) -> named fields (header layout of crb_solver_params.trace)."""
+    o = 5 * N
+
+    def ring(off):
+        S = rec[off:off + m * N].reshape(m, N); Y = rec[off + m * N:off + 2 * m * N].reshape(m, N)
+        rho = rec[off + 2 * m * N:off + 2 * m * N + m]; cnt = int(rec[off + 2 * m * N + m])
+        return S[:cnt], Y[:cnt], rho[:cnt], cnt
+    sc = rec[-24:]
+    return dict(x=rec[:N], g=rec[N:2 * N], xp=rec[2 * N:3 * N], gp=rec[3 * N:4 * N], d=rec[4 * N:5 * N],
+                ring_before=ring(o), ring_after=ring(o + 2 * m * N + m + 1), g0d=sc[0], c=sc[1],
+                istar=int(sc[2]), sy=sc[3], ca=sc[4:12], gda=sc[12:20], it=int(sc[20]), best=sc[21])
 
 
 class Context:
@@ -274,8 +298,9 @@ class Context:
         return pe, re
 
     def solve(self, sp: inputs.SolverParams, seeds, goal, start=None, env=None, seed_base: int = 0,
-              seed_outputs: bool = False, problem_base: int = 0, dt=None):
-        """seeds [P,S,H,D] (TO) or [P,S,D] (IK).  Returns dict of device tensors."""
+              seed_outputs: bool = False, problem_base: int = 0, dt=None, trace_iters=()):
+        """seeds [P,S,H,D] (TO) or [P,S,D] (IK).  Returns dict of device tensors; with trace_iters
+        (<= 8 iteration numbers) also "trace" [P,S,len(trace_iters),CRB_TRACE_REC] (parse_trace)."""
         import torch
         P, S = seeds.shape[0], seeds.shape[1]
         H = 1 if seeds.dim() == 3 else seeds.shape[2]
@@ -287,7 +312,12 @@ class Context:
         if seed_outputs:
             out["seed_best_cost"] = torch.empty(P, S, device=dev, dtype=torch.float32)
             out["seed_best_traj"] = torch.empty_like(seeds)
-        s = solver_params_struct(sp, seed_base, problem_base)
+        tr = None
+        if trace_iters:
+            tr = torch.zeros(P, S, len(trace_iters), trace_rec(H * D if H > 1 else D, sp.history), device=dev,
+                             dtype=torch.float32)
+            out["trace"] = tr
+        s = solver_params_struct(sp, seed_base, problem_base, tr, tuple(trace_iters))
         self._chk(_lib.crb_lbfgs_solve_dt(self.h, C.byref(s), P, S, H, _ptr(seeds), _ptr(env), _ptr(start), _ptr(goal),
                                           _ptr(dt), _ptr(out["best_traj"]), _ptr(out["best_cost"]),
                                           _ptr(out["best_key"]), _ptr(out.get("seed_best_cost")),

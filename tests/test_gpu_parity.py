@@ -46,11 +46,17 @@ def make(native, rb, worlds, cp):
 
 
 class Stats:
+    """Per-evaluation parity bookkeeping: the cost and the gradient's 2-norm rule,
+    plus a per-element gradient rule |dg_i| <= 1e-3 ||g||_inf + 1e-5 (no small-magnitude component
+    can hide behind the norm); the worst max-component error over ||g||_inf is reported, and so is
+    the fraction of evaluations excluded by the oracle's branch margin (asserted below 2 %)."""
+
     def __init__(self):
         self.n = 0
         self.excluded = 0
         self.worst_c = 0.0
         self.worst_g = 0.0
+        self.worst_gi = 0.0
 
     def check(self, c_gpu, g_gpu, c_ref, g_ref, margin, label, cost_slack=0.0):
         # cost_slack (converged solutions only, reading B19): an absolute allowance for a cost that
@@ -61,13 +67,20 @@ class Stats:
             return
         ec = abs(c_gpu - c_ref) / (abs(c_ref) * COST_RTOL + COST_ATOL + cost_slack)
         eg = np.linalg.norm(g_gpu - g_ref) / (np.linalg.norm(g_ref) * GRAD_RTOL + GRAD_ATOL * np.sqrt(g_ref.size))
+        ginf = np.abs(g_ref).max() if g_ref.size else 0.0
+        egi = np.abs(g_gpu - g_ref).max() / (GRAD_RTOL * ginf + GRAD_ATOL) if g_ref.size else 0.0
         self.worst_c = max(self.worst_c, ec)
         self.worst_g = max(self.worst_g, eg)
+        self.worst_gi = max(self.worst_gi, egi)
         assert ec <= 1.0, f"{label}: cost gpu={c_gpu} ref={c_ref}"
         assert eg <= 1.0, f"{label}: grad err {np.linalg.norm(g_gpu - g_ref)} vs |g|={np.linalg.norm(g_ref)}"
+        assert egi <= 1.0, f"{label}: grad component err {np.abs(g_gpu - g_ref).max()} vs |g|inf={ginf}"
 
-    def done(self, max_excluded=0.2):
+    def done(self, max_excluded=0.02):
         assert self.n > 0
+        print(f"[parity] {self.n} evals, excluded {self.excluded} ({100.0 * self.excluded / self.n:.2f} %), "
+              f"worst cost {self.worst_c:.3f}, grad-norm {self.worst_g:.3f}, grad-component {self.worst_gi:.3f} "
+              f"(of the tolerances)")
         assert self.excluded <= max_excluded * self.n, f"excluded {self.excluded}/{self.n}"
 
 
@@ -164,7 +177,7 @@ def test_eval_to_parity_planar_cfg1(native, O):
         c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, W, cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"planar {b}")
         active += (t_ref[3] > 0) + (t_ref[4] > 0)
-    stats.done(0.25)
+    stats.done()
     assert active >= 5
     ctx.close()
 
@@ -191,7 +204,7 @@ def test_eval_edge_worlds(native, O):
         stats.check(float(cost[b]), grad[b].cpu().numpy().astype(np.float64), c_ref, g_ref, margin, f"edge {b}")
         if env[b] < 2:
             assert float(terms[b, 4]) == 0.0
-    stats.done(0.5)
+    stats.done()
     ctx.close()
 
 
@@ -216,7 +229,7 @@ def test_eval_ik_parity(native, O, B):
         c_ref, g_ref, t_ref, margin, _ = O.eval_ik(R, O.World(worlds[env[b]]), cp, gl[b], q[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"ik {b}")
         active += t_ref[4] > 0
-    stats.done(0.25)
+    stats.done()
     if B >= 32:
         assert active >= B // 10
     ctx.close()
@@ -488,8 +501,10 @@ def _success_to(O, R, W, cp, start, goal, traj):
 
 
 def test_solve_to_statistical_vs_oracle_planar(native, O):
-    """Config 1: GPU and oracle full solves from the same seeds; success rates agree."""
-    P, S, H = 12, 4, 16
+    """Config 1: GPU and oracle full solves from the same seeds; the GPU's success rate is not
+    below the oracle's by a one-sided two-proportion test at p = 0.01, nor its median best cost
+    above the oracle's by 25 %."""
+    P, S, H = 48, 4, 16
     rb, starts, goals = planar_problems(O, P)
     world = inputs.planar_scene()
     cp = inputs.CostParams(dt=0.25)
@@ -503,34 +518,99 @@ def test_solve_to_statistical_vs_oracle_planar(native, O):
     g_ok = sum(_success_to(O, R, W, cp, starts[p], goals[p], g_traj[p]) for p in range(P))
     o_best = o_traj[np.arange(P), o_cost.argmin(1)]
     o_ok = sum(_success_to(O, R, W, cp, starts[p], goals[p], o_best[p]) for p in range(P))
-    assert g_ok >= o_ok - 2, (g_ok, o_ok)
     g_best = out["best_cost"].cpu().numpy()
-    assert np.median(g_best / o_cost.min(1)) < 2.0
+    ratio = np.median(g_best / o_cost.min(1))
+    print(f"[cfg1 full solve] success GPU {g_ok}/{P} oracle {o_ok}/{P}; median best-cost ratio {ratio:.3f}")
+    assert _two_proportion_z(o_ok, g_ok, P) < 2.326, (g_ok, o_ok)
+    assert ratio < 1.25, ratio
+    ctx.close()
+
+
+def _two_proportion_z(k_a, k_b, n):
+    """z of H0 'the rates are equal' for k_a, k_b successes out of n each (pooled)."""
+    p = (k_a + k_b) / (2.0 * n)
+    if p in (0.0, 1.0):
+        return 0.0
+    return (k_a / n - k_b / n) / np.sqrt(p * (1 - p) * 2.0 / n)
+
+
+def test_solve_to_statistical_vs_oracle_franka_cfg2(native, O):
+    """Config 2 (Franka TO, tabletop K = 20, SWEEP + SPEED, 100 iterations; SURVEY §8(c).4 full-solve
+    comparison on configs 1-3): 32 problems x 8 seeds solved by the GPU and by the fp64 oracle from
+    the same seeds.  Full solves are chaotic (A37), so the comparison is statistical: success (B18
+    pose thresholds 5 mm / 0.05, plus self- and world-collision-free at the evaluated states), the
+    collision-free rate and the pose-error quantiles; the GPU must not be worse than the oracle by a
+    one-sided two-proportion test at p = 0.01 (z < 2.326), and its median best cost must not exceed
+    the oracle's by more than 25 %."""
+    import os
+    from paper_2310_17274_b200 import workload
+    P, S = 32, 8
+    wl = workload.franka_to(0, list(range(P)), S=S, H=32, iters=100, run_seed=4)
+    R = O.Robot(wl.robot)
+    Ws = [O.World(w) for w in wl.worlds]
+    ctx = make(native, wl.robot, wl.worlds, wl.cost)
+    out = ctx.solve(wl.solver, T(wl.seeds), T(wl.goal), start=T(wl.start), env=T(wl.env, torch.int32))
+    g_traj = out["best_traj"].cpu().numpy().astype(np.float64)
+    g_cost = out["best_cost"].cpu().numpy().astype(np.float64)
+    seeds = wl.seeds.astype(np.float64)
+    o_traj, o_cost = O.solve_to(R, Ws, wl.env, wl.cost, wl.solver, seeds, wl.start.astype(np.float64),
+                                wl.goal.astype(np.float64), nthreads=os.cpu_count() or 8)
+    o_best = o_traj[np.arange(P), o_cost.argmin(1)]
+
+    def outcome(p, traj):
+        _, _, t, _, _ = O.eval_traj(R, Ws[p], wl.cost, wl.start[p], wl.goal[p], traj)
+        _, _, ee = O.fk(R, traj[-1])
+        pe = np.linalg.norm(ee[:3] - wl.goal[p][:3])
+        re = 1.0 - abs(float(np.dot(ee[3:], wl.goal[p][3:])))
+        free = t[3] == 0 and t[4] == 0
+        return pe, re, free, pe < 0.005 and re < 0.05 and free
+    g = [outcome(p, g_traj[p]) for p in range(P)]
+    o = [outcome(p, o_best[p]) for p in range(P)]
+    g_ok, o_ok = sum(x[3] for x in g), sum(x[3] for x in o)
+    g_free, o_free = sum(x[2] for x in g), sum(x[2] for x in o)
+    qs = (0.25, 0.5, 0.9)
+    g_pe, o_pe = np.quantile([x[0] for x in g], qs), np.quantile([x[0] for x in o], qs)
+    ratio = np.median(g_cost / o_cost.min(1))
+    print(f"[cfg2 full solve] success GPU {g_ok}/{P} oracle {o_ok}/{P}; collision-free GPU {g_free} oracle {o_free}; "
+          f"pose err q25/50/90 GPU {np.round(g_pe * 1e3, 2)} mm oracle {np.round(o_pe * 1e3, 2)} mm; "
+          f"median best-cost ratio GPU/oracle {ratio:.3f}")
+    assert _two_proportion_z(o_ok, g_ok, P) < 2.326, (g_ok, o_ok)
+    assert _two_proportion_z(o_free, g_free, P) < 2.326, (g_free, o_free)
+    assert ratio < 1.25, ratio
+    assert o_ok >= P // 4, "too few successes to compare: adjust the generator"
     ctx.close()
 
 
 def test_solve_ik_statistical_vs_oracle(native, O):
-    """Config 3 in miniature: collision-free IK, 30 Halton seeds, GPU vs oracle success rates."""
+    """Config 3 in miniature: collision-free IK, 32 goals x 30 Halton seeds, GPU vs oracle: the
+    GPU's success rate (position within 5 mm and orientation within 0.05, B18, collision-free) is
+    not below the oracle's by a one-sided two-proportion test at p = 0.01."""
+    import os
     rb = robots.franka64()
     R = O.Robot(rb)
     world = inputs.tabletop_scene(3, 0, 20)
     W = O.World(world)
     cp = inputs.CostParams()
     ctx = make(native, rb, [world], cp)
-    P, S = 6, 30
+    P, S = 32, 30
     g = np.random.default_rng(11)
     goals = f32(np.array([O.fk(R, g.uniform(rb.lo * 0.6, rb.hi * 0.6))[2] for _ in range(P)]))
     seeds = f32(np.stack([inputs.ik_seeds(rb, p, S) for p in range(P)]))
     sp = inputs.SolverParams(iters=60)
     out = ctx.solve(sp, T(seeds), T(goals), seed_outputs=True)
-    o_q, o_c = O.solve_ik(R, [W], np.zeros(P, np.int32), cp, sp, seeds, goals, nthreads=8)
+    o_q, o_c = O.solve_ik(R, [W], np.zeros(P, np.int32), cp, sp, seeds, goals, nthreads=os.cpu_count() or 8)
 
-    def pos_err(q, goal):
-        return np.linalg.norm(O.fk(R, q)[2][:3] - goal[:3])
+    def success(q, goal):
+        _, _, ee = O.fk(R, q)
+        _, _, t, _, _ = O.eval_ik(R, W, cp, goal, q)
+        return (np.linalg.norm(ee[:3] - goal[:3]) < 0.005 and 1.0 - abs(float(ee[3:] @ goal[3:])) < 0.05
+                and t[3] == 0 and t[4] == 0)
     gq = out["best_traj"].cpu().numpy().astype(np.float64)
-    g_ok = sum(pos_err(gq[p], goals[p]) < 0.01 for p in range(P))
-    o_ok = sum(pos_err(o_q[p, o_c[p].argmin()], goals[p]) < 0.01 for p in range(P))
-    assert g_ok >= o_ok - 1, (g_ok, o_ok)
+    g_ok = sum(success(gq[p], goals[p]) for p in range(P))
+    o_ok = sum(success(o_q[p, o_c[p].argmin()], goals[p]) for p in range(P))
+    print(f"[cfg3 full solve] success GPU {g_ok}/{P} oracle {o_ok}/{P}")
+    assert _two_proportion_z(o_ok, g_ok, P) < 2.326, (g_ok, o_ok)
+    assert o_ok >= P // 4
     sbc = out["seed_best_cost"].cpu().numpy()
     c0, _, _ = ctx.evaluate(T(seeds.reshape(-1, 7)), T(np.repeat(goals, S, 0)))
     assert np.all(sbc.reshape(-1) <= c0.cpu().numpy() * (1 + 1e-6))
@@ -582,7 +662,7 @@ def test_eval_to_parity_dense_k1000(native, O):
         c_ref, g_ref, t_ref, margin, cnt = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"dense {b}")
         active += t_ref[4] > 0
-    stats.done(0.34)
+    stats.done()
     assert active >= 2
     ctx.close()
 
@@ -607,7 +687,7 @@ def test_full_size_solve_sampled_against_oracle(native, O):
                                                  f32(wl.goal[p]), bt[p])
         stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"winner {p}")
         assert bc[p] == sbc[p].min()
-    stats.done(0.5)
+    stats.done()
     # every seed improved on its initial cost
     c0, _, _ = ctx.evaluate(T(wl.seeds.reshape(-1, 32, 7)), T(np.repeat(wl.goal, 32, 0)),
                             start=T(np.repeat(wl.start, 32, 0)), env=T(np.repeat(wl.env, 32), torch.int32))
@@ -644,7 +724,7 @@ def test_full_size_ik_solve_sampled_against_oracle(native, O):
         stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"ik winner {p}",
                     cost_slack=pose_cost_slack(O, R, wl.cost, f32(wl.goal[p]), bq[p].reshape(-1)))
         assert bc[p] == sbc[p].min()
-    stats.done(0.5)
+    stats.done()
     c0, _, _ = ctx.evaluate(T(wl.seeds.reshape(-1, 7)), T(np.repeat(wl.goal, 30, 0)))
     assert np.all(sbc.reshape(-1) <= c0.cpu().numpy() * (1 + 1e-6))
     ctx.close()
@@ -670,7 +750,7 @@ def test_full_size_dense_solve_sampled_against_oracle(native, O):
                                                  f32(wl.goal[p]), bt[p])
         stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"dense winner {p}")
         assert bc[p] == sbc[p].min()
-    stats.done(0.67)
+    stats.done()
     c0, _, _ = ctx.evaluate(T(wl.seeds.reshape(-1, 32, 7)), T(np.repeat(wl.goal, 32, 0)),
                             start=T(np.repeat(wl.start, 32, 0)), env=T(np.repeat(wl.env, 32), torch.int32))
     assert np.all(sbc.reshape(-1) <= c0.cpu().numpy() * (1 + 1e-6))

@@ -96,7 +96,7 @@ def test_eval_to_parity_mma_range(native, O, K, lo, hi, dmax):
         c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"K={K} traj {b}")
         active += t_ref[4] > 0
-    stats.done(0.34)
+    stats.done()
     assert active >= B // 4
     ctx.close()
 
@@ -130,7 +130,7 @@ def test_mma_far_and_huge_cuboids(native, O):
         c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Wo, cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"far {b}")
         assert t_ref[4] > 0                          # the huge cuboid contains the base spheres
-    stats.done(0.34)
+    stats.done()
     # the 20-cuboid prefix through both builds: bitwise equal
     ffma, mma = _pair(native, rb, [small], cp)
     env = T(np.zeros(B, np.int32), torch.int32)
@@ -168,7 +168,7 @@ def test_fp16x2_screen_far_and_huge_cuboids_against_oracle(native, O):
         c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Wo, cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"h2 far {b}")
         assert t_ref[4] > 0
-    stats.done(0.5)        # deep inside the huge cuboid: many nearest-face ties (margin exclusions)
+    stats.done()        # deep inside the huge cuboid: many nearest-face ties (margin exclusions)
     ctx.close()
 
 
@@ -219,7 +219,7 @@ def test_random_robot_eval_parity_both_builds(native, O, seed, big):
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"rand TO {b}")
         active_w += t_ref[4] > 0
         active_s += t_ref[3] > 0
-    stats.done(0.34)
+    stats.done()
     assert active_w >= 2 and active_s >= 2
     # IK mode (one configuration per row, all in the first environment)
     Q = f32(g.uniform(-1.5, 1.5, (40, D)))
@@ -230,7 +230,7 @@ def test_random_robot_eval_parity_both_builds(native, O, seed, big):
     for b in range(40):
         c_ref, g_ref, _, margin, _ = O.eval_ik(R, Ws[0], cp, glq[b], Q[b])
         stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, margin, f"rand IK {b}")
-    stats.done(0.34)
+    stats.done()
     ctx.close()
 
 
@@ -283,7 +283,7 @@ def test_capacity_robot_parity(native, O, big):
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"cap TO {b}")
         active_w += t_ref[4] > 0
         active_s += t_ref[3] > 0
-    stats.done(0.34)
+    stats.done()
     assert active_w >= 2 and active_s >= 2, (active_w, active_s)   # not vacuous
     Q = f32(g.uniform(-1.5, 1.5, (40, D)))
     glq = f32(np.repeat(gl[:1], 40, 0))
@@ -293,7 +293,7 @@ def test_capacity_robot_parity(native, O, big):
     for b in range(40):
         c_ref, g_ref, _, margin, _ = O.eval_ik(R, Ws[0], cp, glq[b], Q[b])
         stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, margin, f"cap IK {b}")
-    stats.done(0.34)
+    stats.done()
     sp = inputs.SolverParams(iters=8)
     seeds = V.reshape(2, 5, H, D)
     runs = [ctx.solve(sp, T(seeds), T(gl[:2]), start=T(st[:2]), env=T(env[:2], torch.int32), seed_outputs=True)
