@@ -19,8 +19,28 @@
 #define ORC_INF (1.0 / 0.0)
 #define ORC_NAN (0.0 / 0.0)
 
-static void upd_margin(double *margin, double v) {
-    if (margin && fabs(v) < *margin) *margin = fabs(v);
+/* O10 margin kinds (diagnostics: which branch set the smallest margin of the last evaluation):
+ * 1 self max(0, P*) switch, 2 self top-2 gap, 3 inside-box nearest-face tie, 4 sweep exit,
+ * 5 sign of <q_g, q>. */
+static _Thread_local int g_margin_kind = 0;
+
+int orc_margin_kind(void) { return g_margin_kind; }
+
+/* Per-state split of the margin (O10, optional; orc_set_state_margins): the margins of the
+ * branches evaluated at state h (gradient discontinuities there move only the gradient rows of
+ * that state) and, separately, the margins of COST discontinuities (the sweep exit). */
+static _Thread_local double *g_state_margin = NULL;   /* [H] or NULL */
+static _Thread_local int g_state_idx = -1;
+static _Thread_local double g_cost_margin = 1.0 / 0.0;
+
+void orc_set_state_margins(double *buf) { g_state_margin = buf; }
+double orc_cost_margin(void) { return g_cost_margin; }
+
+static void upd_margin_k(double *margin, double v, int kind) {
+    if (margin && fabs(v) < *margin) { *margin = fabs(v); g_margin_kind = kind; }
+    if (margin && g_state_margin && g_state_idx >= 0 && fabs(v) < g_state_margin[g_state_idx])
+        g_state_margin[g_state_idx] = fabs(v);
+    if (margin && kind == 4 && fabs(v) < g_cost_margin) g_cost_margin = fabs(v);
 }
 
 /* Margin kinds: upd_margin for branches where the COST jumps (a sweep sample that appears or
@@ -31,8 +51,8 @@ static _Thread_local int g_cost_only_margins = 0;
 
 void orc_set_margin_mode(int cost_only) { g_cost_only_margins = cost_only; }
 
-static void upd_margin_grad(double *margin, double v) {
-    if (!g_cost_only_margins) upd_margin(margin, v);
+static void upd_margin_grad(double *margin, double v, int kind) {
+    if (!g_cost_only_margins) upd_margin_k(margin, v, kind);
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -272,7 +292,7 @@ static double box_sdf_impl(const double *p, const double *pos, const double *qua
             double second = -ORC_INF;
             for (int i = 0; i < 3; ++i)
                 if (i != imax && qv[i] > second) second = qv[i];
-            upd_margin_grad(margin, qmax - second);
+            upd_margin_grad(margin, qmax - second, 3);
         }
     }
     if (grad)
@@ -354,7 +374,7 @@ double orc_sphere_world(const orc_world *w, const double *c, const double *cprev
                     double kb = j / L;
                     double pb[3] = {c[0] + kb * dv[0], c[1] + kb * dv[1], c[2] + kb * dv[2]};
                     double sdb = box_sdf_impl(pb, w->pos + 3 * k, w->quat + 4 * k, w->half + 3 * k, NULL, NULL);
-                    if (rp - sdb > -1e-6) upd_margin(margin, j - bound);
+                    if (rp - sdb > -1e-6) upd_margin_k(margin, j - bound, 4);
                 }
                 if (j >= bound) break;
                 double kappa = j / L;
@@ -397,9 +417,9 @@ double orc_self_collision(const orc_robot *rb, const double *spheres, double bet
     }
     if (arg_pair) *arg_pair = -1;
     if (ibest < 0) return 0.0;
-    upd_margin_grad(margin, best);
+    upd_margin_grad(margin, best, 1);
     if (best <= 0) return 0.0;
-    if (margin && second > -ORC_INF) upd_margin_grad(margin, best - second);
+    if (margin && second > -ORC_INF) upd_margin_grad(margin, best - second, 2);
     if (arg_pair) *arg_pair = ibest;
     int i = rb->pairs[2 * ibest], j = rb->pairs[2 * ibest + 1];
     double u[3] = {spheres[i * 4] - spheres[j * 4], spheres[i * 4 + 1] - spheres[j * 4 + 1],
@@ -526,6 +546,10 @@ double orc_eval_traj(const orc_robot *rb, const orc_world *w, const orc_params *
                      const double *start, const double *goal, const double *V, int H,
                      double *grad, double *terms, double *margin, long long *counters) {
     int D = rb->n_dof, M = rb->n_spheres;
+    g_margin_kind = 0;
+    g_cost_margin = 1.0 / 0.0;
+    if (g_state_margin)
+        for (int h = 0; h < H; ++h) g_state_margin[h] = 1.0 / 0.0;
     double *x = calloc((size_t)(H + 5) * D, sizeof(double));
     double *v = calloc((size_t)H * D, sizeof(double)), *a = calloc((size_t)H * D, sizeof(double)),
            *jk = calloc((size_t)H * D, sizeof(double));
@@ -560,6 +584,7 @@ double orc_eval_traj(const orc_robot *rb, const orc_world *w, const orc_params *
         /* FK (O4) */
         orc_fk(rb, XR(h), NULL, sph + h * M * 4, (h == H) ? ee : NULL);
         /* self-collision (O5) */
+        g_state_idx = h - 1;
         tm[3] += orc_self_collision(rb, sph + h * M * 4, pr->beta_self, gs + h * M * 3, NULL,
                                     margin, counters);
     }
@@ -570,6 +595,7 @@ double orc_eval_traj(const orc_robot *rb, const orc_world *w, const orc_params *
             double r = rb->sph[m * 4 + 3];
             if (r < 0) continue;                                        /* P:2842 */
             const double *c = sph + (h * M + m) * 4;
+            g_state_idx = h - 1;
             const double *cp = (h > 1) ? sph + ((h - 1) * M + m) * 4 : NULL;
             const double *cn = (h < H) ? sph + ((h + 1) * M + m) * 4 : NULL;
             double sp = 1.0;
@@ -593,8 +619,10 @@ double orc_eval_traj(const orc_robot *rb, const orc_world *w, const orc_params *
         for (int d = 0; d < D; ++d) GX(H)[d] += tmp[d];
     } else {
         tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
-        if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
+        g_state_idx = H - 1;
+        if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6], 5);
     }
+    g_state_idx = -1;
     /* backward (O6) per evaluated configuration */
     for (int h = 1; h <= H; ++h) {
         int pose = (h == H) && !cspace;
@@ -635,6 +663,10 @@ double orc_eval_ik(const orc_robot *rb, const orc_world *w, const orc_params *pr
                    const double *goal, const double *q, double *grad, double *terms,
                    double *margin, long long *counters) {
     int D = rb->n_dof, M = rb->n_spheres;
+    g_margin_kind = 0;
+    g_cost_margin = 1.0 / 0.0;
+    if (g_state_margin) g_state_margin[0] = 1.0 / 0.0;
+    g_state_idx = 0;
     double *sph = calloc((size_t)M * 4, sizeof(double)), *gs = calloc((size_t)M * 3, sizeof(double));
     double *gb = calloc((size_t)D, sizeof(double));
     double ee[7], tm[5] = {0, 0, 0, 0, 0};
@@ -658,8 +690,9 @@ double orc_eval_ik(const orc_robot *rb, const orc_world *w, const orc_params *pr
         tm[0] = orc_cspace_cost(pr, D, q, goal, gc);          /* Eq. cspace-cost */
     } else {
         tm[0] = orc_pose_cost(pr, ee, goal, gp, gq);
-        if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6]);
+        if (margin) upd_margin_grad(margin, goal[3] * ee[3] + goal[4] * ee[4] + goal[5] * ee[5] + goal[6] * ee[6], 5);
     }
+    g_state_idx = -1;
     if (grad) {
         orc_fk_backward(rb, q, gs, cspace ? NULL : gp, cspace ? NULL : gq, grad);
         for (int d = 0; d < D; ++d) grad[d] += gb[d] + gc[d];

@@ -79,6 +79,17 @@ typedef struct {
  * switch (j += r' vs j += sd: equal at sd = r') and the gap test are C1 there and need no margin.
  * counters[] layout: */
 void orc_set_margin_mode(int cost_only);   /* 1: record cost-discontinuity margins only (this thread) */
+/* Which branch set the smallest margin of this thread's last orc_eval_traj / orc_eval_ik: 0 none,
+ * 1 self max(0, P*) switch, 2 self top-2 gap, 3 inside-box nearest-face tie, 4 sweep exit,
+ * 5 sign of <q_g, q> (diagnostics of the parity exclusions). */
+int  orc_margin_kind(void);
+/* Optional per-state margins of this thread's next evaluations: buf[H] (IK: buf[1]) receives, per
+ * evaluated state h = 1..H at index h - 1, the smallest margin of the branches evaluated at that
+ * state (their gradient discontinuities move only that state's gradient rows); NULL turns it off.
+ * orc_cost_margin() is the smallest margin of a COST discontinuity (the sweep exit) of the last
+ * evaluation.  Diagnostics for the parity tests (O10). */
+void orc_set_state_margins(double *buf);
+double orc_cost_margin(void);
 enum { ORC_CNT_BOX_TESTS = 0, ORC_CNT_BOX_HITS, ORC_CNT_SWEEP_SAMPLES, ORC_CNT_SWEEP_HITS,
        ORC_CNT_PAIR_TESTS, ORC_CNT_PAIR_PEN, ORC_CNT_ACTIVE_SPHERES, ORC_CNT_N };
 

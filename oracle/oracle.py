@@ -78,6 +78,8 @@ def lib():
     if _lib is None:
         build()
         L = C.CDLL(LIB)
+        L.orc_set_state_margins.argtypes = [D_P]
+        L.orc_cost_margin.restype = C.c_double
         L.orc_box_sdf.restype = C.c_double
         L.orc_activation.restype = C.c_double
         L.orc_bound.restype = C.c_double
@@ -270,9 +272,14 @@ def cspace_cost(cp, q, goal):
     return c, g
 
 
-def eval_traj(robot: Robot, world: World, cp, start, goal, V):
+def eval_traj(robot: Robot, world: World, cp, start, goal, V, state_margins=False):
+    """O7 whole evaluation: (cost, grad [H][D], terms[5], margin, counters); with state_margins=True
+    also (per-state margins [H], cost-discontinuity margin) appended (O10 split)."""
     V = _d(V)
     H = V.shape[0]
+    sm = np.full(H, np.inf)
+    if state_margins:
+        lib().orc_set_state_margins(_dp(sm))
     g = np.zeros_like(V)
     terms = np.zeros(5)
     margin = C.c_double(np.inf)
@@ -280,9 +287,15 @@ def eval_traj(robot: Robot, world: World, cp, start, goal, V):
     pr = params(cp)
     lib().orc_eval_traj.argtypes = [C.POINTER(_Robot), C.POINTER(_World), C.POINTER(_Params),
                                     D_P, D_P, D_P, C.c_int, D_P, D_P, D_P, LL_P]
-    c = lib().orc_eval_traj(C.byref(robot.s), C.byref(world.s), C.byref(pr), _dp(_d(start)),
-                            _dp(_d(goal)), _dp(V), H, _dp(g), _dp(terms), C.byref(margin),
-                            cnt.ctypes.data_as(LL_P))
+    try:
+        c = lib().orc_eval_traj(C.byref(robot.s), C.byref(world.s), C.byref(pr), _dp(_d(start)),
+                                _dp(_d(goal)), _dp(V), H, _dp(g), _dp(terms), C.byref(margin),
+                                cnt.ctypes.data_as(LL_P))
+    finally:
+        if state_margins:
+            lib().orc_set_state_margins(None)
+    if state_margins:
+        return c, g, terms, margin.value, cnt, sm, lib().orc_cost_margin()
     return c, g, terms, margin.value, cnt
 
 
@@ -484,6 +497,11 @@ def steer(robot: Robot, world: World, src, dst, dw, r, margin=0.0):
     n = L.orc_steer(C.byref(robot.s), C.byref(world.s), E, _dp(src), _dp(dst), _dp(_d(dw)), float(r),
                     float(margin), _ip(h), _dp(v), _dp(dist), _dp(mg))
     return n, h, v, dist, mg
+
+
+def margin_kind():
+    """O10: the branch kind behind the last evaluation's margin (oracle.h orc_margin_kind)."""
+    return int(lib().orc_margin_kind())
 
 
 class cost_only_margins:

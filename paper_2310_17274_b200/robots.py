@@ -50,16 +50,18 @@ _FRANKA_LINKS = [
     (10, 0, -1, _F(_I, [0, 0, 0])),                 # 13 attached object (spheres disabled)
 ]
 
-# (link, n, start, end, radius)
+# (link, n, start, end, radius).  A child link's first sphere starts 1-1.5 cm past its joint origin,
+# where the parent's last sphere sits: coincident duplicate spheres would give every pair with a
+# third sphere an exact twin (ties of the self-collision arg-max, A28, at every configuration).
 _FRANKA_SEGMENTS = [
     (0, 4, [0, 0, 0.06], [0, 0, 0.20], 0.08),
     (1, 6, [0, 0, -0.13], [0, 0, 0.0], 0.07),
-    (2, 6, [0, 0, 0.0], [0, -0.18, 0.0], 0.07),
+    (2, 6, [0, -0.015, 0.0], [0, -0.18, 0.0], 0.07),
     (3, 7, [0, 0, -0.14], [0.0825, 0, 0.0], 0.065),
-    (4, 7, [0, 0, 0.0], [-0.0825, 0.12, 0.0], 0.065),
+    (4, 7, [-0.01, 0.015, 0.0], [-0.0825, 0.12, 0.0], 0.065),
     (5, 10, [0, 0, -0.26], [0, 0, 0.0], 0.06),
-    (6, 6, [0, 0, 0.0], [0.088, 0, 0.0], 0.06),
-    (7, 5, [0, 0, 0.0], [0, 0, 0.08], 0.05),
+    (6, 6, [0.012, 0, 0.0], [0.088, 0, 0.0], 0.06),
+    (7, 5, [0, 0, 0.012], [0, 0, 0.08], 0.05),
     (9, 7, [0, -0.09, 0.04], [0, 0.09, 0.04], 0.04),
     (11, 2, [0, 0.008, 0.015], [0, 0.008, 0.04], 0.02),
     (12, 2, [0, -0.008, 0.015], [0, -0.008, 0.04], 0.02),

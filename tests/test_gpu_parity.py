@@ -45,15 +45,33 @@ def make(native, rb, worlds, cp):
     return ctx
 
 
+def traj_rows(H, state_mask):
+    """V rows whose gradient takes the FK-backward contribution of the masked states (O2 routing:
+    x_1..x_3 pinned -> none, x_h for 4 <= h <= H-4 -> V_{h-1}, x_{H-3..H} -> V_{H-1})."""
+    rows = set()
+    for h in np.flatnonzero(state_mask) + 1:
+        if 4 <= h <= H - 4:
+            rows.add(h - 1)
+        elif h >= H - 3:
+            rows.add(H - 1)
+    return sorted(rows)
+
+
 class Stats:
     """Per-evaluation parity bookkeeping: the cost and the gradient's 2-norm rule,
     plus a per-element gradient rule |dg_i| <= 1e-3 ||g||_inf + 1e-5 (no small-magnitude component
-    can hide behind the norm); the worst max-component error over ||g||_inf is reported, and so is
-    the fraction of evaluations excluded by the oracle's branch margin (asserted below 2 %)."""
+    can hide behind the norm).  Exclusions follow the oracle's O10 margins (< 2e-5): a margin may
+    be a float (whole evaluation), ("ik", m) (IK: every branch there is a gradient
+    discontinuity, so only the gradient is excluded) or (state_margins [H], cost_margin) from
+    O.eval_traj(..., state_margins=True) (TO: a COST discontinuity, the sweep exit, excludes the
+    trajectory; a gradient discontinuity at state h excludes only the V rows state h feeds).  The
+    worst errors and the excluded fractions are printed; both fractions are asserted below 2 %."""
 
     def __init__(self):
         self.n = 0
-        self.excluded = 0
+        self.excluded = 0          # evaluations whose cost is not compared
+        self.rows = 0              # gradient rows (TO: V rows, IK: one per evaluation)
+        self.rows_excluded = 0
         self.worst_c = 0.0
         self.worst_g = 0.0
         self.worst_gi = 0.0
@@ -62,26 +80,57 @@ class Stats:
         # cost_slack (converged solutions only, reading B19): an absolute allowance for a cost that
         # is a small residual of fp32 kinematics (see pose_cost_slack)
         self.n += 1
-        if margin < MARGIN:
+        g_gpu = np.asarray(g_gpu, np.float64)
+        g_ref = np.asarray(g_ref, np.float64)
+        if isinstance(margin, tuple) and margin[0] == "ik":
+            cost_ok, keep = True, margin[1] >= MARGIN
+            rows, nrows = (slice(None) if keep else slice(0, 0)), 1
+            self.rows += 1
+            self.rows_excluded += 0 if keep else 1
+        elif isinstance(margin, tuple):
+            sm, cm = margin
+            cost_ok = cm >= MARGIN
+            H = g_ref.shape[0]
+            bad = traj_rows(H, np.asarray(sm) < MARGIN)
+            rows = [h for h in range(H) if h not in bad]
+            self.rows += H
+            self.rows_excluded += len(bad)
+        else:
+            cost_ok = margin >= MARGIN
+            rows = slice(None) if cost_ok else slice(0, 0)
+            self.rows += 1
+            self.rows_excluded += 0 if cost_ok else 1
+        if not cost_ok:
             self.excluded += 1
             return
         ec = abs(c_gpu - c_ref) / (abs(c_ref) * COST_RTOL + COST_ATOL + cost_slack)
-        eg = np.linalg.norm(g_gpu - g_ref) / (np.linalg.norm(g_ref) * GRAD_RTOL + GRAD_ATOL * np.sqrt(g_ref.size))
-        ginf = np.abs(g_ref).max() if g_ref.size else 0.0
-        egi = np.abs(g_gpu - g_ref).max() / (GRAD_RTOL * ginf + GRAD_ATOL) if g_ref.size else 0.0
         self.worst_c = max(self.worst_c, ec)
+        assert ec <= 1.0, f"{label}: cost gpu={c_gpu} ref={c_ref}"
+        gg, gr = g_gpu[rows], g_ref[rows]
+        if gr.size == 0:
+            return
+        eg = np.linalg.norm(gg - gr) / (np.linalg.norm(gr) * GRAD_RTOL + GRAD_ATOL * np.sqrt(gr.size))
+        ginf = np.abs(gr).max()
+        egi = np.abs(gg - gr).max() / (GRAD_RTOL * ginf + GRAD_ATOL)
         self.worst_g = max(self.worst_g, eg)
         self.worst_gi = max(self.worst_gi, egi)
-        assert ec <= 1.0, f"{label}: cost gpu={c_gpu} ref={c_ref}"
-        assert eg <= 1.0, f"{label}: grad err {np.linalg.norm(g_gpu - g_ref)} vs |g|={np.linalg.norm(g_ref)}"
-        assert egi <= 1.0, f"{label}: grad component err {np.abs(g_gpu - g_ref).max()} vs |g|inf={ginf}"
+        assert eg <= 1.0, f"{label}: grad err {np.linalg.norm(gg - gr)} vs |g|={np.linalg.norm(gr)}"
+        assert egi <= 1.0, f"{label}: grad component err {np.abs(gg - gr).max()} vs |g|inf={ginf}"
 
     def done(self, max_excluded=0.02):
         assert self.n > 0
-        print(f"[parity] {self.n} evals, excluded {self.excluded} ({100.0 * self.excluded / self.n:.2f} %), "
-              f"worst cost {self.worst_c:.3f}, grad-norm {self.worst_g:.3f}, grad-component {self.worst_gi:.3f} "
-              f"(of the tolerances)")
+        print(f"[parity] {self.n} evals: cost excluded {self.excluded} ({100.0 * self.excluded / self.n:.2f} %), "
+              f"gradient rows excluded {self.rows_excluded}/{self.rows} "
+              f"({100.0 * self.rows_excluded / max(self.rows, 1):.2f} %); worst cost {self.worst_c:.3f}, "
+              f"grad-norm {self.worst_g:.3f}, grad-component {self.worst_gi:.3f} (of the tolerances)")
         assert self.excluded <= max_excluded * self.n, f"excluded {self.excluded}/{self.n}"
+        assert self.rows_excluded <= max_excluded * self.rows, f"rows excluded {self.rows_excluded}/{self.rows}"
+
+
+def ref_traj(O, R, W, cp, start, goal, V):
+    """Oracle evaluation with the per-state margin split: (c, g, terms, (state_margins, cost_margin))."""
+    c, g, t, _, _, sm, cm = O.eval_traj(R, W, cp, start, goal, V, state_margins=True)
+    return c, g, t, (sm, cm)
 
 
 # ------------------------------------------------------------------------------------------ FK
@@ -128,7 +177,7 @@ def franka_trajs(seed, B, H, noise=0.25):
     (8, inputs.SPEED | inputs.JERK, "random"),
 ])
 def test_eval_to_parity_franka(native, O, H, flags, scene):
-    B = 24
+    B = 96
     rb, starts, goals_cfg, trajs = franka_trajs(10 + H + flags, B, H)
     if scene == "tabletop":
         worlds = [inputs.tabletop_scene(1, e, 20) for e in range(3)]
@@ -147,9 +196,9 @@ def test_eval_to_parity_franka(native, O, H, flags, scene):
     stats = Stats()
     world_active = 0
     for b in range(B):
-        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, Ws[env[b]], cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"traj {b}")
-        if margin >= MARGIN:
+        if margin[1] >= MARGIN:
             np.testing.assert_allclose(terms[b], t_ref, rtol=1e-4, atol=1e-3)
         world_active += t_ref[4] > 0
     stats.done()
@@ -174,7 +223,7 @@ def test_eval_to_parity_planar_cfg1(native, O):
     stats = Stats()
     active = 0
     for b in range(B):
-        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, W, cp, st[b], gl[b], V[b])
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, W, cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"planar {b}")
         active += (t_ref[3] > 0) + (t_ref[4] > 0)
     stats.done()
@@ -200,7 +249,7 @@ def test_eval_edge_worlds(native, O):
     cost, grad, terms = ctx.evaluate(T(V), T(gl), start=T(st), env=T(env, torch.int32))
     stats = Stats()
     for b in range(6):
-        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, O.World(worlds[env[b]]), cp, st[b], gl[b], V[b])
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, O.World(worlds[env[b]]), cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].cpu().numpy().astype(np.float64), c_ref, g_ref, margin, f"edge {b}")
         if env[b] < 2:
             assert float(terms[b, 4]) == 0.0
@@ -227,7 +276,7 @@ def test_eval_ik_parity(native, O, B):
     active = 0
     for b in range(B):
         c_ref, g_ref, t_ref, margin, _ = O.eval_ik(R, O.World(worlds[env[b]]), cp, gl[b], q[b])
-        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"ik {b}")
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, ("ik", margin), f"ik {b}")
         active += t_ref[4] > 0
     stats.done()
     if B >= 32:
@@ -644,7 +693,7 @@ def test_error_statuses(native):
 def test_eval_to_parity_dense_k1000(native, O):
     """Config 5 geometry: 1000 small cuboids per environment, swept + speed (cuboid table 64 KB in
     shared memory, so one CTA per SM)."""
-    B, H = 6, 32
+    B, H = 24, 32
     rb, starts, goals_cfg, trajs = franka_trajs(555, B, H, noise=0.4)
     worlds = [inputs.dense_scene(4, e, 1000) for e in range(2)]
     cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED, dt=0.25)
@@ -659,7 +708,7 @@ def test_eval_to_parity_dense_k1000(native, O):
     stats = Stats()
     active = 0
     for b in range(B):
-        c_ref, g_ref, t_ref, margin, cnt = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, Ws[env[b]], cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"dense {b}")
         active += t_ref[4] > 0
     stats.done()
@@ -683,7 +732,7 @@ def test_full_size_solve_sampled_against_oracle(native, O):
     R = O.Robot(wl.robot)
     stats = Stats()
     for p in (0, 17, 38, 63):
-        c_ref, g_ref, _, margin, _ = O.eval_traj(R, O.World(wl.worlds[p]), wl.cost, f32(wl.start[p]),
+        c_ref, g_ref, _, margin = ref_traj(O, R, O.World(wl.worlds[p]), wl.cost, f32(wl.start[p]),
                                                  f32(wl.goal[p]), bt[p])
         stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"winner {p}")
         assert bc[p] == sbc[p].min()
@@ -721,7 +770,7 @@ def test_full_size_ik_solve_sampled_against_oracle(native, O):
     stats = Stats()
     for p in (0, 1, 257, 511, 768, 999):
         c_ref, g_ref, _, margin, _ = O.eval_ik(R, W, wl.cost, f32(wl.goal[p]), bq[p].reshape(-1))
-        stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"ik winner {p}",
+        stats.check(float(bc[p]), g_ref, c_ref, g_ref, ("ik", margin), f"ik winner {p}",
                     cost_slack=pose_cost_slack(O, R, wl.cost, f32(wl.goal[p]), bq[p].reshape(-1)))
         assert bc[p] == sbc[p].min()
     stats.done()
@@ -746,7 +795,7 @@ def test_full_size_dense_solve_sampled_against_oracle(native, O):
     R = O.Robot(wl.robot)
     stats = Stats()
     for p in (0, 7, 15):
-        c_ref, g_ref, _, margin, _ = O.eval_traj(R, O.World(wl.worlds[p]), wl.cost, f32(wl.start[p]),
+        c_ref, g_ref, _, margin = ref_traj(O, R, O.World(wl.worlds[p]), wl.cost, f32(wl.start[p]),
                                                  f32(wl.goal[p]), bt[p])
         stats.check(float(bc[p]), g_ref, c_ref, g_ref, margin, f"dense winner {p}")
         assert bc[p] == sbc[p].min()

@@ -15,7 +15,7 @@ import torch
 
 from paper_2310_17274_b200 import inputs, robots
 
-from test_gpu_parity import MARGIN, Stats, T, f32, franka_trajs, make  # noqa: F401
+from test_gpu_parity import ref_traj, MARGIN, Stats, T, f32, franka_trajs, make  # noqa: F401
 
 pytestmark = pytest.mark.gpu
 
@@ -77,7 +77,7 @@ def test_mma_and_ffma_builds_bitwise_equal_ik_and_solves(native, O):
 def test_eval_to_parity_mma_range(native, O, K, lo, hi, dmax):
     """Oracle parity with the HMMA build: K = 72, 77 (ragged last 8-cuboid tile), 203 (~10 %
     disabled, so the enabled counts stay >= 64); rotated cuboids."""
-    B, H = 16, 32
+    B, H = 48, 32
     rb, starts, goals_cfg, trajs = franka_trajs(300 + K, B, H, noise=0.4)
     worlds = [inputs.random_world(11, e, K, lo=lo, hi=hi, dmax=dmax) for e in range(2)]
     assert max(int(w.enabled.sum()) for w in worlds) >= MMA_MIN_K     # the HMMA build runs
@@ -93,7 +93,7 @@ def test_eval_to_parity_mma_range(native, O, K, lo, hi, dmax):
     stats = Stats()
     active = 0
     for b in range(B):
-        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, Ws[env[b]], cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"K={K} traj {b}")
         active += t_ref[4] > 0
     stats.done()
@@ -105,7 +105,7 @@ def test_mma_far_and_huge_cuboids(native, O):
     """Cuboids far outside the workspace (large offsets, still inside the fp16 range) and one
     beyond it (|offset| > 3e4 m: the pre-screen flags it and the exact test decides) next to a
     cuboid the arm penetrates: costs equal the FFMA build and the oracle."""
-    B, H = 8, 32
+    B, H = 32, 32
     rb, starts, goals_cfg, trajs = franka_trajs(808, B, H, noise=0.3)
     base = inputs.random_world(12, 0, 70, lo=-0.8, hi=0.8, disabled_frac=0.0)
     pos = base.pos.copy(); dims = base.dims.copy()
@@ -127,7 +127,7 @@ def test_mma_far_and_huge_cuboids(native, O):
     Wo = O.World(w)
     stats = Stats()
     for b in range(B):
-        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Wo, cp, st[b], gl[b], V[b])
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, Wo, cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"far {b}")
         assert t_ref[4] > 0                          # the huge cuboid contains the base spheres
     stats.done()
@@ -145,7 +145,7 @@ def test_fp16x2_screen_far_and_huge_cuboids_against_oracle(native, O):
     """The small-world build (fp16x2 pre-screen, K < 64) on cuboids far outside the workspace, one
     beyond the fp16 range (forced to the exact test), one huge cuboid containing the arm's base,
     and one in the arm's way: oracle parity."""
-    B, H = 16, 32
+    B, H = 48, 32
     rb, starts, goals_cfg, trajs = franka_trajs(809, B, H, noise=0.3)
     base = inputs.random_world(13, 0, 24, lo=-0.8, hi=0.8, disabled_frac=0.0)
     pos = base.pos.copy(); dims = base.dims.copy(); quat = base.quat.copy()
@@ -165,7 +165,7 @@ def test_fp16x2_screen_far_and_huge_cuboids_against_oracle(native, O):
     Wo = O.World(w)
     stats = Stats()
     for b in range(B):
-        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Wo, cp, st[b], gl[b], V[b])
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, Wo, cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"h2 far {b}")
         assert t_ref[4] > 0
     stats.done()        # deep inside the huge cuboid: many nearest-face ties (margin exclusions)
@@ -196,7 +196,7 @@ def test_random_robot_eval_parity_both_builds(native, O, seed, big):
     fp16x2 build (K = 30) and the HMMA build (an extra 70-cuboid environment), plus an empty
     environment."""
     rb = _random_robot(seed)
-    D, H, B = rb.n_dof, 16, 12
+    D, H, B = rb.n_dof, 16, 48
     g = np.random.default_rng(seed)
     worlds = [inputs.random_world(20 + seed, 0, 30, lo=-0.9, hi=0.9, dmax=0.3),
               inputs.World(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros(0, np.int32))]
@@ -215,7 +215,7 @@ def test_random_robot_eval_parity_both_builds(native, O, seed, big):
     stats = Stats()
     active_w = active_s = 0
     for b in range(B):
-        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, Ws[env[b]], cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"rand TO {b}")
         active_w += t_ref[4] > 0
         active_s += t_ref[3] > 0
@@ -229,7 +229,7 @@ def test_random_robot_eval_parity_both_builds(native, O, seed, big):
     stats = Stats()
     for b in range(40):
         c_ref, g_ref, _, margin, _ = O.eval_ik(R, Ws[0], cp, glq[b], Q[b])
-        stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, margin, f"rand IK {b}")
+        stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, ("ik", margin), f"rand IK {b}")
     stats.done()
     ctx.close()
 
@@ -259,7 +259,7 @@ def test_capacity_robot_parity(native, O, big):
     and IK evaluations against the oracle in both world builds; short solves are bitwise
     repeatable and never worse than their seeds."""
     rb = capacity_robot()
-    D, H, B = rb.n_dof, 32, 10
+    D, H, B = rb.n_dof, 32, 40
     g = np.random.default_rng(43)
     worlds = [inputs.random_world(61, 0, 24, lo=-1.2, hi=1.2, dmax=0.3)]
     if big:
@@ -279,7 +279,7 @@ def test_capacity_robot_parity(native, O, big):
     stats = Stats()
     active_w = active_s = 0
     for b in range(B):
-        c_ref, g_ref, t_ref, margin, _ = O.eval_traj(R, Ws[env[b]], cp, st[b], gl[b], V[b])
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, Ws[env[b]], cp, st[b], gl[b], V[b])
         stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"cap TO {b}")
         active_w += t_ref[4] > 0
         active_s += t_ref[3] > 0
@@ -292,17 +292,17 @@ def test_capacity_robot_parity(native, O, big):
     stats = Stats()
     for b in range(40):
         c_ref, g_ref, _, margin, _ = O.eval_ik(R, Ws[0], cp, glq[b], Q[b])
-        stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, margin, f"cap IK {b}")
+        stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, ("ik", margin), f"cap IK {b}")
     stats.done()
     sp = inputs.SolverParams(iters=8)
-    seeds = V.reshape(2, 5, H, D)
+    seeds = V[:10].reshape(2, 5, H, D)
     runs = [ctx.solve(sp, T(seeds), T(gl[:2]), start=T(st[:2]), env=T(env[:2], torch.int32), seed_outputs=True)
             for _ in range(2)]
     for k in runs[0]:
         assert torch.equal(runs[0][k], runs[1][k]), k
     sbc = runs[0]["seed_best_cost"].cpu().numpy().reshape(-1)
     # seeds of problem p were evaluated above with env[p * 5 + s]; re-evaluate with the problem's env
-    ce, _, _ = ctx.evaluate(T(V), T(np.repeat(gl[:2], 5, 0)), start=T(np.repeat(st[:2], 5, 0)),
+    ce, _, _ = ctx.evaluate(T(V[:10]), T(np.repeat(gl[:2], 5, 0)), start=T(np.repeat(st[:2], 5, 0)),
                             env=T(np.repeat(env[:2], 5), torch.int32))
     assert np.all(sbc <= ce.cpu().numpy() * (1 + 1e-6))
     ik = ctx.solve(sp, T(f32(g.uniform(-1.5, 1.5, (2, 33, D)))), T(gl[:2]), env=T(env[:2], torch.int32),
