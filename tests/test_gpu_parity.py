@@ -82,7 +82,7 @@ class Stats:
         self.n += 1
         g_gpu = np.asarray(g_gpu, np.float64)
         g_ref = np.asarray(g_ref, np.float64)
-        if isinstance(margin, tuple) and margin[0] == "ik":
+        if isinstance(margin, tuple) and isinstance(margin[0], str):    # ("ik", m)
             cost_ok, keep = True, margin[1] >= MARGIN
             rows, nrows = (slice(None) if keep else slice(0, 0)), 1
             self.rows += 1
@@ -607,11 +607,13 @@ def test_solve_to_statistical_vs_oracle_franka_cfg2(native, O):
     o_best = o_traj[np.arange(P), o_cost.argmin(1)]
 
     def outcome(p, traj):
-        _, _, t, _, _ = O.eval_traj(R, Ws[p], wl.cost, wl.start[p], wl.goal[p], traj)
+        # the evaluated states (Table 5 map) must all be valid: no self pair and no sphere
+        # penetrating (mask_samples, B12, margin 0); the pose within the B18 thresholds
+        x = O.state_map(wl.start[p], traj)
+        free = all(O.mask_sample(R, Ws[p], x[h + 2])[0] for h in range(1, traj.shape[0] + 1))
         _, _, ee = O.fk(R, traj[-1])
         pe = np.linalg.norm(ee[:3] - wl.goal[p][:3])
         re = 1.0 - abs(float(np.dot(ee[3:], wl.goal[p][3:])))
-        free = t[3] == 0 and t[4] == 0
         return pe, re, free, pe < 0.005 and re < 0.05 and free
     g = [outcome(p, g_traj[p]) for p in range(P)]
     o = [outcome(p, o_best[p]) for p in range(P)]
