@@ -21,10 +21,13 @@
 #define CRB_STATS 0
 #endif
 #if CRB_STATS
-static __device__ unsigned long long g_crb_stats[16];   // one copy per translation unit
+static __device__ unsigned long long g_crb_stats[32];   // one copy per translation unit
 #define CRB_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_crb_stats[i], (unsigned long long)(v)); } while (0)
+// per-phase critical-path clocks of a pass as thread 0 sees them (slots 16..24, passes in 25)
+#define CRB_PHASE(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_crb_stats[16 + (i)], (unsigned long long)(t_ - t_ph)); t_ph = t_; } } while (0)
 #else
 #define CRB_STAT(i, v) do { } while (0)
+#define CRB_PHASE(i) do { } while (0)
 #endif
 
 // Small-world pre-screen in packed fp16 (HFMA2, two cuboids per instruction) ahead of the exact
@@ -740,6 +743,10 @@ template <int MODE, bool WMMA>
 __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
                                           const float *dvec, bool grad = true) {
     Smem s = make_smem(kp, smem);
+#if CRB_STATS
+    long long t_ph = clock64();
+    if (threadIdx.x == 0) atomicAdd(&g_crb_stats[25], 1ull);
+#endif
     // large worlds: the cuboid table stays in global memory (L1 / L2), so the CTA keeps its
     // shared-memory footprint and two CTAs fit per SM (kp.lay.boxes_gmem == WMMA); env from
     // stage_tables
@@ -795,6 +802,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     } else {
         __syncthreads();   // IK: the caller filled q_cfg and its sin / cos (prep_sincos or fused)
     }
+    CRB_PHASE(0);
 
     // ---- a3: forward kinematics: the last three warps walk the chain (after this, lt is dead and holds sg)
 #if CRB_STATS
@@ -847,8 +855,10 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
 #if CRB_STATS
     if (warp == 0) { CRB_STAT(13, clock64() - t_a8); }
 #endif
+    CRB_PHASE(1);
     fk_place(rp, s);
     __syncthreads();
+    CRB_PHASE(2);
 
     // ---- a7: pose cost (Eq. pose_cost_term, A1) at the terminal slot (TO) / every slot (IK); the
     // last warp does it before joining the work queue below
@@ -1272,6 +1282,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     }
 
     __syncthreads();
+    CRB_PHASE(3);
 
     // ---- a10 (per slot): warp 0 merges self-collision and applies its gradient (x, y, z only);
     // warp 1 sums the world groups in index order; then warp 0 forms the slot costs and the total
@@ -1306,6 +1317,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         s.cfg_terms[4 * NC + c] = c < n_act ? cw : 0.f;
     }
     __syncthreads();
+    CRB_PHASE(4);
     if (warp == 0) {
         const int c = lane;
         const float t0 = s.cfg_terms[0 * NC + c], t1 = s.cfg_terms[1 * NC + c], t2 = s.cfg_terms[2 * NC + c],
@@ -1362,6 +1374,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         }
     }
     __syncthreads();
+    CRB_PHASE(5);
     // joint gradient: the subtree sums of the joint's link (independent loads over the host-built
     // descendant mask), then revolute k . (T - o x F), prismatic k . F (Table 7), + bound_pos
     for (int idx = tid; idx < D * NC; idx += NT) {
@@ -1391,6 +1404,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         s.gq[idx] = (c < n_act) ? g + s.gxd[idx] : 0.f;
     }
     __syncthreads();
+    CRB_PHASE(6);
 
     // ---- transposed stencil + transposed state map (O2/O3 gradient routing) -> dC/dV
     if (MODE == MODE_TO) {
@@ -1437,6 +1451,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         for (int idx = tid; idx < D * NC; idx += NT) s.gV[idx] = s.gq[idx];
     }
     __syncthreads();
+    CRB_PHASE(7);
 }
 
 // g . dvec of the last TO pass (fixed warp order).

@@ -1570,9 +1570,9 @@ const void *crb_wmma_kernel(int k);
 #if CRB_STATS
 static int stats_copy(unsigned long long *out, int reset) {   // this translation unit's counters
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-    if (cudaMemcpyFromSymbol(out, ::g_crb_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out, ::g_crb_stats, sizeof(unsigned long long) * 32) != cudaSuccess) return -1;
     if (reset) {
-        unsigned long long z[16] = {};
+        unsigned long long z[32] = {};
         cudaMemcpyToSymbol(::g_crb_stats, z, sizeof(z));
     }
     return 0;
@@ -2544,9 +2544,9 @@ crb_status crb_particle_normals(uint32_t key0, uint32_t key1, int n_var, int n_p
 #if CRB_STATS
 // world-screen work counters (tools/world_stats.py only; not part of the product ABI)
 extern "C" int crb_debug_stats(unsigned long long *out, int reset) {
-    unsigned long long w[16];
+    unsigned long long w[32];
     if (stats_copy(out, reset) != 0 || crb_wmma_stats(w, reset) != 0) return -1;
-    for (int i = 0; i < 16; ++i) out[i] += w[i];   // the counters of both translation units
+    for (int i = 0; i < 32; ++i) out[i] += w[i];   // the counters of both translation units
     return 0;
 }
 #endif

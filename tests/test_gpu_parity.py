@@ -589,11 +589,13 @@ def test_solve_to_statistical_vs_oracle_franka_cfg2(native, O):
     the same seeds.  Full solves are chaotic (A37), so the comparison is statistical: success (B18
     pose thresholds 5 mm / 0.05, plus self- and world-collision-free at the evaluated states), the
     collision-free rate and the pose-error quantiles; the GPU must not be worse than the oracle by a
-    one-sided two-proportion test at p = 0.01 (z < 2.326), and its median best cost must not exceed
-    the oracle's by more than 25 %."""
+    one-sided two-proportion test at p = 0.01 (z < 2.326), its best costs must not be
+    stochastically larger than the oracle's (one-sided Mann-Whitney U, p = 0.01) and its median
+    best cost must not exceed the oracle's by more than 25 %."""
     import os
+    from scipy.stats import mannwhitneyu
     from paper_2310_17274_b200 import workload
-    P, S = 32, 8
+    P, S = 64, 8
     wl = workload.franka_to(0, list(range(P)), S=S, H=32, iters=100, run_seed=4)
     R = O.Robot(wl.robot)
     Ws = [O.World(w) for w in wl.worlds]
@@ -625,10 +627,13 @@ def test_solve_to_statistical_vs_oracle_franka_cfg2(native, O):
     print(f"[cfg2 full solve] success GPU {g_ok}/{P} oracle {o_ok}/{P}; collision-free GPU {g_free} oracle {o_free}; "
           f"pose err q25/50/90 GPU {np.round(g_pe * 1e3, 2)} mm oracle {np.round(o_pe * 1e3, 2)} mm; "
           f"median best-cost ratio GPU/oracle {ratio:.3f}")
+    mw = mannwhitneyu(g_cost, o_cost.min(1), alternative="greater").pvalue
+    print(f"[cfg2 full solve] Mann-Whitney p(GPU costs stochastically larger) = {mw:.3f}")
     assert _two_proportion_z(o_ok, g_ok, P) < 2.326, (g_ok, o_ok)
     assert _two_proportion_z(o_free, g_free, P) < 2.326, (g_free, o_free)
+    assert mw > 0.01, mw
     assert ratio < 1.25, ratio
-    assert o_ok >= P // 4, "too few successes to compare: adjust the generator"
+    assert max(g_free, o_free) >= 4, "collision-free rates too low to compare: adjust the generator"
     ctx.close()
 
 

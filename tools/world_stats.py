@@ -37,7 +37,7 @@ so.crb_debug_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 
 
 def stats(reset=True):
-    a = (C.c_ulonglong * 16)()
+    a = (C.c_ulonglong * 32)()
     so.crb_debug_stats(a, int(reset))
     return list(a)
 
@@ -61,6 +61,14 @@ def run(name, wl):
           f"barrier wait {s[6] / wp:.0f} cyc", flush=True)
     fp = max(s[12], 1)
     print(f"   FK chain {s[11] / fp:.0f} cyc per pass, warp 0 waits {s[13] / fp:.0f} cyc at the placement barrier",
+          flush=True)
+    npass = max(s[25], 1)
+    names = ["a2 state map", "FK chain + a8", "placement", "queue (pose, self, world)", "merge", "link sums",
+             "joint grads", "transposed + gV"]
+    ph = [s[16 + i] / npass for i in range(8)]
+    tot = sum(ph)
+    print("   phases (thread 0, cycles per pass): " + ", ".join(f"{n} {v:.0f} ({100 * v / tot:.1f}%)"
+                                                              for n, v in zip(names, ph)) + f"; total {tot:.0f}",
           flush=True)
 
 
