@@ -59,6 +59,16 @@ def dist_env():
     return rank, world, local
 
 
+def pipes_summary():
+    """Issued-instruction roofline per pipe of the dominant kernel from the committed ncu capture
+    (profiles/r02_pipes.json, tools/pipes_from_ncu.py; an ncu number, never re-measured here)."""
+    path = os.path.join(ROOT, "profiles", "r02_pipes.json")
+    try:
+        return json.load(open(path))
+    except Exception:
+        return None
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -168,16 +178,33 @@ def oracle_sample_rate(wl, problem: int, iters: int, nthreads: int):
     return evals / dt, dt, evals
 
 
-def cpu_baseline(wl, target_s: float = 12.0):
-    """Oracle on the host cores, bounded sample of problem 0 (about target_s seconds)."""
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(wl, target_s: float = 12.0, target_1t_s: float = 4.0):
+    """Oracle on the host cores, bounded sample of problem 0 (about target_s seconds on all host
+    threads, and about target_1t_s on one thread)."""
     nthreads = os.cpu_count() or 1
     rate1, dt1, _ = oracle_sample_rate(wl, 0, 1, nthreads)
     per_iter = dt1 / 1.0
     iters = int(max(1, min(wl.solver.iters, target_s / max(per_iter, 1e-3))))
     rate, dt, evals = oracle_sample_rate(wl, 0, iters, nthreads)
+    _, d1, _ = oracle_sample_rate(wl, 0, 1, 1)
+    it1 = int(max(1, min(wl.solver.iters, target_1t_s / max(d1, 1e-3))))
+    r1, t1, e1 = oracle_sample_rate(wl, 0, it1, 1)
     return {"value": rate, "unit": UNIT, "cores": nthreads, "kind": "oracle",
             "sample": f"problem 0 of {wl.name}: {wl.S} seeds x {iters} L-BFGS iterations ({evals} evals, {dt:.1f} s, "
-                      f"fp64 C oracle, {nthreads} threads)"}
+                      f"fp64 C oracle, {nthreads} threads)",
+            "cpu_model": cpu_model(), "host_threads": nthreads,
+            "single_thread": {"value": r1, "unit": UNIT, "cores": 1,
+                              "sample": f"problem 0: {wl.S} seeds x {it1} iterations ({e1} evals, {t1:.1f} s, 1 thread)"}}
 
 
 def run_reference(args):
@@ -252,7 +279,7 @@ def motion_gen_metrics(local, rank, world, dev, steps):
     import torch.distributed as dist
     from paper_2310_17274_b200 import motion_gen, native, parallel, workload
     res = {}
-    for P in (64, 1):
+    for P in (64,):
         lo = rank * P
         wl = workload.franka_to(local, list(range(lo, lo + P)), S=12, H=32, iters=100)
         ctx = native.Context(local)
@@ -298,6 +325,42 @@ def motion_gen_metrics(local, rank, world, dev, steps):
                         "up_to_3_attempts": {"ms_per_batch": ms3, "problems_per_s": P * world / (ms3 * 1e-3),
                                              "success": succ3}}
         ctx.close()
+    # single-problem latency (the paper's ~50 ms mean) over 16 different problems, each
+    # planned alone (batch 1, the cluster latency mode), with its success
+    n1 = 16
+    lo = rank * n1
+    wl = workload.franka_to(local, list(range(lo, lo + n1)), S=12, H=32, iters=100)
+    ctx = native.Context(local)
+    ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
+    mg = motion_gen.MotionGen(ctx, wl.robot, wl.cost)
+    st_all, gl_all = torch.tensor(wl.start, device=dev), torch.tensor(wl.goal, device=dev)
+    env_all = torch.tensor(wl.env, device=dev)
+    iks = torch.tensor(mg.ik_seed_batch(wl.robot, range(lo, lo + n1), 32), device=dev)
+    one = lambda k: (st_all[k:k + 1], gl_all[k:k + 1], env_all[k:k + 1], iks[k:k + 1])
+    mg.plan(*one(0))
+    torch.cuda.synchronize()
+    lat, oks, lat3, ok3 = [], [], [], 0
+    for k in range(n1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        o = mg.plan(*one(k))
+        b.record()
+        torch.cuda.synchronize()
+        lat.append(a.elapsed_time(b))
+        oks.append(bool(o["success"].item()))
+        a.record()
+        o3 = mg.plan_retry(*one(k)[:3], [lo + k], attempts=3)
+        b.record()
+        torch.cuda.synchronize()
+        lat3.append(a.elapsed_time(b))
+        ok3 += int(o3["success"].item())
+    ctx.close()
+    ok = sum(oks)
+    res["P1"] = {"problems": n1, "each_planned_alone": True, "median_ms": statistics.median(lat),
+                 "p90_ms": float(np.quantile(lat, 0.9)), "success": ok,
+                 "median_ms_successful": statistics.median([t for t, s in zip(lat, oks) if s]) if ok else None,
+                 "up_to_3_attempts": {"median_ms": statistics.median(lat3), "p90_ms": float(np.quantile(lat3, 0.9)),
+                                      "success": ok3}}
     return res
 
 
@@ -370,20 +433,53 @@ def side_metrics(local, rank, world, dev, flush, steps=2):
     # f2: the whole motion-generation pipeline (IK -> seeds -> TO -> retime -> TO at dt_opt ->
     # retime -> success), batched and for one problem (the paper's ~50 ms figure)
     out["f2_motion_gen"] = motion_gen_metrics(local, rank, world, dev, steps)
-    n_dense = 16
-    lo = rank * n_dense
-    wl = workload.franka_to(local, list(range(lo, lo + n_dense)), S=32, H=32, n_boxes=1000, iters=100, dense=True)
+    # config 5 at its stated size: 256 problems x 32 seeds x 32 timesteps x 100 iterations against
+    # K = 1000 dense cuboids each, swept + speed, seed-sharded over the GPUs: each
+    # rank solves its 32 / N seeds of all 256 problems, then C1 + C2 pick the winners
+    from paper_2310_17274_b200 import parallel
+    n_dense, S5 = 256, 32
+    s_lo, s_hi = parallel.seed_block(S5, world, rank)
+    wl = workload.franka_to(local, list(range(n_dense)), S=S5, H=32, n_boxes=1000, iters=100, dense=True)
     ctx = native.Context(local)
     ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
-    ms = _timed_solves(ctx, wl.solver, torch.tensor(wl.seeds, device=dev), torch.tensor(wl.goal, device=dev),
-                       torch.tensor(wl.start, device=dev), torch.tensor(wl.env, device=dev), steps, flush, world, dev)
     fl = workload.nominal_flops_per_eval(wl)
-    ev = wl.evals_per_solve() * world / (ms * 1e-3)
-    out["cfg5_dense_sample"] = {"problems_per_gpu": n_dense, "seeds": 32, "timesteps": 32, "boxes": 1000,
-                                "iters": 100, "ms_per_solve": ms, "evals_per_s": ev,
-                                "problems_per_s": n_dense * world / (ms * 1e-3), "flops_per_eval": fl,
-                                "achieved_tflops": ev / world * fl / 1e12,
-                                "ctas_per_sm": ctx.solver_occupancy(32)[0]}
+    seeds5 = torch.tensor(np.ascontiguousarray(wl.seeds[:, s_lo:s_hi]), device=dev)
+    g5, st5, e5 = (torch.tensor(wl.goal, device=dev), torch.tensor(wl.start, device=dev),
+                   torch.tensor(wl.env, device=dev))
+
+    def solve5(sd, base):
+        o = ctx.solve(wl.solver, sd, g5, start=st5, env=e5, seed_base=base)
+        if world > 1:
+            parallel.merge_seed_sharded(o["best_key"], o["best_traj"], S5)
+    solve5(seeds5, s_lo)
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        if world > 1:
+            torch.distributed.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        solve5(seeds5, s_lo)
+        b.record()
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    ms = tot / steps
+    if world > 1:
+        ms = parallel.max_over_ranks(ms, dev)
+    evals5 = n_dense * S5 * (len(wl.solver.alpha) * 32 * 100 + 32)
+    out["cfg5_dense"] = {"problems": n_dense, "seeds": S5, "seeds_per_gpu": s_hi - s_lo, "timesteps": 32,
+                         "boxes": 1000, "iters": 100, "sharding": f"seed-sharded x{world} (C1 + C2 inside the timing)",
+                         "ms_per_solve": ms, "evals_per_s": evals5 / (ms * 1e-3),
+                         "problems_per_s": n_dense / (ms * 1e-3), "flops_per_eval": fl,
+                         "nominal_tflops_per_gpu": evals5 / world / (ms * 1e-3) * fl / 1e12,
+                         "ctas_per_sm": ctx.solver_occupancy(32)[0]}
+    # the per-GPU share of the 8-GPU run (256 problems x 4 seeds), timed alone on this GPU
+    if world == 1:
+        sd8 = torch.tensor(np.ascontiguousarray(wl.seeds[:, :S5 // 8]), device=dev)
+        ms8 = _timed_solves(ctx, wl.solver, sd8, g5, st5, e5, steps, flush, 1, dev)
+        out["cfg5_dense"]["share_of_8_gpus"] = {"seeds_per_gpu": S5 // 8, "ms_per_solve": ms8,
+                                                "evals_per_s": evals5 / 8 / (ms8 * 1e-3)}
     ctx.close()
     return out
 
@@ -423,8 +519,10 @@ def run_native(args):
     evals_per_step = wl.evals_per_solve()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
 
+    p_base = 0 if seed_mode else rank * P      # global index of this rank's first problem (RNG key)
+
     def step():
-        out = ctx.solve(sp, seeds, goal, start=start, env=env, seed_base=s_lo)
+        out = ctx.solve(sp, seeds, goal, start=start, env=env, seed_base=s_lo, problem_base=p_base)
         if seed_mode and dist.is_initialized():   # the real exchange step of seed sharding: C1 + C2
             out["best_key"], out["best_traj"], out["best_cost"] = parallel.merge_seed_sharded(
                 out["best_key"], out["best_traj"], S_total)
@@ -535,6 +633,8 @@ def run_native(args):
                                           f"problem-sharded x{world}, no data-path collective"},
                 "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                              "frac": achieved_tf / peak_tf, "traffic": traffic,
+                             "frac_of_unit_count_peak": achieved_tf / (2 * peak_tf),
+                             "pipes": pipes_summary(),
                              "kernel": "solve_to_kernel", "flops_per_eval": flops_eval,
                              "peak_basis": f"register-operand FFMA: 148 SMs x 64 FFMA/clk x 2 flops x {sm_max:.0f} MHz "
                                            "(sm_max_mhz of MEASURED_PEAKS.json); measured 37.3 TF by tools/ffma_peak.cu; "

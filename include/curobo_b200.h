@@ -216,9 +216,10 @@ crb_status crb_evaluate_cost_grad(crb_ctx *ctx, const float *q, int B, int H, co
 
 /* Same with a per-row timestep (Alg. 4 "run trajectory optimization with new dt", reading B15):
  * dt[B] (device, > 0; NULL = the cost params' dt).  The five-point stencil and the speed metric
- * use dt[b]; the smoothness weights are rescaled relative to dt_ref = the cost params' dt:
- * alpha_8 (dt/dt_ref)^4, alpha_9 (dt/dt_ref)^6 (the terms keep their magnitude when the same
- * path is re-timed); the bound weights are physical limits and stay.  IK rows ignore dt. */
+ * use dt[b]; every term that relates to velocity, acceleration or jerk is rescaled relative to
+ * dt_ref = the cost params' dt: alpha_8 (dt/dt_ref)^4, alpha_9 (dt/dt_ref)^6 and the
+ * velocity / acceleration / jerk limit weights (dt/dt_ref)^1, ^2, ^3 (each term keeps its
+ * magnitude when the same path is re-timed); the position limit weight stays.  IK rows ignore dt. */
 crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H, const int *env,
                                      const float *start, const float *goal, const float *dt,
                                      float *cost, float *grad, float *term_costs, void *stream);
@@ -329,6 +330,17 @@ crb_status crb_linear_seeds(int P, int S, int H, int D, const float *q0, const f
  * pinned V_0..V_2 and aliased V_{H-4..H-2} are not states).  V[B][H][D] -> x[B][H][D]. */
 crb_status crb_trajectory_states(int B, int H, int D, const float *V, const float *start, int start_div,
                                  float *x, void *stream);
+
+/* Interpolation to a fine time grid ("interpolate the trajectory to a fixed dt of 0.025 to
+ * validate success"; reading B21): B trajectories of states x[B][H][D] (device,
+ * e.g. crb_trajectory_states) sampled at spacing dt[B] (device) -> out[B][n_max][D] (device):
+ * point k is the joint-space linear interpolation at t_k = min(k dt_fine, (H-1) dt[b]) between the
+ * bracketing states, for k < n_b = ceil((H-1) dt[b] / dt_fine) + 1 (the last point is x_H); rows
+ * from min(n_b, n_max) on repeat x_H.  n_out[B] (device int32, may be NULL) receives n_b before
+ * clamping, so a caller can detect truncation.  Errors: CRB_E_ARG (H < 2, dt_fine <= 0, n_max < 1,
+ * NULL pointers), CRB_E_LIMIT (B > 65535). */
+crb_status crb_interpolate(int B, int H, int D, const float *x, const float *dt, float dt_fine, int n_max,
+                           float *out, int *n_out, void *stream);
 
 /* dst[p][:] = src[p][idx[p * idx_stride]][:] for rows of n floats, src[P][S][n] (idx < 0: zeros). */
 crb_status crb_gather_rows(int P, int S, int n, const float *src, const int *idx, int idx_stride,

@@ -826,8 +826,15 @@ void orc_scale_params(const orc_params *in, double dt, double dt_ref, int jerk_o
     *out = *in;
     double r = dt / dt_ref;
     out->dt = dt;
+    /* P:2053 "scale all our cost terms that relate to velocity, acceleration, and jerk": each term
+     * keeps its magnitude when the same path is re-timed from dt_ref to dt (reading B15): the
+     * squared acceleration / jerk by r^4 / r^6, the velocity / acceleration / jerk limit terms
+     * (slope 1 in the derivative beyond the band) by r, r^2, r^3; the position limit term stays. */
     out->a8 = in->a8 * r * r * r * r;
     out->a9 = in->a9 * r * r * r * r * r * r;
+    out->w_bound[1] = in->w_bound[1] * r;
+    out->w_bound[2] = in->w_bound[2] * r * r;
+    out->w_bound[3] = in->w_bound[3] * r * r * r;
     if (jerk_on) out->flags |= ORC_JERK;
 }
 
@@ -849,6 +856,26 @@ void orc_goal_error(const orc_robot *rb, const double *q, const double *goal, do
 void orc_linear_seed(const double *start, const double *qT, int H, int D, double *V) {
     for (int h = 0; h < H; ++h)
         for (int d = 0; d < D; ++d) V[h * D + d] = start[d] + ((double)h / (H - 1)) * (qT[d] - start[d]);
+}
+
+/* Interpolation of a solved trajectory to a fine time grid ("interpolate the trajectory
+ * to a fixed dt of 0.025 to validate success"; reading B21): the states x_1..x_H sit at
+ * t = 0, dt, .., (H-1) dt; the fine grid t_k = min(k dt_fine, T), k = 0..n-1 with T = (H-1) dt and
+ * n = ceil(T / dt_fine) + 1 (so the last point is x_H), decided in fp64; linear in joint space
+ * between the bracketing states: i = min(floor(t_k / dt), H - 2), f = t_k / dt - i,
+ * x(t_k) = (1 - f) x_i + f x_{i+1}.  Writes min(n, n_max) points of out [n_max][D]; returns n. */
+int orc_interpolate(const double *x, int H, int D, double dt, double dt_fine, int n_max, double *out) {
+    const double T = (H - 1) * dt;
+    const int n = (int)ceil(T / dt_fine) + 1;
+    for (int k = 0; k < n && k < n_max; ++k) {
+        double t = k * dt_fine;
+        double u = (t >= T) ? (double)(H - 1) : t / dt;        /* the last point is x_H exactly */
+        int i = (int)floor(u);
+        if (i > H - 2) i = H - 2;
+        double f = u - i;
+        for (int d = 0; d < D; ++d) out[k * D + d] = (1.0 - f) * x[i * D + d] + f * x[(i + 1) * D + d];
+    }
+    return n;
 }
 
 /* Scores (App. B, reading B18).  IK: "a lowest weighted sum of pose error and the

@@ -140,6 +140,8 @@ void   orc_scale_params(const orc_params *in, double dt, double dt_ref, int jerk
 void   orc_goal_error(const orc_robot *rb, const double *q, const double *goal, double *pos_err,
                       double *rot_err);
 void   orc_linear_seed(const double *start, const double *qT, int H, int D, double *V);
+/* B21: linear interpolation of states x[H][D] at spacing dt to the grid k dt_fine. */
+int    orc_interpolate(const double *x, int H, int D, double dt, double dt_fine, int n_max, double *out);
 double orc_ik_score(int D, const double *q, const double *q0, double pos_err, double rot_err,
                     double w_pose, double w_dist);
 double orc_blended_score(double pos_err, double rot_err, double max_jerk, double motion_time,

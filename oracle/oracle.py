@@ -429,17 +429,20 @@ def scale_params(cp, dt, dt_ref=0.25, jerk_on=True):
     """O13 Alg. 4 weight scaling (reading B15) on an inputs.CostParams; returns a new CostParams."""
     import dataclasses
     r = dt / dt_ref
+    wb = tuple(cp.w_bound)
     return dataclasses.replace(cp, dt=dt, a8=cp.a8 * r ** 4, a9=cp.a9 * r ** 6,
+                               w_bound=(wb[0], wb[1] * r, wb[2] * r * r, wb[3] * r * r * r),
                                flags=cp.flags | (4 if jerk_on else 0))
 
 
 def scale_params_c(cp, dt, dt_ref=0.25, jerk_on=True):
-    """The same scaling done by the C oracle (orc_scale_params), returned as (dt, a8, a9, flags)."""
+    """The same scaling done by the C oracle (orc_scale_params), returned as
+    (dt, a8, a9, flags, w_bound[0..3])."""
     L = lib()
     L.orc_scale_params.argtypes = [C.POINTER(_Params), C.c_double, C.c_double, C.c_int, C.POINTER(_Params)]
     pin = params(cp); pout = _Params()
     L.orc_scale_params(C.byref(pin), float(dt), float(dt_ref), int(jerk_on), C.byref(pout))
-    return pout.dt, pout.a8, pout.a9, pout.flags
+    return (pout.dt, pout.a8, pout.a9, pout.flags) + tuple(pout.w_bound)
 
 
 def goal_error(robot: Robot, q, goal):
@@ -458,6 +461,19 @@ def linear_seed(start, qT, H):
     L.orc_linear_seed.argtypes = [D_P, D_P, C.c_int, C.c_int, D_P]
     L.orc_linear_seed(_dp(start), _dp(qT), H, D, _dp(V))
     return V
+
+
+def interpolate(x, dt, dt_fine=0.025, n_max=4096):
+    """B21: states x [H][D] at spacing dt -> (n, points [min(n, n_max)][D]) on the grid
+    k dt_fine, linear in joint space, the last point x_H."""
+    x = _d(x)
+    H, D = x.shape
+    out = np.zeros((n_max, D))
+    L = lib()
+    L.orc_interpolate.restype = C.c_int
+    L.orc_interpolate.argtypes = [D_P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, D_P]
+    n = L.orc_interpolate(_dp(x), H, D, float(dt), float(dt_fine), int(n_max), _dp(out))
+    return n, out[:min(n, n_max)]
 
 
 def ik_score(q, q0, pos_err, rot_err, w_pose, w_dist):

@@ -720,14 +720,16 @@ static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const
 // the kernel parameters left in the constant bank.
 // The dt-dependent scalars of one problem into s.tdp (thread 0; the caller synchronises):
 // [0] 1/(2 dt) (speed metric), [1..3] 1/(12 dt), 1/(12 dt^2), 1/(2 dt^3) (five-point stencil),
-// [4] a8, [5] a9.  With a per-problem dt the smoothness weights follow reading B15 relative to the
-// context's dt_ref = cp.dt: a8 (dt/dt_ref)^4, a9 (dt/dt_ref)^6 (Alg. 4 "scale weights by new dt").
+// [4] a8, [5] a9, [6..8] the velocity / acceleration / jerk limit weights.  With a per-problem dt
+// the weights follow reading B15 relative to the context's dt_ref = cp.dt: a8 (dt/dt_ref)^4, a9
+// (dt/dt_ref)^6, the limit weights (dt/dt_ref)^1,2,3 (Alg. 4 "scale weights by new dt").
 __device__ __forceinline__ void stage_dt(const KParams &kp, const Smem &s, int row) {
     if (threadIdx.x != 0) return;
     const CostP &cf = kp.cp;
     if (!kp.dt_arr) {
         s.tdp[0] = cf.inv_2dt; s.tdp[1] = cf.inv_12dt; s.tdp[2] = cf.inv_12dt2; s.tdp[3] = cf.inv_2dt3;
         s.tdp[4] = cf.a8; s.tdp[5] = cf.a9;
+        s.tdp[6] = cf.wb[1]; s.tdp[7] = cf.wb[2]; s.tdp[8] = cf.wb[3];
         return;
     }
     const double dt = kp.dt_arr[row], r = dt / (double)cf.dt, r2 = r * r;
@@ -737,6 +739,11 @@ __device__ __forceinline__ void stage_dt(const KParams &kp, const Smem &s, int r
     s.tdp[3] = (float)(1.0 / (2.0 * dt * dt * dt));
     s.tdp[4] = (float)(cf.a8 * (r2 * r2));
     s.tdp[5] = (float)(cf.a9 * (r2 * r2 * r2));
+    // P:2053 "scale all our cost terms that relate to velocity, acceleration, and jerk": the limit
+    // terms too, by r, r^2, r^3 (slope 1 in a derivative that scales like dt^-1, -2, -3; B15)
+    s.tdp[6] = (float)(cf.wb[1] * r);
+    s.tdp[7] = (float)(cf.wb[2] * r2);
+    s.tdp[8] = (float)(cf.wb[3] * (r2 * r));
 }
 
 template <int MODE, bool WMMA>
@@ -831,9 +838,10 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     const float j = (xp2 - 2.f * xp1 + 2.f * xm1 - xm2) * s.tdp[3];
                     const float vm = lim[2 * D + d], am = lim[3 * D + d], jm = lim[4 * D + d];
                     cb += cf.wb[0] * bound_cost(x0, lo, hi, cf.eta_bound, cf.inv_eta_bound, dd); gx = cf.wb[0] * dd;
-                    cb += cf.wb[1] * bound_cost(v, -vm, vm, cf.eta_bound, cf.inv_eta_bound, dd); gv = cf.wb[1] * dd;
-                    cb += cf.wb[2] * bound_cost(a, -am, am, cf.eta_bound, cf.inv_eta_bound, dd); ga = cf.wb[2] * dd;
-                    cb += cf.wb[3] * bound_cost(j, -jm, jm, cf.eta_bound, cf.inv_eta_bound, dd); gj = cf.wb[3] * dd;
+                    const float w1 = s.tdp[6], w2 = s.tdp[7], w3 = s.tdp[8];   // per-problem dt (B15)
+                    cb += w1 * bound_cost(v, -vm, vm, cf.eta_bound, cf.inv_eta_bound, dd); gv = w1 * dd;
+                    cb += w2 * bound_cost(a, -am, am, cf.eta_bound, cf.inv_eta_bound, dd); ga = w2 * dd;
+                    cb += w3 * bound_cost(j, -jm, jm, cf.eta_bound, cf.inv_eta_bound, dd); gj = w3 * dd;
                     const float a8 = s.tdp[4], a9 = s.tdp[5];
                     cs = a8 * a * a;
                     ga += 2.f * a8 * a;

@@ -1468,6 +1468,34 @@ __global__ void states_kernel(int B, int H, int D, const float *V, const float *
     }
 }
 
+// Interpolation to a fine time grid (reading B21): trajectory b's states x[b][H][D] at
+// spacing dt[b] -> out[b][k][D] at t_k = min(k dt_fine, T), T = (H-1) dt[b], k < n_b = ceil(T /
+// dt_fine) + 1 (the count and the bracketing index decided in fp64 from the fp32 inputs, as the
+// oracle decides them); rows k >= min(n_b, n_max) repeat x_H (neutral for a validity mask).
+__global__ void interp_kernel(int B, int H, int D, const float *x, const float *dt, float dt_fine, int n_max,
+                              float *out, int *n_out) {
+    const int b = blockIdx.y;
+    if (b >= B) return;
+    const double dtb = (double)dt[b], T = (H - 1) * dtb;
+    const int n = (int)ceil(T / (double)dt_fine) + 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && n_out) n_out[b] = n;
+    const float *xb = x + (size_t)b * H * D;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_max * D; e += gridDim.x * blockDim.x) {
+        const int k = e / D, d = e - k * D;
+        float v;
+        if (k >= n - 1) {
+            v = xb[(H - 1) * D + d];
+        } else {
+            const double u = (k * (double)dt_fine) / dtb;
+            int i = (int)floor(u);
+            if (i > H - 2) i = H - 2;
+            const float f = (float)(u - i);
+            v = fmaf(f, xb[(i + 1) * D + d] - xb[i * D + d], xb[i * D + d]);
+        }
+        out[((size_t)b * n_max + k) * D + d] = v;
+    }
+}
+
 // dst[p][:] = src[p][idx[p]][:] (rows of n floats; idx < 0 -> zeros)
 __global__ void gather_kernel(int P, int S, int n, const float *src, const int *idx, int idx_stride, float *dst) {
     const size_t tot = (size_t)P * n;
@@ -1694,7 +1722,7 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.gq = take(D * NC);
     L.gva = take(mode == MODE_TO ? 3 * D * NC : 4);
     L.pose_ft = take(6 * NC);
-    L.tdp = take(8);
+    L.tdp = take(12);
     L.goal = take(std::max(7, D) * NC);   // pose [7][32] or joint-space goal [D][32] (CRB_CSPACE)
     L.cfg_cost = take(NC);
     L.cfg_terms = take(5 * NC);
@@ -2516,6 +2544,16 @@ crb_status crb_trajectory_states(int B, int H, int D, const float *V, const floa
     const size_t n = (size_t)B * H * D;
     const int grid = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
     states_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(B, H, D, V, start, start_div, x);
+    return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
+}
+
+crb_status crb_interpolate(int B, int H, int D, const float *x, const float *dt, float dt_fine, int n_max, float *out,
+                           int *n_out, void *stream) {
+    if (B < 0 || H < 2 || D < 1 || !(dt_fine > 0.f) || n_max < 1 || (B > 0 && (!x || !dt || !out))) return CRB_E_ARG;
+    if (B == 0) return CRB_OK;
+    if (B > 65535) return CRB_E_LIMIT;
+    const int gx = std::min((n_max * D + 255) / 256, 64);
+    interp_kernel<<<dim3(gx, B), 256, 0, (cudaStream_t)stream>>>(B, H, D, x, dt, dt_fine, n_max, out, n_out);
     return cudaGetLastError() == cudaSuccess ? CRB_OK : CRB_E_CUDA;
 }
 

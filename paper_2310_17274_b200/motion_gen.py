@@ -13,7 +13,10 @@ Every step of the computation runs in the library's kernels (libcurobo_b200.so, 
   5. retime every seed (Alg. 4 line 2), goal errors + state validity -> blended score -> best seed;
   6. trajectory optimisation #2 of that seed at its dt_opt with the weights re-scaled (B15) and the
      jerk term on (Alg. 4 lines 3-5);
-  7. final retime (Alg. 4 line 6) and the success test: pose thresholds and every state valid.
+  7. final retime (Alg. 4 line 6) and the success test: pose thresholds and every state valid;
+  8. interpolation of the final trajectory to a fixed dt of 0.025 s and the validity of every
+     interpolated state ("interpolate the trajectory to a fixed dt of 0.025 to validate
+     success"; reading B21) -- part of the success test.
 
 One context holds the robot, the worlds (env per problem) and the cost parameters; the jerk flag
 is switched between the two optimisations by re-setting the parameters (dt stays the reference
@@ -54,6 +57,9 @@ class MotionGenConfig:
     invalid_penalty: float = 1e6    # TO selection: an invalid seed still ranks after every valid one
     attempts: int = 1               # plan_retry: the paper re-attempts with new linear seeds up to 3x
                                     # before its graph planner (the planner is not built)
+    dt_fine: float = 0.025          # validation grid (B21)
+    interp_max: int = 1024          # fine points per trajectory (a multiple of 32: mask groups); a
+                                    # longer trajectory ((H-1) dt_f > 25.6 s) counts as a failure
 
 
 class MotionGen:
@@ -79,7 +85,8 @@ class MotionGen:
         seeds = torch.tensor(self.ik_seed_batch(self.robot, problems, S), device=start.device)
         out = self.plan(start, goal, env, seeds)
         out["attempt"] = torch.ones(start.shape[0], dtype=torch.int32, device=start.device)
-        keys = ("traj", "variables", "dt", "final_score", "success", "pos_err", "rot_err", "max_jerk")
+        keys = ("traj", "variables", "dt", "final_score", "success", "pos_err", "rot_err", "max_jerk", "fine_valid",
+                "fine_points")
         for a in range(1, n):
             fail = torch.nonzero(~out["success"]).flatten()
             if fail.numel() == 0:
@@ -141,8 +148,14 @@ class MotionGen:
         final = N.to_scores(pe2.view(P, 1), re2.view(P, 1), jerk2.view(P, 1), dt_f.view(P, 1), v2.view(P, 1, H), H,
                             c.pos_thr, c.rot_thr, c.w_pose, c.w_jerk, c.w_time)
         ctx.set_cost_params(self.cost_to1)
-        # success: the final blended score is finite (pose thresholds met, every state valid)
-        return dict(traj=x2, variables=tr2, dt=dt_f, final_score=final.view(P), success=final.view(P) < float("inf"),
+        # 8: the final trajectory on the fixed fine grid (B21), every interpolated state valid
+        xi, ni = N.interpolate(x2, dt_f, c.dt_fine, c.interp_max)
+        vi = ctx.mask_samples(xi.view(P * c.interp_max, D), env=env, env_div=c.interp_max)
+        fine_ok = (vi.view(P, c.interp_max) != 0).all(1) & (ni <= c.interp_max)
+        # success: the final blended score is finite (pose thresholds met, every state valid) and
+        # every interpolated state is valid
+        return dict(traj=x2, variables=tr2, dt=dt_f, final_score=final.view(P),
+                    success=(final.view(P) < float("inf")) & fine_ok, fine_valid=fine_ok, fine_points=ni,
                     pos_err=pe2, rot_err=re2, max_jerk=jerk2, ik_count=ik_count, ik_q=q_ik, ik_idx=ik_idx,
                     to1_traj=tr1, to1_dt=dt1, to1_score=s1, best1=best1, dt_opt=dt_opt)
 

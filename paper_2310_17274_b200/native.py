@@ -105,6 +105,7 @@ _lib.crb_rank_seeds.argtypes = [C.c_int, C.c_int, _V, C.c_int, _V, _V, _V]
 _lib.crb_linear_seeds.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _V, _V, C.c_int, _V, _V, _V]
 _lib.crb_trajectory_states.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, C.c_int, _V, _V]
 _lib.crb_gather_rows.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, C.c_int, _V, _V]
+_lib.crb_interpolate.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, C.c_float, C.c_int, _V, _V, _V]
 _lib.crb_particle_normals.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_uint32, _V, _V]
 _lib.crb_launch_count.argtypes = [_V]
 _lib.crb_launch_count.restype = C.c_int64
@@ -114,7 +115,7 @@ SYMBOLS = ["crb_create", "crb_destroy", "crb_last_error", "crb_version", "crb_se
            "crb_ls_select", "crb_argmin_keys", "crb_lbfgs_direction", "crb_launch_count", "crb_solver_occupancy",
            "crb_particle_normals", "crb_mask_samples", "crb_steer", "crb_evaluate_cost_grad_dt",
            "crb_lbfgs_solve_dt", "crb_retime", "crb_goal_error", "crb_ik_scores", "crb_to_scores",
-           "crb_rank_seeds", "crb_linear_seeds", "crb_gather_rows", "crb_trajectory_states"]
+           "crb_rank_seeds", "crb_linear_seeds", "crb_gather_rows", "crb_trajectory_states", "crb_interpolate"]
 
 
 def _ptr(t):
@@ -448,6 +449,17 @@ def gather_rows(src, idx, idx_stride=1):
     dst = torch.empty((P,) + tuple(src.shape[2:]), device=src.device, dtype=torch.float32)
     _check_free(_lib.crb_gather_rows(P, S, n, _ptr(src), _ptr(idx), int(idx_stride), _ptr(dst), _stream()))
     return dst
+
+
+def interpolate(x, dt, dt_fine=0.025, n_max=1024):
+    """B21: states x [B,H,D] at spacing dt [B] -> (points [B,n_max,D], n [B] int32 before clamping)."""
+    import torch
+    B, H, D = x.shape
+    out = torch.empty(B, n_max, D, device=x.device, dtype=torch.float32)
+    n = torch.empty(B, device=x.device, dtype=torch.int32)
+    _check_free(_lib.crb_interpolate(B, H, D, _ptr(x), _ptr(dt), float(dt_fine), int(n_max), _ptr(out), _ptr(n),
+                                     _stream()))
+    return out, n
 
 
 def particle_normals(key0, key1, n_var, n_particles, it, seed):

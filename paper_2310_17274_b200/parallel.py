@@ -56,7 +56,9 @@ def merge_seed_sharded(best_key: torch.Tensor, best_traj: torch.Tensor, S_total:
     owner = (seed // (S_total // world)).long()
     P = best_key.shape[0]
     out = trajs[owner, torch.arange(P, device=best_traj.device)]
-    cost = torch.from_numpy(((key.cpu().numpy() >> 32).astype("uint32")).view("float32").copy()).to(best_traj.device)
+    # the winner's cost straight from the key's high word (device-side bit cast, no host round
+    # trip): costs are >= 0 and NaN maps to the +inf bits, so the word is < 2^31
+    cost = (key >> 32).to(torch.int32).view(torch.float32)
     return key, out, cost
 
 

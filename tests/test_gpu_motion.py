@@ -133,6 +133,28 @@ def test_per_problem_dt_eval_parity(native, O, H):
     ctx.close()
 
 
+def test_interpolate_parity(native, O):
+    """B21: the interpolation kernel against the oracle on random state sequences and
+    spacings (including a spacing below dt_fine and one that truncates at n_max): the count n is
+    decided exactly, points agree to fp32 rounding, rows past n repeat x_H."""
+    g = np.random.default_rng(8)
+    B, H, D, n_max = 9, 32, 7, 256
+    x = f32(g.uniform(-2.5, 2.5, (B, H, D)))
+    dt = f32(np.array([0.25, 0.1, 0.137, 0.02, 0.0253, 0.3, 0.2083, 0.05, 0.4]))
+    pts, n = native.interpolate(T(x), T(dt), 0.025, n_max)
+    pts, n = pts.cpu().numpy(), n.cpu().numpy()
+    for b in range(B):
+        nr, ref = O.interpolate(x[b], float(dt[b]), 0.025, n_max)
+        assert n[b] == nr, (b, n[b], nr)
+        m = min(nr, n_max)
+        np.testing.assert_allclose(pts[b, :m], ref, rtol=0, atol=3e-6)
+        if nr <= n_max:
+            np.testing.assert_array_equal(pts[b, m - 1], x[b, -1])
+        if m < n_max:
+            np.testing.assert_array_equal(pts[b, m:], np.broadcast_to(x[b, -1], (n_max - m, D)))
+    assert (n > n_max).any() and (n <= n_max).any()
+
+
 def test_motion_gen_pipeline_end_to_end(native, O):
     from paper_2310_17274_b200 import motion_gen, workload
     P = 6
@@ -156,7 +178,13 @@ def test_motion_gen_pipeline_end_to_end(native, O):
         assert sum(v for v, mg_ in ok if mg_ > 2e-5) == sum(1 for v, mg_ in ok if mg_ > 2e-5)
         s, _, _ = O.retime(R, wl.start[p], out["variables"][p].cpu().numpy().astype(np.float64), dt[p])   # limits at dt_f
         assert s == pytest.approx(1.0, rel=1e-3)
+        # the success claim includes every state of the 0.025 s grid (B21), re-checked
+        _, fine = O.interpolate(traj[p], dt[p], 0.025)
+        okf = [O.mask_sample(R, W, q) for q in fine]
+        assert all(v for v, mg_ in okf if mg_ > 2e-5)
     assert np.all(out["ik_count"].cpu().numpy() > 0)
+    assert np.array_equal(out["success"].cpu().numpy(),
+                          (out["final_score"] < float("inf")).cpu().numpy() & out["fine_valid"].cpu().numpy())
     ctx.close()
 
 

@@ -88,10 +88,38 @@ def test_weight_scaling_keeps_the_smoothness_term(O):
     base = O.eval_traj(R, W, cp, start, goal, V)[2][2]
     for dt in (0.05, 0.1, 0.4):
         cps = O.scale_params(cp, dt)
-        assert O.scale_params_c(cp, dt) == pytest.approx((dt, cps.a8, cps.a9, cps.flags))
+        assert O.scale_params_c(cp, dt) == pytest.approx((dt, cps.a8, cps.a9, cps.flags) + tuple(cps.w_bound))
         assert O.eval_traj(R, W, cps, start, goal, V)[2][2] == pytest.approx(base, rel=1e-10)
     # jerk enabled by the second optimisation (Alg. 4 enable_jerk_cost)
     assert O.scale_params(inputs.CostParams(flags=0), 0.1).flags & inputs.JERK
+
+
+def test_weight_scaling_keeps_large_limit_violations(O):
+    """B15 for the limit terms (P:2053 'all our cost terms that relate to velocity, acceleration,
+    and jerk'): beyond its band the limit cost grows with slope 1 in the derivative, which scales
+    like dt^-1, dt^-2, dt^-3 for v, a, j under re-timing; with the weights scaled by r, r^2, r^3 the
+    limit term of a path violating every limit by ~1e9x re-timed from 0.25 s to dt keeps its value
+    up to the band offsets (relative 1e-3).  (The position-limit weight does not change.)"""
+    rb = robots.franka64()
+    R = O.Robot(rb)
+    W = O.World(inputs.World(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros(0, np.int32)))
+    import dataclasses
+    big = dataclasses.replace(rb, vmax=rb.vmax * 1e-9, amax=rb.amax * 1e-9, jmax=rb.jmax * 1e-9,
+                              lo=rb.lo - 100.0, hi=rb.hi + 100.0)
+    Rb = O.Robot(big)
+    start, V = _traj(rb, 11)
+    goal = O.fk(R, V[-1])[2]
+    # a tiny activation band (eta_2): beyond it the limit cost is exactly |x| - limit + eta_2 / 2
+    cp = inputs.CostParams(flags=inputs.JERK, dt=0.25, a8=0.0, a9=0.0, eta_bound=1e-7)
+    base = O.eval_traj(Rb, W, cp, start, goal, V)[2][1]
+    assert base > 1e3
+    for dt in (0.05, 0.1, 0.4):
+        t = O.eval_traj(Rb, W, O.scale_params(cp, dt), start, goal, V)[2][1]
+        assert t == pytest.approx(base, rel=1e-3), dt
+        # the unscaled weights would change it by orders of magnitude
+        t0 = O.eval_traj(Rb, W, dataclasses.replace(cp, dt=dt), start, goal, V)[2][1]
+        assert abs(t0 / base - 1) > 0.5
+    assert O.scale_params(cp, 0.1).w_bound[0] == cp.w_bound[0]
 
 
 def test_goal_error_closed_forms(O):
@@ -125,3 +153,30 @@ def test_scores(O):
     assert b(0.001, 0.0, 100.0, 2.0) < b(0.002, 0.0, 100.0, 2.0)
     assert b(0.001, 0.0, 100.0, 2.0) < b(0.001, 0.0, 200.0, 2.0)
     assert O.blended_score(0.001, 0.0, 100.0, 2.0, 1e4, 1e-2, 10.0) == pytest.approx(10 * b(0.001, 0.0, 100.0, 2.0))
+
+
+def test_interpolation_pins(O):
+    """B21: the fine grid reproduces every coarse state that falls on it, the
+    end point is x_H, n = ceil((H - 1) dt / dt_fine) + 1, and a path linear in time (x_h = a + b h)
+    is reproduced exactly at every fine time t (x(t) = a + b t / dt)."""
+    g = np.random.default_rng(3)
+    H, D = 32, 7
+    a, b = g.normal(size=D), g.normal(size=D)
+    x = a + b * np.arange(H)[:, None]
+    for dt, dtf in ((0.25, 0.025), (0.1, 0.025), (0.137, 0.025), (0.02, 0.025)):
+        n, pts = O.interpolate(x, dt, dtf)
+        T = (H - 1) * dt
+        assert n == math.ceil(T / dtf) + 1
+        t = np.minimum(np.arange(n) * dtf, T)
+        np.testing.assert_allclose(pts, a + b * (t / dt)[:, None], rtol=0, atol=1e-12)
+        np.testing.assert_array_equal(pts[-1], x[-1])
+    # states on the fine grid are reproduced: dt = 4 dt_fine -> every 4th point is a state
+    y = g.normal(size=(H, D))
+    n, pts = O.interpolate(y, 0.1, 0.025)
+    np.testing.assert_allclose(pts[::4], y, rtol=0, atol=1e-12)
+    # between two states the points stay on the segment (convex combination)
+    mid = pts[2]
+    np.testing.assert_allclose(mid, 0.5 * (y[0] + y[1]), atol=1e-12)
+    # n_max truncates the output but reports the full count
+    n2, p2 = O.interpolate(y, 0.1, 0.025, n_max=10)
+    assert n2 == n and p2.shape == (10, D)
