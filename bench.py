@@ -31,7 +31,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "seed-timestep cost+grad evals/s"
 UNIT = "evals/s"
-FFMA_PER_CLK_PER_SM, SMS = 64, 148
+FP32_LANES_PER_SM, SMS = 128, 148
 
 
 def parse():
@@ -555,13 +555,16 @@ def run_native(args):
     evals_all = evals_per_step * args.steps * world   # seed mode: evals_per_step counts this rank's seeds
     value = evals_all / (total_ms * 1e-3)
 
-    # ---- roofline of the dominant kernel (solve_to_kernel; the select kernel is ~us).  FP32 peak for
-    # register-operand FFMA: 4 SMSPs x 32 lanes / 2-cycle reciprocal throughput (B300_MICROARCH pipe
-    # table) = 64 FFMA/clk/SM x 2 flops x 148 SMs x sm_max_mhz = 37.2 TFLOP/s; the FFMA
-    # microbenchmark tools/ffma_peak.cu measured 37.3 on this pool (profiles/r01_ffma_peak.json).
+    # ---- roofline of the dominant kernel (solve_to_kernel; the select kernel is ~us).  The path is
+    # bound by plain FP32 / ALU arithmetic ("alu"); the peak is the unit count: 148 SMs x 128 FP32
+    # lanes x 2 flops x sm_max_mhz (MEASURED_PEAKS.json) = 74.4 TFLOP/s.  tools/ffma_peak.cu on
+    # this pool (profiles/r02_ffma_peak.json): immediate-operand FFMA 72.4 TF (97 % of it), FADD /
+    # FMUL 124.5 lanes/clk/SM; register-operand FFMA 37.4 TF with shared operands, 45.9 with
+    # distinct ones (register-file bandwidth).  The round-1 denominator (64 FFMA/clk, 37.2 TF) is
+    # kept as `frac_of_register_ffma_ceiling` for continuity.
     pk = peaks()
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
-    peak_tf = SMS * FFMA_PER_CLK_PER_SM * 2 * sm_max * 1e6 / 1e12
+    peak_tf = SMS * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
     flops_eval = workload.nominal_flops_per_eval(wl)
     launch_s = statistics.mean(step_ms) * 1e-3
     achieved_tf = evals_per_step * flops_eval / launch_s / 1e12
@@ -633,12 +636,14 @@ def run_native(args):
                                           f"problem-sharded x{world}, no data-path collective"},
                 "roofline": {"bound": "alu", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                              "frac": achieved_tf / peak_tf, "traffic": traffic,
-                             "frac_of_unit_count_peak": achieved_tf / (2 * peak_tf),
+                             "frac_of_register_ffma_ceiling": achieved_tf / (0.5 * peak_tf),
                              "pipes": pipes_summary(),
                              "kernel": "solve_to_kernel", "flops_per_eval": flops_eval,
-                             "peak_basis": f"register-operand FFMA: 148 SMs x 64 FFMA/clk x 2 flops x {sm_max:.0f} MHz "
-                                           "(sm_max_mhz of MEASURED_PEAKS.json); measured 37.3 TF by tools/ffma_peak.cu; "
-                                           "the 128-lane unit count (74.4 TF) needs immediate-operand FFMA"},
+                             "peak_basis": f"FP32 unit count: 148 SMs x 128 lanes x 2 flops x {sm_max:.0f} MHz "
+                                           "(sm_max_mhz of MEASURED_PEAKS.json); tools/ffma_peak.cu measured 72.4 TF "
+                                           "immediate-operand FFMA, 37.4-45.9 TF register-operand FFMA "
+                                           "(profiles/r02_ffma_peak.json); achieved = nominal algorithmic flops "
+                                           "(SURVEY 8(d).2) / launch time; executed per-pipe rates in `pipes` (ncu)"},
                 "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
                 "extras": extras}
         print(json.dumps(line), flush=True)

@@ -144,7 +144,8 @@ def test_interpolate_parity(native, O):
     pts, n = native.interpolate(T(x), T(dt), 0.025, n_max)
     pts, n = pts.cpu().numpy(), n.cpu().numpy()
     for b in range(B):
-        nr, ref = O.interpolate(x[b], float(dt[b]), 0.025, n_max)
+        # identical inputs: the kernel receives dt_fine as fp32 (the count is decided in fp64 from it)
+        nr, ref = O.interpolate(x[b], float(dt[b]), float(np.float32(0.025)), n_max)
         assert n[b] == nr, (b, n[b], nr)
         m = min(nr, n_max)
         np.testing.assert_allclose(pts[b, :m], ref, rtol=0, atol=3e-6)
