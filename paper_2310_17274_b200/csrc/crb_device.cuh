@@ -35,6 +35,10 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #ifndef CRB_WORLD_H2
 #define CRB_WORLD_H2 1
 #endif
+// ... as a bounding-sphere test (1) or the Chebyshev box test in the cuboid frame (0)
+#ifndef CRB_WORLD_L1
+#define CRB_WORLD_L1 1
+#endif
 
 // World pre-screen on the tensor cores: 1 = the affine cuboid-frame
 // transform of a world group runs as HMMA.16816 on an fp16 hi/lo split, 0 = the FFMA screen only.
@@ -85,13 +89,14 @@ struct RobotPack {
 
 // Shared-memory layout (offsets in 4-byte words from the dynamic smem base).
 struct Layout {
-    int robot, boxes, mbar;
+    int robot, boxes, boxl1, mbar;
     int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, cbb, csm, gxd, gq, gva, pose_ft, tdp,
         goal, cfg_cost, cfg_terms, gV, red, st, scal, wq;
     int solver;      // start of the solver region
     int total;       // words
     int XS;          // row length of xs (H + 5)
     int boxes_gmem;  // 1: the cuboid table is read from global memory (large-world build), not staged
+    int stage_l1;    // 1: also stage the bounding-sphere pairs (solver / evaluation kernels, small worlds)
 };
 
 // Cost parameters (App. A), copied by value into registers by eval_pass.
@@ -113,6 +118,7 @@ struct KParams {
     const float4 *robot;     // packed robot blob (global)
     const float4 *boxes;     // [n_env][kmax][4] float4: (R col i, -col_i . t) x3, (h, M)
     const uint4 *boxes_h2;   // [n_env][kpairs][4] uint4: fp16x2 cuboid pairs (set_world)
+    const uint4 *boxes_l1;   // [n_env][kpairs] uint4: fp16x2 bounding-sphere pairs (cx, cy, cz, rho')
     int kpairs;
     const int *box_count;    // [n_env] enabled (compacted) boxes
     int kmax, n_env;
@@ -215,9 +221,12 @@ __device__ __forceinline__ int stage_tables(const KParams &kp, float *smem, int 
         mbar_init(bar, 1);
         const uint32_t rbytes = (uint32_t)kp.rp.words * 4u;
         const uint32_t bbytes = kp.lay.boxes_gmem ? 0u : (uint32_t)K * 64u;
-        mbar_expect_tx(bar, rbytes + bbytes);
+        // the bounding-sphere pairs of the small-world pre-screen (solver / evaluation kernels)
+        const uint32_t lbytes = (kp.lay.boxes_gmem || !kp.lay.stage_l1) ? 0u : (uint32_t)((K + 1) / 2) * 16u;
+        mbar_expect_tx(bar, rbytes + bbytes + lbytes);
         bulk_g2s(smem + kp.lay.robot, kp.robot, rbytes, bar);
         if (bbytes > 0) bulk_g2s(smem + kp.lay.boxes, kp.boxes + (size_t)env * kp.kmax * 4, bbytes, bar);
+        if (lbytes > 0) bulk_g2s(smem + kp.lay.boxl1, kp.boxes_l1 + (size_t)env * kp.kpairs, lbytes, bar);
     }
     {   // world work-queue order: identity, no cost history yet
         const int nwg = (kp.rp.M + 3) >> 2;
@@ -1144,7 +1153,60 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     }
                     } else
 #endif
-#if CRB_WORLD_H2
+#if CRB_WORLD_H2 && CRB_WORLD_L1
+                    {
+                    // fp16x2 bounding-sphere pre-screen, cuboids k, k+1 in the two halves, each
+                    // thread's 4 spheres broadcast: the cuboid lies inside the sphere (c_k, rho_k),
+                    // so an exact flag (box distance < th) implies |w - c_k| < rho_k + th.  In fp16:
+                    //   v = dx^2 + dy^2 + dz^2 - Rinf^2 < 0,  Rinf = (rho'_k + th)(1 + 10 u) + 4 u B_w,
+                    // u = 2^-11, rho'_k = rho_k + 4 u |c_k|_inf rounded up (set_world), B_w the
+                    // group's largest |w|_1: the input roundings of w and c move each difference by
+                    // at most 2 u (|w| + |c|), the three HFMA2 accumulations and the rounding of
+                    // Rinf^2 by at most ~6 u Rinf^2 at the decision point; (1 + 10 u) and 4 u B_w
+                    // cover both, so every cuboid the exact fp32 test would flag is flagged here.
+                    // Flagged cuboids go through the exact fp32 test in increasing k: the world term
+                    // is bitwise the all-fp32 screen's.  A group with |w| beyond the fp16 range (or
+                    // NaN) sends every cuboid to the exact test.
+                    unsigned sb = 0u;
+                    __half2 hx[4], hy[4], hz[4], hth[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        sb = max(sb, __float_as_uint(fabsf(cx[u]) + fabsf(cy[u]) + fabsf(cz[u])));
+                        const bool on = th2[u] > 0.f;   // disabled: far away, never flags
+                        hx[u] = __float2half2_rn(on ? cx[u] : 6e4f); hy[u] = __float2half2_rn(on ? cy[u] : 6e4f);
+                        hz[u] = __float2half2_rn(on ? cz[u] : 6e4f); hth[u] = __float2half2_rn(on ? sqrtf(th2[u]) : 0.f);
+                    }
+                    const float Bw = __uint_as_float(__reduce_max_sync(FULL, sb));
+                    const bool force = !(Bw < 3e4f);
+                    const __half2 ha = __float2half2_rn(force ? 0.f : 4.f * 4.8828125e-4f * Bw);
+                    const __half2 kinf = __float2half2_rn(1.0048828125f);   // 1 + 10 u, exact in fp16
+                    const uint4 *l1 = reinterpret_cast<const uint4 *>(smem + kp.lay.boxl1);
+                    for (int kb = 0; kb < K; kb += 2) {
+                        const uint4 w0 = l1[kb >> 1];
+                        const __half2 *W0 = reinterpret_cast<const __half2 *>(&w0);
+                        const __half2 cxp = W0[0], cyp = W0[1], czp = W0[2], rho = W0[3];
+                        __half2 mn = __float2half2_rn(1.f);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const __half2 dx = __hsub2(hx[u], cxp), dy = __hsub2(hy[u], cyp), dz = __hsub2(hz[u], czp);
+                            const __half2 R = __hfma2(__hadd2(rho, hth[u]), kinf, ha);
+                            __half2 acc = __hmul2(__hneg2(R), R);
+                            acc = __hfma2(dz, dz, acc);
+                            acc = __hfma2(dy, dy, acc);
+                            acc = __hfma2(dx, dx, acc);
+                            mn = __hmin2(mn, acc);
+                        }
+                        const unsigned fl = *reinterpret_cast<const unsigned *>(&mn) & 0x80008000u;
+                        const unsigned f = force ? 0x80008000u : __reduce_or_sync(FULL, fl);
+                        if (f) {
+                            CRB_STAT(1, ((f & 0x8000u) ? 1 : 0) + ((f & 0x80000000u) ? 1 : 0));
+#pragma unroll 1   // one copy of the exact path (instruction cache)
+                            for (int j = 0; j < 2; ++j)
+                                if ((f & (0x8000u << (16 * j))) && kb + j < K) exact_box(kb + j, true);
+                        }
+                    }
+                    }
+#elif CRB_WORLD_H2
                     {
                     // fp16x2 pre-screen, cuboids k, k+1 in the two halves, each thread's 4 spheres
                     // broadcast.  Chebyshev test max_i(|l_i| - (h_i + delta)) < th per sphere, with

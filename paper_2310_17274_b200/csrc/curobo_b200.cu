@@ -1639,7 +1639,8 @@ struct crb_ctx {
     // world
     bool world_ok = false;
     float4 *d_boxes = nullptr;
-    uint4 *d_boxes_h2 = nullptr;          // fp16x2 cuboid pairs of the small-world pre-screen
+    uint4 *d_boxes_h2 = nullptr;          // fp16x2 cuboid pairs (Chebyshev pre-screen, CRB_WORLD_L1 = 0)
+    uint4 *d_boxes_l1 = nullptr;          // fp16x2 bounding-sphere pairs of the small-world pre-screen
     int kpairs = 1;                       // pairs per environment in d_boxes_h2
     int *d_box_count = nullptr;
     int n_env = 0, kmax = 0, kmax_enabled = 0;
@@ -1705,6 +1706,7 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     auto take = [&](int words) { int o = w; w += r4(words); return o; };
     L.robot = take(rp.words);
     L.boxes = take(kmax * 16);
+    L.boxl1 = take(((kmax + 1) / 2) * 4);   // bounding-sphere pairs (small-world build; 0 when kmax = 0)
     L.mbar = take(4);
     L.XS = mode == MODE_TO ? H + 5 : 0;
     L.q_cfg = take(D * NC);
@@ -1750,6 +1752,7 @@ KParams base_params(const crb_ctx *ctx) {
     kp.robot = ctx->d_robot;
     kp.boxes = ctx->d_boxes;
     kp.boxes_h2 = ctx->d_boxes_h2;
+    kp.boxes_l1 = ctx->d_boxes_l1;
     kp.kpairs = ctx->kpairs;
     kp.box_count = ctx->d_box_count;
     kp.kmax = ctx->kmax;
@@ -1828,6 +1831,7 @@ crb_status crb_destroy(crb_ctx *ctx) {
     if (!ctx) return CRB_E_ARG;
     cudaSetDevice(ctx->device);
     cudaFree(ctx->d_robot); cudaFree(ctx->d_boxes); cudaFree(ctx->d_boxes_h2); cudaFree(ctx->d_box_count);
+    cudaFree(ctx->d_boxes_l1);
     cudaFree(ctx->ws_cost); cudaFree(ctx->ws_traj); cudaFree(ctx->ws_mask); cudaFree(ctx->ws_n);
     cudaFree(ctx->h_seeds); cudaFree(ctx->h_start); cudaFree(ctx->h_goal); cudaFree(ctx->h_best);
     cudaFree(ctx->h_bcost); cudaFree(ctx->h_env); cudaFree(ctx->h_key);
@@ -2087,6 +2091,7 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
     if (st != CRB_OK) return st;
     if (n_env < 1 || k_max < 0 || !boxes_per_env || (k_max > 0 && !boxes)) return fail(ctx, CRB_E_ARG, "bad world arguments");
     std::vector<float> packed((size_t)n_env * std::max(k_max, 1) * 16, 0.f);
+    std::vector<double> sph_c((size_t)n_env * std::max(k_max, 1) * 4, 0.0);   // bounding sphere (centre, radius)
     std::vector<int> count(n_env, 0);
     int kmax_en = 0;
     for (int e = 0; e < n_env; ++e) {
@@ -2113,6 +2118,10 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
                 o[4 * i2 + 3] = (float)(-(R[0][i2] * b.pos[0] + R[1][i2] * b.pos[1] + R[2][i2] * b.pos[2]));
             }
             o[12] = 0.5f * b.dims[0]; o[13] = 0.5f * b.dims[1]; o[14] = 0.5f * b.dims[2];
+            double *bs = &sph_c[((size_t)e * k_max + k) * 4];
+            bs[0] = b.pos[0]; bs[1] = b.pos[1]; bs[2] = b.pos[2];
+            bs[3] = 0.5 * std::sqrt((double)b.dims[0] * b.dims[0] + (double)b.dims[1] * b.dims[1] +
+                                    (double)b.dims[2] * b.dims[2]);
             // cuboid magnitude M = max(|off_i|, h_i) for the rounding slack of the reduced-precision
             // pre-screens (crb_device.cuh: HMMA hi/lo split, fp16x2 screen); NaN beyond the fp16
             // range, which makes both screens send every sphere to the exact fp32 test
@@ -2143,9 +2152,53 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
             }
             for (int i = 0; i < 16; ++i) ph[((size_t)e * kpairs + p2) * 16 + i] = __floats2half2_rn(v[0][i], v[1][i]);
         }
-    cudaFree(ctx->d_boxes); cudaFree(ctx->d_boxes_h2); cudaFree(ctx->d_box_count);
-    ctx->d_boxes = nullptr; ctx->d_boxes_h2 = nullptr; ctx->d_box_count = nullptr;
+    // fp16x2 bounding-sphere pairs for the small-world pre-screen (crb_device.cuh "bounding-sphere
+    // pre-screen"): per pair the centres (x, y, z) rounded to nearest and rho' = circumradius +
+    // 4 u max|c| (the centre's fp16 rounding, u = 2^-11) rounded UP.  A cuboid beyond the fp16 range
+    // gets centre 0 and rho' = 6e4 (always flagged); a missing second cuboid sits at 6e4 on every
+    // axis with rho' = 0 (its squared distance overflows to +inf: never flagged).
+    std::vector<__half2> pl1((size_t)n_env * kpairs * 4, __floats2half2_rn(0.f, 0.f));
+    auto half_up = [](double v) {   // smallest half >= v (v >= 0, below the fp16 maximum)
+        __half h = __float2half_rn((float)v);
+        while ((double)__half2float(h) < v) {
+            unsigned short bits;
+            memcpy(&bits, &h, 2);
+            ++bits;
+            memcpy(&h, &bits, 2);
+        }
+        return h;
+    };
+    for (int e = 0; e < n_env; ++e)
+        for (int p2 = 0; p2 < kpairs; ++p2) {
+            __half c[2][4];
+            for (int j = 0; j < 2; ++j) {
+                const int k = 2 * p2 + j;
+                if (k >= count[e]) {
+                    for (int i = 0; i < 3; ++i) c[j][i] = __float2half_rn(6e4f);
+                    c[j][3] = __float2half_rn(0.f);
+                    continue;
+                }
+                const double *bs = &sph_c[((size_t)e * k_max + k) * 4];
+                const double cm = std::max({std::fabs(bs[0]), std::fabs(bs[1]), std::fabs(bs[2])});
+                const double rp = bs[3] + 4.0 * 4.8828125e-4 * cm;
+                if (!(cm < 3e4) || !(rp < 3e4)) {
+                    for (int i = 0; i < 3; ++i) c[j][i] = __float2half_rn(0.f);
+                    c[j][3] = __float2half_rn(6e4f);
+                    continue;
+                }
+                for (int i = 0; i < 3; ++i) c[j][i] = __float2half_rn((float)bs[i]);
+                c[j][3] = half_up(rp);
+            }
+            for (int i = 0; i < 4; ++i) pl1[((size_t)e * kpairs + p2) * 4 + i] = __halves2half2(c[0][i], c[1][i]);
+        }
+    cudaFree(ctx->d_boxes); cudaFree(ctx->d_boxes_h2); cudaFree(ctx->d_box_count); cudaFree(ctx->d_boxes_l1);
+    ctx->d_boxes = nullptr; ctx->d_boxes_h2 = nullptr; ctx->d_box_count = nullptr; ctx->d_boxes_l1 = nullptr;
     ctx->world_ok = false;
+    st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes_l1, pl1.size() * sizeof(__half2)), "cudaMalloc boxes l1");
+    if (st != CRB_OK) return st;
+    st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes_l1, pl1.data(), pl1.size() * sizeof(__half2), cudaMemcpyHostToDevice),
+                    "upload boxes l1");
+    if (st != CRB_OK) return st;
     st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes, packed.size() * 4), "cudaMalloc boxes");
     if (st != CRB_OK) return st;
     st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes_h2, ph.size() * sizeof(__half2)), "cudaMalloc boxes h2");
@@ -2213,6 +2266,7 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
     kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs; kp.dt_arr = dt;
     const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
     kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
+    kp.lay.stage_l1 = use_world_mma(ctx) ? 0 : 1;
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
     const bool wm = use_world_mma(ctx);
     if (mode == MODE_TO)
@@ -2275,6 +2329,7 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     kp.seed_best_cost = sbc; kp.seed_best_traj = sbt;
     const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
     kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
+    kp.lay.stage_l1 = use_world_mma(ctx) ? 0 : 1;
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids + solver)");
     const bool wm = use_world_mma(ctx);
     // latency mode: A CTAs per seed in a cluster when the whole batch fits one wave (2 CTAs / SM)
@@ -2376,6 +2431,7 @@ crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, i
     const int mode = H == 1 ? MODE_IK : MODE_TO;
     const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, history, n_alpha, true, kp.lay);
     kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
+    kp.lay.stage_l1 = use_world_mma(ctx) ? 0 : 1;
     if (smem_bytes) *smem_bytes = (int)bytes;
     if (bytes > SMEM_MAX) { if (ctas_per_sm) *ctas_per_sm = 0; return CRB_OK; }
     int n = 0;
