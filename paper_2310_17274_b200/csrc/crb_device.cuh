@@ -39,6 +39,11 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #ifndef CRB_WORLD_L1
 #define CRB_WORLD_L1 1
 #endif
+// The large-world build (cuboid table in global memory) with the fp16x2 bounding-sphere screen (1)
+// instead of the tensor-core screen (0)
+#ifndef CRB_LARGE_L1
+#define CRB_LARGE_L1 0
+#endif
 
 // World pre-screen on the tensor cores: 1 = the affine cuboid-frame
 // transform of a world group runs as HMMA.16816 on an fp16 hi/lo split, 0 = the FFMA screen only.
@@ -1069,7 +1074,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
                     CRB_STAT(0, K);
 #if CRB_WORLD_MMA
-                    if (WMMA) {
+                    if (WMMA && !CRB_LARGE_L1) {
                     // tensor-core pre-screen, 8 cuboids per step; only cuboids with a flagged row
                     // go through exact_box, in increasing k (the accumulation order of the FFMA path)
                     const int g8 = lane >> 2, t4 = lane & 3;
@@ -1180,9 +1185,13 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     const bool force = !(Bw < 3e4f);
                     const __half2 ha = __float2half2_rn(force ? 0.f : 4.f * 4.8828125e-4f * Bw);
                     const __half2 kinf = __float2half2_rn(1.0048828125f);   // 1 + 10 u, exact in fp16
-                    const uint4 *l1 = reinterpret_cast<const uint4 *>(smem + kp.lay.boxl1);
+                    // small worlds: the pairs staged in shared memory; large worlds (CRB_LARGE_L1):
+                    // read through the read-only cache
+                    const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
+                    const uint4 *l1 = WMMA ? kp.boxes_l1 + (size_t)envc * kp.kpairs
+                                           : reinterpret_cast<const uint4 *>(smem + kp.lay.boxl1);
                     for (int kb = 0; kb < K; kb += 2) {
-                        const uint4 w0 = l1[kb >> 1];
+                        const uint4 w0 = WMMA ? __ldg(l1 + (kb >> 1)) : l1[kb >> 1];
                         const __half2 *W0 = reinterpret_cast<const __half2 *>(&w0);
                         const __half2 cxp = W0[0], cyp = W0[1], czp = W0[2], rho = W0[3];
                         __half2 mn = __float2half2_rn(1.f);

@@ -62,6 +62,28 @@ MUTATIONS = [
     ("direction_not_negated", "A18: d = r instead of -r",
      "for (int t = 0; t < n; ++t) d[t] = -q[t];",
      "for (int t = 0; t < n; ++t) d[t] = q[t];"),
+    # round-2 additions: kinematics, geometry, stencil, pose, B15, B21
+    ("revolute_x_sign", "Table 6 revolute-x rotation with the sine sign swapped",
+     "J[1][1] = c; J[1][2] = -s; J[2][1] = s; J[2][2] = c; break;",
+     "J[1][1] = c; J[1][2] = s; J[2][1] = -s; J[2][2] = c; break;"),
+    ("activation_quadratic_scale", "Eq. smooth-distance-cases: d'^2/eta instead of d'^2/(2 eta)",
+     "return dprime * dprime / (2.0 * eta); }",
+     "return dprime * dprime / (eta); }"),
+    ("self_tie_last_pair", "A28: the LAST maximal pair instead of the first",
+     "if (P > best) { second = best; best = P; ibest = p; }",
+     "if (P >= best) { second = best; best = P; ibest = p; }"),
+    ("stencil_velocity_coeff", "O3: five-point velocity with 7 instead of 8",
+     "v[(h - 1) * D + d] = (-xp2 + 8 * xp1 - 8 * xm1 + xm2) / (12 * dt);",
+     "v[(h - 1) * D + d] = (-xp2 + 7 * xp1 - 8 * xm1 + xm2) / (12 * dt);"),
+    ("pose_orientation_weight", "Eq. pose_cost_term: alpha_2 in place of alpha_3 in the orientation term",
+     "double C = pr->a0 * orc_logcosh(pr->a2 * n) + pr->a1 * orc_logcosh(pr->a3 * er);",
+     "double C = pr->a0 * orc_logcosh(pr->a2 * n) + pr->a1 * orc_logcosh(pr->a2 * er);"),
+    ("b15_acc_limit_exponent", "B15 / P:2053: acceleration-limit weight scaled by r instead of r^2",
+     "out->w_bound[2] = in->w_bound[2] * r * r;",
+     "out->w_bound[2] = in->w_bound[2] * r;"),
+    ("b21_nearest_not_linear", "B21 / P:1606: nearest state instead of linear interpolation",
+     "        double f = u - i;",
+     "        double f = (u - i) < 0.5 ? 0.0 : 1.0;"),
 ]
 
 
