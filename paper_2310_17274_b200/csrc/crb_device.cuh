@@ -40,9 +40,11 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #define CRB_WORLD_L1 1
 #endif
 // The large-world build (cuboid table in global memory) with the fp16x2 bounding-sphere screen (1)
-// instead of the tensor-core screen (0)
+// instead of the tensor-core screen (0).  Measured (tools/k_sweep.py, 32 problems x 32 seeds x 30
+// iterations, M evals/s, HMMA -> bounding sphere): K = 64 162.5 -> 171.4, 128 95.0 -> 99.7,
+// 256 52.0 -> 54.6, dense K = 1000 22.4 -> 23.9 (gpurun_out/ksweep_l1.txt, profiles/r02_*)
 #ifndef CRB_LARGE_L1
-#define CRB_LARGE_L1 0
+#define CRB_LARGE_L1 1
 #endif
 
 // World pre-screen on the tensor cores: 1 = the affine cuboid-frame
@@ -474,71 +476,61 @@ __device__ __forceinline__ float *ee_frame(const Smem &s, int D) { return s.fram
 // sw[m][3][32] = R_link c_m + t_link.
 __device__ __forceinline__ void fk_chain(const RobotPack &rp, const Smem &s) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    {
-        const int r = warp - FK_W0;   // chain row
-        float *fee = ee_frame(s, rp.D);
-        float4 cur = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int l = 0; l < rp.L; ++l) {
-            const float *F = s.fw + rp.o_links + 16 * l;
-            const int parent = s.iw[rp.o_links + 16 * l + 12];
-            const int type = s.iw[rp.o_links + 16 * l + 13];
-            const int dof = s.iw[rp.o_links + 16 * l + 14];
-            float4 pr;
-            if (parent < 0) pr = make_float4(r == 0, r == 1, r == 2, 0.f);
-            else if (parent == l - 1) pr = cur;
-            else {
-                const float *src = s.lt + (parent * 12 + r * 4) * NC + lane;
-                pr = make_float4(src[0], src[NC], src[2 * NC], src[3 * NC]);
-            }
-            // local transform M = F * J(v): Table 6 "Full Link Transformation" column (A25 fixed)
-            float m00 = F[0], m01 = F[1], m02 = F[2], m03 = F[3];
-            float m10 = F[4], m11 = F[5], m12 = F[6], m13 = F[7];
-            float m20 = F[8], m21 = F[9], m22 = F[10], m23 = F[11];
-            if (type != 0) {
-                const float v = s.q_cfg[dof * NC + lane];
-                if (type <= 3) {           // prismatic: col3 += v * col_axis
-                    if (type == 1) { m03 = fmaf(m00, v, m03); m13 = fmaf(m10, v, m13); m23 = fmaf(m20, v, m23); }
-                    else if (type == 2) { m03 = fmaf(m01, v, m03); m13 = fmaf(m11, v, m13); m23 = fmaf(m21, v, m23); }
-                    else { m03 = fmaf(m02, v, m03); m13 = fmaf(m12, v, m13); m23 = fmaf(m22, v, m23); }
-                } else {
-                    const float sn = s.scs[dof * NC + lane], cs = s.scs[(rp.D + dof) * NC + lane];
-                    if (type == 4) {        // revolute x: col1' = c f1 + s f2, col2' = -s f1 + c f2
-                        const float a0 = m01, a1 = m11, a2 = m21;
-                        m01 = cs * a0 + sn * m02; m11 = cs * a1 + sn * m12; m21 = cs * a2 + sn * m22;
-                        m02 = -sn * a0 + cs * m02; m12 = -sn * a1 + cs * m12; m22 = -sn * a2 + cs * m22;
-                    } else if (type == 5) { // revolute y: col0' = c f0 - s f2, col2' = s f0 + c f2
-                        const float a0 = m00, a1 = m10, a2 = m20;
-                        m00 = cs * a0 - sn * m02; m10 = cs * a1 - sn * m12; m20 = cs * a2 - sn * m22;
-                        m02 = sn * a0 + cs * m02; m12 = sn * a1 + cs * m12; m22 = sn * a2 + cs * m22;
-                    } else {                // revolute z: col0' = c f0 + s f1, col1' = -s f0 + c f1
-                        const float a0 = m00, a1 = m10, a2 = m20;
-                        m00 = cs * a0 + sn * m01; m10 = cs * a1 + sn * m11; m20 = cs * a2 + sn * m21;
-                        m01 = -sn * a0 + cs * m01; m11 = -sn * a1 + cs * m11; m21 = -sn * a2 + cs * m21;
-                    }
-                }
-            }
-            float4 nr;
-            nr.x = pr.x * m00 + pr.y * m10 + pr.z * m20;
-            nr.y = pr.x * m01 + pr.y * m11 + pr.z * m21;
-            nr.z = pr.x * m02 + pr.y * m12 + pr.z * m22;
-            nr.w = pr.x * m03 + pr.y * m13 + pr.z * m23 + pr.w;
-            float *dst = s.lt + (l * 12 + r * 4) * NC + lane;
-            dst[0] = nr.x; dst[NC] = nr.y; dst[2 * NC] = nr.z; dst[3 * NC] = nr.w;
-            if (type != 0) {   // joint axis = column `ax` of R_l, origin = t_l (Table 7)
-                const int ax = type >= 4 ? type - 4 : type - 1;
-                float *fr = s.frames + dof * 6 * NC + lane;
-                fr[r * NC] = ax == 0 ? nr.x : (ax == 1 ? nr.y : nr.z);
-                fr[(3 + r) * NC] = nr.w;
-            }
-            if (l == rp.ee) {   // EE = T_frame * C_ee (the folded fixed offset)
-                const float *E = s.fw + rp.o_eeoff;
-                fee[(3 * r + 0) * NC + lane] = nr.x * E[0] + nr.y * E[4] + nr.z * E[8];
-                fee[(3 * r + 1) * NC + lane] = nr.x * E[1] + nr.y * E[5] + nr.z * E[9];
-                fee[(3 * r + 2) * NC + lane] = nr.x * E[2] + nr.y * E[6] + nr.z * E[10];
-                fee[(9 + r) * NC + lane] = nr.x * E[3] + nr.y * E[7] + nr.z * E[11] + nr.w;
-            }
-            cur = nr;
+    const int r = warp - FK_W0;   // chain row
+    float *fee = ee_frame(s, rp.D);
+    const float4 *L4 = reinterpret_cast<const float4 *>(s.fw + rp.o_links);   // 16 words per frame
+    float4 cur = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int l = 0; l < rp.L; ++l) {
+        const float4 f0 = L4[4 * l], f1 = L4[4 * l + 1], f2 = L4[4 * l + 2];   // rows of F (3x4)
+        const int4 md = reinterpret_cast<const int4 *>(L4)[4 * l + 3];         // parent, type, dof
+        const int parent = md.x, type = md.y, dof = md.z;
+        float4 pr;
+        if (parent < 0) pr = make_float4(r == 0, r == 1, r == 2, 0.f);
+        else if (parent == l - 1) pr = cur;
+        else {
+            const float *src = s.lt + (parent * 12 + r * 4) * NC + lane;
+            pr = make_float4(src[0], src[NC], src[2 * NC], src[3 * NC]);
         }
+        // row r of T_l = row r of T_parent . F . J(v) (Table 6, A25 fixed): first u = pr . F (the
+        // parent row times F's columns, translation column + pr.w), then the joint acts on u --
+        // a rotation of two of its rotation entries, or a shift of the translation along an axis
+        float u0 = fmaf(pr.z, f2.x, fmaf(pr.y, f1.x, pr.x * f0.x));
+        float u1 = fmaf(pr.z, f2.y, fmaf(pr.y, f1.y, pr.x * f0.y));
+        float u2 = fmaf(pr.z, f2.z, fmaf(pr.y, f1.z, pr.x * f0.z));
+        float u3 = fmaf(pr.z, f2.w, fmaf(pr.y, f1.w, fmaf(pr.x, f0.w, pr.w)));
+        if (type >= 4) {
+            const float sn = s.scs[dof * NC + lane], cs = s.scs[(rp.D + dof) * NC + lane];
+            if (type == 4) {        // revolute x: (u1, u2) <- (c u1 + s u2, -s u1 + c u2)
+                const float a = u1;
+                u1 = fmaf(sn, u2, cs * a); u2 = fmaf(-sn, a, cs * u2);
+            } else if (type == 5) { // revolute y: (u0, u2) <- (c u0 - s u2, s u0 + c u2)
+                const float a = u0;
+                u0 = fmaf(-sn, u2, cs * a); u2 = fmaf(sn, a, cs * u2);
+            } else {                // revolute z: (u0, u1) <- (c u0 + s u1, -s u0 + c u1)
+                const float a = u0;
+                u0 = fmaf(sn, u1, cs * a); u1 = fmaf(-sn, a, cs * u1);
+            }
+        } else if (type >= 1) {     // prismatic: translation += v * (pr . F column axis)
+            const float v = s.q_cfg[dof * NC + lane];
+            u3 = fmaf(v, type == 1 ? u0 : (type == 2 ? u1 : u2), u3);
+        }
+        const float4 nr = make_float4(u0, u1, u2, u3);
+        float *dst = s.lt + (l * 12 + r * 4) * NC + lane;
+        dst[0] = nr.x; dst[NC] = nr.y; dst[2 * NC] = nr.z; dst[3 * NC] = nr.w;
+        if (type != 0) {   // joint axis = column `ax` of R_l, origin = t_l (Table 7)
+            const int ax = type >= 4 ? type - 4 : type - 1;
+            float *fr = s.frames + dof * 6 * NC + lane;
+            fr[r * NC] = ax == 0 ? nr.x : (ax == 1 ? nr.y : nr.z);
+            fr[(3 + r) * NC] = nr.w;
+        }
+        if (l == rp.ee) {   // EE = T_frame * C_ee (the folded fixed offset)
+            const float *E = s.fw + rp.o_eeoff;
+            fee[(3 * r + 0) * NC + lane] = nr.x * E[0] + nr.y * E[4] + nr.z * E[8];
+            fee[(3 * r + 1) * NC + lane] = nr.x * E[1] + nr.y * E[5] + nr.z * E[9];
+            fee[(3 * r + 2) * NC + lane] = nr.x * E[2] + nr.y * E[6] + nr.z * E[10];
+            fee[(9 + r) * NC + lane] = nr.x * E[3] + nr.y * E[7] + nr.z * E[11] + nr.w;
+        }
+        cur = nr;
     }
 }
 
