@@ -1155,12 +1155,14 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     // fp16x2 bounding-sphere pre-screen, cuboids k, k+1 in the two halves, each
                     // thread's 4 spheres broadcast: the cuboid lies inside the sphere (c_k, rho_k),
                     // so an exact flag (box distance < th) implies |w - c_k| < rho_k + th.  In fp16:
-                    //   v = dx^2 + dy^2 + dz^2 - Rinf^2 < 0,  Rinf = (rho'_k + th)(1 + 10 u) + 4 u B_w,
-                    // u = 2^-11, rho'_k = rho_k + 4 u |c_k|_inf rounded up (set_world), B_w the
-                    // group's largest |w|_1: the input roundings of w and c move each difference by
-                    // at most 2 u (|w| + |c|), the three HFMA2 accumulations and the rounding of
-                    // Rinf^2 by at most ~6 u Rinf^2 at the decision point; (1 + 10 u) and 4 u B_w
-                    // cover both, so every cuboid the exact fp32 test would flag is flagged here.
+                    //   v = dx^2 + dy^2 + dz^2 - Rinf^2 < 0,  Rinf = rk_k + tk,
+                    //   rk_k = (rho_k + 4 u |c_k|_inf)(1 + 12 u) rounded up (set_world),
+                    //   tk = th (1 + 12 u) + 4 u B_w (per sphere and slot, once per item),
+                    // u = 2^-11, B_w the group's largest |w|_1: the input roundings of w and c move
+                    // each difference by at most 2 u (|w| + |c|), the three HFMA2 accumulations, the
+                    // sum rk + tk, the rounding of tk and of Rinf^2 by at most ~8 u Rinf^2 at the
+                    // decision point; (1 + 12 u) and 4 u B_w cover them, so every cuboid the exact
+                    // fp32 test would flag is flagged here.
                     // Flagged cuboids go through the exact fp32 test in increasing k: the world term
                     // is bitwise the all-fp32 screen's.  A group with |w| beyond the fp16 range (or
                     // NaN) sends every cuboid to the exact test.
@@ -1176,7 +1178,9 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     const float Bw = __uint_as_float(__reduce_max_sync(FULL, sb));
                     const bool force = !(Bw < 3e4f);
                     const __half2 ha = __float2half2_rn(force ? 0.f : 4.f * 4.8828125e-4f * Bw);
-                    const __half2 kinf = __float2half2_rn(1.0048828125f);   // 1 + 10 u, exact in fp16
+                    const __half2 kinf = __float2half2_rn(1.005859375f);   // 1 + 12 u, exact in fp16
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) hth[u] = __hfma2(hth[u], kinf, ha);   // tk
                     // small worlds: the pairs staged in shared memory; large worlds (CRB_LARGE_L1):
                     // read through the read-only cache
                     const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
@@ -1190,7 +1194,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const __half2 dx = __hsub2(hx[u], cxp), dy = __hsub2(hy[u], cyp), dz = __hsub2(hz[u], czp);
-                            const __half2 R = __hfma2(__hadd2(rho, hth[u]), kinf, ha);
+                            const __half2 R = __hadd2(rho, hth[u]);
                             __half2 acc = __hmul2(__hneg2(R), R);
                             acc = __hfma2(dz, dz, acc);
                             acc = __hfma2(dy, dy, acc);

@@ -2152,9 +2152,9 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
             }
             for (int i = 0; i < 16; ++i) ph[((size_t)e * kpairs + p2) * 16 + i] = __floats2half2_rn(v[0][i], v[1][i]);
         }
-    // fp16x2 bounding-sphere pairs for the small-world pre-screen (crb_device.cuh "bounding-sphere
-    // pre-screen"): per pair the centres (x, y, z) rounded to nearest and rho' = circumradius +
-    // 4 u max|c| (the centre's fp16 rounding, u = 2^-11) rounded UP.  A cuboid beyond the fp16 range
+    // fp16x2 bounding-sphere pairs for the pre-screen (crb_device.cuh "bounding-sphere pre-screen"):
+    // per pair the centres (x, y, z) rounded to nearest and rk = (circumradius + 4 u max|c|) (1 +
+    // 12 u) (the centre's fp16 rounding and the screen's rounding factor, u = 2^-11) rounded UP.  A cuboid beyond the fp16 range
     // gets centre 0 and rho' = 6e4 (always flagged); a missing second cuboid sits at 6e4 on every
     // axis with rho' = 0 (its squared distance overflows to +inf: never flagged).
     std::vector<__half2> pl1((size_t)n_env * kpairs * 4, __floats2half2_rn(0.f, 0.f));
@@ -2180,7 +2180,7 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
                 }
                 const double *bs = &sph_c[((size_t)e * k_max + k) * 4];
                 const double cm = std::max({std::fabs(bs[0]), std::fabs(bs[1]), std::fabs(bs[2])});
-                const double rp = bs[3] + 4.0 * 4.8828125e-4 * cm;
+                const double rp = (bs[3] + 4.0 * 4.8828125e-4 * cm) * (1.0 + 12.0 * 4.8828125e-4);
                 if (!(cm < 3e4) || !(rp < 3e4)) {
                     for (int i = 0; i < 3; ++i) c[j][i] = __float2half_rn(0.f);
                     c[j][3] = __float2half_rn(6e4f);
