@@ -22,30 +22,42 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 FTZ = {SRC: ["-ftz=true"], SRC_WMMA: []}
 
 
-def compile_lib(out: str, defs=(), ptxas_verbose: bool = False, ftz: bool = True) -> str:
+def compile_lib(out: str, defs=(), ptxas_verbose: bool = False, ftz: bool = True, ftz_all: bool = False) -> str:
     """Compile both translation units (in parallel) and link them into the shared library `out`;
-    returns ptxas's report.  `defs` are extra nvcc arguments (tools/variant.py)."""
+    returns ptxas's report.  `defs` are extra nvcc arguments (tools/variant.py); ftz_all compiles
+    the large-world unit with flush-to-zero too (A/B).  Every compiler process is waited for (or
+    killed) before an error is raised, and the object files are removed in all cases."""
     objs, procs = [], []
-    for src in (SRC, SRC_WMMA):
-        obj = f"{out}.{os.path.basename(src)}.o"
-        cmd = [NVCC, *FLAGS, *(FTZ[src] if ftz else []), *(["-Xptxas", "-v"] if ptxas_verbose else []), *defs,
-               "-c", "-o", obj, src]
-        procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
-        objs.append(obj)
     report = ""
-    for p in procs:
-        o, e = p.communicate()
-        report += o + e
-        if p.returncode != 0:
-            sys.stderr.write(o + e)
+    try:
+        for src in (SRC, SRC_WMMA):
+            obj = f"{out}.{os.path.basename(src)}.o"
+            fz = (["-ftz=true"] if ftz_all else FTZ[src]) if ftz else []
+            cmd = [NVCC, *FLAGS, *fz, *(["-Xptxas", "-v"] if ptxas_verbose else []), *defs, "-c", "-o", obj, src]
+            procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+            objs.append(obj)
+        failed = None
+        for p in procs:
+            o, e = p.communicate()
+            report += o + e
+            if p.returncode != 0 and failed is None:
+                failed = o + e
+        if failed is not None:
+            sys.stderr.write(failed)
             raise RuntimeError(f"nvcc failed building {os.path.basename(out)}")
-    r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs],
-                       capture_output=True, text=True)
-    for obj in objs:
-        os.remove(obj)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError(f"nvcc failed linking {os.path.basename(out)}")
+        r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed linking {os.path.basename(out)}")
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+                p.wait()
+        for obj in objs:
+            if os.path.exists(obj):
+                os.remove(obj)
     return report
 
 

@@ -1015,15 +1015,12 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 }
                 __syncwarp();   // the zeroed accumulators are visible to the lanes that flush into them
                 // exact fp32 test of cuboid k for the group (the screen of record)
-                // (umask: the spheres of the group some lane's pre-screen flagged for this cuboid;
-                // the others cannot be flagged by the exact test either and are skipped)
-                auto exact_box = [&](int k, bool reload, unsigned umask) {
+                auto exact_box = [&](int k, bool reload) {
                         const BoxView b = load_box(s.boxes, k);
                         float s2[4];
                         bool any = false;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            if (!((umask >> u) & 1u)) { s2[u] = INFINITY; continue; }   // warp-uniform
                             if (reload) {   // after the tensor-core screen: reload instead of holding it
                                 const float4 c = m0 + u < rp.M ? s.sw[(m0 + u) * NC + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
                                 s2[u] = box_screen(c.x, c.y, c.z, b);
@@ -1147,7 +1144,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                             while (mask) {
                                 const int b = __ffs(mask) - 1;
                                 mask &= mask - 1u;
-                                exact_box(kb + b, true, 0xFu);
+                                exact_box(kb + b, true);
                             }
                         }
                     }
@@ -1193,31 +1190,24 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         const uint4 w0 = WMMA ? __ldg(l1 + (kb >> 1)) : l1[kb >> 1];
                         const __half2 *W0 = reinterpret_cast<const __half2 *>(&w0);
                         const __half2 cxp = W0[0], cyp = W0[1], czp = W0[2], rho = W0[3];
-                        __half2 mn = __float2half2_rn(1.f), acc[4];
+                        __half2 mn = __float2half2_rn(1.f);
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const __half2 dx = __hsub2(hx[u], cxp), dy = __hsub2(hy[u], cyp), dz = __hsub2(hz[u], czp);
                             const __half2 R = __hadd2(rho, hth[u]);
-                            acc[u] = __hmul2(__hneg2(R), R);
-                            acc[u] = __hfma2(dz, dz, acc[u]);
-                            acc[u] = __hfma2(dy, dy, acc[u]);
-                            acc[u] = __hfma2(dx, dx, acc[u]);
-                            mn = __hmin2(mn, acc[u]);
+                            __half2 acc = __hmul2(__hneg2(R), R);
+                            acc = __hfma2(dz, dz, acc);
+                            acc = __hfma2(dy, dy, acc);
+                            acc = __hfma2(dx, dx, acc);
+                            mn = __hmin2(mn, acc);
                         }
                         const unsigned fl = *reinterpret_cast<const unsigned *>(&mn) & 0x80008000u;
                         const unsigned f = force ? 0x80008000u : __reduce_or_sync(FULL, fl);
                         if (f) {
                             CRB_STAT(1, ((f & 0x8000u) ? 1 : 0) + ((f & 0x80000000u) ? 1 : 0));
-                            // which spheres flagged which cuboid: sign bits of acc[u] -> bit u (cuboid
-                            // kb) and bit 16 + u (cuboid kb + 1), OR-ed over the warp
-                            unsigned fb = 0u;
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                fb |= (*reinterpret_cast<const unsigned *>(&acc[u]) & 0x80008000u) >> (15 - u);
-                            const unsigned um = force ? 0x000F000Fu : __reduce_or_sync(FULL, fb);
 #pragma unroll 1   // one copy of the exact path (instruction cache)
                             for (int j = 0; j < 2; ++j)
-                                if ((f & (0x8000u << (16 * j))) && kb + j < K) exact_box(kb + j, true, (um >> (16 * j)) & 0xFu);
+                                if ((f & (0x8000u << (16 * j))) && kb + j < K) exact_box(kb + j, true);
                         }
                     }
                     }
@@ -1274,12 +1264,12 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                             CRB_STAT(1, ((f & 0x8000u) ? 1 : 0) + ((f & 0x80000000u) ? 1 : 0));
 #pragma unroll 1   // one copy of the exact path (instruction cache)
                             for (int j = 0; j < 2; ++j)
-                                if (f & (0x8000u << (16 * j))) exact_box(kb + j, true, 0xFu);
+                                if (f & (0x8000u << (16 * j))) exact_box(kb + j, true);
                         }
                     }
                     }
 #else
-                    for (int k = 0; k < K; ++k) exact_box(k, false, 0xFu);
+                    for (int k = 0; k < K; ++k) exact_box(k, false);
 #endif
                 }
                 // the group's cost goes to the .w of its first sphere (unused by the backward):

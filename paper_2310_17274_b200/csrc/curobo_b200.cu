@@ -1150,6 +1150,7 @@ __global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ 
     }
 }
 
+#if CRB_PART == 0   // the non-template kernels: only in the main translation unit
 __global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b0 = blockIdx.x * NC;
@@ -1588,6 +1589,8 @@ __global__ void __launch_bounds__(NT, 2) lbfgs_direction_kernel(int n, int count
     two_loop_block(n, Np, count, order, Sb, Yb, rho, syv, yyv, gg, dd, red, ph);
     for (int e = t; e < n; e += NT) d[(size_t)b * n + e] = dd[e];
 }
+
+#endif  // CRB_PART == 0
 
 }  // namespace
 
