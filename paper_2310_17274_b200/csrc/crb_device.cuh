@@ -1186,28 +1186,46 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
                     const uint4 *l1 = WMMA ? kp.boxes_l1 + (size_t)envc * kp.kpairs
                                            : reinterpret_cast<const uint4 *>(smem + kp.lay.boxl1);
-                    for (int kb = 0; kb < K; kb += 2) {
-                        const uint4 w0 = WMMA ? __ldg(l1 + (kb >> 1)) : l1[kb >> 1];
-                        const __half2 *W0 = reinterpret_cast<const __half2 *>(&w0);
-                        const __half2 cxp = W0[0], cyp = W0[1], czp = W0[2], rho = W0[3];
-                        __half2 mn = __float2half2_rn(1.f);
+                    // two pairs (4 cuboids) per step: their sign bits share one warp reduction
+                    // (pair A at bits 15 / 31, pair B at 14 / 30), and the two pairs' arithmetic
+                    // interleaves; a missing pair B reads as "never flagged"
+                    for (int kb = 0; kb < K; kb += 4) {
+                        const bool hasB = kb + 2 < K;
+                        const uint4 wA = WMMA ? __ldg(l1 + (kb >> 1)) : l1[kb >> 1];
+                        const uint4 wB = hasB ? (WMMA ? __ldg(l1 + (kb >> 1) + 1) : l1[(kb >> 1) + 1]) : wA;
+                        const __half2 *WA = reinterpret_cast<const __half2 *>(&wA), *WB = reinterpret_cast<const __half2 *>(&wB);
+                        __half2 mnA = __float2half2_rn(1.f), mnB = mnA;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const __half2 dx = __hsub2(hx[u], cxp), dy = __hsub2(hy[u], cyp), dz = __hsub2(hz[u], czp);
-                            const __half2 R = __hadd2(rho, hth[u]);
-                            __half2 acc = __hmul2(__hneg2(R), R);
-                            acc = __hfma2(dz, dz, acc);
-                            acc = __hfma2(dy, dy, acc);
-                            acc = __hfma2(dx, dx, acc);
-                            mn = __hmin2(mn, acc);
+                            {
+                                const __half2 dx = __hsub2(hx[u], WA[0]), dy = __hsub2(hy[u], WA[1]), dz = __hsub2(hz[u], WA[2]);
+                                const __half2 R = __hadd2(WA[3], hth[u]);
+                                __half2 acc = __hmul2(__hneg2(R), R);
+                                acc = __hfma2(dz, dz, acc);
+                                acc = __hfma2(dy, dy, acc);
+                                acc = __hfma2(dx, dx, acc);
+                                mnA = __hmin2(mnA, acc);
+                            }
+                            {
+                                const __half2 dx = __hsub2(hx[u], WB[0]), dy = __hsub2(hy[u], WB[1]), dz = __hsub2(hz[u], WB[2]);
+                                const __half2 R = __hadd2(WB[3], hth[u]);
+                                __half2 acc = __hmul2(__hneg2(R), R);
+                                acc = __hfma2(dz, dz, acc);
+                                acc = __hfma2(dy, dy, acc);
+                                acc = __hfma2(dx, dx, acc);
+                                mnB = __hmin2(mnB, acc);
+                            }
                         }
-                        const unsigned fl = *reinterpret_cast<const unsigned *>(&mn) & 0x80008000u;
-                        const unsigned f = force ? 0x80008000u : __reduce_or_sync(FULL, fl);
+                        const unsigned flA = *reinterpret_cast<const unsigned *>(&mnA) & 0x80008000u;
+                        const unsigned flB = hasB ? (*reinterpret_cast<const unsigned *>(&mnB) & 0x80008000u) >> 1 : 0u;
+                        const unsigned f = force ? 0xC000C000u : __reduce_or_sync(FULL, flA | flB);
                         if (f) {
-                            CRB_STAT(1, ((f & 0x8000u) ? 1 : 0) + ((f & 0x80000000u) ? 1 : 0));
+                            CRB_STAT(1, __popc(f));
 #pragma unroll 1   // one copy of the exact path (instruction cache)
-                            for (int j = 0; j < 2; ++j)
-                                if ((f & (0x8000u << (16 * j))) && kb + j < K) exact_box(kb + j, true);
+                            for (int j = 0; j < 4; ++j) {
+                                const unsigned bit = (j & 2) ? (0x4000u << (16 * (j & 1))) : (0x8000u << (16 * (j & 1)));
+                                if ((f & bit) && kb + j < K) exact_box(kb + j, true);
+                            }
                         }
                     }
                     }
