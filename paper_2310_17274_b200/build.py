@@ -8,8 +8,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "curobo_b200.cu")            # kernels (CRB_PART 0) + host side, -ftz=true
-SRC_WMMA = os.path.join(HERE, "csrc", "curobo_b200_wmma.cu")  # the <WMMA = true> kernels, no -ftz
+SRC = os.path.join(HERE, "csrc", "curobo_b200.cu")            # kernels (CRB_PART 0) + host side
+SRC_WMMA = os.path.join(HERE, "csrc", "curobo_b200_wmma.cu")  # the <WMMA = true> (large-world) kernels
 DEPS = [SRC, SRC_WMMA, os.path.join(HERE, "csrc", "crb_device.cuh"), os.path.join(ROOT, "include", "curobo_b200.h"),
         os.path.abspath(__file__)]   # the flags live here
 LIB = os.path.join(HERE, "libcurobo_b200.so")
@@ -18,8 +18,11 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-prec-div=false", "-prec-sqrt=false", "-Xcompiler", "-fPIC", f"-I{os.path.join(ROOT, 'include')}",
          "--expt-relaxed-constexpr"]
-# flush-to-zero for the small-world builds only (measured: +2-3 % there, -9 % on the tensor-core build)
-FTZ = {SRC: ["-ftz=true"], SRC_WMMA: []}
+# flush-to-zero in both units (round 2: the large-world build now runs the same fp16x2 bounding-sphere
+# screen as the small-world one and gains 2-3 % from it, profiles/r02_ksweep_ftz.txt; round 1 kept
+# it off there because the tensor-core screen lost 9 %).  One setting for every kernel: the
+# numerics of an environment no longer depend on which build the context picks.
+FTZ = {SRC: ["-ftz=true"], SRC_WMMA: ["-ftz=true"]}
 
 
 def compile_lib(out: str, defs=(), ptxas_verbose: bool = False, ftz: bool = True, ftz_all: bool = False) -> str:

@@ -10,11 +10,12 @@
 //   select_kernel     per-problem packed-key argmin over seeds (O9)
 //   + the test-hook kernels (ls_select, argmin_keys, lbfgs_direction)
 //
-// Two translation units: this file (CRB_PART 0: every kernel except the tensor-core-screen
-// builds, plus the host side) is compiled with -ftz=true; curobo_b200_wmma.cu includes it with
-// CRB_PART 1 and instantiates only the <WMMA = true> kernels, compiled without -ftz
-// (build.py; measured: flush-to-zero speeds the small-world builds by 2-3 % but slows the
-// tensor-core build by 9 %).  crb_wmma_kernel() hands those kernels to the host side.
+// Two translation units, compiled in parallel with the same flags (build.py): this file
+// (CRB_PART 0: the small-world <WMMA = false> kernels, every non-template kernel and the host
+// side) and curobo_b200_wmma.cu, which includes it with CRB_PART 1 and instantiates only the
+// large-world <WMMA = true> kernels (cuboid tables read from global memory; the template
+// parameter keeps its round-1 name: the optional tensor-core screen, CRB_LARGE_L1 = 0).
+// crb_wmma_kernel() hands those kernels to the host side.
 #ifndef CRB_PART
 #define CRB_PART 0
 #endif
