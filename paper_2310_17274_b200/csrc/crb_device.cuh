@@ -1440,6 +1440,21 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     }
     __syncthreads();
     CRB_PHASE(4);
+    // the link sums go to the sphere-gradient area (dead after the barrier: read only by the sums
+    // and the world-group sum), so the registers are free and nothing waits for the sphere reads
+    float *ls = reinterpret_cast<float *>(s.sg);   // [L][6][32]
+    if (grad) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int idx = tid + it * NT;
+            if (idx < rp.L * NC) {
+                const int l = idx / NC, c = idx - l * NC;
+                float *o = ls + l * 6 * NC + c;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) o[k * NC] = acc[it][k];
+            }
+        }
+    }
     if (warp == 0) {
         const int c = lane;
         const float t0 = s.cfg_terms[0 * NC + c], t1 = s.cfg_terms[1 * NC + c], t2 = s.cfg_terms[2 * NC + c],
@@ -1458,41 +1473,30 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     }
 
     // ---- a9 (continued): the self-collision gradient of each slot's winning pair enters the link
-    // sums of the two spheres' links, then the sums are written over the dead sphere positions
+    // sums of the two spheres' links (each (link, slot) entry by the thread that wrote it)
     {
         const int *sphlink = s.iw + rp.o_sphlink;
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            const int idx = tid + it * NT;
-            if (idx < rp.L * NC) {
-                const int l = idx / NC, c = idx - l * NC;
-                const int bij = s.sij[c];
-                if (bij >= 0) {
-                    const int i = bij & 0x1ff, j = (bij >> 9) & 0x1ff;
-                    const float bx = s.sbest[c], by = s.sbest[NC + c], bz = s.sbest[2 * NC + c];
-                    if (sphlink[i] == l) {   // G_i = -beta u
-                        const float4 w = s.sw[i * NC + c];
-                        acc[it][0] -= bx; acc[it][1] -= by; acc[it][2] -= bz;
-                        acc[it][3] -= w.y * bz - w.z * by; acc[it][4] -= w.z * bx - w.x * bz; acc[it][5] -= w.x * by - w.y * bx;
-                    }
-                    if (sphlink[j] == l) {   // G_j = +beta u
-                        const float4 w = s.sw[j * NC + c];
-                        acc[it][0] += bx; acc[it][1] += by; acc[it][2] += bz;
-                        acc[it][3] += w.y * bz - w.z * by; acc[it][4] += w.z * bx - w.x * bz; acc[it][5] += w.x * by - w.y * bx;
-                    }
-                }
+        for (int idx = tid; idx < rp.L * NC; idx += NT) {
+            const int l = idx / NC, c = idx - l * NC;
+            const int bij = s.sij[c];
+            if (bij < 0) continue;
+            const int i = bij & 0x1ff, j = (bij >> 9) & 0x1ff;
+            const bool on_i = sphlink[i] == l, on_j = sphlink[j] == l;
+            if (!on_i && !on_j) continue;
+            const float bx = s.sbest[c], by = s.sbest[NC + c], bz = s.sbest[2 * NC + c];
+            float *o = ls + l * 6 * NC + c;
+            float F0 = o[0], F1 = o[NC], F2 = o[2 * NC], T0 = o[3 * NC], T1 = o[4 * NC], T2 = o[5 * NC];
+            if (on_i) {   // G_i = -beta u
+                const float4 w = s.sw[i * NC + c];
+                F0 -= bx; F1 -= by; F2 -= bz;
+                T0 -= w.y * bz - w.z * by; T1 -= w.z * bx - w.x * bz; T2 -= w.x * by - w.y * bx;
             }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            const int idx = tid + it * NT;
-            if (idx < rp.L * NC) {
-                const int l = idx / NC, c = idx - l * NC;
-                float *o = s.ls + l * 6 * NC + c;
-#pragma unroll
-                for (int k = 0; k < 6; ++k) o[k * NC] = acc[it][k];
+            if (on_j) {   // G_j = +beta u
+                const float4 w = s.sw[j * NC + c];
+                F0 += bx; F1 += by; F2 += bz;
+                T0 += w.y * bz - w.z * by; T1 += w.z * bx - w.x * bz; T2 += w.x * by - w.y * bx;
             }
+            o[0] = F0; o[NC] = F1; o[2 * NC] = F2; o[3 * NC] = T0; o[4 * NC] = T1; o[5 * NC] = T2;
         }
     }
     __syncthreads();
@@ -1508,7 +1512,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         while (mask) {
             const int l2 = __ffs(mask) - 1;
             mask &= mask - 1;
-            const float *S6 = s.ls + l2 * 6 * NC + c;
+            const float *S6 = ls + l2 * 6 * NC + c;
             F0 += S6[0]; F1 += S6[NC]; F2 += S6[2 * NC]; T0 += S6[3 * NC]; T1 += S6[4 * NC]; T2 += S6[5 * NC];
         }
         const float *fr = s.frames + d * 6 * NC + c;
