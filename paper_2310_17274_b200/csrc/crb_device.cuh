@@ -1377,11 +1377,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     __syncthreads();
     CRB_PHASE(3);
 
-    // ---- a10 (per slot) and the first half of a9 side by side: warp 0 merges the self-collision
-    // partials (publishing the winning pair and beta_1 u per slot), warp 1 sums the world groups in
-    // index order, and every warp (0 and 1 after that) sums the world + pose gradients per link into
-    // registers (Alg. 8 / Table 7 as subtree sums: F_l = sum G_m, T_l = sum w_m x G_m);
-    // the self-collision gradient on its two spheres joins those link sums after the barrier
+    // ---- a10 (per slot): warp 0 merges self-collision and applies its gradient (x, y, z only);
+    // warp 1 sums the world groups in index order; then warp 0 forms the slot costs and the total
     if (warp == 0) {
         const int c = lane;
         float bp = 0.f;
@@ -1391,7 +1388,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             const int r = s.srank[w * NC + c];
             if (p > bp || (p == bp && p > 0.f && r < br)) { bp = p; br = r; bij = s.sij[w * NC + c]; }
         }
-        float cself = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
+        float cself = 0.f;
         if (bij >= 0 && bp > 0.f) {
             const int i = bij & 0x1ff, j = (bij >> 9) & 0x1ff;
             const float4 wi = s.sw[i * NC + c], wj = s.sw[j * NC + c];
@@ -1400,13 +1397,11 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             if (nu < 1e-12f) { ux = 1.f; uy = 0.f; uz = 0.f; }
             else { ux /= nu; uy /= nu; uz /= nu; }
             const float b = cf.beta_self;
-            bx = b * ux; by = b * uy; bz = b * uz;   // dC/dw_i = -beta u, dC/dw_j = +beta u
+            float *gi = reinterpret_cast<float *>(s.sg + i * NC + c), *gj = reinterpret_cast<float *>(s.sg + j * NC + c);
+            gi[0] -= b * ux; gi[1] -= b * uy; gi[2] -= b * uz;   // .w (group cost) is read by warp 1
+            gj[0] += b * ux; gj[1] += b * uy; gj[2] += b * uz;
             cself = b * bp;
-        } else {
-            bij = -1;
         }
-        s.sij[c] = bij;                              // row 0, read above by this lane only
-        s.sbest[c] = bx; s.sbest[NC + c] = by; s.sbest[2 * NC + c] = bz;
         s.cfg_terms[3 * NC + c] = c < n_act ? cself : 0.f;
     } else if (warp == 1) {
         const int c = lane;
@@ -1414,8 +1409,30 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         for (int q = 0; q < ((rp.M + 3) >> 2); ++q) cw += s.sg[(q << 2) * NC + c].w;   // fixed order
         s.cfg_terms[4 * NC + c] = c < n_act ? cw : 0.f;
     }
-    float acc[4][6];   // L <= 32 links x 32 slots <= 4 items per thread
-    if (grad) {
+    __syncthreads();
+    CRB_PHASE(4);
+    if (warp == 0) {
+        const int c = lane;
+        const float t0 = s.cfg_terms[0 * NC + c], t1 = s.cfg_terms[1 * NC + c], t2 = s.cfg_terms[2 * NC + c],
+                    t3 = s.cfg_terms[3 * NC + c], t4 = s.cfg_terms[4 * NC + c];
+        // an env index outside [0, n_env) (staged as an empty world) poisons the cost: NaN, so the
+        // row never looks collision-free and its seeds never win (packed key +inf)
+        const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
+        const float cc = (envc >= 0 && envc < kp.n_env) ? (((t0 + t1) + t2) + t3) + t4 : __int_as_float(0x7fc00000);
+        s.cfg_cost[c] = cc;
+        const float tot = warp_sum(cc);
+        if (c == 0) s.scal[0] = tot;
+    }
+    if (!grad) {          // cost-only pass (particle warm-up, f1): no backward
+        __syncthreads();
+        return;
+    }
+
+    // ---- a9: backward to joint space (Alg. 8 / Table 7 as subtree sums):
+    // per link: F_l = sum G_m, T_l = sum w_m x G_m over its spheres (+ the pose pseudo-sphere);
+    // computed into registers, then (after a barrier) written over the dead sphere positions.
+    {
+        float acc[4][6];   // L <= 32 links x 32 slots <= 4 items per thread
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
             const int idx = tid + it * NT;
@@ -1437,66 +1454,16 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             }
             acc[it][0] = F0; acc[it][1] = F1; acc[it][2] = F2; acc[it][3] = T0; acc[it][4] = T1; acc[it][5] = T2;
         }
-    }
-    __syncthreads();
-    CRB_PHASE(4);
-    // the link sums go to the sphere-gradient area (dead after the barrier: read only by the sums
-    // and the world-group sum), so the registers are free and nothing waits for the sphere reads
-    float *ls = reinterpret_cast<float *>(s.sg);   // [L][6][32]
-    if (grad) {
+        __syncthreads();
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
             const int idx = tid + it * NT;
             if (idx < rp.L * NC) {
                 const int l = idx / NC, c = idx - l * NC;
-                float *o = ls + l * 6 * NC + c;
+                float *o = s.ls + l * 6 * NC + c;
 #pragma unroll
                 for (int k = 0; k < 6; ++k) o[k * NC] = acc[it][k];
             }
-        }
-    }
-    if (warp == 0) {
-        const int c = lane;
-        const float t0 = s.cfg_terms[0 * NC + c], t1 = s.cfg_terms[1 * NC + c], t2 = s.cfg_terms[2 * NC + c],
-                    t3 = s.cfg_terms[3 * NC + c], t4 = s.cfg_terms[4 * NC + c];
-        // an env index outside [0, n_env) (staged as an empty world) poisons the cost: NaN, so the
-        // row never looks collision-free and its seeds never win (packed key +inf)
-        const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
-        const float cc = (envc >= 0 && envc < kp.n_env) ? (((t0 + t1) + t2) + t3) + t4 : __int_as_float(0x7fc00000);
-        s.cfg_cost[c] = cc;
-        const float tot = warp_sum(cc);
-        if (c == 0) s.scal[0] = tot;
-    }
-    if (!grad) {          // cost-only pass (particle warm-up, f1): no backward
-        __syncthreads();
-        return;
-    }
-
-    // ---- a9 (continued): the self-collision gradient of each slot's winning pair enters the link
-    // sums of the two spheres' links (each (link, slot) entry by the thread that wrote it)
-    {
-        const int *sphlink = s.iw + rp.o_sphlink;
-        for (int idx = tid; idx < rp.L * NC; idx += NT) {
-            const int l = idx / NC, c = idx - l * NC;
-            const int bij = s.sij[c];
-            if (bij < 0) continue;
-            const int i = bij & 0x1ff, j = (bij >> 9) & 0x1ff;
-            const bool on_i = sphlink[i] == l, on_j = sphlink[j] == l;
-            if (!on_i && !on_j) continue;
-            const float bx = s.sbest[c], by = s.sbest[NC + c], bz = s.sbest[2 * NC + c];
-            float *o = ls + l * 6 * NC + c;
-            float F0 = o[0], F1 = o[NC], F2 = o[2 * NC], T0 = o[3 * NC], T1 = o[4 * NC], T2 = o[5 * NC];
-            if (on_i) {   // G_i = -beta u
-                const float4 w = s.sw[i * NC + c];
-                F0 -= bx; F1 -= by; F2 -= bz;
-                T0 -= w.y * bz - w.z * by; T1 -= w.z * bx - w.x * bz; T2 -= w.x * by - w.y * bx;
-            }
-            if (on_j) {   // G_j = +beta u
-                const float4 w = s.sw[j * NC + c];
-                F0 += bx; F1 += by; F2 += bz;
-                T0 += w.y * bz - w.z * by; T1 += w.z * bx - w.x * bz; T2 += w.x * by - w.y * bx;
-            }
-            o[0] = F0; o[NC] = F1; o[2 * NC] = F2; o[3 * NC] = T0; o[4 * NC] = T1; o[5 * NC] = T2;
         }
     }
     __syncthreads();
@@ -1512,7 +1479,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         while (mask) {
             const int l2 = __ffs(mask) - 1;
             mask &= mask - 1;
-            const float *S6 = ls + l2 * 6 * NC + c;
+            const float *S6 = s.ls + l2 * 6 * NC + c;
             F0 += S6[0]; F1 += S6[NC]; F2 += S6[2 * NC]; T0 += S6[3 * NC]; T1 += S6[4 * NC]; T2 += S6[5 * NC];
         }
         const float *fr = s.frames + d * 6 * NC + c;

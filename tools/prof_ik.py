@@ -1,12 +1,20 @@
-"""One cfg-3 IK solve (for ncu): 300 goals x 30 seeds x 100 iterations, shared K = 20 scene."""
-import os, sys
+"""One cfg-3 IK solve (for ncu): P goals x 30 seeds x 100 iterations, shared K = 20 scene.
+usage: python tools/prof_ik.py [P=1000] [cluster=-1 (auto) | 0 | 1]"""
+import dataclasses, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2310_17274_b200 import native, workload
-wl = workload.franka_ik(0, list(range(300)), S=30, iters=100)
+P = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
+cl = int(sys.argv[2]) if len(sys.argv) > 2 else -1
+wl = workload.franka_ik(0, list(range(P)), S=30, iters=100)
 ctx = native.Context(0)
 ctx.set_robot(wl.robot); ctx.set_world(wl.worlds); ctx.set_cost_params(wl.cost)
-ctx.solve(wl.solver, torch.tensor(wl.seeds, device="cuda"), torch.tensor(wl.goal, device="cuda"),
-          env=torch.tensor(wl.env, device="cuda"))
+sp = dataclasses.replace(wl.solver, cluster=cl)
+args = (torch.tensor(wl.seeds, device="cuda"), torch.tensor(wl.goal, device="cuda"))
+kw = dict(env=torch.tensor(wl.env, device="cuda"))
+ctx.solve(sp, *args, **kw)
 torch.cuda.synchronize()
-print("done")
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); ctx.solve(sp, *args, **kw); e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1)
+print(f"IK P={P} cluster={cl}: {ms:.2f} ms, {P / (ms * 1e-3):.0f} queries/s")
