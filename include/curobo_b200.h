@@ -19,17 +19,21 @@
  *   - An empty batch (B == 0 or P == 0) is validated like any other and returns CRB_OK without a
  *     launch; its batch pointers may then be NULL.
  *   - Numeric types: all results are fp32 arithmetic (the paper's kernels are fp32).  The
- *     sphere-cuboid screen runs a conservative reduced-precision pre-screen (packed fp16 below 60
- *     enabled cuboids per environment, tensor-core fp16 hi/lo products from 60) that only selects
- *     the cuboids given the exact fp32 test: results are bitwise those of the all-fp32 screen.
- *     The small-world kernels flush fp32 subnormals to zero (-ftz); the tensor-core-screen
- *     kernels keep them, so the two builds agree bitwise unless an intermediate falls below 2^-126.
+ *     sphere-cuboid screen runs a conservative packed-fp16 bounding-sphere pre-screen that only
+ *     selects the cuboids given the exact fp32 test: results are bitwise those of the all-fp32
+ *     screen.  Every kernel flushes fp32 subnormals to zero (-ftz).  Environments below 60
+ *     enabled cuboids stage their cuboid tables in shared memory, larger ones read them from
+ *     global memory (same arithmetic).
  *   - Non-finite inputs are not scanned: a NaN propagates into the cost, a NaN cost packs to the
  *     +inf key and never wins a selection (SURVEY §8(b) deviation).
- *   - Capacity limits (CRB_E_LIMIT): D <= 16, L <= 32, M <= 512, pairs <= 16384, H*D <= 512,
- *     history <= 32, n_alpha <= 8, TO mode requires 8 <= H <= 32, IK mode has H == 1, and the
- *     per-CTA shared memory (robot tables + solver state, plus one environment's cuboids below
- *     60 cuboids; from 60 the cuboids are read from global memory) must fit in 227 KB.
+ *   - Capacity limits (CRB_E_LIMIT): D <= 31 (D + 1 kinematic frames after folding the fixed
+ *     links, 32-bit subtree masks), L <= 64 links, M <= 512 spheres and pairs <= 16384 by the
+ *     packed tables, H*D <= 512, history <= 32, n_alpha <= 8, TO mode requires 8 <= H <= 32 (one
+ *     timestep per lane of a warp), IK mode has H == 1, and the per-CTA shared memory (robot
+ *     tables, M x 32 sphere positions and gradients of 16 B each, the solver state, plus one
+ *     environment's cuboids below 60 cuboids) must fit in 227 KB, which in practice bounds M at
+ *     about 150 (the Franka problem: M = 64, 113 KB, two CTAs per SM).  SURVEY §8(b) sketched
+ *     D <= 32 and M <= 1024 (the paper's self-collision kernel limit); DESIGN.md §11.
  */
 #ifndef CUROBO_B200_H
 #define CUROBO_B200_H

@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             }
             for (int d = 0; d < D; ++d) { thp[d * NC + lane] = th[d * NC + lane]; gp[d * NC + lane] = g[d * NC + lane]; }
             // ---- two-loop recursion per seed (Alg. 6)
-            float q[16], al[32];
+            float q[32], al[32];
             for (int d = 0; d < D; ++d) q[d] = g[d * NC + lane];
             for (int i = cnt - 1; i >= 0; --i) {
                 const int sl = order[i * NC + lane];
@@ -961,7 +961,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
             }
             for (int d = 0; d < D; ++d) { thp[d * NC + lane] = th[d * NC + lane]; gp[d * NC + lane] = g[d * NC + lane]; }
             // ---- two-loop recursion per seed (Alg. 6)
-            float q[16], al[32];
+            float q[32], al[32];
             for (int d = 0; d < D; ++d) q[d] = g[d * NC + lane];
             for (int i = cnt - 1; i >= 0; --i) {
                 const int sl = order[i * NC + lane];
@@ -1854,8 +1854,8 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         (r->n_spheres > 0 && (!r->spheres || !r->sphere_link)) || (r->n_pairs > 0 && !r->pairs))
         return fail(ctx, CRB_E_ARG, "null pointer in robot description");
     const int L = r->n_links, D = r->n_dof, M = r->n_spheres, P = r->n_pairs;
-    if (L < 1 || L > 32 || D < 1 || D > 16 || M < 0 || M > 512 || P < 0 || P > 16383)
-        return fail(ctx, CRB_E_LIMIT, "robot size outside limits (L<=32, D<=16, M<=512, pairs<=16384)");
+    if (L < 1 || L > 64 || D < 1 || D > 31 || M < 0 || M > 512 || P < 0 || P > 16383)
+        return fail(ctx, CRB_E_LIMIT, "robot size outside limits (L<=64, D<=31, M<=512, pairs<=16384)");
     if (r->ee_link < 0 || r->ee_link >= L) return fail(ctx, CRB_E_ROBOT, "ee_link out of range");
     std::vector<int> doflink(D, -1);
     for (int l = 0; l < L; ++l) {

@@ -310,3 +310,60 @@ def test_capacity_robot_parity(native, O, big):
                    seed_outputs=True)
     assert torch.isfinite(ik["seed_best_cost"]).all()
     ctx.close()
+
+
+def test_capacity_d31_parity(native, O):
+    """D = 31 (32 kinematic frames after folding, the subtree-mask limit) on 36 links with all
+    Table 6 joint types, 40 spheres: TO evaluation at H = 16 (H*D = 496 <= 512) and IK evaluation
+    against the oracle; D = 32 is refused with CRB_E_LIMIT."""
+    from test_oracle_kinematics import random_chain
+    import dataclasses
+    types = [0] + [4, 5, 6, 1, 2, 3, 4, 0] * 5
+    types = types[:36]
+    rb = random_chain(77, 36, 40, types=types)
+    D = rb.n_dof
+    assert D == 31, D
+    g = np.random.default_rng(78)
+    sph = rb.spheres.copy()
+    sph[:, 3] = g.uniform(0.02, 0.05, 40)
+    pairs = [(i, j) for i in range(40) for j in range(i + 1, 40) if g.random() < 0.3]
+    rb = dataclasses.replace(rb, spheres=sph, pairs=np.array(pairs, np.int32), lo=-np.ones(D) * 1.5,
+                             hi=np.ones(D) * 1.5, vmax=np.ones(D) * 2.0, amax=np.ones(D) * 15.0, jmax=np.ones(D) * 500.0)
+    worlds = [inputs.random_world(63, 0, 24, lo=-1.5, hi=1.5, dmax=0.3)]
+    cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED | inputs.JERK, dt=0.1)
+    ctx = make(native, rb, worlds, cp)
+    R, W = O.Robot(rb), O.World(worlds[0])
+    H, B = 16, 24
+    st = f32(g.uniform(-0.5, 0.5, (B, D)))
+    V = f32(np.clip(st[:, None, :] + np.cumsum(g.normal(0, 0.03, (B, H, D)), axis=1), -1.5, 1.5))
+    gl = f32(np.array([O.fk(R, g.uniform(-0.5, 0.5, D))[2] for _ in range(B)]))
+    cost, grad, _ = ctx.evaluate(T(V), T(gl), start=T(st), env=T(np.zeros(B, np.int32), torch.int32))
+    cost, grad = cost.cpu().numpy(), grad.cpu().numpy()
+    stats = Stats()
+    for b in range(B):
+        c_ref, g_ref, t_ref, margin = ref_traj(O, R, W, cp, st[b], gl[b], V[b])
+        stats.check(float(cost[b]), grad[b].astype(np.float64), c_ref, g_ref, margin, f"d31 TO {b}")
+    stats.done()
+    Q = f32(g.uniform(-1.0, 1.0, (40, D)))
+    glq = f32(np.repeat(gl[:1], 40, 0))
+    cq, gq, _ = ctx.evaluate(T(Q), T(glq), env=T(np.zeros(40, np.int32), torch.int32))
+    cq, gq = cq.cpu().numpy(), gq.cpu().numpy()
+    stats = Stats()
+    for b in range(40):
+        c_ref, g_ref, _, margin, _ = O.eval_ik(R, W, cp, glq[b], Q[b])
+        stats.check(float(cq[b]), gq[b].astype(np.float64), c_ref, g_ref, ("ik", margin), f"d31 IK {b}")
+    stats.done()
+    # short solves run (TO and IK with the particle warm-up: D * 32 = 992 elements per group)
+    out = ctx.solve(inputs.SolverParams(iters=5), T(V.reshape(2, 12, H, D)), T(gl[:2]), start=T(st[:2]), seed_outputs=True)
+    assert torch.isfinite(out["seed_best_cost"]).all()
+    ik = ctx.solve(inputs.SolverParams(iters=5, particle_iters=2, n_particles=8), T(Q.reshape(2, 20, D)), T(gl[:2]),
+                   seed_outputs=True)
+    assert torch.isfinite(ik["seed_best_cost"]).all()
+    ctx.close()
+    big = random_chain(79, 40, 10, types=[0] + [4] * 39)
+    assert big.n_dof == 39
+    c2 = native.Context(0)
+    with pytest.raises(native.CrbError) as e:
+        c2.set_robot(big)
+    assert e.value.code == -6
+    c2.close()
