@@ -1377,136 +1377,6 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     __syncthreads();
     CRB_PHASE(3);
 
-    // Two orderings of the merge and the first half of the backward: IK passes
-    // (fewer live registers) compute the link sums while warp 0 merges the self-collision partials
-    // and store them over the dead sphere gradients; TO passes (at the register limit, where the
-    // longer-lived sums spill the solver state: measured 393-399 vs 408 M evals/s) merge first and
-    // apply the self gradient to the sphere gradients.
-    float *ls = s.ls;
-    if (MODE == MODE_IK) {
-    // ---- a10 (per slot) and the first half of a9 side by side: warp 0 merges the self-collision
-    // partials (publishing the winning pair and beta_1 u per slot), warp 1 sums the world groups in
-    // index order, and every warp (0 and 1 after that) sums the world + pose gradients per link into
-    // registers (Alg. 8 / Table 7 as subtree sums: F_l = sum G_m, T_l = sum w_m x G_m);
-    // the self-collision gradient on its two spheres joins those link sums after the barrier
-    if (warp == 0) {
-        const int c = lane;
-        float bp = 0.f;
-        int br = 0x7fffffff, bij = -1;
-        for (int w = 0; w < NW; ++w) {
-            const float p = s.sbest[w * NC + c];
-            const int r = s.srank[w * NC + c];
-            if (p > bp || (p == bp && p > 0.f && r < br)) { bp = p; br = r; bij = s.sij[w * NC + c]; }
-        }
-        float cself = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
-        if (bij >= 0 && bp > 0.f) {
-            const int i = bij & 0x1ff, j = (bij >> 9) & 0x1ff;
-            const float4 wi = s.sw[i * NC + c], wj = s.sw[j * NC + c];
-            float ux = wi.x - wj.x, uy = wi.y - wj.y, uz = wi.z - wj.z;
-            const float nu = sqrtf(ux * ux + uy * uy + uz * uz);
-            if (nu < 1e-12f) { ux = 1.f; uy = 0.f; uz = 0.f; }
-            else { ux /= nu; uy /= nu; uz /= nu; }
-            const float b = cf.beta_self;
-            bx = b * ux; by = b * uy; bz = b * uz;   // dC/dw_i = -beta u, dC/dw_j = +beta u
-            cself = b * bp;
-        } else {
-            bij = -1;
-        }
-        s.sij[c] = bij;                              // row 0, read above by this lane only
-        s.sbest[c] = bx; s.sbest[NC + c] = by; s.sbest[2 * NC + c] = bz;
-        s.cfg_terms[3 * NC + c] = c < n_act ? cself : 0.f;
-    } else if (warp == 1) {
-        const int c = lane;
-        float cw = 0.f;
-        for (int q = 0; q < ((rp.M + 3) >> 2); ++q) cw += s.sg[(q << 2) * NC + c].w;   // fixed order
-        s.cfg_terms[4 * NC + c] = c < n_act ? cw : 0.f;
-    }
-    float acc[4][6];   // L <= 32 links x 32 slots <= 4 items per thread
-    if (grad) {
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            const int idx = tid + it * NT;
-            float F0 = 0.f, F1 = 0.f, F2 = 0.f, T0 = 0.f, T1 = 0.f, T2 = 0.f;
-            if (idx < rp.L * NC) {
-                const int l = idx / NC, c = idx - l * NC;
-                const int b = s.iw[rp.o_sbeg + l], e = s.iw[rp.o_sbeg + l + 1];
-                for (int m = b; m < e; ++m) {
-                    const float4 g = s.sg[m * NC + c], w = s.sw[m * NC + c];
-                    const float gx = g.x, gy = g.y, gz = g.z;
-                    const float wx = w.x, wy = w.y, wz = w.z;
-                    F0 += gx; F1 += gy; F2 += gz;
-                    T0 += wy * gz - wz * gy; T1 += wz * gx - wx * gz; T2 += wx * gy - wy * gx;
-                }
-                if (l == rp.ee) {
-                    F0 += s.pose_ft[0 * NC + c]; F1 += s.pose_ft[1 * NC + c]; F2 += s.pose_ft[2 * NC + c];
-                    T0 += s.pose_ft[3 * NC + c]; T1 += s.pose_ft[4 * NC + c]; T2 += s.pose_ft[5 * NC + c];
-                }
-            }
-            acc[it][0] = F0; acc[it][1] = F1; acc[it][2] = F2; acc[it][3] = T0; acc[it][4] = T1; acc[it][5] = T2;
-        }
-    }
-    __syncthreads();
-    CRB_PHASE(4);
-    // the link sums go to the sphere-gradient area (dead after the barrier: read only by the sums
-    // and the world-group sum), so the registers are free and nothing waits for the sphere reads
-    ls = reinterpret_cast<float *>(s.sg);   // [L][6][32]
-    if (grad) {
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            const int idx = tid + it * NT;
-            if (idx < rp.L * NC) {
-                const int l = idx / NC, c = idx - l * NC;
-                float *o = ls + l * 6 * NC + c;
-#pragma unroll
-                for (int k = 0; k < 6; ++k) o[k * NC] = acc[it][k];
-            }
-        }
-    }
-    if (warp == 0) {
-        const int c = lane;
-        const float t0 = s.cfg_terms[0 * NC + c], t1 = s.cfg_terms[1 * NC + c], t2 = s.cfg_terms[2 * NC + c],
-                    t3 = s.cfg_terms[3 * NC + c], t4 = s.cfg_terms[4 * NC + c];
-        // an env index outside [0, n_env) (staged as an empty world) poisons the cost: NaN, so the
-        // row never looks collision-free and its seeds never win (packed key +inf)
-        const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
-        const float cc = (envc >= 0 && envc < kp.n_env) ? (((t0 + t1) + t2) + t3) + t4 : __int_as_float(0x7fc00000);
-        s.cfg_cost[c] = cc;
-        const float tot = warp_sum(cc);
-        if (c == 0) s.scal[0] = tot;
-    }
-    if (!grad) {          // cost-only pass (particle warm-up, f1): no backward
-        __syncthreads();
-        return;
-    }
-
-    // ---- a9 (continued): the self-collision gradient of each slot's winning pair enters the link
-    // sums of the two spheres' links (each (link, slot) entry by the thread that wrote it)
-    {
-        const int *sphlink = s.iw + rp.o_sphlink;
-        for (int idx = tid; idx < rp.L * NC; idx += NT) {
-            const int l = idx / NC, c = idx - l * NC;
-            const int bij = s.sij[c];
-            if (bij < 0) continue;
-            const int i = bij & 0x1ff, j = (bij >> 9) & 0x1ff;
-            const bool on_i = sphlink[i] == l, on_j = sphlink[j] == l;
-            if (!on_i && !on_j) continue;
-            const float bx = s.sbest[c], by = s.sbest[NC + c], bz = s.sbest[2 * NC + c];
-            float *o = ls + l * 6 * NC + c;
-            float F0 = o[0], F1 = o[NC], F2 = o[2 * NC], T0 = o[3 * NC], T1 = o[4 * NC], T2 = o[5 * NC];
-            if (on_i) {   // G_i = -beta u
-                const float4 w = s.sw[i * NC + c];
-                F0 -= bx; F1 -= by; F2 -= bz;
-                T0 -= w.y * bz - w.z * by; T1 -= w.z * bx - w.x * bz; T2 -= w.x * by - w.y * bx;
-            }
-            if (on_j) {   // G_j = +beta u
-                const float4 w = s.sw[j * NC + c];
-                F0 += bx; F1 += by; F2 += bz;
-                T0 += w.y * bz - w.z * by; T1 += w.z * bx - w.x * bz; T2 += w.x * by - w.y * bx;
-            }
-            o[0] = F0; o[NC] = F1; o[2 * NC] = F2; o[3 * NC] = T0; o[4 * NC] = T1; o[5 * NC] = T2;
-        }
-    }
-    } else {
     // ---- a10 (per slot): warp 0 merges self-collision and applies its gradient (x, y, z only);
     // warp 1 sums the world groups in index order; then warp 0 forms the slot costs and the total
     if (warp == 0) {
@@ -1596,7 +1466,6 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             }
         }
     }
-    }
     __syncthreads();
     CRB_PHASE(5);
     // joint gradient: the subtree sums of the joint's link (independent loads over the host-built
@@ -1610,7 +1479,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         while (mask) {
             const int l2 = __ffs(mask) - 1;
             mask &= mask - 1;
-            const float *S6 = ls + l2 * 6 * NC + c;
+            const float *S6 = s.ls + l2 * 6 * NC + c;
             F0 += S6[0]; F1 += S6[NC]; F2 += S6[2 * NC]; T0 += S6[3 * NC]; T1 += S6[4 * NC]; T2 += S6[5 * NC];
         }
         const float *fr = s.frames + d * 6 * NC + c;
