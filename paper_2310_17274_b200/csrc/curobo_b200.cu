@@ -1734,7 +1734,7 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.cfg_terms = take(5 * NC);
     L.gV = take(std::max(H * D, D * NC));
     L.red = take(3 * NW);
-    L.st = take(16);
+    L.st = take(std::max(D, 16));   // start state (TO), D <= 31
     L.scal = take(8);
     L.wq = take(2 * ((rp.M + 3) / 4));   // world work-queue order + last-pass cost per group
     L.solver = w;
