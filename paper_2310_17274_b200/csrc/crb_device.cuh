@@ -49,6 +49,12 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 
 // World pre-screen on the tensor cores: 1 = the affine cuboid-frame
 // transform of a world group runs as HMMA.16816 on an fp16 hi/lo split, 0 = the FFMA screen only.
+// Self-collision screen tightened to the pairs that can still reach the lane's current best
+// penetration (1), or the plain d < R test throughout (0)
+#ifndef CRB_SELF_PRUNE
+#define CRB_SELF_PRUNE 1
+#endif
+
 #ifndef CRB_WORLD_MMA
 #define CRB_WORLD_MMA 1
 #endif
@@ -1311,13 +1317,23 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 float4 wi[4];
                 float ri[4], thr[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = u < na ? ia + u : ia;
-                    wi[u] = s.sw[i * NC + lane];
-                    ri[u] = rself[i];
-                    // flag iff w_i.w_j + r_i r_j + hb_j > -slack - hb_i  (u >= na never flags)
-                    thr[u] = u < na ? -1e-5f - wi[u].w : 1e30f;
-                }
+                for (int u = 0; u < 4; ++u) wi[u] = s.sw[(u < na ? ia + u : ia) * NC + lane];
+                // Screen thresholds for the lane's current best penetration p (0: none yet).  Only a
+                // pair with pen = R - d >= p can change the arg-max (A28 ties included), and
+                // R - d >= p <=> d^2 <= (R - p)^2 (R >= p; R < p leaves a conservative flag), i.e.
+                //   w_i.w_j + (r_i - p) r_j + hb_j > -slack - hb_i + p (r_i - p/2),
+                // the same 4 FFMA per pair with ri = r_i - p.  p = 0 is the plain test d^2 < R^2.
+                auto set_thr = [&](float p) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float r = rself[u < na ? ia + u : ia];
+                        ri[u] = CRB_SELF_PRUNE ? r - p : r;
+                        // u >= na never flags
+                        thr[u] = u < na ? (CRB_SELF_PRUNE ? fmaf(p, r - 0.5f * p, -1e-5f - wi[u].w) : -1e-5f - wi[u].w) : 1e30f;
+                    }
+                };
+                float pcur = best;
+                set_thr(pcur);
                 const float4 *wjp = s.sw + jb * NC + lane;
                 const float *rjp = rself + jb;
                 // 4 partners per step: the screen only (4 FFMA + 1 compare per pair); a partner
@@ -1345,7 +1361,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                 if (!(fmaf(wi[u].x, wj.x, fmaf(wi[u].y, wj.y, fmaf(wi[u].z, wj.z, fmaf(ri[u], rj, wj.w)))) >
                                       thr[u]))
                                     continue;
-                                const float R = ri[u] + rj;
+                                const float R = rself[u < na ? ia + u : ia] + rj;
                                 const float dx = wi[u].x - wj.x, dy = wi[u].y - wj.y, dz = wi[u].z - wj.z;
                                 const float d2 = dx * dx + dy * dy + dz * dz;
                                 if (!(d2 < R * R)) continue;
@@ -1358,6 +1374,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                 }
                             }
                         }
+                        if (CRB_SELF_PRUNE && best != pcur) { pcur = best; set_thr(pcur); }
                     }
                 }
             }

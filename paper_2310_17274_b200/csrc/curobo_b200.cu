@@ -645,6 +645,97 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
     }
 }
 
+// One seed's L-BFGS step of the IK solver (Alg. 6 ring push and two-loop recursion, A18-A20) on
+// the lane that owns the seed (warp 0 of the CTA).  The per-dof vectors of the recursion live in
+// registers (DM >= D, loops unrolled and predicated) so its dependent dot-product / update chains
+// run without local memory; alpha_i of the first loop goes to `alv` [m][32] (shared scratch, dead
+// between passes).  Returns g.d; sy = s'y of the pushed pair (trace).
+template <int DM>
+__device__ __forceinline__ float ik_step_lane(int D, int m, int DC, int lane, int it, int &cnt, int &fs, float &sy,
+                                              const float *th, const float *g, float *dd, float *thp, float *gp,
+                                              float *Sb, float *Yb, float *rho, float *syv, float *yyv, int *order,
+                                              float *alv) {
+    sy = 0.f;
+    if (it > 0) {   // ---- ring push (per seed, A20)
+        float yy = 0.f;
+#pragma unroll
+        for (int d = 0; d < DM; ++d)
+            if (d < D) {
+                const int e = d * NC + lane;
+                const float sv = th[e] - thp[e], yv = g[e] - gp[e];
+                Sb[fs * DC + e] = sv; Yb[fs * DC + e] = yv;
+                sy += sv * yv; yy += yv * yv;
+            }
+        if (m > 0 && sy > 1e-12f) {
+            rho[fs * NC + lane] = 1.f / sy; syv[fs * NC + lane] = sy; yyv[fs * NC + lane] = yy;
+            if (cnt < m) { order[cnt * NC + lane] = fs; ++cnt; fs = cnt; }
+            else {
+                const int ev = order[lane];
+                for (int i = 0; i < m - 1; ++i) order[i * NC + lane] = order[(i + 1) * NC + lane];
+                order[(m - 1) * NC + lane] = fs;
+                fs = ev;
+            }
+        }
+    }
+    float q[DM];
+#pragma unroll
+    for (int d = 0; d < DM; ++d) {
+        q[d] = 0.f;
+        if (d < D) {
+            const int e = d * NC + lane;
+            const float gv = g[e];
+            thp[e] = th[e]; gp[e] = gv; q[d] = gv;
+        }
+    }
+    // ---- two-loop recursion per seed (Alg. 6)
+    for (int i = cnt - 1; i >= 0; --i) {
+        const int sl = order[i * NC + lane];
+        const float *S = Sb + sl * DC + lane, *Y = Yb + sl * DC + lane;
+        float ai = 0.f;
+#pragma unroll
+        for (int d = 0; d < DM; ++d)
+            if (d < D) ai += S[d * NC] * q[d];
+        ai *= rho[sl * NC + lane];
+        alv[i * NC + lane] = ai;
+#pragma unroll
+        for (int d = 0; d < DM; ++d)
+            if (d < D) q[d] -= ai * Y[d * NC];
+    }
+    float gamma = 1.f;
+    if (cnt > 0) { const int sl = order[(cnt - 1) * NC + lane]; gamma = syv[sl * NC + lane] / yyv[sl * NC + lane]; }
+#pragma unroll
+    for (int d = 0; d < DM; ++d) q[d] *= gamma;
+    for (int i = 0; i < cnt; ++i) {
+        const int sl = order[i * NC + lane];
+        const float *S = Sb + sl * DC + lane, *Y = Yb + sl * DC + lane;
+        float bi = 0.f;
+#pragma unroll
+        for (int d = 0; d < DM; ++d)
+            if (d < D) bi += Y[d * NC] * q[d];
+        bi *= rho[sl * NC + lane];
+        const float k = alv[i * NC + lane] - bi;
+#pragma unroll
+        for (int d = 0; d < DM; ++d)
+            if (d < D) q[d] += k * S[d * NC];
+    }
+    float g0d = 0.f;
+#pragma unroll
+    for (int d = 0; d < DM; ++d)
+        if (d < D) { dd[d * NC + lane] = -q[d]; g0d += g[d * NC + lane] * (-q[d]); }
+    return g0d;
+}
+
+// the register bucket of the IK step for D (<= 8, <= 16, <= 32), warp-uniform
+__device__ __forceinline__ float ik_step(int D, int m, int DC, int lane, int it, int &cnt, int &fs, float &sy,
+                                         const float *th, const float *g, float *dd, float *thp, float *gp, float *Sb,
+                                         float *Yb, float *rho, float *syv, float *yyv, int *order, float *alv) {
+    if (D <= 8)
+        return ik_step_lane<8>(D, m, DC, lane, it, cnt, fs, sy, th, g, dd, thp, gp, Sb, Yb, rho, syv, yyv, order, alv);
+    if (D <= 16)
+        return ik_step_lane<16>(D, m, DC, lane, it, cnt, fs, sy, th, g, dd, thp, gp, Sb, Yb, rho, syv, yyv, order, alv);
+    return ik_step_lane<32>(D, m, DC, lane, it, cnt, fs, sy, th, g, dd, thp, gp, Sb, Yb, rho, syv, yyv, order, alv);
+}
+
 // ------------------------------------------------------------------------------------------
 template <bool WMMA>
 __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__ KParams kp) {
@@ -716,51 +807,8 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             const int it = (lpass - 1) / A;
             const int tj = active ? trace_slot(kp, it) : -1;
             if (tj >= 0) trace_ik(kp, 0, (size_t)p * kp.S + sd, it, tj, cnt, c, 0.f, 0.f, 0, 0.f);
-            float sy = 0.f;
-            // ---- ring push (per seed, A20)
-            if (it > 0) {
-                float yy = 0.f;
-                for (int d = 0; d < D; ++d) {
-                    const int e = d * NC + lane;
-                    const float sv = th[e] - thp[e], yv = g[e] - gp[e];
-                    Sb[fs * DC + e] = sv; Yb[fs * DC + e] = yv;
-                    sy += sv * yv; yy += yv * yv;
-                }
-                if (m > 0 && sy > 1e-12f) {
-                    rho[fs * NC + lane] = 1.f / sy; syv[fs * NC + lane] = sy; yyv[fs * NC + lane] = yy;
-                    if (cnt < m) { order[cnt * NC + lane] = fs; ++cnt; fs = cnt; }
-                    else {
-                        const int ev = order[lane];
-                        for (int i = 0; i < m - 1; ++i) order[i * NC + lane] = order[(i + 1) * NC + lane];
-                        order[(m - 1) * NC + lane] = fs;
-                        fs = ev;
-                    }
-                }
-            }
-            for (int d = 0; d < D; ++d) { thp[d * NC + lane] = th[d * NC + lane]; gp[d * NC + lane] = g[d * NC + lane]; }
-            // ---- two-loop recursion per seed (Alg. 6)
-            float q[32], al[32];
-            for (int d = 0; d < D; ++d) q[d] = g[d * NC + lane];
-            for (int i = cnt - 1; i >= 0; --i) {
-                const int sl = order[i * NC + lane];
-                float ai = 0.f;
-                for (int d = 0; d < D; ++d) ai += Sb[sl * DC + d * NC + lane] * q[d];
-                ai *= rho[sl * NC + lane];
-                al[i] = ai;
-                for (int d = 0; d < D; ++d) q[d] -= ai * Yb[sl * DC + d * NC + lane];
-            }
-            float gamma = 1.f;
-            if (cnt > 0) { const int sl = order[(cnt - 1) * NC + lane]; gamma = syv[sl * NC + lane] / yyv[sl * NC + lane]; }
-            for (int d = 0; d < D; ++d) q[d] *= gamma;
-            for (int i = 0; i < cnt; ++i) {
-                const int sl = order[i * NC + lane];
-                float bi = 0.f;
-                for (int d = 0; d < D; ++d) bi += Yb[sl * DC + d * NC + lane] * q[d];
-                bi *= rho[sl * NC + lane];
-                for (int d = 0; d < D; ++d) q[d] += (al[i] - bi) * Sb[sl * DC + d * NC + lane];
-            }
-            g0d = 0.f;
-            for (int d = 0; d < D; ++d) { dd[d * NC + lane] = -q[d]; g0d += g[d * NC + lane] * (-q[d]); }
+            float sy;
+            g0d = ik_step(D, m, DC, lane, it, cnt, fs, sy, th, g, dd, thp, gp, Sb, Yb, rho, syv, yyv, order, s.ls);
             if (tj >= 0) trace_ik(kp, 1, (size_t)p * kp.S + sd, it, tj, cnt, c, g0d, sy, 0, 0.f);
         }
         if (a >= 0) {
@@ -939,50 +987,8 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
             }
         if (a >= 0 && warp == 0) {
             const int it = lpass - 1;
-            // ---- ring push (per seed, A20)
-            if (it > 0) {
-                float sy = 0.f, yy = 0.f;
-                for (int d = 0; d < D; ++d) {
-                    const int e = d * NC + lane;
-                    const float sv = th[e] - thp[e], yv = g[e] - gp[e];
-                    Sb[fs * DC + e] = sv; Yb[fs * DC + e] = yv;
-                    sy += sv * yv; yy += yv * yv;
-                }
-                if (m > 0 && sy > 1e-12f) {
-                    rho[fs * NC + lane] = 1.f / sy; syv[fs * NC + lane] = sy; yyv[fs * NC + lane] = yy;
-                    if (cnt < m) { order[cnt * NC + lane] = fs; ++cnt; fs = cnt; }
-                    else {
-                        const int ev = order[lane];
-                        for (int i = 0; i < m - 1; ++i) order[i * NC + lane] = order[(i + 1) * NC + lane];
-                        order[(m - 1) * NC + lane] = fs;
-                        fs = ev;
-                    }
-                }
-            }
-            for (int d = 0; d < D; ++d) { thp[d * NC + lane] = th[d * NC + lane]; gp[d * NC + lane] = g[d * NC + lane]; }
-            // ---- two-loop recursion per seed (Alg. 6)
-            float q[32], al[32];
-            for (int d = 0; d < D; ++d) q[d] = g[d * NC + lane];
-            for (int i = cnt - 1; i >= 0; --i) {
-                const int sl = order[i * NC + lane];
-                float ai = 0.f;
-                for (int d = 0; d < D; ++d) ai += Sb[sl * DC + d * NC + lane] * q[d];
-                ai *= rho[sl * NC + lane];
-                al[i] = ai;
-                for (int d = 0; d < D; ++d) q[d] -= ai * Yb[sl * DC + d * NC + lane];
-            }
-            float gamma = 1.f;
-            if (cnt > 0) { const int sl = order[(cnt - 1) * NC + lane]; gamma = syv[sl * NC + lane] / yyv[sl * NC + lane]; }
-            for (int d = 0; d < D; ++d) q[d] *= gamma;
-            for (int i = 0; i < cnt; ++i) {
-                const int sl = order[i * NC + lane];
-                float bi = 0.f;
-                for (int d = 0; d < D; ++d) bi += Yb[sl * DC + d * NC + lane] * q[d];
-                bi *= rho[sl * NC + lane];
-                for (int d = 0; d < D; ++d) q[d] += (al[i] - bi) * Sb[sl * DC + d * NC + lane];
-            }
-            g0d = 0.f;
-            for (int d = 0; d < D; ++d) { dd[d * NC + lane] = -q[d]; g0d += g[d * NC + lane] * (-q[d]); }
+            float sy;
+            g0d = ik_step(D, m, DC, lane, it, cnt, fs, sy, th, g, dd, thp, gp, Sb, Yb, rho, syv, yyv, order, s.ls);
         }
         if (a >= 0) {
             __syncthreads();               // the L-BFGS step (warp 0) wrote the directions
@@ -1717,7 +1723,7 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.xs = take(D * L.XS);
     L.ltg = take(std::max(rp.L * 12, rp.M * 4) * NC);     // link transforms, then sphere gradients + E
     L.frames = take((D * 6 + 12) * NC);
-    L.swl = take(std::max(std::max(rp.M * 4, rp.L * 6), 2 * D) * NC);   // joint sin/cos (before the chain),
+    L.swl = take(std::max(std::max(rp.M * 4, rp.L * 6), std::max(2 * D, m)) * NC);   // joint sin/cos (before the chain),
     L.scs = L.swl;                                                      // then sphere centres (+hb), then link sums
     L.sbest = take(NW * NC);
     L.srank = take(NW * NC);
