@@ -49,6 +49,17 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 
 // World pre-screen on the tensor cores: 1 = the affine cuboid-frame
 // transform of a world group runs as HMMA.16816 on an fp16 hi/lo split, 0 = the FFMA screen only.
+// World term: cuboids culled per work item by the group's AABB over the pass's slots, then a
+// per-lane world-AABB test ahead of the exact fp32 test (1); or the fp16x2 pre-screens below (0)
+#ifndef CRB_WORLD_CULL
+#define CRB_WORLD_CULL 1
+#endif
+
+// Self-collision blocks culled per pass by their proxy-sphere bound (1) or always screened (0)
+#ifndef CRB_SELF_CULL_DEV
+#define CRB_SELF_CULL_DEV 1
+#endif
+
 // Self-collision screen tightened to the pairs that can still reach the lane's current best
 // penetration (1), or the plain d < R test throughout (0)
 #ifndef CRB_SELF_PRUNE
@@ -88,8 +99,9 @@ struct RobotPack {
     int o_sphlink;  // M ints
     int o_sbeg;     // L+1 ints: spheres of link l are [sbeg[l], sbeg[l+1])
     int o_rself;    // M floats: self-collision radius r + o (Alg. 9)
-    int o_blocks;   // NB x uint2: pair block (ia | (na-1) << 9 | jb << 11 | len << 20, rank base):
-                    //   the pairs {ia..ia+na-1} x {jb..jb+len-1}, all in S (na <= 4)
+    int o_blocks;   // NB x uint4: pair block (ia | (na-1) << 9 | jb << 11 | len << 20, rank base,
+                    //   proxy spheres pa | pb << 16, T^2 as float bits): the pairs {ia..ia+na-1} x
+                    //   {jb..jb+len-1}, all in S (na <= 4); culled when |w_pa - w_pb|^2 >= T^2 in every slot
     int NB;         // number of pair blocks (stored in decreasing cost order: a work queue)
     int o_blocks_ik, NB_ik;   // the same pairs in pieces of <= CRB_SELF_LEN partners (IK passes)
     int o_rank;     // u16 ranks in S of the block pairs, [v][u] from the block's rank base
@@ -132,6 +144,7 @@ struct KParams {
     const float4 *boxes;     // [n_env][kmax][4] float4: (R col i, -col_i . t) x3, (h, M)
     const uint4 *boxes_h2;   // [n_env][kpairs][4] uint4: fp16x2 cuboid pairs (set_world)
     const uint4 *boxes_l1;   // [n_env][kpairs] uint4: fp16x2 bounding-sphere pairs (cx, cy, cz, rho')
+    const float4 *boxes_ab;  // [n_env][kmax][2] float4: world-frame AABB centre, half extents (+ margin)
     int kpairs;
     const int *box_count;    // [n_env] enabled (compacted) boxes
     int kmax, n_env;
@@ -664,6 +677,13 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
 }
 
+// order-preserving float <-> int map (for warp min / max with __reduce_{min,max}_sync); an involution
+__device__ __forceinline__ int f2o(float x) {
+    const int i = __float_as_int(x);
+    return i ^ ((i >> 31) & 0x7fffffff);
+}
+__device__ __forceinline__ float o2f(int i) { return __int_as_float(i ^ ((i >> 31) & 0x7fffffff)); }
+
 // inside the cuboid expanded by e along every axis (Chebyshev bound of the Euclidean test);
 // written as !(|p| >= e) so a NaN coordinate is flagged and left to the exact test
 __device__ __forceinline__ bool in_ebox(float px, float py, float pz, float ex, float ey, float ez) {
@@ -954,7 +974,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         // go to the lowest rank in S (first maximal pair, A28).
         float best = 0.f;
         int brank = 0x7fffffff, bij = -1;
-        const uint2 *blk = reinterpret_cast<const uint2 *>(s.iw + (MODE == MODE_IK ? rp.o_blocks_ik : rp.o_blocks));
+        const uint4 *blk = reinterpret_cast<const uint4 *>(s.iw + (MODE == MODE_IK ? rp.o_blocks_ik : rp.o_blocks));
         const float *rself = s.fw + rp.o_rself;
         const unsigned short *rk = reinterpret_cast<const unsigned short *>(s.iw + rp.o_rank);
         // world (Alg. 10 + Algs. 11-12, Eq. world-collision-cost): each thread carries the 4
@@ -1156,7 +1176,57 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     }
                     } else
 #endif
-#if CRB_WORLD_H2 && CRB_WORLD_L1
+#if CRB_WORLD_CULL
+                    {
+                    // World culling.  An exact flag needs s2 < th2, i.e. the
+                    // sphere's centre within th of the cuboid, hence within th of the cuboid's world
+                    // AABB on every axis: max_a (|w_a - c_a| - e_a) < th (e = the AABB half extents,
+                    // widened by the host for rounding).  (1) Per item: the AABB of the group's
+                    // centres +- th over all lanes (warp min / max) against every cuboid's AABB, one
+                    // cuboid per lane and a ballot: the cuboids no slot of the group can reach drop
+                    // out.  (2) Per kept cuboid: the per-lane AABB test of the 4 spheres, and the exact
+                    // fp32 test (exact_box) when some lane passes it, in increasing k -- so the world
+                    // term is bitwise the all-fp32 screen's.  NaN centres never pass (neither does
+                    // the exact test), and fminf / fmaxf leave them out of the group AABB.
+                    float th[4];
+                    float lx = INFINITY, ly = INFINITY, lz = INFINITY, hx = -INFINITY, hy = -INFINITY, hz = -INFINITY;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const bool on = th2[u] > 0.f;
+                        th[u] = on ? sqrtf(th2[u]) : -INFINITY;
+                        if (on) {
+                            lx = fminf(lx, cx[u] - th[u]); ly = fminf(ly, cy[u] - th[u]); lz = fminf(lz, cz[u] - th[u]);
+                            hx = fmaxf(hx, cx[u] + th[u]); hy = fmaxf(hy, cy[u] + th[u]); hz = fmaxf(hz, cz[u] + th[u]);
+                        }
+                    }
+                    lx = o2f(__reduce_min_sync(FULL, f2o(lx))); ly = o2f(__reduce_min_sync(FULL, f2o(ly)));
+                    lz = o2f(__reduce_min_sync(FULL, f2o(lz))); hx = o2f(__reduce_max_sync(FULL, f2o(hx)));
+                    hy = o2f(__reduce_max_sync(FULL, f2o(hy))); hz = o2f(__reduce_max_sync(FULL, f2o(hz)));
+                    const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
+                    const float4 *ab = kp.boxes_ab + (size_t)envc * kp.kmax * 2;
+                    for (int kb = 0; kb < K; kb += 32) {
+                        bool keep = false;
+                        if (kb + lane < K) {
+                            const float4 c = __ldg(ab + 2 * (kb + lane)), e = __ldg(ab + 2 * (kb + lane) + 1);
+                            keep = !(c.x - e.x > hx) && !(c.x + e.x < lx) && !(c.y - e.y > hy) && !(c.y + e.y < ly) &&
+                                   !(c.z - e.z > hz) && !(c.z + e.z < lz);
+                        }
+                        unsigned mk = __ballot_sync(FULL, keep);
+                        CRB_STAT(1, __popc(mk));
+#pragma unroll 1   // one copy of the exact path (instruction cache)
+                        while (mk) {
+                            const int k = kb + __ffs(mk) - 1;
+                            mk &= mk - 1u;
+                            const float4 c = __ldg(ab + 2 * k), e = __ldg(ab + 2 * k + 1);
+                            bool f = false;
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                f |= fmaxf(fabsf(cx[u] - c.x) - e.x, fmaxf(fabsf(cy[u] - c.y) - e.y, fabsf(cz[u] - c.z) - e.z)) < th[u];
+                            if (__any_sync(FULL, f)) exact_box(k, true);
+                        }
+                    }
+                    }
+#elif CRB_WORLD_H2 && CRB_WORLD_L1
                     {
                     // fp16x2 bounding-sphere pre-screen, cuboids k, k+1 in the two halves, each
                     // thread's 4 spheres broadcast: the cuboid lies inside the sphere (c_k, rho_k),
@@ -1311,7 +1381,18 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 }
                 s.sg[m0 * NC + lane].w = gsum;
             } else {
-                const uint2 B = blk[item - nwg];
+                const uint4 B = blk[item - nwg];
+                // Block culling: the block's first spheres lie on one
+                // rigid frame and its partners on another, so with proxy spheres pa, pb of the two
+                // sides and T = max_i (|c_i - c_pa| + r_i) + max_j (|c_j - c_pb| + r_j) + 2 mm (host),
+                // |w_pa - w_pb| >= T puts every pair at d >= R + 2 mm, where neither the screen nor
+                // the exact test fires.  The block is skipped when that holds in every active slot
+                // (a NaN position keeps it).  pa = 0xffff: never culled.
+                if (CRB_SELF_CULL_DEV && B.z != 0xffffffffu) {
+                    const float4 pa = s.sw[(B.z & 0xffff) * NC + lane], pb = s.sw[(B.z >> 16) * NC + lane];
+                    const float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
+                    if (!__any_sync(FULL, !(dx * dx + dy * dy + dz * dz >= __uint_as_float(B.w)) && lane < n_act)) continue;
+                }
                 const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff,
                           len = (B.x >> 20) & 0x1ff;
                 float4 wi[4];

@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <limits>
 #include <string>
 #include <vector>
@@ -34,6 +35,9 @@
 #include "curobo_b200.h"
 #include "crb_device.cuh"
 
+#ifndef CRB_SELF_CULL
+#define CRB_SELF_CULL 1   // frame-pair culling of the self-collision blocks (0: every block screened)
+#endif
 #ifndef CRB_SELF_LEN
 #define CRB_SELF_LEN 16   // partners per self-collision work item (<= 511)
 #endif
@@ -1251,10 +1255,10 @@ __global__ void __launch_bounds__(NT, 2) mask_kernel(const __grid_constant__ KPa
             if (v < lim[d] || v > lim[D + d]) bad |= 1;
         }
     {                                                 // self pairs (every pair of S with r + o > 0)
-        const uint2 *blk = reinterpret_cast<const uint2 *>(s.iw + rp.o_blocks);
+        const uint4 *blk = reinterpret_cast<const uint4 *>(s.iw + rp.o_blocks);
         const float *rself = s.fw + rp.o_rself;
         for (int bi = warp; bi < rp.NB; bi += NW) {
-            const uint2 B = blk[bi];
+            const uint4 B = blk[bi];
             const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff, len = (B.x >> 20) & 0x1ff;
             for (int u = 0; u < na; ++u) {
                 const float4 wi = s.sw[(ia + u) * NC + lane];
@@ -1651,6 +1655,7 @@ struct crb_ctx {
     float4 *d_boxes = nullptr;
     uint4 *d_boxes_h2 = nullptr;          // fp16x2 cuboid pairs (Chebyshev pre-screen, CRB_WORLD_L1 = 0)
     uint4 *d_boxes_l1 = nullptr;          // fp16x2 bounding-sphere pairs of the small-world pre-screen
+    float4 *d_boxes_ab = nullptr;         // world-frame AABB (centre, half extents) per cuboid (culling)
     int kpairs = 1;                       // pairs per environment in d_boxes_h2
     int *d_box_count = nullptr;
     int n_env = 0, kmax = 0, kmax_enabled = 0;
@@ -1763,6 +1768,7 @@ KParams base_params(const crb_ctx *ctx) {
     kp.boxes = ctx->d_boxes;
     kp.boxes_h2 = ctx->d_boxes_h2;
     kp.boxes_l1 = ctx->d_boxes_l1;
+    kp.boxes_ab = ctx->d_boxes_ab;
     kp.kpairs = ctx->kpairs;
     kp.box_count = ctx->d_box_count;
     kp.kmax = ctx->kmax;
@@ -1842,6 +1848,7 @@ crb_status crb_destroy(crb_ctx *ctx) {
     cudaSetDevice(ctx->device);
     cudaFree(ctx->d_robot); cudaFree(ctx->d_boxes); cudaFree(ctx->d_boxes_h2); cudaFree(ctx->d_box_count);
     cudaFree(ctx->d_boxes_l1);
+    cudaFree(ctx->d_boxes_ab);
     cudaFree(ctx->ws_cost); cudaFree(ctx->ws_traj); cudaFree(ctx->ws_mask); cudaFree(ctx->ws_n);
     cudaFree(ctx->h_seeds); cudaFree(ctx->h_start); cudaFree(ctx->h_goal); cudaFree(ctx->h_best);
     cudaFree(ctx->h_bcost); cudaFree(ctx->h_env); cudaFree(ctx->h_key);
@@ -1984,16 +1991,49 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         if (rank_of[(size_t)a * M + b] < 0) ++npairs;
         rank_of[(size_t)a * M + b] = rank_of[(size_t)a * M + b] < 0 ? p : std::min(rank_of[(size_t)a * M + b], p);
     }
+    // packed sphere k -> its frame (spheres are sorted by frame)
+    std::vector<int> pf(M);
+    for (int k = 0; k < M; ++k) pf[k] = sframe[ord[k]];
     auto runs_of = [&](int a) {
+        // partner runs of first sphere a; with CRB_SELF_CULL a run is also cut where the partner
+        // frame changes, so every block below lies within one frame pair
         std::vector<std::pair<int, int>> rr;
         for (int b = a + 1; b < M;) {
             if (rank_of[(size_t)a * M + b] < 0) { ++b; continue; }
             int e = b;
-            while (e < M && rank_of[(size_t)a * M + e] >= 0) ++e;
+            while (e < M && rank_of[(size_t)a * M + e] >= 0 && (!CRB_SELF_CULL || pf[e] == pf[b])) ++e;
             rr.push_back({b, e});
             b = e;
         }
         return rr;
+    };
+    // Block culling (crb_device.cuh): per block a proxy sphere on each
+    // side (the one minimising the side's bound) and T^2, T = max_i (|c_i - c_pa| + r_i) +
+    // max_j (|c_j - c_pb| + r_j) + 2 mm in frame coordinates (both sides rigid: one frame each).
+    auto proxy = [&](int b0, int n, int &pbest) {
+        double best = 1e300;
+        for (int c = b0; c < b0 + n; ++c) {
+            double mx = 0.0;
+            for (int k = b0; k < b0 + n; ++k) {
+                double d2 = 0.0;
+                for (int i = 0; i < 3; ++i) d2 += (scen[ord[k]][i] - scen[ord[c]][i]) * (scen[ord[k]][i] - scen[ord[c]][i]);
+                mx = std::max(mx, std::sqrt(d2) + (double)rself[k]);
+            }
+            if (mx < best) { best = mx; pbest = c; }
+        }
+        return best;
+    };
+    auto cull_of = [&](int ia, int na, int jb, int len, uint32_t &z, uint32_t &wv) {
+        z = 0xffffffffu; wv = 0u;
+        bool one = true;
+        for (int k = ia; k < ia + na; ++k) one = one && pf[k] == pf[ia];
+        for (int k = jb; k < jb + len; ++k) one = one && pf[k] == pf[jb];
+        if (!CRB_SELF_CULL || !one) return;
+        int pa = ia, pb = jb;
+        const double T = proxy(ia, na, pa) + proxy(jb, len, pb) + 2e-3;
+        const float T2 = (float)(T * T * (1.0 + 1e-6));
+        z = (uint32_t)pa | ((uint32_t)pb << 16);
+        memcpy(&wv, &T2, 4);
     };
     // Two work-item tables over the same pairs: TO passes take whole runs (<= 511 partners: fewer,
     // longer items), IK passes runs cut into pieces of at most CRB_SELF_LEN partners (the random IK
@@ -2006,7 +2046,7 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
     for (int a = 0; a < M;) {
         const auto ra = runs_of(a);
         int na = 1;
-        while (na < 4 && a + na < M && runs_of(a + na) == ra) ++na;
+        while (na < 4 && a + na < M && (!CRB_SELF_CULL || pf[a + na] == pf[a]) && runs_of(a + na) == ra) ++na;
         for (const auto &rn : ra) {
             const int base = (int)ranks.size(), len = rn.second - rn.first;
             for (int v = 0; v < len; ++v)
@@ -2026,6 +2066,10 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         for (const Blk &b : blks) {
             bk.push_back((uint32_t)b.ia | ((uint32_t)(b.na - 1) << 9) | ((uint32_t)b.jb << 11) | ((uint32_t)b.len << 20));
             bk.push_back((uint32_t)b.rbase);
+            uint32_t z, wv;
+            cull_of(b.ia, b.na, b.jb, b.len, z, wv);
+            bk.push_back(z);
+            bk.push_back(wv);
         }
     };
     std::vector<uint32_t> bk, bk_ik;
@@ -2060,6 +2104,7 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         blob[rp.o_sphlink + k] = (uint32_t)sframe[m];
         blob[rp.o_perm + k] = (uint32_t)m;
     }
+
     for (int f = 0, k = 0; f <= NF; ++f) {
         while (k < M && sframe[ord[k]] < f) ++k;
         blob[rp.o_sbeg + f] = (uint32_t)k;
@@ -2102,6 +2147,10 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
     if (n_env < 1 || k_max < 0 || !boxes_per_env || (k_max > 0 && !boxes)) return fail(ctx, CRB_E_ARG, "bad world arguments");
     std::vector<float> packed((size_t)n_env * std::max(k_max, 1) * 16, 0.f);
     std::vector<double> sph_c((size_t)n_env * std::max(k_max, 1) * 4, 0.0);   // bounding sphere (centre, radius)
+    // world-frame AABB of each enabled cuboid (crb_device.cuh "World culling"): centre and half
+    // extents e_i = sum_j |R_ij| h_j, widened by 1e-4 m + 1e-6 (|c| + e) (fp32 rounding of the
+    // device-side test, far below the margin)
+    std::vector<float4> aabb((size_t)n_env * std::max(k_max, 1) * 2, make_float4(0.f, 0.f, 0.f, 0.f));
     std::vector<int> count(n_env, 0);
     int kmax_en = 0;
     for (int e = 0; e < n_env; ++e) {
@@ -2130,6 +2179,18 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
             o[12] = 0.5f * b.dims[0]; o[13] = 0.5f * b.dims[1]; o[14] = 0.5f * b.dims[2];
             double *bs = &sph_c[((size_t)e * k_max + k) * 4];
             bs[0] = b.pos[0]; bs[1] = b.pos[1]; bs[2] = b.pos[2];
+            {
+                double ext[3], cm = 0.0;
+                for (int i2 = 0; i2 < 3; ++i2) {
+                    ext[i2] = 0.0;
+                    for (int j2 = 0; j2 < 3; ++j2) ext[i2] += std::fabs(R[i2][j2]) * 0.5 * (double)b.dims[j2];
+                    cm = std::max(cm, std::fabs((double)b.pos[i2]) + ext[i2]);
+                }
+                const double mg = 1e-4 + 1e-6 * cm;
+                aabb[((size_t)e * k_max + k) * 2] = make_float4(b.pos[0], b.pos[1], b.pos[2], 0.f);
+                aabb[((size_t)e * k_max + k) * 2 + 1] =
+                    make_float4((float)(ext[0] + mg), (float)(ext[1] + mg), (float)(ext[2] + mg), 0.f);
+            }
             bs[3] = 0.5 * std::sqrt((double)b.dims[0] * b.dims[0] + (double)b.dims[1] * b.dims[1] +
                                     (double)b.dims[2] * b.dims[2]);
             // cuboid magnitude M = max(|off_i|, h_i) for the rounding slack of the reduced-precision
@@ -2202,8 +2263,15 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
             for (int i = 0; i < 4; ++i) pl1[((size_t)e * kpairs + p2) * 4 + i] = __halves2half2(c[0][i], c[1][i]);
         }
     cudaFree(ctx->d_boxes); cudaFree(ctx->d_boxes_h2); cudaFree(ctx->d_box_count); cudaFree(ctx->d_boxes_l1);
+    cudaFree(ctx->d_boxes_ab);
     ctx->d_boxes = nullptr; ctx->d_boxes_h2 = nullptr; ctx->d_box_count = nullptr; ctx->d_boxes_l1 = nullptr;
+    ctx->d_boxes_ab = nullptr;
     ctx->world_ok = false;
+    st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes_ab, aabb.size() * sizeof(float4)), "cudaMalloc boxes aabb");
+    if (st != CRB_OK) return st;
+    st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes_ab, aabb.data(), aabb.size() * sizeof(float4), cudaMemcpyHostToDevice),
+                    "upload boxes aabb");
+    if (st != CRB_OK) return st;
     st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes_l1, pl1.size() * sizeof(__half2)), "cudaMalloc boxes l1");
     if (st != CRB_OK) return st;
     st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes_l1, pl1.data(), pl1.size() * sizeof(__half2), cudaMemcpyHostToDevice),
