@@ -109,6 +109,7 @@ struct RobotPack {
     int o_doflink;  // D ints: link carrying dof d
     int o_desc;     // L ints: bit l' set iff link l' is in the subtree of link l (l itself included)
     int o_perm;     // M ints: packed sphere index -> caller's sphere index
+    int o_doff;     // D ints: frame driven by dof d | prismatic << 16 (joint_csq)
     int words;      // total (multiple of 4)
 };
 
@@ -475,15 +476,24 @@ __device__ __forceinline__ Smem make_smem(const KParams &kp, float *smem) {
     return s;
 }
 
-// sin / cos of every joint value of the 32 slots, computed by all threads before the serial FK
-// chain (scs[0..D) = sin, scs[D..2D) = cos).
-__device__ __forceinline__ void prep_sincos(const Smem &s, int D) {
-    for (int idx = threadIdx.x; idx < D * NC; idx += NT) {
-        float sn, cs;
-        sincosf(s.q_cfg[idx], &sn, &cs);
-        s.scs[idx] = sn;
-        s.scs[D * NC + idx] = cs;
-    }
+// The joint term of the frame driven by dof d = idx / 32 at slot idx % 32, for the serial chain: the
+// host normalises every joint to the z axis of its frame (crb_set_robot), so the chain applies
+// (u0, u1) <- (c u0 + s u1, c u1 - s u0), u3 <- u3 + t u2 with (c, s, t) = (cos q, sin q, 0) for a
+// revolute and (1, 0, q) for a prismatic joint: no branch on the joint type, and the chain reads
+// scs[frame][3][32] at an address that does not depend on its frame record.
+__device__ __forceinline__ void joint_csq(const Smem &s, const RobotPack &rp, int idx, float v) {
+    const int d = idx / NC, c = idx - d * NC;
+    const int fi = s.iw[rp.o_doff + d];   // frame | prismatic << 16
+    float sn = 0.f, cs = 1.f, t = 0.f;
+    if (fi >> 16) t = v;
+    else sincosf(v, &sn, &cs);
+    float *o = s.scs + (fi & 0xffff) * 3 * NC + c;
+    o[0] = cs; o[NC] = sn; o[2 * NC] = t;
+}
+
+// the joint terms of every dof of the 32 slots from q_cfg, by all threads before the serial chain
+__device__ __forceinline__ void prep_sincos(const Smem &s, const RobotPack &rp) {
+    for (int idx = threadIdx.x; idx < rp.D * NC; idx += NT) joint_csq(s, rp, idx, s.q_cfg[idx]);
 }
 
 // frames[d][6][32]: world axis k and origin o of the joint carrying dof d; then EE R (9) + p (3).
@@ -496,61 +506,48 @@ __device__ __forceinline__ float *ee_frame(const Smem &s, int D) { return s.fram
 __device__ __forceinline__ void fk_chain(const RobotPack &rp, const Smem &s) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r = warp - FK_W0;   // chain row
-    float *fee = ee_frame(s, rp.D);
     const float4 *L4 = reinterpret_cast<const float4 *>(s.fw + rp.o_links);   // 16 words per frame
-    float4 cur = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int l = 0; l < rp.L; ++l) {
+    // frame 0 (the root, no joint): row r of its fixed transform
+    float4 cur = L4[r];
+    {
+        float *dst = s.lt + (r * 4) * NC + lane;
+        dst[0] = cur.x; dst[NC] = cur.y; dst[2 * NC] = cur.z; dst[3 * NC] = cur.w;
+    }
+    for (int l = 1; l < rp.L; ++l) {
         const float4 f0 = L4[4 * l], f1 = L4[4 * l + 1], f2 = L4[4 * l + 2];   // rows of F (3x4)
         const int4 md = reinterpret_cast<const int4 *>(L4)[4 * l + 3];         // parent, type, dof
-        const int parent = md.x, type = md.y, dof = md.z;
-        float4 pr;
-        if (parent < 0) pr = make_float4(r == 0, r == 1, r == 2, 0.f);
-        else if (parent == l - 1) pr = cur;
-        else {
+        const float *jc = s.scs + l * 3 * NC + lane;                              // (c, s, t) of frame l
+        const float jcs = jc[0], jsn = jc[NC], jt = jc[2 * NC];
+        const int parent = md.x, dof = md.z;
+        float4 pr = cur;
+        if (parent != l - 1) {
             const float *src = s.lt + (parent * 12 + r * 4) * NC + lane;
             pr = make_float4(src[0], src[NC], src[2 * NC], src[3 * NC]);
         }
-        // row r of T_l = row r of T_parent . F . J(v) (Table 6, A25 fixed): first u = pr . F (the
-        // parent row times F's columns, translation column + pr.w), then the joint acts on u --
-        // a rotation of two of its rotation entries, or a shift of the translation along an axis
-        float u0 = fmaf(pr.z, f2.x, fmaf(pr.y, f1.x, pr.x * f0.x));
-        float u1 = fmaf(pr.z, f2.y, fmaf(pr.y, f1.y, pr.x * f0.y));
-        float u2 = fmaf(pr.z, f2.z, fmaf(pr.y, f1.z, pr.x * f0.z));
-        float u3 = fmaf(pr.z, f2.w, fmaf(pr.y, f1.w, fmaf(pr.x, f0.w, pr.w)));
-        if (type >= 4) {
-            const float sn = s.scs[dof * NC + lane], cs = s.scs[(rp.D + dof) * NC + lane];
-            if (type == 4) {        // revolute x: (u1, u2) <- (c u1 + s u2, -s u1 + c u2)
-                const float a = u1;
-                u1 = fmaf(sn, u2, cs * a); u2 = fmaf(-sn, a, cs * u2);
-            } else if (type == 5) { // revolute y: (u0, u2) <- (c u0 - s u2, s u0 + c u2)
-                const float a = u0;
-                u0 = fmaf(-sn, u2, cs * a); u2 = fmaf(sn, a, cs * u2);
-            } else {                // revolute z: (u0, u1) <- (c u0 + s u1, -s u0 + c u1)
-                const float a = u0;
-                u0 = fmaf(sn, u1, cs * a); u1 = fmaf(-sn, a, cs * u1);
-            }
-        } else if (type >= 1) {     // prismatic: translation += v * (pr . F column axis)
-            const float v = s.q_cfg[dof * NC + lane];
-            u3 = fmaf(v, type == 1 ? u0 : (type == 2 ? u1 : u2), u3);
-        }
-        const float4 nr = make_float4(u0, u1, u2, u3);
+        // row r of T_l = row r of T_parent . F . J(v) (Table 6, A25 fixed; z-axis joints after the
+        // host's normalisation): u = pr . F (translation column + pr.w), then the joint acts on u
+        const float u0 = fmaf(pr.z, f2.x, fmaf(pr.y, f1.x, pr.x * f0.x));
+        const float u1 = fmaf(pr.z, f2.y, fmaf(pr.y, f1.y, pr.x * f0.y));
+        const float u2 = fmaf(pr.z, f2.z, fmaf(pr.y, f1.z, pr.x * f0.z));
+        const float u3 = fmaf(pr.z, f2.w, fmaf(pr.y, f1.w, fmaf(pr.x, f0.w, pr.w)));
+        const float4 nr = make_float4(fmaf(jsn, u1, jcs * u0), fmaf(-jsn, u0, jcs * u1), u2, fmaf(jt, u2, u3));
         float *dst = s.lt + (l * 12 + r * 4) * NC + lane;
         dst[0] = nr.x; dst[NC] = nr.y; dst[2 * NC] = nr.z; dst[3 * NC] = nr.w;
-        if (type != 0) {   // joint axis = column `ax` of R_l, origin = t_l (Table 7)
-            const int ax = type >= 4 ? type - 4 : type - 1;
-            float *fr = s.frames + dof * 6 * NC + lane;
-            fr[r * NC] = ax == 0 ? nr.x : (ax == 1 ? nr.y : nr.z);
-            fr[(3 + r) * NC] = nr.w;
-        }
-        if (l == rp.ee) {   // EE = T_frame * C_ee (the folded fixed offset)
-            const float *E = s.fw + rp.o_eeoff;
-            fee[(3 * r + 0) * NC + lane] = nr.x * E[0] + nr.y * E[4] + nr.z * E[8];
-            fee[(3 * r + 1) * NC + lane] = nr.x * E[1] + nr.y * E[5] + nr.z * E[9];
-            fee[(3 * r + 2) * NC + lane] = nr.x * E[2] + nr.y * E[6] + nr.z * E[10];
-            fee[(9 + r) * NC + lane] = nr.x * E[3] + nr.y * E[7] + nr.z * E[11] + nr.w;
-        }
+        // joint axis = column z of R_l, origin = t_l (Table 7)
+        float *fr = s.frames + dof * 6 * NC + lane;
+        fr[r * NC] = nr.z;
+        fr[(3 + r) * NC] = nr.w;
         cur = nr;
     }
+    // EE = T_frame * C_ee (the folded fixed offset), from the frame's stored row
+    const float *E = s.fw + rp.o_eeoff;
+    const float *t = s.lt + (rp.ee * 12 + r * 4) * NC + lane;
+    const float t0 = t[0], t1 = t[NC], t2 = t[2 * NC], t3 = t[3 * NC];
+    float *fee = ee_frame(s, rp.D);
+    fee[(3 * r + 0) * NC + lane] = t0 * E[0] + t1 * E[4] + t2 * E[8];
+    fee[(3 * r + 1) * NC + lane] = t0 * E[1] + t1 * E[5] + t2 * E[9];
+    fee[(3 * r + 2) * NC + lane] = t0 * E[2] + t1 * E[6] + t2 * E[10];
+    fee[(9 + r) * NC + lane] = t0 * E[3] + t1 * E[7] + t2 * E[11] + t3;
 }
 
 // Sphere placement (all warps), after the chain: sw[m][lane] = (R_link c_m + t_link, hb).
@@ -832,10 +829,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             else if (h >= H - 3) v = thA[(H - 1) * D + d];
             else v = thA[(h - 1) * D + d];
             s.q_cfg[idx] = v;
-            float sn, cs;
-            sincosf(v, &sn, &cs);
-            s.scs[idx] = sn;
-            s.scs[D * NC + idx] = cs;
+            joint_csq(s, rp, idx, v);
         }
         __syncthreads();
     } else {

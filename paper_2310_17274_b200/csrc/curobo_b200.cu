@@ -770,7 +770,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             s.q_cfg[d * NC + lane] = v;
         }
     __syncthreads();
-    prep_sincos(s, D);
+    prep_sincos(s, kp.rp);
     // single eval_pass call site: the particle warm-up (f1, cost only: thread t < D*32 owns
     // element t with mu in th, Theta_sigma in g, the UPDATE sums in dd / thp), then pass 0 =
     // Theta_0 and (L-BFGS step, A candidates) per iteration
@@ -802,10 +802,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
                 const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
                 const float v = fminf(fmaxf(fmaf(sqrtf(g[idx]), z, th[idx]), lim[d]), lim[D + d]);
                 s.q_cfg[idx] = v;
-                float sn, cs;
-                sincosf(v, &sn, &cs);
-                s.scs[idx] = sn;
-                s.scs[DC + idx] = cs;
+                joint_csq(s, kp.rp, idx, v);
             }
         if (a == 0 && warp == 0) {
             const int it = (lpass - 1) / A;
@@ -821,10 +818,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
                 const int d = idx / NC;
                 const float v = candidate(th[idx], kp.alpha[a], dd[idx], lim[d], lim[D + d]);
                 s.q_cfg[idx] = v;
-                float sn, cs;
-                sincosf(v, &sn, &cs);
-                s.scs[idx] = sn;
-                s.scs[DC + idx] = cs;
+                joint_csq(s, kp.rp, idx, v);
             }
         }
         eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
@@ -863,10 +857,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
                     if (pass == npart - 1) {   // Theta_0 of L-BFGS = mu
                         const float v = th[idx];
                         s.q_cfg[idx] = v;
-                        float sn, cs;
-                        sincosf(v, &sn, &cs);
-                        s.scs[idx] = sn;
-                        s.scs[DC + idx] = cs;
+                        joint_csq(s, kp.rp, idx, v);
                     }
                 }
                 pacc.reset();
@@ -950,7 +941,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
             s.q_cfg[d * NC + lane] = v;
         }
     __syncthreads();
-    prep_sincos(s, D);
+    prep_sincos(s, kp.rp);
     // single eval_pass call site: the particle warm-up (f1, cost only: thread t < D*32 owns
     // element t with mu in th, Theta_sigma in g, the UPDATE sums in dd / thp), then pass 0 =
     // Theta_0 and (L-BFGS step, A candidates) per iteration
@@ -984,10 +975,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
                 const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
                 const float v = fminf(fmaxf(fmaf(sqrtf(g[idx]), z, th[idx]), lim[d]), lim[D + d]);
                 s.q_cfg[idx] = v;
-                float sn, cs;
-                sincosf(v, &sn, &cs);
-                s.scs[idx] = sn;
-                s.scs[DC + idx] = cs;
+                joint_csq(s, kp.rp, idx, v);
             }
         if (a >= 0 && warp == 0) {
             const int it = lpass - 1;
@@ -1000,10 +988,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
                 const int d = idx / NC;
                 const float v = candidate(th[idx], kp.alpha[a], dd[idx], lim[d], lim[D + d]);
                 s.q_cfg[idx] = v;
-                float sn, cs;
-                sincosf(v, &sn, &cs);
-                s.scs[idx] = sn;
-                s.scs[DC + idx] = cs;
+                joint_csq(s, kp.rp, idx, v);
             }
         }
         eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
@@ -1045,10 +1030,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
                     if (pass == npart - 1) {   // Theta_0 of L-BFGS = mu
                         const float v = th[idx];
                         s.q_cfg[idx] = v;
-                        float sn, cs;
-                        sincosf(v, &sn, &cs);
-                        s.scs[idx] = sn;
-                        s.scs[DC + idx] = cs;
+                        joint_csq(s, kp.rp, idx, v);
                     }
                 }
                 pacc.reset();
@@ -1148,7 +1130,7 @@ __global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ 
             s.goal[k * NC + lane] = act ? kp.goal[(size_t)(b0 + lane) * gw + k] : (k == 3 && gw == 7 ? 1.f : 0.f);
     }
     __syncthreads();
-    prep_sincos(s, D);
+    prep_sincos(s, kp.rp);
     eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr);
     if (warp == 0 && lane < n_act) {
         const int b = b0 + lane;
@@ -1173,7 +1155,7 @@ __global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KPara
     if (warp == 0)
         for (int d = 0; d < D; ++d) s.q_cfg[d * NC + lane] = lane < n_act ? kp.q_in[(size_t)(b0 + lane) * kp.q_stride + d] : 0.f;
     __syncthreads();
-    prep_sincos(s, D);
+    prep_sincos(s, kp.rp);
     __syncthreads();
     fk_phase(kp.rp, s);
     const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
@@ -1245,7 +1227,7 @@ __global__ void __launch_bounds__(NT, 2) mask_kernel(const __grid_constant__ KPa
         if (!edges && kp.env && lane < n_act && kp.env[(b0 + lane) / kp.env_div] != env) flag[lane] = 8;   // env group rule
     }
     __syncthreads();
-    prep_sincos(s, D);
+    prep_sincos(s, kp.rp);
     __syncthreads();
     fk_phase(rp, s);
     int bad = (env < 0 || env >= kp.n_env) ? 16 : 0;  // env index outside [0, n_env): invalid
@@ -1956,6 +1938,49 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
     }
     M34 eeoff;
     const int fee = frame_and_offset(r->ee_link, eeoff);
+    // Joint-axis normalisation: frame f is re-expressed as T'_f = T_f P_f, P_f the cyclic axis
+    // permutation taking z to the joint's axis (R_a(q) = P R_z(q) P^T, Trans(q e_a) = P Trans(q e_z)
+    // P^T), so every device joint is a z-axis joint: F'_f = P_parent^T F_f P_f, spheres and the EE
+    // offset of frame f pre-multiplied by P_f^T.  World poses are unchanged; the joint axis of the
+    // backward is column z of R'_f (= column a of R_f).  Entries are permuted, not rounded.
+    {
+        auto P_of = [&](int f) {   // columns (P e_x, P e_y, P e_z) as a row-major 3x3
+            std::array<double, 9> P{1, 0, 0, 0, 1, 0, 0, 0, 1};
+            if (f == 0) return P;
+            const int a = (ftype[f] - 1) % 3;
+            if (a == 0) P = {0, 0, 1, 1, 0, 0, 0, 1, 0};        // z -> x (e_x -> e_y, e_y -> e_z)
+            else if (a == 1) P = {0, 1, 0, 0, 0, 1, 1, 0, 0};   // z -> y (e_x -> e_z, e_y -> e_x)
+            return P;
+        };
+        auto xform = [&](const std::array<double, 9> &Pl, const M34 &A, const std::array<double, 9> &Pr) {
+            M34 B;   // [Pl^T R Pr | Pl^T t]
+            for (int i = 0; i < 3; ++i) {
+                for (int j = 0; j < 3; ++j) {
+                    double v = 0.0;
+                    for (int k = 0; k < 3; ++k)
+                        for (int q = 0; q < 3; ++q) v += Pl[k * 3 + i] * A[k * 4 + q] * Pr[q * 3 + j];
+                    B[i * 4 + j] = v;
+                }
+                double t = 0.0;
+                for (int k = 0; k < 3; ++k) t += Pl[k * 3 + i] * A[k * 4 + 3];
+                B[i * 4 + 3] = t;
+            }
+            return B;
+        };
+        const std::array<double, 9> I3{1, 0, 0, 0, 1, 0, 0, 0, 1};
+        std::vector<std::array<double, 9>> Pf(NF);
+        for (int f = 0; f < NF; ++f) Pf[f] = P_of(f);
+        for (int f = 1; f < NF; ++f) fC[f] = xform(Pf[fparent[f]], fC[f], Pf[f]);
+        for (int m = 0; m < M; ++m) {
+            const auto &Pm = Pf[sframe[m]];
+            std::array<double, 3> c{};
+            for (int i = 0; i < 3; ++i)
+                for (int k = 0; k < 3; ++k) c[i] += Pm[k * 3 + i] * scen[m][k];
+            scen[m] = c;
+        }
+        eeoff = xform(Pf[fee], eeoff, I3);
+        for (int f = 1; f < NF; ++f) ftype[f] = ftype[f] <= 3 ? 3 : 6;
+    }
     // ---- pack: spheres grouped by frame (stable), pairs remapped, disabled pairs dropped
     std::vector<int> ord(M);
     for (int m = 0; m < M; ++m) ord[m] = m;
@@ -2087,6 +2112,7 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
     rp.o_doflink = w; w += r4(D);
     rp.o_desc = w; w += r4(NF);
     rp.o_perm = w; w += r4(M);
+    rp.o_doff = w; w += r4(D);
     rp.words = r4(w);
     std::vector<uint32_t> blob(rp.words, 0);
     auto fput = [&](int o, float v) { memcpy(&blob[o], &v, 4); };
@@ -2104,6 +2130,7 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *r) {
         blob[rp.o_sphlink + k] = (uint32_t)sframe[m];
         blob[rp.o_perm + k] = (uint32_t)m;
     }
+    for (int f = 1; f < NF; ++f) blob[rp.o_doff + fdof[f]] = (uint32_t)f | ((ftype[f] == 3 ? 1u : 0u) << 16);
 
     for (int f = 0, k = 0; f <= NF; ++f) {
         while (k < M && sframe[ord[k]] < f) ++k;
