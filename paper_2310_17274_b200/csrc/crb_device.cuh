@@ -348,14 +348,15 @@ __device__ __forceinline__ float box_sdf_grad(const BoxView &b, float px, float 
 
 // Alg. 1 lines 4-9 in fp32 with a fixed operation order and no FMA contraction (the same
 // function runs in the solver and in the crb_ls_select test hook).
+// (ca, gda: candidate a at ca[a * st], gda[a * st])
 __device__ __forceinline__ int ls_select(int A, const float *alpha, float c0, float g0d, const float *ca,
-                                         const float *gda, float c1, float c2, int mode) {
+                                         const float *gda, float c1, float c2, int mode, int st = 1) {
     int best = 0;
     for (int a = 0; a < A; ++a) {
         const float rhs = __fadd_rn(c0, __fmul_rn(__fmul_rn(c1, alpha[a]), g0d));
-        bool ok = ca[a] <= rhs;
-        if (mode == 1) ok = ok && (gda[a] >= __fmul_rn(c2, g0d));
-        if (mode == 2) ok = ok && (fabsf(gda[a]) <= __fmul_rn(c2, fabsf(g0d)));
+        bool ok = ca[a * st] <= rhs;
+        if (mode == 1) ok = ok && (gda[a * st] >= __fmul_rn(c2, g0d));
+        if (mode == 2) ok = ok && (fabsf(gda[a * st]) <= __fmul_rn(c2, fabsf(g0d)));
         if (ok) best = a;
     }
     return best;

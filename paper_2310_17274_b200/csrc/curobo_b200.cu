@@ -740,6 +740,50 @@ __device__ __forceinline__ float ik_step(int D, int m, int DC, int lane, int it,
     return ik_step_lane<32>(D, m, DC, lane, it, cnt, fs, sy, th, g, dd, thp, gp, Sb, Yb, rho, syv, yyv, order, alv);
 }
 
+// The per-candidate bookkeeping of the IK solver on the seed's lane (warp 0) after a pass: the
+// candidate's cost, gradient and g.d; after the last candidate the line-search selection (Alg. 1
+// lines 4-9, ls_select in fp32), the accepted point and the best update (strict <, A23).  Per-dof
+// loops unrolled over DM >= D so the loads issue back to back.  istar = the selected candidate.
+template <int DM>
+__device__ __forceinline__ void ik_post_pass(const KParams &kp, const Smem &s, int a, int D, int lane, float *th,
+                                             float *g, const float *dd, float *best, float *cg, float *cc,
+                                             float *cgd, const float *lim, float &c, float &cbest, float g0d,
+                                             int &istar) {
+    const int DC = D * NC, A = kp.A;
+    cc[a * NC + lane] = s.cfg_cost[lane];
+    float gd = 0.f;
+#pragma unroll
+    for (int d = 0; d < DM; ++d)
+        if (d < D) {
+            const float v = s.gV[d * NC + lane];
+            cg[a * DC + d * NC + lane] = v;
+            gd += v * dd[d * NC + lane];
+        }
+    cgd[a * NC + lane] = gd;
+    if (a != A - 1) return;
+    const int i = ls_select(A, kp.alpha, c, g0d, cc + lane, cgd + lane, kp.c1, kp.c2, kp.ls_mode, NC);
+    const float al = kp.alpha[i];
+    float nt[DM];
+#pragma unroll
+    for (int d = 0; d < DM; ++d) {
+        nt[d] = 0.f;
+        if (d < D) {
+            const int e = d * NC + lane;
+            nt[d] = candidate(th[e], al, dd[e], lim[d], lim[D + d]);
+            th[e] = nt[d];
+            g[e] = cg[i * DC + e];
+        }
+    }
+    c = cc[i * NC + lane];
+    if (c < cbest) {
+        cbest = c;
+#pragma unroll
+        for (int d = 0; d < DM; ++d)
+            if (d < D) best[d * NC + lane] = nt[d];
+    }
+    istar = i;
+}
+
 // ------------------------------------------------------------------------------------------
 template <bool WMMA>
 __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__ KParams kp) {
@@ -871,28 +915,11 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
             for (int d = 0; d < D; ++d) { g[d * NC + lane] = s.gV[d * NC + lane]; best[d * NC + lane] = th[d * NC + lane]; }
             continue;
         }
-        cc[a * NC + lane] = s.cfg_cost[lane];
-        float gd = 0.f;
-        for (int d = 0; d < D; ++d) {
-            const float v = s.gV[d * NC + lane];
-            cg[a * DC + d * NC + lane] = v;
-            gd += v * dd[d * NC + lane];
-        }
-        cgd[a * NC + lane] = gd;
+        int i = 0;
+        if (D <= 8) ik_post_pass<8>(kp, s, a, D, lane, th, g, dd, best, cg, cc, cgd, lim, c, cbest, g0d, i);
+        else if (D <= 16) ik_post_pass<16>(kp, s, a, D, lane, th, g, dd, best, cg, cc, cgd, lim, c, cbest, g0d, i);
+        else ik_post_pass<32>(kp, s, a, D, lane, th, g, dd, best, cg, cc, cgd, lim, c, cbest, g0d, i);
         if (a == A - 1) {
-            float ca[8], gda[8];
-            for (int k = 0; k < A; ++k) { ca[k] = cc[k * NC + lane]; gda[k] = cgd[k * NC + lane]; }
-            const int i = ls_select(A, kp.alpha, c, g0d, ca, gda, kp.c1, kp.c2, kp.ls_mode);
-            for (int d = 0; d < D; ++d) {
-                const int e = d * NC + lane;
-                th[e] = candidate(th[e], kp.alpha[i], dd[e], lim[d], lim[D + d]);
-                g[e] = cg[i * DC + e];
-            }
-            c = ca[i];
-            if (c < cbest) {
-                cbest = c;
-                for (int d = 0; d < D; ++d) best[d * NC + lane] = th[d * NC + lane];
-            }
             if (kp.trace && active) {
                 const int tj = trace_slot(kp, (lpass - 1) / A);
                 if (tj >= 0) trace_ik(kp, 2, (size_t)p * kp.S + sd, 0, tj, cnt, c, 0.f, 0.f, i, cbest);
