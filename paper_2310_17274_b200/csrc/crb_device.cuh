@@ -154,6 +154,9 @@ struct KParams {
     float alpha[8], c1, c2;
     long long seed_base;
     // particle warm-up (Alg. 5; f1)
+    float *ik_state;              // persistent IK: saved solver state per seed group (global)
+    int *ik_flags;                // [0] unit counter, [1] flat mapping, [2 + g] chunks done of group g
+    int ik_chunks;                // iteration chunks per seed group (1: whole solve per unit)
     float *trace;                 // solver trace for teacher-forced parity (NULL: off; header)
     int n_trace, trace_iter[8];
     int check_every;              // chunked convergence exit of TO solves (0: off; reading B20)
@@ -262,6 +265,27 @@ __device__ __forceinline__ int stage_tables(const KParams &kp, float *smem, int 
     }
     __syncthreads();
     mbar_wait(bar, 0);
+    return K;
+}
+
+// The environment `env`'s cuboids into shared memory for a CTA that already staged the tables
+// once (persistent kernels: a later work unit of another environment).  All threads; a plain
+// cooperative copy (the TMA barrier of stage_tables is not re-armed).  Returns K.
+__device__ __forceinline__ int restage_world(const KParams &kp, float *smem, int env) {
+    __syncthreads();   // every thread is done with the previous environment
+    const int K = (env >= 0 && env < kp.n_env) ? kp.box_count[env] : 0;
+    if (!kp.lay.boxes_gmem) {
+        const float4 *src = kp.boxes + (size_t)env * kp.kmax * 4;
+        float4 *dst = reinterpret_cast<float4 *>(smem + kp.lay.boxes);
+        for (int i = threadIdx.x; i < 4 * K; i += NT) dst[i] = src[i];
+        if (kp.lay.stage_l1) {
+            const uint4 *l1s = kp.boxes_l1 + (size_t)env * kp.kpairs;
+            uint4 *l1d = reinterpret_cast<uint4 *>(smem + kp.lay.boxl1);
+            for (int i = threadIdx.x; i < (K + 1) / 2; i += NT) l1d[i] = l1s[i];
+        }
+    }
+    if (threadIdx.x == 0) reinterpret_cast<int *>(smem + kp.lay.mbar)[2] = env;
+    __syncthreads();
     return K;
 }
 

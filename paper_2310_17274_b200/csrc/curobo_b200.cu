@@ -785,152 +785,235 @@ __device__ __forceinline__ void ik_post_pass(const KParams &kp, const Smem &s, i
 }
 
 // ------------------------------------------------------------------------------------------
-template <bool WMMA>
+template <bool WMMA, bool PERSIST>
 __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
-    const int G = (kp.S + NC - 1) / NC;
-    const int p = blockIdx.x / G, grp = blockIdx.x - p * G;
-    const int env = kp.env ? kp.env[p] : 0;
-    const int K = stage_tables(kp, smem, env);
     const Smem s = make_smem(kp, smem);
     const int D = kp.rp.D, m = kp.m, A = kp.A;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int n_act = min(NC, kp.S - grp * NC);
     const int DC = D * NC;
+    const int G = (kp.S + NC - 1) / NC;
+    // Work units.  Sequential kernel: one 32-seed group of one problem
+    // per CTA, all iterations.  Persistent kernel (PERSIST): the grid holds one wave of CTAs that
+    // take units u = c * NG + g (chunk-major) from a global counter; unit (g, c) runs iterations
+    // [c iters / C, (c + 1) iters / C) of seed group g, restoring the solver state that (g, c - 1)
+    // saved to global memory (it waits on its completion flag; the chunk-major order makes the
+    // wait rare).  With one environment for every problem (ik_flags[1], set by a device check)
+    // the groups are flat: 32 consecutive seeds of the P x S batch, so no lane idles when S is
+    // not a multiple of 32.  Each seed's arithmetic is the same in every mapping (bitwise).
+    const bool flat = PERSIST && kp.ik_flags[1] != 0;
+    const long long PS = (long long)kp.P * kp.S;
+    const int NG = flat ? (int)((PS + NC - 1) / NC) : kp.P * G;
+    const int C = PERSIST ? kp.ik_chunks : 1;
+    const int SW = (6 + 2 * (m + 1)) * DC + 3 * (m + 1) * NC;   // saved solver words: th .. yyv
+    const int SWT = SW + (m + 5) * NC;                            // + ring order, 4 per-lane scalars
     float *base = smem + kp.lay.solver;
     float *th = base, *g = th + DC, *dd = g + DC, *thp = dd + DC, *gp = thp + DC, *best = gp + DC,
           *Sb = best + DC, *Yb = Sb + (m + 1) * DC, *rho = Yb + (m + 1) * DC, *syv = rho + (m + 1) * NC,
           *yyv = syv + (m + 1) * NC, *cg = yyv + (m + 1) * NC, *cc = cg + A * DC, *cgd = cc + A * NC;
     int *order = reinterpret_cast<int *>(cgd + A * NC);   // [m][32]
     const float *lim = s.fw + kp.rp.o_lim;
-    const int sd = grp * NC + lane;
-    const bool active = lane < n_act;
-
-    if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[p * kp.cp.gw + t / NC];
-    if (warp == 0)
-        for (int d = 0; d < D; ++d) {
-            const float v = active ? kp.q_in[((size_t)p * kp.S + sd) * D + d] : lim[d];
-            th[d * NC + lane] = v;
-            s.q_cfg[d * NC + lane] = v;
-        }
-    __syncthreads();
-    prep_sincos(s, kp.rp);
-    // single eval_pass call site: the particle warm-up (f1, cost only: thread t < D*32 owns
-    // element t with mu in th, Theta_sigma in g, the UPDATE sums in dd / thp), then pass 0 =
-    // Theta_0 and (L-BFGS step, A candidates) per iteration
-    float c = 0.f, cbest = 0.f, g0d = 0.f;
-    int cnt = 0, fs = 0;
-    const int npart = kp.pn_iters * kp.pn;
-    const int npass = npart + 1 + kp.iters * A;
-    const unsigned pk1 = (unsigned)(kp.prob_base + p);
-    const unsigned psd = (unsigned)(kp.seed_base + grp * NC + (t & 31));
-    ParticleAcc pacc;
-    pacc.reset();
-    float tm = -INFINITY, tZ = 0.f;   // merged particle chunks of the current warm-up iteration
-    if (npart > 0)
-        for (int idx = t; idx < DC; idx += NT) {   // D * 32 elements: D > 8 needs more than one per thread
-            const int d = idx / NC;
-            const float s0 = kp.s0_frac * (lim[D + d] - lim[d]);   // B8
-            g[idx] = s0 * s0;
-        }
-    for (int pass = 0; pass < npass; ++pass) {
-        const bool part = pass < npart;
-        const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
-        const int lpass = pass - npart;
-        const int a = part ? -2 : (lpass == 0 ? -1 : (lpass - 1) % A);
-        if (part)
-            for (int idx = t; idx < DC; idx += NT) {
-                // ---- f1 SAMPLE (Alg. 5) for every seed of the group: variable d of seed idx & 31
-                // (idx & 31 == t & 31: psd is this thread's seed for all its elements)
-                const int d = idx / NC;
-                const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
-                const float v = fminf(fmaxf(fmaf(sqrtf(g[idx]), z, th[idx]), lim[d]), lim[D + d]);
-                s.q_cfg[idx] = v;
-                joint_csq(s, kp.rp, idx, v);
-            }
-        if (a == 0 && warp == 0) {
-            const int it = (lpass - 1) / A;
-            const int tj = active ? trace_slot(kp, it) : -1;
-            if (tj >= 0) trace_ik(kp, 0, (size_t)p * kp.S + sd, it, tj, cnt, c, 0.f, 0.f, 0, 0.f);
-            float sy;
-            g0d = ik_step(D, m, DC, lane, it, cnt, fs, sy, th, g, dd, thp, gp, Sb, Yb, rho, syv, yyv, order, s.ls);
-            if (tj >= 0) trace_ik(kp, 1, (size_t)p * kp.S + sd, it, tj, cnt, c, g0d, sy, 0, 0.f);
-        }
-        if (a >= 0) {
-            if (a == 0) __syncthreads();   // the L-BFGS step (warp 0) wrote the directions
-            for (int idx = t; idx < DC; idx += NT) {   // all threads: candidate + its sin / cos
-                const int d = idx / NC;
-                const float v = candidate(th[idx], kp.alpha[a], dd[idx], lim[d], lim[D + d]);
-                s.q_cfg[idx] = v;
-                joint_csq(s, kp.rp, idx, v);
-            }
-        }
-        eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
-        if (part) {
-            // ---- f1 UPDATE, streamed over the particles of a chunk (Eqs. particle_1/2, B6), per
-            // seed; the chunks merged in order (chunk_merge; totals in cg, unused during the warm-up)
-            const int nch = A >= 2 ? A : 1, ch = particle_chunk(pl, kp.pn, nch);
-            const int clo = ch * kp.pn / nch, chi = (ch + 1) * kp.pn / nch;
-            float *S1t = cg, *S2t = cg + DC;
-            float r;
-            const float w = pacc.add(s.cfg_cost[t & 31], kp.p_inv_beta, r);
-            for (int idx = t; idx < DC; idx += NT) {   // w, r: seed idx & 31 == t & 31
-                const float x = s.q_cfg[idx], dx = x - th[idx];
-                dd[idx] = (pl == clo ? 0.f : dd[idx] * r) + w * x;
-                thp[idx] = (pl == clo ? 0.f : thp[idx] * r) + w * dx * dx;
-            }
-            if (pl == chi - 1 && nch > 1) {
-                if (clo == 0) { tm = -INFINITY; tZ = 0.f; }   // the iteration's first (non-empty) chunk
-                float ft, fc;
-                chunk_merge(tm, tZ, pacc.m, pacc.Z, ft, fc);
-                for (int idx = t; idx < DC; idx += NT) {
-                    S1t[idx] = (clo == 0 ? 0.f : S1t[idx]) * ft + dd[idx] * fc;
-                    S2t[idx] = (clo == 0 ? 0.f : S2t[idx]) * ft + thp[idx] * fc;
-                }
-                pacc.reset();
-            }
-            if (pl == kp.pn - 1) {
-                const float Zs = nch > 1 ? tZ : pacc.Z;
-                const float *S1 = nch > 1 ? S1t : dd, *S2 = nch > 1 ? S2t : thp;
-                for (int idx = t; idx < DC; idx += NT) {
-                    if (Zs > 0.f) {
-                        const float iz = 1.f / Zs;
-                        th[idx] = (1.f - kp.k_mu) * th[idx] + kp.k_mu * (S1[idx] * iz);
-                        g[idx] = (1.f - kp.k_sigma) * g[idx] + kp.k_sigma * (S2[idx] * iz);
-                    }
-                    if (pass == npart - 1) {   // Theta_0 of L-BFGS = mu
-                        const float v = th[idx];
-                        s.q_cfg[idx] = v;
-                        joint_csq(s, kp.rp, idx, v);
-                    }
-                }
-                pacc.reset();
-            }
-            continue;
-        }
-        if (warp != 0) continue;
-        if (a < 0) {
-            c = s.cfg_cost[lane];
-            cbest = c;
-            for (int d = 0; d < D; ++d) { g[d * NC + lane] = s.gV[d * NC + lane]; best[d * NC + lane] = th[d * NC + lane]; }
-            continue;
-        }
-        int i = 0;
-        if (D <= 8) ik_post_pass<8>(kp, s, a, D, lane, th, g, dd, best, cg, cc, cgd, lim, c, cbest, g0d, i);
-        else if (D <= 16) ik_post_pass<16>(kp, s, a, D, lane, th, g, dd, best, cg, cc, cgd, lim, c, cbest, g0d, i);
-        else ik_post_pass<32>(kp, s, a, D, lane, th, g, dd, best, cg, cc, cgd, lim, c, cbest, g0d, i);
-        if (a == A - 1) {
-            if (kp.trace && active) {
-                const int tj = trace_slot(kp, (lpass - 1) / A);
-                if (tj >= 0) trace_ik(kp, 2, (size_t)p * kp.S + sd, 0, tj, cnt, c, 0.f, 0.f, i, cbest);
-            }
-        }
+    int *bcast = reinterpret_cast<int *>(smem + kp.lay.mbar) + 3;
+    int staged = -0x7fffffff, K = 0;
+    int unit = blockIdx.x;
+    if (PERSIST) {
+        if (t == 0) *bcast = atomicAdd(kp.ik_flags, 1);
+        __syncthreads();
+        unit = *bcast;
     }
-    __syncthreads();
-    if (warp == 0 && active) {
-        const size_t u = (size_t)p * kp.S + sd;
-        kp.seed_best_cost[u] = cbest;
-        for (int d = 0; d < D; ++d) kp.seed_best_traj[u * D + d] = best[d * NC + lane];
+    while (unit < NG * C) {
+        const int ch = unit / NG, gi = unit - ch * NG;
+        // this lane's seed: flat index fsd = p * S + sd
+        long long fsd;
+        int n_act;
+        if (flat) {
+            fsd = (long long)gi * NC + lane;
+            n_act = (int)min((long long)NC, PS - (long long)gi * NC);
+        } else {
+            const int pg = gi / G, grp = gi - pg * G;
+            fsd = (long long)pg * kp.S + grp * NC + lane;
+            n_act = min(NC, kp.S - grp * NC);
+        }
+        const bool active = lane < n_act;
+        const int p = (int)(min(fsd, PS - 1) / kp.S), sd = (int)(min(fsd, PS - 1) - (long long)p * kp.S);
+        {   // the unit's environment (flat: one for all problems)
+            const int p0 = flat ? 0 : gi / G;
+            const int env = kp.env ? kp.env[p0] : 0;
+            if (staged == -0x7fffffff) K = stage_tables(kp, smem, env);
+            else if (env != staged) K = restage_world(kp, smem, env);
+            staged = env;
+        }
+        const int npart = kp.pn_iters * kp.pn;
+        const int it_lo = (int)((long long)ch * kp.iters / C), it_hi = (int)((long long)(ch + 1) * kp.iters / C);
+        const int pass_lo = ch == 0 ? 0 : npart + 1 + it_lo * A, pass_hi = npart + 1 + it_hi * A;
+        if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[(size_t)p * kp.cp.gw + t / NC];   // t & 31 == lane of thread t
+        float c = 0.f, cbest = 0.f, g0d = 0.f;
+        int cnt = 0, fs = 0;
+        if (ch == 0) {
+            if (warp == 0)
+                for (int d = 0; d < D; ++d) {
+                    const float v = active ? kp.q_in[(size_t)fsd * D + d] : lim[d];
+                    th[d * NC + lane] = v;
+                    s.q_cfg[d * NC + lane] = v;
+                }
+            __syncthreads();
+            prep_sincos(s, kp.rp);
+        } else {
+            if (t == 0) {   // (g, c - 1) has saved its state
+                int *flag = kp.ik_flags + 2 + gi;
+                int v;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+                    if (v >= ch) break;
+                    __nanosleep(256);
+                }
+            }
+            __syncthreads();
+            const float *src = kp.ik_state + (size_t)gi * SWT;
+            for (int i = t; i < SW; i += NT) base[i] = __ldcg(src + i);
+            for (int i = t; i < (m + 1) * NC; i += NT) order[i] = __float_as_int(__ldcg(src + SW + i));
+            if (warp == 0) {
+                const float *sc = src + SW + (m + 1) * NC;   // per-lane scalars
+                c = __ldcg(sc + lane); cbest = __ldcg(sc + NC + lane);
+                cnt = __float_as_int(__ldcg(sc + 2 * NC + lane)); fs = __float_as_int(__ldcg(sc + 3 * NC + lane));
+            }
+            __syncthreads();
+        }
+        // single eval_pass call site: the particle warm-up (f1, cost only: thread t < D*32 owns
+        // element t with mu in th, Theta_sigma in g, the UPDATE sums in dd / thp), then pass 0 =
+        // Theta_0 and (L-BFGS step, A candidates) per iteration
+        const unsigned pk1 = (unsigned)(kp.prob_base + p);
+        const unsigned psd = (unsigned)(kp.seed_base + sd);
+        ParticleAcc pacc;
+        pacc.reset();
+        float tm = -INFINITY, tZ = 0.f;   // merged particle chunks of the current warm-up iteration
+        if (ch == 0 && npart > 0)
+            for (int idx = t; idx < DC; idx += NT) {   // D * 32 elements: D > 8 needs more than one per thread
+                const int d = idx / NC;
+                const float s0 = kp.s0_frac * (lim[D + d] - lim[d]);   // B8
+                g[idx] = s0 * s0;
+            }
+        for (int pass = pass_lo; pass < pass_hi; ++pass) {
+            const bool part = pass < npart;
+            const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
+            const int lpass = pass - npart;
+            const int a = part ? -2 : (lpass == 0 ? -1 : (lpass - 1) % A);
+            if (part)
+                for (int idx = t; idx < DC; idx += NT) {
+                    // ---- f1 SAMPLE (Alg. 5) for every seed of the group: variable d of seed idx & 31
+                    // (idx & 31 == t & 31: psd is this thread's seed for all its elements)
+                    const int d = idx / NC;
+                    const float z = particle_normal(kp.rng_key, pk1, (unsigned)d, (unsigned)pl, (unsigned)pit, psd);
+                    const float v = fminf(fmaxf(fmaf(sqrtf(g[idx]), z, th[idx]), lim[d]), lim[D + d]);
+                    s.q_cfg[idx] = v;
+                    joint_csq(s, kp.rp, idx, v);
+                }
+            if (a == 0 && warp == 0) {
+                const int it = (lpass - 1) / A;
+                const int tj = active ? trace_slot(kp, it) : -1;
+                if (tj >= 0) trace_ik(kp, 0, (size_t)fsd, it, tj, cnt, c, 0.f, 0.f, 0, 0.f);
+                float sy;
+                g0d = ik_step(D, m, DC, lane, it, cnt, fs, sy, th, g, dd, thp, gp, Sb, Yb, rho, syv, yyv, order, s.ls);
+                if (tj >= 0) trace_ik(kp, 1, (size_t)fsd, it, tj, cnt, c, g0d, sy, 0, 0.f);
+            }
+            if (a >= 0) {
+                if (a == 0) __syncthreads();   // the L-BFGS step (warp 0) wrote the directions
+                for (int idx = t; idx < DC; idx += NT) {   // all threads: candidate + its sin / cos
+                    const int d = idx / NC;
+                    const float v = candidate(th[idx], kp.alpha[a], dd[idx], lim[d], lim[D + d]);
+                    s.q_cfg[idx] = v;
+                    joint_csq(s, kp.rp, idx, v);
+                }
+            }
+            eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
+            if (part) {
+                // ---- f1 UPDATE, streamed over the particles of a chunk (Eqs. particle_1/2, B6), per
+                // seed; the chunks merged in order (chunk_merge; totals in cg, unused during the warm-up)
+                const int nch = A >= 2 ? A : 1, pch = particle_chunk(pl, kp.pn, nch);
+                const int clo = pch * kp.pn / nch, chi = (pch + 1) * kp.pn / nch;
+                float *S1t = cg, *S2t = cg + DC;
+                float r;
+                const float w = pacc.add(s.cfg_cost[t & 31], kp.p_inv_beta, r);
+                for (int idx = t; idx < DC; idx += NT) {   // w, r: seed idx & 31 == t & 31
+                    const float x = s.q_cfg[idx], dx = x - th[idx];
+                    dd[idx] = (pl == clo ? 0.f : dd[idx] * r) + w * x;
+                    thp[idx] = (pl == clo ? 0.f : thp[idx] * r) + w * dx * dx;
+                }
+                if (pl == chi - 1 && nch > 1) {
+                    if (clo == 0) { tm = -INFINITY; tZ = 0.f; }   // the iteration's first (non-empty) chunk
+                    float ft, fc;
+                    chunk_merge(tm, tZ, pacc.m, pacc.Z, ft, fc);
+                    for (int idx = t; idx < DC; idx += NT) {
+                        S1t[idx] = (clo == 0 ? 0.f : S1t[idx]) * ft + dd[idx] * fc;
+                        S2t[idx] = (clo == 0 ? 0.f : S2t[idx]) * ft + thp[idx] * fc;
+                    }
+                    pacc.reset();
+                }
+                if (pl == kp.pn - 1) {
+                    const float Zs = nch > 1 ? tZ : pacc.Z;
+                    const float *S1 = nch > 1 ? S1t : dd, *S2 = nch > 1 ? S2t : thp;
+                    for (int idx = t; idx < DC; idx += NT) {
+                        if (Zs > 0.f) {
+                            const float iz = 1.f / Zs;
+                            th[idx] = (1.f - kp.k_mu) * th[idx] + kp.k_mu * (S1[idx] * iz);
+                            g[idx] = (1.f - kp.k_sigma) * g[idx] + kp.k_sigma * (S2[idx] * iz);
+                        }
+                        if (pass == npart - 1) {   // Theta_0 of L-BFGS = mu
+                            const float v = th[idx];
+                            s.q_cfg[idx] = v;
+                            joint_csq(s, kp.rp, idx, v);
+                        }
+                    }
+                    pacc.reset();
+                }
+                continue;
+            }
+            if (warp != 0) continue;
+            if (a < 0) {
+                c = s.cfg_cost[lane];
+                cbest = c;
+                for (int d = 0; d < D; ++d) { g[d * NC + lane] = s.gV[d * NC + lane]; best[d * NC + lane] = th[d * NC + lane]; }
+                continue;
+            }
+            int i = 0;
+            if (D <= 8) ik_post_pass<8>(kp, s, a, D, lane, th, g, dd, best, cg, cc, cgd, lim, c, cbest, g0d, i);
+            else if (D <= 16) ik_post_pass<16>(kp, s, a, D, lane, th, g, dd, best, cg, cc, cgd, lim, c, cbest, g0d, i);
+            else ik_post_pass<32>(kp, s, a, D, lane, th, g, dd, best, cg, cc, cgd, lim, c, cbest, g0d, i);
+            if (a == A - 1) {
+                if (kp.trace && active) {
+                    const int tj = trace_slot(kp, (lpass - 1) / A);
+                    if (tj >= 0) trace_ik(kp, 2, (size_t)fsd, 0, tj, cnt, c, 0.f, 0.f, i, cbest);
+                }
+            }
+        }
+        __syncthreads();
+        if (ch == C - 1) {
+            if (warp == 0 && active) {
+                kp.seed_best_cost[fsd] = cbest;
+                for (int d = 0; d < D; ++d) kp.seed_best_traj[(size_t)fsd * D + d] = best[d * NC + lane];
+            }
+        } else {   // save the state for (g, c + 1), then publish the chunk
+            float *dst = kp.ik_state + (size_t)gi * SWT;
+            for (int i = t; i < SW; i += NT) __stcg(dst + i, base[i]);
+            for (int i = t; i < (m + 1) * NC; i += NT) __stcg(dst + SW + i, __int_as_float(order[i]));
+            if (warp == 0) {
+                float *sc = dst + SW + (m + 1) * NC;
+                __stcg(sc + lane, c); __stcg(sc + NC + lane, cbest);
+                __stcg(sc + 2 * NC + lane, __int_as_float(cnt)); __stcg(sc + 3 * NC + lane, __int_as_float(fs));
+            }
+            __syncthreads();
+            if (t == 0) {
+                __threadfence();
+                int *flag = kp.ik_flags + 2 + gi;
+                const int v = ch + 1;
+                asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+            }
+        }
+        if (!PERSIST) break;
+        if (t == 0) *bcast = atomicAdd(kp.ik_flags, 1);
+        __syncthreads();
+        unit = *bcast;
+        __syncthreads();   // every thread has read the unit before thread 0 may overwrite it
     }
 }
 
@@ -1171,6 +1254,21 @@ __global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ 
 }
 
 #if CRB_PART == 0   // the non-template kernels: only in the main translation unit
+// Persistent IK scheduling set-up (solve_ik_kernel<., true>): flags[0] = unit counter (0),
+// flags[1] = 1 iff every problem uses the same environment (env = NULL counts as env 0), flags[2..]
+// = completed chunks per seed group (0).
+__global__ void ik_persist_init_kernel(const int *env, int P, int NG, int *flags) {
+    __shared__ int diff;
+    if (threadIdx.x == 0) diff = 0;
+    __syncthreads();
+    if (env)
+        for (int p = threadIdx.x; p < P; p += blockDim.x)
+            if (env[p] != env[0]) diff = 1;
+    for (int i = threadIdx.x; i < NG; i += blockDim.x) flags[2 + i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) { flags[0] = 0; flags[1] = diff ? 0 : 1; }
+}
+
 __global__ void __launch_bounds__(NT, 2) fk_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b0 = blockIdx.x * NC;
@@ -1615,7 +1713,7 @@ __global__ void __launch_bounds__(NT, 2) lbfgs_direction_kernel(int n, int count
 }  // namespace
 
 // the <WMMA = true> kernels, instantiated in CRB_PART 1 (no flush-to-zero)
-enum { KW_EVAL_TO, KW_EVAL_IK, KW_SOLVE_TO, KW_SOLVE_IK, KW_SOLVE_TO_CLUSTER, KW_SOLVE_IK_CLUSTER };
+enum { KW_EVAL_TO, KW_EVAL_IK, KW_SOLVE_TO, KW_SOLVE_IK, KW_SOLVE_TO_CLUSTER, KW_SOLVE_IK_CLUSTER, KW_SOLVE_IK_PERSIST };
 const void *crb_wmma_kernel(int k);
 
 #if CRB_STATS
@@ -1640,7 +1738,8 @@ const void *crb_wmma_kernel(int k) {
     case KW_EVAL_TO: return (const void *)eval_to_kernel<true>;
     case KW_EVAL_IK: return (const void *)eval_ik_kernel<true>;
     case KW_SOLVE_TO: return (const void *)solve_to_kernel<true>;
-    case KW_SOLVE_IK: return (const void *)solve_ik_kernel<true>;
+    case KW_SOLVE_IK: return (const void *)solve_ik_kernel<true, false>;
+    case KW_SOLVE_IK_PERSIST: return (const void *)solve_ik_kernel<true, true>;
     case KW_SOLVE_TO_CLUSTER: return (const void *)solve_to_cluster_kernel<true>;
     case KW_SOLVE_IK_CLUSTER: return (const void *)solve_ik_cluster_kernel<true>;
     }
@@ -1679,6 +1778,10 @@ struct crb_ctx {
     size_t cap_mask = 0;
     int *ws_n = nullptr;                  // steering step count (used, unclamped)
     size_t cap_n = 0;
+    float *ws_ik_state = nullptr;         // persistent IK: solver state per seed group
+    size_t cap_ik_state = 0;
+    int *ws_ik_flags = nullptr;           // persistent IK: unit counter, flat flag, chunk flags
+    size_t cap_ik_flags = 0;
     // host-API buffers
     float *h_seeds = nullptr, *h_start = nullptr, *h_goal = nullptr, *h_best = nullptr, *h_bcost = nullptr;
     int *h_env = nullptr;
@@ -1730,7 +1833,7 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     auto take = [&](int words) { int o = w; w += r4(words); return o; };
     L.robot = take(rp.words);
     L.boxes = take(kmax * 16);
-    L.boxl1 = take(((kmax + 1) / 2) * 4);   // bounding-sphere pairs (small-world build; 0 when kmax = 0)
+    L.boxl1 = take(CRB_WORLD_CULL ? 0 : ((kmax + 1) / 2) * 4);   // bounding-sphere pairs (fp16x2 pre-screen builds only)
     L.mbar = take(4);
     L.XS = mode == MODE_TO ? H + 5 : 0;
     L.q_cfg = take(D * NC);
@@ -1859,6 +1962,7 @@ crb_status crb_destroy(crb_ctx *ctx) {
     cudaFree(ctx->d_boxes_l1);
     cudaFree(ctx->d_boxes_ab);
     cudaFree(ctx->ws_cost); cudaFree(ctx->ws_traj); cudaFree(ctx->ws_mask); cudaFree(ctx->ws_n);
+    cudaFree(ctx->ws_ik_state); cudaFree(ctx->ws_ik_flags);
     cudaFree(ctx->h_seeds); cudaFree(ctx->h_start); cudaFree(ctx->h_goal); cudaFree(ctx->h_best);
     cudaFree(ctx->h_bcost); cudaFree(ctx->h_env); cudaFree(ctx->h_key);
     delete ctx;
@@ -2398,7 +2502,7 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
     kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs; kp.dt_arr = dt;
     const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
     kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
-    kp.lay.stage_l1 = use_world_mma(ctx) ? 0 : 1;
+    kp.lay.stage_l1 = (use_world_mma(ctx) || CRB_WORLD_CULL) ? 0 : 1;
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
     const bool wm = use_world_mma(ctx);
     if (mode == MODE_TO)
@@ -2461,7 +2565,7 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     kp.seed_best_cost = sbc; kp.seed_best_traj = sbt;
     const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
     kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
-    kp.lay.stage_l1 = use_world_mma(ctx) ? 0 : 1;
+    kp.lay.stage_l1 = (use_world_mma(ctx) || CRB_WORLD_CULL) ? 0 : 1;
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids + solver)");
     const bool wm = use_world_mma(ctx);
     // latency mode: A CTAs per seed in a cluster when the whole batch fits one wave (2 CTAs / SM)
@@ -2502,10 +2606,38 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     } else if (mode == MODE_TO)
         st = launch_fn(ctx, wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false>, P * S, bytes, stream_,
                        kp, "solve_to_kernel");
-    else
-        st = launch_fn(ctx, wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false>, P * ((S + NC - 1) / NC),
-                       bytes, stream_,
-                    kp, "solve_ik_kernel");
+    else {
+        // IK scheduling: the persistent chunked kernel when the batch
+        // spans at least two waves of groups (sp->persist = -1: 4 iteration chunks), else one
+        // CTA per 32-seed group.  sp->persist = 0 forces the latter, k >= 1 k chunks.
+        const int G = (S + NC - 1) / NC;
+        const long long NGg = (long long)P * G;
+        int chunks = sp->persist;
+        if (chunks < 0) chunks = (NGg >= 2 * W && sp->iters >= 8) ? 4 : 0;
+        chunks = std::min(chunks, std::max(sp->iters, 1));
+        if (chunks >= 1) {
+            const int m = sp->history, DC = D * NC;
+            const size_t swt = (size_t)(6 + 2 * (m + 1)) * DC + 3 * (m + 1) * NC + (m + 5) * NC;
+            if ((st = grow(ctx, &ctx->ws_ik_state, &ctx->cap_ik_state, (size_t)NGg * swt)) != CRB_OK) return st;
+            if ((st = grow(ctx, &ctx->ws_ik_flags, &ctx->cap_ik_flags, (size_t)NGg + 2)) != CRB_OK) return st;
+            kp.ik_state = ctx->ws_ik_state; kp.ik_flags = ctx->ws_ik_flags; kp.ik_chunks = chunks;
+            ik_persist_init_kernel<<<1, 256, 0, stream_>>>(env, P, (int)NGg, ctx->ws_ik_flags);
+            ctx->launches++;
+            if ((st = cuda_check(ctx, cudaGetLastError(), "ik_persist_init_kernel")) != CRB_OK) return st;
+            const void *kern = wm ? crb_wmma_kernel(KW_SOLVE_IK_PERSIST) : (const void *)solve_ik_kernel<false, true>;
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+            if (e != cudaSuccess) return cuda_check(ctx, e, "solve_ik_kernel (persistent)");
+            int per_sm = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes);
+            if (e != cudaSuccess || per_sm < 1) return cuda_check(ctx, e != cudaSuccess ? e : cudaErrorInvalidConfiguration, "occupancy");
+            const long long grid = std::min<long long>(NGg * chunks, (long long)per_sm * ctx->sm_count);
+            st = launch_fn(ctx, kern, (int)grid, bytes, stream_, kp, "solve_ik_kernel (persistent)");
+        } else {
+            kp.ik_chunks = 1;
+            st = launch_fn(ctx, wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false, false>, (int)NGg,
+                           bytes, stream_, kp, "solve_ik_kernel");
+        }
+    }
     if (st != CRB_OK) return st;
     if (P > 0 && (best_traj || best_cost || best_key)) {
         select_kernel<<<P, 128, 0, stream_>>>(P, S, N, sbc, sbt, (long long)sp->global_seed_base, best_traj,
@@ -2563,13 +2695,13 @@ crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, i
     const int mode = H == 1 ? MODE_IK : MODE_TO;
     const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, history, n_alpha, true, kp.lay);
     kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
-    kp.lay.stage_l1 = use_world_mma(ctx) ? 0 : 1;
+    kp.lay.stage_l1 = (use_world_mma(ctx) || CRB_WORLD_CULL) ? 0 : 1;
     if (smem_bytes) *smem_bytes = (int)bytes;
     if (bytes > SMEM_MAX) { if (ctas_per_sm) *ctas_per_sm = 0; return CRB_OK; }
     int n = 0;
     const bool wm = use_world_mma(ctx);
     const void *fn = mode == MODE_TO ? (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false>)
-                                     : (wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false>);
+                                     : (wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false, false>);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     st = cuda_check(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, NT, bytes), "occupancy");
     if (ctas_per_sm) *ctas_per_sm = n;

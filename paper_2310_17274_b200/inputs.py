@@ -125,6 +125,9 @@ class SolverParams:
     # latency mode: the line-search candidates of an iteration on the CTAs of a cluster
     # (-1 automatic for batches that fit one wave, 0 off, 1 on); bitwise identical results
     cluster: int = -1
+    # IK scheduling: -1 automatic (persistent kernel over (seed group, iteration chunk) units for
+    # batches of two or more waves), 0 one CTA per group, k >= 1 persistent with k chunks
+    persist: int = -1
 
 
 # --------------------------------------------------------------------------------------------

@@ -68,7 +68,7 @@ class crb_solver_params(C.Structure):
                 ("k_mu", C.c_float), ("k_sigma", C.c_float), ("sigma0_frac", C.c_float),
                 ("rng_key", C.c_uint32), ("global_problem_base", C.c_int64), ("check_every", C.c_int),
                 ("conv_rtol", C.c_float), ("cluster", C.c_int), ("trace", C.c_void_p), ("n_trace", C.c_int),
-                ("trace_iter", C.c_int * 8)]
+                ("trace_iter", C.c_int * 8), ("persist", C.c_int)]
 
 
 _V = C.c_void_p
@@ -152,7 +152,7 @@ def solver_params_struct(sp: inputs.SolverParams, seed_base: int = 0, problem_ba
                              float(sp.sigma0_frac), int(sp.rng_key) & 0xFFFFFFFF, int(problem_base),
                              int(sp.check_every), float(sp.conv_rtol), int(sp.cluster),
                              None if trace is None else C.c_void_p(trace.data_ptr()), len(trace_iters),
-                             (C.c_int * 8)(*ti))
+                             (C.c_int * 8)(*ti), int(getattr(sp, "persist", -1)))
 
 
 def trace_rec(N: int, m: int) -> int:

@@ -48,15 +48,15 @@ def test_sass_is_sm100a(lib_path):
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True).stdout
     assert "UBLKCP" in sass            # TMA bulk copy of the robot / cuboid tables
-    # both builds (small-world: template argument false, large-world: true) run the cuboid
-    # pre-screen as packed fp16 (HFMA2 on half2 pairs of cuboids); the tensor-core screen of round 1
-    # is compiled only with CRB_LARGE_L1 = 0
+    # both builds (small-world: template argument false, large-world: true) cull the cuboids of a
+    # work item with the group's AABB (warp min / max: REDUX) and a ballot, and never use the
+    # round-1 tensor-core screen (compiled only with CRB_WORLD_CULL = 0, CRB_LARGE_L1 = 0)
     funcs = re.split(r"\n\s+Function : ", sass)
     for kern in ("solve_to_kernel", "solve_ik_kernel", "eval_to_kernel", "eval_ik_kernel"):
         body = {("ILb1E" in f.split("\n", 1)[0]): f for f in funcs if kern in f.split("\n", 1)[0]}
         assert set(body) == {False, True}, kern
         for b in (False, True):
-            assert re.search(r"HFMA2 R\d+, R\d+.*\.H0_H0", body[b]), (kern, b)   # broadcast sphere coordinate
+            assert re.search(r"REDUX\.(MIN|MAX)", body[b]), (kern, b)   # group AABB over the slots
             assert "HMMA" not in body[b], (kern, b)
 
 
