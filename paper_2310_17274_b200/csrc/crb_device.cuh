@@ -60,6 +60,12 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #define CRB_SELF_CULL_DEV 1
 #endif
 
+// Unroll factor of the once-per-pass per-slot loops (link sums, pose terms, world-group sum): code
+// size against the instruction cache
+#ifndef CRB_COLD_UNROLL
+#define CRB_COLD_UNROLL 2
+#endif
+
 // Self-collision screen tightened to the pairs that can still reach the lane's current best
 // penetration (1), or the plain d < R test throughout (0)
 #ifndef CRB_SELF_PRUNE
@@ -76,6 +82,8 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #endif
 
 namespace crb {
+
+constexpr int kColdUnroll = CRB_COLD_UNROLL;
 
 constexpr int NT = 256;          // threads per CTA
 constexpr int NW = NT / 32;      // warps per CTA
@@ -970,6 +978,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         // per-slot goal, bound and smoothness terms here (a8 finished before the placement
         // barrier), off the merge's critical path
         float cb = 0.f, cs = 0.f;
+#pragma unroll kColdUnroll
         for (int d = 0; d < D; ++d) { cb += s.cbb[d * NC + c]; cs += s.csm[d * NC + c]; }
         const bool valid = c < n_act;
         s.cfg_terms[0 * NC + c] = valid ? C : 0.f;
@@ -1523,6 +1532,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     } else if (warp == 1) {
         const int c = lane;
         float cw = 0.f;
+#pragma unroll kColdUnroll
         for (int q = 0; q < ((rp.M + 3) >> 2); ++q) cw += s.sg[(q << 2) * NC + c].w;   // fixed order
         s.cfg_terms[4 * NC + c] = c < n_act ? cw : 0.f;
     }
@@ -1557,6 +1567,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             if (idx < rp.L * NC) {
                 const int l = idx / NC, c = idx - l * NC;
                 const int b = s.iw[rp.o_sbeg + l], e = s.iw[rp.o_sbeg + l + 1];
+#pragma unroll kColdUnroll
                 for (int m = b; m < e; ++m) {
                     const float4 g = s.sg[m * NC + c], w = s.sw[m * NC + c];
                     const float gx = g.x, gy = g.y, gz = g.z;
@@ -1649,6 +1660,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             else if (hx == H) { xlo = H - 3; xhi = H + 2; }
             else { s.gV[h * D + d] = 0.f; continue; }
             float acc = 0.f;
+#pragma unroll 1
             for (int xi = xlo; xi <= xhi; ++xi) acc += s.xs[d * XS + xi];
             s.gV[h * D + d] = acc;
             if (dvec) gdp += acc * dvec[h * D + d];
