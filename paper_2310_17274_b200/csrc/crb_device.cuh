@@ -84,6 +84,14 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 namespace crb {
 
 constexpr int kColdUnroll = CRB_COLD_UNROLL;
+#ifndef CRB_MERGE_UNROLL
+#define CRB_MERGE_UNROLL 2
+#endif
+#ifndef CRB_LS_UNROLL
+#define CRB_LS_UNROLL 1
+#endif
+constexpr int kMergeUnroll = CRB_MERGE_UNROLL;   // self-collision merge over the NW warps
+constexpr int kLsUnroll = CRB_LS_UNROLL;         // line-search selection over the candidates
 
 constexpr int NT = 256;          // threads per CTA
 constexpr int NW = NT / 32;      // warps per CTA
@@ -384,6 +392,7 @@ __device__ __forceinline__ float box_sdf_grad(const BoxView &b, float px, float 
 __device__ __forceinline__ int ls_select(int A, const float *alpha, float c0, float g0d, const float *ca,
                                          const float *gda, float c1, float c2, int mode, int st = 1) {
     int best = 0;
+#pragma unroll kLsUnroll
     for (int a = 0; a < A; ++a) {
         const float rhs = __fadd_rn(c0, __fmul_rn(__fmul_rn(c1, alpha[a]), g0d));
         bool ok = ca[a * st] <= rhs;
@@ -1509,6 +1518,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         const int c = lane;
         float bp = 0.f;
         int br = 0x7fffffff, bij = -1;
+#pragma unroll kMergeUnroll
         for (int w = 0; w < NW; ++w) {
             const float p = s.sbest[w * NC + c];
             const int r = s.srank[w * NC + c];
