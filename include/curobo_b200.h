@@ -28,8 +28,9 @@
  *     +inf key and never wins a selection (SURVEY §8(b) deviation).
  *   - Capacity limits (CRB_E_LIMIT): D <= 31 (D + 1 kinematic frames after folding the fixed
  *     links, 32-bit subtree masks), L <= 64 links, M <= 512 spheres and pairs <= 16384 by the
- *     packed tables, H*D <= 512, history <= 32, n_alpha <= 8, TO mode requires 8 <= H <= 32 (one
- *     timestep per lane of a warp), IK mode has H == 1, and the per-CTA shared memory (robot
+ *     packed tables, H*D <= 512, history <= 32, n_alpha <= 8, TO mode requires 8 <= H <= 64 (one
+ *     timestep per lane of a warp; H > 32 runs each evaluation as 2-3 windows of 30-31 owned
+ *     timesteps with a halo timestep, P:2217 uses 44), IK mode has H == 1, and the per-CTA shared memory (robot
  *     tables, M x 32 sphere positions and gradients of 16 B each, the solver state, plus one
  *     environment's cuboids below 60 cuboids) must fit in 227 KB, which in practice bounds M at
  *     about 150 (the Franka problem: M = 64, 113 KB, two CTAs per SM).  SURVEY §8(b) sketched

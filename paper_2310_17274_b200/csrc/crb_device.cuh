@@ -137,6 +137,7 @@ struct Layout {
     int solver;      // start of the solver region
     int total;       // words
     int XS;          // row length of xs (H + 5)
+    int HS;          // slot stride of the state-gradient rows gq / gva (TO: H rounded up to 32; IK: 32)
     int boxes_gmem;  // 1: the cuboid table is read from global memory (large-world build), not staged
     int stage_l1;    // 1: also stage the bounding-sphere pairs (solver / evaluation kernels, small worlds)
 };
@@ -817,7 +818,7 @@ __device__ __forceinline__ void stage_dt(const KParams &kp, const Smem &s, int r
     s.tdp[8] = (float)(cf.wb[3] * (r2 * r));
 }
 
-template <int MODE, bool WMMA>
+template <int MODE, bool WMMA, bool LONG = false>
 __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
                                           const float *dvec, bool grad = true) {
     Smem s = make_smem(kp, smem);
@@ -836,8 +837,15 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = rp.D, H = cf.H, XS = kp.lay.XS;
     const float *lim = s.fw + rp.o_lim;
+    // Timestep windows (TO with H > 32): lane c holds slot base + c;
+    // window w owns slots [olo, ohi) -- [0, 31), then 30 per window, the last up to 31 -- and its
+    // other lanes are halo (an owned slot's sweep and speed read its neighbours).  Costs add up
+    // over the windows; the state gradients gq / gva are slot-indexed (stride HS) and the
+    // transposed stencil runs once after the last window.  H <= 32 and IK: one window, base 0.
+    const int HS = LONG ? kp.lay.HS : NC;   // (the host sets lay.HS = 32 unless H > 32)
+    // (LONG: the H > 32 instantiation; the others fold the windows away at compile time)
+    const int nwin = (LONG && MODE == MODE_TO && H > NC) ? 2 + max(0, (H - 62 + 29) / 30) : 1;
     if (tid == 0) {
-        reinterpret_cast<int *>(s.scal + 4)[0] = 0;   // work-queue counter (read after 2 barriers)
         // world items in decreasing cost of the previous pass (longest first: the queue's tail is
         // then the short self items); ties keep index order.  Which warp takes which item never
         // changes a result (fixed-order merges).
@@ -853,8 +861,16 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         }
     }
 
+    for (int win = 0; win < nwin; ++win) {
+    const int olo = win == 0 ? 0 : 31 + 30 * (win - 1);
+    const int ohi = MODE == MODE_IK ? n_act : (win == nwin - 1 ? H : (win == 0 ? 31 : olo + 30));
+    const int base = win == 0 ? 0 : olo - 1;
+    const bool own_l = base + lane >= olo && base + lane < ohi;   // this lane's slot is owned
+    if (tid == 0) reinterpret_cast<int *>(s.scal + 4)[0] = 0;   // work-queue counter (read after 2 barriers)
+
     // ---- a2: state map (O2, Table 5 last row) into xs[D][H+5] and the slot configurations
     if (MODE == MODE_TO) {
+        if (win == 0)
         for (int idx = tid; idx < D * XS; idx += NT) {
             const int d = idx / XS, i = idx - d * XS, h = i - 2;
             float v;
@@ -865,7 +881,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         }
         for (int idx = tid; idx < D * NC; idx += NT) {
             const int d = idx / NC, c = idx - d * NC;
-            const int h = c + 1 <= H ? c + 1 : H;
+            const int h = base + c + 1 <= H ? base + c + 1 : H;
             float v;
             if (h <= 3) v = s.st[d];
             else if (h >= H - 3) v = thA[(H - 1) * D + d];
@@ -894,11 +910,13 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         for (int idx = tid; idx < D * NC; idx += FK_W0 * NC) {
             const int d = idx / NC, c = idx - d * NC;
             float cb = 0.f, cs = 0.f, gx = 0.f, gv = 0.f, ga = 0.f, gj = 0.f;
-            if (c < n_act) {
+            const int sl = base + c;
+            const bool own = sl >= olo && sl < ohi;
+            if (own) {
                 const float lo = lim[d], hi = lim[D + d];
                 float dd;
                 if (MODE == MODE_TO) {
-                    const float *x = s.xs + d * XS + c + 3;   // x_h with h = c + 1
+                    const float *x = s.xs + d * XS + sl + 3;   // x_h with h = slot + 1
                     const float xm2 = x[-2], xm1 = x[-1], x0 = x[0], xp1 = x[1], xp2 = x[2];
                     // O3 five-point stencil (§A.5, A15)
                     const float v = (-xp2 + 8.f * xp1 - 8.f * xm1 + xm2) * s.tdp[1];
@@ -921,7 +939,10 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 }
             }
             s.cbb[idx] = cb; s.csm[idx] = cs; s.gxd[idx] = gx;
-            if (MODE == MODE_TO) { s.gva[idx] = gv; s.gva[D * NC + idx] = ga; s.gva[2 * D * NC + idx] = gj; }
+            if (MODE == MODE_TO && own) {   // slot-indexed [3][D][HS]
+                const int gi = d * HS + sl;
+                s.gva[gi] = gv; s.gva[D * HS + gi] = ga; s.gva[2 * D * HS + gi] = gj;
+            }
         }
     }
 #if CRB_STATS
@@ -940,7 +961,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     // last warp does it before joining the work queue below
     if (warp == NW - 1) {
         const int c = lane;
-        const bool on = (MODE == MODE_TO) ? (c == H - 1) : (c < n_act);
+        const bool on = (MODE == MODE_TO) ? (base + c == H - 1) : (c < n_act);
         float ft[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, C = 0.f;
         if (on && (cf.flags & F_CSPACE)) {
             // Eq. cspace-cost: C = a4 logcosh(a5 |theta_g - theta_T|^2); its joint-space gradient
@@ -989,10 +1010,10 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         float cb = 0.f, cs = 0.f;
 #pragma unroll kColdUnroll
         for (int d = 0; d < D; ++d) { cb += s.cbb[d * NC + c]; cs += s.csm[d * NC + c]; }
-        const bool valid = c < n_act;
-        s.cfg_terms[0 * NC + c] = valid ? C : 0.f;
-        s.cfg_terms[1 * NC + c] = valid ? cb : 0.f;
-        s.cfg_terms[2 * NC + c] = valid ? cs : 0.f;
+        const bool valid = own_l;   // (the terms add up over the timestep windows)
+        s.cfg_terms[0 * NC + c] = (valid ? C : 0.f) + (win ? s.cfg_terms[0 * NC + c] : 0.f);
+        s.cfg_terms[1 * NC + c] = (valid ? cb : 0.f) + (win ? s.cfg_terms[1 * NC + c] : 0.f);
+        s.cfg_terms[2 * NC + c] = (valid ? cs : 0.f) + (win ? s.cfg_terms[2 * NC + c] : 0.f);
     }
 
     // ---- a4 + a5/a6: self-collision and world collision as ONE dynamic work queue.  Items are the
@@ -1020,8 +1041,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         const bool sweepf = to && (cf.flags & F_SWEEP);
         const bool speedf = to && (cf.flags & F_SPEED);
         const float4 *sph = reinterpret_cast<const float4 *>(s.fw + rp.o_sph);
-        const bool hasp = to && lane > 0 && lane < H;
-        const bool hasn = to && lane + 1 < H;
+        const bool hasp = to && lane > 0 && base + lane < H;
+        const bool hasn = to && base + lane + 1 < H && lane + 1 < NC;
         const int nwg = (rp.M + 3) >> 2, nitems = nwg + (MODE == MODE_IK ? rp.NB_ik : rp.NB);
         int *qctr = reinterpret_cast<int *>(s.scal + 4);
 #if CRB_STATS
@@ -1115,7 +1136,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                 const float4 c = pc[0];
                                 const float rpr = sph[m].w + cf.eta;
                                 float maxb2;
-                                const bool hp = to && src > 0 && src < H, hn = to && src + 1 < H;
+                                const bool hp = to && src > 0 && base + src < H, hn = to && base + src + 1 < H && src + 1 < NC;
                                 const int dr = sweep_dirs(hp ? pc[-1] : c, hn ? pc[1] : c, c.x, c.y, c.z, rpr, hp, hn,
                                                           sweepf, maxb2);
                                 box_slow(s.sg + m * NC + src, pc, s.boxes, k, c.x, c.y, c.z, box_screen(c.x, c.y, c.z, b),
@@ -1428,7 +1449,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 if (CRB_SELF_CULL_DEV && B.z != 0xffffffffu) {
                     const float4 pa = s.sw[(B.z & 0xffff) * NC + lane], pb = s.sw[(B.z >> 16) * NC + lane];
                     const float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
-                    if (!__any_sync(FULL, !(dx * dx + dy * dy + dz * dz >= __uint_as_float(B.w)) && lane < n_act)) continue;
+                    if (!__any_sync(FULL, !(dx * dx + dy * dy + dz * dz >= __uint_as_float(B.w)) && own_l)) continue;
                 }
                 const int ia = B.x & 0x1ff, na = ((B.x >> 9) & 3) + 1, jb = (B.x >> 11) & 0x1ff,
                           len = (B.x >> 20) & 0x1ff;
@@ -1538,13 +1559,13 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             gj[0] += b * ux; gj[1] += b * uy; gj[2] += b * uz;
             cself = b * bp;
         }
-        s.cfg_terms[3 * NC + c] = c < n_act ? cself : 0.f;
+        s.cfg_terms[3 * NC + c] = (own_l ? cself : 0.f) + (win ? s.cfg_terms[3 * NC + c] : 0.f);
     } else if (warp == 1) {
         const int c = lane;
         float cw = 0.f;
 #pragma unroll kColdUnroll
         for (int q = 0; q < ((rp.M + 3) >> 2); ++q) cw += s.sg[(q << 2) * NC + c].w;   // fixed order
-        s.cfg_terms[4 * NC + c] = c < n_act ? cw : 0.f;
+        s.cfg_terms[4 * NC + c] = (own_l ? cw : 0.f) + (win ? s.cfg_terms[4 * NC + c] : 0.f);
     }
     __syncthreads();
     CRB_PHASE(4);
@@ -1562,7 +1583,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     }
     if (!grad) {          // cost-only pass (particle warm-up, f1): no backward
         __syncthreads();
-        return;
+        continue;
     }
 
     // ---- a9: backward to joint space (Alg. 8 / Table 7 as subtree sums):
@@ -1632,10 +1653,14 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         } else {
             g = kx * F0 + ky * F1 + kz * F2;
         }
-        s.gq[idx] = (c < n_act) ? g + s.gxd[idx] : 0.f;
+        const int sl = base + c;
+        const bool own = sl >= olo && sl < ohi;
+        if (own || nwin == 1) s.gq[d * HS + sl] = own ? g + s.gxd[idx] : 0.f;   // slot-indexed [D][HS]
     }
     __syncthreads();
     CRB_PHASE(6);
+    }   // timestep windows
+    if (!grad) return;
 
     // ---- transposed stencil + transposed state map (O2/O3 gradient routing) -> dC/dV
     if (MODE == MODE_TO) {
@@ -1647,8 +1672,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         // makes one lane per dof loop over six states while the others wait
         for (int idx = tid; idx < D * (H - 1); idx += NT) {
             const int d = idx / (H - 1), xi = idx - d * (H - 1) + 4;
-            const float *gv = s.gva + d * NC - 1, *ga = gv + D * NC, *gj = ga + D * NC;   // [hp] for hp = 1..H
-            float gx = (xi >= 1 && xi <= H) ? s.gq[d * NC + xi - 1] : 0.f;
+            const float *gv = s.gva + d * HS - 1, *ga = gv + D * HS, *gj = ga + D * HS;   // [hp] for hp = 1..H
+            float gx = (xi >= 1 && xi <= H) ? s.gq[d * HS + xi - 1] : 0.f;
             // x_xi enters the stencil of hp = xi - o with the coefficient of offset o
             if (xi + 2 <= H) { const int e = xi + 2; gx += iv * gv[e] - ia * ga[e] - ij * gj[e]; }             // o = -2
             if (xi + 1 >= 1 && xi + 1 <= H) { const int e = xi + 1; gx += -8.f * iv * gv[e] + 16.f * ia * ga[e] + 2.f * ij * gj[e]; }  // o = -1
@@ -1661,8 +1686,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         // (2) the transposed state map: a free variable takes its state, V_{H-1} the sum of the
         // aliased states x_{H-3..H} and the pads x_{H+1}, x_{H+2} (in that order), the rest 0
         float gdp = 0.f;
-        for (int idx = tid; idx < D * NC; idx += NT) {
-            const int d = idx / NC, h = idx - d * NC;   // V_h <-> x_{h+1}
+        for (int idx = tid; idx < D * HS; idx += NT) {
+            const int d = idx / HS, h = idx - d * HS;   // V_h <-> x_{h+1}
             if (h >= H) continue;
             const int hx = h + 1;
             int xlo, xhi;

@@ -241,7 +241,7 @@ static __device__ __noinline__ void trace_ik(const KParams &kp, int phase, size_
 // ------------------------------------------------------------------------------------------
 // persistent TO solver: one CTA per (problem, seed)
 // ------------------------------------------------------------------------------------------
-template <bool WMMA>
+template <bool WMMA, bool LONG>
 __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int unit = blockIdx.x;
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             __syncthreads();
         }
         // ---- a2..a10: one evaluation pass (cost only for particles)
-        eval_pass<MODE_TO, WMMA>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr, !part);
+        eval_pass<MODE_TO, WMMA, LONG>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr, !part);
         if (part) {
             // ---- f1 UPDATE, streamed over the particles of a chunk (Eqs. particle_1/2, B6), the
             // chunks merged in order (chunk_merge; totals in cg, unused during the warm-up)
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
 // winner's gradient from the owners' shared memory (DSMEM), so every step is bitwise the
 // sequential kernel's.  The particle warm-up and pass 0 run redundantly in every CTA.
 // ------------------------------------------------------------------------------------------
-template <bool WMMA>
+template <bool WMMA, bool LONG>
 __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     namespace cg = cooperative_groups;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
             }
             __syncthreads();
         }
-        eval_pass<MODE_TO, WMMA>(kp, smem, thA, K, H, lpass > 0 ? dd : nullptr, !part);
+        eval_pass<MODE_TO, WMMA, LONG>(kp, smem, thA, K, H, lpass > 0 ? dd : nullptr, !part);
         if (part) {
             float r;
             const float w = pacc.add(s.scal[0], kp.p_inv_beta, r);
@@ -1194,7 +1194,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
 // ------------------------------------------------------------------------------------------
 // one-shot evaluation, FK, selection
 // ------------------------------------------------------------------------------------------
-template <bool WMMA>
+template <bool WMMA, bool LONG>
 __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b = blockIdx.x;
@@ -1208,7 +1208,7 @@ __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ 
     stage_dt(kp, s, b);
     for (int i = t; i < N; i += NT) thA[i] = kp.q_in[(size_t)b * N + i];
     __syncthreads();
-    eval_pass<MODE_TO, WMMA>(kp, smem, thA, K, H, nullptr);
+    eval_pass<MODE_TO, WMMA, LONG>(kp, smem, thA, K, H, nullptr);
     if (t < 32) {
         float tr[5];
         for (int k = 0; k < 5; ++k) tr[k] = warp_sum(s.cfg_terms[k * NC + t]);
@@ -1713,7 +1713,8 @@ __global__ void __launch_bounds__(NT, 2) lbfgs_direction_kernel(int n, int count
 }  // namespace
 
 // the <WMMA = true> kernels, instantiated in CRB_PART 1 (no flush-to-zero)
-enum { KW_EVAL_TO, KW_EVAL_IK, KW_SOLVE_TO, KW_SOLVE_IK, KW_SOLVE_TO_CLUSTER, KW_SOLVE_IK_CLUSTER, KW_SOLVE_IK_PERSIST };
+enum { KW_EVAL_TO, KW_EVAL_IK, KW_SOLVE_TO, KW_SOLVE_IK, KW_SOLVE_TO_CLUSTER, KW_SOLVE_IK_CLUSTER, KW_SOLVE_IK_PERSIST,
+       KW_EVAL_TO_LONG, KW_SOLVE_TO_LONG, KW_SOLVE_TO_CLUSTER_LONG };
 const void *crb_wmma_kernel(int k);
 
 #if CRB_STATS
@@ -1735,12 +1736,15 @@ int crb_wmma_stats(unsigned long long *out, int reset) { return stats_copy(out, 
 #endif
 const void *crb_wmma_kernel(int k) {
     switch (k) {
-    case KW_EVAL_TO: return (const void *)eval_to_kernel<true>;
+    case KW_EVAL_TO: return (const void *)eval_to_kernel<true, false>;
+    case KW_EVAL_TO_LONG: return (const void *)eval_to_kernel<true, true>;
     case KW_EVAL_IK: return (const void *)eval_ik_kernel<true>;
-    case KW_SOLVE_TO: return (const void *)solve_to_kernel<true>;
+    case KW_SOLVE_TO: return (const void *)solve_to_kernel<true, false>;
+    case KW_SOLVE_TO_LONG: return (const void *)solve_to_kernel<true, true>;
     case KW_SOLVE_IK: return (const void *)solve_ik_kernel<true, false>;
     case KW_SOLVE_IK_PERSIST: return (const void *)solve_ik_kernel<true, true>;
-    case KW_SOLVE_TO_CLUSTER: return (const void *)solve_to_cluster_kernel<true>;
+    case KW_SOLVE_TO_CLUSTER: return (const void *)solve_to_cluster_kernel<true, false>;
+    case KW_SOLVE_TO_CLUSTER_LONG: return (const void *)solve_to_cluster_kernel<true, true>;
     case KW_SOLVE_IK_CLUSTER: return (const void *)solve_ik_cluster_kernel<true>;
     }
     return nullptr;
@@ -1848,8 +1852,9 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.cbb = take(D * NC);
     L.csm = take(D * NC);
     L.gxd = take(D * NC);
-    L.gq = take(D * NC);
-    L.gva = take(mode == MODE_TO ? 3 * D * NC : 4);
+    L.HS = mode == MODE_TO ? ((std::max(H, 1) + NC - 1) / NC) * NC : NC;   // slot stride (timestep windows)
+    L.gq = take(D * L.HS);
+    L.gva = take(mode == MODE_TO ? 3 * D * L.HS : 4);
     L.pose_ft = take(6 * NC);
     L.tdp = take(12);
     L.goal = take(std::max(7, D) * NC);   // pose [7][32] or joint-space goal [D][32] (CRB_CSPACE)
@@ -2495,8 +2500,8 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
     if ((st = ready(ctx, true)) != CRB_OK) return st;
     if (B < 0 || (B > 0 && (!q || !goal || !cost))) return fail(ctx, CRB_E_ARG, "bad evaluate arguments");
     const int mode = H == 1 ? MODE_IK : MODE_TO;
-    if (mode == MODE_TO && (H < 8 || H > 32 || H * ctx->rp.D > 512 || (B > 0 && !start)))
-        return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 32, H*D <= 512 and start");
+    if (mode == MODE_TO && (H < 8 || H > 64 || H * ctx->rp.D > 512 || (B > 0 && !start)))
+        return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 64, H*D <= 512 and start");
     KParams kp = base_params(ctx);
     kp.B = B; kp.H = H; kp.cp.H = H; kp.mode = mode; kp.q_in = q; kp.env = env; kp.start = start; kp.goal = goal;
     kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs; kp.dt_arr = dt;
@@ -2506,7 +2511,8 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
     const bool wm = use_world_mma(ctx);
     if (mode == MODE_TO)
-        return launch_fn(ctx, wm ? crb_wmma_kernel(KW_EVAL_TO) : (const void *)eval_to_kernel<false>, B, bytes,
+        return launch_fn(ctx, H > NC ? (wm ? crb_wmma_kernel(KW_EVAL_TO_LONG) : (const void *)eval_to_kernel<false, true>)
+                                     : (wm ? crb_wmma_kernel(KW_EVAL_TO) : (const void *)eval_to_kernel<false, false>), B, bytes,
                          (cudaStream_t)stream, kp,
                       "eval_to_kernel");
     return launch_fn(ctx, wm ? crb_wmma_kernel(KW_EVAL_IK) : (const void *)eval_ik_kernel<false>, (B + NC - 1) / NC, bytes,
@@ -2541,8 +2547,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
         return fail(ctx, CRB_E_ARG, "trace: 0 <= n_trace <= 8");
     const int mode = H == 1 ? MODE_IK : MODE_TO;
     const int D = ctx->rp.D;
-    if (mode == MODE_TO && (H < 8 || H > 32 || H * D > 512 || (P > 0 && !start)))
-        return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 32, H*D <= 512 and start");
+    if (mode == MODE_TO && (H < 8 || H > 64 || H * D > 512 || (P > 0 && !start)))
+        return fail(ctx, H < 8 ? CRB_E_SHAPE : CRB_E_LIMIT, "TO mode needs 8 <= H <= 64, H*D <= 512 and start");
     if (P == 0) return CRB_OK;   // empty batch: validated, nothing launched
     const int N = H * D;
     cudaStream_t stream_ = (cudaStream_t)stream;
@@ -2582,7 +2588,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
                       (sp->cluster == 1 || (sp->cluster == -1 && (fits || parts || waves)));
     if (clus && units > 0) {
         const void *kern = mode == MODE_TO
-                               ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_CLUSTER) : (const void *)solve_to_cluster_kernel<false>)
+                               ? (H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_CLUSTER_LONG) : (const void *)solve_to_cluster_kernel<false, true>)
+                                         : (wm ? crb_wmma_kernel(KW_SOLVE_TO_CLUSTER) : (const void *)solve_to_cluster_kernel<false, false>))
                                : (wm ? crb_wmma_kernel(KW_SOLVE_IK_CLUSTER) : (const void *)solve_ik_cluster_kernel<false>);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         if (e != cudaSuccess) return cuda_check(ctx, e, "solve_cluster_kernel");
@@ -2604,7 +2611,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
         if (e != cudaSuccess) return cuda_check(ctx, e, "solve_cluster_kernel");
         st = cuda_check(ctx, cudaGetLastError(), "solve_cluster_kernel");
     } else if (mode == MODE_TO)
-        st = launch_fn(ctx, wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false>, P * S, bytes, stream_,
+        st = launch_fn(ctx, H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true>)
+                                   : (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false>), P * S, bytes, stream_,
                        kp, "solve_to_kernel");
     else {
         // IK scheduling: the persistent chunked kernel when the batch
@@ -2700,7 +2708,8 @@ crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, i
     if (bytes > SMEM_MAX) { if (ctas_per_sm) *ctas_per_sm = 0; return CRB_OK; }
     int n = 0;
     const bool wm = use_world_mma(ctx);
-    const void *fn = mode == MODE_TO ? (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false>)
+    const void *fn = mode == MODE_TO ? (H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true>)
+                                                : (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false>))
                                      : (wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false, false>);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     st = cuda_check(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, NT, bytes), "occupancy");

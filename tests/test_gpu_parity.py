@@ -175,6 +175,13 @@ def franka_trajs(seed, B, H, noise=0.25):
     (16, 0, "random"),
     (13, inputs.SWEEP, "tabletop"),
     (8, inputs.SPEED | inputs.JERK, "random"),
+    # H > 32: timestep windows ([0, 31), then 30 owned per window, the last up to 31, one halo
+    # timestep each side): two windows at 33 / 44 / 62, three at 63 / 64 (P:2217 uses 44)
+    (33, inputs.SWEEP | inputs.SPEED, "random"),
+    (44, inputs.SWEEP | inputs.SPEED, "tabletop"),
+    (62, inputs.SPEED, "tabletop"),
+    (63, inputs.SWEEP | inputs.SPEED | inputs.JERK, "random"),
+    (64, inputs.SWEEP | inputs.SPEED | inputs.JERK, "random"),
 ])
 def test_eval_to_parity_franka(native, O, H, flags, scene):
     B = 96
@@ -896,4 +903,37 @@ def test_solve_ik_cluster_mode_bitwise(native, O, particles):
     clu = ctx.solve(dataclasses.replace(sp, cluster=1), *args, **kw)
     for k in ("seed_best_cost", "seed_best_traj", "best_cost", "best_traj", "best_key"):
         assert torch.equal(seq[k], clu[k]), k
+    ctx.close()
+
+
+def test_solve_to_long_horizon(native, O):
+    """H = 44 (the paper's long-horizon scene) through the solver: repeatable, every seed's
+    best no worse than its start and equal to the evaluation of its best trajectory, and the
+    latency-mode cluster kernel bitwise equal to the sequential one."""
+    H, P, S = 44, 3, 4
+    rb, starts, goals_cfg, trajs = franka_trajs(4444, P * S, H)
+    worlds = [inputs.tabletop_scene(3, e, 20) for e in range(P)]
+    cp = inputs.CostParams(dt=0.25)
+    ctx = make(native, rb, worlds, cp)
+    R = O.Robot(rb)
+    gl = f32(np.array([O.fk(R, q)[2] for q in goals_cfg[::S]]))
+    st = f32(starts[::S])
+    V = f32(trajs).reshape(P, S, H, 7)
+    V[:, :, 0] = st[:, None]
+    env = np.arange(P, dtype=np.int32)
+    sp = inputs.SolverParams(iters=20)
+    kw = dict(start=T(st), env=T(env, torch.int32), seed_outputs=True)
+    seq = [ctx.solve(dataclasses.replace(sp, cluster=0), T(V), T(gl), **kw) for _ in range(2)]
+    clu = ctx.solve(dataclasses.replace(sp, cluster=1), T(V), T(gl), **kw)
+    for k in seq[0]:
+        assert torch.equal(seq[0][k], seq[1][k]), k
+        assert torch.equal(seq[0][k], clu[k]), k
+    c0, _, _ = ctx.evaluate(T(V.reshape(P * S, H, 7)), T(np.repeat(gl, S, 0)), start=T(np.repeat(st, S, 0)),
+                            env=T(np.repeat(env, S), torch.int32))
+    sbc = seq[0]["seed_best_cost"].cpu().numpy().reshape(-1)
+    assert np.all(np.isfinite(sbc)) and np.all(sbc <= c0.cpu().numpy() * (1 + 1e-6))
+    sbt = seq[0]["seed_best_traj"].reshape(P * S, H, 7)
+    cb, _, _ = ctx.evaluate(sbt, T(np.repeat(gl, S, 0)), start=T(np.repeat(st, S, 0)),
+                            env=T(np.repeat(env, S), torch.int32))
+    np.testing.assert_allclose(cb.cpu().numpy(), sbc, rtol=1e-6)
     ctx.close()
