@@ -172,14 +172,17 @@ typedef struct {
     float *trace;
     int n_trace;               /* 0..8                                                            */
     int trace_iter[8];
-    /* IK scheduling (H = 1; ignored for TO and in cluster mode).  -1 (default): automatic -- a
+    /* Scheduling (ignored in cluster mode).  IK: -1 (default): automatic -- a
      * persistent kernel of one wave of CTAs takes (seed group, iteration chunk) work units from a
      * global counter when the batch has at least two waves of 32-seed groups (4 chunks of
      * iters / 4 iterations; the solver state of a group moves through a context-owned device
      * buffer between its chunks, so the last wave is not left to a few long CTAs); when every
      * problem uses the same environment the groups are 32 consecutive seeds of the flat P x S
      * batch (no idle lanes when S % 32 != 0).  0: one CTA per 32-seed group of a problem.  k >= 1:
-     * the persistent kernel with k chunks.  Every seed's result is bitwise the same in all modes. */
+     * the persistent kernel with k chunks.  TO: the same persistent kernel over (seed, iteration
+     * chunk) units (one CTA per seed trajectory otherwise); automatic when the seeds span >= 2
+     * waves and the last wave is less than 95 % predicted-full (e.g. 1536 seeds on 296 CTA slots);
+     * 0 off, k >= 1 k chunks.  Every seed's result is bitwise the same in all modes. */
     int persist;
 } crb_solver_params;
 

@@ -241,13 +241,9 @@ static __device__ __noinline__ void trace_ik(const KParams &kp, int phase, size_
 // ------------------------------------------------------------------------------------------
 // persistent TO solver: one CTA per (problem, seed)
 // ------------------------------------------------------------------------------------------
-template <bool WMMA, bool LONG>
+template <bool WMMA, bool LONG, bool PERSIST>
 __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
-    const int unit = blockIdx.x;
-    const int p = unit / kp.S;
-    const int env = kp.env ? kp.env[p] : 0;
-    const int K = stage_tables(kp, smem, env);
     const Smem s = make_smem(kp, smem);
     const int D = kp.rp.D, H = kp.H, N = H * D, Np = (N + 3) & ~3, m = kp.m, A = kp.A;
     const int t = threadIdx.x;
@@ -260,42 +256,88 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
     int *ring = reinterpret_cast<int *>(scal + 24);   // [0] count, [1] free slot
     const float *lim = s.fw + kp.rp.o_lim;
     int ph = 0;
-
+    // Work units: one seed trajectory per CTA and all iterations, or
+    // (kp.ik_chunks = C > 0, persistent launch of one wave) units (seed, iteration chunk) in
+    // chunk-major order from a global counter, the solver state crossing global memory between a
+    // seed's chunks as in the persistent IK kernel.  Every seed's arithmetic is the same (bitwise).
+    const int C = PERSIST ? kp.ik_chunks : 1;
+    const int NU = kp.P * kp.S;
+    // saved per seed: th, g, dd, thp, gp, best (6 Np) | Sb .. order (2 (m + 1) Np + 160) | ring,
+    // c, cbest, chunk_best, done
+    const int SWA = 6 * Np, SWB = 2 * (m + 1) * Np + 160, SWT = SWA + SWB + 8;
+    int *bcast = reinterpret_cast<int *>(smem + kp.lay.mbar) + 3;
+    int staged = -0x7fffffff, K = 0;
+    int unit = blockIdx.x;
+    if (PERSIST) {
+        if (t == 0) *bcast = atomicAdd(kp.ik_flags, 1);
+        __syncthreads();
+        unit = *bcast;
+    }
+    while (unit < NU * C) {
+    const int ch = PERSIST ? unit / NU : 0, u = unit - ch * NU;
+    const int p = u / kp.S;
+    {
+        const int env = kp.env ? kp.env[p] : 0;
+        if (staged == -0x7fffffff) K = stage_tables(kp, smem, env);
+        else if (env != staged) K = restage_world(kp, smem, env);
+        staged = env;
+    }
     if (t < D) s.st[t] = kp.start[p * D + t];
     if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[p * kp.cp.gw + t / NC];
     stage_dt(kp, s, p);
-    const float *seed = kp.q_in + (size_t)unit * N;
+    const float *seed = kp.q_in + (size_t)u * N;
     float lo_e[2], hi_e[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         const int i = t + e * NT;
         lo_e[e] = i < N ? lim[i % D] : 0.f;
         hi_e[e] = i < N ? lim[D + i % D] : 0.f;
-        if (i < N) { th[i] = seed[i]; thA[i] = seed[i]; }
+        if (ch == 0 && i < N) { th[i] = seed[i]; thA[i] = seed[i]; }
     }
-    if (t == 0) { ring[0] = 0; ring[1] = 0; }
-    __syncthreads();
-
     // One loop over evaluation passes with a single eval_pass call site: first the particle
     // warm-up (f1: pn_iters x pn cost-only passes, Alg. 5), then pass 0 evaluates Theta_0 (O8
     // initialise) and every iteration is an L-BFGS step followed by A candidate passes.
     // During the warm-up th holds mu, g holds Theta_sigma, dd / thp the UPDATE sums S1 / S2.
     float c = 0.f, cbest = 0.f, g0d = 0.f, chunk_best = 0.f;
+    int done = 0;
     float d_e[2] = {0.f, 0.f};
     const int npart = kp.pn_iters * kp.pn;
-    const int npass = npart + 1 + kp.iters * A;
-    const unsigned pk1 = (unsigned)(kp.prob_base + p), psd = (unsigned)(kp.seed_base + (unit - p * kp.S));
+    const int it_lo = (int)((long long)ch * kp.iters / C), it_hi = (int)((long long)(ch + 1) * kp.iters / C);
+    const int pass_lo = ch == 0 ? 0 : npart + 1 + it_lo * A, pass_hi = npart + 1 + it_hi * A;
+    if (ch == 0) {
+        if (t == 0) { ring[0] = 0; ring[1] = 0; }
+        __syncthreads();
+    } else {   // (u, ch - 1) has saved the seed's state
+        if (t == 0) {
+            int *flag = kp.ik_flags + 2 + u;
+            int v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+                if (v >= ch) break;
+                __nanosleep(256);
+            }
+        }
+        __syncthreads();
+        const float *src = kp.ik_state + (size_t)u * SWT;
+        for (int i = t; i < SWA; i += NT) base[i] = __ldcg(src + i);
+        for (int i = t; i < SWB; i += NT) Sb[i] = __ldcg(src + SWA + i);
+        const float *sc = src + SWA + SWB;
+        if (t < 2) ring[t] = __float_as_int(__ldcg(sc + t));
+        c = __ldcg(sc + 2); cbest = __ldcg(sc + 3); chunk_best = __ldcg(sc + 4); done = __float_as_int(__ldcg(sc + 5));
+        __syncthreads();
+    }
+    const unsigned pk1 = (unsigned)(kp.prob_base + p), psd = (unsigned)(kp.seed_base + (u - p * kp.S));
     ParticleAcc pacc;
     pacc.reset();
     float tm = -INFINITY, tZ = 0.f;   // merged particle chunks of the current warm-up iteration
-    if (npart > 0) {
+    if (ch == 0 && npart > 0) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const int i = t + e * NT;
             if (i < N) { const float s0 = kp.s0_frac * (hi_e[e] - lo_e[e]); g[i] = s0 * s0; }   // B8
         }
     }
-    for (int pass = 0; pass < npass; ++pass) {
+    for (int pass = pass_lo; pass < (done ? pass_lo : pass_hi); ++pass) {
         const bool part = pass < npart;
         const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
         const int lpass = pass - npart;
@@ -315,10 +357,10 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
         if (a == 0) {
             const int it = (lpass - 1) / A;
             const int tj = trace_slot(kp, it);
-            if (tj >= 0) trace_to(kp, 0, unit, it, tj, c, 0.f, 0.f, 0, 0.f);
+            if (tj >= 0) trace_to(kp, 0, u, it, tj, c, 0.f, 0.f, 0, 0.f);
             float sy;
             g0d = lbfgs_step_to(it, N, Np, m, th, g, thp, gp, dd, Sb, Yb, rho, syv, yyv, order, ring, s.red, ph, d_e, sy);
-            if (tj >= 0) trace_to(kp, 1, unit, it, tj, c, g0d, sy, 0, 0.f);
+            if (tj >= 0) trace_to(kp, 1, u, it, tj, c, g0d, sy, 0, 0.f);
         }
         // ---- a1: candidate a = clip(theta + alpha_a d) (pass 0: theta_0 is already in thA)
         if (a >= 0) {
@@ -424,25 +466,49 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             }
             if (kp.trace) {
                 const int tj = trace_slot(kp, (lpass - 1) / A);
-                if (tj >= 0) trace_to(kp, 2, unit, 0, tj, c, 0.f, 0.f, istar, cbest);
+                if (tj >= 0) trace_to(kp, 2, u, 0, tj, c, 0.f, 0.f, istar, cbest);
             }
             // ---- a14: "up to" iters in chunks (B20): every thread holds the same cbest, so the
             // exit is CTA-uniform
             if (kp.check_every > 0) {
                 const int it = (lpass - 1) / A + 1;   // iterations done
                 if (it % kp.check_every == 0) {
-                    if (!(cbest < chunk_best - kp.conv_rtol * fabsf(chunk_best))) break;
+                    if (!(cbest < chunk_best - kp.conv_rtol * fabsf(chunk_best))) { done = 1; break; }
                     chunk_best = cbest;
                 }
             }
         }
     }
     __syncthreads();
-    if (t == 0) kp.seed_best_cost[unit] = cbest;
+    if (ch == C - 1) {
+        if (t == 0) kp.seed_best_cost[u] = cbest;
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const int i = t + e * NT;
-        if (i < N) kp.seed_best_traj[(size_t)unit * N + i] = best[i];
+        for (int e = 0; e < 2; ++e) {
+            const int i = t + e * NT;
+            if (i < N) kp.seed_best_traj[(size_t)u * N + i] = best[i];
+        }
+    } else {   // save the seed's state for (u, ch + 1), then publish the chunk
+        float *dst = kp.ik_state + (size_t)u * SWT;
+        for (int i = t; i < SWA; i += NT) __stcg(dst + i, base[i]);
+        for (int i = t; i < SWB; i += NT) __stcg(dst + SWA + i, Sb[i]);
+        if (t == 0) {
+            float *sc = dst + SWA + SWB;
+            __stcg(sc, __int_as_float(ring[0])); __stcg(sc + 1, __int_as_float(ring[1]));
+            __stcg(sc + 2, c); __stcg(sc + 3, cbest); __stcg(sc + 4, chunk_best); __stcg(sc + 5, __int_as_float(done));
+        }
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            int *flag = kp.ik_flags + 2 + u;
+            const int v = ch + 1;
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+        }
+    }
+    if (!PERSIST) break;
+    if (t == 0) *bcast = atomicAdd(kp.ik_flags, 1);
+    __syncthreads();
+    unit = *bcast;
+    __syncthreads();   // every thread has read the unit before thread 0 may overwrite it
     }
 }
 
@@ -1714,7 +1780,7 @@ __global__ void __launch_bounds__(NT, 2) lbfgs_direction_kernel(int n, int count
 
 // the <WMMA = true> kernels, instantiated in CRB_PART 1 (no flush-to-zero)
 enum { KW_EVAL_TO, KW_EVAL_IK, KW_SOLVE_TO, KW_SOLVE_IK, KW_SOLVE_TO_CLUSTER, KW_SOLVE_IK_CLUSTER, KW_SOLVE_IK_PERSIST,
-       KW_EVAL_TO_LONG, KW_SOLVE_TO_LONG, KW_SOLVE_TO_CLUSTER_LONG };
+       KW_EVAL_TO_LONG, KW_SOLVE_TO_LONG, KW_SOLVE_TO_CLUSTER_LONG, KW_SOLVE_TO_PERSIST, KW_SOLVE_TO_LONG_PERSIST };
 const void *crb_wmma_kernel(int k);
 
 #if CRB_STATS
@@ -1739,8 +1805,10 @@ const void *crb_wmma_kernel(int k) {
     case KW_EVAL_TO: return (const void *)eval_to_kernel<true, false>;
     case KW_EVAL_TO_LONG: return (const void *)eval_to_kernel<true, true>;
     case KW_EVAL_IK: return (const void *)eval_ik_kernel<true>;
-    case KW_SOLVE_TO: return (const void *)solve_to_kernel<true, false>;
-    case KW_SOLVE_TO_LONG: return (const void *)solve_to_kernel<true, true>;
+    case KW_SOLVE_TO: return (const void *)solve_to_kernel<true, false, false>;
+    case KW_SOLVE_TO_LONG: return (const void *)solve_to_kernel<true, true, false>;
+    case KW_SOLVE_TO_PERSIST: return (const void *)solve_to_kernel<true, false, true>;
+    case KW_SOLVE_TO_LONG_PERSIST: return (const void *)solve_to_kernel<true, true, true>;
     case KW_SOLVE_IK: return (const void *)solve_ik_kernel<true, false>;
     case KW_SOLVE_IK_PERSIST: return (const void *)solve_ik_kernel<true, true>;
     case KW_SOLVE_TO_CLUSTER: return (const void *)solve_to_cluster_kernel<true, false>;
@@ -2610,10 +2678,44 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
         ctx->launches++;
         if (e != cudaSuccess) return cuda_check(ctx, e, "solve_cluster_kernel");
         st = cuda_check(ctx, cudaGetLastError(), "solve_cluster_kernel");
-    } else if (mode == MODE_TO)
-        st = launch_fn(ctx, H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true>)
-                                   : (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false>), P * S, bytes, stream_,
-                       kp, "solve_to_kernel");
+    } else if (mode == MODE_TO) {
+        // TO scheduling: the persistent chunked kernel when the seed
+        // trajectories span >= 2 waves and the last one is poorly filled (predicted one-CTA-per-
+        // seed efficiency < 95 %), 4 iteration chunks; sp->persist = 0 forces one CTA per seed,
+        // k >= 1 k chunks.
+        const void *kern = H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true, false>)
+                                  : (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false, false>);
+        const void *kern_p = H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG_PERSIST) : (const void *)solve_to_kernel<false, true, true>)
+                                    : (wm ? crb_wmma_kernel(KW_SOLVE_TO_PERSIST) : (const void *)solve_to_kernel<false, false, true>);
+        const long long NU = (long long)P * S;
+        int chunks = sp->persist;
+        int per_sm = 0;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes);
+        if (e != cudaSuccess || per_sm < 1) return cuda_check(ctx, e != cudaSuccess ? e : cudaErrorInvalidConfiguration, "occupancy");
+        const long long Wr = (long long)per_sm * ctx->sm_count;
+        if (chunks < 0) {
+            const double waves = (double)NU / (double)Wr;
+            chunks = (NU >= 2 * Wr && waves / std::ceil(waves) < 0.95 && sp->iters >= 8 && !kp.trace) ? 4 : 0;
+        }
+        chunks = std::min(chunks, std::max(sp->iters, 1));
+        if (chunks >= 1) {
+            const int m = sp->history, Np = (N + 3) & ~3;
+            const size_t swt = (size_t)6 * Np + (size_t)2 * (m + 1) * Np + 160 + 8;
+            if ((st = grow(ctx, &ctx->ws_ik_state, &ctx->cap_ik_state, (size_t)NU * swt)) != CRB_OK) return st;
+            if ((st = grow(ctx, &ctx->ws_ik_flags, &ctx->cap_ik_flags, (size_t)NU + 2)) != CRB_OK) return st;
+            kp.ik_state = ctx->ws_ik_state; kp.ik_flags = ctx->ws_ik_flags; kp.ik_chunks = chunks;
+            ik_persist_init_kernel<<<1, 256, 0, stream_>>>(nullptr, P, (int)NU, ctx->ws_ik_flags);
+            ctx->launches++;
+            if ((st = cuda_check(ctx, cudaGetLastError(), "ik_persist_init_kernel")) != CRB_OK) return st;
+            e = cudaFuncSetAttribute(kern_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+            if (e != cudaSuccess) return cuda_check(ctx, e, "solve_to_kernel (persistent)");
+            st = launch_fn(ctx, kern_p, (int)std::min<long long>(NU * chunks, Wr), bytes, stream_, kp,
+                           "solve_to_kernel (persistent)");
+        } else {
+            st = launch_fn(ctx, kern, P * S, bytes, stream_, kp, "solve_to_kernel");
+        }
+    }
     else {
         // IK scheduling: the persistent chunked kernel when the batch
         // spans at least two waves of groups (sp->persist = -1: 4 iteration chunks), else one
@@ -2708,8 +2810,8 @@ crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, i
     if (bytes > SMEM_MAX) { if (ctas_per_sm) *ctas_per_sm = 0; return CRB_OK; }
     int n = 0;
     const bool wm = use_world_mma(ctx);
-    const void *fn = mode == MODE_TO ? (H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true>)
-                                                : (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false>))
+    const void *fn = mode == MODE_TO ? (H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true, false>)
+                                                : (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false, false>))
                                      : (wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false, false>);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     st = cuda_check(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, NT, bytes), "occupancy");

@@ -1,0 +1,62 @@
+"""GPU: the persistent chunked TO schedule (crb_solver_params.persist)
+against one CTA per seed trajectory: every output bitwise identical -- several environments
+(re-staged per unit), 1 to 5 iteration chunks (the seed's solver state crosses global memory
+between chunks), the particle warm-up in chunk 0, the chunked convergence exit (a seed that
+stopped stays stopped in later chunks), the solver trace, and H = 44 (timestep windows)."""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2310_17274_b200 import inputs, workload
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+KEYS = ("seed_best_cost", "seed_best_traj", "best_cost", "best_traj", "best_key")
+
+
+def T(x, dtype=torch.float32):
+    return torch.tensor(np.ascontiguousarray(x), dtype=dtype, device=DEV)
+
+
+@pytest.fixture(scope="module")
+def native():
+    from paper_2310_17274_b200 import native as N
+    return N
+
+
+def _solve_all(native, wl, sp, variants, **extra):
+    ctx = native.Context(0)
+    ctx.set_robot(wl.robot)
+    ctx.set_world(wl.worlds)
+    ctx.set_cost_params(wl.cost)
+    args = (T(wl.seeds), T(wl.goal))
+    kw = dict(start=T(wl.start), env=T(wl.env, torch.int32), seed_outputs=True, **extra)
+    outs = [ctx.solve(dataclasses.replace(sp, cluster=0, persist=v), *args, **kw) for v in variants]
+    ctx.close()
+    return outs
+
+
+@pytest.mark.parametrize("particles,check_every", [(0, 0), (2, 0), (0, 4)])
+def test_persistent_to_bitwise(native, particles, check_every):
+    wl = workload.franka_to(0, list(range(5)), S=7, H=32, iters=17)
+    sp = dataclasses.replace(wl.solver, particle_iters=particles, n_particles=8, check_every=check_every,
+                             conv_rtol=0.05 if check_every else 0.0)
+    outs = _solve_all(native, wl, sp, [0, 1, 2, 5])
+    assert torch.isfinite(outs[0]["seed_best_cost"]).all()
+    for o in outs[1:]:
+        for k in KEYS:
+            assert torch.equal(outs[0][k], o[k]), k
+
+
+def test_persistent_to_trace_and_long_horizon(native):
+    wl = workload.franka_to(0, list(range(3)), S=4, H=32, iters=12)
+    sp = wl.solver
+    outs = _solve_all(native, wl, sp, [0, 3], trace_iters=(0, 5, 11))
+    for k in KEYS + ("trace",):
+        assert torch.equal(outs[0][k], outs[1][k]), k
+    wl44 = workload.franka_to(0, list(range(3)), S=4, H=44, iters=9)
+    outs = _solve_all(native, wl44, wl44.solver, [0, 2])
+    for k in KEYS:
+        assert torch.equal(outs[0][k], outs[1][k]), ("H=44", k)
