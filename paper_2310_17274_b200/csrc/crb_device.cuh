@@ -66,6 +66,11 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #define CRB_COLD_UNROLL 2
 #endif
 
+// The compaction's r-th flagged slot by popc bisection (1) or __fns (0)
+#ifndef CRB_NTH_BIT
+#define CRB_NTH_BIT 1
+#endif
+
 // Self-collision screen tightened to the pairs that can still reach the lane's current best
 // penetration (1), or the plain d < R test throughout (0)
 #ifndef CRB_SELF_PRUNE
@@ -717,6 +722,21 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], 
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
 }
 
+// Position of the n-th (0-based) set bit of m (n < popc(m)): a 5-step popc bisection, branch-free
+// (__fns is a loop on this architecture)
+__device__ __forceinline__ int nth_set_bit(unsigned m, int n) {
+    int pos = 0;
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        const int c = __popc(m & ((1u << w) - 1u));
+        const bool hi = n >= c;
+        n = hi ? n - c : n;
+        pos = hi ? pos + w : pos;
+        m = hi ? m >> w : m;
+    }
+    return pos;
+}
+
 // order-preserving float <-> int map (for warp min / max with __reduce_{min,max}_sync); an involution
 __device__ __forceinline__ int f2o(float x) {
     const int i = __float_as_int(x);
@@ -1130,7 +1150,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                 int u = 0, r = e;
                                 if (r >= n0) { r -= n0; u = 1; if (r >= n1) { r -= n1; u = 2; if (r >= n2) { r -= n2; u = 3; } } }
                                 const unsigned bm = u == 0 ? bal[0] : u == 1 ? bal[1] : u == 2 ? bal[2] : bal[3];
-                                const int src = __fns(bm, 0, r + 1);          // the r-th flagged slot
+                                const int src = CRB_NTH_BIT ? nth_set_bit(bm, r) : __fns(bm, 0, r + 1);   // the r-th flagged slot
                                 const int m = m0 + u;
                                 const float4 *pc = s.sw + m * NC + src;
                                 const float4 c = pc[0];
