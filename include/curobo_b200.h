@@ -193,6 +193,10 @@ crb_status crb_create(int cuda_device, crb_ctx **out);
 crb_status crb_destroy(crb_ctx *ctx);
 const char *crb_last_error(const crb_ctx *ctx);
 const char *crb_version(void);
+/* ABI self-description for bindings: writes min(n, 5) struct sizes in bytes -- crb_link,
+ * crb_robot_desc, crb_cuboid, crb_cost_params, crb_solver_params -- into out (host) and returns
+ * 5.  A binding compares its mirrors against these before the first call. */
+int crb_abi_sizes(int *out, int n);
 
 /* Validate, pack (spheres grouped by link, disabled self pairs dropped, float4 layout P:3014)
  * and upload the robot tables. */

@@ -2013,7 +2013,14 @@ crb_status launch(crb_ctx *ctx, Kern k, int grid, size_t smem, cudaStream_t st, 
 
 extern "C" {
 
-const char *crb_version(void) { return "curobo_b200 0.1 (sm_100a)"; }
+const char *crb_version(void) { return "curobo_b200 0.2 (sm_100a)"; }
+
+int crb_abi_sizes(int *out, int n) {
+    const int v[5] = {(int)sizeof(crb_link), (int)sizeof(crb_robot_desc), (int)sizeof(crb_cuboid),
+                      (int)sizeof(crb_cost_params), (int)sizeof(crb_solver_params)};
+    for (int i = 0; i < 5 && i < n && out; ++i) out[i] = v[i];
+    return 5;
+}
 
 crb_status crb_create(int cuda_device, crb_ctx **out) {
     if (!out) return CRB_E_ARG;

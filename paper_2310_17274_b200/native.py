@@ -109,13 +109,29 @@ _lib.crb_interpolate.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, C.c_float, C
 _lib.crb_particle_normals.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_uint32, _V, _V]
 _lib.crb_launch_count.argtypes = [_V]
 _lib.crb_launch_count.restype = C.c_int64
+_lib.crb_abi_sizes.argtypes = [C.POINTER(C.c_int), C.c_int]
+_lib.crb_abi_sizes.restype = C.c_int
+
+
+def _check_abi():
+    """The ctypes mirrors must match the library's struct sizes (header drift fails loudly)."""
+    got = (C.c_int * 5)()
+    _lib.crb_abi_sizes(got, 5)
+    mine = [C.sizeof(crb_link), C.sizeof(crb_robot_desc), C.sizeof(crb_cuboid), C.sizeof(crb_cost_params),
+            C.sizeof(crb_solver_params)]
+    if list(got) != mine:
+        raise ImportError(f"libcurobo_b200 struct sizes {list(got)} != binding {mine}: rebuild or update native.py")
+
+
+_check_abi()
 
 SYMBOLS = ["crb_create", "crb_destroy", "crb_last_error", "crb_version", "crb_set_robot", "crb_set_world",
            "crb_set_cost_params", "crb_fk", "crb_evaluate_cost_grad", "crb_lbfgs_solve", "crb_lbfgs_solve_host",
            "crb_ls_select", "crb_argmin_keys", "crb_lbfgs_direction", "crb_launch_count", "crb_solver_occupancy",
            "crb_particle_normals", "crb_mask_samples", "crb_steer", "crb_evaluate_cost_grad_dt",
            "crb_lbfgs_solve_dt", "crb_retime", "crb_goal_error", "crb_ik_scores", "crb_to_scores",
-           "crb_rank_seeds", "crb_linear_seeds", "crb_gather_rows", "crb_trajectory_states", "crb_interpolate"]
+           "crb_rank_seeds", "crb_linear_seeds", "crb_gather_rows", "crb_trajectory_states", "crb_interpolate",
+           "crb_abi_sizes"]
 
 
 def _ptr(t):

@@ -38,6 +38,17 @@ def test_library_exports_every_declared_symbol(lib_path):
         assert re.search(rf"\bT {s}\b", nm), s
 
 
+def test_struct_sizes_match_the_binding(lib_path):
+    """crb_abi_sizes (sizeof of the five public structs in the library) against the ctypes mirrors;
+    the binding also checks this at import."""
+    from paper_2310_17274_b200 import native
+    got = (ctypes.c_int * 5)()
+    assert native._lib.crb_abi_sizes(got, 5) == 5
+    assert list(got) == [ctypes.sizeof(native.crb_link), ctypes.sizeof(native.crb_robot_desc),
+                         ctypes.sizeof(native.crb_cuboid), ctypes.sizeof(native.crb_cost_params),
+                         ctypes.sizeof(native.crb_solver_params)]
+
+
 def test_binding_lists_all_symbols(lib_path):
     from paper_2310_17274_b200 import native
     assert sorted(native.SYMBOLS) == declared_symbols()
