@@ -109,12 +109,15 @@ _lib.crb_interpolate.argtypes = [C.c_int, C.c_int, C.c_int, _V, _V, C.c_float, C
 _lib.crb_particle_normals.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_uint32, _V, _V]
 _lib.crb_launch_count.argtypes = [_V]
 _lib.crb_launch_count.restype = C.c_int64
-_lib.crb_abi_sizes.argtypes = [C.POINTER(C.c_int), C.c_int]
-_lib.crb_abi_sizes.restype = C.c_int
 
 
 def _check_abi():
-    """The ctypes mirrors must match the library's struct sizes (header drift fails loudly)."""
+    """The ctypes mirrors must match the library's struct sizes (header drift fails loudly).  A
+    CRB_LIB build older than crb_abi_sizes (tools/ab*.sh A/B runs) is not checked."""
+    if os.environ.get("CRB_LIB") and not hasattr(_lib, "crb_abi_sizes"):
+        return
+    _lib.crb_abi_sizes.argtypes = [C.POINTER(C.c_int), C.c_int]
+    _lib.crb_abi_sizes.restype = C.c_int
     got = (C.c_int * 5)()
     _lib.crb_abi_sizes(got, 5)
     mine = [C.sizeof(crb_link), C.sizeof(crb_robot_desc), C.sizeof(crb_cuboid), C.sizeof(crb_cost_params),
