@@ -71,6 +71,12 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #define CRB_NTH_BIT 1
 #endif
 
+// Sweep samples evaluated in the cuboid frame (affine interpolation of the endpoints' local
+// coordinates; world gradient only on hits) (1), or each sample transformed (0)
+#ifndef CRB_SWEEP_LOCAL
+#define CRB_SWEEP_LOCAL 1
+#endif
+
 // Self-collision screen tightened to the pairs that can still reach the lane's current best
 // penetration (1), or the plain d < R test throughout (0)
 #ifndef CRB_SELF_PRUNE
@@ -364,14 +370,13 @@ __device__ __forceinline__ void box_local(const BoxView &b, float px, float py, 
     lz = fmaf(b.c2.x, px, fmaf(b.c2.y, py, fmaf(b.c2.z, pz, b.c2.w)));
 }
 
-// Exact Euclidean box SDF (A4) + world-frame gradient at a point (hits and sweep samples).
-__device__ __forceinline__ float box_sdf_grad(const BoxView &b, float px, float py, float pz, float &gx,
-                                              float &gy, float &gz) {
-    float lx, ly, lz;
-    box_local(b, px, py, pz, lx, ly, lz);
+// Exact Euclidean box SDF (A4) at a point given in the cuboid frame, with the cuboid-frame gradient.
+__device__ __forceinline__ float box_sdf_local(const BoxView &b, float lx, float ly, float lz, float &glx, float &gly,
+                                               float &glz) {
     const float qx = fabsf(lx) - b.h.x, qy = fabsf(ly) - b.h.y, qz = fabsf(lz) - b.h.z;
     const float qm = fmaxf(qx, fmaxf(qy, qz));
-    float glx = 0.f, gly = 0.f, glz = 0.f, sd;
+    float sd;
+    glx = 0.f; gly = 0.f; glz = 0.f;
     if (qm > 0.f) {
         const float mx = fmaxf(qx, 0.f), my = fmaxf(qy, 0.f), mz = fmaxf(qz, 0.f);
         sd = sqrtf(mx * mx + my * my + mz * mz);
@@ -385,10 +390,24 @@ __device__ __forceinline__ float box_sdf_grad(const BoxView &b, float px, float 
         else if (qy >= qz) gly = ly >= 0.f ? 1.f : -1.f;
         else glz = lz >= 0.f ? 1.f : -1.f;
     }
-    // grad sd (world) = R grad_loc = sum_i grad_loc_i * col_i
+    return sd;
+}
+
+// grad sd (world) = R grad_loc = sum_i grad_loc_i * col_i
+__device__ __forceinline__ void box_grad_world(const BoxView &b, float glx, float gly, float glz, float &gx, float &gy,
+                                               float &gz) {
     gx = glx * b.c0.x + gly * b.c1.x + glz * b.c2.x;
     gy = glx * b.c0.y + gly * b.c1.y + glz * b.c2.y;
     gz = glx * b.c0.z + gly * b.c1.z + glz * b.c2.z;
+}
+
+// Exact Euclidean box SDF (A4) + world-frame gradient at a point (hits and sweep samples).
+__device__ __forceinline__ float box_sdf_grad(const BoxView &b, float px, float py, float pz, float &gx, float &gy,
+                                              float &gz) {
+    float lx, ly, lz, glx, gly, glz;
+    box_local(b, px, py, pz, lx, ly, lz);
+    const float sd = box_sdf_local(b, lx, ly, lz, glx, gly, glz);
+    box_grad_world(b, glx, gly, glz, gx, gy, gz);
     return sd;
 }
 
@@ -770,6 +789,10 @@ static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const
     }
     if (dirs) {
         const float J0 = (rp - sd0 > 0.f) ? rp : sd0;
+#if CRB_SWEEP_LOCAL
+        float lcx, lcy, lcz;
+        box_local(b, cx, cy, cz, lcx, lcy, lcz);
+#endif
 #pragma unroll 1
         for (int dir = 0; dir < 2; ++dir) {
             if (!(dirs & (1 << dir))) continue;
@@ -777,15 +800,30 @@ static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const
             const float vx = q.x - cx, vy = q.y - cy, vz = q.z - cz;
             const float L = sqrtf(vx * vx + vy * vy + vz * vz);
             const float iL = 1.f / L, bound = 0.5f * L;
+#if CRB_SWEEP_LOCAL
+            // samples in the cuboid frame: l(c + kappa v) = l(c) + kappa (l(q) - l(c)) (affine), and
+            // the world-frame gradient only for the samples that hit
+            float lqx, lqy, lqz;
+            box_local(b, q.x, q.y, q.z, lqx, lqy, lqz);
+            const float dlx = lqx - lcx, dly = lqy - lcy, dlz = lqz - lcz;
+#endif
             float j = J0;
             for (int st = 0; st < steps; ++st) {
                 if (j >= bound) break;
                 const float kap = j * iL;
-                const float px = fmaf(kap, vx, cx), py = fmaf(kap, vy, cy), pz = fmaf(kap, vz, cz);
                 float gx, gy, gz;
+#if CRB_SWEEP_LOCAL
+                float glx, gly, glz;
+                const float sd = box_sdf_local(b, fmaf(kap, dlx, lcx), fmaf(kap, dly, lcy), fmaf(kap, dlz, lcz), glx, gly, glz);
+#else
+                const float px = fmaf(kap, vx, cx), py = fmaf(kap, vy, cy), pz = fmaf(kap, vz, cz);
                 const float sd = box_sdf_grad(b, px, py, pz, gx, gy, gz);
+#endif
                 const float dp = rp - sd;
                 if (dp > 0.f) {
+#if CRB_SWEEP_LOCAL
+                    box_grad_world(b, glx, gly, glz, gx, gy, gz);
+#endif
                     float dphi;
                     E += activation(dp, eta, inv_eta, dphi);
                     const float f = (1.f - kap) * dphi;
