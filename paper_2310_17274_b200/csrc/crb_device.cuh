@@ -77,6 +77,12 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #define CRB_SWEEP_LOCAL 1
 #endif
 
+// World culling: a kept cuboid's AABB reaches the per-lane test by warp shuffles from the lane
+// that tested it (1) or is reloaded (0)
+#ifndef CRB_AB_SHFL
+#define CRB_AB_SHFL 1
+#endif
+
 // Self-collision screen tightened to the pairs that can still reach the lane's current best
 // penetration (1), or the plain d < R test throughout (0)
 #ifndef CRB_SELF_PRUNE
@@ -1322,18 +1328,26 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     const float4 *ab = kp.boxes_ab + (size_t)envc * kp.kmax * 2;
                     for (int kb = 0; kb < K; kb += 32) {
                         bool keep = false;
+                        float4 cl = make_float4(0.f, 0.f, 0.f, 0.f), el = cl;   // this lane's cuboid kb + lane
                         if (kb + lane < K) {
-                            const float4 c = __ldg(ab + 2 * (kb + lane)), e = __ldg(ab + 2 * (kb + lane) + 1);
-                            keep = !(c.x - e.x > hx) && !(c.x + e.x < lx) && !(c.y - e.y > hy) && !(c.y + e.y < ly) &&
-                                   !(c.z - e.z > hz) && !(c.z + e.z < lz);
+                            cl = __ldg(ab + 2 * (kb + lane)); el = __ldg(ab + 2 * (kb + lane) + 1);
+                            keep = !(cl.x - el.x > hx) && !(cl.x + el.x < lx) && !(cl.y - el.y > hy) &&
+                                   !(cl.y + el.y < ly) && !(cl.z - el.z > hz) && !(cl.z + el.z < lz);
                         }
                         unsigned mk = __ballot_sync(FULL, keep);
                         CRB_STAT(1, __popc(mk));
 #pragma unroll 1   // one copy of the exact path (instruction cache)
                         while (mk) {
-                            const int k = kb + __ffs(mk) - 1;
+                            const int kl = __ffs(mk) - 1, k = kb + kl;
                             mk &= mk - 1u;
+#if CRB_AB_SHFL   // the cuboid's AABB from the lane that tested it (no reload)
+                            const float4 c = make_float4(__shfl_sync(FULL, cl.x, kl), __shfl_sync(FULL, cl.y, kl),
+                                                         __shfl_sync(FULL, cl.z, kl), 0.f);
+                            const float4 e = make_float4(__shfl_sync(FULL, el.x, kl), __shfl_sync(FULL, el.y, kl),
+                                                         __shfl_sync(FULL, el.z, kl), 0.f);
+#else
                             const float4 c = __ldg(ab + 2 * k), e = __ldg(ab + 2 * k + 1);
+#endif
                             bool f = false;
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
