@@ -15,12 +15,16 @@
  *     asynchronous on `stream` (a cudaStream_t, NULL = legacy default stream).
  *   - crb_lbfgs_solve_host takes HOST pointers (pinned memory recommended), performs the
  *     host->device copies, the solve and the device->host copies on `stream`, and synchronises.
- *   - A context is bound to one CUDA device and used by one host thread at a time.
+ *   - A context is bound to one CUDA device and used by one host thread at a time.  Its solves
+ *     share context-owned device workspaces (per-seed results when the caller passes none, the
+ *     persistent schedules' state buffer and flags): solves of one context must not overlap in
+ *     time on different streams (use one context per stream).
  *   - An empty batch (B == 0 or P == 0) is validated like any other and returns CRB_OK without a
  *     launch; its batch pointers may then be NULL.
  *   - Numeric types: all results are fp32 arithmetic (the paper's kernels are fp32).  The
- *     sphere-cuboid screen runs a conservative packed-fp16 bounding-sphere pre-screen that only
- *     selects the cuboids given the exact fp32 test: results are bitwise those of the all-fp32
+ *     sphere-cuboid and sphere-pair terms run conservative culling (group AABBs over the slots,
+ *     per-lane AABB tests, proxy-sphere bounds of rigid pair blocks) that only selects what gets
+ *     the exact fp32 tests, in the paper's order: results are bitwise those of the all-pairs fp32
  *     screen.  Every kernel flushes fp32 subnormals to zero (-ftz).  Environments below 60
  *     enabled cuboids stage their cuboid tables in shared memory, larger ones read them from
  *     global memory (same arithmetic).
