@@ -9,8 +9,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "curobo_b200.cu")            # kernels (CRB_PART 0) + host side
-SRC_WMMA = os.path.join(HERE, "csrc", "curobo_b200_wmma.cu")  # the <WMMA = true> (large-world) kernels
-DEPS = [SRC, SRC_WMMA, os.path.join(HERE, "csrc", "crb_device.cuh"), os.path.join(ROOT, "include", "curobo_b200.h"),
+SRC_GMEM = os.path.join(HERE, "csrc", "curobo_b200_gmem.cu")  # the <GMEM = true> (large-world) kernels
+DEPS = [SRC, SRC_GMEM, os.path.join(HERE, "csrc", "crb_device.cuh"), os.path.join(ROOT, "include", "curobo_b200.h"),
         os.path.abspath(__file__)]   # the flags live here
 LIB = os.path.join(HERE, "libcurobo_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -22,7 +22,7 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 # screen as the small-world one and gains 2-3 % from it, profiles/r02_ksweep_ftz.txt; round 1 kept
 # it off there because the tensor-core screen lost 9 %).  One setting for every kernel: the
 # numerics of an environment no longer depend on which build the context picks.
-FTZ = {SRC: ["-ftz=true"], SRC_WMMA: ["-ftz=true"]}
+FTZ = {SRC: ["-ftz=true"], SRC_GMEM: ["-ftz=true"]}
 
 
 def compile_lib(out: str, defs=(), ptxas_verbose: bool = False, ftz: bool = True, ftz_all: bool = False) -> str:
@@ -33,7 +33,7 @@ def compile_lib(out: str, defs=(), ptxas_verbose: bool = False, ftz: bool = True
     objs, procs = [], []
     report = ""
     try:
-        for src in (SRC, SRC_WMMA):
+        for src in (SRC, SRC_GMEM):
             obj = f"{out}.{os.path.basename(src)}.o"
             fz = (["-ftz=true"] if ftz_all else FTZ[src]) if ftz else []
             cmd = [NVCC, *FLAGS, *fz, *(["-Xptxas", "-v"] if ptxas_verbose else []), *defs, "-c", "-o", obj, src]

@@ -30,57 +30,9 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #define CRB_PHASE(i) do { } while (0)
 #endif
 
-// Small-world pre-screen in packed fp16 (HFMA2, two cuboids per instruction) ahead of the exact
-// fp32 test; 0 = the fp32 screen of every (sphere, cuboid).
-#ifndef CRB_WORLD_H2
-#define CRB_WORLD_H2 1
-#endif
-// ... as a bounding-sphere test (1) or the Chebyshev box test in the cuboid frame (0)
-#ifndef CRB_WORLD_L1
-#define CRB_WORLD_L1 1
-#endif
-// The large-world build (cuboid table in global memory) with the fp16x2 bounding-sphere screen (1)
-// instead of the tensor-core screen (0).  Measured (tools/k_sweep.py, 32 problems x 32 seeds x 30
-// iterations, M evals/s, HMMA -> bounding sphere): K = 64 162.5 -> 171.4, 128 95.0 -> 99.7,
-// 256 52.0 -> 54.6, dense K = 1000 22.4 -> 23.9 (gpurun_out/ksweep_l1.txt, profiles/r02_*)
-#ifndef CRB_LARGE_L1
-#define CRB_LARGE_L1 1
-#endif
-
-// World pre-screen on the tensor cores: 1 = the affine cuboid-frame
-// transform of a world group runs as HMMA.16816 on an fp16 hi/lo split, 0 = the FFMA screen only.
-// World term: cuboids culled per work item by the group's AABB over the pass's slots, then a
-// per-lane world-AABB test ahead of the exact fp32 test (1); or the fp16x2 pre-screens below (0)
-#ifndef CRB_WORLD_CULL
-#define CRB_WORLD_CULL 1
-#endif
-
 // Self-collision blocks culled per pass by their proxy-sphere bound (1) or always screened (0)
 #ifndef CRB_SELF_CULL_DEV
 #define CRB_SELF_CULL_DEV 1
-#endif
-
-// Unroll factor of the once-per-pass per-slot loops (link sums, pose terms, world-group sum): code
-// size against the instruction cache (DESIGN.md "Instruction fetch")
-#ifndef CRB_COLD_UNROLL
-#define CRB_COLD_UNROLL 2
-#endif
-
-// The compaction's r-th flagged slot by popc bisection (1) or __fns (0)
-#ifndef CRB_NTH_BIT
-#define CRB_NTH_BIT 1
-#endif
-
-// Sweep samples evaluated in the cuboid frame (affine interpolation of the endpoints' local
-// coordinates; world gradient only on hits) (1), or each sample transformed (0)
-#ifndef CRB_SWEEP_LOCAL
-#define CRB_SWEEP_LOCAL 1
-#endif
-
-// World culling: a kept cuboid's AABB reaches the per-lane test by warp shuffles from the lane
-// that tested it (1) or is reloaded (0)
-#ifndef CRB_AB_SHFL
-#define CRB_AB_SHFL 1
 #endif
 
 // Self-collision screen tightened to the pairs that can still reach the lane's current best
@@ -89,13 +41,17 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #define CRB_SELF_PRUNE 1
 #endif
 
-#ifndef CRB_WORLD_MMA
-#define CRB_WORLD_MMA 1
+// Unroll factor of the once-per-pass per-slot loops (link sums, pose terms, world-group sum): code
+// size against the instruction cache (DESIGN.md "Instruction fetch")
+#ifndef CRB_COLD_UNROLL
+#define CRB_COLD_UNROLL 2
 #endif
-// ... used when the environment has at least this many cuboids (below it the FFMA screen is as
-// fast and its smaller code keeps the instruction cache warm: DESIGN.md "World screen")
-#ifndef CRB_MMA_MIN_K
-#define CRB_MMA_MIN_K 60
+
+// Environments with at least this many enabled cuboids read the cuboid table from global memory
+// (the GMEM kernel instantiations) so that two CTAs fit per SM; below it the table is staged in
+// shared memory
+#ifndef CRB_GMEM_MIN_K
+#define CRB_GMEM_MIN_K 60
 #endif
 
 namespace crb {
@@ -148,7 +104,7 @@ struct RobotPack {
 
 // Shared-memory layout (offsets in 4-byte words from the dynamic smem base).
 struct Layout {
-    int robot, boxes, boxl1, mbar;
+    int robot, boxes, mbar;
     int q_cfg, scs, xs, ltg, frames, swl, sbest, srank, sij, cbb, csm, gxd, gq, gva, pose_ft, tdp,
         goal, cfg_cost, cfg_terms, gV, red, st, scal, wq;
     int solver;      // start of the solver region
@@ -156,7 +112,6 @@ struct Layout {
     int XS;          // row length of xs (H + 5)
     int HS;          // slot stride of the state-gradient rows gq / gva (TO: H rounded up to 32; IK: 32)
     int boxes_gmem;  // 1: the cuboid table is read from global memory (large-world build), not staged
-    int stage_l1;    // 1: also stage the bounding-sphere pairs (solver / evaluation kernels, small worlds)
 };
 
 // Cost parameters (App. A), copied by value into registers by eval_pass.
@@ -177,10 +132,7 @@ struct KParams {
     CostP cp;
     const float4 *robot;     // packed robot blob (global)
     const float4 *boxes;     // [n_env][kmax][4] float4: (R col i, -col_i . t) x3, (h, M)
-    const uint4 *boxes_h2;   // [n_env][kpairs][4] uint4: fp16x2 cuboid pairs (set_world)
-    const uint4 *boxes_l1;   // [n_env][kpairs] uint4: fp16x2 bounding-sphere pairs (cx, cy, cz, rho')
     const float4 *boxes_ab;  // [n_env][kmax][2] float4: world-frame AABB centre, half extents (+ margin)
-    int kpairs;
     const int *box_count;    // [n_env] enabled (compacted) boxes
     int kmax, n_env;
     // solver parameters (Alg. 6, Alg. 1)
@@ -281,16 +233,13 @@ __device__ __forceinline__ int stage_tables(const KParams &kp, float *smem, int 
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + kp.lay.mbar);
     const int K = (env >= 0 && env < kp.n_env) ? kp.box_count[env] : 0;
     if (threadIdx.x == 0) {
-        reinterpret_cast<int *>(smem + kp.lay.mbar)[2] = env;   // for the fp16x2 cuboid table
+        reinterpret_cast<int *>(smem + kp.lay.mbar)[2] = env;   // the staged environment (world terms)
         mbar_init(bar, 1);
         const uint32_t rbytes = (uint32_t)kp.rp.words * 4u;
         const uint32_t bbytes = kp.lay.boxes_gmem ? 0u : (uint32_t)K * 64u;
-        // the bounding-sphere pairs of the small-world pre-screen (solver / evaluation kernels)
-        const uint32_t lbytes = (kp.lay.boxes_gmem || !kp.lay.stage_l1) ? 0u : (uint32_t)((K + 1) / 2) * 16u;
-        mbar_expect_tx(bar, rbytes + bbytes + lbytes);
+        mbar_expect_tx(bar, rbytes + bbytes);
         bulk_g2s(smem + kp.lay.robot, kp.robot, rbytes, bar);
         if (bbytes > 0) bulk_g2s(smem + kp.lay.boxes, kp.boxes + (size_t)env * kp.kmax * 4, bbytes, bar);
-        if (lbytes > 0) bulk_g2s(smem + kp.lay.boxl1, kp.boxes_l1 + (size_t)env * kp.kpairs, lbytes, bar);
     }
     {   // world work-queue order: identity, no cost history yet
         const int nwg = (kp.rp.M + 3) >> 2;
@@ -312,11 +261,6 @@ __device__ __forceinline__ int restage_world(const KParams &kp, float *smem, int
         const float4 *src = kp.boxes + (size_t)env * kp.kmax * 4;
         float4 *dst = reinterpret_cast<float4 *>(smem + kp.lay.boxes);
         for (int i = threadIdx.x; i < 4 * K; i += NT) dst[i] = src[i];
-        if (kp.lay.stage_l1) {
-            const uint4 *l1s = kp.boxes_l1 + (size_t)env * kp.kpairs;
-            uint4 *l1d = reinterpret_cast<uint4 *>(smem + kp.lay.boxl1);
-            for (int i = threadIdx.x; i < (K + 1) / 2; i += NT) l1d[i] = l1s[i];
-        }
     }
     if (threadIdx.x == 0) reinterpret_cast<int *>(smem + kp.lay.mbar)[2] = env;
     __syncthreads();
@@ -722,31 +666,6 @@ __device__ __forceinline__ float box_screen(float cx, float cy, float cz, const 
     return fmaf(mx, mx, fmaf(my, my, mz * mz));
 }
 
-// ---- tensor-core pre-screen of the cuboid test.  For a world group
-// (4 spheres x 32 slots = 128 rows) and 8 cuboids, the cuboid-frame coordinates
-// p_loc_c = col_c . w + off_c are a dense [128 x 4] x [4 x 8] product per coordinate c.  One
-// mma.m16n8k16 (fp16 in, fp32 accumulate) per 16 rows, 8 cuboids and coordinate computes it on
-// an fp16 hi/lo split of both operands:
-//   A row = (wh, 1 | wh, 1 | wl, 0 | 0),  B col = (Bh | Bl | Bh | 0)  =>  A.B = wh.(Bh + Bl) + wl.Bh,
-// i.e. (wh + wl).(Bh + Bl) without the wl.Bl term: |error| <= ~5e-6 (1 + |w|)(1 + |B|) m, covered
-// by the slack 2e-5 (2 + M)(1 + max|w|), M = max(|off|, h) in h.w (set_world).  The result only
-// decides which cuboids go through the exact fp32 test below, so the world term is bitwise the
-// FFMA path's.
-__device__ __forceinline__ void split_h2(float x, float y, unsigned &hi, unsigned &lo) {
-    const __half2 h = __floats2half2_rn(x, y);
-    const float2 f = __half22float2(h);
-    const __half2 l = __floats2half2_rn(x - f.x, y - f.y);
-    hi = *reinterpret_cast<const unsigned *>(&h);
-    lo = *reinterpret_cast<const unsigned *>(&l);
-}
-
-__device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
-    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%10,%10,%10,%10};"
-        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
-}
-
 // Position of the n-th (0-based) set bit of m (n < popc(m)): a 5-step popc bisection, branch-free
 // (__fns is a loop on this architecture)
 __device__ __forceinline__ int nth_set_bit(unsigned m, int n) {
@@ -769,12 +688,6 @@ __device__ __forceinline__ int f2o(float x) {
 }
 __device__ __forceinline__ float o2f(int i) { return __int_as_float(i ^ ((i >> 31) & 0x7fffffff)); }
 
-// inside the cuboid expanded by e along every axis (Chebyshev bound of the Euclidean test);
-// written as !(|p| >= e) so a NaN coordinate is flagged and left to the exact test
-__device__ __forceinline__ bool in_ebox(float px, float py, float pz, float ex, float ey, float ez) {
-    return !(fabsf(px) >= ex) && !(fabsf(py) >= ey) && !(fabsf(pz) >= ez);
-}
-
 // Rare path: the hit's activation and gradient, then the backward / forward marches (A6-A12):
 // L = |n - c|, bound = L/2, j = J0 (r' on a hit, else sd), at most n_s samples p = c + (j/L)(n - c);
 // a hit adds phi and (1 - kappa) phi' (-grad sd) and jumps r', a miss jumps sd.
@@ -795,10 +708,8 @@ static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const
     }
     if (dirs) {
         const float J0 = (rp - sd0 > 0.f) ? rp : sd0;
-#if CRB_SWEEP_LOCAL
         float lcx, lcy, lcz;
         box_local(b, cx, cy, cz, lcx, lcy, lcz);
-#endif
 #pragma unroll 1
         for (int dir = 0; dir < 2; ++dir) {
             if (!(dirs & (1 << dir))) continue;
@@ -806,30 +717,20 @@ static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const
             const float vx = q.x - cx, vy = q.y - cy, vz = q.z - cz;
             const float L = sqrtf(vx * vx + vy * vy + vz * vz);
             const float iL = 1.f / L, bound = 0.5f * L;
-#if CRB_SWEEP_LOCAL
             // samples in the cuboid frame: l(c + kappa v) = l(c) + kappa (l(q) - l(c)) (affine), and
             // the world-frame gradient only for the samples that hit
             float lqx, lqy, lqz;
             box_local(b, q.x, q.y, q.z, lqx, lqy, lqz);
             const float dlx = lqx - lcx, dly = lqy - lcy, dlz = lqz - lcz;
-#endif
             float j = J0;
             for (int st = 0; st < steps; ++st) {
                 if (j >= bound) break;
                 const float kap = j * iL;
-                float gx, gy, gz;
-#if CRB_SWEEP_LOCAL
-                float glx, gly, glz;
+                float gx, gy, gz, glx, gly, glz;
                 const float sd = box_sdf_local(b, fmaf(kap, dlx, lcx), fmaf(kap, dly, lcy), fmaf(kap, dlz, lcz), glx, gly, glz);
-#else
-                const float px = fmaf(kap, vx, cx), py = fmaf(kap, vy, cy), pz = fmaf(kap, vz, cz);
-                const float sd = box_sdf_grad(b, px, py, pz, gx, gy, gz);
-#endif
                 const float dp = rp - sd;
                 if (dp > 0.f) {
-#if CRB_SWEEP_LOCAL
                     box_grad_world(b, glx, gly, glz, gx, gy, gz);
-#endif
                     float dphi;
                     E += activation(dp, eta, inv_eta, dphi);
                     const float f = (1.f - kap) * dphi;
@@ -882,7 +783,7 @@ __device__ __forceinline__ void stage_dt(const KParams &kp, const Smem &s, int r
     s.tdp[8] = (float)(cf.wb[3] * (r2 * r));
 }
 
-template <int MODE, bool WMMA, bool LONG = false>
+template <int MODE, bool GMEM, bool LONG = false>
 __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const float *thA, int K, int n_act,
                                           const float *dvec, bool grad = true) {
     Smem s = make_smem(kp, smem);
@@ -891,9 +792,9 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
     if (threadIdx.x == 0) atomicAdd(&g_crb_stats[25], 1ull);
 #endif
     // large worlds: the cuboid table stays in global memory (L1 / L2), so the CTA keeps its
-    // shared-memory footprint and two CTAs fit per SM (kp.lay.boxes_gmem == WMMA); env from
+    // shared-memory footprint and two CTAs fit per SM (kp.lay.boxes_gmem == GMEM); env from
     // stage_tables
-    if (WMMA)
+    if (GMEM)
         s.boxes = reinterpret_cast<const float *>(
             kp.boxes + (size_t)reinterpret_cast<const int *>(smem + kp.lay.mbar)[2] * kp.kmax * 4);
     const RobotPack &rp = kp.rp;
@@ -914,7 +815,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         // then the short self items); ties keep index order.  Which warp takes which item never
         // changes a result (fixed-order merges).
         const int nwg = (rp.M + 3) >> 2;
-        if (WMMA && nwg <= 32) {   // large worlds only: few, long world items
+        if (GMEM && nwg <= 32) {   // large worlds only: few, long world items
             int *ord = s.wq, *cost = s.wq + nwg;
             for (int i = 1; i < nwg; ++i) {
                 const int g = ord[i], cg = cost[g];
@@ -1125,14 +1026,14 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             } stat_t{t_start, item < nwg};
 #endif
             if (item < nwg) {
-                const int grp = WMMA ? s.wq[item] : item;
+                const int grp = GMEM ? s.wq[item] : item;
                 const int m0 = grp << 2;
                 struct ItemCost {   // large worlds: the group's cost for the next pass's order (lane 0)
                     int *dst; long long t0;
                     __device__ ~ItemCost() {
-                        if (WMMA && (threadIdx.x & 31) == 0) *dst = (int)min(clock64() - t0, (long long)0x3fffffff);
+                        if (GMEM && (threadIdx.x & 31) == 0) *dst = (int)min(clock64() - t0, (long long)0x3fffffff);
                     }
-                } item_cost{s.wq + nwg + grp, WMMA ? clock64() : 0ll};
+                } item_cost{s.wq + nwg + grp, GMEM ? clock64() : 0ll};
                 float cx[4], cy[4], cz[4], th2[4], sp[4];
                 int dirs[4];
 #pragma unroll
@@ -1194,7 +1095,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                 int u = 0, r = e;
                                 if (r >= n0) { r -= n0; u = 1; if (r >= n1) { r -= n1; u = 2; if (r >= n2) { r -= n2; u = 3; } } }
                                 const unsigned bm = u == 0 ? bal[0] : u == 1 ? bal[1] : u == 2 ? bal[2] : bal[3];
-                                const int src = CRB_NTH_BIT ? nth_set_bit(bm, r) : __fns(bm, 0, r + 1);   // the r-th flagged slot
+                                const int src = nth_set_bit(bm, r);   // the r-th flagged slot
                                 const int m = m0 + u;
                                 const float4 *pc = s.sw + m * NC + src;
                                 const float4 c = pc[0];
@@ -1213,92 +1114,6 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 };
                 if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
                     CRB_STAT(0, K);
-#if CRB_WORLD_MMA
-                    if (WMMA && !CRB_LARGE_L1) {
-                    // tensor-core pre-screen, 8 cuboids per step; only cuboids with a flagged row
-                    // go through exact_box, in increasing k (the accumulation order of the FFMA path)
-                    const int g8 = lane >> 2, t4 = lane & 3;
-                    const bool odd = t4 & 1, hi_only = t4 >= 2;
-                    unsigned thb = 0u, wb = 0u;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        thb = max(thb, th2[u] > 0.f ? __float_as_uint(th2[u]) : 0u);
-                        wb = max(wb, max(__float_as_uint(fabsf(cx[u])),
-                                         max(__float_as_uint(fabsf(cy[u])), __float_as_uint(fabsf(cz[u])))));
-                    }
-                    // group threshold: the largest sqrt(th2) (>= every row's), and the |w| factor of the
-                    // rounding slack (NaN bits order above inf: a NaN makes every cuboid flagged)
-                    const float thg = sqrtf(__uint_as_float(__reduce_max_sync(FULL, thb)));
-                    // (|w| >= 3e4 m would overflow fp16: the NaN factor then flags every cuboid)
-                    const float wm = __uint_as_float(__reduce_max_sync(FULL, wb));
-                    const float wfac = wm < 3e4f ? 1.f + wm : __uint_as_float(0x7fc00000u);
-                    unsigned af[8][4];   // A fragments: m-tile mt = (sphere mt>>1, slots 16(mt&1) + 0..15)
-#pragma unroll
-                    for (int mt = 0; mt < 8; ++mt) {
-                        const int m = min(m0 + (mt >> 1), rp.M - 1), sl = ((mt & 1) << 4) + g8;
-                        const float4 w0 = s.sw[m * NC + sl], w1 = s.sw[m * NC + sl + 8];
-                        unsigned h0, l0, h1, l1;
-                        split_h2(odd ? w0.z : w0.x, odd ? 1.f : w0.y, h0, l0);
-                        split_h2(odd ? w1.z : w1.x, odd ? 1.f : w1.y, h1, l1);
-                        af[mt][0] = h0; af[mt][1] = h1;
-                        af[mt][2] = hi_only ? 0u : l0; af[mt][3] = hi_only ? 0u : l1;
-                    }
-                    const float4 *bx4 = reinterpret_cast<const float4 *>(s.boxes);
-                    for (int kb = 0; kb < K; kb += 8) {
-                        // B fragments of cuboid kb + g8 (column g8), one per coordinate
-                        const float4 *bk = bx4 + 4 * min(kb + g8, K - 1);
-                        unsigned b0[3], b1[3];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            const float2 v = reinterpret_cast<const float2 *>(bk + c)[odd];
-                            unsigned hi, lo;
-                            split_h2(v.x, v.y, hi, lo);
-                            b0[c] = hi_only ? lo : hi;
-                            b1[c] = hi_only ? 0u : hi;
-                        }
-                        // expanded half extents of this thread's C columns: cuboids kb + 2 t4 + j
-                        float ex[2], ey[2], ez[2];
-#pragma unroll
-                        for (int j = 0; j < 2; ++j) {
-                            const int kk = kb + 2 * t4 + j;
-                            const float4 h = bx4[4 * min(kk, K - 1) + 3];
-                            const float e = fmaf(2e-5f * (2.f + h.w), wfac, thg);   // NaN h.w: always flagged
-                            const bool ok = kk < K;
-                            ex[j] = ok ? h.x + e : -1.f; ey[j] = ok ? h.y + e : -1.f; ez[j] = ok ? h.z + e : -1.f;
-                        }
-                        bool f0 = false, f1 = false;
-#pragma unroll
-                        for (int mt = 0; mt < 8; ++mt) {
-                            float px[4], py[4], pz[4];
-                            mma16816(px, af[mt], b0[0], b1[0]);
-                            mma16816(py, af[mt], b0[1], b1[1]);
-                            mma16816(pz, af[mt], b0[2], b1[2]);
-                            f0 |= in_ebox(px[0], py[0], pz[0], ex[0], ey[0], ez[0]) |
-                                  in_ebox(px[2], py[2], pz[2], ex[0], ey[0], ez[0]);
-                            f1 |= in_ebox(px[1], py[1], pz[1], ex[1], ey[1], ez[1]) |
-                                  in_ebox(px[3], py[3], pz[3], ex[1], ey[1], ez[1]);
-                        }
-                        const unsigned q0 = __ballot_sync(FULL, f0), q1 = __ballot_sync(FULL, f1);
-                        if (q0 | q1) {
-                            // column 2t + j is flagged iff a lane with lane & 3 == t has its bit
-                            unsigned n0 = q0 | (q0 >> 16), n1 = q1 | (q1 >> 16);
-                            n0 |= n0 >> 8; n1 |= n1 >> 8;
-                            n0 = (n0 | (n0 >> 4)) & 0xfu; n1 = (n1 | (n1 >> 4)) & 0xfu;
-                            unsigned mask = 0u;
-#pragma unroll
-                            for (int t = 0; t < 4; ++t) mask |= ((n0 >> t) & 1u) << (2 * t) | ((n1 >> t) & 1u) << (2 * t + 1);
-                            if (K - kb < 8) mask &= (1u << (K - kb)) - 1u;
-                            CRB_STAT(1, __popc(mask));
-                            while (mask) {
-                                const int b = __ffs(mask) - 1;
-                                mask &= mask - 1u;
-                                exact_box(kb + b, true);
-                            }
-                        }
-                    }
-                    } else
-#endif
-#if CRB_WORLD_CULL
                     {
                     // World culling.  An exact flag needs s2 < th2, i.e. the
                     // sphere's centre within th of the cuboid, hence within th of the cuboid's world
@@ -1340,14 +1155,11 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         while (mk) {
                             const int kl = __ffs(mk) - 1, k = kb + kl;
                             mk &= mk - 1u;
-#if CRB_AB_SHFL   // the cuboid's AABB from the lane that tested it (no reload)
+                            // the cuboid's AABB from the lane that tested it (no reload)
                             const float4 c = make_float4(__shfl_sync(FULL, cl.x, kl), __shfl_sync(FULL, cl.y, kl),
                                                          __shfl_sync(FULL, cl.z, kl), 0.f);
                             const float4 e = make_float4(__shfl_sync(FULL, el.x, kl), __shfl_sync(FULL, el.y, kl),
                                                          __shfl_sync(FULL, el.z, kl), 0.f);
-#else
-                            const float4 c = __ldg(ab + 2 * k), e = __ldg(ab + 2 * k + 1);
-#endif
                             bool f = false;
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
@@ -1356,145 +1168,6 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         }
                     }
                     }
-#elif CRB_WORLD_H2 && CRB_WORLD_L1
-                    {
-                    // fp16x2 bounding-sphere pre-screen, cuboids k, k+1 in the two halves, each
-                    // thread's 4 spheres broadcast: the cuboid lies inside the sphere (c_k, rho_k),
-                    // so an exact flag (box distance < th) implies |w - c_k| < rho_k + th.  In fp16:
-                    //   v = dx^2 + dy^2 + dz^2 - Rinf^2 < 0,  Rinf = rk_k + tk,
-                    //   rk_k = (rho_k + 4 u |c_k|_inf)(1 + 12 u) rounded up (set_world),
-                    //   tk = th (1 + 12 u) + 4 u B_w (per sphere and slot, once per item),
-                    // u = 2^-11, B_w the group's largest |w|_1: the input roundings of w and c move
-                    // each difference by at most 2 u (|w| + |c|), the three HFMA2 accumulations, the
-                    // sum rk + tk, the rounding of tk and of Rinf^2 by at most ~8 u Rinf^2 at the
-                    // decision point; (1 + 12 u) and 4 u B_w cover them, so every cuboid the exact
-                    // fp32 test would flag is flagged here.
-                    // Flagged cuboids go through the exact fp32 test in increasing k: the world term
-                    // is bitwise the all-fp32 screen's.  A group with |w| beyond the fp16 range (or
-                    // NaN) sends every cuboid to the exact test.
-                    unsigned sb = 0u;
-                    __half2 hx[4], hy[4], hz[4], hth[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        sb = max(sb, __float_as_uint(fabsf(cx[u]) + fabsf(cy[u]) + fabsf(cz[u])));
-                        const bool on = th2[u] > 0.f;   // disabled: far away, never flags
-                        hx[u] = __float2half2_rn(on ? cx[u] : 6e4f); hy[u] = __float2half2_rn(on ? cy[u] : 6e4f);
-                        hz[u] = __float2half2_rn(on ? cz[u] : 6e4f); hth[u] = __float2half2_rn(on ? sqrtf(th2[u]) : 0.f);
-                    }
-                    const float Bw = __uint_as_float(__reduce_max_sync(FULL, sb));
-                    const bool force = !(Bw < 3e4f);
-                    const __half2 ha = __float2half2_rn(force ? 0.f : 4.f * 4.8828125e-4f * Bw);
-                    const __half2 kinf = __float2half2_rn(1.005859375f);   // 1 + 12 u, exact in fp16
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) hth[u] = __hfma2(hth[u], kinf, ha);   // tk
-                    // small worlds: the pairs staged in shared memory; large worlds (CRB_LARGE_L1):
-                    // read through the read-only cache
-                    const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
-                    const uint4 *l1 = WMMA ? kp.boxes_l1 + (size_t)envc * kp.kpairs
-                                           : reinterpret_cast<const uint4 *>(smem + kp.lay.boxl1);
-                    // two pairs (4 cuboids) per step: their sign bits share one warp reduction
-                    // (pair A at bits 15 / 31, pair B at 14 / 30), and the two pairs' arithmetic
-                    // interleaves; a missing pair B reads as "never flagged"
-                    for (int kb = 0; kb < K; kb += 4) {
-                        const bool hasB = kb + 2 < K;
-                        const uint4 wA = WMMA ? __ldg(l1 + (kb >> 1)) : l1[kb >> 1];
-                        const uint4 wB = hasB ? (WMMA ? __ldg(l1 + (kb >> 1) + 1) : l1[(kb >> 1) + 1]) : wA;
-                        const __half2 *WA = reinterpret_cast<const __half2 *>(&wA), *WB = reinterpret_cast<const __half2 *>(&wB);
-                        __half2 mnA = __float2half2_rn(1.f), mnB = mnA;
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            {
-                                const __half2 dx = __hsub2(hx[u], WA[0]), dy = __hsub2(hy[u], WA[1]), dz = __hsub2(hz[u], WA[2]);
-                                const __half2 R = __hadd2(WA[3], hth[u]);
-                                __half2 acc = __hmul2(__hneg2(R), R);
-                                acc = __hfma2(dz, dz, acc);
-                                acc = __hfma2(dy, dy, acc);
-                                acc = __hfma2(dx, dx, acc);
-                                mnA = __hmin2(mnA, acc);
-                            }
-                            {
-                                const __half2 dx = __hsub2(hx[u], WB[0]), dy = __hsub2(hy[u], WB[1]), dz = __hsub2(hz[u], WB[2]);
-                                const __half2 R = __hadd2(WB[3], hth[u]);
-                                __half2 acc = __hmul2(__hneg2(R), R);
-                                acc = __hfma2(dz, dz, acc);
-                                acc = __hfma2(dy, dy, acc);
-                                acc = __hfma2(dx, dx, acc);
-                                mnB = __hmin2(mnB, acc);
-                            }
-                        }
-                        const unsigned flA = *reinterpret_cast<const unsigned *>(&mnA) & 0x80008000u;
-                        const unsigned flB = hasB ? (*reinterpret_cast<const unsigned *>(&mnB) & 0x80008000u) >> 1 : 0u;
-                        const unsigned f = force ? 0xC000C000u : __reduce_or_sync(FULL, flA | flB);
-                        if (f) {
-                            CRB_STAT(1, __popc(f));
-#pragma unroll 1   // one copy of the exact path (instruction cache)
-                            for (int j = 0; j < 4; ++j) {
-                                const unsigned bit = (j & 2) ? (0x4000u << (16 * (j & 1))) : (0x8000u << (16 * (j & 1)));
-                                if ((f & bit) && kb + j < K) exact_box(kb + j, true);
-                            }
-                        }
-                    }
-                    }
-#elif CRB_WORLD_H2
-                    {
-                    // fp16x2 pre-screen, cuboids k, k+1 in the two halves, each thread's 4 spheres
-                    // broadcast.  Chebyshev test max_i(|l_i| - (h_i + delta)) < th per sphere, with
-                    // l = R^T (w - t) in fp16: |error| <= 2^-11 (5 S + 4 |off| + 3 h + th), S the
-                    // group's largest |w|_1 (HFMA2 rounds each partial sum; 1.5x margin in delta).
-                    // Only the cuboids a lane flags go through the exact fp32 test, in increasing k:
-                    // the world term is bitwise the all-fp32 screen's.
-                    unsigned sb = 0u, tb = 0u;
-                    __half2 hx[4], hy[4], hz[4], hth[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        sb = max(sb, __float_as_uint(fabsf(cx[u]) + fabsf(cy[u]) + fabsf(cz[u])));
-                        const float th = th2[u] > 0.f ? sqrtf(th2[u]) : -6e4f;   // disabled: never flags
-                        tb = max(tb, th > 0.f ? __float_as_uint(th) : 0u);
-                        hx[u] = __float2half2_rn(cx[u]); hy[u] = __float2half2_rn(cy[u]);
-                        hz[u] = __float2half2_rn(cz[u]); hth[u] = __float2half2_rn(th);
-                    }
-                    // delta_k = U (5 S + th_max + 7 M_k), U = 1.5 * 2^-11
-                    const float U = 1.5f * 4.8828125e-4f;
-                    const float d0r = U * fmaf(5.f, __uint_as_float(__reduce_max_sync(FULL, sb)),
-                                               __uint_as_float(__reduce_max_sync(FULL, tb)));
-                    const float d0 = d0r < 6e4f ? d0r : 6e4f;   // NaN / huge |w|: every cuboid flagged
-                    const int envc = reinterpret_cast<const int *>(smem + kp.lay.mbar)[2];
-                    const uint4 *bh = kp.boxes_h2 + (size_t)envc * kp.kpairs * 4;
-                    const __half2 u7 = __float2half2_rn(7.f * U), dd = __float2half2_rn(d0);
-                    for (int kb = 0; kb < K; kb += 2) {
-                        const uint4 w0 = __ldg(bh), w1 = __ldg(bh + 1), w2 = __ldg(bh + 2), w3 = __ldg(bh + 3);
-                        bh += 4;
-                        const __half2 *W0 = reinterpret_cast<const __half2 *>(&w0), *W1 = reinterpret_cast<const __half2 *>(&w1),
-                                      *W2 = reinterpret_cast<const __half2 *>(&w2), *W3 = reinterpret_cast<const __half2 *>(&w3);
-                        const __half2 r00 = W0[0], r01 = W0[1], r02 = W0[2], o0 = W0[3];
-                        const __half2 r10 = W1[0], r11 = W1[1], r12 = W1[2], o1 = W1[3];
-                        const __half2 r20 = W2[0], r21 = W2[1], r22 = W2[2], o2 = W2[3];
-                        const __half2 e = __hfma2(u7, W3[3], dd);   // delta of each cuboid
-                        const __half2 ex = __hadd2(W3[0], e), ey = __hadd2(W3[1], e), ez = __hadd2(W3[2], e);
-                        __half2 mn = __float2half2_rn(1.f);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const __half2 lx = __hfma2(r00, hx[u], __hfma2(r01, hy[u], __hfma2(r02, hz[u], o0)));
-                            const __half2 ly = __hfma2(r10, hx[u], __hfma2(r11, hy[u], __hfma2(r12, hz[u], o1)));
-                            const __half2 lz = __hfma2(r20, hx[u], __hfma2(r21, hy[u], __hfma2(r22, hz[u], o2)));
-                            const __half2 q = __hmax2(__hsub2(__habs2(lx), ex),
-                                                      __hmax2(__hsub2(__habs2(ly), ey), __hsub2(__habs2(lz), ez)));
-                            mn = __hmin2(mn, __hsub2(q, hth[u]));
-                        }
-                        // sign bit of a half: that cuboid is within reach of some sphere of this lane
-                        const unsigned fl = *reinterpret_cast<const unsigned *>(&mn) & 0x80008000u;
-                        const unsigned f = __reduce_or_sync(FULL, fl);
-                        if (f) {
-                            CRB_STAT(1, ((f & 0x8000u) ? 1 : 0) + ((f & 0x80000000u) ? 1 : 0));
-#pragma unroll 1   // one copy of the exact path (instruction cache)
-                            for (int j = 0; j < 2; ++j)
-                                if (f & (0x8000u << (16 * j))) exact_box(kb + j, true);
-                        }
-                    }
-                    }
-#else
-                    for (int k = 0; k < K; ++k) exact_box(k, false);
-#endif
                 }
                 // the group's cost goes to the .w of its first sphere (unused by the backward):
                 // the merge sums the groups in index order, whichever warp took them

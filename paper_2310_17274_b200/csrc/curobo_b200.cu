@@ -1,21 +1,23 @@
 // curobo_b200.cu -- kernels and host side of the C-ABI declared in include/curobo_b200.h.
 //
 // Kernels (all sm_100a, NT = 256 threads, 2 CTAs per SM by shared-memory footprint):
-//   solve_to_kernel   persistent per-seed L-BFGS for trajectory optimisation: one CTA = one seed
-//                     trajectory, all iterations in one launch (replaces the paper's ~20 kernels
-//                     x 25-iteration CUDA graph)
-//   solve_ik_kernel   same for collision-free IK: one CTA = 32 seeds of one problem
+//   solve_to_kernel   per-seed L-BFGS for trajectory optimisation: one CTA = one seed trajectory,
+//                     all iterations in one launch (replaces the paper's ~20 kernels x 25-iteration
+//                     CUDA graph); PERSIST: one wave taking (seed, iteration chunk)
+//                     units; LONG: H > 32 in timestep windows
+//   solve_ik_kernel   same for collision-free IK: one CTA = 32 seeds (PERSIST: chunked units)
+//   solve_*_cluster_kernel   latency mode: the line-search candidates on a thread-block cluster
 //   eval_to_kernel / eval_ik_kernel   one-shot batched cost+gradient (crb_evaluate_cost_grad)
 //   fk_kernel         forward kinematics only (crb_fk)
 //   select_kernel     per-problem packed-key argmin over seeds (O9)
-//   + the test-hook kernels (ls_select, argmin_keys, lbfgs_direction)
+//   + the motion-generation, mask / steering and test-hook kernels
 //
 // Two translation units, compiled in parallel with the same flags (build.py): this file
-// (CRB_PART 0: the small-world <WMMA = false> kernels, every non-template kernel and the host
-// side) and curobo_b200_wmma.cu, which includes it with CRB_PART 1 and instantiates only the
-// large-world <WMMA = true> kernels (cuboid tables read from global memory; the template
-// parameter keeps its round-1 name: the optional tensor-core screen, CRB_LARGE_L1 = 0).
-// crb_wmma_kernel() hands those kernels to the host side.
+// (CRB_PART 0: the <GMEM = false> kernels that stage the cuboid table in shared memory, every
+// non-template kernel and the host side) and curobo_b200_gmem.cu, which includes it with
+// CRB_PART 1 and instantiates only the <GMEM = true> kernels (environments of >= CRB_GMEM_MIN_K
+// cuboids: the cuboid table is read from global memory through L1 / L2 so two CTAs fit per SM).
+// crb_gmem_kernel() hands those kernels to the host side.
 #ifndef CRB_PART
 #define CRB_PART 0
 #endif
@@ -241,7 +243,7 @@ static __device__ __noinline__ void trace_ik(const KParams &kp, int phase, size_
 // ------------------------------------------------------------------------------------------
 // persistent TO solver: one CTA per (problem, seed)
 // ------------------------------------------------------------------------------------------
-template <bool WMMA, bool LONG, bool PERSIST>
+template <bool GMEM, bool LONG, bool PERSIST>
 __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const Smem s = make_smem(kp, smem);
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             __syncthreads();
         }
         // ---- a2..a10: one evaluation pass (cost only for particles)
-        eval_pass<MODE_TO, WMMA, LONG>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr, !part);
+        eval_pass<MODE_TO, GMEM, LONG>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr, !part);
         if (part) {
             // ---- f1 UPDATE, streamed over the particles of a chunk (Eqs. particle_1/2, B6), the
             // chunks merged in order (chunk_merge; totals in cg, unused during the warm-up)
@@ -522,7 +524,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
 // winner's gradient from the owners' shared memory (DSMEM), so every step is bitwise the
 // sequential kernel's.  The particle warm-up and pass 0 run redundantly in every CTA.
 // ------------------------------------------------------------------------------------------
-template <bool WMMA, bool LONG>
+template <bool GMEM, bool LONG>
 __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     namespace cg = cooperative_groups;
@@ -607,7 +609,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
             }
             __syncthreads();
         }
-        eval_pass<MODE_TO, WMMA, LONG>(kp, smem, thA, K, H, lpass > 0 ? dd : nullptr, !part);
+        eval_pass<MODE_TO, GMEM, LONG>(kp, smem, thA, K, H, lpass > 0 ? dd : nullptr, !part);
         if (part) {
             float r;
             const float w = pacc.add(s.scal[0], kp.p_inv_beta, r);
@@ -851,7 +853,7 @@ __device__ __forceinline__ void ik_post_pass(const KParams &kp, const Smem &s, i
 }
 
 // ------------------------------------------------------------------------------------------
-template <bool WMMA, bool PERSIST>
+template <bool GMEM, bool PERSIST>
 __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const Smem s = make_smem(kp, smem);
@@ -991,7 +993,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
                     joint_csq(s, kp.rp, idx, v);
                 }
             }
-            eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
+            eval_pass<MODE_IK, GMEM>(kp, smem, nullptr, K, n_act, nullptr, !part);
             if (part) {
                 // ---- f1 UPDATE, streamed over the particles of a chunk (Eqs. particle_1/2, B6), per
                 // seed; the chunks merged in order (chunk_merge; totals in cg, unused during the warm-up)
@@ -1085,7 +1087,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_kernel(const __grid_constant__
 
 // latency mode of the IK solver: the A candidates of an iteration on the A CTAs of a cluster (as
 // solve_to_cluster_kernel; per-seed selection on warp 0 from the peers' costs and gradients)
-template <bool WMMA>
+template <bool GMEM>
 __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
@@ -1167,7 +1169,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
                 joint_csq(s, kp.rp, idx, v);
             }
         }
-        eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr, !part);
+        eval_pass<MODE_IK, GMEM>(kp, smem, nullptr, K, n_act, nullptr, !part);
         if (part) {
             // ---- f1 UPDATE over this CTA's chunk, then all chunks merged in order (DSMEM)
             float r;
@@ -1260,7 +1262,7 @@ __global__ void __launch_bounds__(NT, 2) solve_ik_cluster_kernel(const __grid_co
 // ------------------------------------------------------------------------------------------
 // one-shot evaluation, FK, selection
 // ------------------------------------------------------------------------------------------
-template <bool WMMA, bool LONG>
+template <bool GMEM, bool LONG>
 __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b = blockIdx.x;
@@ -1274,7 +1276,7 @@ __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ 
     stage_dt(kp, s, b);
     for (int i = t; i < N; i += NT) thA[i] = kp.q_in[(size_t)b * N + i];
     __syncthreads();
-    eval_pass<MODE_TO, WMMA, LONG>(kp, smem, thA, K, H, nullptr);
+    eval_pass<MODE_TO, GMEM, LONG>(kp, smem, thA, K, H, nullptr);
     if (t < 32) {
         float tr[5];
         for (int k = 0; k < 5; ++k) tr[k] = warp_sum(s.cfg_terms[k * NC + t]);
@@ -1288,7 +1290,7 @@ __global__ void __launch_bounds__(NT, 2) eval_to_kernel(const __grid_constant__ 
         for (int i = t; i < N; i += NT) kp.grad_out[(size_t)b * N + i] = s.gV[i];
 }
 
-template <bool WMMA>
+template <bool GMEM>
 __global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ KParams kp) {
     extern __shared__ __align__(16) float smem[];
     const int b0 = blockIdx.x * NC;
@@ -1307,7 +1309,7 @@ __global__ void __launch_bounds__(NT, 2) eval_ik_kernel(const __grid_constant__ 
     }
     __syncthreads();
     prep_sincos(s, kp.rp);
-    eval_pass<MODE_IK, WMMA>(kp, smem, nullptr, K, n_act, nullptr);
+    eval_pass<MODE_IK, GMEM>(kp, smem, nullptr, K, n_act, nullptr);
     if (warp == 0 && lane < n_act) {
         const int b = b0 + lane;
         const bool ok = !kp.env || kp.env[b] == env0;
@@ -1778,10 +1780,10 @@ __global__ void __launch_bounds__(NT, 2) lbfgs_direction_kernel(int n, int count
 
 }  // namespace
 
-// the <WMMA = true> kernels, instantiated in CRB_PART 1 (no flush-to-zero)
+// the <GMEM = true> kernels, instantiated in CRB_PART 1
 enum { KW_EVAL_TO, KW_EVAL_IK, KW_SOLVE_TO, KW_SOLVE_IK, KW_SOLVE_TO_CLUSTER, KW_SOLVE_IK_CLUSTER, KW_SOLVE_IK_PERSIST,
        KW_EVAL_TO_LONG, KW_SOLVE_TO_LONG, KW_SOLVE_TO_CLUSTER_LONG, KW_SOLVE_TO_PERSIST, KW_SOLVE_TO_LONG_PERSIST };
-const void *crb_wmma_kernel(int k);
+const void *crb_gmem_kernel(int k);
 
 #if CRB_STATS
 static int stats_copy(unsigned long long *out, int reset) {   // this translation unit's counters
@@ -1793,14 +1795,14 @@ static int stats_copy(unsigned long long *out, int reset) {   // this translatio
     }
     return 0;
 }
-int crb_wmma_stats(unsigned long long *out, int reset);
+int crb_gmem_stats(unsigned long long *out, int reset);
 #endif
 
 #if CRB_PART == 1
 #if CRB_STATS
-int crb_wmma_stats(unsigned long long *out, int reset) { return stats_copy(out, reset); }
+int crb_gmem_stats(unsigned long long *out, int reset) { return stats_copy(out, reset); }
 #endif
-const void *crb_wmma_kernel(int k) {
+const void *crb_gmem_kernel(int k) {
     switch (k) {
     case KW_EVAL_TO: return (const void *)eval_to_kernel<true, false>;
     case KW_EVAL_TO_LONG: return (const void *)eval_to_kernel<true, true>;
@@ -1833,10 +1835,7 @@ struct crb_ctx {
     // world
     bool world_ok = false;
     float4 *d_boxes = nullptr;
-    uint4 *d_boxes_h2 = nullptr;          // fp16x2 cuboid pairs (Chebyshev pre-screen, CRB_WORLD_L1 = 0)
-    uint4 *d_boxes_l1 = nullptr;          // fp16x2 bounding-sphere pairs of the small-world pre-screen
     float4 *d_boxes_ab = nullptr;         // world-frame AABB (centre, half extents) per cuboid (culling)
-    int kpairs = 1;                       // pairs per environment in d_boxes_h2
     int *d_box_count = nullptr;
     int n_env = 0, kmax = 0, kmax_enabled = 0;
     int sm_count = 148;
@@ -1905,7 +1904,6 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     auto take = [&](int words) { int o = w; w += r4(words); return o; };
     L.robot = take(rp.words);
     L.boxes = take(kmax * 16);
-    L.boxl1 = take(CRB_WORLD_CULL ? 0 : ((kmax + 1) / 2) * 4);   // bounding-sphere pairs (fp16x2 pre-screen builds only)
     L.mbar = take(4);
     L.XS = mode == MODE_TO ? H + 5 : 0;
     L.q_cfg = take(D * NC);
@@ -1951,10 +1949,7 @@ KParams base_params(const crb_ctx *ctx) {
     kp.rp = ctx->rp;
     kp.robot = ctx->d_robot;
     kp.boxes = ctx->d_boxes;
-    kp.boxes_h2 = ctx->d_boxes_h2;
-    kp.boxes_l1 = ctx->d_boxes_l1;
     kp.boxes_ab = ctx->d_boxes_ab;
-    kp.kpairs = ctx->kpairs;
     kp.box_count = ctx->d_box_count;
     kp.kmax = ctx->kmax;
     kp.n_env = ctx->n_env;
@@ -1982,10 +1977,10 @@ crb_status ready(crb_ctx *ctx, bool need_world) {
     return CRB_OK;
 }
 
-// The solver / evaluation kernels come in two builds of the world screen (crb_device.cuh "tensor-
-// core pre-screen"): with it when some environment holds >= CRB_MMA_MIN_K enabled cuboids, else
-// the FFMA-only build (its smaller register footprint is faster on small worlds).
-bool use_world_mma(const crb_ctx *ctx) { return CRB_WORLD_MMA && ctx->kmax_enabled >= CRB_MMA_MIN_K; }
+// The solver / evaluation kernels come in two builds: <GMEM = true> (cuboid table read from global
+// memory) when some environment holds >= CRB_GMEM_MIN_K enabled cuboids, else the table is staged
+// in shared memory.  The world arithmetic is the same.
+bool use_gmem_world(const crb_ctx *ctx) { return ctx->kmax_enabled >= CRB_GMEM_MIN_K; }
 
 crb_status launch_fn(crb_ctx *ctx, const void *fn, int grid, size_t smem, cudaStream_t st, const KParams &kp,
                      const char *nm) {
@@ -2038,8 +2033,7 @@ crb_status crb_create(int cuda_device, crb_ctx **out) {
 crb_status crb_destroy(crb_ctx *ctx) {
     if (!ctx) return CRB_E_ARG;
     cudaSetDevice(ctx->device);
-    cudaFree(ctx->d_robot); cudaFree(ctx->d_boxes); cudaFree(ctx->d_boxes_h2); cudaFree(ctx->d_box_count);
-    cudaFree(ctx->d_boxes_l1);
+    cudaFree(ctx->d_robot); cudaFree(ctx->d_boxes); cudaFree(ctx->d_box_count);
     cudaFree(ctx->d_boxes_ab);
     cudaFree(ctx->ws_cost); cudaFree(ctx->ws_traj); cudaFree(ctx->ws_mask); cudaFree(ctx->ws_n);
     cudaFree(ctx->ws_ik_state); cudaFree(ctx->ws_ik_flags);
@@ -2384,7 +2378,6 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
     if (st != CRB_OK) return st;
     if (n_env < 1 || k_max < 0 || !boxes_per_env || (k_max > 0 && !boxes)) return fail(ctx, CRB_E_ARG, "bad world arguments");
     std::vector<float> packed((size_t)n_env * std::max(k_max, 1) * 16, 0.f);
-    std::vector<double> sph_c((size_t)n_env * std::max(k_max, 1) * 4, 0.0);   // bounding sphere (centre, radius)
     // world-frame AABB of each enabled cuboid (crb_device.cuh "World culling"): centre and half
     // extents e_i = sum_j |R_ij| h_j, widened by 1e-4 m + 1e-6 (|c| + e) (fp32 rounding of the
     // device-side test, far below the margin)
@@ -2415,8 +2408,6 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
                 o[4 * i2 + 3] = (float)(-(R[0][i2] * b.pos[0] + R[1][i2] * b.pos[1] + R[2][i2] * b.pos[2]));
             }
             o[12] = 0.5f * b.dims[0]; o[13] = 0.5f * b.dims[1]; o[14] = 0.5f * b.dims[2];
-            double *bs = &sph_c[((size_t)e * k_max + k) * 4];
-            bs[0] = b.pos[0]; bs[1] = b.pos[1]; bs[2] = b.pos[2];
             {
                 double ext[3], cm = 0.0;
                 for (int i2 = 0; i2 < 3; ++i2) {
@@ -2429,100 +2420,22 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
                 aabb[((size_t)e * k_max + k) * 2 + 1] =
                     make_float4((float)(ext[0] + mg), (float)(ext[1] + mg), (float)(ext[2] + mg), 0.f);
             }
-            bs[3] = 0.5 * std::sqrt((double)b.dims[0] * b.dims[0] + (double)b.dims[1] * b.dims[1] +
-                                    (double)b.dims[2] * b.dims[2]);
-            // cuboid magnitude M = max(|off_i|, h_i) for the rounding slack of the reduced-precision
-            // pre-screens (crb_device.cuh: HMMA hi/lo split, fp16x2 screen); NaN beyond the fp16
-            // range, which makes both screens send every sphere to the exact fp32 test
-            const double om = std::max({std::fabs((double)o[3]), std::fabs((double)o[7]), std::fabs((double)o[11]),
-                                        (double)o[12], (double)o[13], (double)o[14]});
-            o[15] = om < 3e4 ? (float)om : std::numeric_limits<float>::quiet_NaN();
+            o[15] = 0.f;   // unused
             ++k;
         }
         count[e] = k;
         kmax_en = std::max(kmax_en, k);
     }
-    // fp16x2 pairs (2p, 2p+1) of each environment's enabled cuboids for the small-world pre-screen
-    // (crb_device.cuh "fp16x2 pre-screen"): words 0-11 = rows of R^T with -col . t as (k0, k1)
-    // half pairs, 12-14 = half extents, 15 = magnitude M.  A cuboid beyond the fp16 range gets zero
-    // rows and h = +6e4 (always flagged), a missing second cuboid h = -6e4 (never flagged).
-    const int kpairs = std::max(1, (kmax_en + 1) / 2);
-    std::vector<__half2> ph((size_t)n_env * kpairs * 16, __floats2half2_rn(0.f, 0.f));
-    for (int e = 0; e < n_env; ++e)
-        for (int p2 = 0; p2 < kpairs; ++p2) {
-            float v[2][16];
-            for (int j = 0; j < 2; ++j) {
-                const int k = 2 * p2 + j;
-                const float *o = &packed[((size_t)e * k_max + std::min(k, std::max(k_max - 1, 0))) * 16];
-                const bool have = k < count[e], ok = have && o[15] < 3e4f;
-                for (int i = 0; i < 12; ++i) v[j][i] = ok ? o[i] : 0.f;
-                for (int i = 12; i < 15; ++i) v[j][i] = ok ? o[i] : (have ? 6e4f : -6e4f);
-                v[j][15] = ok ? o[15] : 0.f;
-            }
-            for (int i = 0; i < 16; ++i) ph[((size_t)e * kpairs + p2) * 16 + i] = __floats2half2_rn(v[0][i], v[1][i]);
-        }
-    // fp16x2 bounding-sphere pairs for the pre-screen (crb_device.cuh "bounding-sphere pre-screen"):
-    // per pair the centres (x, y, z) rounded to nearest and rk = (circumradius + 4 u max|c|) (1 +
-    // 12 u) (the centre's fp16 rounding and the screen's rounding factor, u = 2^-11) rounded UP.  A cuboid beyond the fp16 range
-    // gets centre 0 and rho' = 6e4 (always flagged); a missing second cuboid sits at 6e4 on every
-    // axis with rho' = 0 (its squared distance overflows to +inf: never flagged).
-    std::vector<__half2> pl1((size_t)n_env * kpairs * 4, __floats2half2_rn(0.f, 0.f));
-    auto half_up = [](double v) {   // smallest half >= v (v >= 0, below the fp16 maximum)
-        __half h = __float2half_rn((float)v);
-        while ((double)__half2float(h) < v) {
-            unsigned short bits;
-            memcpy(&bits, &h, 2);
-            ++bits;
-            memcpy(&h, &bits, 2);
-        }
-        return h;
-    };
-    for (int e = 0; e < n_env; ++e)
-        for (int p2 = 0; p2 < kpairs; ++p2) {
-            __half c[2][4];
-            for (int j = 0; j < 2; ++j) {
-                const int k = 2 * p2 + j;
-                if (k >= count[e]) {
-                    for (int i = 0; i < 3; ++i) c[j][i] = __float2half_rn(6e4f);
-                    c[j][3] = __float2half_rn(0.f);
-                    continue;
-                }
-                const double *bs = &sph_c[((size_t)e * k_max + k) * 4];
-                const double cm = std::max({std::fabs(bs[0]), std::fabs(bs[1]), std::fabs(bs[2])});
-                const double rp = (bs[3] + 4.0 * 4.8828125e-4 * cm) * (1.0 + 12.0 * 4.8828125e-4);
-                if (!(cm < 3e4) || !(rp < 3e4)) {
-                    for (int i = 0; i < 3; ++i) c[j][i] = __float2half_rn(0.f);
-                    c[j][3] = __float2half_rn(6e4f);
-                    continue;
-                }
-                for (int i = 0; i < 3; ++i) c[j][i] = __float2half_rn((float)bs[i]);
-                c[j][3] = half_up(rp);
-            }
-            for (int i = 0; i < 4; ++i) pl1[((size_t)e * kpairs + p2) * 4 + i] = __halves2half2(c[0][i], c[1][i]);
-        }
-    cudaFree(ctx->d_boxes); cudaFree(ctx->d_boxes_h2); cudaFree(ctx->d_box_count); cudaFree(ctx->d_boxes_l1);
-    cudaFree(ctx->d_boxes_ab);
-    ctx->d_boxes = nullptr; ctx->d_boxes_h2 = nullptr; ctx->d_box_count = nullptr; ctx->d_boxes_l1 = nullptr;
-    ctx->d_boxes_ab = nullptr;
+    cudaFree(ctx->d_boxes); cudaFree(ctx->d_box_count); cudaFree(ctx->d_boxes_ab);
+    ctx->d_boxes = nullptr; ctx->d_box_count = nullptr; ctx->d_boxes_ab = nullptr;
     ctx->world_ok = false;
     st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes_ab, aabb.size() * sizeof(float4)), "cudaMalloc boxes aabb");
     if (st != CRB_OK) return st;
     st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes_ab, aabb.data(), aabb.size() * sizeof(float4), cudaMemcpyHostToDevice),
                     "upload boxes aabb");
     if (st != CRB_OK) return st;
-    st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes_l1, pl1.size() * sizeof(__half2)), "cudaMalloc boxes l1");
-    if (st != CRB_OK) return st;
-    st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes_l1, pl1.data(), pl1.size() * sizeof(__half2), cudaMemcpyHostToDevice),
-                    "upload boxes l1");
-    if (st != CRB_OK) return st;
     st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes, packed.size() * 4), "cudaMalloc boxes");
     if (st != CRB_OK) return st;
-    st = cuda_check(ctx, cudaMalloc(&ctx->d_boxes_h2, ph.size() * sizeof(__half2)), "cudaMalloc boxes h2");
-    if (st != CRB_OK) return st;
-    st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes_h2, ph.data(), ph.size() * sizeof(__half2), cudaMemcpyHostToDevice),
-                    "upload boxes h2");
-    if (st != CRB_OK) return st;
-    ctx->kpairs = kpairs;
     st = cuda_check(ctx, cudaMalloc(&ctx->d_box_count, n_env * sizeof(int)), "cudaMalloc box count");
     if (st != CRB_OK) return st;
     st = cuda_check(ctx, cudaMemcpy(ctx->d_boxes, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "upload boxes");
@@ -2580,17 +2493,16 @@ crb_status crb_evaluate_cost_grad_dt(crb_ctx *ctx, const float *q, int B, int H,
     KParams kp = base_params(ctx);
     kp.B = B; kp.H = H; kp.cp.H = H; kp.mode = mode; kp.q_in = q; kp.env = env; kp.start = start; kp.goal = goal;
     kp.cost_out = cost; kp.grad_out = grad; kp.terms_out = term_costs; kp.dt_arr = dt;
-    const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
-    kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
-    kp.lay.stage_l1 = (use_world_mma(ctx) || CRB_WORLD_CULL) ? 0 : 1;
+    const size_t bytes = make_layout(ctx->rp, use_gmem_world(ctx) ? 0 : ctx->kmax_enabled, mode, H, 1, 1, false, kp.lay);
+    kp.lay.boxes_gmem = use_gmem_world(ctx) ? 1 : 0;
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids)");
-    const bool wm = use_world_mma(ctx);
+    const bool wm = use_gmem_world(ctx);
     if (mode == MODE_TO)
-        return launch_fn(ctx, H > NC ? (wm ? crb_wmma_kernel(KW_EVAL_TO_LONG) : (const void *)eval_to_kernel<false, true>)
-                                     : (wm ? crb_wmma_kernel(KW_EVAL_TO) : (const void *)eval_to_kernel<false, false>), B, bytes,
+        return launch_fn(ctx, H > NC ? (wm ? crb_gmem_kernel(KW_EVAL_TO_LONG) : (const void *)eval_to_kernel<false, true>)
+                                     : (wm ? crb_gmem_kernel(KW_EVAL_TO) : (const void *)eval_to_kernel<false, false>), B, bytes,
                          (cudaStream_t)stream, kp,
                       "eval_to_kernel");
-    return launch_fn(ctx, wm ? crb_wmma_kernel(KW_EVAL_IK) : (const void *)eval_ik_kernel<false>, (B + NC - 1) / NC, bytes,
+    return launch_fn(ctx, wm ? crb_gmem_kernel(KW_EVAL_IK) : (const void *)eval_ik_kernel<false>, (B + NC - 1) / NC, bytes,
                   (cudaStream_t)stream, kp, "eval_ik_kernel");
 }
 
@@ -2644,11 +2556,10 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     kp.trace = sp->n_trace > 0 ? sp->trace : nullptr; kp.n_trace = sp->n_trace;
     for (int j = 0; j < 8; ++j) kp.trace_iter[j] = j < sp->n_trace ? sp->trace_iter[j] : -1;
     kp.seed_best_cost = sbc; kp.seed_best_traj = sbt;
-    const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
-    kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
-    kp.lay.stage_l1 = (use_world_mma(ctx) || CRB_WORLD_CULL) ? 0 : 1;
+    const size_t bytes = make_layout(ctx->rp, use_gmem_world(ctx) ? 0 : ctx->kmax_enabled, mode, H, sp->history, sp->n_alpha, true, kp.lay);
+    kp.lay.boxes_gmem = use_gmem_world(ctx) ? 1 : 0;
     if (bytes > SMEM_MAX) return fail(ctx, CRB_E_LIMIT, "shared memory footprint too large (robot + cuboids + solver)");
-    const bool wm = use_world_mma(ctx);
+    const bool wm = use_gmem_world(ctx);
     // latency mode: A CTAs per seed in a cluster when the whole batch fits one wave (2 CTAs / SM)
     const long long units = mode == MODE_TO ? (long long)P * S : (long long)P * ((S + NC - 1) / NC);
     // automatic choice (tools/cluster_vs_seq.py): the batch fits one wave in cluster mode; or the
@@ -2663,9 +2574,9 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
                       (sp->cluster == 1 || (sp->cluster == -1 && (fits || parts || waves)));
     if (clus && units > 0) {
         const void *kern = mode == MODE_TO
-                               ? (H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_CLUSTER_LONG) : (const void *)solve_to_cluster_kernel<false, true>)
-                                         : (wm ? crb_wmma_kernel(KW_SOLVE_TO_CLUSTER) : (const void *)solve_to_cluster_kernel<false, false>))
-                               : (wm ? crb_wmma_kernel(KW_SOLVE_IK_CLUSTER) : (const void *)solve_ik_cluster_kernel<false>);
+                               ? (H > NC ? (wm ? crb_gmem_kernel(KW_SOLVE_TO_CLUSTER_LONG) : (const void *)solve_to_cluster_kernel<false, true>)
+                                         : (wm ? crb_gmem_kernel(KW_SOLVE_TO_CLUSTER) : (const void *)solve_to_cluster_kernel<false, false>))
+                               : (wm ? crb_gmem_kernel(KW_SOLVE_IK_CLUSTER) : (const void *)solve_ik_cluster_kernel<false>);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         if (e != cudaSuccess) return cuda_check(ctx, e, "solve_cluster_kernel");
         cudaLaunchConfig_t cfg = {};
@@ -2690,10 +2601,10 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
         // trajectories span >= 2 waves and the last one is poorly filled (predicted one-CTA-per-
         // seed efficiency < 95 %), 4 iteration chunks; sp->persist = 0 forces one CTA per seed,
         // k >= 1 k chunks.
-        const void *kern = H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true, false>)
-                                  : (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false, false>);
-        const void *kern_p = H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG_PERSIST) : (const void *)solve_to_kernel<false, true, true>)
-                                    : (wm ? crb_wmma_kernel(KW_SOLVE_TO_PERSIST) : (const void *)solve_to_kernel<false, false, true>);
+        const void *kern = H > NC ? (wm ? crb_gmem_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true, false>)
+                                  : (wm ? crb_gmem_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false, false>);
+        const void *kern_p = H > NC ? (wm ? crb_gmem_kernel(KW_SOLVE_TO_LONG_PERSIST) : (const void *)solve_to_kernel<false, true, true>)
+                                    : (wm ? crb_gmem_kernel(KW_SOLVE_TO_PERSIST) : (const void *)solve_to_kernel<false, false, true>);
         const long long NU = (long long)P * S;
         int chunks = sp->persist;
         int per_sm = 0;
@@ -2741,7 +2652,7 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
             ik_persist_init_kernel<<<1, 256, 0, stream_>>>(env, P, (int)NGg, ctx->ws_ik_flags);
             ctx->launches++;
             if ((st = cuda_check(ctx, cudaGetLastError(), "ik_persist_init_kernel")) != CRB_OK) return st;
-            const void *kern = wm ? crb_wmma_kernel(KW_SOLVE_IK_PERSIST) : (const void *)solve_ik_kernel<false, true>;
+            const void *kern = wm ? crb_gmem_kernel(KW_SOLVE_IK_PERSIST) : (const void *)solve_ik_kernel<false, true>;
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
             if (e != cudaSuccess) return cuda_check(ctx, e, "solve_ik_kernel (persistent)");
             int per_sm = 0;
@@ -2751,7 +2662,7 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
             st = launch_fn(ctx, kern, (int)grid, bytes, stream_, kp, "solve_ik_kernel (persistent)");
         } else {
             kp.ik_chunks = 1;
-            st = launch_fn(ctx, wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false, false>, (int)NGg,
+            st = launch_fn(ctx, wm ? crb_gmem_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false, false>, (int)NGg,
                            bytes, stream_, kp, "solve_ik_kernel");
         }
     }
@@ -2810,16 +2721,15 @@ crb_status crb_solver_occupancy(crb_ctx *ctx, int H, int history, int n_alpha, i
     if ((st = ready(ctx, true)) != CRB_OK) return st;
     KParams kp = base_params(ctx);
     const int mode = H == 1 ? MODE_IK : MODE_TO;
-    const size_t bytes = make_layout(ctx->rp, use_world_mma(ctx) ? 0 : ctx->kmax_enabled, mode, H, history, n_alpha, true, kp.lay);
-    kp.lay.boxes_gmem = use_world_mma(ctx) ? 1 : 0;
-    kp.lay.stage_l1 = (use_world_mma(ctx) || CRB_WORLD_CULL) ? 0 : 1;
+    const size_t bytes = make_layout(ctx->rp, use_gmem_world(ctx) ? 0 : ctx->kmax_enabled, mode, H, history, n_alpha, true, kp.lay);
+    kp.lay.boxes_gmem = use_gmem_world(ctx) ? 1 : 0;
     if (smem_bytes) *smem_bytes = (int)bytes;
     if (bytes > SMEM_MAX) { if (ctas_per_sm) *ctas_per_sm = 0; return CRB_OK; }
     int n = 0;
-    const bool wm = use_world_mma(ctx);
-    const void *fn = mode == MODE_TO ? (H > NC ? (wm ? crb_wmma_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true, false>)
-                                                : (wm ? crb_wmma_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false, false>))
-                                     : (wm ? crb_wmma_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false, false>);
+    const bool wm = use_gmem_world(ctx);
+    const void *fn = mode == MODE_TO ? (H > NC ? (wm ? crb_gmem_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true, false>)
+                                                : (wm ? crb_gmem_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false, false>))
+                                     : (wm ? crb_gmem_kernel(KW_SOLVE_IK) : (const void *)solve_ik_kernel<false, false>);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     st = cuda_check(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, NT, bytes), "occupancy");
     if (ctas_per_sm) *ctas_per_sm = n;
@@ -3021,7 +2931,7 @@ crb_status crb_particle_normals(uint32_t key0, uint32_t key1, int n_var, int n_p
 // world-screen work counters (tools/world_stats.py only; not part of the product ABI)
 extern "C" int crb_debug_stats(unsigned long long *out, int reset) {
     unsigned long long w[32];
-    if (stats_copy(out, reset) != 0 || crb_wmma_stats(w, reset) != 0) return -1;
+    if (stats_copy(out, reset) != 0 || crb_gmem_stats(w, reset) != 0) return -1;
     for (int i = 0; i < 32; ++i) out[i] += w[i];   // the counters of both translation units
     return 0;
 }

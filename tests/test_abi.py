@@ -61,7 +61,7 @@ def test_sass_is_sm100a(lib_path):
     assert "UBLKCP" in sass            # TMA bulk copy of the robot / cuboid tables
     # both builds (small-world: template argument false, large-world: true) cull the cuboids of a
     # work item with the group's AABB (warp min / max: REDUX) and a ballot, and never use the
-    # round-1 tensor-core screen (compiled only with CRB_WORLD_CULL = 0, CRB_LARGE_L1 = 0)
+    # round-1 tensor-core screen (removed in round 2)
     funcs = re.split(r"\n\s+Function : ", sass)
     for kern in ("solve_to_kernel", "solve_ik_kernel", "eval_to_kernel", "eval_ik_kernel"):
         body = {("ILb1E" in f.split("\n", 1)[0]): f for f in funcs if kern in f.split("\n", 1)[0]}

@@ -795,7 +795,7 @@ def test_full_size_ik_solve_sampled_against_oracle(native, O):
 
 def test_full_size_dense_solve_sampled_against_oracle(native, O):
     """BASELINE configs[4] per GPU at the bench's sample size (16 problems x 32 seeds x 32
-    timesteps, K = 1000 per problem, swept + speed, 100 iterations; the HMMA pre-screen build):
+    timesteps, K = 1000 per problem, swept + speed, 100 iterations; the GMEM build):
     sampled winners re-evaluated by the oracle, argmin of the per-seed results, every seed
     improved on its initial cost."""
     from paper_2310_17274_b200 import workload
@@ -868,7 +868,7 @@ def test_solve_to_cluster_mode_bitwise(native, O, variant):
     from paper_2310_17274_b200 import workload
     wl = workload.franka_to(0, list(range(3)), S=5, H=32, iters=60, n_boxes=80 if variant == "big_world" else 20)
     sp = wl.solver
-    if variant == "big_world":     # the HMMA build (cuboids in global memory, longest-first world items)
+    if variant == "big_world":     # the GMEM build (cuboids in global memory, longest-first world items)
         sp = dataclasses.replace(sp, particle_iters=1, n_particles=8)
     if variant == "particles":
         sp = dataclasses.replace(sp, particle_iters=2, n_particles=16)

@@ -149,7 +149,7 @@ def test_particle_warmup_ik_parity_d16(native, O, cluster):
     """D = 16 makes D * 32 = 512 particle elements per 32-seed group, two per
     thread of the 256-thread CTA.  Every dof (not only the first 8) must be sampled, updated and
     given fresh sin / cos; sequential and latency-mode (cluster) kernels against the oracle."""
-    from test_gpu_world_mma import capacity_robot
+    from test_gpu_world_builds import capacity_robot
     rb = capacity_robot()
     D = rb.n_dof
     R = O.Robot(rb)

@@ -1,13 +1,12 @@
-"""GPU: the tensor-core cuboid pre-screen (crb_device.cuh "tensor-core pre-screen", DESIGN.md
-"World screen").
+"""GPU: the two world builds and large worlds against the oracle.
 
-The library builds its solver / evaluation kernels twice: with the HMMA pre-screen when some
-environment holds >= CRB_MMA_MIN_K (60) enabled cuboids, else FFMA only.  The pre-screen only
-chooses which cuboids go through the exact fp32 test, so on the SAME environments both builds must
-return bitwise the same costs, gradients and solves (the FFMA build flushes subnormals, the HMMA
-build keeps them: no intermediate of these inputs falls below 2^-126); a context whose world list
-includes one large environment runs the HMMA build for all of them.  Parity against the fp64 oracle at K in the HMMA
-range (ragged K, far and huge cuboids) uses the tolerances of test_gpu_parity.py.
+The library builds its solver / evaluation kernels twice: <GMEM = true> reads the cuboid table from
+global memory when some environment holds >= CRB_GMEM_MIN_K (60) enabled cuboids, else the table is
+staged in shared memory.  The world arithmetic (culling, exact fp32 tests, accumulation order) is the
+same, so on the SAME environments both builds return bitwise the same costs, gradients and solves;
+a context whose world list includes one large environment runs the GMEM build for all of them.
+Parity against the fp64 oracle at K in the GMEM range (ragged K, far and huge cuboids) uses the
+tolerances of test_gpu_parity.py.
 """
 import numpy as np
 import pytest
@@ -19,7 +18,7 @@ from test_gpu_parity import ref_traj, MARGIN, Stats, T, f32, franka_trajs, make 
 
 pytestmark = pytest.mark.gpu
 
-MMA_MIN_K = 60
+GMEM_MIN_K = 60
 
 
 @pytest.fixture(scope="module")
@@ -29,59 +28,60 @@ def native():
 
 
 def _pair(native, rb, small, cp, big_k=80):
-    """(FFMA context over `small`, HMMA context over `small` + one big environment)."""
+    """(shared-memory-table context over `small`, global-memory-table context over `small` + one big
+    environment)."""
     big = inputs.random_world(9, 0, big_k, lo=-0.9, hi=0.9, disabled_frac=0.0)
     return make(native, rb, small, cp), make(native, rb, list(small) + [big], cp)
 
 
 @pytest.mark.parametrize("flags", [inputs.SWEEP | inputs.SPEED, inputs.SPEED | inputs.JERK, 0])
-def test_mma_and_ffma_builds_bitwise_equal_eval_to(native, O, flags):
+def test_gmem_and_smem_builds_bitwise_equal_eval_to(native, O, flags):
     B, H = 48, 32
     rb, starts, goals_cfg, trajs = franka_trajs(70 + flags, B, H, noise=0.4)
     small = [inputs.tabletop_scene(1, e, 20) for e in range(2)] + [inputs.random_world(3, 0, 30, lo=-0.8, hi=0.8)]
     cp = inputs.CostParams(flags=flags, dt=0.25)
-    ffma, mma = _pair(native, rb, small, cp)
+    smem, gmem = _pair(native, rb, small, cp)
     R = O.Robot(rb)
     goals = np.array([O.fk(R, q)[2] for q in goals_cfg])
     env = T((np.arange(B) % 3).astype(np.int32), torch.int32)
-    a = ffma.evaluate(T(f32(trajs)), T(f32(goals)), start=T(f32(starts)), env=env)
-    b = mma.evaluate(T(f32(trajs)), T(f32(goals)), start=T(f32(starts)), env=env)
+    a = smem.evaluate(T(f32(trajs)), T(f32(goals)), start=T(f32(starts)), env=env)
+    b = gmem.evaluate(T(f32(trajs)), T(f32(goals)), start=T(f32(starts)), env=env)
     for x, y in zip(a, b):
         assert torch.equal(x, y)
     assert (a[2][:, 4] > 0).sum() >= B // 4          # the world term is active on many trajectories
-    ffma.close(); mma.close()
+    smem.close(); gmem.close()
 
 
-def test_mma_and_ffma_builds_bitwise_equal_ik_and_solves(native, O):
+def test_gmem_and_smem_builds_bitwise_equal_ik_and_solves(native, O):
     from paper_2310_17274_b200 import workload
     wl = workload.franka_to(0, list(range(4)), S=8, H=32, iters=15)
-    ffma, mma = _pair(native, wl.robot, wl.worlds, wl.cost)
+    smem, gmem = _pair(native, wl.robot, wl.worlds, wl.cost)
     outs = []
-    for ctx in (ffma, mma):
+    for ctx in (smem, gmem):
         outs.append(ctx.solve(wl.solver, T(wl.seeds), T(wl.goal), start=T(wl.start), env=T(wl.env, torch.int32),
                               seed_outputs=True))
     for k in ("best_cost", "best_traj", "best_key", "seed_best_cost"):
         assert torch.equal(outs[0][k], outs[1][k]), k
     ik = workload.franka_ik(0, list(range(40)), S=30, iters=20)
     outs = []
-    for ctx in (ffma, mma):
+    for ctx in (smem, gmem):
         ctx.set_cost_params(ik.cost)
-        ctx.set_world(ik.worlds if ctx is ffma else list(ik.worlds) + [inputs.random_world(9, 0, 80, disabled_frac=0.0)])
+        ctx.set_world(ik.worlds if ctx is smem else list(ik.worlds) + [inputs.random_world(9, 0, 80, disabled_frac=0.0)])
         outs.append(ctx.solve(ik.solver, T(ik.seeds), T(ik.goal), env=T(ik.env, torch.int32), seed_outputs=True))
     for k in ("best_cost", "best_traj", "seed_best_cost"):
         assert torch.equal(outs[0][k], outs[1][k]), k
-    ffma.close(); mma.close()
+    smem.close(); gmem.close()
 
 
 @pytest.mark.parametrize("K,lo,hi,dmax", [(72, -0.8, 0.8, 0.3), (77, -0.7, 0.7, 0.25), (203, -0.9, 0.9, 0.12)])
-def test_eval_to_parity_mma_range(native, O, K, lo, hi, dmax):
-    """Oracle parity with the HMMA build: K = 72, 77 (ragged last 8-cuboid tile), 203 (~10 %
+def test_eval_to_parity_gmem_range(native, O, K, lo, hi, dmax):
+    """Oracle parity with the GMEM build: K = 72, 77 (ragged last 32-cuboid culling block), 203 (~10 %
     disabled, so the enabled counts stay >= 64); rotated cuboids.  (Clutter and seed noise are
     sized so that sweep exits within the exclusion margin stay under the 2 % rule.)"""
     B, H = 128, 32
     rb, starts, goals_cfg, trajs = franka_trajs(300 + K, B, H, noise=0.3)
     worlds = [inputs.random_world(11, e, K, lo=lo, hi=hi, dmax=dmax) for e in range(2)]
-    assert max(int(w.enabled.sum()) for w in worlds) >= MMA_MIN_K     # the HMMA build runs
+    assert max(int(w.enabled.sum()) for w in worlds) >= GMEM_MIN_K     # the GMEM build runs
     cp = inputs.CostParams(flags=inputs.SWEEP | inputs.SPEED, dt=0.25)
     ctx = make(native, rb, worlds, cp)
     R = O.Robot(rb)
@@ -102,7 +102,7 @@ def test_eval_to_parity_mma_range(native, O, K, lo, hi, dmax):
     ctx.close()
 
 
-def test_mma_far_and_huge_cuboids(native, O):
+def test_gmem_far_and_huge_cuboids(native, O):
     """Cuboids far outside the workspace (large offsets, still inside the fp16 range) and one
     beyond it (|offset| > 3e4 m: the pre-screen flags it and the exact test decides) next to a
     cuboid the arm penetrates: costs equal the FFMA build and the oracle."""
@@ -133,17 +133,17 @@ def test_mma_far_and_huge_cuboids(native, O):
         assert t_ref[4] > 0                          # the huge cuboid contains the base spheres
     stats.done()
     # the 20-cuboid prefix through both builds: bitwise equal
-    ffma, mma = _pair(native, rb, [small], cp)
+    smem, gmem = _pair(native, rb, [small], cp)
     env = T(np.zeros(B, np.int32), torch.int32)
-    a = ffma.evaluate(T(V), T(gl), start=T(st), env=env)
-    b2 = mma.evaluate(T(V), T(gl), start=T(st), env=env)
+    a = smem.evaluate(T(V), T(gl), start=T(st), env=env)
+    b2 = gmem.evaluate(T(V), T(gl), start=T(st), env=env)
     for x, y in zip(a, b2):
         assert torch.equal(x, y)
-    ctx.close(); ffma.close(); mma.close()
+    ctx.close(); smem.close(); gmem.close()
 
 
-def test_fp16x2_screen_far_and_huge_cuboids_against_oracle(native, O):
-    """The small-world build (fp16x2 pre-screen, K < 64) on cuboids far outside the workspace, one
+def test_smem_build_far_and_huge_cuboids_against_oracle(native, O):
+    """The small-world build (cuboid table in shared memory, K < 60) on cuboids far outside the workspace, one
     beyond the fp16 range (forced to the exact test), one huge cuboid containing the arm's base,
     and one in the arm's way: oracle parity."""
     B, H = 128, 32
@@ -194,7 +194,7 @@ def _random_robot(seed, n_links=9, n_spheres=23):
 def test_random_robot_eval_parity_both_builds(native, O, seed, big):
     """Random robots (prismatic and revolute x/y/z joints, folded fixed links, 23 spheres of which
     3 disabled, random self pairs) through the TO and IK evaluations against the oracle, in the
-    fp16x2 build (K = 30) and the HMMA build (an extra 70-cuboid environment), plus an empty
+    shared-memory-table build (K = 30) and the GMEM build (an extra 70-cuboid environment), plus an empty
     environment."""
     rb = _random_robot(seed)
     D, H, B = rb.n_dof, 16, 48

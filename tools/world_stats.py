@@ -1,10 +1,10 @@
 """World-screen work counters (analysis tool, not the product path).
 
 Builds a CRB_STATS=1 variant of the library next to this file (tools/libcurobo_stats.so, optionally
-with -DCRB_WORLD_MMA=0) and runs the bench workloads through it:
-  [0] (group, cuboid) pairs examined, [1] pairs flagged by the tensor-core pre-screen,
+with the cuboid table forced to global memory, --gmem 1) and runs the bench workloads through it:
+  [0] (group, cuboid) pairs examined, [1] pairs kept by the group-AABB culling,
   [2] pairs with an exact flag (some entry needs the slow path), [3] flagged entries (slow calls).
-usage: python tools/world_stats.py [--mma 0|1]
+usage: python tools/world_stats.py [--mma 0|1]   (1: every environment on the GMEM build)
 """
 import argparse
 import ctypes as C
@@ -25,8 +25,8 @@ from paper_2310_17274_b200 import build as B  # noqa: E402
 
 lib = os.path.join(ROOT, "tools", f"libcurobo_stats{args.mma}{'' if args.ftz else '_noftz'}.so")
 if not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(d) for d in B.DEPS):
-    B.compile_lib(lib, ["-DCRB_STATS=1", f"-DCRB_WORLD_MMA={args.mma}",
-                        "-DCRB_MMA_MIN_K=0" if args.mma else "-DCRB_MMA_MIN_K=100000"], ftz=bool(args.ftz))
+    B.compile_lib(lib, ["-DCRB_STATS=1", "-DCRB_GMEM_MIN_K=0" if args.mma else "-DCRB_GMEM_MIN_K=100000"],
+                  ftz=bool(args.ftz))
 os.environ["CRB_LIB"] = lib
 
 import torch  # noqa: E402
