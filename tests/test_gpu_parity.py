@@ -928,6 +928,12 @@ def test_solve_to_long_horizon(native, O):
     for k in seq[0]:
         assert torch.equal(seq[0][k], seq[1][k]), k
         assert torch.equal(seq[0][k], clu[k]), k
+    # the particle warm-up over the windows: sequential = cluster = persistent, bitwise
+    spp = dataclasses.replace(sp, iters=8, particle_iters=1, n_particles=8)
+    outs = [ctx.solve(dataclasses.replace(spp, cluster=c, persist=q), T(V), T(gl), **kw) for c, q in ((0, 0), (1, 0), (0, 2))]
+    for o in outs[1:]:
+        for k in outs[0]:
+            assert torch.equal(outs[0][k], o[k]), ("particles", k)
     c0, _, _ = ctx.evaluate(T(V.reshape(P * S, H, 7)), T(np.repeat(gl, S, 0)), start=T(np.repeat(st, S, 0)),
                             env=T(np.repeat(env, S), torch.int32))
     sbc = seq[0]["seed_best_cost"].cpu().numpy().reshape(-1)

@@ -8,6 +8,8 @@ a context whose world list includes one large environment runs the GMEM build fo
 Parity against the fp64 oracle at K in the GMEM range (ragged K, far and huge cuboids) uses the
 tolerances of test_gpu_parity.py.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 import torch
@@ -359,6 +361,18 @@ def test_capacity_d31_parity(native, O):
     ik = ctx.solve(inputs.SolverParams(iters=5, particle_iters=2, n_particles=8), T(Q.reshape(2, 20, D)), T(gl[:2]),
                    seed_outputs=True)
     assert torch.isfinite(ik["seed_best_cost"]).all()
+    # the persistent schedules at D = 31 (the IK step's 32-register bucket, 992-element groups in the
+    # saved state) against one CTA per group / seed, bitwise
+    for sp in (inputs.SolverParams(iters=6, persist=3), inputs.SolverParams(iters=6, particle_iters=1, n_particles=8,
+                                                                             persist=2)):
+        ik_p = ctx.solve(sp, T(Q.reshape(2, 20, D)), T(gl[:2]), seed_outputs=True)
+        ik_0 = ctx.solve(dataclasses.replace(sp, persist=0), T(Q.reshape(2, 20, D)), T(gl[:2]), seed_outputs=True)
+        to_p = ctx.solve(sp, T(V.reshape(2, 12, H, D)), T(gl[:2]), start=T(st[:2]), seed_outputs=True)
+        to_0 = ctx.solve(dataclasses.replace(sp, persist=0), T(V.reshape(2, 12, H, D)), T(gl[:2]), start=T(st[:2]),
+                         seed_outputs=True)
+        for k in ik_p:
+            assert torch.equal(ik_p[k], ik_0[k]), ("IK", k)
+            assert torch.equal(to_p[k], to_0[k]), ("TO", k)
     ctx.close()
     big = random_chain(79, 40, 10, types=[0] + [4] * 39)
     assert big.n_dof == 39
