@@ -630,6 +630,10 @@ def run_native(args):
                            "boxes": 20, "iters": args.iters, "line_search": list(sp.alpha), "history": sp.history,
                            "flags": "sweep+speed", "evals_per_step_per_gpu": evals_per_step,
                            "ctas_per_sm": ctas_per_sm, "smem_bytes_per_cta": smem_per_cta,
+                           "schedule": ("persistent: one wave of CTAs over (seed, 10-iteration-chunk) units"
+                                        if int(wl.seeds.shape[0]) * int(wl.seeds.shape[1]) >= 2 * ctas_per_sm *
+                                        torch.cuda.get_device_properties(dev).multi_processor_count
+                                        else "one CTA per seed trajectory"),
                            "l2": "flushed between timed steps (256 MB write, outside the events)",
                            "parallelism": (f"seed-sharded x{world}: C1 all_reduce(MIN) of packed keys + C2 all_gather "
                                            f"of winners inside the timed step") if seed_mode else

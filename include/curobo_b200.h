@@ -178,15 +178,14 @@ typedef struct {
     int trace_iter[8];
     /* Scheduling (ignored in cluster mode).  IK: -1 (default): automatic -- a
      * persistent kernel of one wave of CTAs takes (seed group, iteration chunk) work units from a
-     * global counter when the batch has at least two waves of 32-seed groups (4 chunks of
-     * iters / 4 iterations; the solver state of a group moves through a context-owned device
+     * global counter when the batch has at least two waves of 32-seed groups (16 chunks of
+     * iters / 16 iterations; the solver state of a group moves through a context-owned device
      * buffer between its chunks, so the last wave is not left to a few long CTAs); when every
      * problem uses the same environment the groups are 32 consecutive seeds of the flat P x S
      * batch (no idle lanes when S % 32 != 0).  0: one CTA per 32-seed group of a problem.  k >= 1:
      * the persistent kernel with k chunks.  TO: the same persistent kernel over (seed, iteration
-     * chunk) units (one CTA per seed trajectory otherwise); automatic when the seeds span >= 2
-     * waves and the last wave is less than 95 % predicted-full (e.g. 1536 seeds on 296 CTA slots);
-     * 0 off, k >= 1 k chunks.  Every seed's result is bitwise the same in all modes. */
+     * chunk) units (one CTA per seed trajectory otherwise); automatic (10 chunks) when the seeds
+     * span >= 2 waves of CTAs (e.g. 2048 seeds on 296 CTA slots); 0 off, k >= 1 k chunks.  Every seed's result is bitwise the same in all modes. */
     int persist;
 } crb_solver_params;
 

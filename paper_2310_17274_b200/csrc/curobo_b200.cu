@@ -2598,9 +2598,8 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
         st = cuda_check(ctx, cudaGetLastError(), "solve_cluster_kernel");
     } else if (mode == MODE_TO) {
         // TO scheduling: the persistent chunked kernel when the seed
-        // trajectories span >= 2 waves and the last one is poorly filled (predicted one-CTA-per-
-        // seed efficiency < 95 %), 4 iteration chunks; sp->persist = 0 forces one CTA per seed,
-        // k >= 1 k chunks.
+        // trajectories span >= 2 waves, 10 iteration chunks (measured best of 2..25 at cfg 2 / 4);
+        // sp->persist = 0 forces one CTA per seed, k >= 1 k chunks.
         const void *kern = H > NC ? (wm ? crb_gmem_kernel(KW_SOLVE_TO_LONG) : (const void *)solve_to_kernel<false, true, false>)
                                   : (wm ? crb_gmem_kernel(KW_SOLVE_TO) : (const void *)solve_to_kernel<false, false, false>);
         const void *kern_p = H > NC ? (wm ? crb_gmem_kernel(KW_SOLVE_TO_LONG_PERSIST) : (const void *)solve_to_kernel<false, true, true>)
@@ -2612,10 +2611,7 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
         if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, bytes);
         if (e != cudaSuccess || per_sm < 1) return cuda_check(ctx, e != cudaSuccess ? e : cudaErrorInvalidConfiguration, "occupancy");
         const long long Wr = (long long)per_sm * ctx->sm_count;
-        if (chunks < 0) {
-            const double waves = (double)NU / (double)Wr;
-            chunks = (NU >= 2 * Wr && waves / std::ceil(waves) < 0.95 && sp->iters >= 8 && !kp.trace) ? 4 : 0;
-        }
+        if (chunks < 0) chunks = (NU >= 2 * Wr && sp->iters >= 8 && !kp.trace) ? 10 : 0;
         chunks = std::min(chunks, std::max(sp->iters, 1));
         if (chunks >= 1) {
             const int m = sp->history, Np = (N + 3) & ~3;
@@ -2636,12 +2632,13 @@ crb_status crb_lbfgs_solve_dt(crb_ctx *ctx, const crb_solver_params *sp, int P, 
     }
     else {
         // IK scheduling: the persistent chunked kernel when the batch
-        // spans at least two waves of groups (sp->persist = -1: 4 iteration chunks), else one
-        // CTA per 32-seed group.  sp->persist = 0 forces the latter, k >= 1 k chunks.
+        // spans at least two waves of groups (sp->persist = -1: 16 iteration chunks, measured best
+        // of 2..25 at cfg 3), else one CTA per 32-seed group.  sp->persist = 0 forces the latter,
+        // k >= 1 k chunks.
         const int G = (S + NC - 1) / NC;
         const long long NGg = (long long)P * G;
         int chunks = sp->persist;
-        if (chunks < 0) chunks = (NGg >= 2 * W && sp->iters >= 8) ? 4 : 0;
+        if (chunks < 0) chunks = (NGg >= 2 * W && sp->iters >= 8) ? 16 : 0;
         chunks = std::min(chunks, std::max(sp->iters, 1));
         if (chunks >= 1) {
             const int m = sp->history, DC = D * NC;
