@@ -207,9 +207,8 @@ crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *robot);
 
 /* Upload n_env environments of cuboids: boxes[n_env * k_max], env e using its first
  * boxes_per_env[e] entries.  Disabled cuboids are compacted away (Alg. 10 skips them).  Also
- * builds the fp16 pair table of the small-world pre-screen and each cuboid's magnitude
- * max(|R^T t|, h) that sizes both pre-screens' rounding slack (cuboids beyond the fp16 range,
- * 3e4 m, always get the exact test).  Stream-ordered on the legacy stream: synchronises before
+ * builds each cuboid's world-frame AABB (centre, half extents widened by 1e-4 m + 1e-6 |.|) for
+ * the culling ahead of the exact tests.  Stream-ordered on the legacy stream: synchronises before
  * returning. */
 crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_per_env,
                          const crb_cuboid *boxes);

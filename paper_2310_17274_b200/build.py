@@ -18,10 +18,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-prec-div=false", "-prec-sqrt=false", "-Xcompiler", "-fPIC", f"-I{os.path.join(ROOT, 'include')}",
          "--expt-relaxed-constexpr"]
-# flush-to-zero in both units (round 2: the large-world build now runs the same fp16x2 bounding-sphere
-# screen as the small-world one and gains 2-3 % from it, profiles/r02_ksweep_ftz.txt; round 1 kept
-# it off there because the tensor-core screen lost 9 %).  One setting for every kernel: the
-# numerics of an environment no longer depend on which build the context picks.
+# flush-to-zero in both units (round 1 kept it off in the large-world unit because its tensor-core
+# screen lost 9 %; that screen is gone).  One setting for every kernel: the numerics of an
+# environment do not depend on which build the context picks.
 FTZ = {SRC: ["-ftz=true"], SRC_GMEM: ["-ftz=true"]}
 
 

@@ -14,7 +14,6 @@
 // P:n = line n of the paper; A* = readings listed in DESIGN.md.
 #pragma once
 #include <cstdint>
-#include <cuda_fp16.h>
 
 // Work counters of the world screen (tools/world_stats.py builds a separate library with 1).
 #ifndef CRB_STATS
@@ -1070,7 +1069,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         bool any = false;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            if (reload) {   // after the tensor-core screen: reload instead of holding it
+                            if (reload) {   // reload the centres instead of holding them across the culling loop
                                 const float4 c = m0 + u < rp.M ? s.sw[(m0 + u) * NC + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
                                 s2[u] = box_screen(c.x, c.y, c.z, b);
                             } else {
