@@ -60,3 +60,22 @@ def test_persistent_to_trace_and_long_horizon(native):
     outs = _solve_all(native, wl44, wl44.solver, [0, 2])
     for k in KEYS:
         assert torch.equal(outs[0][k], outs[1][k]), ("H=44", k)
+
+
+def test_persistent_degenerate(native):
+    """iters = 0 and iters < chunks (the chunk count clamps to iters), a single seed, and a batch
+    smaller than one wave: outputs equal one CTA per seed / group."""
+    wl = workload.franka_to(0, list(range(2)), S=3, H=16, iters=5)
+    for iters, chunks in ((0, 3), (2, 5), (5, 9)):
+        sp = dataclasses.replace(wl.solver, iters=iters)
+        outs = _solve_all(native, wl, sp, [0, chunks])
+        for k in KEYS:
+            assert torch.equal(outs[0][k], outs[1][k]), (iters, chunks, k)
+    ik = workload.franka_ik(0, [3], S=1, iters=4)
+    ctx = native.Context(0)
+    ctx.set_robot(ik.robot); ctx.set_world(ik.worlds); ctx.set_cost_params(ik.cost)
+    a = ctx.solve(dataclasses.replace(ik.solver, persist=0), T(ik.seeds), T(ik.goal), seed_outputs=True)
+    b = ctx.solve(dataclasses.replace(ik.solver, persist=7), T(ik.seeds), T(ik.goal), seed_outputs=True)
+    for k in ("seed_best_cost", "seed_best_traj", "best_cost", "best_traj"):
+        assert torch.equal(a[k], b[k]), ("IK", k)
+    ctx.close()
