@@ -268,10 +268,14 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
     // c, cbest, chunk_best, done
     const int SWA = 6 * Np, SWB = 2 * (m + 1) * Np + 160, SWT = SWA + SWB + 8;
     int *bcast = reinterpret_cast<int *>(smem + kp.lay.mbar) + 3;
-    int staged = -0x7fffffff, K = 0;
+    // the persistent kernel keeps its unit bookkeeping in shared memory (the staged environment in
+    // mbar[2], K in s.scal[6], the unit in mbar[3]) so the pass loop does not carry it in registers
+    int *envs = reinterpret_cast<int *>(smem + kp.lay.mbar) + 2, *Ks = reinterpret_cast<int *>(s.scal + 6);
+    int *PHs = Ks + 1;   // the pass loop's end (PERSIST), -1 after the chunked convergence exit
+    int K = 0;
     int unit = blockIdx.x;
     if (PERSIST) {
-        if (t == 0) *bcast = atomicAdd(kp.ik_flags, 1);
+        if (t == 0) { *bcast = atomicAdd(kp.ik_flags, 1); *envs = -0x7fffffff; }
         __syncthreads();
         unit = *bcast;
     }
@@ -280,9 +284,14 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
     const int p = u / kp.S;
     {
         const int env = kp.env ? kp.env[p] : 0;
-        if (staged == -0x7fffffff) K = stage_tables(kp, smem, env);
-        else if (env != staged) K = restage_world(kp, smem, env);
-        staged = env;
+        if (!PERSIST) K = stage_tables(kp, smem, env);
+        else {
+            const int staged = *envs;
+            if (staged == -0x7fffffff) K = stage_tables(kp, smem, env);
+            else if (env != staged) K = restage_world(kp, smem, env);
+            else K = *Ks;
+            if (t == 0) *Ks = K;
+        }
     }
     if (t < D) s.st[t] = kp.start[p * D + t];
     if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[p * kp.cp.gw + t / NC];
@@ -328,7 +337,14 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
         c = __ldcg(sc + 2); cbest = __ldcg(sc + 3); chunk_best = __ldcg(sc + 4); done = __float_as_int(__ldcg(sc + 5));
         __syncthreads();
     }
-    const unsigned pk1 = (unsigned)(kp.prob_base + p), psd = (unsigned)(kp.seed_base + (u - p * kp.S));
+    if (PERSIST) {
+        __syncthreads();   // every thread has read PHs of the previous unit
+        if (t == 0) *PHs = done ? -1 : pass_hi;
+        __syncthreads();
+    }
+    // the seed of this unit (PERSIST: re-derived from the broadcast unit where needed, so the pass
+    // loop does not carry it)
+    auto seed_u = [&]() { if (PERSIST) { const int un = *bcast; return un - (un / NU) * NU; } return u; };
     ParticleAcc pacc;
     pacc.reset();
     float tm = -INFINITY, tZ = 0.f;   // merged particle chunks of the current warm-up iteration
@@ -339,7 +355,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             if (i < N) { const float s0 = kp.s0_frac * (hi_e[e] - lo_e[e]); g[i] = s0 * s0; }   // B8
         }
     }
-    for (int pass = pass_lo; pass < (done ? pass_lo : pass_hi); ++pass) {
+    for (int pass = pass_lo; PERSIST ? pass < *PHs : pass < (done ? pass_lo : pass_hi); ++pass) {
         const bool part = pass < npart;
         const int pit = part ? pass / kp.pn : 0, pl = pass - pit * kp.pn;
         const int lpass = pass - npart;
@@ -350,7 +366,9 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             for (int e = 0; e < 2; ++e) {
                 const int i = t + e * NT;
                 if (i < N) {
-                    const float z = particle_normal(kp.rng_key, pk1, (unsigned)i, (unsigned)pl, (unsigned)pit, psd);
+                    const int su = seed_u(), sp_ = su / kp.S;
+                    const float z = particle_normal(kp.rng_key, (unsigned)(kp.prob_base + sp_), (unsigned)i, (unsigned)pl,
+                                                    (unsigned)pit, (unsigned)(kp.seed_base + (su - sp_ * kp.S)));
                     thA[i] = fminf(fmaxf(fmaf(sqrtf(g[i]), z, th[i]), lo_e[e]), hi_e[e]);
                 }
             }
@@ -359,22 +377,22 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
         if (a == 0) {
             const int it = (lpass - 1) / A;
             const int tj = trace_slot(kp, it);
-            if (tj >= 0) trace_to(kp, 0, u, it, tj, c, 0.f, 0.f, 0, 0.f);
+            if (tj >= 0) trace_to(kp, 0, seed_u(), it, tj, c, 0.f, 0.f, 0, 0.f);
             float sy;
             g0d = lbfgs_step_to(it, N, Np, m, th, g, thp, gp, dd, Sb, Yb, rho, syv, yyv, order, ring, s.red, ph, d_e, sy);
-            if (tj >= 0) trace_to(kp, 1, u, it, tj, c, g0d, sy, 0, 0.f);
+            if (tj >= 0) trace_to(kp, 1, seed_u(), it, tj, c, g0d, sy, 0, 0.f);
         }
         // ---- a1: candidate a = clip(theta + alpha_a d) (pass 0: theta_0 is already in thA)
         if (a >= 0) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int i = t + e * NT;
-                if (i < N) thA[i] = candidate(th[i], kp.alpha[a], d_e[e], lo_e[e], hi_e[e]);
+                if (i < N) thA[i] = candidate(th[i], kp.alpha[a], dd[i], lo_e[e], hi_e[e]);   // d from dd (the step's output)
             }
             __syncthreads();
         }
         // ---- a2..a10: one evaluation pass (cost only for particles)
-        eval_pass<MODE_TO, GMEM, LONG>(kp, smem, thA, K, H, a >= 0 ? dd : nullptr, !part);
+        eval_pass<MODE_TO, GMEM, LONG>(kp, smem, thA, PERSIST ? *Ks : K, H, a >= 0 ? dd : nullptr, !part);
         if (part) {
             // ---- f1 UPDATE, streamed over the particles of a chunk (Eqs. particle_1/2, B6), the
             // chunks merged in order (chunk_merge; totals in cg, unused during the warm-up)
@@ -452,7 +470,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             for (int e = 0; e < 2; ++e) {
                 const int i = t + e * NT;
                 if (i < N) {
-                    th[i] = candidate(th[i], kp.alpha[istar], d_e[e], lo_e[e], hi_e[e]);
+                    th[i] = candidate(th[i], kp.alpha[istar], dd[i], lo_e[e], hi_e[e]);
                     g[i] = cg[istar * Np + i];
                 }
             }
@@ -468,20 +486,28 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             }
             if (kp.trace) {
                 const int tj = trace_slot(kp, (lpass - 1) / A);
-                if (tj >= 0) trace_to(kp, 2, u, 0, tj, c, 0.f, 0.f, istar, cbest);
+                if (tj >= 0) trace_to(kp, 2, seed_u(), 0, tj, c, 0.f, 0.f, istar, cbest);
             }
             // ---- a14: "up to" iters in chunks (B20): every thread holds the same cbest, so the
             // exit is CTA-uniform
             if (kp.check_every > 0) {
                 const int it = (lpass - 1) / A + 1;   // iterations done
                 if (it % kp.check_every == 0) {
-                    if (!(cbest < chunk_best - kp.conv_rtol * fabsf(chunk_best))) { done = 1; break; }
+                    if (!(cbest < chunk_best - kp.conv_rtol * fabsf(chunk_best))) {   // (CTA-uniform)
+                        done = 1;
+                        if (PERSIST && t == 0) *PHs = -1;   // read after the barrier below
+                        break;
+                    }
                     chunk_best = cbest;
                 }
             }
         }
     }
     __syncthreads();
+    {   // (PERSIST: the unit re-derived from shared memory, not carried through the pass loop)
+    const int un = PERSIST ? *bcast : unit;
+    const int ch = PERSIST ? un / NU : 0, u = un - ch * NU;
+    const int done_ = PERSIST ? (*PHs == -1 ? 1 : 0) : done;
     if (ch == C - 1) {
         if (t == 0) kp.seed_best_cost[u] = cbest;
 #pragma unroll
@@ -496,7 +522,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
         if (t == 0) {
             float *sc = dst + SWA + SWB;
             __stcg(sc, __int_as_float(ring[0])); __stcg(sc + 1, __int_as_float(ring[1]));
-            __stcg(sc + 2, c); __stcg(sc + 3, cbest); __stcg(sc + 4, chunk_best); __stcg(sc + 5, __int_as_float(done));
+            __stcg(sc + 2, c); __stcg(sc + 3, cbest); __stcg(sc + 4, chunk_best); __stcg(sc + 5, __int_as_float(done_));
         }
         __syncthreads();
         if (t == 0) {
@@ -505,6 +531,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_kernel(const __grid_constant__
             const int v = ch + 1;
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
         }
+    }
     }
     if (!PERSIST) break;
     if (t == 0) *bcast = atomicAdd(kp.ik_flags, 1);
