@@ -680,6 +680,19 @@ __device__ __forceinline__ int nth_set_bit(unsigned m, int n) {
     return pos;
 }
 
+// Large worlds: the world items in decreasing cost of the previous pass (insertion sort of ord[n] by
+// cost[ord[.]], ties keep index order), by one thread at the pass start; out of line so that its
+// registers do not weigh on the pass (ord = wq, cost = wq + n)
+static __device__ __noinline__ void lpt_order(int *ord, int n) {
+    const int *cost = ord + n;
+    for (int i = 1; i < n; ++i) {
+        const int g = ord[i], cg = cost[g];
+        int j = i - 1;
+        while (j >= 0 && (cost[ord[j]] < cg || (cost[ord[j]] == cg && ord[j] > g))) { ord[j + 1] = ord[j]; --j; }
+        ord[j + 1] = g;
+    }
+}
+
 // order-preserving float <-> int map (for warp min / max with __reduce_{min,max}_sync); an involution
 __device__ __forceinline__ int f2o(float x) {
     const int i = __float_as_int(x);
@@ -814,15 +827,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         // then the short self items); ties keep index order.  Which warp takes which item never
         // changes a result (fixed-order merges).
         const int nwg = (rp.M + 3) >> 2;
-        if (GMEM && nwg <= 32) {   // large worlds only: few, long world items
-            int *ord = s.wq, *cost = s.wq + nwg;
-            for (int i = 1; i < nwg; ++i) {
-                const int g = ord[i], cg = cost[g];
-                int j = i - 1;
-                while (j >= 0 && (cost[ord[j]] < cg || (cost[ord[j]] == cg && ord[j] > g))) { ord[j + 1] = ord[j]; --j; }
-                ord[j + 1] = g;
-            }
-        }
+        if (GMEM && nwg <= 32) lpt_order(s.wq, nwg);   // large worlds only: few, long world items
     }
 
     for (int win = 0; win < nwin; ++win) {
@@ -1027,12 +1032,9 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             if (item < nwg) {
                 const int grp = GMEM ? s.wq[item] : item;
                 const int m0 = grp << 2;
-                struct ItemCost {   // large worlds: the group's cost for the next pass's order (lane 0)
-                    int *dst; long long t0;
-                    __device__ ~ItemCost() {
-                        if (GMEM && (threadIdx.x & 31) == 0) *dst = (int)min(clock64() - t0, (long long)0x3fffffff);
-                    }
-                } item_cost{s.wq + nwg + grp, GMEM ? clock64() : 0ll};
+                // large worlds: the group's cost for the next pass's order (lane 0); the start clock
+                // waits in the cost slot itself, so no register carries it through the item
+                if (GMEM && lane == 0) s.wq[nwg + grp] = (int)clock();
                 float cx[4], cy[4], cz[4], th2[4], sp[4];
                 int dirs[4];
 #pragma unroll
@@ -1182,6 +1184,10 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     }
                 }
                 s.sg[m0 * NC + lane].w = gsum;
+                if (GMEM && lane == 0) {
+                    const unsigned dt = (unsigned)clock() - (unsigned)s.wq[nwg + grp];
+                    s.wq[nwg + grp] = (int)min(dt, 0x3fffffffu);
+                }
             } else {
                 const uint4 B = blk[item - nwg];
                 // Block culling: the block's first spheres lie on one
