@@ -22,10 +22,12 @@
 #if CRB_STATS
 static __device__ unsigned long long g_crb_stats[32];   // one copy per translation unit
 #define CRB_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_crb_stats[i], (unsigned long long)(v)); } while (0)
+#define CRB_STAT_T(i, v) atomicAdd(&g_crb_stats[i], (unsigned long long)(v))   // every calling thread
 // per-phase critical-path clocks of a pass as thread 0 sees them (slots 16..24, passes in 25)
 #define CRB_PHASE(i) do { if (threadIdx.x == 0) { const long long t_ = clock64(); atomicAdd(&g_crb_stats[16 + (i)], (unsigned long long)(t_ - t_ph)); t_ph = t_; } } while (0)
 #else
 #define CRB_STAT(i, v) do { } while (0)
+#define CRB_STAT_T(i, v) do { } while (0)
 #define CRB_PHASE(i) do { } while (0)
 #endif
 
@@ -38,6 +40,31 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 // penetration (1), or the plain d < R test throughout (0)
 #ifndef CRB_SELF_PRUNE
 #define CRB_SELF_PRUNE 1
+#endif
+
+// Sweep directions whose half-segment cannot reach the cuboid (a conservative segment-AABB bound
+// in the cuboid frame) skip the sample march (1), or march anyway (0).  Measured at K = 20: 64 % of
+// the marched directions are skippable, but a march averages 1.1 samples, so no gain (and more
+// spills in the callers of the out-of-line box_slow); kept for the statistics build
+#ifndef CRB_SEG_SKIP
+#define CRB_SEG_SKIP 0
+#endif
+
+// Slow-path entries (a flagged sphere, slot and cuboid) batched across cuboids and work items into
+// full warp rounds, with the group epilogues deferred until their entries are flushed (1), or one
+// compacted round per flagged cuboid (0)
+// (default: the large-world unit only -- measured: dense K = 1000 +14 %, K = 20 -4 %)
+#ifndef CRB_SLOW_BATCH
+#if defined(CRB_PART) && CRB_PART == 1
+#define CRB_SLOW_BATCH 1
+#else
+#define CRB_SLOW_BATCH 0
+#endif
+#endif
+
+// FK chain software-pipelined over frames (1) or loading each frame's record in its iteration (0)
+#ifndef CRB_FK_PF
+#define CRB_FK_PF 0
 #endif
 
 // Unroll factor of the once-per-pass per-slot loops (link sums, pose terms, world-group sum): code
@@ -529,11 +556,32 @@ __device__ __forceinline__ void fk_chain(const RobotPack &rp, const Smem &s) {
         float *dst = s.lt + (r * 4) * NC + lane;
         dst[0] = cur.x; dst[NC] = cur.y; dst[2 * NC] = cur.z; dst[3 * NC] = cur.w;
     }
+#if CRB_FK_PF
+    // software pipelined: frame l + 1's record and joint terms load while frame l composes (they do
+    // not depend on the chain), so the shared-memory latency leaves the serial path
+    float4 nf0, nf1, nf2;
+    int4 nmd;
+    float njc, njs, njt;
+    auto ld = [&](int l) {
+        nf0 = L4[4 * l]; nf1 = L4[4 * l + 1]; nf2 = L4[4 * l + 2];
+        nmd = reinterpret_cast<const int4 *>(L4)[4 * l + 3];
+        const float *jc = s.scs + l * 3 * NC + lane;
+        njc = jc[0]; njs = jc[NC]; njt = jc[2 * NC];
+    };
+    if (rp.L > 1) ld(1);
+#endif
     for (int l = 1; l < rp.L; ++l) {
+#if CRB_FK_PF
+        const float4 f0 = nf0, f1 = nf1, f2 = nf2;
+        const int4 md = nmd;
+        const float jcs = njc, jsn = njs, jt = njt;
+        if (l + 1 < rp.L) ld(l + 1);
+#else
         const float4 f0 = L4[4 * l], f1 = L4[4 * l + 1], f2 = L4[4 * l + 2];   // rows of F (3x4)
         const int4 md = reinterpret_cast<const int4 *>(L4)[4 * l + 3];         // parent, type, dof
         const float *jc = s.scs + l * 3 * NC + lane;                              // (c, s, t) of frame l
         const float jcs = jc[0], jsn = jc[NC], jt = jc[2 * NC];
+#endif
         const int parent = md.x, dof = md.z;
         float4 pr = cur;
         if (parent != l - 1) {
@@ -703,7 +751,7 @@ __device__ __forceinline__ float o2f(int i) { return __int_as_float(i ^ ((i >> 3
 // Rare path: the hit's activation and gradient, then the backward / forward marches (A6-A12):
 // L = |n - c|, bound = L/2, j = J0 (r' on a hit, else sd), at most n_s samples p = c + (j/L)(n - c);
 // a hit adds phi and (1 - kappa) phi' (-grad sd) and jumps r', a miss jumps sd.
-static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const float *boxes, int k, float cx, float cy,
+__device__ __forceinline__ float4 box_slow_val(const float4 *p, const float *boxes, int k, float cx, float cy,
                                       float cz, float s2, float rp, int dirs, float eta, float inv_eta, int steps) {
     const BoxView b = load_box(boxes, k);              // reloaded here: keeps the screen loop spill-free
     float E = 0.f, Gx = 0.f, Gy = 0.f, Gz = 0.f;
@@ -734,14 +782,39 @@ static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const
             float lqx, lqy, lqz;
             box_local(b, q.x, q.y, q.z, lqx, lqy, lqz);
             const float dlx = lqx - lcx, dly = lqy - lcy, dlz = lqz - lcz;
+            // Every sample lies on l(c) + kappa dl with kappa in [0, 1/2] (j < bound = L/2), so its
+            // exact sd is at least the distance between the cuboid and the AABB of that
+            // half-segment.  When this bound exceeds r' by a margin far above the fp32 rounding of
+            // the samples and of their sd, no sample can hit: the march would add nothing (misses
+            // only move j), so it is skipped -- the result is bitwise the march's.  NaN: no skip.
+            const float hx = 0.5f * dlx, hy = 0.5f * dly, hz = 0.5f * dlz;
+            const float gpx = fmaxf(fmaxf(fminf(lcx, lcx + hx) - b.h.x, -b.h.x - fmaxf(lcx, lcx + hx)), 0.f);
+            const float gpy = fmaxf(fmaxf(fminf(lcy, lcy + hy) - b.h.y, -b.h.y - fmaxf(lcy, lcy + hy)), 0.f);
+            const float gpz = fmaxf(fmaxf(fminf(lcz, lcz + hz) - b.h.z, -b.h.z - fmaxf(lcz, lcz + hz)), 0.f);
+            const float mg = rp + 1e-5f * (1.f + fabsf(lcx) + fabsf(lcy) + fabsf(lcz) + fabsf(dlx) + fabsf(dly) + fabsf(dlz));
+            const bool noreach = gpx * gpx + gpy * gpy + gpz * gpz > mg * mg;
+            CRB_STAT_T(14, 1);
+            CRB_STAT_T(27, noreach ? 1 : 0);
+#if CRB_SEG_SKIP && !CRB_STATS
+            if (noreach) continue;
+#endif
+#if CRB_STATS
+            bool anyhit = false;
+#endif
             float j = J0;
             for (int st = 0; st < steps; ++st) {
                 if (j >= bound) break;
+#if CRB_STATS
+                CRB_STAT_T(26, 1);
+#endif
                 const float kap = j * iL;
                 float gx, gy, gz, glx, gly, glz;
                 const float sd = box_sdf_local(b, fmaf(kap, dlx, lcx), fmaf(kap, dly, lcy), fmaf(kap, dlz, lcz), glx, gly, glz);
                 const float dp = rp - sd;
                 if (dp > 0.f) {
+#if CRB_STATS
+                    anyhit = true;
+#endif
                     box_grad_world(b, glx, gly, glz, gx, gy, gz);
                     float dphi;
                     E += activation(dp, eta, inv_eta, dphi);
@@ -752,12 +825,47 @@ static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const
                     j += sd;
                 }
             }
+#if CRB_STATS
+            CRB_STAT_T(15, anyhit ? 1 : 0);
+            CRB_STAT_T(28, (anyhit && noreach) ? 1 : 0);   // a skip that would have lost a hit: must stay 0
+#endif
         }
     }
+    return make_float4(Gx, Gy, Gz, E);
+}
+
+// ... added to the entry's accumulator (out of line: keeps the screen loop's registers free)
+static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const float *boxes, int k, float cx, float cy,
+                                             float cz, float s2, float rp, int dirs, float eta, float inv_eta, int steps) {
+    const float4 c = box_slow_val(p, boxes, k, cx, cy, cz, s2, rp, dirs, eta, inv_eta, steps);
     float4 a = *acc;
-    a.x += Gx; a.y += Gy; a.z += Gz; a.w += E;
+    a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
     *acc = a;
 }
+
+// A13 speed metric of a sphere from its neighbours a (previous slot) and z (next slot), scaled by
+// 1 / (2 dt); one function for the work item's set-up and its deferred epilogue (bitwise equal)
+__device__ __forceinline__ float sphere_speed(float4 a, float4 z, float inv_2dt) {
+    const float dx = z.x - a.x, dy = z.y - a.y, dz = z.z - a.z;
+    return sqrtf(dx * dx + dy * dy + dz * dz) * inv_2dt;
+}
+
+#if CRB_SLOW_BATCH
+// One slow-path entry (sphere m at slot src against cuboid k): its sweep directions and screen value
+// exactly as the work item's set-up and exact test formed them, then the box_slow contribution
+static __device__ __noinline__ float4 slow_entry(const float4 *sw, const float4 *sph, const float *boxes, int m,
+                                                 int src, int k, int base, int H, bool to, bool sweepf, float eta,
+                                                 float inv_eta, int steps) {
+    const float4 *pc = sw + m * NC + src;
+    const float4 c = pc[0];
+    const float rpr = sph[m].w + eta;
+    float maxb2;
+    const bool hp = to && src > 0 && base + src < H, hn = to && base + src + 1 < H && src + 1 < NC;
+    const int dr = sweep_dirs(hp ? pc[-1] : c, hn ? pc[1] : c, c.x, c.y, c.z, rpr, hp, hn, sweepf, maxb2);
+    const BoxView b = load_box(boxes, k);
+    return box_slow_val(pc, boxes, k, c.x, c.y, c.z, box_screen(c.x, c.y, c.z, b), rpr, dr, eta, inv_eta, steps);
+}
+#endif
 
 // One evaluation pass over the 32 slots.  Inputs already in shared memory:
 //   TO: the candidate V[H][D] in `thA`, start in s.st, goal in s.goal[7][32].
@@ -1017,11 +1125,86 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
 #if CRB_STATS
         const long long t_q0 = clock64();
 #endif
+#if CRB_SLOW_BATCH
+        // Pending slow entries, one per lane below npend (src | m << 5 | k << 15), and the work items
+        // whose epilogue waits for them, one per lane below npit.  Lanes fill in flag order: per
+        // cuboid in increasing k, so every accumulator (one item's sphere at one slot) still sees
+        // its additions in increasing k, bitwise as a flush per cuboid would.
+        int npend = 0, npit = 0, pit = 0;
+        unsigned pend = 0u;
+        // the group epilogue: the speed-scaled world gradient, and the group's cost into the .w of
+        // its first sphere (unused by the backward), which the merge sums in index order
+        auto epilogue = [&](int grp, const float *spv) {
+            const int m0 = grp << 2;
+            float gsum = 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int m = m0 + u;
+                if (m < rp.M) {
+                    const float sc = cf.beta_world * spv[u];
+                    float4 g = s.sg[m * NC + lane];
+                    gsum += sc * g.w;
+                    s.sg[m * NC + lane] = make_float4(sc * g.x, sc * g.y, sc * g.z, 0.f);
+                }
+            }
+            s.sg[m0 * NC + lane].w = gsum;
+        };
+        // one warp round over the pending entries: contributions in parallel, then added in lane
+        // order among the lanes that share an accumulator; then the deferred epilogues
+        auto flush = [&]() {
+            if (npend) {
+                float4 ctr = make_float4(0.f, 0.f, 0.f, 0.f);
+                int key = -1 - lane;   // unique for the idle lanes
+                if (lane < npend) {
+                    const int src = pend & 31, m = (pend >> 5) & 1023, k = (int)(pend >> 15);
+                    key = m * NC + src;
+                    ctr = slow_entry(s.sw, sph, s.boxes, m, src, k, base, H, to, sweepf, cf.eta, cf.inv_eta,
+                                     cf.sweep_steps);
+                }
+                const unsigned mm = __match_any_sync(FULL, key);
+                const int rank = __popc(mm & ((1u << lane) - 1u));
+                const int maxr = __reduce_max_sync(FULL, (unsigned)rank);
+                for (int r = 0; r <= maxr; ++r) {
+                    if (lane < npend && rank == r) {
+                        float4 a = s.sg[key];
+                        a.x += ctr.x; a.y += ctr.y; a.z += ctr.z; a.w += ctr.w;
+                        s.sg[key] = a;
+                    }
+                    __syncwarp();
+                }
+                npend = 0;
+            }
+#pragma unroll 1
+            for (int i = 0; i < npit; ++i) {
+                const int grp = __shfl_sync(FULL, pit, i);
+                float spv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int m = (grp << 2) + u;
+                    spv[u] = 0.f;
+                    if (m < rp.M) {
+                        spv[u] = 1.f;
+                        if (speedf) {
+                            const float4 *p = s.sw + m * NC + lane;
+                            const float4 c = p[0];
+                            spv[u] = sphere_speed(hasp ? p[-1] : c, hasn ? p[1] : c, s.tdp[0]);
+                        }
+                    }
+                }
+                epilogue(grp, spv);
+            }
+            npit = 0;
+        };
+#endif
         for (;;) {
             int item = 0;
             if (lane == 0) item = atomicAdd(qctr, 1);
             item = __shfl_sync(FULL, item, 0);
+#if CRB_SLOW_BATCH
+            if (item >= nitems) { flush(); __syncwarp(); break; }
+#else
             if (item >= nitems) break;
+#endif
 #if CRB_STATS
             const long long t_start = clock64();
             struct StatT {
@@ -1050,10 +1233,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                         cx[u] = c.x; cy[u] = c.y; cz[u] = c.z;
                         s.sg[m * NC + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
                         float spd = 1.f;
-                        if (speedf) {   // A13: central difference, missing neighbour -> w_h
-                            const float dx = z.x - a.x, dy = z.y - a.y, dz = z.z - a.z;
-                            spd = sqrtf(dx * dx + dy * dy + dz * dz) * s.tdp[0];
-                        }
+                        if (speedf) spd = sphere_speed(a, z, s.tdp[0]);   // A13: central difference, missing neighbour -> w_h
                         sp[u] = spd;
                         const float r = sph[m].w;
                         const float rpr = r + cf.eta;   // Alg. 10 "sph.radius += eta"
@@ -1091,6 +1271,21 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                             const int n0 = __popc(bal[0]), n1 = __popc(bal[1]), n2 = __popc(bal[2]);
                             const int tot = n0 + n1 + n2 + __popc(bal[3]);
                             CRB_STAT(3, tot);
+#if CRB_SLOW_BATCH
+                            // append the flagged entries to the pending lanes; a full warp flushes
+#pragma unroll 1
+                            for (int done = 0; done < tot;) {
+                                const int take = min(32 - npend, tot - done);
+                                if (lane >= npend && lane < npend + take) {
+                                    int u = 0, r = lane - npend + done;
+                                    if (r >= n0) { r -= n0; u = 1; if (r >= n1) { r -= n1; u = 2; if (r >= n2) { r -= n2; u = 3; } } }
+                                    const unsigned bm = u == 0 ? bal[0] : u == 1 ? bal[1] : u == 2 ? bal[2] : bal[3];
+                                    pend = (unsigned)nth_set_bit(bm, r) | ((unsigned)(m0 + u) << 5) | ((unsigned)k << 15);
+                                }
+                                npend += take; done += take;
+                                if (npend == 32) flush();
+                            }
+#else
                             for (int e = lane; e - lane < tot; e += 32) {
                                 if (e >= tot) continue;
                                 int u = 0, r = e;
@@ -1111,6 +1306,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                             // lanes wrote other lanes' accumulators: order those writes before any
                             // later access to them (the next cuboid's flush, the group's own reads)
                             __syncwarp();
+#endif
                         }
                 };
                 if (__any_sync(FULL, th2[0] > 0.f || th2[1] > 0.f || th2[2] > 0.f || th2[3] > 0.f)) {
@@ -1170,6 +1366,15 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     }
                     }
                 }
+#if CRB_SLOW_BATCH
+                // the epilogue now if no entry of this item is pending, else when they are flushed
+                if (npend == 0) {
+                    epilogue(grp, sp);
+                } else {
+                    if (lane == npit) pit = grp;
+                    ++npit;
+                }
+#else
                 // the group's cost goes to the .w of its first sphere (unused by the backward):
                 // the merge sums the groups in index order, whichever warp took them
                 float gsum = 0.f;
@@ -1184,6 +1389,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                     }
                 }
                 s.sg[m0 * NC + lane].w = gsum;
+#endif
                 if (GMEM && lane == 0) {
                     const unsigned dt = (unsigned)clock() - (unsigned)s.wq[nwg + grp];
                     s.wq[nwg + grp] = (int)min(dt, 0x3fffffffu);

@@ -55,6 +55,9 @@ def run(name, wl):
     ex = max(s[0], 1)
     print(f"{name}: pairs {s[0]}  pre-screen-flagged {s[1] / ex:.3f}  exact-flagged {s[2] / ex:.3f}  "
           f"entries/pair {s[3] / ex:.3f}", flush=True)
+    nd = max(s[14], 1)
+    print(f"   sweep directions {s[14]}: with a hit sample {s[15] / nd:.3f}, segment bound skips {s[27] / nd:.3f} "
+          f"(skips that would lose a hit: {s[28]}), samples per direction {s[26] / nd:.2f}", flush=True)
     wp = max(s[10], 1)
     print(f"   queue: world item {s[4] / max(s[8], 1):.0f} cyc x {s[8] / wp * 8:.1f}/pass, self item "
           f"{s[5] / max(s[9], 1):.0f} cyc x {s[9] / wp * 8:.1f}/pass; per warp-pass: in queue {s[7] / wp:.0f} cyc, "
