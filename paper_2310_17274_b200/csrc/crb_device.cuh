@@ -834,15 +834,6 @@ __device__ __forceinline__ float4 box_slow_val(const float4 *p, const float *box
     return make_float4(Gx, Gy, Gz, E);
 }
 
-// ... added to the entry's accumulator (out of line: keeps the screen loop's registers free)
-static __device__ __noinline__ void box_slow(float4 *acc, const float4 *p, const float *boxes, int k, float cx, float cy,
-                                             float cz, float s2, float rp, int dirs, float eta, float inv_eta, int steps) {
-    const float4 c = box_slow_val(p, boxes, k, cx, cy, cz, s2, rp, dirs, eta, inv_eta, steps);
-    float4 a = *acc;
-    a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
-    *acc = a;
-}
-
 // A13 speed metric of a sphere from its neighbours a (previous slot) and z (next slot), scaled by
 // 1 / (2 dt); one function for the work item's set-up and its deferred epilogue (bitwise equal)
 __device__ __forceinline__ float sphere_speed(float4 a, float4 z, float inv_2dt) {
@@ -850,7 +841,6 @@ __device__ __forceinline__ float sphere_speed(float4 a, float4 z, float inv_2dt)
     return sqrtf(dx * dx + dy * dy + dz * dz) * inv_2dt;
 }
 
-#if CRB_SLOW_BATCH
 // One slow-path entry (sphere m at slot src against cuboid k): its sweep directions and screen value
 // exactly as the work item's set-up and exact test formed them, then the box_slow contribution
 static __device__ __noinline__ float4 slow_entry(const float4 *sw, const float4 *sph, const float *boxes, int m,
@@ -865,7 +855,6 @@ static __device__ __noinline__ float4 slow_entry(const float4 *sw, const float4 
     const BoxView b = load_box(boxes, k);
     return box_slow_val(pc, boxes, k, c.x, c.y, c.z, box_screen(c.x, c.y, c.z, b), rpr, dr, eta, inv_eta, steps);
 }
-#endif
 
 // One evaluation pass over the 32 slots.  Inputs already in shared memory:
 //   TO: the candidate V[H][D] in `thA`, start in s.st, goal in s.goal[7][32].
@@ -1293,15 +1282,13 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                                 const unsigned bm = u == 0 ? bal[0] : u == 1 ? bal[1] : u == 2 ? bal[2] : bal[3];
                                 const int src = nth_set_bit(bm, r);   // the r-th flagged slot
                                 const int m = m0 + u;
-                                const float4 *pc = s.sw + m * NC + src;
-                                const float4 c = pc[0];
-                                const float rpr = sph[m].w + cf.eta;
-                                float maxb2;
-                                const bool hp = to && src > 0 && base + src < H, hn = to && base + src + 1 < H && src + 1 < NC;
-                                const int dr = sweep_dirs(hp ? pc[-1] : c, hn ? pc[1] : c, c.x, c.y, c.z, rpr, hp, hn,
-                                                          sweepf, maxb2);
-                                box_slow(s.sg + m * NC + src, pc, s.boxes, k, c.x, c.y, c.z, box_screen(c.x, c.y, c.z, b),
-                                         rpr, dr, cf.eta, cf.inv_eta, cf.sweep_steps);
+                                // (the same out-of-line entry function as the batched rounds of the
+                                // large-world build: bitwise the same contribution in both builds)
+                                const float4 ctr = slow_entry(s.sw, sph, s.boxes, m, src, k, base, H, to, sweepf, cf.eta,
+                                                              cf.inv_eta, cf.sweep_steps);
+                                float4 a = s.sg[m * NC + src];
+                                a.x += ctr.x; a.y += ctr.y; a.z += ctr.z; a.w += ctr.w;
+                                s.sg[m * NC + src] = a;
                             }
                             // lanes wrote other lanes' accumulators: order those writes before any
                             // later access to them (the next cuboid's flush, the group's own reads)
