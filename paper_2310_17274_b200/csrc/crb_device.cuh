@@ -62,11 +62,6 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #endif
 #endif
 
-// FK chain software-pipelined over frames (1) or loading each frame's record in its iteration (0)
-#ifndef CRB_FK_PF
-#define CRB_FK_PF 0
-#endif
-
 // Unroll factor of the once-per-pass per-slot loops (link sums, pose terms, world-group sum): code
 // size against the instruction cache
 #ifndef CRB_COLD_UNROLL
@@ -556,32 +551,11 @@ __device__ __forceinline__ void fk_chain(const RobotPack &rp, const Smem &s) {
         float *dst = s.lt + (r * 4) * NC + lane;
         dst[0] = cur.x; dst[NC] = cur.y; dst[2 * NC] = cur.z; dst[3 * NC] = cur.w;
     }
-#if CRB_FK_PF
-    // software pipelined: frame l + 1's record and joint terms load while frame l composes (they do
-    // not depend on the chain), so the shared-memory latency leaves the serial path
-    float4 nf0, nf1, nf2;
-    int4 nmd;
-    float njc, njs, njt;
-    auto ld = [&](int l) {
-        nf0 = L4[4 * l]; nf1 = L4[4 * l + 1]; nf2 = L4[4 * l + 2];
-        nmd = reinterpret_cast<const int4 *>(L4)[4 * l + 3];
-        const float *jc = s.scs + l * 3 * NC + lane;
-        njc = jc[0]; njs = jc[NC]; njt = jc[2 * NC];
-    };
-    if (rp.L > 1) ld(1);
-#endif
     for (int l = 1; l < rp.L; ++l) {
-#if CRB_FK_PF
-        const float4 f0 = nf0, f1 = nf1, f2 = nf2;
-        const int4 md = nmd;
-        const float jcs = njc, jsn = njs, jt = njt;
-        if (l + 1 < rp.L) ld(l + 1);
-#else
         const float4 f0 = L4[4 * l], f1 = L4[4 * l + 1], f2 = L4[4 * l + 2];   // rows of F (3x4)
         const int4 md = reinterpret_cast<const int4 *>(L4)[4 * l + 3];         // parent, type, dof
         const float *jc = s.scs + l * 3 * NC + lane;                              // (c, s, t) of frame l
         const float jcs = jc[0], jsn = jc[NC], jt = jc[2 * NC];
-#endif
         const int parent = md.x, dof = md.z;
         float4 pr = cur;
         if (parent != l - 1) {
