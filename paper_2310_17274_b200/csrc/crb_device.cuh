@@ -679,12 +679,15 @@ __device__ __forceinline__ int sweep_dirs(float4 qp, float4 qn, float cx, float 
 // Cheap screening test of one box: returns s2 = sd^2 outside (0 inside), no square root.  The
 // box matters iff s2 < thr2: a discrete hit (sd < r') or a possible sweep sample (sd < the larger
 // half-segment).
-__device__ __forceinline__ float box_screen(float cx, float cy, float cz, const BoxView &b) {
-    float lx, ly, lz;
-    box_local(b, cx, cy, cz, lx, ly, lz);
+__device__ __forceinline__ float box_screen_local(float lx, float ly, float lz, const BoxView &b) {
     const float mx = fmaxf(fabsf(lx) - b.h.x, 0.f), my = fmaxf(fabsf(ly) - b.h.y, 0.f),
                 mz = fmaxf(fabsf(lz) - b.h.z, 0.f);
     return fmaf(mx, mx, fmaf(my, my, mz * mz));
+}
+__device__ __forceinline__ float box_screen(float cx, float cy, float cz, const BoxView &b) {
+    float lx, ly, lz;
+    box_local(b, cx, cy, cz, lx, ly, lz);
+    return box_screen_local(lx, ly, lz, b);
 }
 
 // Position of the n-th (0-based) set bit of m (n < popc(m)): a 5-step popc bisection, branch-free
@@ -725,15 +728,18 @@ __device__ __forceinline__ float o2f(int i) { return __int_as_float(i ^ ((i >> 3
 // Rare path: the hit's activation and gradient, then the backward / forward marches (A6-A12):
 // L = |n - c|, bound = L/2, j = J0 (r' on a hit, else sd), at most n_s samples p = c + (j/L)(n - c);
 // a hit adds phi and (1 - kappa) phi' (-grad sd) and jumps r', a miss jumps sd.
-__device__ __forceinline__ float4 box_slow_val(const float4 *p, const float *boxes, int k, float cx, float cy,
-                                      float cz, float s2, float rp, int dirs, float eta, float inv_eta, int steps) {
-    const BoxView b = load_box(boxes, k);              // reloaded here: keeps the screen loop spill-free
+// (lcx, lcy, lcz: the centre in the cuboid frame, box_local(b, c), formed once by the caller for the
+// screen value s2, the hit and the sweep samples)
+__device__ __forceinline__ float4 box_slow_val(const float4 *p, const BoxView &b, float lcx, float lcy, float lcz,
+                                               float cx, float cy, float cz, float s2, float rp, int dirs, float eta,
+                                               float inv_eta, int steps) {
     float E = 0.f, Gx = 0.f, Gy = 0.f, Gz = 0.f;
     const bool hit = s2 < rp * rp;                     // inside (s2 = 0) or within r'
     float sd0;
     if (hit) {
-        float gx, gy, gz;
-        sd0 = box_sdf_grad(b, cx, cy, cz, gx, gy, gz);
+        float gx, gy, gz, glx, gly, glz;
+        sd0 = box_sdf_local(b, lcx, lcy, lcz, glx, gly, glz);
+        box_grad_world(b, glx, gly, glz, gx, gy, gz);
         float dphi;
         E += activation(rp - sd0, eta, inv_eta, dphi);
         Gx -= dphi * gx; Gy -= dphi * gy; Gz -= dphi * gz;
@@ -742,8 +748,6 @@ __device__ __forceinline__ float4 box_slow_val(const float4 *p, const float *box
     }
     if (dirs) {
         const float J0 = (rp - sd0 > 0.f) ? rp : sd0;
-        float lcx, lcy, lcz;
-        box_local(b, cx, cy, cz, lcx, lcy, lcz);
 #pragma unroll 1
         for (int dir = 0; dir < 2; ++dir) {
             if (!(dirs & (1 << dir))) continue;
@@ -827,7 +831,10 @@ static __device__ __noinline__ float4 slow_entry(const float4 *sw, const float4 
     const bool hp = to && src > 0 && base + src < H, hn = to && base + src + 1 < H && src + 1 < NC;
     const int dr = sweep_dirs(hp ? pc[-1] : c, hn ? pc[1] : c, c.x, c.y, c.z, rpr, hp, hn, sweepf, maxb2);
     const BoxView b = load_box(boxes, k);
-    return box_slow_val(pc, boxes, k, c.x, c.y, c.z, box_screen(c.x, c.y, c.z, b), rpr, dr, eta, inv_eta, steps);
+    float lx, ly, lz;
+    box_local(b, c.x, c.y, c.z, lx, ly, lz);   // once: the screen value, the hit and the sweep samples
+    return box_slow_val(pc, b, lx, ly, lz, c.x, c.y, c.z, box_screen_local(lx, ly, lz, b), rpr, dr, eta, inv_eta,
+                        steps);
 }
 
 // One evaluation pass over the 32 slots.  Inputs already in shared memory:
