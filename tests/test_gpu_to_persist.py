@@ -79,3 +79,28 @@ def test_persistent_degenerate(native):
     for k in ("seed_best_cost", "seed_best_traj", "best_cost", "best_traj"):
         assert torch.equal(a[k], b[k]), ("IK", k)
     ctx.close()
+
+
+def test_persistent_large_world_build_bitwise(native):
+    """The large-world (GMEM) build -- cuboid table in global memory, slow-path entries batched
+    across cuboids and work items -- under the persistent schedule: every output
+    bitwise equal to one CTA per seed, and, on the small environments, to the shared-memory build
+    (one round per flagged cuboid).  A dense 1000-cuboid environment is in the list, so the context
+    runs the GMEM kernels for every environment."""
+    wl = workload.franka_to(0, list(range(6)), S=8, H=32, iters=12)
+    dense = workload.franka_to(0, [0], S=8, H=32, n_boxes=1000, iters=12, dense=True)
+    big = dataclasses.replace(wl, worlds=list(wl.worlds) + list(dense.worlds))
+    assert max(w.n_boxes for w in big.worlds) >= 1000
+    env = np.array(wl.env, np.int32)
+    env[-2:] = len(big.worlds) - 1                      # two problems in the dense world
+    big = dataclasses.replace(big, env=env)
+    sp = wl.solver
+    outs = _solve_all(native, big, sp, [0, 1, 3])
+    for o in outs[1:]:
+        for k in KEYS:
+            assert torch.equal(outs[0][k], o[k]), ("persist", k)
+    assert torch.isfinite(outs[0]["seed_best_cost"]).all()
+    small = _solve_all(native, wl, sp, [0])[0]        # shared-memory build on the small worlds
+    for k in ("seed_best_cost", "seed_best_traj"):    # problems 0..3 keep their small environments
+        a, b = outs[0][k].reshape(6, 8, -1)[:4], small[k].reshape(6, 8, -1)[:4]
+        assert torch.equal(a, b), ("builds", k)
