@@ -206,10 +206,11 @@ int crb_abi_sizes(int *out, int n);
 crb_status crb_set_robot(crb_ctx *ctx, const crb_robot_desc *robot);
 
 /* Upload n_env environments of cuboids: boxes[n_env * k_max], env e using its first
- * boxes_per_env[e] entries.  Disabled cuboids are compacted away (Alg. 10 skips them).  Also
+ * boxes_per_env[e] entries.  k_max <= CRB_MAX_CUBOIDS, else CRB_E_SHAPE (nothing uploaded).  Disabled cuboids are compacted away (Alg. 10 skips them).  Also
  * builds each cuboid's world-frame AABB (centre, half extents widened by 1e-4 m + 1e-6 |.|) for
  * the culling ahead of the exact tests.  Stream-ordered on the legacy stream: synchronises before
  * returning. */
+#define CRB_MAX_CUBOIDS 131071   /* cuboids per environment (17-bit index in the slow-path entries) */
 crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_per_env,
                          const crb_cuboid *boxes);
 

@@ -2404,6 +2404,8 @@ crb_status crb_set_world(crb_ctx *ctx, int n_env, int k_max, const int *boxes_pe
     crb_status st = enter(ctx);
     if (st != CRB_OK) return st;
     if (n_env < 1 || k_max < 0 || !boxes_per_env || (k_max > 0 && !boxes)) return fail(ctx, CRB_E_ARG, "bad world arguments");
+    // the large-world slow path packs (slot, sphere, cuboid) into 32 bits: 5 + 10 + 17
+    if (k_max > CRB_MAX_CUBOIDS) return fail(ctx, CRB_E_SHAPE, "k_max > CRB_MAX_CUBOIDS (131071)");
     std::vector<float> packed((size_t)n_env * std::max(k_max, 1) * 16, 0.f);
     // world-frame AABB of each enabled cuboid (crb_device.cuh "World culling"): centre and half
     // extents e_i = sum_j |R_ij| h_j, widened by 1e-4 m + 1e-6 (|c| + e) (fp32 rounding of the

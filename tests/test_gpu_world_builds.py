@@ -381,3 +381,16 @@ def test_capacity_d31_parity(native, O):
         c2.set_robot(big)
     assert e.value.code == -6
     c2.close()
+
+
+def test_set_world_rejects_more_than_max_cuboids(native):
+    """crb_set_world: k_max above CRB_MAX_CUBOIDS (131071; the large-world slow path packs the
+    cuboid index in 17 bits) returns CRB_E_SHAPE before reading any cuboid."""
+    import ctypes as C
+    ctx = native.Context(0)
+    counts = (C.c_int * 1)(0)
+    arr = (native.crb_cuboid * 1)()
+    rc = native._lib.crb_set_world(ctx.h, 1, 131072, counts, arr)
+    assert rc == -2                                    # CRB_E_SHAPE
+    assert native._lib.crb_set_world(ctx.h, 1, 131071, counts, arr) == 0
+    ctx.close()
