@@ -50,6 +50,15 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 #define CRB_SEG_SKIP 0
 #endif
 
+// Large worlds: the world items in decreasing cost of the previous pass (longest first), ordered by a
+// warp-level bitonic sort on warp 0 while it waits for the kinematic chain (1), or by thread 0's
+// insertion sort at the pass start (0).  Measured: dense K = 1000 +1.8 %, K = 64 / 128 +2 %; the
+// small-world build keeps index order (the order's indirection costs it spills: cfg 2 -7.6 %)
+#ifndef CRB_LPT_WARP
+#define CRB_LPT_WARP 1
+#endif
+#define CRB_LPT_ON GMEM
+
 // Slow-path entries (a flagged sphere, slot and cuboid) batched across cuboids and work items into
 // full warp rounds, with the group epilogues deferred until their entries are flushed (1), or one
 // compacted round per flagged cuboid (0)
@@ -718,6 +727,22 @@ static __device__ __noinline__ void lpt_order(int *ord, int n) {
     }
 }
 
+// Large worlds (CRB_LPT_WARP): the same order by one warp, a bitonic sort of the keys
+// (cost << 5 | 31 - item) in decreasing order (ties: lower item first); nwg <= 32 items, ord = wq,
+// cost = wq + n.  Run by warp 0 during the kinematic chain, so it is off the pass's critical path.
+static __device__ __noinline__ void lpt_order_warp(int *ord, int n, int lane) {
+    const int *cost = ord + n;
+    unsigned v = lane < n ? ((unsigned)min(cost[lane], (1 << 26) - 1) << 5) | (unsigned)(31 - lane) : 0u;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const unsigned o = __shfl_xor_sync(FULL, v, j);
+            v = (((lane & k) == 0) == ((lane & j) == 0)) ? max(v, o) : min(v, o);
+        }
+    if (lane < n) ord[lane] = 31 - (int)(v & 31u);
+}
+
 // order-preserving float <-> int map (for warp min / max with __reduce_{min,max}_sync); an involution
 __device__ __forceinline__ int f2o(float x) {
     const int i = __float_as_int(x);
@@ -905,7 +930,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         // then the short self items); ties keep index order.  Which warp takes which item never
         // changes a result (fixed-order merges).
         const int nwg = (rp.M + 3) >> 2;
-        if (GMEM && nwg <= 32) lpt_order(s.wq, nwg);   // large worlds only: few, long world items
+        if (GMEM && !CRB_LPT_WARP && nwg <= 32) lpt_order(s.wq, nwg);   // large worlds only: few, long world items
     }
 
     for (int win = 0; win < nwin; ++win) {
@@ -991,6 +1016,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 s.gva[gi] = gv; s.gva[D * HS + gi] = ga; s.gva[2 * D * HS + gi] = gj;
             }
         }
+        // the world items' order for this pass's queue (read after the next two barriers)
+        if (GMEM && CRB_LPT_WARP && warp == 0 && ((rp.M + 3) >> 2) <= 32) lpt_order_warp(s.wq, (rp.M + 3) >> 2, lane);
     }
 #if CRB_STATS
     const long long t_a8 = clock64();
@@ -1183,11 +1210,11 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             } stat_t{t_start, item < nwg};
 #endif
             if (item < nwg) {
-                const int grp = GMEM ? s.wq[item] : item;
+                const int grp = CRB_LPT_ON ? s.wq[item] : item;
                 const int m0 = grp << 2;
                 // large worlds: the group's cost for the next pass's order (lane 0); the start clock
                 // waits in the cost slot itself, so no register carries it through the item
-                if (GMEM && lane == 0) s.wq[nwg + grp] = (int)clock();
+                if (CRB_LPT_ON && lane == 0) s.wq[nwg + grp] = (int)clock();
                 float cx[4], cy[4], cz[4], th2[4], sp[4];
                 int dirs[4];
 #pragma unroll
@@ -1358,7 +1385,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 }
                 s.sg[m0 * NC + lane].w = gsum;
 #endif
-                if (GMEM && lane == 0) {
+                if (CRB_LPT_ON && lane == 0) {
                     const unsigned dt = (unsigned)clock() - (unsigned)s.wq[nwg + grp];
                     s.wq[nwg + grp] = (int)min(dt, 0x3fffffffu);
                 }
