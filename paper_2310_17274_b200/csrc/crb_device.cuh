@@ -52,12 +52,17 @@ static __device__ unsigned long long g_crb_stats[32];   // one copy per translat
 
 // Large worlds: the world items in decreasing cost of the previous pass (longest first), ordered by a
 // warp-level bitonic sort on warp 0 while it waits for the kinematic chain (1), or by thread 0's
-// insertion sort at the pass start (0).  Measured: dense K = 1000 +1.8 %, K = 64 / 128 +2 %; the
-// small-world build keeps index order (the order's indirection costs it spills: cfg 2 -7.6 %)
+// insertion sort at the pass start (0); the item durations are taken by lane 0 when the warp claims
+// its next item.  Measured against the thread-0 sort with in-item clocks: dense K = 1000 +9 %,
+// K = 64 / 128 +10 %.  The small-world build keeps index order (CRB_LPT_SMALL = 1: cfg 2 -2.8 %,
+// IK -3 %; the items are short and similar, and the order costs more than it balances)
 #ifndef CRB_LPT_WARP
 #define CRB_LPT_WARP 1
 #endif
-#define CRB_LPT_ON GMEM
+#ifndef CRB_LPT_SMALL
+#define CRB_LPT_SMALL 0
+#endif
+#define CRB_LPT_ON (GMEM || CRB_LPT_SMALL)
 
 // Slow-path entries (a flagged sphere, slot and cuboid) batched across cuboids and work items into
 // full warp rounds, with the group epilogues deferred until their entries are flushed (1), or one
@@ -274,7 +279,7 @@ __device__ __forceinline__ int stage_tables(const KParams &kp, float *smem, int 
     {   // world work-queue order: identity, no cost history yet
         const int nwg = (kp.rp.M + 3) >> 2;
         int *wq = reinterpret_cast<int *>(smem + kp.lay.wq);
-        for (int i = threadIdx.x; i < 2 * nwg; i += blockDim.x) wq[i] = i < nwg ? i : 0;
+        for (int i = threadIdx.x; i < 2 * nwg + NW; i += blockDim.x) wq[i] = i < nwg ? i : (i < 2 * nwg ? 0 : -1);
     }
     __syncthreads();
     mbar_wait(bar, 0);
@@ -1017,7 +1022,7 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             }
         }
         // the world items' order for this pass's queue (read after the next two barriers)
-        if (GMEM && CRB_LPT_WARP && warp == 0 && ((rp.M + 3) >> 2) <= 32) lpt_order_warp(s.wq, (rp.M + 3) >> 2, lane);
+        if (CRB_LPT_ON && CRB_LPT_WARP && warp == 0 && ((rp.M + 3) >> 2) <= 32) lpt_order_warp(s.wq, (rp.M + 3) >> 2, lane);
     }
 #if CRB_STATS
     const long long t_a8 = clock64();
@@ -1194,9 +1199,29 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
         };
 #endif
         for (;;) {
-            int item = 0;
-            if (lane == 0) item = atomicAdd(qctr, 1);
-            item = __shfl_sync(FULL, item, 0);
+            int item = 0, grpv = 0;
+            if (CRB_LPT_ON) {
+                // (longest-first order) lane 0 also reads the item's world group, and closes the
+                // duration of the warp's previous world group: its cost slot holds the start clock,
+                // the per-warp slot its index, so no register carries timing through an item
+                if (lane == 0) {
+                    const int now = (int)clock();
+                    int *cur = s.wq + 2 * nwg + warp;
+                    if (*cur >= 0) {
+                        const unsigned dt = (unsigned)now - (unsigned)s.wq[nwg + *cur];
+                        s.wq[nwg + *cur] = (int)min(dt, 0x3fffffffu);
+                    }
+                    item = atomicAdd(qctr, 1);
+                    grpv = item < nwg ? s.wq[item] : 0;
+                    if (item < nwg) s.wq[nwg + grpv] = now;
+                    *cur = item < nwg ? grpv : -1;
+                }
+                const int pk = __shfl_sync(FULL, (item << 10) | grpv, 0);
+                item = pk >> 10; grpv = pk & 1023;
+            } else {
+                if (lane == 0) item = atomicAdd(qctr, 1);
+                item = __shfl_sync(FULL, item, 0);
+            }
 #if CRB_SLOW_BATCH
             if (item >= nitems) { flush(); __syncwarp(); break; }
 #else
@@ -1210,11 +1235,8 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
             } stat_t{t_start, item < nwg};
 #endif
             if (item < nwg) {
-                const int grp = CRB_LPT_ON ? s.wq[item] : item;
+                const int grp = CRB_LPT_ON ? grpv : item;
                 const int m0 = grp << 2;
-                // large worlds: the group's cost for the next pass's order (lane 0); the start clock
-                // waits in the cost slot itself, so no register carries it through the item
-                if (CRB_LPT_ON && lane == 0) s.wq[nwg + grp] = (int)clock();
                 float cx[4], cy[4], cz[4], th2[4], sp[4];
                 int dirs[4];
 #pragma unroll
@@ -1385,10 +1407,6 @@ __device__ __forceinline__ void eval_pass(const KParams &kp, float *smem, const 
                 }
                 s.sg[m0 * NC + lane].w = gsum;
 #endif
-                if (CRB_LPT_ON && lane == 0) {
-                    const unsigned dt = (unsigned)clock() - (unsigned)s.wq[nwg + grp];
-                    s.wq[nwg + grp] = (int)min(dt, 0x3fffffffu);
-                }
             } else {
                 const uint4 B = blk[item - nwg];
                 // Block culling: the block's first spheres lie on one

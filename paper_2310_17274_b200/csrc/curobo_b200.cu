@@ -1957,7 +1957,7 @@ size_t make_layout(const RobotPack &rp, int kmax, int mode, int H, int m, int A,
     L.red = take(3 * NW);
     L.st = take(std::max(D, 16));   // start state (TO), D <= 31
     L.scal = take(8);
-    L.wq = take(2 * ((rp.M + 3) / 4));   // world work-queue order + last-pass cost per group
+    L.wq = take(2 * ((rp.M + 3) / 4) + NW);   // world work-queue order + last-pass cost per group + per-warp current group
     L.solver = w;
     const int N = H * D, Np = r4(N), DC = D * NC;
     if (mode == MODE_TO) {
