@@ -364,7 +364,7 @@ __device__ __forceinline__ float box_sdf_local(const BoxView &b, float lx, float
     glx = 0.f; gly = 0.f; glz = 0.f;
     if (qm > 0.f) {
         const float mx = fmaxf(qx, 0.f), my = fmaxf(qy, 0.f), mz = fmaxf(qz, 0.f);
-        sd = sqrtf(mx * mx + my * my + mz * mz);
+        sd = sqrtf(fmaf(mx, mx, fmaf(my, my, mz * mz)));   // (box_sd_local: the same operations)
         const float inv = 1.f / sd;
         glx = (lx >= 0.f ? mx : -mx) * inv;
         gly = (ly >= 0.f ? my : -my) * inv;
@@ -376,6 +376,18 @@ __device__ __forceinline__ float box_sdf_local(const BoxView &b, float lx, float
         else glz = lz >= 0.f ? 1.f : -1.f;
     }
     return sd;
+}
+
+// The same SDF value without the gradient (the sweep samples: most miss, and a hit re-forms the
+// gradient with box_sdf_local, whose value is bitwise this one)
+__device__ __forceinline__ float box_sd_local(const BoxView &b, float lx, float ly, float lz) {
+    const float qx = fabsf(lx) - b.h.x, qy = fabsf(ly) - b.h.y, qz = fabsf(lz) - b.h.z;
+    const float qm = fmaxf(qx, fmaxf(qy, qz));
+    if (qm > 0.f) {
+        const float mx = fmaxf(qx, 0.f), my = fmaxf(qy, 0.f), mz = fmaxf(qz, 0.f);
+        return sqrtf(fmaf(mx, mx, fmaf(my, my, mz * mz)));
+    }
+    return qm;
 }
 
 // grad sd (world) = R grad_loc = sum_i grad_loc_i * col_i
@@ -816,13 +828,15 @@ __device__ __forceinline__ float4 box_slow_val(const float4 *p, const BoxView &b
                 CRB_STAT_T(26, 1);
 #endif
                 const float kap = j * iL;
-                float gx, gy, gz, glx, gly, glz;
-                const float sd = box_sdf_local(b, fmaf(kap, dlx, lcx), fmaf(kap, dly, lcy), fmaf(kap, dlz, lcz), glx, gly, glz);
+                const float slx = fmaf(kap, dlx, lcx), sly = fmaf(kap, dly, lcy), slz = fmaf(kap, dlz, lcz);
+                const float sd = box_sd_local(b, slx, sly, slz);
                 const float dp = rp - sd;
                 if (dp > 0.f) {
 #if CRB_STATS
                     anyhit = true;
 #endif
+                    float gx, gy, gz, glx, gly, glz;
+                    (void)box_sdf_local(b, slx, sly, slz, glx, gly, glz);   // the gradient of the hit (same sd)
                     box_grad_world(b, glx, gly, glz, gx, gy, gz);
                     float dphi;
                     E += activation(dp, eta, inv_eta, dphi);
