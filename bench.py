@@ -406,6 +406,15 @@ def side_metrics(local, rank, world, dev, flush, steps=2):
     args_ = (torch.tensor(wl.seeds, device=dev), torch.tensor(wl.goal, device=dev),
              torch.tensor(wl.start, device=dev), torch.tensor(wl.env, device=dev))
     ms0 = _timed_solves(ctx, wl.solver, *args_, steps, flush, world, dev)
+    # config 2 single-problem latency: one problem (32 seeds x 32 timesteps x 100 iterations) per
+    # call, batch 1 (the cluster latency mode), median over 8 different problems, device-timed
+    lat = []
+    for p in range(8):
+        one = tuple(t[p:p + 1] for t in args_)
+        lat.append(_timed_solves(ctx, wl.solver, *one, max(1, min(steps, 3)), flush, 1, dev))
+    out["cfg2_single_problem"] = {"problems": 8, "each_solved_alone": True, "seeds": 32, "timesteps": 32,
+                                  "iters": 100, "median_ms": float(np.median(lat)), "max_ms": float(max(lat)),
+                                  "evals_per_s_median": wl.evals_per_solve() / n_f1 / (float(np.median(lat)) * 1e-3)}
     spp = dataclasses.replace(wl.solver, particle_iters=2, n_particles=64)
     msp = _timed_solves(ctx, spp, *args_, steps, flush, world, dev)
     sp0 = dataclasses.replace(wl.solver, iters=0, particle_iters=2, n_particles=64)
