@@ -27,7 +27,9 @@
  *     the exact fp32 tests, in the paper's order: results are bitwise those of the all-pairs fp32
  *     screen.  Every kernel flushes fp32 subnormals to zero (-ftz).  Environments below 60
  *     enabled cuboids stage their cuboid tables in shared memory, larger ones read them from
- *     global memory (same arithmetic).
+ *     global memory and batch the flagged (sphere, slot, cuboid) entries of the exact path into
+ *     full warp rounds; every accumulator still receives its cuboids in increasing index, so the
+ *     arithmetic and the results are the same in both builds.
  *   - Non-finite inputs are not scanned: a NaN propagates into the cost, a NaN cost packs to the
  *     +inf key and never wins a selection (SURVEY §8(b) deviation).
  *   - Capacity limits (CRB_E_LIMIT): D <= 31 (D + 1 kinematic frames after folding the fixed
