@@ -16,7 +16,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:solv
 python tools/ncu_summary.py $O/${T}_ik.ncu-rep > $O/${T}_ik_summary.txt 2>&1
 ncu -i $O/${T}_to.ncu-rep --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum > $O/${T}_to_dram.csv 2>&1
 rm -f $O/${T}_ik.ncu-rep
-# config-5 slice of the large-world build (application replay: kernel replay does not launch it under ncu)
+# config-5 slice of the large-world build (application replay: an earlier build did not launch under kernel replay)
 timeout 1200 ncu --replay-mode application --set full --clock-control none --import-source on -k regex:solve_to_kernel -c 1 \
   -o $O/${T}_c5 python tools/prof_cfg5.py 64 10 > $O/${T}_c5.log 2>&1
 python tools/ncu_summary.py $O/${T}_c5.ncu-rep > $O/${T}_c5_summary.txt 2>&1
