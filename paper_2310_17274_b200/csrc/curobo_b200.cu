@@ -579,12 +579,11 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
     if (t < kp.cp.gw * NC) s.goal[t] = kp.goal[p * kp.cp.gw + t / NC];
     stage_dt(kp, s, p);
     const float *seed = kp.q_in + (size_t)unit * N;
-    float lo_e[2], hi_e[2];
+    // (the joint limits are read from the staged tables where used, and the direction from dd:
+    // no per-thread copies live across the evaluation passes)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         const int i = t + e * NT;
-        lo_e[e] = i < N ? lim[i % D] : 0.f;
-        hi_e[e] = i < N ? lim[D + i % D] : 0.f;
         if (i < N) { th[i] = seed[i]; thA[i] = seed[i]; }
     }
     if (t == 0) { ring[0] = 0; ring[1] = 0; }
@@ -605,7 +604,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const int i = t + e * NT;
-            if (i < N) { const float s0 = kp.s0_frac * (hi_e[e] - lo_e[e]); g[i] = s0 * s0; }   // B8
+            if (i < N) { const float s0 = kp.s0_frac * (lim[D + i % D] - lim[i % D]); g[i] = s0 * s0; }   // B8
         }
     }
     for (int pass = 0; pass < npass; ++pass) {
@@ -618,7 +617,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
                 const int i = t + e * NT;
                 if (i < N) {
                     const float z = particle_normal(kp.rng_key, pk1, (unsigned)i, (unsigned)pl, (unsigned)pit, psd);
-                    thA[i] = fminf(fmaxf(fmaf(sqrtf(g[i]), z, th[i]), lo_e[e]), hi_e[e]);
+                    thA[i] = fminf(fmaxf(fmaf(sqrtf(g[i]), z, th[i]), lim[i % D]), lim[D + i % D]);
                 }
             }
             __syncthreads();
@@ -632,7 +631,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int i = t + e * NT;
-                if (i < N) thA[i] = candidate(th[i], kp.alpha[rank], d_e[e], lo_e[e], hi_e[e]);
+                if (i < N) thA[i] = candidate(th[i], kp.alpha[rank], dd[i], lim[i % D], lim[D + i % D]);   // d from dd
             }
             __syncthreads();
         }
@@ -714,7 +713,7 @@ __global__ void __launch_bounds__(NT, 2) solve_to_cluster_kernel(const __grid_co
         for (int e = 0; e < 2; ++e) {
             const int i = t + e * NT;
             if (i < N) {
-                th[i] = candidate(th[i], kp.alpha[istar], d_e[e], lo_e[e], hi_e[e]);
+                th[i] = candidate(th[i], kp.alpha[istar], dd[i], lim[i % D], lim[D + i % D]);
                 g[i] = gsrc[i];
             }
         }
