@@ -93,7 +93,7 @@ namespace crb {
 
 constexpr int kColdUnroll = CRB_COLD_UNROLL;
 #ifndef CRB_MERGE_UNROLL
-#define CRB_MERGE_UNROLL 2
+#define CRB_MERGE_UNROLL 4
 #endif
 #ifndef CRB_LS_UNROLL
 #define CRB_LS_UNROLL 1
