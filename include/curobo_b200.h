@@ -41,6 +41,8 @@
  *     environment's cuboids below 60 cuboids) must fit in 227 KB, which in practice bounds M at
  *     about 150 (the Franka problem: M = 64, 113 KB, two CTAs per SM).  SURVEY §8(b) sketched
  *     D <= 32 and M <= 1024 (the paper's self-collision kernel limit); DESIGN.md §11.
+ *     Cuboids per environment: k_max <= CRB_MAX_CUBOIDS (131071; crb_set_world returns
+ *     CRB_E_SHAPE above it).
  */
 #ifndef CUROBO_B200_H
 #define CUROBO_B200_H
